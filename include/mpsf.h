@@ -1,0 +1,166 @@
+/*
+ * mpsf.h -- C ABI of libmpsf.so, the B200 (sm_100a) batched MMU-fault-buffer
+ * processing path and recovery remap for the fault-resilient MPS design
+ * (arxiv/paper_2605_26461; reference package `mpssim`, paths below are relative
+ * to the reference's pkg/src/mpssim/).
+ *
+ * Plain C: fixed-layout structs, device pointers + sizes, a cudaStream_t passed
+ * as void*.  No exceptions cross this boundary: every call returns 0 or a
+ * negative MPSF_E_* code (see mpsf_strerror).  The Python host side
+ * (paper_2605_26461_b200/engine.py) binds it with ctypes; INTEGRATION.md shows
+ * the binding a maintainer would add to the reference.
+ *
+ * What each entry point replaces in the reference:
+ *   mpsf_upload_world  -- the state classify/range_at read: MemoryModel.ranges
+ *                         (memory.py:122-237), UvmHandler.channel_to_pid
+ *                         (pipeline.py:73,89-91), client/TSG wiring (execmodel.py:164-204)
+ *   mpsf_process       -- per batch: raise_mmu_fault's classify (pipeline.py:96-129,
+ *                         faults.py:134-171, range_at memory.py:233-237) for every entry,
+ *                         then service_bottom_half (pipeline.py:160-183) with
+ *                         intercept_and_isolate (270-304), _report_fatal/rc_recovery
+ *                         (224-265, execmodel.py:345-374), benign completion drop
+ *                         (pipeline.py:198-200) and raise_sm_trap (151-155), evaluated
+ *                         with the batch rules C0-C9 of SURVEY.md Appendix C
+ *   mpsf_remap         -- MemoryModel.vmm_map's per-page mapping (memory.py:269-283) as
+ *                         called from recovery.deploy_pair (recovery.py:175-184)
+ *   mpsf_remap_blocks  -- complete_wake's block-table restore (recovery.py:342-344)
+ */
+#ifndef MPSF_H
+#define MPSF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPSF_ABI_VERSION 1
+
+/* ---- packed fault-buffer entry (16 B; FaultSeed memory.py:104-109 + record kind) ---- */
+typedef struct {
+  uint64_t va;        /* faulting virtual address (translation entries)                 */
+  uint32_t channel;   /* channel index into the uploaded channel table                  */
+  uint8_t engine;     /* 0 SM, 1 CE, 2 PBDMA (EngineClass, execmodel.py:19-22)          */
+  uint8_t access;     /* 0 read, 1 write, 2 prefetch (AccessType, memory.py:50-53)      */
+  uint8_t kind;       /* 0 translation; 1..5 parse-time category (faults.py:289-292);
+                         8..12 SM trap EXC_2/4/5/6/7 (faults.py:116-122)                */
+  uint8_t flags;      /* bit0 valid; entries without it are skipped                     */
+} mpsf_fault_entry;
+
+/* ---- interval table row (32 B; VaRange memory.py:83-101), sorted by (client, base) ---- */
+typedef struct {
+  uint64_t base, end; /* [base, end), 4 KiB aligned                                      */
+  uint32_t client;    /* client index                                                    */
+  uint32_t page_off;  /* first page-state slot; the range owns npages+1 slots (last = guard) */
+  uint8_t kind;       /* 0 managed, 1 external (RangeKind)                               */
+  uint8_t lifecycle;  /* 0 live, 1 zombie                                                */
+  uint8_t migratable; /* 0/1                                                             */
+  uint8_t state;      /* uniform page-state byte, or 0xFF = read page_state[]           */
+  uint32_t rid;       /* reference VaRange.rid                                           */
+} mpsf_range_entry;
+
+typedef struct { uint32_t client; uint8_t engine; uint8_t pad[3]; } mpsf_channel_entry;
+/* mode: 0 MPS client, 1 standalone.  flags: bit0 alive, bit1 CE TSG already destroyed */
+typedef struct { uint8_t mode, flags; uint16_t pad; } mpsf_client_entry;
+
+/* ---- per-entry result (8 B) ----
+ * verdict bits: [1:0] outcome 0 none (trap/invalid) 1 serviced 2 isolated 3 fatal
+ *               [3:2] mechanism 0 none 1 M1 2 M2 3 M3
+ *               [4] cancelled  [5] dup (coalesced, C2)  [6] replayable buffer          */
+typedef struct { uint32_t rid; uint8_t scenario; uint8_t verdict; uint16_t client; } mpsf_out_record;
+
+/* ---- per-client fate (4 B): state 0 running 1 terminated; reason 0 '-' 1 isolation
+ * 2 fault-propagation 3 unchanged (dead before the batch); notifier: scenario id,
+ * 0xFF none, 0xFE unchanged                                                             */
+typedef struct { uint8_t state, reason, notifier, flags; } mpsf_client_verdict;
+
+typedef struct { uint64_t va; uint64_t phys; } mpsf_remap_entry;
+
+#define MPSF_PF_ISOLATION 0x1u
+#define MPSF_WF_GR_DEAD 0x1u
+
+typedef struct {
+  uint32_t flags;      /* MPSF_PF_ISOLATION = uvm.isolation_enabled                     */
+  uint32_t benign_us;  /* SimParams latencies (kernel.py:34-37)                          */
+  uint32_t m1_us, m2_us, m3_us;
+  uint32_t reserved;
+  uint64_t base_index; /* global index of entry 0 (sharded runs); base_index+n <= 2^29   */
+} mpsf_params;
+
+typedef struct {
+  int32_t status;           /* 0 or MPSF_E_*                                              */
+  uint32_t path;            /* bit0: general (release-aware) path ran                     */
+  uint64_t n_dedup;         /* dedup-set size U                                           */
+  uint64_t n_cancel;        /* cancel-list size C                                         */
+  uint64_t error_index;     /* first offending entry for entry errors                     */
+  uint64_t hash_used;       /* wild-page hash slots claimed                               */
+} mpsf_summary;
+
+#define MPSF_OK 0
+#define MPSF_E_CUDA (-1)
+#define MPSF_E_ARG (-2)
+#define MPSF_E_NO_CHANNEL (-3)      /* NoChannelAttribution (errors.py:59-60)             */
+#define MPSF_E_BAD_ENTRY (-4)
+#define MPSF_E_ENGINE_MISMATCH (-5)
+#define MPSF_E_VA_RANGE (-6)
+#define MPSF_E_WORLD (-7)           /* overlapping / unsorted / unaligned interval table   */
+#define MPSF_E_OVERFLOW (-8)        /* wild-page hash table full: call again (it grows)    */
+#define MPSF_E_NO_WORLD (-9)
+#define MPSF_E_TOO_LARGE (-10)
+
+typedef struct mpsf_ctx mpsf_ctx;
+
+int mpsf_version(void);
+const char* mpsf_strerror(int code);
+
+/* One context per device; owns the uploaded world tables and its scratch. */
+int mpsf_create(mpsf_ctx** out, int device);
+void mpsf_destroy(mpsf_ctx* ctx);
+
+/* Host pointers; synchronous copy into HBM.  Validates sortedness/overlap/alignment. */
+int mpsf_upload_world(mpsf_ctx* ctx, const mpsf_range_entry* ranges, uint32_t n_ranges,
+                      const uint8_t* page_state, uint64_t n_pages,
+                      const mpsf_channel_entry* channels, uint32_t n_channels,
+                      const mpsf_client_entry* clients, uint32_t n_clients,
+                      uint32_t world_flags);
+
+/* Device pointers, asynchronous on `stream`.  Output capacities: out[n],
+ * verdict[n_clients], counts[n_clients*28], dedup_keys/dedup_idx/cancel[n].
+ * dedup key = client<<48 | engine<<46 | scenario<<41 | page.
+ * Lists are in entry-index order and hold global indices (base_index + i).
+ * Call mpsf_get_summary to wait and read the status and list lengths. */
+int mpsf_process(mpsf_ctx* ctx, const mpsf_fault_entry* d_entries, uint64_t n,
+                 const mpsf_params* params, mpsf_out_record* d_out,
+                 mpsf_client_verdict* d_verdict, uint64_t* d_counts,
+                 uint64_t* d_dedup_keys, uint32_t* d_dedup_idx, uint32_t* d_cancel,
+                 void* stream);
+
+/* Waits for the last mpsf_process on this context and reports it. */
+int mpsf_get_summary(mpsf_ctx* ctx, mpsf_summary* out);
+
+/* End-to-end form with HOST buffers (pinned for full speed): chunked H2D of the
+ * entries overlapped with the first pass, D2H of every output; synchronous. */
+int mpsf_process_host(mpsf_ctx* ctx, const mpsf_fault_entry* h_entries, uint64_t n,
+                      const mpsf_params* params, mpsf_out_record* h_out,
+                      mpsf_client_verdict* h_verdict, uint64_t* h_counts,
+                      uint64_t* h_dedup_keys, uint32_t* h_dedup_idx, uint32_t* h_cancel,
+                      mpsf_summary* summary);
+
+/* Remap table of one shared allocation: entry k = (va_base + k*G, phys[k*G/4096]),
+ * G = 1<<gran_log2 (12..30), ceil(npages4k*4096/G) entries.  Device pointers, async. */
+int mpsf_remap(mpsf_ctx* ctx, uint64_t va_base, const uint64_t* d_phys_pages,
+               uint64_t npages4k, uint32_t gran_log2, mpsf_remap_entry* d_out, void* stream);
+
+/* Live-KV remap from folded block ids: entry j = (va_base + b_j*4096, phys[b_j]). */
+int mpsf_remap_blocks(mpsf_ctx* ctx, uint64_t va_base, const uint64_t* d_phys_pages,
+                      uint64_t npages4k, const uint32_t* d_block_ids, uint64_t nblocks,
+                      mpsf_remap_entry* d_out, void* stream);
+
+/* Number of kernel launches the last mpsf_process / mpsf_remap enqueued. */
+int mpsf_last_launches(mpsf_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPSF_H */

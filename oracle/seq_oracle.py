@@ -264,6 +264,10 @@ def process_batch(w: FlatWorld, entries: np.ndarray, params: Params | None = Non
     params = params or Params()
     n = len(entries)
     C = w.n_clients
+    if w.world_flags & K.WF_GR_DEAD and any(
+            int(w.clients["mode"][c]) == K.MODE_MPS and int(w.clients["flags"][c]) & K.CF_ALIVE
+            for c in range(C)):
+        raise OracleError(-7, "GR TSG destroyed while an MPS client is alive")
     recs = decode(w, entries)
     out = np.zeros(n, OUT_DTYPE)
     out["rid"] = K.NO_RID

@@ -1,0 +1,480 @@
+// C ABI of libmpsf.so (declared in include/mpsf.h): context, world upload, batch
+// processing, summary, host-buffer end-to-end form, remap.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "mpsf.h"
+#include "mpsf_device.cuh"
+#include "mpsf_kernels.h"
+
+using namespace mpsf;
+
+namespace {
+
+struct DevSummary {
+  uint32_t ctrl[C_NCTRL];
+  unsigned long long err_idx;
+  unsigned long long n_cancel;
+  unsigned long long n_dedup;
+};
+
+struct InitSegs {
+  void* p[8];
+  uint64_t words[8];
+  uint32_t val[8];
+  int n;
+};
+
+__global__ void k_init(InitSegs segs) {
+  const int s = blockIdx.y;
+  if (s >= segs.n) return;
+  uint32_t* p = reinterpret_cast<uint32_t*>(segs.p[s]);
+  const uint64_t w = segs.words[s];
+  const uint32_t v = segs.val[s];
+  const uint64_t w4 = w / 4;
+  uint4* p4 = reinterpret_cast<uint4*>(p);
+  const uint4 v4 = make_uint4(v, v, v, v);
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < w4; i += stride) p4[i] = v4;
+  for (uint64_t i = w4 * 4 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < w; i += stride) p[i] = v;
+}
+
+__global__ void k_summary(const uint32_t* ctrl, const unsigned long long* err_idx,
+                          const unsigned long long* tiles, uint64_t ntiles, DevSummary* out) {
+  for (int i = 0; i < C_NCTRL; ++i) out->ctrl[i] = ctrl[i];
+  out->err_idx = *err_idx;
+  if (ntiles == 0 || ctrl[C_ERR] != 0) {
+    out->n_cancel = 0;
+    out->n_dedup = 0;
+  } else {
+    const unsigned long long d = tiles[ntiles - 1];
+    out->n_cancel = d & 0x7FFFFFFFull;
+    out->n_dedup = (d >> 31) & 0x7FFFFFFFull;
+  }
+}
+
+uint64_t next_pow2(uint64_t x) {
+  uint64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace
+
+struct mpsf_ctx {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  // world
+  void* d_world = nullptr;
+  World W{};
+  bool has_world = false;
+  // scratch
+  uint32_t* d_dd = nullptr;
+  uint32_t* d_nr1 = nullptr;
+  uint64_t pages_cap = 0;
+  uint8_t* d_small = nullptr;
+  size_t small_cap = 0;
+  size_t small_empty_bytes = 0, small_zero_off = 0, small_zero_bytes = 0;
+  unsigned long long* d_tiles = nullptr;
+  uint64_t tiles_cap = 0;
+  unsigned long long* d_hdd = nullptr;  // keys then vals
+  uint64_t hcap_dd = 0;
+  unsigned long long* d_hnr = nullptr;
+  uint64_t hcap_nr = 0;
+  uint64_t want_dd = 0, want_nr = 0;
+  Scratch S{};
+  // summary (mapped pinned host memory)
+  DevSummary* h_sum = nullptr;
+  DevSummary* d_sum = nullptr;
+  cudaEvent_t ev_done = nullptr;
+  bool pending = false;
+  uint64_t last_n = 0;
+  int last_launches = 0;
+  uint32_t* d_remap_err = nullptr;
+  // host-path buffers
+  uint8_t* d_io = nullptr;
+  size_t io_cap = 0;
+};
+
+#define CK(x)                                \
+  do {                                       \
+    if ((x) != cudaSuccess) return MPSF_E_CUDA; \
+  } while (0)
+
+extern "C" {
+
+int mpsf_version(void) { return MPSF_ABI_VERSION; }
+
+const char* mpsf_strerror(int code) {
+  switch (code) {
+    case MPSF_OK: return "ok";
+    case MPSF_E_CUDA: return "CUDA error (see cudaGetLastError)";
+    case MPSF_E_ARG: return "invalid argument";
+    case MPSF_E_NO_CHANNEL: return "fault entry channel has no client attribution";
+    case MPSF_E_BAD_ENTRY: return "malformed fault entry (engine/access/kind)";
+    case MPSF_E_ENGINE_MISMATCH: return "fault entry engine differs from its channel's engine";
+    case MPSF_E_VA_RANGE: return "fault VA >= 2^53";
+    case MPSF_E_WORLD: return "interval table not sorted/aligned/disjoint or inconsistent TSG state";
+    case MPSF_E_OVERFLOW: return "wild-page hash table overflowed; call again (it has grown)";
+    case MPSF_E_NO_WORLD: return "no world uploaded";
+    case MPSF_E_TOO_LARGE: return "base_index + n exceeds 2^29 entries";
+    default: return "unknown error";
+  }
+}
+
+int mpsf_create(mpsf_ctx** out, int device) {
+  if (!out) return MPSF_E_ARG;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return MPSF_E_CUDA;
+  CK(cudaSetDevice(device));
+  mpsf_ctx* c = new mpsf_ctx();
+  c->device = device;
+  if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming) != cudaSuccess ||
+      cudaHostAlloc(reinterpret_cast<void**>(&c->h_sum), sizeof(DevSummary), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->d_sum), c->h_sum, 0) != cudaSuccess ||
+      cudaMalloc(&c->d_remap_err, sizeof(uint32_t)) != cudaSuccess) {
+    mpsf_destroy(c);
+    return MPSF_E_CUDA;
+  }
+  memset(c->h_sum, 0, sizeof(DevSummary));
+  *out = c;
+  return MPSF_OK;
+}
+
+void mpsf_destroy(mpsf_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  cudaFree(c->d_world);
+  cudaFree(c->d_dd);
+  cudaFree(c->d_nr1);
+  cudaFree(c->d_small);
+  cudaFree(c->d_tiles);
+  cudaFree(c->d_hdd);
+  cudaFree(c->d_hnr);
+  cudaFree(c->d_io);
+  cudaFree(c->d_remap_err);
+  if (c->h_sum) cudaFreeHost(c->h_sum);
+  if (c->ev_done) cudaEventDestroy(c->ev_done);
+  if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  delete c;
+}
+
+int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, const uint8_t* page_state,
+                      uint64_t np, const mpsf_channel_entry* channels, uint32_t nch,
+                      const mpsf_client_entry* clients, uint32_t ncl, uint32_t world_flags) {
+  if (!c || (nr && !ranges) || (np && !page_state) || (nch && !channels) || (ncl && !clients)) return MPSF_E_ARG;
+  if (ncl > 65535) return MPSF_E_ARG;
+  CK(cudaSetDevice(c->device));
+  // validation: sorted by (client, base), 4 KiB aligned, disjoint per client, slots in range
+  std::vector<uint32_t> off(ncl + 1, 0);
+  for (uint32_t i = 0; i < nr; ++i) {
+    const mpsf_range_entry& r = ranges[i];
+    if (r.client >= ncl || r.base >= r.end || (r.base & 0xFFF) || (r.end & 0xFFF)) return MPSF_E_WORLD;
+    if (i > 0) {
+      const mpsf_range_entry& p = ranges[i - 1];
+      if (p.client > r.client) return MPSF_E_WORLD;
+      if (p.client == r.client && p.end > r.base) return MPSF_E_WORLD;
+    }
+    const uint64_t npg = (r.end - r.base) >> 12;
+    if ((uint64_t)r.page_off + npg + 1 > np) return MPSF_E_WORLD;
+    off[r.client + 1]++;
+  }
+  for (uint32_t i = 0; i < ncl; ++i) off[i + 1] += off[i];
+  uint32_t has_mps = 0;
+  for (uint32_t i = 0; i < ncl; ++i) {
+    if (clients[i].mode > 1) return MPSF_E_WORLD;
+    if (clients[i].mode == 0) {
+      has_mps = 1;
+      if ((world_flags & MPSF_WF_GR_DEAD) && (clients[i].flags & 1)) return MPSF_E_WORLD;
+    }
+  }
+  for (uint32_t i = 0; i < nch; ++i)
+    if (channels[i].engine > 2) return MPSF_E_WORLD;
+  const size_t o_r = 0, o_off = a256(o_r + sizeof(mpsf_range_entry) * nr);
+  const size_t o_ps = a256(o_off + sizeof(uint32_t) * (ncl + 1));
+  const size_t o_ch = a256(o_ps + np);
+  const size_t o_cl = a256(o_ch + sizeof(mpsf_channel_entry) * nch);
+  const size_t total = a256(o_cl + sizeof(mpsf_client_entry) * ncl) + 256;
+  cudaFree(c->d_world);
+  c->d_world = nullptr;
+  c->has_world = false;
+  CK(cudaMalloc(&c->d_world, total));
+  uint8_t* b = reinterpret_cast<uint8_t*>(c->d_world);
+  if (nr) CK(cudaMemcpy(b + o_r, ranges, sizeof(mpsf_range_entry) * nr, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(b + o_off, off.data(), sizeof(uint32_t) * (ncl + 1), cudaMemcpyHostToDevice));
+  if (np) CK(cudaMemcpy(b + o_ps, page_state, np, cudaMemcpyHostToDevice));
+  if (nch) CK(cudaMemcpy(b + o_ch, channels, sizeof(mpsf_channel_entry) * nch, cudaMemcpyHostToDevice));
+  if (ncl) CK(cudaMemcpy(b + o_cl, clients, sizeof(mpsf_client_entry) * ncl, cudaMemcpyHostToDevice));
+  World& W = c->W;
+  W.ranges = reinterpret_cast<const mpsf_range_entry*>(b + o_r);
+  W.client_off = reinterpret_cast<const uint32_t*>(b + o_off);
+  W.page_state = b + o_ps;
+  W.channels = reinterpret_cast<const mpsf_channel_entry*>(b + o_ch);
+  W.clients = reinterpret_cast<const mpsf_client_entry*>(b + o_cl);
+  W.n_ranges = nr;
+  W.n_clients = ncl;
+  W.n_channels = nch;
+  W.world_flags = world_flags;
+  W.n_pages = np;
+  W.has_mps = has_mps;
+  W.pad = 0;
+  // page-sized scratch
+  if (np > c->pages_cap) {
+    cudaFree(c->d_dd);
+    cudaFree(c->d_nr1);
+    c->d_dd = c->d_nr1 = nullptr;
+    c->pages_cap = 0;
+    CK(cudaMalloc(&c->d_dd, sizeof(uint32_t) * std::max<uint64_t>(np, 1)));
+    CK(cudaMalloc(&c->d_nr1, sizeof(uint32_t) * std::max<uint64_t>(np, 1)));
+    c->pages_cap = np;
+  }
+  // small scratch: [EMPTY-init][ZERO-init][uninit]
+  const uint32_t C = ncl, R = nr;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o = (o + bytes + 15) & ~size_t(15); return r; };
+  const size_t s_nr0 = take(4ull * R), s_ext = take(4ull * R);
+  const size_t s_ftce = take(8ull * C), s_ftsa = take(8ull * C), s_trsa = take(8ull * C);
+  const size_t s_elig = take(4ull * C), s_iso1 = take(4ull * C), s_iso2 = take(4ull * C), s_iso3 = take(4ull * C);
+  const size_t s_giso = take(12ull * C), s_glob = take(sizeof(Globals)), s_err = take(8);
+  const size_t empty_bytes = o;
+  const size_t s_ctrl = take(4 * C_NCTRL);
+  const size_t zero_bytes = o - empty_bytes;
+  const size_t s_cst = take(sizeof(CState) * std::max<uint32_t>(C, 1));
+  if (o > c->small_cap) {
+    cudaFree(c->d_small);
+    c->d_small = nullptr;
+    c->small_cap = 0;
+    CK(cudaMalloc(&c->d_small, o));
+    c->small_cap = o;
+  }
+  c->small_empty_bytes = empty_bytes;
+  c->small_zero_off = empty_bytes;
+  c->small_zero_bytes = zero_bytes;
+  uint8_t* s = c->d_small;
+  Scratch& S = c->S;
+  S.dd = c->d_dd;
+  S.nr1 = c->d_nr1;
+  S.nr0 = reinterpret_cast<uint32_t*>(s + s_nr0);
+  S.ext = reinterpret_cast<uint32_t*>(s + s_ext);
+  S.ft_ce = reinterpret_cast<unsigned long long*>(s + s_ftce);
+  S.ft_sa = reinterpret_cast<unsigned long long*>(s + s_ftsa);
+  S.trap_sa = reinterpret_cast<unsigned long long*>(s + s_trsa);
+  S.elig = reinterpret_cast<uint32_t*>(s + s_elig);
+  S.iso1 = reinterpret_cast<uint32_t*>(s + s_iso1);
+  S.iso2 = reinterpret_cast<uint32_t*>(s + s_iso2);
+  S.iso3 = reinterpret_cast<uint32_t*>(s + s_iso3);
+  S.giso = reinterpret_cast<uint32_t*>(s + s_giso);
+  S.glob = reinterpret_cast<Globals*>(s + s_glob);
+  S.err_idx = reinterpret_cast<unsigned long long*>(s + s_err);
+  S.ctrl = reinterpret_cast<uint32_t*>(s + s_ctrl);
+  S.cstate = reinterpret_cast<CState*>(s + s_cst);
+  c->has_world = true;
+  return MPSF_OK;
+}
+
+static int ensure_call_scratch(mpsf_ctx* c, uint64_t n) {
+  const uint64_t nt = tiles_for(n);
+  if (nt > c->tiles_cap) {
+    cudaFree(c->d_tiles);
+    c->d_tiles = nullptr;
+    c->tiles_cap = 0;
+    CK(cudaMalloc(&c->d_tiles, 8 * std::max<uint64_t>(nt, 1)));
+    c->tiles_cap = nt;
+  }
+  const uint64_t floor_cap = 1ull << 16;
+  if (c->want_dd == 0 || c->last_n != n) {
+    const uint64_t guess = next_pow2(std::max<uint64_t>(floor_cap, std::min<uint64_t>(n / 32, 1ull << 24)));
+    c->want_dd = std::max(c->want_dd, guess);
+    c->want_nr = std::max(c->want_nr, guess);
+  }
+  if (c->want_dd != c->hcap_dd) {
+    cudaFree(c->d_hdd);
+    c->d_hdd = nullptr;
+    c->hcap_dd = 0;
+    CK(cudaMalloc(&c->d_hdd, 12 * c->want_dd));
+    c->hcap_dd = c->want_dd;
+  }
+  if (c->want_nr != c->hcap_nr) {
+    cudaFree(c->d_hnr);
+    c->d_hnr = nullptr;
+    c->hcap_nr = 0;
+    CK(cudaMalloc(&c->d_hnr, 12 * c->want_nr));
+    c->hcap_nr = c->want_nr;
+  }
+  Scratch& S = c->S;
+  S.hdd.keys = c->d_hdd;
+  S.hdd.vals = reinterpret_cast<uint32_t*>(c->d_hdd + c->hcap_dd);
+  S.hdd.mask = (uint32_t)(c->hcap_dd - 1);
+  S.hdd.used_slot = C_HASH_DD;
+  S.hnr.keys = c->d_hnr;
+  S.hnr.vals = reinterpret_cast<uint32_t*>(c->d_hnr + c->hcap_nr);
+  S.hnr.mask = (uint32_t)(c->hcap_nr - 1);
+  S.hnr.used_slot = C_HASH_NR;
+  S.tiles = c->d_tiles;
+  return MPSF_OK;
+}
+
+int mpsf_process(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const mpsf_params* p,
+                 mpsf_out_record* d_out, mpsf_client_verdict* d_verdict, uint64_t* d_counts,
+                 uint64_t* d_dkeys, uint32_t* d_didx, uint32_t* d_cancel, void* stream) {
+  if (!c || !p) return MPSF_E_ARG;
+  if (!c->has_world) return MPSF_E_NO_WORLD;
+  if (n && (!d_in || !d_out || !d_dkeys || !d_didx || !d_cancel)) return MPSF_E_ARG;
+  if (c->W.n_clients && (!d_verdict || !d_counts)) return MPSF_E_ARG;
+  if (p->base_index + n > MAX_GIDX) return MPSF_E_TOO_LARGE;
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int rc = ensure_call_scratch(c, n);
+  if (rc) return rc;
+  const uint64_t nt = tiles_for(n);
+  InitSegs segs{};
+  int k = 0;
+  segs.p[k] = c->d_dd; segs.words[k] = c->W.n_pages; segs.val[k++] = EMPTY32;
+  segs.p[k] = c->d_small; segs.words[k] = c->small_empty_bytes / 4; segs.val[k++] = EMPTY32;
+  segs.p[k] = c->d_small + c->small_zero_off; segs.words[k] = c->small_zero_bytes / 4; segs.val[k++] = 0;
+  segs.p[k] = c->d_tiles; segs.words[k] = 2 * nt; segs.val[k++] = 0;
+  segs.p[k] = c->d_hdd; segs.words[k] = 3 * c->hcap_dd; segs.val[k++] = EMPTY32;
+  segs.p[k] = c->d_hnr; segs.words[k] = 3 * c->hcap_nr; segs.val[k++] = EMPTY32;
+  if (c->W.n_clients) { segs.p[k] = d_counts; segs.words[k] = 2ull * NSCEN * c->W.n_clients; segs.val[k++] = 0; }
+  segs.n = k;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  k_init<<<dim3(2 * sms, k), 256, 0, st>>>(segs);
+  Params P;
+  P.flags = p->flags;
+  P.benign_us = p->benign_us;
+  P.m1_us = p->m1_us;
+  P.m2_us = p->m2_us;
+  P.m3_us = p->m3_us;
+  P.base_index = p->base_index;
+  int launches = 0;
+  if (launch_fault_path(c->W, c->S, d_in, n, P, d_out, d_verdict, reinterpret_cast<unsigned long long*>(d_counts),
+                        reinterpret_cast<unsigned long long*>(d_dkeys), d_didx, d_cancel, st, &launches))
+    return MPSF_E_CUDA;
+  k_summary<<<1, 1, 0, st>>>(c->S.ctrl, c->S.err_idx, c->d_tiles, nt, c->d_sum);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(c->ev_done, st));
+  c->pending = true;
+  c->last_n = n;
+  c->last_launches = launches + 2;
+  return MPSF_OK;
+}
+
+int mpsf_get_summary(mpsf_ctx* c, mpsf_summary* out) {
+  if (!c || !out) return MPSF_E_ARG;
+  CK(cudaSetDevice(c->device));
+  if (c->pending) {
+    CK(cudaEventSynchronize(c->ev_done));
+    c->pending = false;
+  }
+  const DevSummary& d = *c->h_sum;
+  memset(out, 0, sizeof(*out));
+  const uint32_t err = d.ctrl[C_ERR];
+  if (err & EB_NO_CHANNEL) out->status = MPSF_E_NO_CHANNEL;
+  else if (err & EB_BAD_ENTRY) out->status = MPSF_E_BAD_ENTRY;
+  else if (err & EB_MISMATCH) out->status = MPSF_E_ENGINE_MISMATCH;
+  else if (err & EB_VA) out->status = MPSF_E_VA_RANGE;
+  else if (d.ctrl[C_OVF]) out->status = MPSF_E_OVERFLOW;
+  else out->status = MPSF_OK;
+  out->path = d.ctrl[C_PATH];
+  out->n_dedup = d.n_dedup;
+  out->n_cancel = d.n_cancel;
+  out->error_index = d.err_idx;
+  out->hash_used = (uint64_t)d.ctrl[C_HASH_DD] + d.ctrl[C_HASH_NR];
+  // adapt the wild-page hash tables for the next call
+  if (out->status == MPSF_E_OVERFLOW) {
+    if (d.ctrl[C_HASH_DD] * 2ull >= c->hcap_dd / 2) c->want_dd = c->hcap_dd * 4;
+    if (d.ctrl[C_HASH_NR] * 2ull >= c->hcap_nr / 2) c->want_nr = c->hcap_nr * 4;
+    if (c->want_dd == c->hcap_dd && c->want_nr == c->hcap_nr) { c->want_dd *= 4; c->want_nr *= 4; }
+  } else if (out->status == MPSF_OK) {
+    c->want_dd = next_pow2(std::max<uint64_t>(1ull << 16, 4ull * d.ctrl[C_HASH_DD]));
+    c->want_nr = next_pow2(std::max<uint64_t>(1ull << 16, 4ull * d.ctrl[C_HASH_NR]));
+  }
+  return MPSF_OK;
+}
+
+int mpsf_last_launches(mpsf_ctx* c) { return c ? c->last_launches : 0; }
+
+int mpsf_process_host(mpsf_ctx* c, const mpsf_fault_entry* h_in, uint64_t n, const mpsf_params* p,
+                      mpsf_out_record* h_out, mpsf_client_verdict* h_verdict, uint64_t* h_counts,
+                      uint64_t* h_dkeys, uint32_t* h_didx, uint32_t* h_cancel, mpsf_summary* summary) {
+  if (!c || !p || !summary) return MPSF_E_ARG;
+  if (!c->has_world) return MPSF_E_NO_WORLD;
+  if (n && (!h_in || !h_out || !h_dkeys || !h_didx || !h_cancel)) return MPSF_E_ARG;
+  CK(cudaSetDevice(c->device));
+  const uint32_t C = c->W.n_clients;
+  const size_t o_in = 0, o_out = a256(16 * n), o_v = o_out + a256(8 * n), o_cnt = o_v + a256(4ull * C + 4);
+  const size_t o_dk = o_cnt + a256(8ull * NSCEN * C + 8), o_di = o_dk + a256(8 * n), o_ca = o_di + a256(4 * n);
+  const size_t total = o_ca + a256(4 * n + 4);
+  if (total > c->io_cap) {
+    cudaFree(c->d_io);
+    c->d_io = nullptr;
+    c->io_cap = 0;
+    CK(cudaMalloc(&c->d_io, total));
+    c->io_cap = total;
+  }
+  uint8_t* b = c->d_io;
+  cudaStream_t st = c->own_stream;
+  CK(cudaMemcpyAsync(b + o_in, h_in, 16 * n, cudaMemcpyHostToDevice, st));
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    int rc = mpsf_process(c, reinterpret_cast<mpsf_fault_entry*>(b + o_in), n, p,
+                          reinterpret_cast<mpsf_out_record*>(b + o_out),
+                          reinterpret_cast<mpsf_client_verdict*>(b + o_v), reinterpret_cast<uint64_t*>(b + o_cnt),
+                          reinterpret_cast<uint64_t*>(b + o_dk), reinterpret_cast<uint32_t*>(b + o_di),
+                          reinterpret_cast<uint32_t*>(b + o_ca), st);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(h_out, b + o_out, 8 * n, cudaMemcpyDeviceToHost, st));
+    if (C) {
+      CK(cudaMemcpyAsync(h_verdict, b + o_v, 4ull * C, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(h_counts, b + o_cnt, 8ull * NSCEN * C, cudaMemcpyDeviceToHost, st));
+    }
+    rc = mpsf_get_summary(c, summary);
+    if (rc) return rc;
+    if (summary->status == MPSF_E_OVERFLOW) continue;
+    if (summary->status != MPSF_OK) return MPSF_OK;
+    if (summary->n_dedup) {
+      CK(cudaMemcpyAsync(h_dkeys, b + o_dk, 8 * summary->n_dedup, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(h_didx, b + o_di, 4 * summary->n_dedup, cudaMemcpyDeviceToHost, st));
+    }
+    if (summary->n_cancel) CK(cudaMemcpyAsync(h_cancel, b + o_ca, 4 * summary->n_cancel, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return MPSF_OK;
+  }
+  return MPSF_OK;
+}
+
+int mpsf_remap(mpsf_ctx* c, uint64_t va_base, const uint64_t* d_phys, uint64_t npages4k, uint32_t gran_log2,
+               mpsf_remap_entry* d_out, void* stream) {
+  if (!c || gran_log2 < 12 || gran_log2 > 30 || (npages4k && (!d_phys || !d_out))) return MPSF_E_ARG;
+  CK(cudaSetDevice(c->device));
+  if (launch_remap(va_base, d_phys, npages4k, gran_log2, d_out, reinterpret_cast<cudaStream_t>(stream)))
+    return MPSF_E_CUDA;
+  c->last_launches = npages4k ? 1 : 0;
+  return MPSF_OK;
+}
+
+int mpsf_remap_blocks(mpsf_ctx* c, uint64_t va_base, const uint64_t* d_phys, uint64_t npages4k,
+                      const uint32_t* d_blocks, uint64_t nblocks, mpsf_remap_entry* d_out, void* stream) {
+  if (!c || (nblocks && (!d_phys || !d_blocks || !d_out))) return MPSF_E_ARG;
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaMemsetAsync(c->d_remap_err, 0, 4, st));
+  if (launch_remap_blocks(va_base, d_phys, npages4k, d_blocks, nblocks, d_out, c->d_remap_err, st))
+    return MPSF_E_CUDA;
+  uint32_t err = 0;
+  CK(cudaMemcpyAsync(&err, c->d_remap_err, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  c->last_launches = nblocks ? 1 : 0;
+  return err ? MPSF_E_ARG : MPSF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,247 @@
+// Device-side building blocks of the batched fault path (sm_100a).
+//
+// Reference semantics restated here (paths relative to the reference's pkg/src/mpssim/):
+//   classify()   -- faults.classify, faults.py:134-171 (priority order 145-171)
+//   attribute()  -- MemoryModel.range_at, memory.py:233-237, as a binary search over the
+//                   (client, base)-sorted interval table instead of a linear scan
+//   scenario predicates -- the 28-row table faults.py:79-108 (ids = list position)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "mpsf.h"
+
+namespace mpsf {
+
+constexpr uint32_t EMPTY32 = 0xFFFFFFFFu;
+constexpr unsigned long long EMPTY64 = 0xFFFFFFFFFFFFFFFFull;
+constexpr long long REL_NONE = 0x7FFFFFFFFFFFFFFFll;  // client never released in this batch
+constexpr long long REL_PRE = -1;                      // released before the drain (trap / dead)
+constexpr int NSCEN = 28;
+constexpr uint32_t NO_RID = 0xFFFFFFFFu;
+constexpr uint32_t MAX_GIDX = 1u << 29;
+constexpr uint64_t VA_LIMIT = 1ull << 53;
+constexpr int HASH_MAX_PROBE = 256;
+constexpr uint32_t MPSF_ENTRY_VALID = 1u;
+
+// error bits in ctrl[C_ERR]
+constexpr uint32_t EB_NO_CHANNEL = 1u, EB_BAD_ENTRY = 2u, EB_MISMATCH = 4u, EB_VA = 8u;
+
+// ctrl word slots
+enum : int {
+  C_ERR = 0, C_PATH = 1, C_HASH_DD = 2, C_HASH_NR = 3, C_OVF = 4,
+  C_TILE_FIN = 5, C_NCTRL = 16
+};
+
+// per-client derived state written by k_resolve, read by the finalize pass
+enum : uint32_t {
+  CS_ALIVE0 = 1u, CS_SA = 2u, CS_CE_ALIVE0 = 4u, CS_CE_TORN = 8u, CS_KILL_ALL = 16u,
+  CS_TRAPPED = 32u, CS_ELIG = 64u
+};
+struct CState {
+  long long rel;          // release key: REL_PRE, REL_NONE or the ok32 of the teardown record
+  uint32_t ft_ce_ok;      // first CE-TSG fatal (ok32) or EMPTY32
+  uint32_t ft_sa_ok;      // first standalone-TSG fatal (ok32) or EMPTY32
+  uint32_t trap_sa_idx;   // first standalone trap (global idx) or EMPTY32
+  uint32_t kill_tie;      // benign records with ok32 > kill_tie are cancelled (EMPTY32: none)
+  uint32_t flags;
+  uint32_t pad;
+};
+static_assert(sizeof(CState) == 32, "CState layout");
+
+// scalars shared by every client
+struct Globals {
+  unsigned long long ft_gr;     // min (ok32 << 8 | sid) over fatal GR-TSG records
+  unsigned long long trap_mps;  // min (idx << 8 | sid) over traps raised by MPS clients
+  uint32_t ft_gr_ok;            // applied GR teardown record (ok32) or EMPTY32
+  uint32_t trap_mps_idx;        // applied MPS trap (idx) or EMPTY32
+  uint32_t gr_alive0;
+  uint32_t has_elig;
+};
+
+struct World {
+  const mpsf_range_entry* ranges;
+  const uint32_t* client_off;
+  const uint8_t* page_state;
+  const mpsf_channel_entry* channels;
+  const mpsf_client_entry* clients;
+  uint32_t n_ranges, n_clients, n_channels, world_flags;
+  uint64_t n_pages;
+  uint32_t has_mps, pad;
+};
+
+struct Hash {
+  unsigned long long* keys;
+  uint32_t* vals;
+  uint32_t mask;
+  uint32_t used_slot;  // ctrl index counting claimed slots
+};
+
+struct Scratch {
+  uint32_t* dd;        // [n_pages] dense dedup slots: (gidx << 3 | group), EMPTY32
+  uint32_t* nr0;       // [n_ranges] guard-page first-isolation key, epoch 0
+  uint32_t* nr1;       // [n_pages] first-isolation key per page, epoch 1 (general path)
+  Hash hdd;            // dedup keys of pages outside every range's slot span
+  Hash hnr;            // NR keys (client, page, epoch) of such pages
+  uint32_t* ext;       // [n_ranges] first isolation-eligible record per external range
+  unsigned long long* ft_ce;    // [C]
+  unsigned long long* ft_sa;    // [C]
+  unsigned long long* trap_sa;  // [C]
+  uint32_t* elig;      // [C] first isolation-eligible record
+  uint32_t* iso1;      // [C] snapshot-unmapped eligible (M1 candidates)
+  uint32_t* iso2;      // [C] managed-range eligible (M2)
+  uint32_t* iso3;      // [C] external-range eligible (M3 candidates)
+  uint32_t* giso;      // [3*C] exact per-mechanism minima, general path
+  CState* cstate;      // [C]
+  Globals* glob;
+  uint32_t* ctrl;      // [C_NCTRL]
+  unsigned long long* err_idx;
+  unsigned long long* tiles;  // look-back descriptors of the finalize pass
+};
+
+struct Params {
+  uint32_t flags, benign_us, m1_us, m2_us, m3_us;
+  uint64_t base_index;
+};
+
+// ---- scenario table predicates (faults.py:79-108) ----
+__device__ __forceinline__ bool s_serviceable(int s) { return s >= 14 && s <= 17; }
+__device__ __forceinline__ bool s_parse(int s) { return s >= 23; }
+__device__ __forceinline__ bool s_trap(int s) { return s >= 18 && s <= 22; }
+__device__ __forceinline__ bool s_replayable(int s) { return s <= 5 || s == 14 || s == 15 || s >= 23; }
+
+// faults.classify, faults.py:134-171.  eng: 0 SM 1 CE 2 PBDMA; acc: 0 R 1 W 2 PREFETCH.
+__device__ __forceinline__ int classify(int eng, int acc, bool has, int kind, int lifecycle,
+                                        int migratable, uint32_t st) {
+  if (acc == 2) return 15;                                   // invalid prefetch, any engine
+  const int oob = eng == 0 ? 0 : 2 + 4 * eng;                // 0 / 6 / 10
+  if (!has) return oob;
+  if (lifecycle == 1) return 4 + 4 * eng;                    // zombie 4 / 8 / 12
+  const int res = st & 3;
+  const bool ro = (st & 4) != 0;
+  if (!migratable && res == 1) return 5 + 4 * eng;           // non-migratable 5 / 9 / 13
+  if (acc == 1 && ro) {
+    if (eng == 0) return kind == 1 ? 3 : (res == 2 ? 2 : 1); // am_vmm / am_gpu / am_cpu
+    return 3 + 4 * eng;                                      // am.ce 7 / am.pbdma 11
+  }
+  if (kind == 0 && res <= 1) return eng == 0 ? 14 : 15 + eng; // benign 14 / 16 / 17
+  return oob;                                                 // would-hit fallthrough
+}
+
+struct Attr {
+  int ridx;        // range index (in range or owner of the guard page), -1 if wild
+  bool in_range;
+  bool guard;      // page is the unmapped guard page right after ranges[ridx]
+  uint32_t slot;   // dense page slot (in_range or guard)
+  uint32_t st;     // page state byte (in_range)
+  int kind, lifecycle, migratable;
+  uint32_t rid;
+};
+
+// Binary search of client's slice [lo, hi) for the last range with base <= va.
+__device__ __forceinline__ Attr attribute(const mpsf_range_entry* __restrict__ R,
+                                          const uint8_t* __restrict__ page_state,
+                                          uint32_t lo, uint32_t hi, uint64_t va) {
+  uint32_t a = lo, b = hi;
+  while (a < b) {
+    const uint32_t m = (a + b) >> 1;
+    if (R[m].base <= va) a = m + 1; else b = m;
+  }
+  Attr t;
+  t.ridx = -1; t.in_range = false; t.guard = false; t.slot = 0; t.st = 0;
+  t.kind = 0; t.lifecycle = 0; t.migratable = 1; t.rid = NO_RID;
+  if (a > lo) {
+    const uint32_t k = a - 1;
+    const uint64_t base = R[k].base, end = R[k].end;
+    if (va < end) {
+      const uint4 meta = *reinterpret_cast<const uint4*>(&R[k].client);  // client,page_off,kind..state,rid
+      const uint32_t pidx = (uint32_t)((va - base) >> 12);
+      t.ridx = (int)k; t.in_range = true;
+      t.slot = meta.y + pidx;
+      t.kind = meta.z & 0xFF; t.lifecycle = (meta.z >> 8) & 0xFF; t.migratable = (meta.z >> 16) & 0xFF;
+      const uint32_t ust = meta.z >> 24;
+      t.st = ust != 0xFF ? ust : (uint32_t)page_state[t.slot];
+      t.rid = meta.w;
+    } else if (va < end + 4096) {
+      t.ridx = (int)k; t.guard = true;
+      t.slot = R[k].page_off + (uint32_t)((end - base) >> 12);
+    }
+  }
+  return t;
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 33; x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ull;
+  x ^= x >> 33;
+  return x;
+}
+
+// Open addressing, linear probing; value = atomic min.  Returns false on overflow.
+__device__ __forceinline__ bool hash_min(const Hash& h, uint32_t* ctrl, uint64_t key, uint32_t v) {
+  uint32_t s = (uint32_t)mix64(key) & h.mask;
+  for (int p = 0; p < HASH_MAX_PROBE; ++p) {
+    unsigned long long k = __ldcg(h.keys + s);
+    if (k == EMPTY64) {
+      k = atomicCAS(h.keys + s, EMPTY64, (unsigned long long)key);
+      if (k == EMPTY64) { atomicAdd(ctrl + h.used_slot, 1u); k = key; }
+    }
+    if (k == key) {
+      if (__ldcg(h.vals + s) > v) atomicMin(h.vals + s, v);
+      return true;
+    }
+    s = (s + 1) & h.mask;
+  }
+  return false;
+}
+
+__device__ __forceinline__ uint32_t hash_get(const Hash& h, uint64_t key) {
+  uint32_t s = (uint32_t)mix64(key) & h.mask;
+  for (int p = 0; p < HASH_MAX_PROBE; ++p) {
+    const unsigned long long k = __ldcg(h.keys + s);
+    if (k == key) return __ldcg(h.vals + s);
+    if (k == EMPTY64) return EMPTY32;
+    s = (s + 1) & h.mask;
+  }
+  return EMPTY32;
+}
+
+__device__ __forceinline__ void min32(uint32_t* g, uint32_t v) {
+  if (__ldcg(g) > v) atomicMin(g, v);
+}
+__device__ __forceinline__ void min64(unsigned long long* g, unsigned long long v) {
+  if (__ldcg(g) > v) atomicMin(g, v);
+}
+// smem-cached variant: one global atomic per key per block in index order
+__device__ __forceinline__ void min32c(uint32_t* g, uint32_t* c, uint32_t v) {
+  if (*c <= v) return;
+  if (atomicMin(c, v) <= v) return;
+  min32(g, v);
+}
+__device__ __forceinline__ void min64c(unsigned long long* g, unsigned long long* c,
+                                       unsigned long long v) {
+  if (*c <= v) return;
+  if (atomicMin(c, v) <= v) return;
+  min64(g, v);
+}
+
+// dedup key (SURVEY.md Appendix C rule C2)
+__device__ __forceinline__ uint64_t dedup_key(uint32_t c, int eng, int s, uint64_t page) {
+  return ((uint64_t)c << 48) | ((uint64_t)eng << 46) | ((uint64_t)s << 41) | page;
+}
+__device__ __forceinline__ uint64_t nr_key(uint32_t c, int epoch, uint64_t page) {
+  return ((uint64_t)c << 42) | ((uint64_t)epoch << 41) | page;
+}
+
+// Dedup group of a replayable translation record inside one page: SM read-class,
+// SM write-class (merged with read when both classify alike), and PREFETCH per engine.
+__device__ __forceinline__ uint32_t dedup_group(int eng, int acc, int s_read, int s_write) {
+  if (eng == 0) {
+    if (acc == 2) return 2;
+    return (acc == 1 && s_write != s_read) ? 1 : 0;
+  }
+  return eng == 1 ? 3 : 4;
+}
+
+}  // namespace mpsf

@@ -1,0 +1,20 @@
+// Host-side launch entry points of the sm_100a kernels (called by mpsf_abi.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "mpsf.h"
+#include "mpsf_device.cuh"
+
+namespace mpsf {
+int launch_fault_path(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n,
+                      const Params& P, mpsf_out_record* out, mpsf_client_verdict* verdict,
+                      unsigned long long* counts, unsigned long long* dkeys, uint32_t* didx,
+                      uint32_t* cancel, cudaStream_t st, int* launches);
+uint64_t tiles_for(uint64_t n);
+int launch_remap(uint64_t va_base, const uint64_t* phys, uint64_t npages4k, uint32_t gran_log2,
+                 mpsf_remap_entry* out, cudaStream_t st);
+int launch_remap_blocks(uint64_t va_base, const uint64_t* phys, uint64_t npages4k,
+                        const uint32_t* blocks, uint64_t nblocks, mpsf_remap_entry* out,
+                        uint32_t* err_flag, cudaStream_t st);
+}  // namespace mpsf

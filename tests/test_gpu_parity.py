@@ -1,0 +1,224 @@
+"""Parity of the sm_100a path (through the C ABI) with the oracle and the reference's
+golden fixtures.  Bit-exact: every output is integer."""
+
+import random
+
+import numpy as np
+import pytest
+
+from paper_2605_26461_b200 import constants as K
+from paper_2605_26461_b200 import synth
+from paper_2605_26461_b200.engine import BatchParams, DeviceBuffers, FaultEngine
+from paper_2605_26461_b200.errors import EntryError, KindMismatch, NoChannelAttribution
+from paper_2605_26461_b200.world import ENTRY_DTYPE
+
+from oracle import seq_oracle as so
+from tests import golden_io as G
+from tests import randworld as RW
+from tests.observe import observables
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def eng():
+    e = FaultEngine(0)
+    yield e
+    e.close()
+
+
+def bp(p: so.Params) -> BatchParams:
+    return BatchParams(isolation=p.isolation, benign_us=p.benign_us, m1_us=p.m1_us,
+                       m2_us=p.m2_us, m3_us=p.m3_us)
+
+
+def assert_same(got, want, ctx=""):
+    assert np.array_equal(got.out, want.out), (ctx, _first_diff(got.out, want.out))
+    assert np.array_equal(got.verdict, want.verdict), (ctx, got.verdict, want.verdict)
+    assert np.array_equal(got.counts, want.counts), ctx
+    assert np.array_equal(got.dedup_keys, want.dedup_keys), ctx
+    assert np.array_equal(got.dedup_idx, want.dedup_idx), ctx
+    assert np.array_equal(got.cancel, want.cancel), ctx
+
+
+def _first_diff(a, b):
+    bad = np.nonzero(a != b)[0]
+    return (int(bad[0]), a[bad[0]], b[bad[0]]) if len(bad) else None
+
+
+def run_both(eng, w, entries, p):
+    eng.upload_world(w)
+    got = eng.process(entries, bp(p))
+    want = so.process_batch(w, entries, p)
+    return got, want
+
+
+# -- golden fixtures from the reference ---------------------------------------------------
+
+def test_classify_golden_c1(eng):
+    z = G.classify_c1()
+    w, _ = synth.build_synthetic_world(4, 16, 1)
+    eng.upload_world(w)
+    res = eng.process(z["entries"], BatchParams())
+    assert np.array_equal(res.out["scenario"], z["scenario"])
+    assert np.array_equal(res.out["rid"], z["rid"])
+
+
+def test_reference_batches_golden(eng):
+    n = 0
+    for flat, entries, p, expect in G.batches():
+        eng.upload_world(flat)
+        res = eng.process(entries, BatchParams(**p))
+        assert observables(flat, entries, res.out, res.verdict) == G.as_tuples(expect), n
+        n += 1
+    assert n == 400
+
+
+def test_truth_table_golden(eng):
+    for row, flat, entries in G.truth_table():
+        eng.upload_world(flat)
+        res = eng.process(entries, BatchParams(isolation=row["isolation"]))
+        obs = observables(flat, entries, res.out, res.verdict)
+        ex = row["expect"]
+        assert obs["clients"] == {k: tuple(v) for k, v in ex["clients"].items()}, row["trigger"]
+        assert [m for _, m, _ in obs["isolation"]] == ex["mechanisms"], row["trigger"]
+        assert obs["fatal_reports"] == ex["fatal_reports"], row["trigger"]
+
+
+def test_remap_golden(eng):
+    for case in G.load_json("remap.json"):
+        for m in case["maps"].values():
+            t = eng.remap(m["base"], np.array(m["phys"], np.uint64), 12)
+            assert list(t["va"]) == [m["base"] + i * 4096 for i in range(m["npages"])]
+            assert list(t["phys"]) == m["phys"]
+        kv = case["maps"]["kv"]
+        for rid, blocks in case["folded"].items():
+            t = eng.remap_blocks(kv["base"], np.array(kv["phys"], np.uint64), blocks)
+            assert np.array_equal(t, so.remap_blocks(kv["base"], kv["phys"], blocks))
+
+
+# -- oracle parity on the build-defined batch semantics ---------------------------------------
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_batches_vs_oracle(eng, seed):
+    rnd = random.Random(1000 + seed)
+    for it in range(150):
+        w = RW.random_world(rnd, dead_p=0.15 if seed % 2 else 0.0)
+        p = RW.random_params(rnd)
+        entries = RW.random_batch(rnd, w, rnd.randint(1, 64))
+        got, want = run_both(eng, w, entries, p)
+        assert_same(got, want, (seed, it))
+
+
+def test_large_random_batch_vs_oracle(eng):
+    rnd = random.Random(77)
+    for it in range(6):
+        w = RW.random_world(rnd, max_mps=6, max_sa=3)
+        p = RW.random_params(rnd)
+        entries = RW.random_batch(rnd, w, 20_000, parse_p=0.001, trap_p=0.0005, pool=12)
+        got, want = run_both(eng, w, entries, p)
+        assert_same(got, want, it)
+
+
+@pytest.mark.parametrize("iso", [True, False])
+def test_config1_full_vs_oracle(eng, iso):
+    w, trace = synth.make_config("c1")
+    p = so.Params(isolation=iso)
+    got, want = run_both(eng, w, trace, p)
+    assert_same(got, want)
+    assert got.counts.sum() == len(trace)
+
+
+def test_config2b_slice_vs_oracle(eng):
+    w, trace = synth.make_config("c2b", n=60_000)
+    got, want = run_both(eng, w, trace, so.Params(isolation=True))
+    assert_same(got, want)
+
+
+def test_storm_slice_vs_oracle(eng):
+    w, _ = synth.build_synthetic_world(6, 64, 3)
+    trace = synth.generate_storm(w, 50_000, 5_000, 3)
+    got, want = run_both(eng, w, trace, so.Params(isolation=True))
+    assert_same(got, want)
+
+
+# -- size-independent properties at full size ---------------------------------------------------
+
+def test_storm_1e7_properties(eng):
+    w, _ = synth.build_synthetic_world(48, 512, 3)
+    n, u = 10_000_000, 1_000_000
+    trace = synth.generate_storm(w, n, u, 3)
+    eng.upload_world(w)
+    res = eng.process(trace, BatchParams(isolation=True))
+    v = res.out["verdict"]
+    assert len(res.dedup_keys) == u                     # every (client, page) pair has one key
+    assert int(((v & K.V_DUP) != 0).sum()) == n - u
+    assert len(np.unique(res.dedup_keys)) == u
+    assert np.all(np.diff(res.dedup_idx.astype(np.int64)) > 0)
+    assert np.all(np.diff(res.cancel.astype(np.int64)) > 0)
+    assert res.counts.sum() == n
+    # the representative of each key is its first occurrence
+    key_of = ((trace["channel"].astype(np.uint64) // 3) << np.uint64(48))
+    first = np.unique(res.dedup_idx)
+    assert np.all((v[first] & K.V_DUP) == 0)
+    # determinism: a second run is identical
+    res2 = eng.process(trace, BatchParams(isolation=True))
+    assert np.array_equal(res.out, res2.out) and np.array_equal(res.cancel, res2.cancel)
+    del key_of
+
+
+def test_device_resident_matches_host_form(eng):
+    import torch
+    w, trace = synth.make_config("c2a", n=200_000)
+    eng.upload_world(w)
+    host = eng.process(trace, BatchParams())
+    d_in = torch.from_numpy(trace.view(np.uint8)).cuda()
+    bufs = DeviceBuffers(len(trace), w.n_clients)
+    dev = eng.process_resident(d_in, len(trace), BatchParams(), bufs)
+    assert_same(dev, host)
+
+
+# -- edge cases ------------------------------------------------------------------------------
+
+def test_empty_and_invalid_batches(eng):
+    w, _ = synth.build_synthetic_world(2, 4, 1)
+    eng.upload_world(w)
+    empty = np.zeros(0, ENTRY_DTYPE)
+    res = eng.process(empty, BatchParams())
+    assert len(res.out) == 0 and len(res.cancel) == 0
+    assert np.all(res.verdict["state"] == K.ST_RUNNING)
+    invalid = np.zeros(100, ENTRY_DTYPE)      # valid bit clear everywhere
+    res = eng.process(invalid, BatchParams())
+    assert np.all(res.out["scenario"] == 0xFF) and res.counts.sum() == 0
+
+
+def test_entry_errors_map_to_reference_exceptions(eng):
+    w, _ = synth.build_synthetic_world(2, 4, 1)
+    eng.upload_world(w)
+    e = np.zeros(3, ENTRY_DTYPE)
+    e[:] = (0x100000, 0, 0, 0, 0, 1)
+    e[1]["channel"] = 999
+    with pytest.raises(NoChannelAttribution):
+        eng.process(e, BatchParams())
+    e[1]["channel"] = 1                        # CE channel, SM engine
+    with pytest.raises(EntryError):
+        eng.process(e, BatchParams())
+    e[1]["engine"] = 1
+    e[1]["va"] = 1 << 60
+    with pytest.raises(EntryError):
+        eng.process(e, BatchParams())
+    bad = w.ranges.copy()
+    bad[[0, 1]] = bad[[1, 0]]
+    w2 = type(w)(w.clients, w.channels, bad, w.client_off, w.page_state)
+    with pytest.raises(KindMismatch):
+        eng.upload_world(w2)
+
+
+@pytest.mark.parametrize("gran", [12, 16, 21])
+def test_remap_granularities_vs_oracle(eng, gran):
+    rng = np.random.default_rng(gran)
+    npages = 5000 + gran
+    phys = (rng.integers(1, 1 << 40, npages)).astype(np.uint64)
+    got = eng.remap(0x7F00_0000_0000, phys, gran)
+    want = so.remap_table(0x7F00_0000_0000, phys, gran)
+    assert np.array_equal(got, want)
