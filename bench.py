@@ -1,0 +1,426 @@
+#!/usr/bin/env python3
+"""Benchmark of the batched MMU-fault-buffer path (and the recovery remap) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mine|reference]
+
+Headline workload (BASELINE.json configs[1]): 48 MPS clients, a 10^7-entry mixed fault
+trace (translation misses + parse-time + SM-trap entries), isolation on.  A step is one
+``mpsf_process`` call over the whole batch with the trace resident in HBM; ``value`` is
+entries/s over all ranks.  ``e2e`` is the same metric through ``mpsf_process_host`` with
+pinned host buffers (H2D of the entries and D2H of every output inside the timed
+region).  ``extra`` carries config 3 (10^8-entry replayable storm, 90 % duplicate
+pages) and config 4 (64 GiB remap at 64 KiB and 2 MiB) measured the same way.
+
+Under torchrun every rank owns one shard of a globally indexed trace (weak scaling:
+10^7 entries per GPU, ``base_index = rank * n``) and the per-client verdicts are
+combined with NCCL (``paper_2605_26461_b200.parallel``).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fault entries/sec attributed+classified (bit-exact); recovery remap GB/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", FALLBACK_HBM_GBS)), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        except Exception:
+            rows = []
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows]
+        mx = max(float(r[2]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].strip() == "Active"})
+        loaded = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def alg_bytes(n, n_dedup, n_cancel):
+    """16 B entry read + 8 B OutRecord written per entry, 12 B per dedup
+    key, 4 B per cancelled entry."""
+    return 16 * n + 8 * n + 12 * n_dedup + 4 * n_cancel
+
+
+# ------------------------------------------------------------------------------------------
+
+def setup_dist(args):
+    import torch
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(ws, x):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def time_resident(eng, d_in, n, params, bufs, steps, flush):
+    """K device-resident steps; per-step CUDA events on the launching stream, L2 flushed
+    between steps outside the events.  Returns (total_ms, summary, profile)."""
+    import torch
+    stream = torch.cuda.current_stream()
+    eng.set_profiling(True)
+    total = 0.0
+    for _ in range(steps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        eng.process_device(d_in, n, params, bufs, stream)
+        b.record(stream)
+        b.synchronize()
+        total += a.elapsed_time(b)
+    s = eng.summary()
+    prof = eng.profile()
+    eng.set_profiling(False)
+    return total, s, prof
+
+
+def run_mine(args):
+    import torch
+    from paper_2605_26461_b200 import synth
+    from paper_2605_26461_b200.engine import (BatchParams, DeviceBuffers, FaultEngine,
+                                              alloc_host_outputs)
+    from paper_2605_26461_b200.parallel import combine_verdicts_nccl
+
+    ws, rank, local = setup_dist(args)
+    dev = torch.device("cuda", local)
+    hbm_peak, peak_src = peaks()
+    cfg = synth.CONFIGS[args.workload]
+    n = cfg["n"] if args.n is None else args.n
+    w, _ = synth.build_synthetic_world(cfg["clients"], cfg["pages"], cfg["seed"])
+    # each rank's shard of the globally indexed trace: same generator, per-rank seed
+    spec = synth.TraceSpec(n=n, seed=cfg["seed"] + 1000 * rank,
+                           parse_frac=cfg.get("parse_frac", 0.0), trap_frac=cfg.get("trap_frac", 0.0))
+    trace = synth.generate_trace(w, spec)
+    params = BatchParams(isolation=True, base_index=rank * n)
+    eng = FaultEngine(local)
+    eng.upload_world(w)
+    d_in = torch.from_numpy(trace.view(np.uint8)).to(dev)
+    bufs = DeviceBuffers(n, w.n_clients, local)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    # warm-up (also sizes the wild-page hash tables) and a bit-exact check vs the C oracle
+    for _ in range(max(args.warmup, 3)):
+        res = eng.process_resident(d_in, n, params, bufs)
+    parity = None
+    cpu_baseline = None
+    if rank == 0 and not args.no_check:
+        from oracle import c_oracle as co
+        from oracle.seq_oracle import Params as OP
+        threads = os.cpu_count() or 1
+        t0 = time.perf_counter()
+        want = co.process_batch(w, trace, OP(isolation=True), base_index=rank * n, threads=threads)
+        t_cpu = time.perf_counter() - t0
+        same = all(np.array_equal(getattr(res, f), getattr(want, f)) for f in
+                   ("out", "verdict", "counts", "dedup_keys", "dedup_idx", "cancel"))
+        parity = "bit-exact vs C oracle (full trace)" if same else "MISMATCH vs C oracle"
+        if ws == 1:
+            cpu_baseline = {"value": n / t_cpu, "unit": "entries/s", "cores": threads, "kind": "port",
+                            "sample": f"full {args.workload} trace ({n} entries), oracle/mpsf_oracle.c "
+                                      f"(pthreads decode + sequential drain), 1 run"}
+    launches = eng.last_launches()
+
+    barrier(ws)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        barrier(ws)
+        torch.cuda.synchronize()
+        total_ms, summ, prof = time_resident(eng, d_in, n, params, bufs, args.steps, flush)
+        torch.cuda.synchronize()
+        barrier(ws)
+    total_ms = max_over_ranks(ws, total_ms)
+    ms_step = total_ms / args.steps
+    value = ws * n / (ms_step / 1e3)
+    nd, nc = int(summ.n_dedup), int(summ.n_cancel)
+    B = alg_bytes(n, nd, nc)
+    achieved = B / (ms_step / 1e3) / 1e9
+    kernels = {}
+    for name, (cnt, ms) in sorted(prof.items()):
+        kb = {"k_scan": 16 * n, "k_general1": 16 * n, "k_general2": 16 * n,
+              "k_finalize": 16 * n + 8 * n + 12 * nd + 4 * nc}.get(name)
+        per = ms / max(cnt, 1)
+        kernels[name] = {"ms": round(per, 5), "share": round(ms / max(total_ms, 1e-9), 4)}
+        if kb:
+            kernels[name]["alg_GBps"] = round(kb / (per / 1e3) / 1e9, 1)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(args.workload)
+
+    # verdict combine across shards (NCCL allreduce of per-client fates)
+    combined = None
+    if ws > 1:
+        combined = combine_verdicts_nccl(res.verdict)
+
+    # end to end through the C ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        pinned = torch.from_numpy(trace.view(np.uint8)).pin_memory().numpy().view(trace.dtype)
+        hb = alloc_host_outputs(n, w.n_clients, pinned=True)
+        eng.process(pinned, params, hb)
+        barrier(ws)
+        ts = []
+        for _ in range(max(1, min(args.steps, 10))):
+            t0 = time.perf_counter()
+            r2 = eng.process(pinned, params, hb)
+            ts.append(time.perf_counter() - t0)
+        t_e2e = max_over_ranks(ws, statistics.median(ts))
+        d2h = 8 * n + 4 * w.n_clients + 8 * 28 * w.n_clients + 12 * len(r2.dedup_keys) + 4 * len(r2.cancel)
+        e2e = {"value": ws * n / t_e2e, "unit": "entries/s", "h2d_bytes_per_step": 16 * n,
+               "d2h_bytes_per_step": d2h, "ms_per_step": round(t_e2e * 1e3, 3),
+               "api": "mpsf_process_host (pinned host buffers)"}
+
+    extra = {}
+    if not args.no_storm and ws == 1:
+        extra["storm_c3"] = bench_storm(args, eng, hbm_peak, flush)
+    if not args.no_remap:
+        extra["remap_c4"] = bench_remap(args, eng, hbm_peak, flush)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "entries/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: 48 MPS clients x 32 ranges x 16 pages, "
+                                   f"{n} entries/GPU, translation misses + parse-time (1e-4) + SM traps (1e-5), "
+                                   f"isolation on (BASELINE configs[1])",
+                       "entries_per_gpu": n, "clients": w.n_clients, "ranges": int(len(w.ranges)),
+                       "l2_flush": "256 MiB write between timed steps, outside the per-step CUDA events",
+                       "parallelism": f"shard{ws}", "path": "general" if summ.path else "fast",
+                       "n_dedup": nd, "n_cancel": nc},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": traffic,
+                         "kernel": "whole mpsf_process step (k_init..k_summary, every launch)",
+                         "alg_bytes_per_step": B, "peak_source": peak_src},
+            "kernels": kernels,
+            "cpu_baseline": cpu_baseline,
+            "e2e": e2e,
+            "gpu_launches": launches * args.steps,
+            "clocks": clk.summary(),
+            "parity": parity,
+            "extra": extra,
+        }
+        if combined is not None:
+            line["combined_clients_terminated"] = int((combined["state"] == 1).sum())
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def bench_storm(args, eng, hbm_peak, flush):
+    import torch
+    from paper_2605_26461_b200 import synth
+    from paper_2605_26461_b200.engine import BatchParams, DeviceBuffers
+    cfg = synth.CONFIGS["c3"]
+    n = cfg["n"] if args.storm_n is None else args.storm_n
+    u = max(1, n // 10)
+    w, _ = synth.build_synthetic_world(cfg["clients"], cfg["pages"], cfg["seed"])
+    d_in = synth.generate_storm(w, n, u, cfg["seed"], device="cuda")
+    eng.upload_world(w)
+    bufs = DeviceBuffers(n, w.n_clients)
+    params = BatchParams(isolation=True)
+    for _ in range(3):
+        res = eng.process_resident(d_in, n, params, bufs)
+    steps = max(3, min(args.steps, 10))
+    total, s, prof = time_resident(eng, d_in, n, params, bufs, steps, flush)
+    ms = total / steps
+    nd, nc = int(s.n_dedup), int(s.n_cancel)
+    B = alg_bytes(n, nd, nc)
+    ach = B / (ms / 1e3) / 1e9
+    ok = nd == u and int(((res.out["verdict"] & 0x20) != 0).sum()) == n - u
+    del d_in, bufs
+    torch.cuda.empty_cache()
+    return {"workload": f"c3: 48 clients x 32 ranges x 8192 pages, {n} replayable entries, {u} unique "
+                        f"(client,page) pairs, 90% duplicates, isolation on",
+            "value": n / (ms / 1e3), "unit": "entries/s", "ms_per_step": ms, "steps": steps,
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": ach / hbm_peak, "alg_bytes_per_step": B},
+            "kernels": {k: round(v[1] / max(v[0], 1), 5) for k, v in sorted(prof.items())},
+            "n_dedup": nd, "n_cancel": nc, "dedup_exact": bool(ok)}
+
+
+def bench_remap(args, eng, hbm_peak, flush):
+    import torch
+    from oracle.seq_oracle import remap_table
+    state_bytes = 64 << 30
+    npages = state_bytes >> 12
+    # one shared allocation's physical pages (bump-allocated, as _take_pages does)
+    phys = torch.arange(514, 514 + npages, dtype=torch.int64, device="cuda")
+    out = {}
+    for gran in (16, 21):
+        e = npages >> (gran - 12)
+        d_out = torch.empty(16 * e, dtype=torch.uint8, device="cuda")
+        for _ in range(3):
+            eng.remap_device(0x7F00_0000_0000, phys, npages, gran, d_out)
+        torch.cuda.synchronize()
+        eng.set_profiling(True)
+        steps = max(5, min(args.steps, 50))
+        tot = 0.0
+        for _ in range(steps):
+            flush.zero_()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            eng.remap_device(0x7F00_0000_0000, phys, npages, gran, d_out)
+            b.record()
+            b.synchronize()
+            tot += a.elapsed_time(b)
+        prof = eng.profile()
+        eng.set_profiling(False)
+        ms = tot / steps
+        k_ms = prof.get("k_remap", (1, ms))[1] / max(prof.get("k_remap", (1, ms))[0], 1)
+        B = 24 * e
+        # spot-check against the oracle on the first and last 4096 entries
+        host = d_out.view(torch.int64).view(-1, 2)
+        head = host[:4096].cpu().numpy()
+        want = remap_table(0x7F00_0000_0000, np.arange(514, 514 + 4096 * (1 << (gran - 12)), dtype=np.uint64), gran)
+        ok = np.array_equal(head[:, 0].astype(np.uint64), want["va"]) and \
+            np.array_equal(head[:, 1].astype(np.uint64), want["phys"])
+        out[f"{1 << (gran - 10)}KiB"] = {
+            "entries": e, "ms_per_step": ms, "kernel_ms": k_ms,
+            "remap_GBps_of_state": state_bytes / (ms / 1e3) / 1e9,
+            "roofline": {"bound": "hbm", "achieved": B / (k_ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": B / (k_ms / 1e3) / 1e9 / hbm_peak, "alg_bytes": B},
+            "check": "matches oracle" if ok else "MISMATCH"}
+        del d_out
+    return {"state": "64 GiB shared state (one allocation, 16,777,216 x 4 KiB pages)", **out}
+
+
+# ------------------------------------------------------------------------------------------
+
+def run_reference(args):
+    """The reference's CPU implementation of the path (its restatement oracle/mpsf_oracle.c;
+    the reference itself is pure Python and absent on the GPU box) on the host cores."""
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import c_oracle as co
+    from oracle.seq_oracle import Params as OP
+    from paper_2605_26461_b200 import synth
+    cfg = synth.CONFIGS[args.workload]
+    n = cfg["n"] if args.n is None else args.n
+    sample = min(n, 2_000_000)
+    w, _ = synth.build_synthetic_world(cfg["clients"], cfg["pages"], cfg["seed"])
+    trace = synth.generate_trace(w, synth.TraceSpec(n=n, seed=cfg["seed"], parse_frac=cfg.get("parse_frac", 0.0),
+                                                    trap_frac=cfg.get("trap_frac", 0.0)))[:sample]
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        co.process_batch(w, trace, OP(isolation=True), threads=threads)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        co.process_batch(w, trace, OP(isolation=True), threads=threads)
+        ts.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(ts) / len(ts)
+    value = sample / (ms / 1e3)
+    smp = f"first {sample} entries of the {args.workload} trace per step, oracle/mpsf_oracle.c, {threads} threads"
+    line = {"metric": METRIC, "value": value, "unit": "entries/s", "impl": "reference", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": args.workload, "entries_per_step": sample},
+            "cpu_baseline": {"value": value, "unit": "entries/s", "cores": threads, "kind": "port", "sample": smp},
+            "e2e": {"value": value, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="mine", choices=("mine", "reference"))
+    ap.add_argument("--workload", default="c2b", choices=("c1", "c2a", "c2b"))
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--storm-n", type=int, default=None)
+    ap.add_argument("--no-storm", action="store_true")
+    ap.add_argument("--no-remap", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-check", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_mine(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -160,6 +160,18 @@ int mpsf_remap_blocks(mpsf_ctx* ctx, uint64_t va_base, const uint64_t* d_phys_pa
 /* Number of kernel launches the last mpsf_process / mpsf_remap enqueued. */
 int mpsf_last_launches(mpsf_ctx* ctx);
 
+/* Per-kernel device time: with profiling on, a CUDA event is recorded on the launching
+ * stream after every kernel; mpsf_get_profile waits for them and returns the accumulated
+ * per-kernel launches and milliseconds since profiling was (re)enabled. */
+typedef struct {
+  char name[32];
+  uint64_t launches;
+  double total_ms;
+} mpsf_kernel_time;
+
+int mpsf_set_profiling(mpsf_ctx* ctx, int on);
+int mpsf_get_profile(mpsf_ctx* ctx, mpsf_kernel_time* out, int cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -72,7 +72,13 @@ SIGNATURES = {
     "mpsf_remap_blocks": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p,
                                     C.c_uint64, C.c_void_p, C.c_void_p]),
     "mpsf_last_launches": (C.c_int, [C.c_void_p]),
+    "mpsf_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
+    "mpsf_get_profile": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
 }
+
+
+class KernelTime(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("launches", C.c_uint64), ("total_ms", C.c_double)]
 
 _lib = None
 

@@ -657,7 +657,7 @@ template <bool kStaged>
 static int launch_all(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n,
                       const Params& P, mpsf_out_record* out, mpsf_client_verdict* verdict,
                       unsigned long long* counts, unsigned long long* dkeys, uint32_t* didx,
-                      uint32_t* cancel, cudaStream_t st, int* launches) {
+                      uint32_t* cancel, cudaStream_t st, int* launches, const Marker& mk) {
   const size_t smem = kStaged ? staged_smem_bytes(W.n_ranges, W.n_clients, W.n_channels) : 0;
   static bool attr_set = false;
   if (!attr_set) {
@@ -674,27 +674,34 @@ static int launch_all(const World& W, const Scratch& S, const mpsf_fault_entry* 
     int g = grid_for(k_scan<kStaged>, smem);
     if ((uint64_t)g > ntiles) g = (int)ntiles;
     k_scan<kStaged><<<g, BLOCK, smem, st>>>(W, S, in, n, P, counts);
+    mk.mark("k_scan");
     ++nl;
   }
   k_resolve<<<1, 1024, 0, st>>>(W, S, P, verdict);
+  mk.mark("k_resolve");
   ++nl;
   if ((P.flags & MPSF_PF_ISOLATION) && n > 0) {
     k_clear_nr1<<<2 * sm_count(), 256, 0, st>>>(S, W.n_pages);
+    mk.mark("k_clear_nr1");
     int g = grid_for(k_general<kStaged, 1>, smem);
     if ((uint64_t)g > ntiles) g = (int)ntiles;
     k_general<kStaged, 1><<<g, BLOCK, smem, st>>>(W, S, in, n, P);
+    mk.mark("k_general1");
     nl += 2;
     if (P.m2_us <= P.benign_us) {
       k_general<kStaged, 2><<<g, BLOCK, smem, st>>>(W, S, in, n, P);
+      mk.mark("k_general2");
       ++nl;
     }
     k_resolve2<<<1, 1024, 0, st>>>(W, S, P);
+    mk.mark("k_resolve2");
     ++nl;
   }
   if (n > 0) {
     int g = grid_for(k_finalize<kStaged>, smem);
     if ((uint64_t)g > ntiles) g = (int)ntiles;
     k_finalize<kStaged><<<g, BLOCK, smem, st>>>(W, S, in, n, P, out, dkeys, didx, cancel);
+    mk.mark("k_finalize");
     ++nl;
   }
   *launches = nl;
@@ -704,10 +711,10 @@ static int launch_all(const World& W, const Scratch& S, const mpsf_fault_entry* 
 int launch_fault_path(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n,
                       const Params& P, mpsf_out_record* out, mpsf_client_verdict* verdict,
                       unsigned long long* counts, unsigned long long* dkeys, uint32_t* didx,
-                      uint32_t* cancel, cudaStream_t st, int* launches) {
+                      uint32_t* cancel, cudaStream_t st, int* launches, const Marker& mk) {
   if (staged_fits(W))
-    return launch_all<true>(W, S, in, n, P, out, verdict, counts, dkeys, didx, cancel, st, launches);
-  return launch_all<false>(W, S, in, n, P, out, verdict, counts, dkeys, didx, cancel, st, launches);
+    return launch_all<true>(W, S, in, n, P, out, verdict, counts, dkeys, didx, cancel, st, launches, mk);
+  return launch_all<false>(W, S, in, n, P, out, verdict, counts, dkeys, didx, cancel, st, launches, mk);
 }
 
 uint64_t tiles_for(uint64_t n) { return (n + TILE - 1) / TILE; }

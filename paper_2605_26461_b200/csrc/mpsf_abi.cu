@@ -6,6 +6,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
+#include <string>
 #include <vector>
 
 #include "mpsf.h"
@@ -97,6 +99,53 @@ struct mpsf_ctx {
   bool pending = false;
   uint64_t last_n = 0;
   int last_launches = 0;
+  // per-kernel profiling (events recorded after every launch)
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev_pool;
+  struct Pending {
+    std::string name;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pend;
+  std::vector<cudaEvent_t> pend_events;
+  cudaEvent_t last_mark = nullptr;
+  cudaStream_t mark_stream = nullptr;
+  std::map<std::string, std::pair<uint64_t, double>> acc;
+
+  cudaEvent_t new_event() {
+    if (!ev_pool.empty()) {
+      cudaEvent_t e = ev_pool.back();
+      ev_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+  void mark_begin(cudaStream_t st) {
+    if (!profiling) return;
+    mark_stream = st;
+    last_mark = new_event();
+    pend_events.push_back(last_mark);
+    cudaEventRecord(last_mark, st);
+  }
+  static void mark_cb(void* p, const char* name) {
+    mpsf_ctx* c = static_cast<mpsf_ctx*>(p);
+    if (!c->profiling || !c->last_mark) return;
+    cudaEvent_t e = c->new_event();
+    c->pend_events.push_back(e);
+    cudaEventRecord(e, c->mark_stream);
+    c->pend.push_back({name, c->last_mark, e});
+    c->last_mark = e;
+  }
+  mpsf::Marker marker() {
+    mpsf::Marker m;
+    if (profiling) {
+      m.fn = &mpsf_ctx::mark_cb;
+      m.ctx = this;
+    }
+    return m;
+  }
   uint32_t* d_remap_err = nullptr;
   // host-path buffers
   uint8_t* d_io = nullptr;
@@ -162,6 +211,8 @@ void mpsf_destroy(mpsf_ctx* c) {
   cudaFree(c->d_hnr);
   cudaFree(c->d_io);
   cudaFree(c->d_remap_err);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->pend_events) cudaEventDestroy(e);
   if (c->h_sum) cudaFreeHost(c->h_sum);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -348,7 +399,10 @@ int mpsf_process(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const mp
   segs.n = k;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  c->mark_begin(st);
+  const Marker mk = c->marker();
   k_init<<<dim3(2 * sms, k), 256, 0, st>>>(segs);
+  mk.mark("k_init");
   Params P;
   P.flags = p->flags;
   P.benign_us = p->benign_us;
@@ -358,9 +412,10 @@ int mpsf_process(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const mp
   P.base_index = p->base_index;
   int launches = 0;
   if (launch_fault_path(c->W, c->S, d_in, n, P, d_out, d_verdict, reinterpret_cast<unsigned long long*>(d_counts),
-                        reinterpret_cast<unsigned long long*>(d_dkeys), d_didx, d_cancel, st, &launches))
+                        reinterpret_cast<unsigned long long*>(d_dkeys), d_didx, d_cancel, st, &launches, mk))
     return MPSF_E_CUDA;
   k_summary<<<1, 1, 0, st>>>(c->S.ctrl, c->S.err_idx, c->d_tiles, nt, c->d_sum);
+  mk.mark("k_summary");
   CK(cudaGetLastError());
   CK(cudaEventRecord(c->ev_done, st));
   c->pending = true;
@@ -403,6 +458,43 @@ int mpsf_get_summary(mpsf_ctx* c, mpsf_summary* out) {
 }
 
 int mpsf_last_launches(mpsf_ctx* c) { return c ? c->last_launches : 0; }
+
+int mpsf_set_profiling(mpsf_ctx* c, int on) {
+  if (!c) return MPSF_E_ARG;
+  CK(cudaSetDevice(c->device));
+  mpsf_kernel_time dummy;
+  mpsf_get_profile(c, &dummy, 0);  // drain anything pending
+  c->acc.clear();
+  c->profiling = on != 0;
+  return MPSF_OK;
+}
+
+int mpsf_get_profile(mpsf_ctx* c, mpsf_kernel_time* out, int cap) {
+  if (!c || cap < 0 || (cap && !out)) return MPSF_E_ARG;
+  CK(cudaSetDevice(c->device));
+  for (auto& p : c->pend) {
+    CK(cudaEventSynchronize(p.b));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, p.a, p.b));
+    auto& slot = c->acc[p.name];
+    slot.first += 1;
+    slot.second += ms;
+  }
+  c->pend.clear();
+  for (cudaEvent_t e : c->pend_events) c->ev_pool.push_back(e);
+  c->pend_events.clear();
+  c->last_mark = nullptr;
+  int i = 0;
+  for (auto& kv : c->acc) {
+    if (i >= cap) break;
+    memset(out[i].name, 0, sizeof(out[i].name));
+    strncpy(out[i].name, kv.first.c_str(), sizeof(out[i].name) - 1);
+    out[i].launches = kv.second.first;
+    out[i].total_ms = kv.second.second;
+    ++i;
+  }
+  return cap ? i : (int)c->acc.size();
+}
 
 int mpsf_process_host(mpsf_ctx* c, const mpsf_fault_entry* h_in, uint64_t n, const mpsf_params* p,
                       mpsf_out_record* h_out, mpsf_client_verdict* h_verdict, uint64_t* h_counts,
@@ -456,8 +548,10 @@ int mpsf_remap(mpsf_ctx* c, uint64_t va_base, const uint64_t* d_phys, uint64_t n
                mpsf_remap_entry* d_out, void* stream) {
   if (!c || gran_log2 < 12 || gran_log2 > 30 || (npages4k && (!d_phys || !d_out))) return MPSF_E_ARG;
   CK(cudaSetDevice(c->device));
+  c->mark_begin(reinterpret_cast<cudaStream_t>(stream));
   if (launch_remap(va_base, d_phys, npages4k, gran_log2, d_out, reinterpret_cast<cudaStream_t>(stream)))
     return MPSF_E_CUDA;
+  c->marker().mark("k_remap");
   c->last_launches = npages4k ? 1 : 0;
   return MPSF_OK;
 }

@@ -7,10 +7,21 @@
 #include "mpsf_device.cuh"
 
 namespace mpsf {
+
+// Optional per-kernel timing hook: called right after each launch on the same stream
+// (mpsf_abi.cu records a CUDA event there when profiling is on).
+struct Marker {
+  void (*fn)(void* ctx, const char* name) = nullptr;
+  void* ctx = nullptr;
+  void mark(const char* name) const {
+    if (fn) fn(ctx, name);
+  }
+};
+
 int launch_fault_path(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n,
                       const Params& P, mpsf_out_record* out, mpsf_client_verdict* verdict,
                       unsigned long long* counts, unsigned long long* dkeys, uint32_t* didx,
-                      uint32_t* cancel, cudaStream_t st, int* launches);
+                      uint32_t* cancel, cudaStream_t st, int* launches, const Marker& mk);
 uint64_t tiles_for(uint64_t n);
 int launch_remap(uint64_t va_base, const uint64_t* phys, uint64_t npages4k, uint32_t gran_log2,
                  mpsf_remap_entry* out, cudaStream_t st);

@@ -159,6 +159,17 @@ class FaultEngine:
     def last_launches(self) -> int:
         return int(self.lib.mpsf_last_launches(self.ctx))
 
+    def set_profiling(self, on: bool) -> None:
+        self._check(self.lib.mpsf_set_profiling(self.ctx, 1 if on else 0))
+
+    def profile(self) -> dict:
+        """{kernel name: (launches, total ms)} since profiling was enabled (waits)."""
+        arr = (_lib.KernelTime * 32)()
+        k = self.lib.mpsf_get_profile(self.ctx, C.cast(arr, C.c_void_p), 32)
+        if k < 0:
+            self._check(k)
+        return {arr[i].name.decode(): (int(arr[i].launches), float(arr[i].total_ms)) for i in range(k)}
+
     # -- host-buffer form (end to end) ---------------------------------------------------------
     def process(self, entries: np.ndarray, params: BatchParams, out_bufs: Optional[dict] = None) -> BatchResult:
         """``mpsf_process_host``: host entries in, host results out (H2D + D2H inside)."""

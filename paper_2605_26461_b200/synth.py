@@ -200,32 +200,55 @@ def generate_trace(w: FlatWorld, spec: TraceSpec) -> np.ndarray:
 
 
 def generate_storm(w: FlatWorld, n: int, unique: int, seed: int,
-                   wild_frac: float = 0.02) -> np.ndarray:
+                   wild_frac: float = 0.02, device=None):
     """Config 3: ``unique`` distinct (client, page) pairs, each with one fixed
     replayable (engine, access) -- SM, or PREFETCH from any engine -- emitted once,
     then ``n - unique`` resamples of the same pairs (in-page offset re-drawn),
     shuffled.  Exactly ``1 - unique/n`` of the entries are page duplicates."""
     rng = np.random.Generator(np.random.PCG64(seed))
     lk = _Lookup(w)
-    cs, vs, es, as_ = [], [], [], []
-    seen_keys = np.zeros(0, np.uint64)
-    while len(seen_keys) < unique:
-        m = int((unique - len(seen_keys)) * 1.6) + 4096
-        client, va, engine, access = _draw(lk, rng, m, wild_frac)
-        ok = ~would_hit(lk, client, va, engine, access)
-        ok &= (engine == K.ENG_SM) | (access == K.ACC_PREFETCH)
-        client, va, engine, access = client[ok], va[ok], engine[ok], access[ok]
-        key = (client.astype(np.uint64) << np.uint64(44)) | (va >> np.uint64(12))
-        _, first = np.unique(key, return_index=True)
-        first.sort()
-        key, client, va, engine, access = key[first], client[first], va[first], engine[first], access[first]
-        fresh = ~np.isin(key, seen_keys)
-        cs.append(client[fresh]); vs.append(va[fresh]); es.append(engine[fresh]); as_.append(access[fresh])
-        seen_keys = np.concatenate([seen_keys, key[fresh]])
-    client = np.concatenate(cs)[:unique]
-    va = np.concatenate(vs)[:unique]
-    engine = np.concatenate(es)[:unique]
-    access = np.concatenate(as_)[:unique]
+    r = w.ranges
+    # distinct in-world pages (every range's pages plus its guard page) ...
+    npg = ((r["end"] - r["base"]) >> np.uint64(12)).astype(np.int64) + 1
+    starts = np.cumsum(npg) - npg
+    n_wild = int(round(unique * wild_frac))
+    n_world = unique - n_wild
+    if n_world > int(npg.sum()):
+        raise ValueError("world has fewer pages than the requested unique pairs")
+    slots = rng.choice(int(npg.sum()), n_world, replace=False)
+    ridx = np.searchsorted(starts, slots, side="right") - 1
+    client = r["client"][ridx].astype(np.uint32)
+    page_va = r["base"][ridx] + ((slots - starts[ridx]).astype(np.uint64) << np.uint64(12))
+    # ... plus distinct wild pages in [2^32, 2^33)
+    wild_page = rng.choice(1 << 20, n_wild, replace=False).astype(np.uint64)
+    client = np.concatenate([client, rng.integers(0, w.n_clients, n_wild).astype(np.uint32)])
+    page_va = np.concatenate([page_va, (np.uint64(1) << np.uint64(32)) + (wild_page << np.uint64(12))])
+    va = page_va | rng.integers(0, 4096, unique).astype(np.uint64)
+    # one fixed replayable miss per pair: SM, or PREFETCH from any engine
+    engine = rng.choice(3, unique, p=ENGINE_P).astype(np.uint8)
+    access = rng.choice(3, unique, p=ACCESS_P).astype(np.uint8)
+    todo = np.arange(unique)
+    for rnd in range(17):
+        c_, v_, e_, a_ = client[todo], va[todo], engine[todo], access[todo]
+        bad = would_hit(lk, c_, v_, e_, a_) | ((e_ != K.ENG_SM) & (a_ != K.ACC_PREFETCH))
+        todo = todo[bad]
+        nb = len(todo)
+        if nb == 0:
+            break
+        if rnd < 16:
+            engine[todo] = rng.choice(3, nb, p=ENGINE_P).astype(np.uint8)
+            access[todo] = rng.choice(3, nb, p=ACCESS_P).astype(np.uint8)
+        else:
+            # pages where only a rare combination misses: healthy external pages miss
+            # only on PREFETCH; every managed page misses on an SM write
+            ridx = lk.attribute(client[todo], va[todo])
+            managed = (ridx >= 0) & (r["kind"][np.where(ridx >= 0, ridx, 0)] == K.RK_MANAGED)
+            access[todo] = np.where(managed, K.ACC_WRITE, K.ACC_PREFETCH)
+            engine[todo] = np.where(managed, K.ENG_SM, engine[todo])
+    if np.any(would_hit(lk, client, va, engine, access)):
+        raise RuntimeError("could not draw a replayable miss for every storm page")
+    if device is not None:
+        return _expand_storm_torch(client, va, engine, access, n, seed, device)
     pick = np.concatenate([np.arange(unique, dtype=np.int64),
                            rng.integers(0, unique, n - unique)])
     va_all = va[pick]
@@ -243,6 +266,33 @@ def generate_storm(w: FlatWorld, n: int, unique: int, seed: int,
     out["kind"] = K.KIND_TRANSLATION
     out["flags"] = K.ENTRY_FLAG_VALID
     return out
+
+
+def _expand_storm_torch(client, va, engine, access, n, seed, device):
+    """Same expansion as the numpy path (each pair once + uniform resamples with a fresh
+    in-page offset, shuffled) done with torch's Philox generator on the GPU, so a 10^8-entry
+    trace is produced in HBM in well under a second.  Returns a uint8 tensor of n*16 bytes."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    u = len(va)
+    t_va = torch.from_numpy(va.view(np.int64)).to(device)
+    w1 = (client.astype(np.int64) * 3 + engine) | (engine.astype(np.int64) << 32) | \
+         (access.astype(np.int64) << 40) | (np.int64(K.KIND_TRANSLATION) << 48) | \
+         (np.int64(K.ENTRY_FLAG_VALID) << 56)
+    t_w1 = torch.from_numpy(w1).to(device)
+    pick = torch.cat([torch.arange(u, device=device),
+                      torch.randint(0, u, (n - u,), device=device, generator=g)])
+    off = torch.randint(0, 4096, (n,), device=device, generator=g)
+    perm = torch.randperm(n, device=device, generator=g)
+    pick = pick[perm]
+    resampled = perm >= u
+    v = t_va[pick]
+    v = torch.where(resampled, (v & ~0xFFF) | off, v)
+    out = torch.empty((n, 2), dtype=torch.int64, device=device)
+    out[:, 0] = v
+    out[:, 1] = t_w1[pick]
+    return out.view(torch.uint8).reshape(-1)
 
 
 # -- config table (BASELINE.json "configs") -------------------------------------------
