@@ -145,7 +145,7 @@ def test_storm_slice_vs_oracle(eng):
 # -- size-independent properties at full size ---------------------------------------------------
 
 def test_storm_1e7_properties(eng):
-    w, _ = synth.build_synthetic_world(48, 512, 3)
+    w, _ = synth.build_synthetic_world(48, 1024, 3)
     n, u = 10_000_000, 1_000_000
     trace = synth.generate_storm(w, n, u, 3)
     eng.upload_world(w)
