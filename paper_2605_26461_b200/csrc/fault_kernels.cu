@@ -5,22 +5,24 @@
 // (pipeline.py:96-129), service_bottom_half drains replayable-then-non-replayable and
 // acts per record on the evolving world (pipeline.py:160-183).  Here the same result is
 // computed with the parallel recipe C9 of SURVEY.md Appendix C -- every cross-record
-// dependency is a first-in-group minimum over the drain key, so the batch needs:
+// dependency is a first-in-group minimum over the drain key:
 //
-//   k_scan      pass 1 over the entries: decode, attribute (binary search in the smem
-//               interval table), classify, per-(client,scenario) counts, and the group
-//               minima (fatal TSG teardowns, traps, first isolation per external range /
-//               per unmapped page / per client, first record per dedup key)
-//   k_resolve   one block: per-client release keys, kill thresholds, fates, fast/general
-//   k_general1  [general path only] release-aware first-isolation keys (rule C3 epochs)
-//   k_general2  [general path, m2 <= benign] exact per-client M2 minima
+//   k_scan      pass 1: decode, attribute (binary search of the smem interval table),
+//               classify (smem LUT of faults.classify), per-block (client, scenario) counts,
+//               group minima (fatal TSG teardowns, traps, first isolation per external
+//               range / unmapped page / client, first record per dedup key)
+//   k_resolve   block 0: per-client release keys, kill thresholds, fates, fast/general
+//               path; blocks 1..: reduce the per-block count partials
+//   k_general   [general path: a client with isolation-eligible records is released
+//               inside the batch, or m2 <= benign] release-aware first-isolation keys
+//               (rule C3 epochs) and exact per-client mechanism minima
 //   k_resolve2  [general path] kill thresholds from the exact minima
-//   k_finalize  pass 2: re-decode, resolve dup / mechanism / cancel per entry, write the
-//               8-byte OutRecord, compact the cancel list and the dedup set in index order
-//               with a decoupled look-back over tiles
+//   k_finalize  pass 2: dup / mechanism / cancel per entry, the 8-byte OutRecord, and the
+//               cancel list + dedup set compacted in index order (decoupled look-back)
 //
-// The fast path (isolation off, or no client with isolation-eligible records is released
-// in the batch, and m2_us > benign_us) reads the entries exactly twice.
+// Every pass streams the entries with TMA bulk copies (cp.async.bulk, L2 evict-first)
+// into a double-buffered shared-memory tile, completion tracked by mbarriers, so the
+// per-entry loop is a small rolled loop over shared memory while the next tile lands.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -31,96 +33,141 @@ namespace mpsf {
 
 constexpr int BLOCK = 512;
 constexpr int WARPS = BLOCK / 32;
-constexpr int EPT = 8;                  // entries per lane per tile
-constexpr int TILE = BLOCK * EPT;       // 4096 entries per tile
+constexpr int EPT = 4;                  // entries per lane per tile
+constexpr int TILE = BLOCK * EPT;       // 2048 entries = 32 KiB
+constexpr int NBUF = 2;
+constexpr uint32_t TILE_BYTES = TILE * 16;
 
-// ---- shared-memory staging of the world tables ------------------------------------
-struct Smem {
-  mpsf_range_entry* ranges;   // staged interval table (or global pointer)
-  mpsf_channel_entry* channels;
-  uint32_t* client_off;
-  uint8_t* client_mode;
-  // pass-1 write-through caches
-  unsigned long long* ft_ce;
-  unsigned long long* ft_sa;
-  unsigned long long* trap_sa;
-  uint32_t* elig;
-  uint32_t* iso1;
-  uint32_t* iso2;
-  uint32_t* iso3;
-  uint32_t* ext;
-  uint32_t* nr0;
-  uint32_t* counts;
+// ---- PTX: mbarrier + bulk async copy (TMA) ---------------------------------------------
+__device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}" ::"r"(sa(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          sa(dst)),
+      "l"(src), "r"(bytes), "r"(sa(bar)), "l"(pol)
+      : "memory");
+}
+
+// ---- shared-memory layout ---------------------------------------------------------------
+__host__ __device__ inline uint32_t al16(uint64_t x) { return (uint32_t)((x + 15) & ~uint64_t(15)); }
+
+struct Layout {
+  uint32_t tiles, bars, tids, lut, ranges, channels, client_off, cinfo;
+  uint32_t c64, c32, r32, counts, cstate, total;
 };
 
-__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
-
-__host__ __device__ inline size_t staged_smem_bytes(uint32_t nr, uint32_t nc, uint32_t nch) {
-  size_t s = 0;
-  s += align16(sizeof(mpsf_range_entry) * nr);
-  s += align16(sizeof(mpsf_channel_entry) * nch);
-  s += align16(sizeof(uint32_t) * (nc + 1));
-  s += align16(nc);
-  s += align16(sizeof(unsigned long long) * 3 * nc);
-  s += align16(sizeof(uint32_t) * 4 * nc);
-  s += align16(sizeof(uint32_t) * 2 * nr);
-  s += align16(sizeof(uint32_t) * NSCEN * nc);
-  return s;
+// kStaged: the interval table and the per-client/per-range caches live in smem
+__host__ __device__ inline Layout make_layout(uint32_t nr, uint32_t nc, uint32_t nch, bool staged, bool fin) {
+  Layout L;
+  uint32_t o = 0;
+  L.tiles = o; o += NBUF * TILE_BYTES;
+  L.bars = o; o += 16 * NBUF;
+  L.tids = o; o += 16;
+  L.lut = o; o += 2048;
+  L.ranges = o; if (staged) o += al16(32ull * nr);
+  L.channels = o; if (staged) o += al16(8ull * nch);
+  L.client_off = o; if (staged) o += al16(4ull * (nc + 1));
+  L.cinfo = o; if (staged) o += al16(nc);
+  L.c64 = o; if (staged && !fin) o += al16(24ull * nc);
+  L.c32 = o; if (staged && !fin) o += al16(12ull * nc);
+  L.r32 = o; if (staged && !fin) o += al16(8ull * nr);
+  L.counts = o; if (staged && !fin) o += al16(4ull * NSCEN * nc);
+  L.cstate = o; if (staged && fin) o += al16(32ull * nc);
+  L.total = o;
+  return L;
 }
 
-__device__ inline Smem carve(uint8_t* base, const World& W) {
-  Smem s;
-  size_t o = 0;
-  s.ranges = reinterpret_cast<mpsf_range_entry*>(base + o); o += align16(sizeof(mpsf_range_entry) * W.n_ranges);
-  s.channels = reinterpret_cast<mpsf_channel_entry*>(base + o); o += align16(sizeof(mpsf_channel_entry) * W.n_channels);
-  s.client_off = reinterpret_cast<uint32_t*>(base + o); o += align16(sizeof(uint32_t) * (W.n_clients + 1));
-  s.client_mode = base + o; o += align16(W.n_clients);
-  s.ft_ce = reinterpret_cast<unsigned long long*>(base + o);
-  s.ft_sa = s.ft_ce + W.n_clients;
-  s.trap_sa = s.ft_sa + W.n_clients;
-  o += align16(sizeof(unsigned long long) * 3 * W.n_clients);
-  s.elig = reinterpret_cast<uint32_t*>(base + o);
-  s.iso1 = s.elig + W.n_clients; s.iso2 = s.iso1 + W.n_clients; s.iso3 = s.iso2 + W.n_clients;
-  o += align16(sizeof(uint32_t) * 4 * W.n_clients);
-  s.ext = reinterpret_cast<uint32_t*>(base + o); s.nr0 = s.ext + W.n_ranges;
-  o += align16(sizeof(uint32_t) * 2 * W.n_ranges);
-  s.counts = reinterpret_cast<uint32_t*>(base + o);
-  return s;
+// Block-wide view of the world tables (smem when staged, else global).
+struct View {
+  const mpsf_range_entry* ranges;
+  const mpsf_channel_entry* channels;
+  const uint32_t* client_off;
+  const uint8_t* cinfo;     // mode (bit0 = standalone)
+  const uint8_t* lut;       // classify LUT
+  unsigned long long *ft_ce, *ft_sa, *trap_sa;   // pass-1 caches (or null)
+  uint32_t *iso1, *iso2, *iso3, *ext, *nr0, *counts;
+  const CState* cst;
+};
+
+// LUT index of faults.classify inputs: eng | acc<<2 | has<<4 | kind<<5 | zombie<<6 | migr<<7 | st<<8
+__device__ __forceinline__ uint32_t lut_index(int eng, int acc, const Attr& a) {
+  return (uint32_t)eng | ((uint32_t)acc << 2) |
+         (a.in_range ? (16u | ((uint32_t)a.kind << 5) | ((uint32_t)a.lifecycle << 6) |
+                        ((a.migratable ? 1u : 0u) << 7) | ((a.st & 7u) << 8))
+                     : 0u);
 }
 
-// Copy world tables into smem and initialise the caches.  kStaged=false keeps
-// everything in global memory (worlds too large for one CTA's smem).
 template <bool kStaged>
-__device__ inline Smem stage(uint8_t* sm, const World& W, bool with_caches) {
-  Smem s;
-  if (!kStaged) {
-    s.ranges = const_cast<mpsf_range_entry*>(W.ranges);
-    s.channels = const_cast<mpsf_channel_entry*>(W.channels);
-    s.client_off = const_cast<uint32_t*>(W.client_off);
-    s.client_mode = nullptr;
-    return s;
-  }
-  s = carve(sm, W);
+__device__ View setup(uint8_t* sm, const Layout& L, const World& W, const Scratch& S, bool scan, bool fin) {
+  View v;
   const int tid = threadIdx.x;
-  {
+  uint8_t* lut = sm + L.lut;
+  for (uint32_t i = tid; i < 2048; i += blockDim.x) {
+    const int eng = i & 3, acc = (i >> 2) & 3;
+    const bool has = (i >> 4) & 1;
+    lut[i] = (eng > 2 || acc > 2) ? 0xFF
+                                  : (uint8_t)classify(eng, acc, has, (i >> 5) & 1, (i >> 6) & 1, (i >> 7) & 1, (i >> 8) & 7);
+  }
+  v.lut = lut;
+  if (kStaged) {
+    mpsf_range_entry* r = reinterpret_cast<mpsf_range_entry*>(sm + L.ranges);
     const uint4* src = reinterpret_cast<const uint4*>(W.ranges);
-    uint4* dst = reinterpret_cast<uint4*>(s.ranges);
-    for (uint32_t i = tid; i < W.n_ranges * 2; i += blockDim.x) dst[i] = __ldg(src + i);
+    uint4* dst = reinterpret_cast<uint4*>(r);
+    for (uint32_t i = tid; i < 2 * W.n_ranges; i += blockDim.x) dst[i] = __ldg(src + i);
+    mpsf_channel_entry* ch = reinterpret_cast<mpsf_channel_entry*>(sm + L.channels);
+    for (uint32_t i = tid; i < W.n_channels; i += blockDim.x) ch[i] = W.channels[i];
+    uint32_t* off = reinterpret_cast<uint32_t*>(sm + L.client_off);
+    for (uint32_t i = tid; i <= W.n_clients; i += blockDim.x) off[i] = __ldg(W.client_off + i);
+    uint8_t* ci = sm + L.cinfo;
+    for (uint32_t i = tid; i < W.n_clients; i += blockDim.x) ci[i] = W.clients[i].mode;
+    v.ranges = r; v.channels = ch; v.client_off = off; v.cinfo = ci;
+  } else {
+    v.ranges = W.ranges; v.channels = W.channels; v.client_off = W.client_off; v.cinfo = nullptr;
   }
-  for (uint32_t i = tid; i < W.n_channels; i += blockDim.x) s.channels[i] = W.channels[i];
-  for (uint32_t i = tid; i <= W.n_clients; i += blockDim.x) s.client_off[i] = __ldg(W.client_off + i);
-  for (uint32_t i = tid; i < W.n_clients; i += blockDim.x) s.client_mode[i] = W.clients[i].mode;
-  if (with_caches) {
-    for (uint32_t i = tid; i < 3 * W.n_clients; i += blockDim.x) s.ft_ce[i] = EMPTY64;
-    for (uint32_t i = tid; i < 4 * W.n_clients; i += blockDim.x) s.elig[i] = EMPTY32;
-    for (uint32_t i = tid; i < 2 * W.n_ranges; i += blockDim.x) s.ext[i] = EMPTY32;
-    for (uint32_t i = tid; i < NSCEN * W.n_clients; i += blockDim.x) s.counts[i] = 0;
+  v.ft_ce = v.ft_sa = v.trap_sa = nullptr;
+  v.iso1 = v.iso2 = v.iso3 = v.ext = v.nr0 = v.counts = nullptr;
+  v.cst = S.cstate;
+  if (kStaged && scan) {
+    unsigned long long* c64 = reinterpret_cast<unsigned long long*>(sm + L.c64);
+    for (uint32_t i = tid; i < 3 * W.n_clients; i += blockDim.x) c64[i] = EMPTY64;
+    v.ft_ce = c64; v.ft_sa = c64 + W.n_clients; v.trap_sa = c64 + 2 * W.n_clients;
+    uint32_t* c32 = reinterpret_cast<uint32_t*>(sm + L.c32);
+    for (uint32_t i = tid; i < 3 * W.n_clients; i += blockDim.x) c32[i] = EMPTY32;
+    v.iso1 = c32; v.iso2 = c32 + W.n_clients; v.iso3 = c32 + 2 * W.n_clients;
+    uint32_t* r32 = reinterpret_cast<uint32_t*>(sm + L.r32);
+    for (uint32_t i = tid; i < 2 * W.n_ranges; i += blockDim.x) r32[i] = EMPTY32;
+    v.ext = r32; v.nr0 = r32 + W.n_ranges;
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(sm + L.counts);
+    for (uint32_t i = tid; i < NSCEN * W.n_clients; i += blockDim.x) cnt[i] = 0;
+    v.counts = cnt;
   }
-  return s;
-}
-
-__device__ __forceinline__ uint32_t client_mode(const Smem& s, const World& W, uint32_t c, bool staged) {
-  return staged ? s.client_mode[c] : W.clients[c].mode;
+  if (kStaged && fin) {
+    CState* cs = reinterpret_cast<CState*>(sm + L.cstate);
+    for (uint32_t i = tid; i < W.n_clients; i += blockDim.x) cs[i] = S.cstate[i];
+    v.cst = cs;
+  }
+  return v;
 }
 
 __device__ __forceinline__ void raise_err(const Scratch& S, uint32_t bit, uint64_t gidx) {
@@ -133,58 +180,54 @@ struct Rec {
   bool valid;
   uint32_t c;       // client
   int ceng;         // channel engine
-  int eng, acc, kind;
+  int eng, kind;
   int s;            // scenario id
   uint64_t va;
   Attr at;
   bool repl;        // replayable buffer
   uint32_t group;   // dedup group (replayable translation)
+  bool sa;          // client is standalone
 };
 
-// Entry decode, validation, attribution, classification.  Returns valid=false for
-// invalid-flag entries and for malformed ones (after raising the error bit).
 template <bool kStaged>
-__device__ __forceinline__ Rec decode(const World& W, const Smem& sm, const Scratch& S,
-                                      uint64_t va, uint64_t w1, uint64_t gidx) {
+__device__ __forceinline__ Rec decode(const World& W, const View& v, const Scratch& S, uint4 e, uint64_t gidx) {
   Rec r;
   r.valid = false;
-  r.va = va;
-  const uint32_t flags = (uint32_t)(w1 >> 56);
-  if (!(flags & MPSF_ENTRY_VALID)) return r;
-  const uint32_t ch = (uint32_t)w1;
-  r.eng = (int)((w1 >> 32) & 0xFF);
-  r.acc = (int)((w1 >> 40) & 0xFF);
-  r.kind = (int)((w1 >> 48) & 0xFF);
+  r.va = (uint64_t)e.x | ((uint64_t)e.y << 32);
+  const uint32_t w3 = e.w;
+  if (!(w3 >> 24 & MPSF_ENTRY_VALID)) return r;
+  const uint32_t ch = e.z;
+  r.eng = (int)(w3 & 0xFF);
+  const int acc = (int)((w3 >> 8) & 0xFF);
+  r.kind = (int)((w3 >> 16) & 0xFF);
   if (ch >= W.n_channels) { raise_err(S, EB_NO_CHANNEL, gidx); return r; }
-  const mpsf_channel_entry ce = kStaged ? sm.channels[ch] : W.channels[ch];
+  const mpsf_channel_entry ce = v.channels[ch];
   if (ce.client >= W.n_clients) { raise_err(S, EB_NO_CHANNEL, gidx); return r; }
   r.c = ce.client;
   r.ceng = ce.engine;
+  r.sa = (kStaged ? v.cinfo[r.c] : W.clients[r.c].mode) & 1;
   r.group = 0;
+  r.at.ridx = -1; r.at.in_range = false; r.at.guard = false; r.at.rid = NO_RID;
   if (r.kind == 0) {
-    if (r.eng > 2 || r.acc > 2) { raise_err(S, EB_BAD_ENTRY, gidx); return r; }
+    if (r.eng > 2 || acc > 2) { raise_err(S, EB_BAD_ENTRY, gidx); return r; }
     if (r.eng != r.ceng) { raise_err(S, EB_MISMATCH, gidx); return r; }
-    if (va >= VA_LIMIT) { raise_err(S, EB_VA, gidx); return r; }
-    const uint32_t lo = sm.client_off[r.c], hi = sm.client_off[r.c + 1];
-    r.at = attribute(sm.ranges, W.page_state, lo, hi, va);
-    const bool has = r.at.in_range;
-    r.s = classify(r.eng, r.acc, has, r.at.kind, r.at.lifecycle, r.at.migratable, r.at.st);
+    if (r.va >= VA_LIMIT) { raise_err(S, EB_VA, gidx); return r; }
+    r.at = attribute(v.ranges, W.page_state, v.client_off[r.c], v.client_off[r.c + 1], r.va);
+    const uint32_t li = lut_index(r.eng, acc, r.at);
+    r.s = v.lut[li];
     r.repl = s_replayable(r.s);
-    if (r.repl && r.eng == 0 && r.acc != 2) {
-      const int sr = classify(0, 0, has, r.at.kind, r.at.lifecycle, r.at.migratable, r.at.st);
-      const int sw = classify(0, 1, has, r.at.kind, r.at.lifecycle, r.at.migratable, r.at.st);
-      r.group = dedup_group(0, r.acc, sr, sw);
+    if (r.eng == 0 && acc != 2) {
+      const uint32_t base = li & ~12u;                  // acc bits cleared
+      r.group = (acc == 1 && v.lut[base | 4u] != v.lut[base]) ? 1u : 0u;
     } else {
-      r.group = dedup_group(r.eng, r.acc, 0, 0);
+      r.group = r.eng == 0 ? 2u : (uint32_t)(2 + r.eng);
     }
   } else if (r.kind >= 1 && r.kind <= 5) {
     r.s = 23 + r.kind - 1;
     r.repl = true;
-    r.at.ridx = -1; r.at.in_range = false; r.at.guard = false; r.at.rid = NO_RID;
   } else if (r.kind >= 8 && r.kind <= 12) {
     r.s = 18 + r.kind - 8;
     r.repl = false;
-    r.at.ridx = -1; r.at.in_range = false; r.at.guard = false; r.at.rid = NO_RID;
   } else {
     raise_err(S, EB_BAD_ENTRY, gidx);
     return r;
@@ -197,111 +240,155 @@ __device__ __forceinline__ uint32_t ok32_of(bool repl, uint64_t gidx) {
   return (repl ? 0u : 0x80000000u) | (uint32_t)gidx;
 }
 
-// ---- pass 1 ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t dd_slot(const World& W, const Rec& r) {
+  return W.dd_groups == 1 ? r.at.slot : r.at.slot * W.dd_groups + r.group;
+}
+
+// ---- tile pipeline ------------------------------------------------------------------------
+// Thread 0 issues bulk copies; every thread waits on the slot's mbarrier.
+struct Pipe {
+  uint8_t* buf;
+  uint64_t* bar;
+  uint32_t* tids;   // tile id per slot (finalize: dynamic scheduling)
+  uint64_t pol;
+};
+
+__device__ __forceinline__ void pipe_issue(const Pipe& p, int slot, const mpsf_fault_entry* in, uint64_t n, uint64_t t) {
+  const uint64_t start = t * TILE;
+  const uint64_t cnt = n - start < (uint64_t)TILE ? n - start : (uint64_t)TILE;
+  const uint32_t bytes = (uint32_t)(cnt * 16);
+  mbar_expect_tx(p.bar + slot, bytes);
+  bulk_load(p.buf + (size_t)slot * TILE_BYTES, in + start, bytes, p.bar + slot, p.pol);
+}
+
+__device__ __forceinline__ Pipe pipe_init(uint8_t* sm, const Layout& L) {
+  Pipe p;
+  p.buf = sm + L.tiles;
+  p.bar = reinterpret_cast<uint64_t*>(sm + L.bars);
+  p.tids = reinterpret_cast<uint32_t*>(sm + L.tids);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NBUF; ++s) mbar_init(p.bar + s, 1);
+    fence_mbar_init();
+  }
+  p.pol = policy_evict_first();
+  return p;
+}
+
+// ---- pass 1 ---------------------------------------------------------------------------------
 template <bool kStaged>
-__global__ void __launch_bounds__(BLOCK) k_scan(World W, Scratch S, const mpsf_fault_entry* __restrict__ in,
-                                                uint64_t n, Params P, unsigned long long* __restrict__ counts) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  const Smem sm = stage<kStaged>(smem, W, true);
-  if (kStaged) __syncthreads();
-  const bool iso = P.flags & MPSF_PF_ISOLATION;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t ntiles = (n + TILE - 1) / TILE;
-  const ulonglong2* src = reinterpret_cast<const ulonglong2*>(in);
-  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const uint64_t base = t * TILE + (uint64_t)warp * (32 * EPT) + lane;
-    ulonglong2 e[EPT];
-#pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-      const uint64_t i = base + (uint64_t)k * 32;
-      e[k] = i < n ? __ldg(src + i) : make_ulonglong2(0ull, 0ull);
-    }
-#pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-      const uint64_t i = base + (uint64_t)k * 32;
-      const uint64_t gidx = P.base_index + i;
-      const Rec r = decode<kStaged>(W, sm, S, e[k].x, e[k].y, gidx);
-      if (!r.valid) continue;
-      const uint32_t c = r.c;
-      if (kStaged) atomicAdd(sm.counts + c * NSCEN + r.s, 1u);
-      else atomicAdd(counts + (uint64_t)c * NSCEN + r.s, 1ull);
-      const uint32_t mode = client_mode(sm, W, c, kStaged);
-      if (s_trap(r.s)) {
-        const unsigned long long v = (gidx << 8) | (unsigned long long)r.s;
-        if (mode == 0) min64(&S.glob->trap_mps, v);
-        else if (kStaged) min64c(S.trap_sa + c, sm.trap_sa + c, v);
-        else min64(S.trap_sa + c, v);
-        continue;
+__device__ __forceinline__ void scan_entry(const World& W, const View& v, const Scratch& S, const Params& P,
+                                           uint4 e, uint64_t gidx, unsigned long long* counts) {
+  const Rec r = decode<kStaged>(W, v, S, e, gidx);
+  if (!r.valid) return;
+  const uint32_t c = r.c;
+  if (kStaged) atomicAdd(v.counts + c * NSCEN + r.s, 1u);
+  else atomicAdd(counts + (uint64_t)c * NSCEN + r.s, 1ull);
+  if (s_trap(r.s)) {
+    const unsigned long long t = (gidx << 8) | (unsigned long long)r.s;
+    if (!r.sa) min64(&S.glob->trap_mps, t);
+    else if (kStaged) min64c(S.trap_sa + c, v.trap_sa + c, t);
+    else min64(S.trap_sa + c, t);
+    return;
+  }
+  const uint32_t ok = ok32_of(r.repl, gidx);
+  const bool serv = s_serviceable(r.s);
+  if (s_parse(r.s) || (!serv && !(P.flags & MPSF_PF_ISOLATION))) {   // fatal report (pipeline.py:168-182)
+    const unsigned long long t = ((unsigned long long)ok << 8) | (unsigned long long)r.s;
+    if (r.sa) { if (kStaged) min64c(S.ft_sa + c, v.ft_sa + c, t); else min64(S.ft_sa + c, t); }
+    else if (r.ceng == 1) { if (kStaged) min64c(S.ft_ce + c, v.ft_ce + c, t); else min64(S.ft_ce + c, t); }
+    else min64(&S.glob->ft_gr, t);
+  } else if (!serv) {                                                // isolation-eligible (pipeline.py:177-179)
+    if (!r.at.in_range) {
+      if (kStaged) min32c(S.iso1 + c, v.iso1 + c, ok); else min32(S.iso1 + c, ok);
+      if (r.at.guard) {
+        if (kStaged) min32c(S.nr0 + r.at.ridx, v.nr0 + r.at.ridx, ok); else min32(S.nr0 + r.at.ridx, ok);
+      } else if (!hash_min(S.hnr, S.ctrl, nr_key(c, 0, r.va >> 12), ok)) {
+        atomicOr(S.ctrl + C_OVF, 1u);
       }
-      const uint32_t ok = ok32_of(r.repl, gidx);
-      const bool parse = s_parse(r.s);
-      const bool serv = s_serviceable(r.s);
-      if (parse || (!serv && !iso)) {                       // fatal report (pipeline.py:168-182)
-        const unsigned long long v = ((unsigned long long)ok << 8) | (unsigned long long)r.s;
-        if (mode == 1) { if (kStaged) min64c(S.ft_sa + c, sm.ft_sa + c, v); else min64(S.ft_sa + c, v); }
-        else if (r.ceng == 1) { if (kStaged) min64c(S.ft_ce + c, sm.ft_ce + c, v); else min64(S.ft_ce + c, v); }
-        else min64(&S.glob->ft_gr, v);
-      } else if (!serv) {                                   // isolation-eligible (pipeline.py:177-179)
-        if (kStaged) min32c(S.elig + c, sm.elig + c, ok); else min32(S.elig + c, ok);
-        if (!r.at.in_range) {
-          if (kStaged) min32c(S.iso1 + c, sm.iso1 + c, ok); else min32(S.iso1 + c, ok);
-          if (r.at.guard) {
-            if (kStaged) min32c(S.nr0 + r.at.ridx, sm.nr0 + r.at.ridx, ok); else min32(S.nr0 + r.at.ridx, ok);
-          } else if (!hash_min(S.hnr, S.ctrl, nr_key(c, 0, r.va >> 12), ok)) {
-            atomicOr(S.ctrl + C_OVF, 1u);
-          }
-        } else if (r.at.kind == 0) {
-          if (kStaged) min32c(S.iso2 + c, sm.iso2 + c, ok); else min32(S.iso2 + c, ok);
-        } else {
-          if (kStaged) {
-            min32c(S.iso3 + c, sm.iso3 + c, ok);
-            min32c(S.ext + r.at.ridx, sm.ext + r.at.ridx, ok);
-          } else {
-            min32(S.iso3 + c, ok);
-            min32(S.ext + r.at.ridx, ok);
-          }
-        }
-      }
-      if (r.kind == 0 && r.repl) {                          // dedup insert (rule C2)
-        const uint32_t v = ((uint32_t)gidx << 3) | r.group;
-        bool to_hash = !(r.at.in_range || r.at.guard);
-        if (!to_hash) {
-          uint32_t* slot = S.dd + r.at.slot;
-          uint32_t cur = __ldcg(slot);
-          while (true) {
-            if (cur == EMPTY32) {
-              const uint32_t prev = atomicCAS(slot, EMPTY32, v);
-              if (prev == EMPTY32) break;
-              cur = prev;
-              continue;
-            }
-            if ((cur & 7u) == r.group) { if (cur > v) atomicMin(slot, v); break; }
-            to_hash = true;
-            break;
-          }
-        }
-        if (to_hash && !hash_min(S.hdd, S.ctrl, dedup_key(c, r.eng, r.s, r.va >> 12), (uint32_t)gidx))
-          atomicOr(S.ctrl + C_OVF, 1u);
+    } else if (r.at.kind == 0) {
+      if (kStaged) min32c(S.iso2 + c, v.iso2 + c, ok); else min32(S.iso2 + c, ok);
+    } else {
+      if (kStaged) {
+        min32c(S.iso3 + c, v.iso3 + c, ok);
+        min32c(S.ext + r.at.ridx, v.ext + r.at.ridx, ok);
+      } else {
+        min32(S.iso3 + c, ok);
+        min32(S.ext + r.at.ridx, ok);
       }
     }
   }
-  if (kStaged) {
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < NSCEN * W.n_clients; i += blockDim.x) {
-      const uint32_t v = sm.counts[i];
-      if (v) atomicAdd(counts + i, (unsigned long long)v);
+  if (r.kind == 0 && r.repl) {                                       // dedup insert (rule C2)
+    const uint32_t val = ((uint32_t)gidx << 3) | r.group;
+    bool to_hash = !(r.at.in_range || r.at.guard);
+    if (!to_hash) {
+      uint32_t* slot = S.dd + dd_slot(W, r);
+      uint32_t cur = __ldcg(slot);
+      while (true) {
+        if (cur == EMPTY32) {
+          const uint32_t prev = atomicCAS(slot, EMPTY32, val);
+          if (prev == EMPTY32) break;
+          cur = prev;
+          continue;
+        }
+        if ((cur & 7u) == r.group) { if (cur > val) atomicMin(slot, val); break; }
+        to_hash = true;
+        break;
+      }
     }
+    if (to_hash && !hash_min(S.hdd, S.ctrl, dedup_key(c, r.eng, r.s, r.va >> 12), (uint32_t)gidx))
+      atomicOr(S.ctrl + C_OVF, 1u);
   }
 }
 
-// ---- per-client resolution ----------------------------------------------------------
-// Rules C4-C7 of SURVEY.md Appendix C (C9 "ROUND 1" + fate).  One block.
+template <bool kStaged>
+__global__ void __launch_bounds__(BLOCK, 1) k_scan(World W, Scratch S, const mpsf_fault_entry* __restrict__ in,
+                                                   uint64_t n, Params P, unsigned long long* __restrict__ counts,
+                                                   uint32_t* __restrict__ count_part) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const Layout L = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, false);
+  const View v = setup<kStaged>(smem, L, W, S, true, false);
+  Pipe p = pipe_init(smem, L);
+  const uint64_t ntiles = (n + TILE - 1) / TILE;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NBUF; ++s) {
+      const uint64_t t = blockIdx.x + (uint64_t)s * gridDim.x;
+      if (t < ntiles) pipe_issue(p, s, in, n, t);
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t j = 0;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+    const int slot = j & 1;
+    mbar_wait(p.bar + slot, (j >> 1) & 1);
+    const uint4* tile = reinterpret_cast<const uint4*>(p.buf + (size_t)slot * TILE_BYTES);
+    const uint64_t start = t * TILE;
+#pragma unroll 1
+    for (int k = 0; k < EPT; ++k) {
+      const int li = warp * (32 * EPT) + k * 32 + lane;
+      const uint64_t i = start + li;
+      if (i < n) scan_entry<kStaged>(W, v, S, P, tile[li], P.base_index + i, counts);
+    }
+    __syncthreads();
+    const uint64_t nt = t + (uint64_t)NBUF * gridDim.x;
+    if (threadIdx.x == 0 && nt < ntiles) pipe_issue(p, slot, in, n, nt);
+  }
+  if (kStaged) {
+    __syncthreads();
+    uint32_t* part = count_part + (uint64_t)blockIdx.x * NSCEN * W.n_clients;
+    for (uint32_t i = threadIdx.x; i < NSCEN * W.n_clients; i += blockDim.x) part[i] = v.counts[i];
+  }
+}
+
+// ---- per-client resolution ------------------------------------------------------------------
+// Rules C4-C7 of SURVEY.md Appendix C (C9 "ROUND 1" + fate).  Block 0; blocks 1.. reduce counts.
 __device__ inline void kill_thresholds(const Params& P, uint32_t m1, uint32_t m2, uint32_t m3,
                                        bool use_m2, bool& kill_all, uint32_t& tie) {
   kill_all = false;
   tie = EMPTY32;
   const uint32_t lat[3] = {P.m1_us, P.m2_us, P.m3_us};
   const uint32_t v[3] = {m1, m2, m3};
+#pragma unroll
   for (int m = 0; m < 3; ++m) {
     if (m == 1 && !use_m2) continue;
     if (v[m] == EMPTY32) continue;
@@ -310,7 +397,19 @@ __device__ inline void kill_thresholds(const Params& P, uint32_t m1, uint32_t m2
   }
 }
 
-__global__ void k_resolve(World W, Scratch S, Params P, mpsf_client_verdict* __restrict__ verdict) {
+__global__ void k_resolve(World W, Scratch S, Params P, mpsf_client_verdict* __restrict__ verdict,
+                          const uint32_t* __restrict__ count_part, uint32_t n_parts,
+                          unsigned long long* __restrict__ counts) {
+  if (blockIdx.x > 0) {
+    // counts: bins x parts partial sums (parts == 0 when counts went straight to global)
+    const uint32_t bins = NSCEN * W.n_clients;
+    for (uint32_t b = (blockIdx.x - 1) * blockDim.x + threadIdx.x; b < bins; b += (gridDim.x - 1) * blockDim.x) {
+      unsigned long long s = 0;
+      for (uint32_t q = 0; q < n_parts; ++q) s += __ldcg(count_part + (uint64_t)q * bins + b);
+      if (n_parts) counts[b] = s;
+    }
+    return;
+  }
   __shared__ int s_general;
   if (threadIdx.x == 0) s_general = 0;
   __syncthreads();
@@ -337,7 +436,8 @@ __global__ void k_resolve(World W, Scratch S, Params P, mpsf_client_verdict* __r
     else if (sa) rel = trapped ? REL_PRE : (sa_applied ? (long long)(fsa >> 8) : REL_NONE);
     else rel = gr_rel;
     const bool ce_applied = ce_alive0 && fce != EMPTY64 && !(rel < (long long)(fce >> 8));
-    const uint32_t elig = S.elig[c];
+    const uint32_t i1 = S.iso1[c], i2 = S.iso2[c], i3 = S.iso3[c];
+    const bool elig = (i1 & i2 & i3) != EMPTY32;
     CState cs;
     cs.rel = rel;
     cs.ft_ce_ok = fce == EMPTY64 ? EMPTY32 : (uint32_t)(fce >> 8);
@@ -345,11 +445,11 @@ __global__ void k_resolve(World W, Scratch S, Params P, mpsf_client_verdict* __r
     cs.trap_sa_idx = tsa == EMPTY64 ? EMPTY32 : (uint32_t)(tsa >> 8);
     bool kill_all;
     uint32_t tie;
-    kill_thresholds(P, S.iso1[c], S.iso2[c], S.iso3[c], false, kill_all, tie);
+    kill_thresholds(P, i1, i2, i3, false, kill_all, tie);
     cs.kill_tie = tie;
     cs.flags = (alive0 ? CS_ALIVE0 : 0u) | (sa ? CS_SA : 0u) | (ce_alive0 ? CS_CE_ALIVE0 : 0u) |
                ((!sa && (!ce_alive0 || ce_applied)) ? CS_CE_TORN : 0u) | (kill_all ? CS_KILL_ALL : 0u) |
-               (trapped ? CS_TRAPPED : 0u) | (elig != EMPTY32 ? CS_ELIG : 0u);
+               (trapped ? CS_TRAPPED : 0u) | (elig ? CS_ELIG : 0u);
     cs.pad = 0;
     S.cstate[c] = cs;
     mpsf_client_verdict v;
@@ -358,7 +458,7 @@ __global__ void k_resolve(World W, Scratch S, Params P, mpsf_client_verdict* __r
       if (trapped) { v.state = 1; v.reason = 2; v.notifier = (uint8_t)((sa ? tsa : trap_mps) & 0xFF); }
       else if (!sa && gr_applied) { v.state = 1; v.reason = 2; v.notifier = (uint8_t)(ft_gr & 0xFF); }
       else if (sa_applied) { v.state = 1; v.reason = 2; v.notifier = (uint8_t)(fsa & 0xFF); }
-      else if (elig != EMPTY32) { v.state = 1; v.reason = 1; v.notifier = ce_applied ? (uint8_t)(fce & 0xFF) : 0xFF; }
+      else if (elig) { v.state = 1; v.reason = 1; v.notifier = ce_applied ? (uint8_t)(fce & 0xFF) : 0xFF; }
       else if (ce_applied) { v.state = 0; v.reason = 0; v.notifier = (uint8_t)(fce & 0xFF); }
       else { v.state = 0; v.reason = 0; v.notifier = 0xFF; }
     } else {
@@ -367,7 +467,7 @@ __global__ void k_resolve(World W, Scratch S, Params P, mpsf_client_verdict* __r
                    : ((!sa && gr_applied) ? (uint8_t)(ft_gr & 0xFF) : 0xFE);
     }
     verdict[c] = v;
-    if (iso && elig != EMPTY32 && (rel != REL_NONE || P.m2_us <= P.benign_us)) general = 1;
+    if (iso && elig && (rel != REL_NONE || P.m2_us <= P.benign_us)) general = 1;
   }
   if (general) atomicOr(&s_general, 1);
   __syncthreads();
@@ -379,11 +479,11 @@ __global__ void k_resolve(World W, Scratch S, Params P, mpsf_client_verdict* __r
   }
 }
 
-// ---- general path (rule C3 epochs) ----------------------------------------------------
-__device__ __forceinline__ uint32_t dedup_rep(const Scratch& S, const Rec& r) {
+// ---- general path (rule C3 epochs) ----------------------------------------------------------
+__device__ __forceinline__ uint32_t dedup_rep(const World& W, const Scratch& S, const Rec& r) {
   // smallest global index among records of r's dedup key
   if (r.at.in_range || r.at.guard) {
-    const uint32_t cur = __ldcg(S.dd + r.at.slot);
+    const uint32_t cur = __ldcg(S.dd + dd_slot(W, r));
     if (cur != EMPTY32 && (cur & 7u) == r.group) return cur >> 3;
   }
   return hash_get(S.hdd, dedup_key(r.c, r.eng, r.s, r.va >> 12));
@@ -398,72 +498,87 @@ __device__ __forceinline__ uint32_t nr_lookup(const Scratch& S, const Rec& r, bo
   return hash_get(S.hnr, nr_key(r.c, 0, r.va >> 12));
 }
 
-__global__ void k_clear_nr1(Scratch S, uint64_t n_pages) {
-  if (__ldcg(S.ctrl + C_PATH) == 0) return;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_pages; i += (uint64_t)gridDim.x * blockDim.x)
-    S.nr1[i] = EMPTY32;
-}
-
 // stage 1: epoch-1 NR keys, exact M1 / M3 / direct-M2 minima (giso[3*c + m-1])
 // stage 2: noRange non-first records -> M2 minima (needs NR complete)
 template <bool kStaged, int kStage>
-__global__ void __launch_bounds__(BLOCK) k_general(World W, Scratch S, const mpsf_fault_entry* __restrict__ in,
-                                                   uint64_t n, Params P) {
-  if (__ldcg(S.ctrl + C_PATH) == 0) return;
-  extern __shared__ __align__(16) uint8_t smem[];
-  const Smem sm = stage<kStaged>(smem, W, false);
-  if (kStaged) __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t ntiles = (n + TILE - 1) / TILE;
-  const ulonglong2* src = reinterpret_cast<const ulonglong2*>(in);
-  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const uint64_t base = t * TILE + (uint64_t)warp * (32 * EPT) + lane;
-    ulonglong2 e[EPT];
-#pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-      const uint64_t i = base + (uint64_t)k * 32;
-      e[k] = i < n ? __ldg(src + i) : make_ulonglong2(0ull, 0ull);
-    }
-#pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-      const uint64_t i = base + (uint64_t)k * 32;
-      const uint64_t gidx = P.base_index + i;
-      const Rec r = decode<kStaged>(W, sm, S, e[k].x, e[k].y, gidx);
-      if (!r.valid || r.kind != 0 || s_serviceable(r.s)) continue;   // elig translation only
-      if (r.repl && dedup_rep(S, r) != (uint32_t)gidx) continue;      // dups excluded (C2)
-      const uint32_t ok = ok32_of(r.repl, gidx);
-      const long long rel = S.cstate[r.c].rel;
-      const bool epoch1 = rel < (long long)ok;
-      const bool no_range = !r.at.in_range || epoch1;
-      uint32_t* giso = S.giso + 3 * r.c;
-      if (kStage == 1) {
-        if (no_range) {
-          min32(giso + 0, ok);
-          if (epoch1) {
-            if (r.at.in_range || r.at.guard) min32(S.nr1 + r.at.slot, ok);
-            else if (!hash_min(S.hnr, S.ctrl, nr_key(r.c, 1, r.va >> 12), ok)) atomicOr(S.ctrl + C_OVF, 1u);
-          }
-        } else if (r.at.kind == 0) {
-          min32(giso + 1, ok);
-        } else {
-          const uint32_t ext = __ldcg(S.ext + r.at.ridx);
-          if (ok == ext && (long long)ext < rel) min32(giso + 2, ok);
-          else min32(giso + 1, ok);
-        }
-      } else {
-        if (no_range && nr_lookup(S, r, epoch1) != ok) min32(giso + 1, ok);
+__device__ __forceinline__ void general_entry(const World& W, const View& v, const Scratch& S, const Params& P,
+                                              uint4 e, uint64_t gidx) {
+  const Rec r = decode<kStaged>(W, v, S, e, gidx);
+  if (!r.valid || r.kind != 0 || s_serviceable(r.s)) return;      // eligible translation records only
+  const long long rel = v.cst[r.c].rel;
+  const uint32_t ok = ok32_of(r.repl, gidx);
+  if (rel == REL_NONE && P.m2_us > P.benign_us) return;           // pass-1 minima already exact
+  if (r.repl && dedup_rep(W, S, r) != (uint32_t)gidx) return;       // dups excluded (C2)
+  const bool epoch1 = rel < (long long)ok;
+  const bool no_range = !r.at.in_range || epoch1;
+  uint32_t* giso = S.giso + 3 * r.c;
+  if (kStage == 1) {
+    if (no_range) {
+      min32(giso + 0, ok);
+      if (epoch1) {
+        if (r.at.in_range || r.at.guard) min32(S.nr1 + r.at.slot, ok);
+        else if (!hash_min(S.hnr, S.ctrl, nr_key(r.c, 1, r.va >> 12), ok)) atomicOr(S.ctrl + C_OVF, 1u);
       }
+    } else if (r.at.kind == 0) {
+      min32(giso + 1, ok);
+    } else {
+      const uint32_t ext = __ldcg(S.ext + r.at.ridx);
+      if (ok == ext && (long long)ext < rel) min32(giso + 2, ok);
+      else min32(giso + 1, ok);
     }
+  } else {
+    if (no_range && nr_lookup(S, r, epoch1) != ok) min32(giso + 1, ok);
+  }
+}
+
+template <bool kStaged, int kStage>
+__global__ void __launch_bounds__(BLOCK, 1) k_general(World W, Scratch S, const mpsf_fault_entry* __restrict__ in,
+                                                      uint64_t n, Params P) {
+  if (__ldcg(S.ctrl + C_PATH) == 0) return;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const Layout L = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, true);
+  const View v = setup<kStaged>(smem, L, W, S, false, true);
+  Pipe p = pipe_init(smem, L);
+  const uint64_t ntiles = (n + TILE - 1) / TILE;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NBUF; ++s) {
+      const uint64_t t = blockIdx.x + (uint64_t)s * gridDim.x;
+      if (t < ntiles) pipe_issue(p, s, in, n, t);
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t j = 0;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+    const int slot = j & 1;
+    mbar_wait(p.bar + slot, (j >> 1) & 1);
+    const uint4* tile = reinterpret_cast<const uint4*>(p.buf + (size_t)slot * TILE_BYTES);
+    const uint64_t start = t * TILE;
+#pragma unroll 1
+    for (int k = 0; k < EPT; ++k) {
+      const int li = warp * (32 * EPT) + k * 32 + lane;
+      const uint64_t i = start + li;
+      if (i < n) general_entry<kStaged, kStage>(W, v, S, P, tile[li], P.base_index + i);
+    }
+    __syncthreads();
+    const uint64_t nt = t + (uint64_t)NBUF * gridDim.x;
+    if (threadIdx.x == 0 && nt < ntiles) pipe_issue(p, slot, in, n, nt);
   }
 }
 
 __global__ void k_resolve2(World W, Scratch S, Params P) {
   if (__ldcg(S.ctrl + C_PATH) == 0) return;
   for (uint32_t c = threadIdx.x; c < W.n_clients; c += blockDim.x) {
+    CState cs = S.cstate[c];
+    if (cs.rel == REL_NONE && P.m2_us > P.benign_us) continue;     // pass-1 minima are exact
     bool kill_all;
     uint32_t tie;
-    kill_thresholds(P, S.giso[3 * c], S.giso[3 * c + 1], S.giso[3 * c + 2], true, kill_all, tie);
-    CState cs = S.cstate[c];
+    uint32_t g0 = S.giso[3 * c], g1 = S.giso[3 * c + 1], g2 = S.giso[3 * c + 2];
+    if (cs.rel == REL_NONE) {                 // only M2 needed recomputing: keep exact M1 / M3
+      g0 = S.iso1[c];
+      g2 = S.iso3[c];
+    }
+    kill_thresholds(P, g0, g1, g2, true, kill_all, tie);
     cs.kill_tie = tie;
     cs.flags = (cs.flags & ~CS_KILL_ALL) | (kill_all ? CS_KILL_ALL : 0u);
     S.cstate[c] = cs;
@@ -479,109 +594,110 @@ __device__ __forceinline__ unsigned long long lb_pack(uint32_t nc, uint32_t nd) 
   return ((unsigned long long)nd << 31) | nc;
 }
 
+// Resolves one entry; writes the OutRecord and returns (cancel, rep, dedup key).
 template <bool kStaged>
-__global__ void __launch_bounds__(BLOCK) k_finalize(World W, Scratch S, const mpsf_fault_entry* __restrict__ in,
-                                                    uint64_t n, Params P, mpsf_out_record* __restrict__ out,
-                                                    unsigned long long* __restrict__ dkeys,
-                                                    uint32_t* __restrict__ didx, uint32_t* __restrict__ cancel) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ uint32_t s_tile;
+__device__ __forceinline__ void finalize_entry(const World& W, const View& v, const Scratch& S, const Params& P,
+                                               const Globals& G, uint4 e, uint64_t gidx,
+                                               mpsf_out_record& o, bool& canc, bool& rep,
+                                               unsigned long long& key) {
+  o.rid = NO_RID; o.scenario = 0xFF; o.verdict = 0; o.client = 0xFFFF;
+  canc = false; rep = false; key = 0;
+  const Rec r = decode<kStaged>(W, v, S, e, gidx);
+  if (!r.valid) return;
+  const CState cs = v.cst[r.c];
+  o.scenario = (uint8_t)r.s;
+  o.client = (uint16_t)r.c;
+  o.rid = r.at.in_range ? r.at.rid : NO_RID;
+  if (s_trap(r.s)) {
+    // raise_sm_trap at raise time (pipeline.py:151-155); a second trap on a destroyed
+    // TSG is cancelled (the reference raises UnknownTsg)
+    if (!(cs.flags & CS_SA)) canc = !(G.gr_alive0 && (uint32_t)gidx == G.trap_mps_idx);
+    else canc = !((cs.flags & CS_ALIVE0) && (uint32_t)gidx == cs.trap_sa_idx);
+    o.verdict = canc ? 0x10 : 0;
+    return;
+  }
+  const bool parse = s_parse(r.s), serv = s_serviceable(r.s);
+  const int outcome = parse ? 3 : (serv ? 1 : ((P.flags & MPSF_PF_ISOLATION) ? 2 : 3));
+  const uint32_t ok = ok32_of(r.repl, gidx);
+  uint32_t rep_ok = ok;
+  bool dup = false;
+  if (r.kind == 0 && r.repl) {
+    const uint32_t ri = dedup_rep(W, S, r);
+    dup = ri != (uint32_t)gidx;
+    rep_ok = ri;                          // replayable: ok32 == idx
+    rep = !dup;
+    if (rep) key = dedup_key(r.c, r.eng, r.s, r.va >> 12);
+  }
+  int mech = 0;
+  if (outcome == 3) {                     // fatal: applies iff its TSG still lives (C4)
+    bool applied;
+    if (cs.flags & CS_SA) applied = (cs.flags & CS_ALIVE0) && !(cs.flags & CS_TRAPPED) && rep_ok == cs.ft_sa_ok;
+    else if (r.ceng == 1) applied = (cs.flags & CS_CE_ALIVE0) && rep_ok == cs.ft_ce_ok && !(cs.rel < (long long)rep_ok);
+    else applied = rep_ok == G.ft_gr_ok;
+    canc = !applied;
+  } else if (outcome == 1) {              // benign completion dropped on a torn channel (C5)
+    canc = cs.rel != REL_NONE || (r.ceng == 1 && (cs.flags & CS_CE_TORN)) ||
+           (cs.flags & CS_KILL_ALL) || rep_ok > cs.kill_tie;
+  } else if (!dup) {                      // isolation mechanism (C3)
+    const bool epoch1 = cs.rel < (long long)ok;
+    if (!r.at.in_range || epoch1) mech = nr_lookup(S, r, epoch1) == ok ? 1 : 2;
+    else if (r.at.kind == 0) mech = 2;
+    else mech = __ldcg(S.ext + r.at.ridx) == ok ? 3 : 2;
+  }
+  o.verdict = (uint8_t)(outcome | (mech << 2) | (canc ? 0x10 : 0) | (dup ? 0x20 : 0) | (r.repl ? 0x40 : 0));
+}
+
+template <bool kStaged>
+__global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const mpsf_fault_entry* __restrict__ in,
+                                                       uint64_t n, Params P, mpsf_out_record* __restrict__ out,
+                                                       unsigned long long* __restrict__ dkeys,
+                                                       uint32_t* __restrict__ didx, uint32_t* __restrict__ cancel) {
+  extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint32_t s_wc[WARPS], s_wd[WARPS];
   __shared__ uint32_t s_pc, s_pd;
   if (__ldcg(S.ctrl + C_ERR) != 0) return;
-  const Smem sm = stage<kStaged>(smem, W, false);
-  // per-client derived state: reuse the cache region (kStaged) or read from global
-  CState* cst = S.cstate;
-  if (kStaged) {
-    CState* dst = reinterpret_cast<CState*>(sm.ft_ce);   // ft_ce..iso3 region >= 40 B/client
-    for (uint32_t c = threadIdx.x; c < W.n_clients; c += blockDim.x) dst[c] = S.cstate[c];
-    cst = dst;
-    __syncthreads();
-  }
-  const bool iso = P.flags & MPSF_PF_ISOLATION;
+  const Layout L = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, true);
+  const View v = setup<kStaged>(smem, L, W, S, false, true);
+  Pipe p = pipe_init(smem, L);
   const Globals G = *S.glob;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t ntiles = (uint32_t)((n + TILE - 1) / TILE);
-  const ulonglong2* src = reinterpret_cast<const ulonglong2*>(in);
-  const unsigned lt_mask = (1u << lane) - 1u;
-  while (true) {
-    if (threadIdx.x == 0) s_tile = atomicAdd(S.ctrl + C_TILE_FIN, 1u);
-    __syncthreads();
-    const uint32_t t = s_tile;
-    if (t >= ntiles) break;
-    const uint64_t base = (uint64_t)t * TILE + (uint64_t)warp * (32 * EPT) + lane;
-    ulonglong2 e[EPT];
-#pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-      const uint64_t i = base + (uint64_t)k * 32;
-      e[k] = i < n ? __ldcs(src + i) : make_ulonglong2(0ull, 0ull);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NBUF; ++s) {
+      const uint32_t t = atomicAdd(S.ctrl + C_TILE_FIN, 1u);
+      p.tids[s] = t;
+      if (t < ntiles) pipe_issue(p, s, in, n, t);
     }
-    uint32_t cflag = 0, dflag = 0;             // bit k: entry k cancelled / dedup representative
-    unsigned long long key[EPT];
-    uint32_t wc = 0, wd = 0;                   // warp totals
-    uint32_t my_c_off[EPT], my_d_off[EPT];
-#pragma unroll
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (uint32_t j = 0;; ++j) {
+    const int slot = j & 1;
+    const uint32_t t = p.tids[slot];
+    if (t >= ntiles) break;
+    mbar_wait(p.bar + slot, (j >> 1) & 1);
+    uint4* tile = reinterpret_cast<uint4*>(p.buf + (size_t)slot * TILE_BYTES);
+    const uint64_t start = (uint64_t)t * TILE;
+    uint32_t wc = 0, wd = 0;
+#pragma unroll 1
     for (int k = 0; k < EPT; ++k) {
-      const uint64_t i = base + (uint64_t)k * 32;
-      const uint64_t gidx = P.base_index + i;
-      key[k] = 0;
-      const Rec r = decode<kStaged>(W, sm, S, e[k].x, e[k].y, gidx);
+      const int li = warp * (32 * EPT) + k * 32 + lane;
+      const uint64_t i = start + li;
       mpsf_out_record o;
-      o.rid = NO_RID; o.scenario = 0xFF; o.verdict = 0; o.client = 0xFFFF;
       bool canc = false, rep = false;
-      if (r.valid) {
-        const CState cs = cst[r.c];
-        o.scenario = (uint8_t)r.s;
-        o.client = (uint16_t)r.c;
-        o.rid = r.at.in_range ? r.at.rid : NO_RID;
-        if (s_trap(r.s)) {
-          // raise_sm_trap at raise time (pipeline.py:151-155); a second trap on a destroyed
-          // TSG is cancelled (the reference raises UnknownTsg)
-          if (!(cs.flags & CS_SA)) canc = !(G.gr_alive0 && (uint32_t)gidx == G.trap_mps_idx);
-          else canc = !((cs.flags & CS_ALIVE0) && (uint32_t)gidx == cs.trap_sa_idx);
-          o.verdict = canc ? 0x10 : 0;
-        } else {
-          const bool parse = s_parse(r.s), serv = s_serviceable(r.s);
-          const int outcome = parse ? 3 : (serv ? 1 : (iso ? 2 : 3));
-          const uint32_t ok = ok32_of(r.repl, gidx);
-          uint32_t rep_ok = ok;
-          bool dup = false;
-          if (r.kind == 0 && r.repl) {
-            const uint32_t ri = dedup_rep(S, r);
-            dup = ri != (uint32_t)gidx;
-            rep_ok = ri;                          // replayable: ok32 == idx
-            rep = !dup;
-            if (rep) key[k] = dedup_key(r.c, r.eng, r.s, r.va >> 12);
-          }
-          int mech = 0;
-          if (outcome == 3) {                     // fatal: applies iff its TSG still lives (C4)
-            bool applied;
-            if (cs.flags & CS_SA) applied = (cs.flags & CS_ALIVE0) && !(cs.flags & CS_TRAPPED) && rep_ok == cs.ft_sa_ok;
-            else if (r.ceng == 1) applied = (cs.flags & CS_CE_ALIVE0) && rep_ok == cs.ft_ce_ok && !(cs.rel < (long long)rep_ok);
-            else applied = rep_ok == G.ft_gr_ok;
-            canc = !applied;
-          } else if (outcome == 1) {              // benign completion dropped on a torn channel (C5)
-            canc = cs.rel != REL_NONE || (r.ceng == 1 && (cs.flags & CS_CE_TORN)) ||
-                   (cs.flags & CS_KILL_ALL) || rep_ok > cs.kill_tie;
-          } else if (!dup) {                      // isolation mechanism (C3)
-            const bool epoch1 = cs.rel < (long long)ok;
-            if (!r.at.in_range || epoch1) mech = nr_lookup(S, r, epoch1) == ok ? 1 : 2;
-            else if (r.at.kind == 0) mech = 2;
-            else mech = __ldcg(S.ext + r.at.ridx) == ok ? 3 : 2;
-          }
-          o.verdict = (uint8_t)(outcome | (mech << 2) | (canc ? 0x10 : 0) | (dup ? 0x20 : 0) | (r.repl ? 0x40 : 0));
-        }
+      unsigned long long key = 0;
+      if (i < n) {
+        finalize_entry<kStaged>(W, v, S, P, G, tile[li], P.base_index + i, o, canc, rep, key);
+        __stcs(reinterpret_cast<unsigned long long*>(out) + i, *reinterpret_cast<unsigned long long*>(&o));
       }
-      if (base + (uint64_t)k * 32 < n) __stcs(reinterpret_cast<unsigned long long*>(out) + base + (uint64_t)k * 32,
-                                             *reinterpret_cast<unsigned long long*>(&o));
       const unsigned bc = __ballot_sync(0xFFFFFFFFu, canc);
       const unsigned bd = __ballot_sync(0xFFFFFFFFu, rep);
-      my_c_off[k] = wc + __popc(bc & lt_mask);
-      my_d_off[k] = wd + __popc(bd & lt_mask);
+      // park the compaction payload in the (consumed) entry slot
+      tile[li] = make_uint4((uint32_t)key, (uint32_t)(key >> 32),
+                            (canc ? 1u : 0u) | (rep ? 2u : 0u),
+                            (wc + __popc(bc & lt_mask)) | ((wd + __popc(bd & lt_mask)) << 16));
       wc += __popc(bc);
       wd += __popc(bd);
-      cflag |= (canc ? 1u : 0u) << k;
-      dflag |= (rep ? 1u : 0u) << k;
     }
     if (lane == 0) { s_wc[warp] = wc; s_wd[warp] = wd; }
     __syncthreads();
@@ -592,37 +708,47 @@ __global__ void __launch_bounds__(BLOCK) k_finalize(World W, Scratch S, const mp
         s_wc[w] = tc; s_wd[w] = td;
         tc += a; td += b;
       }
-      // decoupled look-back
       volatile unsigned long long* desc = S.tiles;
       uint32_t pc = 0, pd = 0;
       if (t == 0) {
         desc[0] = LB_PRE | lb_pack(tc, td);
       } else {
         desc[t] = LB_AGG | lb_pack(tc, td);
-        int64_t j = (int64_t)t - 1;
-        while (j >= 0) {
-          const unsigned long long d = desc[j];
+        int64_t q = (int64_t)t - 1;
+        while (q >= 0) {
+          const unsigned long long d = desc[q];
           const unsigned long long st = d & ~LB_VAL;
           if (st == 0) continue;
           pc += (uint32_t)(d & 0x7FFFFFFFull);
           pd += (uint32_t)((d >> 31) & 0x7FFFFFFFull);
           if (st == LB_PRE) break;
-          --j;
+          --q;
         }
-        __threadfence();
         desc[t] = LB_PRE | lb_pack(pc + tc, pd + td);
       }
       s_pc = pc; s_pd = pd;
     }
     __syncthreads();
     const uint32_t bc0 = s_pc + s_wc[warp], bd0 = s_pd + s_wd[warp];
-#pragma unroll
+#pragma unroll 1
     for (int k = 0; k < EPT; ++k) {
-      const uint64_t gidx = P.base_index + base + (uint64_t)k * 32;
-      if (cflag & (1u << k)) cancel[bc0 + my_c_off[k]] = (uint32_t)gidx;
-      if (dflag & (1u << k)) {
-        dkeys[bd0 + my_d_off[k]] = key[k];
-        didx[bd0 + my_d_off[k]] = (uint32_t)gidx;
+      const int li = warp * (32 * EPT) + k * 32 + lane;
+      const uint4 q = tile[li];
+      const uint32_t gidx = (uint32_t)(P.base_index + start + li);
+      if (q.z & 1u) cancel[bc0 + (q.w & 0xFFFFu)] = gidx;
+      if (q.z & 2u) {
+        const uint32_t d = bd0 + (q.w >> 16);
+        dkeys[d] = (unsigned long long)q.x | ((unsigned long long)q.y << 32);
+        didx[d] = gidx;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint32_t nt = atomicAdd(S.ctrl + C_TILE_FIN, 1u);
+      p.tids[slot] = nt;
+      if (nt < ntiles) {
+        fence_proxy_async();
+        pipe_issue(p, slot, in, n, nt);
       }
     }
     __syncthreads();
@@ -649,19 +775,25 @@ static int grid_for(K kernel, size_t smem) {
   return per_sm * sm_count();
 }
 
-bool staged_fits(const World& W) {
-  return staged_smem_bytes(W.n_ranges, W.n_clients, W.n_channels) <= 96 * 1024;
+static bool staged_fits(const World& W) {
+  return make_layout(W.n_ranges, W.n_clients, W.n_channels, true, false).total <= 200 * 1024 &&
+         make_layout(W.n_ranges, W.n_clients, W.n_channels, true, true).total <= 200 * 1024;
+}
+
+uint32_t count_parts_needed(const World& W) {
+  return staged_fits(W) ? (uint32_t)(2 * sm_count()) : 0u;
 }
 
 template <bool kStaged>
 static int launch_all(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n,
                       const Params& P, mpsf_out_record* out, mpsf_client_verdict* verdict,
                       unsigned long long* counts, unsigned long long* dkeys, uint32_t* didx,
-                      uint32_t* cancel, cudaStream_t st, int* launches, const Marker& mk) {
-  const size_t smem = kStaged ? staged_smem_bytes(W.n_ranges, W.n_clients, W.n_channels) : 0;
+                      uint32_t* cancel, uint32_t* count_part, cudaStream_t st, int* launches, const Marker& mk) {
+  const uint32_t smem_scan = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, false).total;
+  const uint32_t smem_fin = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, true).total;
   static bool attr_set = false;
   if (!attr_set) {
-    const int mx = 200 * 1024;
+    const int mx = 220 * 1024;
     cudaFuncSetAttribute(k_scan<kStaged>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_general<kStaged, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_general<kStaged, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
@@ -670,37 +802,40 @@ static int launch_all(const World& W, const Scratch& S, const mpsf_fault_entry* 
   }
   const uint64_t ntiles = (n + TILE - 1) / TILE;
   int nl = 0;
+  uint32_t parts = 0;
   if (n > 0) {
-    int g = grid_for(k_scan<kStaged>, smem);
+    int g = grid_for(k_scan<kStaged>, smem_scan);
+    if (kStaged && g > (int)(2 * sm_count())) g = 2 * sm_count();
     if ((uint64_t)g > ntiles) g = (int)ntiles;
-    k_scan<kStaged><<<g, BLOCK, smem, st>>>(W, S, in, n, P, counts);
+    k_scan<kStaged><<<g, BLOCK, smem_scan, st>>>(W, S, in, n, P, counts, count_part);
     mk.mark("k_scan");
     ++nl;
+    parts = kStaged ? (uint32_t)g : 0u;
   }
-  k_resolve<<<1, 1024, 0, st>>>(W, S, P, verdict);
+  const uint32_t bins = NSCEN * W.n_clients;
+  const uint32_t rblocks = 1 + (parts ? (bins + 255) / 256 : 0);
+  k_resolve<<<rblocks, 256, 0, st>>>(W, S, P, verdict, count_part, parts, counts);
   mk.mark("k_resolve");
   ++nl;
   if ((P.flags & MPSF_PF_ISOLATION) && n > 0) {
-    k_clear_nr1<<<2 * sm_count(), 256, 0, st>>>(S, W.n_pages);
-    mk.mark("k_clear_nr1");
-    int g = grid_for(k_general<kStaged, 1>, smem);
+    int g = grid_for(k_general<kStaged, 1>, smem_fin);
     if ((uint64_t)g > ntiles) g = (int)ntiles;
-    k_general<kStaged, 1><<<g, BLOCK, smem, st>>>(W, S, in, n, P);
+    k_general<kStaged, 1><<<g, BLOCK, smem_fin, st>>>(W, S, in, n, P);
     mk.mark("k_general1");
-    nl += 2;
+    ++nl;
     if (P.m2_us <= P.benign_us) {
-      k_general<kStaged, 2><<<g, BLOCK, smem, st>>>(W, S, in, n, P);
+      k_general<kStaged, 2><<<g, BLOCK, smem_fin, st>>>(W, S, in, n, P);
       mk.mark("k_general2");
       ++nl;
     }
-    k_resolve2<<<1, 1024, 0, st>>>(W, S, P);
+    k_resolve2<<<1, 256, 0, st>>>(W, S, P);
     mk.mark("k_resolve2");
     ++nl;
   }
   if (n > 0) {
-    int g = grid_for(k_finalize<kStaged>, smem);
+    int g = grid_for(k_finalize<kStaged>, smem_fin);
     if ((uint64_t)g > ntiles) g = (int)ntiles;
-    k_finalize<kStaged><<<g, BLOCK, smem, st>>>(W, S, in, n, P, out, dkeys, didx, cancel);
+    k_finalize<kStaged><<<g, BLOCK, smem_fin, st>>>(W, S, in, n, P, out, dkeys, didx, cancel);
     mk.mark("k_finalize");
     ++nl;
   }
@@ -711,10 +846,10 @@ static int launch_all(const World& W, const Scratch& S, const mpsf_fault_entry* 
 int launch_fault_path(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n,
                       const Params& P, mpsf_out_record* out, mpsf_client_verdict* verdict,
                       unsigned long long* counts, unsigned long long* dkeys, uint32_t* didx,
-                      uint32_t* cancel, cudaStream_t st, int* launches, const Marker& mk) {
+                      uint32_t* cancel, uint32_t* count_part, cudaStream_t st, int* launches, const Marker& mk) {
   if (staged_fits(W))
-    return launch_all<true>(W, S, in, n, P, out, verdict, counts, dkeys, didx, cancel, st, launches, mk);
-  return launch_all<false>(W, S, in, n, P, out, verdict, counts, dkeys, didx, cancel, st, launches, mk);
+    return launch_all<true>(W, S, in, n, P, out, verdict, counts, dkeys, didx, cancel, count_part, st, launches, mk);
+  return launch_all<false>(W, S, in, n, P, out, verdict, counts, dkeys, didx, cancel, count_part, st, launches, mk);
 }
 
 uint64_t tiles_for(uint64_t n) { return (n + TILE - 1) / TILE; }

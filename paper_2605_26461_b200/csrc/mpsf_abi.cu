@@ -80,6 +80,9 @@ struct mpsf_ctx {
   // scratch
   uint32_t* d_dd = nullptr;
   uint32_t* d_nr1 = nullptr;
+  uint64_t dd_cap = 0;
+  uint32_t* d_count_part = nullptr;
+  uint64_t part_cap = 0;
   uint64_t pages_cap = 0;
   uint8_t* d_small = nullptr;
   size_t small_cap = 0;
@@ -205,6 +208,7 @@ void mpsf_destroy(mpsf_ctx* c) {
   cudaFree(c->d_world);
   cudaFree(c->d_dd);
   cudaFree(c->d_nr1);
+  cudaFree(c->d_count_part);
   cudaFree(c->d_small);
   cudaFree(c->d_tiles);
   cudaFree(c->d_hdd);
@@ -277,16 +281,28 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   W.world_flags = world_flags;
   W.n_pages = np;
   W.has_mps = has_mps;
-  W.pad = 0;
+  // dedup slots: one per (page, group) while that stays small (L2-resident), else one
+  // claimed slot per page with overflow to the hash table
+  W.dd_groups = (np * 5 * 4 <= (64ull << 20)) ? 5 : 1;
   // page-sized scratch
-  if (np > c->pages_cap) {
+  const uint64_t dd_words = np * W.dd_groups;
+  if (dd_words > c->dd_cap || np > c->pages_cap) {
     cudaFree(c->d_dd);
     cudaFree(c->d_nr1);
     c->d_dd = c->d_nr1 = nullptr;
-    c->pages_cap = 0;
-    CK(cudaMalloc(&c->d_dd, sizeof(uint32_t) * std::max<uint64_t>(np, 1)));
+    c->pages_cap = c->dd_cap = 0;
+    CK(cudaMalloc(&c->d_dd, sizeof(uint32_t) * std::max<uint64_t>(dd_words, 1)));
     CK(cudaMalloc(&c->d_nr1, sizeof(uint32_t) * std::max<uint64_t>(np, 1)));
     c->pages_cap = np;
+    c->dd_cap = dd_words;
+  }
+  const uint64_t part_words = (uint64_t)count_parts_needed(W) * NSCEN * ncl;
+  if (part_words > c->part_cap) {
+    cudaFree(c->d_count_part);
+    c->d_count_part = nullptr;
+    c->part_cap = 0;
+    CK(cudaMalloc(&c->d_count_part, 4 * part_words));
+    c->part_cap = part_words;
   }
   // small scratch: [EMPTY-init][ZERO-init][uninit]
   const uint32_t C = ncl, R = nr;
@@ -389,7 +405,8 @@ int mpsf_process(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const mp
   const uint64_t nt = tiles_for(n);
   InitSegs segs{};
   int k = 0;
-  segs.p[k] = c->d_dd; segs.words[k] = c->W.n_pages; segs.val[k++] = EMPTY32;
+  segs.p[k] = c->d_dd; segs.words[k] = c->W.n_pages * c->W.dd_groups; segs.val[k++] = EMPTY32;
+  if (p->flags & MPSF_PF_ISOLATION) { segs.p[k] = c->d_nr1; segs.words[k] = c->W.n_pages; segs.val[k++] = EMPTY32; }
   segs.p[k] = c->d_small; segs.words[k] = c->small_empty_bytes / 4; segs.val[k++] = EMPTY32;
   segs.p[k] = c->d_small + c->small_zero_off; segs.words[k] = c->small_zero_bytes / 4; segs.val[k++] = 0;
   segs.p[k] = c->d_tiles; segs.words[k] = 2 * nt; segs.val[k++] = 0;
@@ -412,7 +429,8 @@ int mpsf_process(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const mp
   P.base_index = p->base_index;
   int launches = 0;
   if (launch_fault_path(c->W, c->S, d_in, n, P, d_out, d_verdict, reinterpret_cast<unsigned long long*>(d_counts),
-                        reinterpret_cast<unsigned long long*>(d_dkeys), d_didx, d_cancel, st, &launches, mk))
+                        reinterpret_cast<unsigned long long*>(d_dkeys), d_didx, d_cancel, c->d_count_part, st,
+                        &launches, mk))
     return MPSF_E_CUDA;
   k_summary<<<1, 1, 0, st>>>(c->S.ctrl, c->S.err_idx, c->d_tiles, nt, c->d_sum);
   mk.mark("k_summary");

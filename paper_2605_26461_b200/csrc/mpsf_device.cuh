@@ -68,7 +68,8 @@ struct World {
   const mpsf_client_entry* clients;
   uint32_t n_ranges, n_clients, n_channels, world_flags;
   uint64_t n_pages;
-  uint32_t has_mps, pad;
+  uint32_t has_mps;
+  uint32_t dd_groups;   // 5: one dense dedup slot per (page, group); 1: one claimed slot per page
 };
 
 struct Hash {

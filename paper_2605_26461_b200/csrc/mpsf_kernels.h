@@ -21,8 +21,10 @@ struct Marker {
 int launch_fault_path(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n,
                       const Params& P, mpsf_out_record* out, mpsf_client_verdict* verdict,
                       unsigned long long* counts, unsigned long long* dkeys, uint32_t* didx,
-                      uint32_t* cancel, cudaStream_t st, int* launches, const Marker& mk);
+                      uint32_t* cancel, uint32_t* count_part, cudaStream_t st, int* launches,
+                      const Marker& mk);
 uint64_t tiles_for(uint64_t n);
+uint32_t count_parts_needed(const World& W);   // per-block count partial rows k_scan may write
 int launch_remap(uint64_t va_base, const uint64_t* phys, uint64_t npages4k, uint32_t gran_log2,
                  mpsf_remap_entry* out, cudaStream_t st);
 int launch_remap_blocks(uint64_t va_base, const uint64_t* phys, uint64_t npages4k,
