@@ -31,7 +31,7 @@
 
 namespace mpsf {
 
-constexpr int BLOCK = 512;
+constexpr int BLOCK = 1024;
 constexpr int WARPS = BLOCK / 32;
 constexpr int EPT = 4;                  // entries per lane per tile
 constexpr int TILE = BLOCK * EPT;       // 2048 entries = 32 KiB

@@ -144,16 +144,18 @@ struct Attr {
 __device__ __forceinline__ Attr attribute(const mpsf_range_entry* __restrict__ R,
                                           const uint8_t* __restrict__ page_state,
                                           uint32_t lo, uint32_t hi, uint64_t va) {
-  uint32_t a = lo, b = hi;
-  while (a < b) {
-    const uint32_t m = (a + b) >> 1;
-    if (R[m].base <= va) a = m + 1; else b = m;
+  // branchless: pos converges on the last range with base <= va (if any)
+  uint32_t pos = lo, len = hi - lo;
+  while (len > 1) {
+    const uint32_t half = len >> 1;
+    pos = (R[pos + half].base <= va) ? pos + half : pos;
+    len -= half;
   }
   Attr t;
   t.ridx = -1; t.in_range = false; t.guard = false; t.slot = 0; t.st = 0;
   t.kind = 0; t.lifecycle = 0; t.migratable = 1; t.rid = NO_RID;
-  if (a > lo) {
-    const uint32_t k = a - 1;
+  if (hi > lo && R[pos].base <= va) {
+    const uint32_t k = pos;
     const uint64_t base = R[k].base, end = R[k].end;
     if (va < end) {
       const uint4 meta = *reinterpret_cast<const uint4*>(&R[k].client);  // client,page_off,kind..state,rid
