@@ -127,7 +127,7 @@ def max_over_ranks(ws, x):
     return float(t.item())
 
 
-def time_resident(eng, d_in, n, params, bufs, steps, flush):
+def time_resident(eng, d_in, n, params, bufs, steps, flush, step_fn=None):
     """K device-resident steps; per-step CUDA events on the launching stream, L2 flushed
     between steps outside the events.  Returns (total_ms, summary, profile)."""
     import torch
@@ -139,7 +139,10 @@ def time_resident(eng, d_in, n, params, bufs, steps, flush):
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        eng.process_device(d_in, n, params, bufs, stream)
+        if step_fn is None:
+            eng.process_device(d_in, n, params, bufs, stream)
+        else:
+            step_fn()
         b.record(stream)
         b.synchronize()
         total += a.elapsed_time(b)
@@ -154,7 +157,7 @@ def run_mine(args):
     from paper_2605_26461_b200 import synth
     from paper_2605_26461_b200.engine import (BatchParams, DeviceBuffers, FaultEngine,
                                               alloc_host_outputs)
-    from paper_2605_26461_b200.parallel import combine_verdicts_nccl
+    from paper_2605_26461_b200.parallel import GpuShard, ShardedFaultPath
 
     ws, rank, local = setup_dist(args)
     dev = torch.device("cuda", local)
@@ -168,17 +171,21 @@ def run_mine(args):
     trace = synth.generate_trace(w, spec)
     params = BatchParams(isolation=True, base_index=rank * n)
     eng = FaultEngine(local)
+    if ws > 1:
+        eng.set_dense_dedup(True)          # dedup slots are combined with an all-reduce MIN
     eng.upload_world(w)
     d_in = torch.from_numpy(trace.view(np.uint8)).to(dev)
     bufs = DeviceBuffers(n, w.n_clients, local)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    sharded = ShardedFaultPath(GpuShard(eng, d_in, n, bufs)) if ws > 1 else None
+    step_fn = (lambda: sharded.process(params)) if ws > 1 else None
 
     # warm-up (also sizes the wild-page hash tables) and a bit-exact check vs the C oracle
     for _ in range(max(args.warmup, 3)):
-        res = eng.process_resident(d_in, n, params, bufs)
+        res = sharded.process(params) if ws > 1 else eng.process_resident(d_in, n, params, bufs)
     parity = None
     cpu_baseline = None
-    if rank == 0 and not args.no_check:
+    if rank == 0 and ws == 1 and not args.no_check:
         from oracle import c_oracle as co
         from oracle.seq_oracle import Params as OP
         threads = os.cpu_count() or 1
@@ -199,7 +206,7 @@ def run_mine(args):
     with ClockSampler(local) as clk:
         barrier(ws)
         torch.cuda.synchronize()
-        total_ms, summ, prof = time_resident(eng, d_in, n, params, bufs, args.steps, flush)
+        total_ms, summ, prof = time_resident(eng, d_in, n, params, bufs, args.steps, flush, step_fn)
         torch.cuda.synchronize()
         barrier(ws)
     total_ms = max_over_ranks(ws, total_ms)
@@ -222,28 +229,36 @@ def run_mine(args):
         with open(tp) as f:
             traffic = json.load(f).get(args.workload)
 
-    # verdict combine across shards (NCCL allreduce of per-client fates)
-    combined = None
-    if ws > 1:
-        combined = combine_verdicts_nccl(res.verdict)
+    # per-client fates are identical on every rank after the exchanges
+    combined = res.verdict if ws > 1 else None
 
     # end to end through the C ABI with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        pinned = torch.from_numpy(trace.view(np.uint8)).pin_memory().numpy().view(trace.dtype)
+        pinned_t = torch.from_numpy(trace.view(np.uint8)).pin_memory()
+        pinned = pinned_t.numpy().view(trace.dtype)
         hb = alloc_host_outputs(n, w.n_clients, pinned=True)
-        eng.process(pinned, params, hb)
+
+        def e2e_step():
+            if ws == 1:
+                return eng.process(pinned, params, hb)
+            d_in.copy_(pinned_t, non_blocking=True)     # H2D of this rank's shard
+            return sharded.process(params)                # exchanges + D2H of every output
+
+        e2e_step()
         barrier(ws)
         ts = []
         for _ in range(max(1, min(args.steps, 10))):
+            torch.cuda.synchronize()
             t0 = time.perf_counter()
-            r2 = eng.process(pinned, params, hb)
+            r2 = e2e_step()
             ts.append(time.perf_counter() - t0)
         t_e2e = max_over_ranks(ws, statistics.median(ts))
         d2h = 8 * n + 4 * w.n_clients + 8 * 28 * w.n_clients + 12 * len(r2.dedup_keys) + 4 * len(r2.cancel)
         e2e = {"value": ws * n / t_e2e, "unit": "entries/s", "h2d_bytes_per_step": 16 * n,
                "d2h_bytes_per_step": d2h, "ms_per_step": round(t_e2e * 1e3, 3),
-               "api": "mpsf_process_host (pinned host buffers)"}
+               "api": "mpsf_process_host (pinned host buffers)" if ws == 1 else
+                      "H2D + sharded phase API + NCCL exchanges + D2H"}
 
     extra = {}
     if not args.no_storm and ws == 1:

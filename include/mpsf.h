@@ -172,6 +172,42 @@ typedef struct {
 int mpsf_set_profiling(mpsf_ctx* ctx, int on);
 int mpsf_get_profile(mpsf_ctx* ctx, mpsf_kernel_time* out, int cap);
 
+/* ---- phase entry points (sharded multi-GPU runs; mpsf_process == their composition) ----
+ * Each rank runs mpsf_scan on its shard (params->base_index = first global index), then the
+ * caller combines the exchange buffers across ranks (MIN on the unsigned values, SUM for
+ * counts) and merges the sparse hash tables, then runs mpsf_resolve; with isolation on, the
+ * general stages follow (exchange stage 2 after stage 1, stage 3 after stage 2); finally
+ * mpsf_finalize writes this shard's outputs.  Because every cross-entry dependency is a
+ * group minimum, the concatenated per-rank outputs equal a single-GPU run bit for bit. */
+int mpsf_set_dense_dedup(mpsf_ctx* ctx, int on);   /* before upload: one dedup slot per (page, group) */
+int mpsf_scan(mpsf_ctx* ctx, const mpsf_fault_entry* d_entries, uint64_t n, const mpsf_params* params,
+              uint64_t* d_counts, void* stream);
+int mpsf_resolve(mpsf_ctx* ctx, const mpsf_params* params, mpsf_client_verdict* d_verdict,
+                 uint64_t* d_counts, void* stream);
+int mpsf_general(mpsf_ctx* ctx, const mpsf_fault_entry* d_entries, uint64_t n, const mpsf_params* params,
+                 int stage, void* stream);
+int mpsf_resolve2(mpsf_ctx* ctx, const mpsf_params* params, void* stream);
+int mpsf_finalize(mpsf_ctx* ctx, const mpsf_fault_entry* d_entries, uint64_t n, const mpsf_params* params,
+                  mpsf_out_record* d_out, uint64_t* d_dedup_keys, uint32_t* d_dedup_idx,
+                  uint32_t* d_cancel, void* stream);
+
+#define MPSF_XOP_MIN 0u
+#define MPSF_XOP_SUM 1u
+typedef struct {
+  void* ptr;            /* device pointer                                   */
+  uint64_t count;       /* elements                                         */
+  uint32_t elem_bytes;  /* 4 or 8 (unsigned)                                */
+  uint32_t op;          /* MPSF_XOP_MIN / MPSF_XOP_SUM                      */
+} mpsf_xbuf;
+/* stage 1: after mpsf_scan; 2: after mpsf_general(stage 1); 3: after stage 2 */
+int mpsf_exchange_buffers(mpsf_ctx* ctx, int stage, mpsf_xbuf* out, int cap);
+/* which: 0 dedup hash, 1 first-isolation (NR) hash.  Export compacts the non-empty slots
+ * (returns the count, waits on the stream); merge inserts keys with atomic-min values. */
+int64_t mpsf_hash_export(mpsf_ctx* ctx, int which, uint64_t* d_keys, uint32_t* d_vals, uint64_t cap,
+                         void* stream);
+int mpsf_hash_merge(mpsf_ctx* ctx, int which, const uint64_t* d_keys, const uint32_t* d_vals,
+                    uint64_t count, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

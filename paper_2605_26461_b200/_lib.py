@@ -74,7 +74,21 @@ SIGNATURES = {
     "mpsf_last_launches": (C.c_int, [C.c_void_p]),
     "mpsf_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
     "mpsf_get_profile": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
+    "mpsf_set_dense_dedup": (C.c_int, [C.c_void_p, C.c_int]),
+    "mpsf_scan": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(Params), C.c_void_p, C.c_void_p]),
+    "mpsf_resolve": (C.c_int, [C.c_void_p, C.POINTER(Params), C.c_void_p, C.c_void_p, C.c_void_p]),
+    "mpsf_general": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(Params), C.c_int, C.c_void_p]),
+    "mpsf_resolve2": (C.c_int, [C.c_void_p, C.POINTER(Params), C.c_void_p]),
+    "mpsf_finalize": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(Params), C.c_void_p,
+                                C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "mpsf_exchange_buffers": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int]),
+    "mpsf_hash_export": (C.c_int64, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
+    "mpsf_hash_merge": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
 }
+
+
+class XBuf(C.Structure):
+    _fields_ = [("ptr", C.c_void_p), ("count", C.c_uint64), ("elem_bytes", C.c_uint32), ("op", C.c_uint32)]
 
 
 class KernelTime(C.Structure):

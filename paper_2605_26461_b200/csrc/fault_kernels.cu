@@ -285,7 +285,7 @@ __device__ __forceinline__ void scan_entry(const World& W, const View& v, const 
   else atomicAdd(counts + (uint64_t)c * NSCEN + r.s, 1ull);
   if (s_trap(r.s)) {
     const unsigned long long t = (gidx << 8) | (unsigned long long)r.s;
-    if (!r.sa) min64(&S.glob->trap_mps, t);
+    if (!r.sa) min64(S.trap_mps, t);
     else if (kStaged) min64c(S.trap_sa + c, v.trap_sa + c, t);
     else min64(S.trap_sa + c, t);
     return;
@@ -296,7 +296,7 @@ __device__ __forceinline__ void scan_entry(const World& W, const View& v, const 
     const unsigned long long t = ((unsigned long long)ok << 8) | (unsigned long long)r.s;
     if (r.sa) { if (kStaged) min64c(S.ft_sa + c, v.ft_sa + c, t); else min64(S.ft_sa + c, t); }
     else if (r.ceng == 1) { if (kStaged) min64c(S.ft_ce + c, v.ft_ce + c, t); else min64(S.ft_ce + c, t); }
-    else min64(&S.glob->ft_gr, t);
+    else min64(S.ft_gr, t);
   } else if (!serv) {                                                // isolation-eligible (pipeline.py:177-179)
     if (!r.at.in_range) {
       if (kStaged) min32c(S.iso1 + c, v.iso1 + c, ok); else min32(S.iso1 + c, ok);
@@ -417,7 +417,7 @@ __global__ void k_resolve(World W, Scratch S, Params P, mpsf_client_verdict* __r
   const bool iso = P.flags & MPSF_PF_ISOLATION;
   Globals* G = S.glob;
   const bool gr_alive0 = W.has_mps && !(W.world_flags & MPSF_WF_GR_DEAD);
-  const unsigned long long trap_mps = G->trap_mps, ft_gr = G->ft_gr;
+  const unsigned long long trap_mps = *S.trap_mps, ft_gr = *S.ft_gr;
   const bool trapped_mps = gr_alive0 && trap_mps != EMPTY64;
   const bool gr_applied = gr_alive0 && !trapped_mps && ft_gr != EMPTY64;
   const long long gr_rel = (!gr_alive0 || trapped_mps) ? REL_PRE
@@ -755,6 +755,26 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const
   }
 }
 
+// ---- sparse hash exchange (multi-GPU) ------------------------------------------------------
+__global__ void k_hash_export(Hash h, uint64_t cap, unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals,
+                              uint32_t* __restrict__ counter, uint64_t out_cap) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap; i += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = h.keys[i];
+    if (k == EMPTY64) continue;
+    const uint32_t o = atomicAdd(counter, 1u);
+    if (o < out_cap) { keys[o] = k; vals[o] = h.vals[i]; }
+  }
+}
+
+__global__ void k_hash_merge(Hash h, uint32_t* ctrl, const unsigned long long* __restrict__ keys,
+                             const uint32_t* __restrict__ vals, uint64_t count) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = keys[i];
+    if (k == EMPTY64) continue;
+    if (!hash_min(h, ctrl, k, vals[i])) atomicOr(ctrl + C_OVF, 1u);
+  }
+}
+
 // ---- launch helpers (host) ----------------------------------------------------------------
 static int g_sms = 0;
 
@@ -785,71 +805,117 @@ uint32_t count_parts_needed(const World& W) {
 }
 
 template <bool kStaged>
-static int launch_all(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n,
-                      const Params& P, mpsf_out_record* out, mpsf_client_verdict* verdict,
-                      unsigned long long* counts, unsigned long long* dkeys, uint32_t* didx,
-                      uint32_t* cancel, uint32_t* count_part, cudaStream_t st, int* launches, const Marker& mk) {
-  const uint32_t smem_scan = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, false).total;
-  const uint32_t smem_fin = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, true).total;
-  static bool attr_set = false;
-  if (!attr_set) {
-    const int mx = 220 * 1024;
-    cudaFuncSetAttribute(k_scan<kStaged>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_general<kStaged, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_general<kStaged, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_finalize<kStaged>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    attr_set = true;
-  }
+static void set_attrs() {
+  static bool done = false;
+  if (done) return;
+  const int mx = 220 * 1024;
+  cudaFuncSetAttribute(k_scan<kStaged>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_general<kStaged, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_general<kStaged, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_finalize<kStaged>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  done = true;
+}
+
+static int ok_or_err() { return cudaGetLastError() == cudaSuccess ? 0 : -1; }
+
+template <bool kStaged>
+static int scan_t(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
+                  unsigned long long* counts, uint32_t* count_part, cudaStream_t st, const Marker& mk,
+                  uint32_t* parts) {
+  set_attrs<kStaged>();
+  *parts = 0;
+  if (n == 0) return 0;
+  const uint32_t smem = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, false).total;
   const uint64_t ntiles = (n + TILE - 1) / TILE;
-  int nl = 0;
-  uint32_t parts = 0;
-  if (n > 0) {
-    int g = grid_for(k_scan<kStaged>, smem_scan);
-    if (kStaged && g > (int)(2 * sm_count())) g = 2 * sm_count();
-    if ((uint64_t)g > ntiles) g = (int)ntiles;
-    k_scan<kStaged><<<g, BLOCK, smem_scan, st>>>(W, S, in, n, P, counts, count_part);
-    mk.mark("k_scan");
-    ++nl;
-    parts = kStaged ? (uint32_t)g : 0u;
+  int g = grid_for(k_scan<kStaged>, smem);
+  if (kStaged && g > (int)(2 * sm_count())) g = 2 * sm_count();
+  if ((uint64_t)g > ntiles) g = (int)ntiles;
+  k_scan<kStaged><<<g, BLOCK, smem, st>>>(W, S, in, n, P, counts, count_part);
+  mk.mark("k_scan");
+  *parts = kStaged ? (uint32_t)g : 0u;
+  return ok_or_err();
+}
+
+template <bool kStaged>
+static int general_t(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
+                     int stage, cudaStream_t st, const Marker& mk) {
+  set_attrs<kStaged>();
+  if (n == 0) return 0;
+  const uint32_t smem = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, true).total;
+  const uint64_t ntiles = (n + TILE - 1) / TILE;
+  int g = grid_for(k_general<kStaged, 1>, smem);
+  if ((uint64_t)g > ntiles) g = (int)ntiles;
+  if (stage == 1) {
+    k_general<kStaged, 1><<<g, BLOCK, smem, st>>>(W, S, in, n, P);
+    mk.mark("k_general1");
+  } else {
+    k_general<kStaged, 2><<<g, BLOCK, smem, st>>>(W, S, in, n, P);
+    mk.mark("k_general2");
   }
+  return ok_or_err();
+}
+
+template <bool kStaged>
+static int finalize_t(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
+                      mpsf_out_record* out, unsigned long long* dkeys, uint32_t* didx, uint32_t* cancel,
+                      cudaStream_t st, const Marker& mk) {
+  set_attrs<kStaged>();
+  if (n == 0) return 0;
+  const uint32_t smem = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, true).total;
+  const uint64_t ntiles = (n + TILE - 1) / TILE;
+  int g = grid_for(k_finalize<kStaged>, smem);
+  if ((uint64_t)g > ntiles) g = (int)ntiles;
+  k_finalize<kStaged><<<g, BLOCK, smem, st>>>(W, S, in, n, P, out, dkeys, didx, cancel);
+  mk.mark("k_finalize");
+  return ok_or_err();
+}
+
+int launch_scan(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
+                unsigned long long* counts, uint32_t* count_part, cudaStream_t st, const Marker& mk, uint32_t* parts) {
+  return staged_fits(W) ? scan_t<true>(W, S, in, n, P, counts, count_part, st, mk, parts)
+                        : scan_t<false>(W, S, in, n, P, counts, count_part, st, mk, parts);
+}
+
+int launch_resolve(const World& W, const Scratch& S, const Params& P, mpsf_client_verdict* verdict,
+                   const uint32_t* count_part, uint32_t parts, unsigned long long* counts, cudaStream_t st,
+                   const Marker& mk) {
   const uint32_t bins = NSCEN * W.n_clients;
   const uint32_t rblocks = 1 + (parts ? (bins + 255) / 256 : 0);
   k_resolve<<<rblocks, 256, 0, st>>>(W, S, P, verdict, count_part, parts, counts);
   mk.mark("k_resolve");
-  ++nl;
-  if ((P.flags & MPSF_PF_ISOLATION) && n > 0) {
-    int g = grid_for(k_general<kStaged, 1>, smem_fin);
-    if ((uint64_t)g > ntiles) g = (int)ntiles;
-    k_general<kStaged, 1><<<g, BLOCK, smem_fin, st>>>(W, S, in, n, P);
-    mk.mark("k_general1");
-    ++nl;
-    if (P.m2_us <= P.benign_us) {
-      k_general<kStaged, 2><<<g, BLOCK, smem_fin, st>>>(W, S, in, n, P);
-      mk.mark("k_general2");
-      ++nl;
-    }
-    k_resolve2<<<1, 256, 0, st>>>(W, S, P);
-    mk.mark("k_resolve2");
-    ++nl;
-  }
-  if (n > 0) {
-    int g = grid_for(k_finalize<kStaged>, smem_fin);
-    if ((uint64_t)g > ntiles) g = (int)ntiles;
-    k_finalize<kStaged><<<g, BLOCK, smem_fin, st>>>(W, S, in, n, P, out, dkeys, didx, cancel);
-    mk.mark("k_finalize");
-    ++nl;
-  }
-  *launches = nl;
-  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  return ok_or_err();
 }
 
-int launch_fault_path(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n,
-                      const Params& P, mpsf_out_record* out, mpsf_client_verdict* verdict,
-                      unsigned long long* counts, unsigned long long* dkeys, uint32_t* didx,
-                      uint32_t* cancel, uint32_t* count_part, cudaStream_t st, int* launches, const Marker& mk) {
-  if (staged_fits(W))
-    return launch_all<true>(W, S, in, n, P, out, verdict, counts, dkeys, didx, cancel, count_part, st, launches, mk);
-  return launch_all<false>(W, S, in, n, P, out, verdict, counts, dkeys, didx, cancel, count_part, st, launches, mk);
+int launch_general(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
+                   int stage, cudaStream_t st, const Marker& mk) {
+  return staged_fits(W) ? general_t<true>(W, S, in, n, P, stage, st, mk)
+                        : general_t<false>(W, S, in, n, P, stage, st, mk);
+}
+
+int launch_resolve2(const World& W, const Scratch& S, const Params& P, cudaStream_t st, const Marker& mk) {
+  k_resolve2<<<1, 256, 0, st>>>(W, S, P);
+  mk.mark("k_resolve2");
+  return ok_or_err();
+}
+
+int launch_finalize(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
+                    mpsf_out_record* out, unsigned long long* dkeys, uint32_t* didx, uint32_t* cancel,
+                    cudaStream_t st, const Marker& mk) {
+  return staged_fits(W) ? finalize_t<true>(W, S, in, n, P, out, dkeys, didx, cancel, st, mk)
+                        : finalize_t<false>(W, S, in, n, P, out, dkeys, didx, cancel, st, mk);
+}
+
+int launch_hash_export(const Hash& h, uint64_t cap, unsigned long long* keys, uint32_t* vals, uint32_t* counter,
+                       uint64_t out_cap, cudaStream_t st) {
+  k_hash_export<<<2 * sm_count(), 256, 0, st>>>(h, cap, keys, vals, counter, out_cap);
+  return ok_or_err();
+}
+
+int launch_hash_merge(const Hash& h, uint32_t* ctrl, const unsigned long long* keys, const uint32_t* vals,
+                      uint64_t count, cudaStream_t st) {
+  if (count == 0) return 0;
+  k_hash_merge<<<2 * sm_count(), 256, 0, st>>>(h, ctrl, keys, vals, count);
+  return ok_or_err();
 }
 
 uint64_t tiles_for(uint64_t n) { return (n + TILE - 1) / TILE; }

@@ -83,6 +83,14 @@ struct mpsf_ctx {
   uint64_t dd_cap = 0;
   uint32_t* d_count_part = nullptr;
   uint64_t part_cap = 0;
+  bool dense_dedup = false;
+  // exchange-group offsets inside d_small
+  size_t x_u64 = 0, x_u32 = 0, x_giso = 0;
+  uint64_t x_u64_n = 0, x_u32_n = 0, x_giso_n = 0;
+  // state carried between phase calls
+  uint32_t parts = 0;
+  uint64_t phase_n = 0;
+  uint32_t* d_counter = nullptr;
   uint64_t pages_cap = 0;
   uint8_t* d_small = nullptr;
   size_t small_cap = 0;
@@ -209,6 +217,7 @@ void mpsf_destroy(mpsf_ctx* c) {
   cudaFree(c->d_dd);
   cudaFree(c->d_nr1);
   cudaFree(c->d_count_part);
+  cudaFree(c->d_counter);
   cudaFree(c->d_small);
   cudaFree(c->d_tiles);
   cudaFree(c->d_hdd);
@@ -283,7 +292,7 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   W.has_mps = has_mps;
   // dedup slots: one per (page, group) while that stays small (L2-resident), else one
   // claimed slot per page with overflow to the hash table
-  W.dd_groups = (np * 5 * 4 <= (64ull << 20)) ? 5 : 1;
+  W.dd_groups = (c->dense_dedup || np * 5 * 4 <= (64ull << 20)) ? 5 : 1;
   // page-sized scratch
   const uint64_t dd_words = np * W.dd_groups;
   if (dd_words > c->dd_cap || np > c->pages_cap) {
@@ -308,10 +317,14 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   const uint32_t C = ncl, R = nr;
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = (o + bytes + 15) & ~size_t(15); return r; };
-  const size_t s_nr0 = take(4ull * R), s_ext = take(4ull * R);
-  const size_t s_ftce = take(8ull * C), s_ftsa = take(8ull * C), s_trsa = take(8ull * C);
-  const size_t s_elig = take(4ull * C), s_iso1 = take(4ull * C), s_iso2 = take(4ull * C), s_iso3 = take(4ull * C);
+  // exchange groups are contiguous: u64 minima [ft_ce | ft_sa | trap_sa | ft_gr | trap_mps],
+  // u32 minima [nr0 | ext | iso1 | iso2 | iso3], general-path u32 minima [giso]
+  const size_t s_u64 = take(8ull * (3ull * C + 2));
+  const size_t s_u32 = take(4ull * (2ull * R + 3ull * C));
   const size_t s_giso = take(12ull * C), s_glob = take(sizeof(Globals)), s_err = take(8);
+  c->x_u64 = s_u64; c->x_u64_n = 3ull * C + 2;
+  c->x_u32 = s_u32; c->x_u32_n = 2ull * R + 3ull * C;
+  c->x_giso = s_giso; c->x_giso_n = 3ull * C;
   const size_t empty_bytes = o;
   const size_t s_ctrl = take(4 * C_NCTRL);
   const size_t zero_bytes = o - empty_bytes;
@@ -330,15 +343,18 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   Scratch& S = c->S;
   S.dd = c->d_dd;
   S.nr1 = c->d_nr1;
-  S.nr0 = reinterpret_cast<uint32_t*>(s + s_nr0);
-  S.ext = reinterpret_cast<uint32_t*>(s + s_ext);
-  S.ft_ce = reinterpret_cast<unsigned long long*>(s + s_ftce);
-  S.ft_sa = reinterpret_cast<unsigned long long*>(s + s_ftsa);
-  S.trap_sa = reinterpret_cast<unsigned long long*>(s + s_trsa);
-  S.elig = reinterpret_cast<uint32_t*>(s + s_elig);
-  S.iso1 = reinterpret_cast<uint32_t*>(s + s_iso1);
-  S.iso2 = reinterpret_cast<uint32_t*>(s + s_iso2);
-  S.iso3 = reinterpret_cast<uint32_t*>(s + s_iso3);
+  unsigned long long* u64 = reinterpret_cast<unsigned long long*>(s + s_u64);
+  S.ft_ce = u64;
+  S.ft_sa = u64 + C;
+  S.trap_sa = u64 + 2ull * C;
+  S.ft_gr = u64 + 3ull * C;
+  S.trap_mps = u64 + 3ull * C + 1;
+  uint32_t* u32 = reinterpret_cast<uint32_t*>(s + s_u32);
+  S.nr0 = u32;
+  S.ext = u32 + R;
+  S.iso1 = u32 + 2ull * R;
+  S.iso2 = u32 + 2ull * R + C;
+  S.iso3 = u32 + 2ull * R + 2ull * C;
   S.giso = reinterpret_cast<uint32_t*>(s + s_giso);
   S.glob = reinterpret_cast<Globals*>(s + s_glob);
   S.err_idx = reinterpret_cast<unsigned long long*>(s + s_err);
@@ -390,13 +406,30 @@ static int ensure_call_scratch(mpsf_ctx* c, uint64_t n) {
   return MPSF_OK;
 }
 
-int mpsf_process(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const mpsf_params* p,
-                 mpsf_out_record* d_out, mpsf_client_verdict* d_verdict, uint64_t* d_counts,
-                 uint64_t* d_dkeys, uint32_t* d_didx, uint32_t* d_cancel, void* stream) {
+static Params to_params(const mpsf_params* p) {
+  Params P;
+  P.flags = p->flags;
+  P.benign_us = p->benign_us;
+  P.m1_us = p->m1_us;
+  P.m2_us = p->m2_us;
+  P.m3_us = p->m3_us;
+  P.base_index = p->base_index;
+  return P;
+}
+
+int mpsf_set_dense_dedup(mpsf_ctx* c, int on) {
+  if (!c) return MPSF_E_ARG;
+  c->dense_dedup = on != 0;
+  return MPSF_OK;
+}
+
+// phase 1: clear scratch + k_scan
+int mpsf_scan(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const mpsf_params* p, uint64_t* d_counts,
+              void* stream) {
   if (!c || !p) return MPSF_E_ARG;
   if (!c->has_world) return MPSF_E_NO_WORLD;
-  if (n && (!d_in || !d_out || !d_dkeys || !d_didx || !d_cancel)) return MPSF_E_ARG;
-  if (c->W.n_clients && (!d_verdict || !d_counts)) return MPSF_E_ARG;
+  if (n && !d_in) return MPSF_E_ARG;
+  if (c->W.n_clients && !d_counts) return MPSF_E_ARG;
   if (p->base_index + n > MAX_GIDX) return MPSF_E_TOO_LARGE;
   CK(cudaSetDevice(c->device));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -420,25 +453,133 @@ int mpsf_process(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const mp
   const Marker mk = c->marker();
   k_init<<<dim3(2 * sms, k), 256, 0, st>>>(segs);
   mk.mark("k_init");
-  Params P;
-  P.flags = p->flags;
-  P.benign_us = p->benign_us;
-  P.m1_us = p->m1_us;
-  P.m2_us = p->m2_us;
-  P.m3_us = p->m3_us;
-  P.base_index = p->base_index;
-  int launches = 0;
-  if (launch_fault_path(c->W, c->S, d_in, n, P, d_out, d_verdict, reinterpret_cast<unsigned long long*>(d_counts),
-                        reinterpret_cast<unsigned long long*>(d_dkeys), d_didx, d_cancel, c->d_count_part, st,
-                        &launches, mk))
+  const Params P = to_params(p);
+  if (launch_scan(c->W, c->S, d_in, n, P, reinterpret_cast<unsigned long long*>(d_counts), c->d_count_part, st, mk,
+                  &c->parts))
     return MPSF_E_CUDA;
-  k_summary<<<1, 1, 0, st>>>(c->S.ctrl, c->S.err_idx, c->d_tiles, nt, c->d_sum);
+  c->phase_n = n;
+  c->last_launches = n ? 2 : 1;
+  return MPSF_OK;
+}
+
+int mpsf_resolve(mpsf_ctx* c, const mpsf_params* p, mpsf_client_verdict* d_verdict, uint64_t* d_counts,
+                 void* stream) {
+  if (!c || !p) return MPSF_E_ARG;
+  if (c->W.n_clients && (!d_verdict || !d_counts)) return MPSF_E_ARG;
+  CK(cudaSetDevice(c->device));
+  if (launch_resolve(c->W, c->S, to_params(p), d_verdict, c->d_count_part, c->parts,
+                     reinterpret_cast<unsigned long long*>(d_counts), reinterpret_cast<cudaStream_t>(stream),
+                     c->marker()))
+    return MPSF_E_CUDA;
+  c->last_launches += 1;
+  return MPSF_OK;
+}
+
+int mpsf_general(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const mpsf_params* p, int stage,
+                 void* stream) {
+  if (!c || !p || (stage != 1 && stage != 2)) return MPSF_E_ARG;
+  if (!(p->flags & MPSF_PF_ISOLATION) || n == 0) return MPSF_OK;
+  CK(cudaSetDevice(c->device));
+  if (launch_general(c->W, c->S, d_in, n, to_params(p), stage, reinterpret_cast<cudaStream_t>(stream), c->marker()))
+    return MPSF_E_CUDA;
+  c->last_launches += 1;
+  return MPSF_OK;
+}
+
+int mpsf_resolve2(mpsf_ctx* c, const mpsf_params* p, void* stream) {
+  if (!c || !p) return MPSF_E_ARG;
+  if (!(p->flags & MPSF_PF_ISOLATION)) return MPSF_OK;
+  CK(cudaSetDevice(c->device));
+  if (launch_resolve2(c->W, c->S, to_params(p), reinterpret_cast<cudaStream_t>(stream), c->marker()))
+    return MPSF_E_CUDA;
+  c->last_launches += 1;
+  return MPSF_OK;
+}
+
+int mpsf_finalize(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const mpsf_params* p,
+                  mpsf_out_record* d_out, uint64_t* d_dkeys, uint32_t* d_didx, uint32_t* d_cancel, void* stream) {
+  if (!c || !p) return MPSF_E_ARG;
+  if (n && (!d_in || !d_out || !d_dkeys || !d_didx || !d_cancel)) return MPSF_E_ARG;
+  if (n != c->phase_n) return MPSF_E_ARG;
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const Marker mk = c->marker();
+  if (launch_finalize(c->W, c->S, d_in, n, to_params(p), d_out, reinterpret_cast<unsigned long long*>(d_dkeys), d_didx,
+                      d_cancel, st, mk))
+    return MPSF_E_CUDA;
+  k_summary<<<1, 1, 0, st>>>(c->S.ctrl, c->S.err_idx, c->d_tiles, tiles_for(n), c->d_sum);
   mk.mark("k_summary");
   CK(cudaGetLastError());
   CK(cudaEventRecord(c->ev_done, st));
   c->pending = true;
   c->last_n = n;
-  c->last_launches = launches + 2;
+  c->last_launches += n ? 2 : 1;
+  return MPSF_OK;
+}
+
+int mpsf_process(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const mpsf_params* p,
+                 mpsf_out_record* d_out, mpsf_client_verdict* d_verdict, uint64_t* d_counts,
+                 uint64_t* d_dkeys, uint32_t* d_didx, uint32_t* d_cancel, void* stream) {
+  if (!c || !p) return MPSF_E_ARG;
+  if (n && (!d_in || !d_out || !d_dkeys || !d_didx || !d_cancel)) return MPSF_E_ARG;
+  int rc = mpsf_scan(c, d_in, n, p, d_counts, stream);
+  if (!rc) rc = mpsf_resolve(c, p, d_verdict, d_counts, stream);
+  if (!rc && (p->flags & MPSF_PF_ISOLATION) && n) {
+    rc = mpsf_general(c, d_in, n, p, 1, stream);
+    if (!rc && p->m2_us <= p->benign_us) rc = mpsf_general(c, d_in, n, p, 2, stream);
+    if (!rc) rc = mpsf_resolve2(c, p, stream);
+  }
+  if (!rc) rc = mpsf_finalize(c, d_in, n, p, d_out, d_dkeys, d_didx, d_cancel, stream);
+  return rc;
+}
+
+int mpsf_exchange_buffers(mpsf_ctx* c, int stage, mpsf_xbuf* out, int cap) {
+  if (!c || (cap && !out)) return MPSF_E_ARG;
+  if (!c->has_world) return MPSF_E_NO_WORLD;
+  mpsf_xbuf b[4];
+  int k = 0;
+  uint8_t* s = c->d_small;
+  if (stage == 1) {
+    b[k++] = {s + c->x_u64, c->x_u64_n, 8, MPSF_XOP_MIN};
+    b[k++] = {s + c->x_u32, c->x_u32_n, 4, MPSF_XOP_MIN};
+    if (c->W.dd_groups != 5) return MPSF_E_ARG;   // claimed slots are not combinable: set dense dedup
+    b[k++] = {c->d_dd, c->W.n_pages * 5, 4, MPSF_XOP_MIN};
+  } else if (stage == 2) {
+    b[k++] = {s + c->x_giso, c->x_giso_n, 4, MPSF_XOP_MIN};
+    b[k++] = {c->d_nr1, c->W.n_pages, 4, MPSF_XOP_MIN};
+  } else if (stage == 3) {
+    b[k++] = {s + c->x_giso, c->x_giso_n, 4, MPSF_XOP_MIN};
+  } else {
+    return MPSF_E_ARG;
+  }
+  for (int i = 0; i < k && i < cap; ++i) out[i] = b[i];
+  return k;
+}
+
+int64_t mpsf_hash_export(mpsf_ctx* c, int which, uint64_t* d_keys, uint32_t* d_vals, uint64_t cap, void* stream) {
+  if (!c || (which != 0 && which != 1) || (cap && (!d_keys || !d_vals))) return MPSF_E_ARG;
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (!c->d_counter) CK(cudaMalloc(&c->d_counter, 4));
+  CK(cudaMemsetAsync(c->d_counter, 0, 4, st));
+  const Hash& h = which == 0 ? c->S.hdd : c->S.hnr;
+  const uint64_t hcap = which == 0 ? c->hcap_dd : c->hcap_nr;
+  if (launch_hash_export(h, hcap, reinterpret_cast<unsigned long long*>(d_keys), d_vals, c->d_counter, cap, st))
+    return MPSF_E_CUDA;
+  uint32_t cnt = 0;
+  CK(cudaMemcpyAsync(&cnt, c->d_counter, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return cnt > cap ? MPSF_E_OVERFLOW : (int64_t)cnt;
+}
+
+int mpsf_hash_merge(mpsf_ctx* c, int which, const uint64_t* d_keys, const uint32_t* d_vals, uint64_t count,
+                    void* stream) {
+  if (!c || (which != 0 && which != 1) || (count && (!d_keys || !d_vals))) return MPSF_E_ARG;
+  CK(cudaSetDevice(c->device));
+  const Hash& h = which == 0 ? c->S.hdd : c->S.hnr;
+  if (launch_hash_merge(h, c->S.ctrl, reinterpret_cast<const unsigned long long*>(d_keys), d_vals, count,
+                        reinterpret_cast<cudaStream_t>(stream)))
+    return MPSF_E_CUDA;
   return MPSF_OK;
 }
 

@@ -52,8 +52,6 @@ static_assert(sizeof(CState) == 32, "CState layout");
 
 // scalars shared by every client
 struct Globals {
-  unsigned long long ft_gr;     // min (ok32 << 8 | sid) over fatal GR-TSG records
-  unsigned long long trap_mps;  // min (idx << 8 | sid) over traps raised by MPS clients
   uint32_t ft_gr_ok;            // applied GR teardown record (ok32) or EMPTY32
   uint32_t trap_mps_idx;        // applied MPS trap (idx) or EMPTY32
   uint32_t gr_alive0;
@@ -89,7 +87,8 @@ struct Scratch {
   unsigned long long* ft_ce;    // [C]
   unsigned long long* ft_sa;    // [C]
   unsigned long long* trap_sa;  // [C]
-  uint32_t* elig;      // [C] first isolation-eligible record
+  unsigned long long* ft_gr;    // min (ok32 << 8 | sid) over fatal GR-TSG records
+  unsigned long long* trap_mps; // min (idx << 8 | sid) over traps raised by MPS clients
   uint32_t* iso1;      // [C] snapshot-unmapped eligible (M1 candidates)
   uint32_t* iso2;      // [C] managed-range eligible (M2)
   uint32_t* iso3;      // [C] external-range eligible (M3 candidates)

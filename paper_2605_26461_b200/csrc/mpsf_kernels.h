@@ -18,13 +18,26 @@ struct Marker {
   }
 };
 
-int launch_fault_path(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n,
-                      const Params& P, mpsf_out_record* out, mpsf_client_verdict* verdict,
-                      unsigned long long* counts, unsigned long long* dkeys, uint32_t* didx,
-                      uint32_t* cancel, uint32_t* count_part, cudaStream_t st, int* launches,
-                      const Marker& mk);
+// pass 1; *parts = number of per-block count partial rows written (0: counts went to global)
+int launch_scan(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
+                unsigned long long* counts, uint32_t* count_part, cudaStream_t st, const Marker& mk,
+                uint32_t* parts);
+int launch_resolve(const World& W, const Scratch& S, const Params& P, mpsf_client_verdict* verdict,
+                   const uint32_t* count_part, uint32_t parts, unsigned long long* counts, cudaStream_t st,
+                   const Marker& mk);
+int launch_general(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
+                   int stage, cudaStream_t st, const Marker& mk);
+int launch_resolve2(const World& W, const Scratch& S, const Params& P, cudaStream_t st, const Marker& mk);
+int launch_finalize(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
+                    mpsf_out_record* out, unsigned long long* dkeys, uint32_t* didx, uint32_t* cancel,
+                    cudaStream_t st, const Marker& mk);
+int launch_hash_export(const Hash& h, uint64_t cap, unsigned long long* keys, uint32_t* vals, uint32_t* counter,
+                       uint64_t out_cap, cudaStream_t st);
+int launch_hash_merge(const Hash& h, uint32_t* ctrl, const unsigned long long* keys, const uint32_t* vals,
+                      uint64_t count, cudaStream_t st);
 uint64_t tiles_for(uint64_t n);
 uint32_t count_parts_needed(const World& W);   // per-block count partial rows k_scan may write
+
 int launch_remap(uint64_t va_base, const uint64_t* phys, uint64_t npages4k, uint32_t gran_log2,
                  mpsf_remap_entry* out, cudaStream_t st);
 int launch_remap_blocks(uint64_t va_base, const uint64_t* phys, uint64_t npages4k,

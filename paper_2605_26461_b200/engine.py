@@ -110,6 +110,11 @@ class FaultEngine:
             raise_for(rc, self.lib.mpsf_strerror(rc).decode(), index)
 
     # -- world ---------------------------------------------------------------------------
+    def set_dense_dedup(self, on: bool = True) -> None:
+        """One dedup slot per (page, group) regardless of world size (required for sharded
+        runs, whose dedup slots are combined with an all-reduce MIN).  Call before upload."""
+        self._check(self.lib.mpsf_set_dense_dedup(self.ctx, 1 if on else 0))
+
     def upload_world(self, w: FlatWorld) -> None:
         """``mpsf_upload_world``: the interval table, page states, channels, clients."""
         r = np.ascontiguousarray(w.ranges)

@@ -1,19 +1,267 @@
-"""Multi-GPU plumbing for sharded fault traces (one process per GPU, torch.distributed).
+"""Sharded multi-GPU fault path: one process per GPU, torch.distributed.
 
-``combine_verdicts_nccl`` reduces per-shard client fates with an elementwise MAX
-all-reduce (state: terminated > running; reason/notifier by the same order).
+A batch is split into contiguous entry ranges; rank r processes entries with global indices
+``base_r .. base_r + n_r`` (``BatchParams.base_index``) against a replicated world.  Every
+cross-entry dependency of the batch rules is a first-in-group minimum over the drain key,
+a sum, or a max of flags, so the shards only need:
+
+1. after pass 1 (``mpsf_scan``): all-reduce MIN of the dense group minima (fatal TSG
+   teardowns, traps, first isolation per external range / guard page / client) and of the
+   dense dedup slots, plus a sparse merge (all-gather + atomic-min insert) of the two
+   wild-page hash tables;
+2. with isolation on, after the release-aware stage (``mpsf_general`` 1): MIN of the exact
+   per-client mechanism minima and of the epoch-1 first-isolation slots, sparse NR merge;
+   after stage 2 (only when m2 <= benign): MIN of the per-client M2 minima;
+3. after ``mpsf_finalize``: SUM of the per-(client, scenario) counts.
+
+Per-client fates come out identical on every rank; each rank's OutRecords, cancel list and
+dedup set cover its own index range, so concatenating them in rank order reproduces the
+single-GPU result bit for bit.  Collectives go through NCCL over NVLink on GPUs and gloo in
+the CPU tests; unsigned MIN is done on signed views with the sign bit flipped.
 """
 
 from __future__ import annotations
 
+import ctypes as C
+
 import numpy as np
 
+from . import _lib
+from .engine import BatchParams, DeviceBuffers, FaultEngine
 from .world import VERDICT_DTYPE
 
 
-def combine_verdicts_nccl(verdict: np.ndarray) -> np.ndarray:
-    import torch
+def _dist():
     import torch.distributed as dist
+    return dist
+
+
+def allreduce_min_unsigned(t, group=None):
+    """MIN over ranks of an unsigned array held in a signed (int32/int64) view, in place."""
+    import torch
+    dist = _dist()
+    flip = torch.tensor(-(1 << 31) if t.dtype == torch.int32 else -(1 << 63), dtype=t.dtype, device=t.device)
+    t.bitwise_xor_(flip)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    t.bitwise_xor_(flip)
+
+
+def allreduce_sum(t, group=None):
+    dist = _dist()
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+
+
+def allgather_ragged(keys, vals, group=None):
+    """All-gather two aligned 1-D tensors of per-rank length; returns the concatenation."""
+    import torch
+    dist = _dist()
+    ws = dist.get_world_size(group)
+    cnt = torch.tensor([keys.numel()], dtype=torch.int64, device=keys.device)
+    cnts = [torch.zeros_like(cnt) for _ in range(ws)]
+    dist.all_gather(cnts, cnt, group=group)
+    m = int(max(int(c.item()) for c in cnts))
+    if m == 0:
+        return keys[:0], vals[:0]
+    kp = torch.full((m,), -1, dtype=keys.dtype, device=keys.device)
+    vp = torch.full((m,), -1, dtype=vals.dtype, device=vals.device)
+    kp[:keys.numel()] = keys
+    vp[:vals.numel()] = vals
+    ka = [torch.empty_like(kp) for _ in range(ws)]
+    va = [torch.empty_like(vp) for _ in range(ws)]
+    dist.all_gather(ka, kp, group=group)
+    dist.all_gather(va, vp, group=group)
+    ks = torch.cat([ka[r][:int(cnts[r].item())] for r in range(ws)])
+    vs = torch.cat([va[r][:int(cnts[r].item())] for r in range(ws)])
+    return ks, vs
+
+
+class ShardedFaultPath:
+    """Drives one shard through the phase API and the cross-rank exchanges."""
+
+    def __init__(self, adapter, group=None):
+        self.a = adapter
+        self.group = group
+
+    def _combine(self, stage):
+        for t, op in self.a.exchange(stage):
+            if op == "min":
+                allreduce_min_unsigned(t, self.group)
+            else:
+                allreduce_sum(t, self.group)
+
+    def _merge_hash(self, which):
+        keys, vals = self.a.hash_export(which)
+        ks, vs = allgather_ragged(keys, vals, self.group)
+        self.a.hash_merge(which, ks, vs)
+
+    def process(self, params: BatchParams):
+        a = self.a
+        a.scan(params)
+        self._combine(1)
+        self._merge_hash(0)
+        self._merge_hash(1)
+        a.resolve(params)
+        if params.isolation:
+            a.general(params, 1)
+            self._combine(2)
+            self._merge_hash(1)
+            if params.m2_us <= params.benign_us:
+                a.general(params, 2)
+                self._combine(3)
+            a.resolve2(params)
+        a.finalize(params)
+        allreduce_sum(a.counts_tensor(), self.group)
+        return a.result()
+
+
+class LocalShardGroup:
+    """The same phase sequence and exchanges as :class:`ShardedFaultPath`, but over several
+    shards held by one process (e.g. several contexts on one device): the reductions are
+    elementwise across the shards' buffers instead of collectives."""
+
+    def __init__(self, adapters):
+        self.ads = adapters
+
+    def _combine(self, stage):
+        import torch
+        groups = list(zip(*[a.exchange(stage) for a in self.ads]))
+        for bufs in groups:
+            ts = [t for t, _ in bufs]
+            op = bufs[0][1]
+            if op == "min":
+                flip = -(1 << 31) if ts[0].dtype == torch.int32 else -(1 << 63)
+                acc = ts[0] ^ flip
+                for t in ts[1:]:
+                    acc = torch.minimum(acc, (t.to(acc.device)) ^ flip)
+                acc = acc ^ flip
+            else:
+                acc = sum(t.to(ts[0].device) for t in ts)
+            for t in ts:
+                t.copy_(acc.to(t.device))
+
+    def _merge_hash(self, which):
+        import torch
+        ex = [a.hash_export(which) for a in self.ads]
+        ks = torch.cat([k.to(ex[0][0].device) for k, _ in ex])
+        vs = torch.cat([v.to(ex[0][1].device) for _, v in ex])
+        for a in self.ads:
+            a.hash_merge(which, ks, vs)
+
+    def process(self, params_list):
+        for a, p in zip(self.ads, params_list):
+            a.scan(p)
+        self._combine(1)
+        self._merge_hash(0)
+        self._merge_hash(1)
+        p0 = params_list[0]
+        for a, p in zip(self.ads, params_list):
+            a.resolve(p)
+        if p0.isolation:
+            for a, p in zip(self.ads, params_list):
+                a.general(p, 1)
+            self._combine(2)
+            self._merge_hash(1)
+            if p0.m2_us <= p0.benign_us:
+                for a, p in zip(self.ads, params_list):
+                    a.general(p, 2)
+                self._combine(3)
+            for a, p in zip(self.ads, params_list):
+                a.resolve2(p)
+        for a, p in zip(self.ads, params_list):
+            a.finalize(p)
+        import torch
+        tot = sum(a.counts_tensor().clone() for a in self.ads)
+        for a in self.ads:
+            a.counts_tensor().copy_(tot)
+        return [a.result() for a in self.ads]
+
+
+class _CAI:
+    """Zero-copy torch view of device memory owned by libmpsf.so (CUDA array interface)."""
+
+    def __init__(self, ptr, count, typestr):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3}
+
+
+def device_view(ptr, count, elem_bytes):
+    import torch
+    return torch.as_tensor(_CAI(ptr, count, "<i8" if elem_bytes == 8 else "<i4"), device="cuda")
+
+
+class GpuShard:
+    """Adapter: the GPU phase entry points of libmpsf.so for one rank's shard."""
+
+    def __init__(self, eng: FaultEngine, d_in, n: int, bufs: DeviceBuffers):
+        import torch
+        self.eng, self.d_in, self.n, self.bufs = eng, d_in, n, bufs
+        self.lib, self.ctx = eng.lib, eng.ctx
+        self.stream = torch.cuda.current_stream()
+        self.sp = C.c_void_p(self.stream.cuda_stream)
+        cap = 1 << 20
+        self.hk = torch.empty(cap, dtype=torch.int64, device="cuda")
+        self.hv = torch.empty(cap, dtype=torch.int32, device="cuda")
+
+    def _p(self, params):
+        self.cp = params.to_c()
+        return C.byref(self.cp)
+
+    def scan(self, params):
+        self.eng._check(self.lib.mpsf_scan(self.ctx, self.d_in.data_ptr(), self.n, self._p(params),
+                                           self.bufs.counts.data_ptr(), self.sp))
+
+    def exchange(self, stage):
+        arr = (_lib.XBuf * 4)()
+        k = self.lib.mpsf_exchange_buffers(self.ctx, stage, C.cast(arr, C.c_void_p), 4)
+        self.eng._check(min(k, 0))
+        return [(device_view(arr[i].ptr, arr[i].count, arr[i].elem_bytes), "min" if arr[i].op == 0 else "sum")
+                for i in range(k)]
+
+    def hash_export(self, which):
+        while True:
+            k = self.lib.mpsf_hash_export(self.ctx, which, self.hk.data_ptr(), self.hv.data_ptr(),
+                                          self.hk.numel(), self.sp)
+            if k >= 0:
+                return self.hk[:k], self.hv[:k]
+            import torch
+            self.hk = torch.empty(self.hk.numel() * 4, dtype=torch.int64, device="cuda")
+            self.hv = torch.empty(self.hv.numel() * 4, dtype=torch.int32, device="cuda")
+
+    def hash_merge(self, which, keys, vals):
+        keys, vals = keys.contiguous(), vals.contiguous()
+        self.eng._check(self.lib.mpsf_hash_merge(self.ctx, which, keys.data_ptr(), vals.data_ptr(),
+                                                 keys.numel(), self.sp))
+
+    def resolve(self, params):
+        self.eng._check(self.lib.mpsf_resolve(self.ctx, self._p(params), self.bufs.verdict.data_ptr(),
+                                              self.bufs.counts.data_ptr(), self.sp))
+
+    def general(self, params, stage):
+        self.eng._check(self.lib.mpsf_general(self.ctx, self.d_in.data_ptr(), self.n, self._p(params), stage,
+                                              self.sp))
+
+    def resolve2(self, params):
+        self.eng._check(self.lib.mpsf_resolve2(self.ctx, self._p(params), self.sp))
+
+    def finalize(self, params):
+        b = self.bufs
+        self.eng._check(self.lib.mpsf_finalize(self.ctx, self.d_in.data_ptr(), self.n, self._p(params),
+                                               b.out.data_ptr(), b.dkeys.data_ptr(), b.didx.data_ptr(),
+                                               b.cancel.data_ptr(), self.sp))
+
+    def counts_tensor(self):
+        from . import constants as K
+        return self.bufs.counts[:8 * K.N_SCENARIOS * self.eng.world.n_clients].view(__import__("torch").int64)
+
+    def result(self):
+        s = self.eng.summary()
+        return self.bufs.fetch(self.n, self.eng.world.n_clients, int(s.n_dedup), int(s.n_cancel), int(s.path))
+
+
+def combine_verdicts_nccl(verdict: np.ndarray) -> np.ndarray:
+    """Elementwise MAX of per-shard client fates (used only by the replica fallback)."""
+    import torch
+    dist = _dist()
     t = torch.from_numpy(verdict.view(np.uint8).astype(np.int32)).cuda()
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return t.to(torch.uint8).cpu().numpy().view(VERDICT_DTYPE)

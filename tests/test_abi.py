@@ -14,7 +14,7 @@ HEADER = open(os.path.join(ROOT, "include", "mpsf.h")).read()
 
 
 def declared_functions():
-    return set(re.findall(r"^\s*(?:int|void|const char\*)\s+(mpsf_\w+)\(", HEADER, re.M))
+    return set(re.findall(r"^\s*(?:int|int64_t|void|const char\*)\s+(mpsf_\w+)\(", HEADER, re.M))
 
 
 def test_library_exports_every_declared_symbol():

@@ -1,0 +1,144 @@
+"""Sharded (multi-rank) fault path on CPU: world_size-2 gloo runs of
+``parallel.ShardedFaultPath`` driving the phase-by-phase CPU mirror of the kernels
+(``oracle/c9_oracle.py``) must equal the sequential oracle on the whole batch, bit for bit
+(SURVEY.md Appendix C, C8).  The GPU adapter (``parallel.GpuShard``) runs the same
+orchestration over NCCL."""
+
+import os
+import random
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2605_26461_b200 import constants as K
+from paper_2605_26461_b200.engine import BatchParams
+from paper_2605_26461_b200.parallel import ShardedFaultPath
+
+from oracle import c9_oracle as c9
+from oracle import seq_oracle as so
+from tests import randworld as RW
+
+
+def oparams(p: BatchParams) -> so.Params:
+    return so.Params(isolation=p.isolation, benign_us=p.benign_us, m1_us=p.m1_us, m2_us=p.m2_us, m3_us=p.m3_us)
+
+
+class C9Shard:
+    """CPU adapter with the same surface as parallel.GpuShard."""
+
+    def __init__(self, w, entries, base):
+        self.e = c9.C9Engine(w)
+        self.entries, self.base = entries, base
+
+    def scan(self, p):
+        self.e.scan(self.entries, oparams(p), self.base)
+
+    def exchange(self, stage):
+        return [(torch.from_numpy(a.view(np.int64 if a.dtype == np.uint64 else np.int32)), op)
+                for a, op in self.e.exchange_buffers(stage)]
+
+    def hash_export(self, which):
+        k, v = self.e.hash_export(which)
+        return torch.from_numpy(k.view(np.int64).copy()), torch.from_numpy(v.view(np.int32).copy())
+
+    def hash_merge(self, which, ks, vs):
+        self.e.hash_merge(which, ks.numpy().view(np.uint64), vs.numpy().view(np.uint32))
+
+    def resolve(self, p):
+        self.verdict = self.e.resolve(oparams(p))
+
+    def general(self, p, stage):
+        self.e.general(oparams(p), stage)
+
+    def resolve2(self, p):
+        self.e.resolve2(oparams(p))
+
+    def finalize(self, p):
+        self.out, self.dk, self.di, self.ca, self.counts = self.e.finalize(self.entries, oparams(p))
+
+    def counts_tensor(self):
+        return torch.from_numpy(self.e.counts.view(np.int64))
+
+    def result(self):
+        return dict(out=self.out, dk=self.dk, di=self.di, ca=self.ca, verdict=self.verdict,
+                    counts=self.e.counts.reshape(-1, K.N_SCENARIOS).copy())
+
+
+def make_case(seed):
+    rnd = random.Random(seed)
+    w = RW.random_world(rnd, max_mps=4, max_sa=2, dead_p=0.1 if seed % 3 == 0 else 0.0)
+    p = RW.random_params(rnd)
+    entries = RW.random_batch(rnd, w, rnd.randint(2, 90), pool=3)
+    bp = BatchParams(isolation=p.isolation, benign_us=p.benign_us, m1_us=p.m1_us, m2_us=p.m2_us, m3_us=p.m3_us)
+    return w, entries, bp
+
+
+def check_against_oracle(w, entries, bp, parts):
+    want = so.process_batch(w, entries, oparams(bp))
+    out = np.concatenate([r["out"] for r in parts])
+    assert np.array_equal(out, want.out)
+    for r in parts:
+        assert np.array_equal(r["verdict"], want.verdict)
+        assert np.array_equal(r["counts"], want.counts)
+    assert np.array_equal(np.concatenate([r["dk"] for r in parts]), want.dedup_keys)
+    assert np.array_equal(np.concatenate([r["di"] for r in parts]), want.dedup_idx)
+    assert np.array_equal(np.concatenate([r["ca"] for r in parts]), want.cancel)
+
+
+class _NoDist:
+    """Single-shard run: the exchanges become identities."""
+
+
+def test_c9_mirror_single_shard_equals_sequential_oracle(monkeypatch):
+    import paper_2605_26461_b200.parallel as par
+    monkeypatch.setattr(par, "allreduce_min_unsigned", lambda t, g=None: None)
+    monkeypatch.setattr(par, "allreduce_sum", lambda t, g=None: None)
+    monkeypatch.setattr(par, "allgather_ragged", lambda k, v, g=None: (k, v))
+    for seed in range(250):
+        w, entries, bp = make_case(seed)
+        res = ShardedFaultPath(C9Shard(w, entries, 0)).process(bp)
+        check_against_oracle(w, entries, bp, [res])
+
+
+def _worker(rank, ws, port, seeds, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    import pickle
+    results = {}
+    for seed in seeds:
+        w, entries, bp = make_case(seed)
+        n = len(entries)
+        cut = [n * r // ws for r in range(ws + 1)]
+        shard = entries[cut[rank]:cut[rank + 1]]
+        res = ShardedFaultPath(C9Shard(w, shard, cut[rank])).process(bp)
+        results[seed] = res
+    with open(os.path.join(outdir, f"r{rank}.pkl"), "wb") as f:
+        pickle.dump(results, f)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("ws", [2, 3])
+def test_sharded_gloo_equals_sequential_oracle(ws):
+    import pickle
+    seeds = list(range(1000, 1060))
+    with tempfile.TemporaryDirectory() as d:
+        mp.start_processes(_worker, args=(ws, _free_port(), seeds, d), nprocs=ws, start_method="fork")
+        per_rank = [pickle.load(open(os.path.join(d, f"r{r}.pkl"), "rb")) for r in range(ws)]
+    for seed in seeds:
+        w, entries, bp = make_case(seed)
+        check_against_oracle(w, entries, bp, [per_rank[r][seed] for r in range(ws)])
