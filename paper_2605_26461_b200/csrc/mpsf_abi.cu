@@ -295,7 +295,7 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   W.dd_groups = (c->dense_dedup || np * 5 * 4 <= (64ull << 20)) ? 5 : 1;
   // page-sized scratch
   const uint64_t dd_words = np * W.dd_groups;
-  if (dd_words > c->dd_cap || np > c->pages_cap) {
+  if (!c->d_dd || dd_words > c->dd_cap || np > c->pages_cap) {
     cudaFree(c->d_dd);
     cudaFree(c->d_nr1);
     c->d_dd = c->d_nr1 = nullptr;

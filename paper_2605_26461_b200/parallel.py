@@ -186,6 +186,8 @@ class _CAI:
 
 def device_view(ptr, count, elem_bytes):
     import torch
+    if not ptr or not count:
+        return torch.empty(0, dtype=torch.int64 if elem_bytes == 8 else torch.int32, device="cuda")
     return torch.as_tensor(_CAI(ptr, count, "<i8" if elem_bytes == 8 else "<i4"), device="cuda")
 
 

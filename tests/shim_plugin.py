@@ -1,0 +1,30 @@
+"""pytest plugin: run the REFERENCE's own test suite with ``mpssim.pipeline.service_bottom_half``
+replaced by the batch drop-in (``paper_2605_26461_b200.shim``).  The engine behind it is the
+C oracle here (CPU container); on a GPU box the same shim takes a ``FaultEngine``."""
+
+import numpy as np
+
+CALLS = {"n": 0, "records": 0}
+
+
+class OracleEngine:
+    def upload_world(self, flat):
+        self.flat = flat
+
+    def process(self, entries, params):
+        from oracle import c_oracle as co
+        from oracle import seq_oracle as so
+        CALLS["n"] += 1
+        CALLS["records"] += len(entries)
+        return co.process_batch(self.flat, entries, so.Params(
+            isolation=params.isolation, benign_us=params.benign_us, m1_us=params.m1_us,
+            m2_us=params.m2_us, m3_us=params.m3_us))
+
+
+def pytest_configure(config):
+    from paper_2605_26461_b200 import shim
+    shim.install(OracleEngine())
+
+
+def pytest_sessionfinish(session, exitstatus):
+    print(f"\nSHIM_CALLS={CALLS['n']} SHIM_RECORDS={CALLS['records']}")
