@@ -31,12 +31,17 @@
 
 namespace mpsf {
 
+// Warp-specialised CTA: warp 0 is the control warp (TMA producer; in the finalize pass also
+// the decoupled look-back, one tile behind the workers), warps 1..31 are workers.
 constexpr int BLOCK = 1024;
 constexpr int WARPS = BLOCK / 32;
-constexpr int EPT = 4;                  // entries per lane per tile
-constexpr int TILE = BLOCK * EPT;       // 2048 entries = 32 KiB
-constexpr int NBUF = 2;
+constexpr int WORKERS = WARPS - 1;
+constexpr int EPT = 2;                     // entries per worker lane per tile
+constexpr int WSEG = 32 * EPT;             // entries per worker warp per tile
+constexpr int TILE = WORKERS * WSEG;       // 1984 entries = 31 KiB
+constexpr int NBUF = 3;
 constexpr uint32_t TILE_BYTES = TILE * 16;
+constexpr uint32_t TID_NONE = 0xFFFFFFFFu;
 
 // ---- PTX: mbarrier + bulk async copy (TMA) ---------------------------------------------
 __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -47,6 +52,9 @@ __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(b)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   asm volatile(
@@ -73,7 +81,7 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 __host__ __device__ inline uint32_t al16(uint64_t x) { return (uint32_t)((x + 15) & ~uint64_t(15)); }
 
 struct Layout {
-  uint32_t tiles, bars, tids, lut, ranges, channels, client_off, cinfo;
+  uint32_t tiles, bars, tids, tot, pre, lut, ranges, channels, client_off, cinfo;
   uint32_t c64, c32, r32, counts, cstate, total;
 };
 
@@ -82,8 +90,10 @@ __host__ __device__ inline Layout make_layout(uint32_t nr, uint32_t nc, uint32_t
   Layout L;
   uint32_t o = 0;
   L.tiles = o; o += NBUF * TILE_BYTES;
-  L.bars = o; o += 16 * NBUF;
-  L.tids = o; o += 16;
+  L.bars = o; o += 4 * 8 * NBUF;          // full, empty, done, pref per buffer
+  L.tids = o; o += al16(4 * NBUF);
+  L.tot = o; o += 8 * 32 * NBUF;          // per buffer, per worker warp: (cancel, dedup) counts
+  L.pre = o; o += 8 * 32 * NBUF;          // per buffer, per worker warp: exclusive output offsets
   L.lut = o; o += 2048;
   L.ranges = o; if (staged) o += al16(32ull * nr);
   L.channels = o; if (staged) o += al16(8ull * nch);
@@ -244,34 +254,69 @@ __device__ __forceinline__ uint32_t dd_slot(const World& W, const Rec& r) {
   return W.dd_groups == 1 ? r.at.slot : r.at.slot * W.dd_groups + r.group;
 }
 
-// ---- tile pipeline ------------------------------------------------------------------------
-// Thread 0 issues bulk copies; every thread waits on the slot's mbarrier.
+// ---- warp-specialised tile pipeline ---------------------------------------------------------
+// full[b]: TMA bytes landed (control arrive.expect_tx + tx count)      -- workers wait
+// empty[b]: every worker warp is done with buffer b (31 arrivals)      -- control waits, refills
+// done[b]/pref[b] (finalize only): worker counts posted / tile offsets known
 struct Pipe {
   uint8_t* buf;
-  uint64_t* bar;
-  uint32_t* tids;   // tile id per slot (finalize: dynamic scheduling)
+  uint64_t *full, *empty, *done, *pref;
+  uint32_t* tids;
+  uint32_t* tot;    // [NBUF][32][2]
+  uint32_t* pre;    // [NBUF][32][2]
   uint64_t pol;
 };
 
-__device__ __forceinline__ void pipe_issue(const Pipe& p, int slot, const mpsf_fault_entry* in, uint64_t n, uint64_t t) {
+__device__ __forceinline__ void pipe_issue(const Pipe& p, int b, const mpsf_fault_entry* in, uint64_t n, uint64_t t) {
   const uint64_t start = t * TILE;
   const uint64_t cnt = n - start < (uint64_t)TILE ? n - start : (uint64_t)TILE;
   const uint32_t bytes = (uint32_t)(cnt * 16);
-  mbar_expect_tx(p.bar + slot, bytes);
-  bulk_load(p.buf + (size_t)slot * TILE_BYTES, in + start, bytes, p.bar + slot, p.pol);
+  mbar_expect_tx(p.full + b, bytes);
+  bulk_load(p.buf + (size_t)b * TILE_BYTES, in + start, bytes, p.full + b, p.pol);
+}
+
+// Buffer b has no more work: complete its full barrier without data (tids[b] = TID_NONE).
+__device__ __forceinline__ void pipe_close(const Pipe& p, int b) {
+  p.tids[b] = TID_NONE;
+  mbar_arrive(p.full + b);
 }
 
 __device__ __forceinline__ Pipe pipe_init(uint8_t* sm, const Layout& L) {
   Pipe p;
   p.buf = sm + L.tiles;
-  p.bar = reinterpret_cast<uint64_t*>(sm + L.bars);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.bars);
+  p.full = bars; p.empty = bars + NBUF; p.done = bars + 2 * NBUF; p.pref = bars + 3 * NBUF;
   p.tids = reinterpret_cast<uint32_t*>(sm + L.tids);
+  p.tot = reinterpret_cast<uint32_t*>(sm + L.tot);
+  p.pre = reinterpret_cast<uint32_t*>(sm + L.pre);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NBUF; ++s) mbar_init(p.bar + s, 1);
+    for (int b = 0; b < NBUF; ++b) {
+      mbar_init(p.full + b, 1);
+      mbar_init(p.empty + b, WORKERS);
+      mbar_init(p.done + b, WORKERS);
+      mbar_init(p.pref + b, 1);
+    }
     fence_mbar_init();
   }
   p.pol = policy_evict_first();
   return p;
+}
+
+// Control-warp loop for the statically scheduled passes (tile t = blockIdx + j*grid).
+__device__ __forceinline__ void control_static(const Pipe& p, const mpsf_fault_entry* in, uint64_t n) {
+  if ((threadIdx.x & 31) != 0) return;
+  const uint64_t ntiles = (n + TILE - 1) / TILE;
+  for (uint32_t j = 0;; ++j) {
+    const int b = j % NBUF;
+    const uint64_t t = blockIdx.x + (uint64_t)j * gridDim.x;
+    if (j >= (uint32_t)NBUF) mbar_wait(p.empty + b, ((j / NBUF) - 1) & 1);
+    if (t >= ntiles) {
+      pipe_close(p, b);
+      return;
+    }
+    p.tids[b] = (uint32_t)t;
+    pipe_issue(p, b, in, n, t);
+  }
 }
 
 // ---- pass 1 ---------------------------------------------------------------------------------
@@ -348,30 +393,28 @@ __global__ void __launch_bounds__(BLOCK, 1) k_scan(World W, Scratch S, const mps
   const Layout L = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, false);
   const View v = setup<kStaged>(smem, L, W, S, true, false);
   Pipe p = pipe_init(smem, L);
-  const uint64_t ntiles = (n + TILE - 1) / TILE;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < NBUF; ++s) {
-      const uint64_t t = blockIdx.x + (uint64_t)s * gridDim.x;
-      if (t < ntiles) pipe_issue(p, s, in, n, t);
-    }
-  }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t j = 0;
-  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
-    const int slot = j & 1;
-    mbar_wait(p.bar + slot, (j >> 1) & 1);
-    const uint4* tile = reinterpret_cast<const uint4*>(p.buf + (size_t)slot * TILE_BYTES);
-    const uint64_t start = t * TILE;
+  if (warp == 0) {
+    control_static(p, in, n);
+  } else {
+    const int seg = (warp - 1) * WSEG;
+    for (uint32_t j = 0;; ++j) {
+      const int b = j % NBUF;
+      mbar_wait(p.full + b, (j / NBUF) & 1);
+      const uint32_t t = p.tids[b];
+      if (t == TID_NONE) break;
+      const uint4* tile = reinterpret_cast<const uint4*>(p.buf + (size_t)b * TILE_BYTES);
+      const uint64_t start = (uint64_t)t * TILE;
 #pragma unroll 1
-    for (int k = 0; k < EPT; ++k) {
-      const int li = warp * (32 * EPT) + k * 32 + lane;
-      const uint64_t i = start + li;
-      if (i < n) scan_entry<kStaged>(W, v, S, P, tile[li], P.base_index + i, counts);
+      for (int k = 0; k < EPT; ++k) {
+        const int li = seg + k * 32 + lane;
+        const uint64_t i = start + li;
+        if (i < n) scan_entry<kStaged>(W, v, S, P, tile[li], P.base_index + i, counts);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p.empty + b);
     }
-    __syncthreads();
-    const uint64_t nt = t + (uint64_t)NBUF * gridDim.x;
-    if (threadIdx.x == 0 && nt < ntiles) pipe_issue(p, slot, in, n, nt);
   }
   if (kStaged) {
     __syncthreads();
@@ -539,30 +582,28 @@ __global__ void __launch_bounds__(BLOCK, 1) k_general(World W, Scratch S, const 
   const Layout L = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, true);
   const View v = setup<kStaged>(smem, L, W, S, false, true);
   Pipe p = pipe_init(smem, L);
-  const uint64_t ntiles = (n + TILE - 1) / TILE;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < NBUF; ++s) {
-      const uint64_t t = blockIdx.x + (uint64_t)s * gridDim.x;
-      if (t < ntiles) pipe_issue(p, s, in, n, t);
-    }
-  }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t j = 0;
-  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
-    const int slot = j & 1;
-    mbar_wait(p.bar + slot, (j >> 1) & 1);
-    const uint4* tile = reinterpret_cast<const uint4*>(p.buf + (size_t)slot * TILE_BYTES);
-    const uint64_t start = t * TILE;
+  if (warp == 0) {
+    control_static(p, in, n);
+    return;
+  }
+  const int seg = (warp - 1) * WSEG;
+  for (uint32_t j = 0;; ++j) {
+    const int b = j % NBUF;
+    mbar_wait(p.full + b, (j / NBUF) & 1);
+    const uint32_t t = p.tids[b];
+    if (t == TID_NONE) break;
+    const uint4* tile = reinterpret_cast<const uint4*>(p.buf + (size_t)b * TILE_BYTES);
+    const uint64_t start = (uint64_t)t * TILE;
 #pragma unroll 1
     for (int k = 0; k < EPT; ++k) {
-      const int li = warp * (32 * EPT) + k * 32 + lane;
+      const int li = seg + k * 32 + lane;
       const uint64_t i = start + li;
       if (i < n) general_entry<kStaged, kStage>(W, v, S, P, tile[li], P.base_index + i);
     }
-    __syncthreads();
-    const uint64_t nt = t + (uint64_t)NBUF * gridDim.x;
-    if (threadIdx.x == 0 && nt < ntiles) pipe_issue(p, slot, in, n, nt);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(p.empty + b);
   }
 }
 
@@ -653,35 +694,127 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const
                                                        unsigned long long* __restrict__ dkeys,
                                                        uint32_t* __restrict__ didx, uint32_t* __restrict__ cancel) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint32_t s_wc[WARPS], s_wd[WARPS];
-  __shared__ uint32_t s_pc, s_pd;
   if (__ldcg(S.ctrl + C_ERR) != 0) return;
   const Layout L = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, true);
   const View v = setup<kStaged>(smem, L, W, S, false, true);
   Pipe p = pipe_init(smem, L);
   const Globals G = *S.glob;
   const uint32_t ntiles = (uint32_t)((n + TILE - 1) / TILE);
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < NBUF; ++s) {
-      const uint32_t t = atomicAdd(S.ctrl + C_TILE_FIN, 1u);
-      p.tids[s] = t;
-      if (t < ntiles) pipe_issue(p, s, in, n, t);
-    }
-  }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    // control warp: dynamic in-order tile ids, TMA refill, and the look-back of tile j
+    // while the workers already process tile j+1
+    auto refill = [&](int b) {
+      if (lane == 0) {
+        const uint32_t t = atomicAdd(S.ctrl + C_TILE_FIN, 1u);
+        if (t < ntiles) {
+          p.tids[b] = t;
+          fence_proxy_async();
+          pipe_issue(p, b, in, n, t);
+        } else {
+          pipe_close(p, b);
+        }
+      }
+      __syncwarp();
+    };
+    for (int b = 0; b < NBUF; ++b) refill(b);
+    for (uint32_t j = 0;; ++j) {
+      const int b = j % NBUF;
+      const uint32_t t = *reinterpret_cast<volatile uint32_t*>(p.tids + b);
+      if (t == TID_NONE) break;
+      mbar_wait(p.done + b, (j / NBUF) & 1);
+      const uint32_t* tot = p.tot + b * 64;
+      uint32_t c = lane ? tot[2 * lane] : 0u, d = lane ? tot[2 * lane + 1] : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {          // inclusive warp scan of the worker counts
+        const uint32_t uc = __shfl_up_sync(0xFFFFFFFFu, c, o), ud = __shfl_up_sync(0xFFFFFFFFu, d, o);
+        if (lane >= o) { c += uc; d += ud; }
+      }
+      const uint32_t tc = __shfl_sync(0xFFFFFFFFu, c, 31), td = __shfl_sync(0xFFFFFFFFu, d, 31);
+      const uint32_t ec = c - (lane ? tot[2 * lane] : 0u), ed = d - (lane ? tot[2 * lane + 1] : 0u);
+      // decoupled look-back, 32 predecessors per step
+      volatile unsigned long long* desc = S.tiles;
+      uint32_t pc = 0, pd = 0;
+      if (t == 0) {
+        if (lane == 0) desc[0] = LB_PRE | lb_pack(tc, td);
+      } else {
+        if (lane == 0) desc[t] = LB_AGG | lb_pack(tc, td);
+        int64_t q = (int64_t)t - 1;
+        while (true) {
+          const int64_t idx = q - lane;
+          unsigned long long dsc = 2ull << 62;          // before tile 0: an empty prefix
+          if (idx >= 0) dsc = desc[idx];
+          const unsigned long long st = dsc & ~LB_VAL;
+          const unsigned notready = __ballot_sync(0xFFFFFFFFu, st == 0);
+          const unsigned isp = __ballot_sync(0xFFFFFFFFu, st == LB_PRE);
+          const int firstp = isp ? __ffs(isp) - 1 : 32;
+          const unsigned need = firstp < 32 ? ((2u << firstp) - 1u) : 0xFFFFFFFFu;
+          if (notready & need) {
+            __nanosleep(64);
+            continue;
+          }
+          uint32_t vc = ((need >> lane) & 1u) ? (uint32_t)(dsc & 0x7FFFFFFFull) : 0u;
+          uint32_t vd = ((need >> lane) & 1u) ? (uint32_t)((dsc >> 31) & 0x7FFFFFFFull) : 0u;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            vc += __shfl_xor_sync(0xFFFFFFFFu, vc, o);
+            vd += __shfl_xor_sync(0xFFFFFFFFu, vd, o);
+          }
+          pc += vc;
+          pd += vd;
+          if (firstp < 32) break;
+          q -= 32;
+        }
+        if (lane == 0) desc[t] = LB_PRE | lb_pack(pc + tc, pd + td);
+      }
+      p.pre[b * 64 + 2 * lane] = pc + ec;
+      p.pre[b * 64 + 2 * lane + 1] = pd + ed;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p.pref + b);
+      // buffer b is refilled once the workers have written tile j's lists out of it
+      if (lane == 0) mbar_wait(p.empty + b, (j / NBUF) & 1);
+      __syncwarp();
+      refill(b);
+    }
+    return;
+  }
+  // worker warps
   const unsigned lt_mask = (1u << lane) - 1u;
-  for (uint32_t j = 0;; ++j) {
-    const int slot = j & 1;
-    const uint32_t t = p.tids[slot];
-    if (t >= ntiles) break;
-    mbar_wait(p.bar + slot, (j >> 1) & 1);
-    uint4* tile = reinterpret_cast<uint4*>(p.buf + (size_t)slot * TILE_BYTES);
+  const int seg = (warp - 1) * WSEG;
+  uint64_t prev_start = 0;
+  auto writeout = [&](uint32_t jj, uint64_t start) {
+    const int b = jj % NBUF;
+    mbar_wait(p.pref + b, (jj / NBUF) & 1);
+    const uint4* tile = reinterpret_cast<const uint4*>(p.buf + (size_t)b * TILE_BYTES);
+    const uint32_t bc0 = p.pre[b * 64 + 2 * warp], bd0 = p.pre[b * 64 + 2 * warp + 1];
+#pragma unroll 1
+    for (int k = 0; k < EPT; ++k) {
+      const int li = seg + k * 32 + lane;
+      const uint4 q = tile[li];
+      const uint32_t gidx = (uint32_t)(P.base_index + start + li);
+      if (q.z & 1u) cancel[bc0 + (q.w & 0xFFFFu)] = gidx;
+      if (q.z & 2u) {
+        const uint32_t d = bd0 + (q.w >> 16);
+        dkeys[d] = (unsigned long long)q.x | ((unsigned long long)q.y << 32);
+        didx[d] = gidx;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(p.empty + b);
+  };
+  uint32_t j = 0;
+  for (;; ++j) {
+    const int b = j % NBUF;
+    mbar_wait(p.full + b, (j / NBUF) & 1);
+    const uint32_t t = p.tids[b];
+    if (t == TID_NONE) break;
+    uint4* tile = reinterpret_cast<uint4*>(p.buf + (size_t)b * TILE_BYTES);
     const uint64_t start = (uint64_t)t * TILE;
     uint32_t wc = 0, wd = 0;
 #pragma unroll 1
     for (int k = 0; k < EPT; ++k) {
-      const int li = warp * (32 * EPT) + k * 32 + lane;
+      const int li = seg + k * 32 + lane;
       const uint64_t i = start + li;
       mpsf_out_record o;
       bool canc = false, rep = false;
@@ -692,67 +825,22 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const
       }
       const unsigned bc = __ballot_sync(0xFFFFFFFFu, canc);
       const unsigned bd = __ballot_sync(0xFFFFFFFFu, rep);
-      // park the compaction payload in the (consumed) entry slot
-      tile[li] = make_uint4((uint32_t)key, (uint32_t)(key >> 32),
-                            (canc ? 1u : 0u) | (rep ? 2u : 0u),
+      // park the compaction payload in the consumed entry slot
+      tile[li] = make_uint4((uint32_t)key, (uint32_t)(key >> 32), (canc ? 1u : 0u) | (rep ? 2u : 0u),
                             (wc + __popc(bc & lt_mask)) | ((wd + __popc(bd & lt_mask)) << 16));
       wc += __popc(bc);
       wd += __popc(bd);
     }
-    if (lane == 0) { s_wc[warp] = wc; s_wd[warp] = wd; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t tc = 0, td = 0;
-      for (int w = 0; w < WARPS; ++w) {
-        const uint32_t a = s_wc[w], b = s_wd[w];
-        s_wc[w] = tc; s_wd[w] = td;
-        tc += a; td += b;
-      }
-      volatile unsigned long long* desc = S.tiles;
-      uint32_t pc = 0, pd = 0;
-      if (t == 0) {
-        desc[0] = LB_PRE | lb_pack(tc, td);
-      } else {
-        desc[t] = LB_AGG | lb_pack(tc, td);
-        int64_t q = (int64_t)t - 1;
-        while (q >= 0) {
-          const unsigned long long d = desc[q];
-          const unsigned long long st = d & ~LB_VAL;
-          if (st == 0) continue;
-          pc += (uint32_t)(d & 0x7FFFFFFFull);
-          pd += (uint32_t)((d >> 31) & 0x7FFFFFFFull);
-          if (st == LB_PRE) break;
-          --q;
-        }
-        desc[t] = LB_PRE | lb_pack(pc + tc, pd + td);
-      }
-      s_pc = pc; s_pd = pd;
+    if (lane == 0) {
+      p.tot[b * 64 + 2 * warp] = wc;
+      p.tot[b * 64 + 2 * warp + 1] = wd;
     }
-    __syncthreads();
-    const uint32_t bc0 = s_pc + s_wc[warp], bd0 = s_pd + s_wd[warp];
-#pragma unroll 1
-    for (int k = 0; k < EPT; ++k) {
-      const int li = warp * (32 * EPT) + k * 32 + lane;
-      const uint4 q = tile[li];
-      const uint32_t gidx = (uint32_t)(P.base_index + start + li);
-      if (q.z & 1u) cancel[bc0 + (q.w & 0xFFFFu)] = gidx;
-      if (q.z & 2u) {
-        const uint32_t d = bd0 + (q.w >> 16);
-        dkeys[d] = (unsigned long long)q.x | ((unsigned long long)q.y << 32);
-        didx[d] = gidx;
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const uint32_t nt = atomicAdd(S.ctrl + C_TILE_FIN, 1u);
-      p.tids[slot] = nt;
-      if (nt < ntiles) {
-        fence_proxy_async();
-        pipe_issue(p, slot, in, n, nt);
-      }
-    }
-    __syncthreads();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(p.done + b);
+    if (j > 0) writeout(j - 1, prev_start);
+    prev_start = start;
   }
+  if (j > 0) writeout(j - 1, prev_start);
 }
 
 // ---- sparse hash exchange (multi-GPU) ------------------------------------------------------
