@@ -81,11 +81,14 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 __host__ __device__ inline uint32_t al16(uint64_t x) { return (uint32_t)((x + 15) & ~uint64_t(15)); }
 
 struct Layout {
-  uint32_t tiles, bars, tids, tot, pre, lut, ranges, channels, client_off, cinfo;
-  uint32_t c64, c32, r32, counts, cstate, total;
+  uint32_t tiles, bars, tids, tot, pre;
+  uint32_t pg_base, pg_end, poff, rattr, rrid, skip, crange, cspan, cshift, chan;
+  uint32_t c64, iso, r32, counts, cstate, total;
+  uint32_t rep_chan;
 };
 
-// kStaged: the interval table and the per-client/per-range caches live in smem
+// kStaged: the interval table (page-granular SoA + skip table, per-client words and the
+// channel table replicated per bank) and the pass-1 caches live in smem
 __host__ __device__ inline Layout make_layout(uint32_t nr, uint32_t nc, uint32_t nch, bool staged, bool fin) {
   Layout L;
   uint32_t o = 0;
@@ -94,13 +97,19 @@ __host__ __device__ inline Layout make_layout(uint32_t nr, uint32_t nc, uint32_t
   L.tids = o; o += al16(4 * NBUF);
   L.tot = o; o += 8 * 32 * NBUF;          // per buffer, per worker warp: (cancel, dedup) counts
   L.pre = o; o += 8 * 32 * NBUF;          // per buffer, per worker warp: exclusive output offsets
-  L.lut = o; o += 2048;
-  L.ranges = o; if (staged) o += al16(32ull * nr);
-  L.channels = o; if (staged) o += al16(8ull * nch);
-  L.client_off = o; if (staged) o += al16(4ull * (nc + 1));
-  L.cinfo = o; if (staged) o += al16(nc);
+  L.rep_chan = (staged && nch <= 256) ? 32u : 0u;
+  L.pg_base = o; if (staged) o += al16(4ull * nr);
+  L.pg_end = o; if (staged) o += al16(4ull * nr);
+  L.poff = o; if (staged) o += al16(4ull * nr);
+  L.rattr = o; if (staged) o += al16(4ull * nr);
+  L.rrid = o; if (staged && fin) o += al16(4ull * nr);
+  L.skip = o; if (staged) o += al16(2ull * SKIP_K * nc);
+  L.crange = o; if (staged) o += al16(128ull * nc);
+  L.cspan = o; if (staged) o += al16(128ull * nc);
+  L.cshift = o; if (staged) o += al16(128ull * nc);
+  L.chan = o; if (staged) o += al16(4ull * nch * (L.rep_chan ? 32 : 1));
   L.c64 = o; if (staged && !fin) o += al16(24ull * nc);
-  L.c32 = o; if (staged && !fin) o += al16(12ull * nc);
+  L.iso = o; if (staged && !fin) o += al16(3ull * 128 * nc);
   L.r32 = o; if (staged && !fin) o += al16(8ull * nr);
   L.counts = o; if (staged && !fin) o += al16(4ull * NSCEN * nc);
   L.cstate = o; if (staged && fin) o += al16(32ull * nc);
@@ -108,73 +117,70 @@ __host__ __device__ inline Layout make_layout(uint32_t nr, uint32_t nc, uint32_t
   return L;
 }
 
-// Block-wide view of the world tables (smem when staged, else global).
+// Block-wide view of the world tables (smem when staged, else global) and pass-1 caches.
 struct View {
-  const mpsf_range_entry* ranges;
-  const mpsf_channel_entry* channels;
-  const uint32_t* client_off;
-  const uint8_t* cinfo;     // mode (bit0 = standalone)
-  const uint8_t* lut;       // classify LUT
+  Tables T;
   unsigned long long *ft_ce, *ft_sa, *trap_sa;   // pass-1 caches (or null)
-  uint32_t *iso1, *iso2, *iso3, *ext, *nr0, *counts;
+  uint32_t* iso;                                  // [3][C][32] per-lane copies (or null)
+  uint32_t *ext, *nr0, *counts;
   const CState* cst;
 };
-
-// LUT index of faults.classify inputs: eng | acc<<2 | has<<4 | kind<<5 | zombie<<6 | migr<<7 | st<<8
-__device__ __forceinline__ uint32_t lut_index(int eng, int acc, const Attr& a) {
-  return (uint32_t)eng | ((uint32_t)acc << 2) |
-         (a.in_range ? (16u | ((uint32_t)a.kind << 5) | ((uint32_t)a.lifecycle << 6) |
-                        ((a.migratable ? 1u : 0u) << 7) | ((a.st & 7u) << 8))
-                     : 0u);
-}
 
 template <bool kStaged>
 __device__ View setup(uint8_t* sm, const Layout& L, const World& W, const Scratch& S, bool scan, bool fin) {
   View v;
-  const int tid = threadIdx.x;
-  uint8_t* lut = sm + L.lut;
-  for (uint32_t i = tid; i < 2048; i += blockDim.x) {
-    const int eng = i & 3, acc = (i >> 2) & 3;
-    const bool has = (i >> 4) & 1;
-    lut[i] = (eng > 2 || acc > 2) ? 0xFF
-                                  : (uint8_t)classify(eng, acc, has, (i >> 5) & 1, (i >> 6) & 1, (i >> 7) & 1, (i >> 8) & 7);
-  }
-  v.lut = lut;
+  const uint32_t tid = threadIdx.x, nb = blockDim.x;
+  const uint32_t R = W.n_ranges, C = W.n_clients;
   if (kStaged) {
-    mpsf_range_entry* r = reinterpret_cast<mpsf_range_entry*>(sm + L.ranges);
-    const uint4* src = reinterpret_cast<const uint4*>(W.ranges);
-    uint4* dst = reinterpret_cast<uint4*>(r);
-    for (uint32_t i = tid; i < 2 * W.n_ranges; i += blockDim.x) dst[i] = __ldg(src + i);
-    mpsf_channel_entry* ch = reinterpret_cast<mpsf_channel_entry*>(sm + L.channels);
-    for (uint32_t i = tid; i < W.n_channels; i += blockDim.x) ch[i] = W.channels[i];
-    uint32_t* off = reinterpret_cast<uint32_t*>(sm + L.client_off);
-    for (uint32_t i = tid; i <= W.n_clients; i += blockDim.x) off[i] = __ldg(W.client_off + i);
-    uint8_t* ci = sm + L.cinfo;
-    for (uint32_t i = tid; i < W.n_clients; i += blockDim.x) ci[i] = W.clients[i].mode;
-    v.ranges = r; v.channels = ch; v.client_off = off; v.cinfo = ci;
+    uint32_t* pb = reinterpret_cast<uint32_t*>(sm + L.pg_base);
+    uint32_t* pe = reinterpret_cast<uint32_t*>(sm + L.pg_end);
+    uint32_t* po = reinterpret_cast<uint32_t*>(sm + L.poff);
+    uint32_t* ra = reinterpret_cast<uint32_t*>(sm + L.rattr);
+    uint32_t* rr = reinterpret_cast<uint32_t*>(sm + L.rrid);
+    for (uint32_t i = tid; i < R; i += nb) {
+      pb[i] = __ldg(W.pg_base + i); pe[i] = __ldg(W.pg_end + i);
+      po[i] = __ldg(W.poff + i); ra[i] = __ldg(W.rattr + i);
+      if (fin) rr[i] = __ldg(W.rrid + i);
+    }
+    uint16_t* sk = reinterpret_cast<uint16_t*>(sm + L.skip);
+    for (uint32_t i = tid; i < SKIP_K * C; i += nb) sk[i] = __ldg(W.skip + i);
+    uint32_t* cr = reinterpret_cast<uint32_t*>(sm + L.crange);
+    uint32_t* cs = reinterpret_cast<uint32_t*>(sm + L.cspan);
+    uint32_t* ch = reinterpret_cast<uint32_t*>(sm + L.cshift);
+    for (uint32_t i = tid; i < 32 * C; i += nb) {
+      cr[i] = __ldg(W.crange + i / 32); cs[i] = __ldg(W.cspan + i / 32); ch[i] = __ldg(W.cshift + i / 32);
+    }
+    uint32_t* cn = reinterpret_cast<uint32_t*>(sm + L.chan);
+    const uint32_t rc = L.rep_chan ? 32u : 1u;
+    for (uint32_t i = tid; i < rc * W.n_channels; i += nb) cn[i] = __ldg(W.chan + i / rc);
+    v.T.pg_base = pb; v.T.pg_end = pe; v.T.poff = po; v.T.rattr = ra; v.T.rrid = fin ? rr : W.rrid;
+    v.T.skip = sk; v.T.crange = cr; v.T.cspan = cs; v.T.cshift = ch; v.T.chan = cn;
+    v.T.rep_client = 32; v.T.rep_chan = L.rep_chan;
   } else {
-    v.ranges = W.ranges; v.channels = W.channels; v.client_off = W.client_off; v.cinfo = nullptr;
+    v.T.pg_base = W.pg_base; v.T.pg_end = W.pg_end; v.T.poff = W.poff; v.T.rattr = W.rattr; v.T.rrid = W.rrid;
+    v.T.skip = W.skip; v.T.crange = W.crange; v.T.cspan = W.cspan; v.T.cshift = W.cshift; v.T.chan = W.chan;
+    v.T.rep_client = 0; v.T.rep_chan = 0;
   }
   v.ft_ce = v.ft_sa = v.trap_sa = nullptr;
-  v.iso1 = v.iso2 = v.iso3 = v.ext = v.nr0 = v.counts = nullptr;
+  v.iso = v.ext = v.nr0 = v.counts = nullptr;
   v.cst = S.cstate;
   if (kStaged && scan) {
     unsigned long long* c64 = reinterpret_cast<unsigned long long*>(sm + L.c64);
-    for (uint32_t i = tid; i < 3 * W.n_clients; i += blockDim.x) c64[i] = EMPTY64;
-    v.ft_ce = c64; v.ft_sa = c64 + W.n_clients; v.trap_sa = c64 + 2 * W.n_clients;
-    uint32_t* c32 = reinterpret_cast<uint32_t*>(sm + L.c32);
-    for (uint32_t i = tid; i < 3 * W.n_clients; i += blockDim.x) c32[i] = EMPTY32;
-    v.iso1 = c32; v.iso2 = c32 + W.n_clients; v.iso3 = c32 + 2 * W.n_clients;
+    for (uint32_t i = tid; i < 3 * C; i += nb) c64[i] = EMPTY64;
+    v.ft_ce = c64; v.ft_sa = c64 + C; v.trap_sa = c64 + 2 * C;
+    uint32_t* iso = reinterpret_cast<uint32_t*>(sm + L.iso);
+    for (uint32_t i = tid; i < 3 * 32 * C; i += nb) iso[i] = EMPTY32;
+    v.iso = iso;
     uint32_t* r32 = reinterpret_cast<uint32_t*>(sm + L.r32);
-    for (uint32_t i = tid; i < 2 * W.n_ranges; i += blockDim.x) r32[i] = EMPTY32;
-    v.ext = r32; v.nr0 = r32 + W.n_ranges;
+    for (uint32_t i = tid; i < 2 * R; i += nb) r32[i] = EMPTY32;
+    v.ext = r32; v.nr0 = r32 + R;
     uint32_t* cnt = reinterpret_cast<uint32_t*>(sm + L.counts);
-    for (uint32_t i = tid; i < NSCEN * W.n_clients; i += blockDim.x) cnt[i] = 0;
+    for (uint32_t i = tid; i < NSCEN * C; i += nb) cnt[i] = 0;
     v.counts = cnt;
   }
   if (kStaged && fin) {
     CState* cs = reinterpret_cast<CState*>(sm + L.cstate);
-    for (uint32_t i = tid; i < W.n_clients; i += blockDim.x) cs[i] = S.cstate[i];
+    for (uint32_t i = tid; i < C; i += nb) cs[i] = S.cstate[i];
     v.cst = cs;
   }
   return v;
@@ -207,28 +213,29 @@ __device__ __forceinline__ Rec decode(const World& W, const View& v, const Scrat
   const uint32_t w3 = e.w;
   if (!(w3 >> 24 & MPSF_ENTRY_VALID)) return r;
   const uint32_t ch = e.z;
+  const uint32_t lane = threadIdx.x & 31;
   r.eng = (int)(w3 & 0xFF);
   const int acc = (int)((w3 >> 8) & 0xFF);
   r.kind = (int)((w3 >> 16) & 0xFF);
   if (ch >= W.n_channels) { raise_err(S, EB_NO_CHANNEL, gidx); return r; }
-  const mpsf_channel_entry ce = v.channels[ch];
-  if (ce.client >= W.n_clients) { raise_err(S, EB_NO_CHANNEL, gidx); return r; }
-  r.c = ce.client;
-  r.ceng = ce.engine;
-  r.sa = (kStaged ? v.cinfo[r.c] : W.clients[r.c].mode) & 1;
+  const uint32_t cw = rep_load(v.T.chan, ch, v.T.rep_chan, lane);
+  if (!(cw & CH_VALID)) { raise_err(S, EB_NO_CHANNEL, gidx); return r; }
+  r.c = cw & 0xFFFFu;
+  r.ceng = (int)((cw >> 16) & 3u);
+  r.sa = (cw >> 18) & 1u;
   r.group = 0;
   r.at.ridx = -1; r.at.in_range = false; r.at.guard = false; r.at.rid = NO_RID;
   if (r.kind == 0) {
     if (r.eng > 2 || acc > 2) { raise_err(S, EB_BAD_ENTRY, gidx); return r; }
     if (r.eng != r.ceng) { raise_err(S, EB_MISMATCH, gidx); return r; }
     if (r.va >= VA_LIMIT) { raise_err(S, EB_VA, gidx); return r; }
-    r.at = attribute(v.ranges, W.page_state, v.client_off[r.c], v.client_off[r.c + 1], r.va);
-    const uint32_t li = lut_index(r.eng, acc, r.at);
-    r.s = v.lut[li];
+    r.at = attribute_pg(v.T, W.page_state, r.c, r.va, lane);
+    const bool has = r.at.in_range;
+    r.s = classify(r.eng, acc, has, r.at.kind, r.at.lifecycle, r.at.migratable, r.at.st);
     r.repl = s_replayable(r.s);
     if (r.eng == 0 && acc != 2) {
-      const uint32_t base = li & ~12u;                  // acc bits cleared
-      r.group = (acc == 1 && v.lut[base | 4u] != v.lut[base]) ? 1u : 0u;
+      r.group = (acc == 1 && classify(0, 0, has, r.at.kind, r.at.lifecycle, r.at.migratable, r.at.st) != r.s)
+                    ? 1u : 0u;
     } else {
       r.group = r.eng == 0 ? 2u : (uint32_t)(2 + r.eng);
     }
@@ -343,23 +350,19 @@ __device__ __forceinline__ void scan_entry(const World& W, const View& v, const 
     else if (r.ceng == 1) { if (kStaged) min64c(S.ft_ce + c, v.ft_ce + c, t); else min64(S.ft_ce + c, t); }
     else min64(S.ft_gr, t);
   } else if (!serv) {                                                // isolation-eligible (pipeline.py:177-179)
+    // per-client minimum: iso1 unmapped / iso2 managed / iso3 external (per-lane smem copies)
+    const int m = !r.at.in_range ? 0 : (r.at.kind == 0 ? 1 : 2);
+    uint32_t* g = (m == 0 ? S.iso1 : (m == 1 ? S.iso2 : S.iso3)) + c;
+    if (kStaged) min32c(g, v.iso + ((uint32_t)m * W.n_clients + c) * 32 + (threadIdx.x & 31), ok);
+    else min32(g, ok);
     if (!r.at.in_range) {
-      if (kStaged) min32c(S.iso1 + c, v.iso1 + c, ok); else min32(S.iso1 + c, ok);
       if (r.at.guard) {
         if (kStaged) min32c(S.nr0 + r.at.ridx, v.nr0 + r.at.ridx, ok); else min32(S.nr0 + r.at.ridx, ok);
       } else if (!hash_min(S.hnr, S.ctrl, nr_key(c, 0, r.va >> 12), ok)) {
         atomicOr(S.ctrl + C_OVF, 1u);
       }
-    } else if (r.at.kind == 0) {
-      if (kStaged) min32c(S.iso2 + c, v.iso2 + c, ok); else min32(S.iso2 + c, ok);
-    } else {
-      if (kStaged) {
-        min32c(S.iso3 + c, v.iso3 + c, ok);
-        min32c(S.ext + r.at.ridx, v.ext + r.at.ridx, ok);
-      } else {
-        min32(S.iso3 + c, ok);
-        min32(S.ext + r.at.ridx, ok);
-      }
+    } else if (r.at.kind != 0) {
+      if (kStaged) min32c(S.ext + r.at.ridx, v.ext + r.at.ridx, ok); else min32(S.ext + r.at.ridx, ok);
     }
   }
   if (r.kind == 0 && r.repl) {                                       // dedup insert (rule C2)
@@ -648,7 +651,7 @@ __device__ __forceinline__ void finalize_entry(const World& W, const View& v, co
   const CState cs = v.cst[r.c];
   o.scenario = (uint8_t)r.s;
   o.client = (uint16_t)r.c;
-  o.rid = r.at.in_range ? r.at.rid : NO_RID;
+  o.rid = r.at.in_range ? v.T.rrid[r.at.ridx] : NO_RID;
   if (s_trap(r.s)) {
     // raise_sm_trap at raise time (pipeline.py:151-155); a second trap on a destroyed
     // TSG is cancelled (the reference raises UnknownTsg)
@@ -884,8 +887,8 @@ static int grid_for(K kernel, size_t smem) {
 }
 
 static bool staged_fits(const World& W) {
-  return make_layout(W.n_ranges, W.n_clients, W.n_channels, true, false).total <= 200 * 1024 &&
-         make_layout(W.n_ranges, W.n_clients, W.n_channels, true, true).total <= 200 * 1024;
+  return make_layout(W.n_ranges, W.n_clients, W.n_channels, true, false).total <= 220 * 1024 &&
+         make_layout(W.n_ranges, W.n_clients, W.n_channels, true, true).total <= 220 * 1024;
 }
 
 uint32_t count_parts_needed(const World& W) {

@@ -263,11 +263,53 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   }
   for (uint32_t i = 0; i < nch; ++i)
     if (channels[i].engine > 2) return MPSF_E_WORLD;
+  if (nr > 65535) return MPSF_E_WORLD;
+  // page-granular SoA interval table + per-client skip tables (device form, mpsf_device.cuh)
+  std::vector<uint32_t> pg_base(nr), pg_end(nr), poff(nr), rattr(nr), rrid(nr);
+  for (uint32_t i = 0; i < nr; ++i) {
+    const mpsf_range_entry& r = ranges[i];
+    if (r.end >= VA_TABLE_LIMIT) return MPSF_E_WORLD;
+    pg_base[i] = (uint32_t)(r.base >> 12);
+    pg_end[i] = (uint32_t)(r.end >> 12);
+    poff[i] = r.page_off;
+    rattr[i] = (uint32_t)r.kind | ((uint32_t)r.lifecycle << 8) | ((uint32_t)r.migratable << 16) |
+               ((uint32_t)r.state << 24);
+    rrid[i] = r.rid;
+  }
+  std::vector<uint16_t> skip((size_t)SKIP_K * ncl, 0);
+  std::vector<uint32_t> crange(ncl), cspan(ncl), cshift(ncl);
+  for (uint32_t cl = 0; cl < ncl; ++cl) {
+    const uint32_t lo = off[cl], hi = off[cl + 1];
+    crange[cl] = lo | (hi << 16);
+    if (lo == hi) { cspan[cl] = 0; cshift[cl] = 0; continue; }
+    const uint64_t span_lo = pg_base[lo], span_hi = (uint64_t)pg_end[hi - 1] + 1;
+    uint32_t sh = 0;
+    while (((span_hi - span_lo + (1ull << sh) - 1) >> sh) > (uint64_t)SKIP_K) ++sh;
+    cspan[cl] = (uint32_t)span_lo;
+    cshift[cl] = sh;
+    uint32_t k = lo;
+    for (int j = 0; j < SKIP_K; ++j) {
+      const uint64_t slot = span_lo + ((uint64_t)j << sh);
+      while (k + 1 < hi && pg_base[k + 1] <= slot) ++k;
+      skip[(size_t)cl * SKIP_K + j] = (uint16_t)k;
+    }
+  }
+  std::vector<uint32_t> chan(nch);
+  for (uint32_t i = 0; i < nch; ++i) {
+    const uint32_t cl = channels[i].client;
+    chan[i] = cl < ncl ? ((cl & 0xFFFFu) | ((uint32_t)channels[i].engine << 16) |
+                          ((uint32_t)(clients[cl].mode & 1) << 18) | CH_VALID)
+                       : 0u;
+  }
   const size_t o_r = 0, o_off = a256(o_r + sizeof(mpsf_range_entry) * nr);
   const size_t o_ps = a256(o_off + sizeof(uint32_t) * (ncl + 1));
   const size_t o_ch = a256(o_ps + np);
   const size_t o_cl = a256(o_ch + sizeof(mpsf_channel_entry) * nch);
-  const size_t total = a256(o_cl + sizeof(mpsf_client_entry) * ncl) + 256;
+  const size_t o_soa = a256(o_cl + sizeof(mpsf_client_entry) * ncl);
+  const size_t o_skip = a256(o_soa + 5ull * 4 * nr);
+  const size_t o_cinfo = a256(o_skip + 2ull * SKIP_K * ncl);
+  const size_t o_chan = a256(o_cinfo + 3ull * 4 * ncl);
+  const size_t total = a256(o_chan + 4ull * nch) + 256;
   cudaFree(c->d_world);
   c->d_world = nullptr;
   c->has_world = false;
@@ -278,12 +320,38 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   if (np) CK(cudaMemcpy(b + o_ps, page_state, np, cudaMemcpyHostToDevice));
   if (nch) CK(cudaMemcpy(b + o_ch, channels, sizeof(mpsf_channel_entry) * nch, cudaMemcpyHostToDevice));
   if (ncl) CK(cudaMemcpy(b + o_cl, clients, sizeof(mpsf_client_entry) * ncl, cudaMemcpyHostToDevice));
+  uint32_t* soa = reinterpret_cast<uint32_t*>(b + o_soa);
+  if (nr) {
+    CK(cudaMemcpy(soa, pg_base.data(), 4ull * nr, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(soa + nr, pg_end.data(), 4ull * nr, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(soa + 2ull * nr, poff.data(), 4ull * nr, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(soa + 3ull * nr, rattr.data(), 4ull * nr, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(soa + 4ull * nr, rrid.data(), 4ull * nr, cudaMemcpyHostToDevice));
+  }
+  uint32_t* cinfo = reinterpret_cast<uint32_t*>(b + o_cinfo);
+  if (ncl) {
+    CK(cudaMemcpy(b + o_skip, skip.data(), 2ull * SKIP_K * ncl, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(cinfo, crange.data(), 4ull * ncl, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(cinfo + ncl, cspan.data(), 4ull * ncl, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(cinfo + 2ull * ncl, cshift.data(), 4ull * ncl, cudaMemcpyHostToDevice));
+  }
+  if (nch) CK(cudaMemcpy(b + o_chan, chan.data(), 4ull * nch, cudaMemcpyHostToDevice));
   World& W = c->W;
   W.ranges = reinterpret_cast<const mpsf_range_entry*>(b + o_r);
   W.client_off = reinterpret_cast<const uint32_t*>(b + o_off);
   W.page_state = b + o_ps;
   W.channels = reinterpret_cast<const mpsf_channel_entry*>(b + o_ch);
   W.clients = reinterpret_cast<const mpsf_client_entry*>(b + o_cl);
+  W.pg_base = soa;
+  W.pg_end = soa + nr;
+  W.poff = soa + 2ull * nr;
+  W.rattr = soa + 3ull * nr;
+  W.rrid = soa + 4ull * nr;
+  W.skip = reinterpret_cast<const uint16_t*>(b + o_skip);
+  W.crange = cinfo;
+  W.cspan = cinfo + ncl;
+  W.cshift = cinfo + 2ull * ncl;
+  W.chan = reinterpret_cast<const uint32_t*>(b + o_chan);
   W.n_ranges = nr;
   W.n_clients = ncl;
   W.n_channels = nch;

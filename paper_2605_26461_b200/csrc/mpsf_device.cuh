@@ -58,17 +58,34 @@ struct Globals {
   uint32_t has_elig;
 };
 
+constexpr int SKIP_K = 64;               // skip-table slots per client
+constexpr uint64_t VA_TABLE_LIMIT = 1ull << 44;   // interval tables hold 32-bit page numbers
+
+// Device form of the interval table, built by mpsf_upload_world (page-granular SoA so a warp's
+// random lookups touch 4-byte words: no 32-byte-row bank conflicts).
 struct World {
-  const mpsf_range_entry* ranges;
+  const mpsf_range_entry* ranges;   // original rows (host order)
   const uint32_t* client_off;
   const uint8_t* page_state;
   const mpsf_channel_entry* channels;
   const mpsf_client_entry* clients;
+  const uint32_t* pg_base;          // [R] base >> 12
+  const uint32_t* pg_end;           // [R] end >> 12
+  const uint32_t* poff;             // [R] first page-state slot
+  const uint32_t* rattr;            // [R] kind | lifecycle << 8 | migratable << 16 | state << 24
+  const uint32_t* rrid;             // [R] reference rid
+  const uint16_t* skip;             // [C][SKIP_K] last range with base <= slot start
+  const uint32_t* crange;           // [C] lo | hi << 16 (range slice)
+  const uint32_t* cspan;            // [C] first page of the client's span
+  const uint32_t* cshift;           // [C] log2 pages per skip slot
+  const uint32_t* chan;             // [nch] client | engine << 16 | standalone << 18 | valid << 31
   uint32_t n_ranges, n_clients, n_channels, world_flags;
   uint64_t n_pages;
   uint32_t has_mps;
   uint32_t dd_groups;   // 5: one dense dedup slot per (page, group); 1: one claimed slot per page
 };
+
+constexpr uint32_t CH_VALID = 1u << 31;
 
 struct Hash {
   unsigned long long* keys;
@@ -138,6 +155,53 @@ struct Attr {
   int kind, lifecycle, migratable;
   uint32_t rid;
 };
+
+// Tables a lookup reads (shared memory when staged, else global).  The per-client words and
+// the channel table may be replicated 32x ([i][lane]) so a warp's lookups are bank-conflict free.
+struct Tables {
+  const uint32_t *pg_base, *pg_end, *poff, *rattr, *rrid;
+  const uint16_t* skip;
+  const uint32_t *crange, *cspan, *cshift, *chan;
+  uint32_t rep_client, rep_chan;   // 32 when replicated per lane, else 0
+};
+
+__device__ __forceinline__ uint32_t rep_load(const uint32_t* a, uint32_t i, uint32_t rep, uint32_t lane) {
+  return rep ? a[i * 32 + lane] : a[i];
+}
+
+// Attribution, restating MemoryModel.range_at (memory.py:233-237): the skip table narrows
+// the client's slice to the range covering the slot start; a short forward walk finishes.
+__device__ __forceinline__ Attr attribute_pg(const Tables& T, const uint8_t* __restrict__ page_state,
+                                             uint32_t c, uint64_t va, uint32_t lane) {
+  Attr t;
+  t.ridx = -1; t.in_range = false; t.guard = false; t.slot = 0; t.st = 0;
+  t.kind = 0; t.lifecycle = 0; t.migratable = 1; t.rid = NO_RID;
+  const uint32_t cr = rep_load(T.crange, c, T.rep_client, lane);
+  const uint32_t lo = cr & 0xFFFFu, hi = cr >> 16;
+  if (lo == hi || va >= VA_TABLE_LIMIT) return t;
+  const uint32_t page = (uint32_t)(va >> 12);
+  const uint32_t span = rep_load(T.cspan, c, T.rep_client, lane);
+  if (page < span) return t;
+  const uint32_t sh = rep_load(T.cshift, c, T.rep_client, lane);
+  uint32_t j = (page - span) >> sh;
+  j = j < (uint32_t)SKIP_K ? j : (uint32_t)(SKIP_K - 1);
+  uint32_t k = T.skip[c * SKIP_K + j];
+  while (k + 1 < hi && T.pg_base[k + 1] <= page) ++k;
+  const uint32_t end = T.pg_end[k];
+  if (page < end) {
+    const uint32_t a = T.rattr[k];
+    const uint32_t base = T.pg_base[k];
+    t.ridx = (int)k; t.in_range = true;
+    t.slot = T.poff[k] + (page - base);
+    t.kind = a & 0xFF; t.lifecycle = (a >> 8) & 0xFF; t.migratable = (a >> 16) & 0xFF;
+    const uint32_t ust = a >> 24;
+    t.st = ust != 0xFF ? ust : (uint32_t)page_state[t.slot];
+  } else if (page == end) {
+    t.ridx = (int)k; t.guard = true;
+    t.slot = T.poff[k] + (end - T.pg_base[k]);
+  }
+  return t;
+}
 
 // Binary search of client's slice [lo, hi) for the last range with base <= va.
 __device__ __forceinline__ Attr attribute(const mpsf_range_entry* __restrict__ R,
