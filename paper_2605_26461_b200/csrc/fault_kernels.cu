@@ -368,7 +368,10 @@ __device__ __forceinline__ void scan_entry(const World& W, const View& v, const 
   if (r.kind == 0 && r.repl) {                                       // dedup insert (rule C2)
     const uint32_t val = ((uint32_t)gidx << 3) | r.group;
     bool to_hash = !(r.at.in_range || r.at.guard);
-    if (!to_hash) {
+    if (!to_hash && W.dd_groups != 1) {
+      // one slot per (page, group): a fire-and-forget reduction, no round trip
+      atomicMin(S.dd + dd_slot(W, r), val);
+    } else if (!to_hash) {
       uint32_t* slot = S.dd + dd_slot(W, r);
       uint32_t cur = __ldcg(slot);
       while (true) {
@@ -850,10 +853,10 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const
 __global__ void k_hash_export(Hash h, uint64_t cap, unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals,
                               uint32_t* __restrict__ counter, uint64_t out_cap) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap; i += (uint64_t)gridDim.x * blockDim.x) {
-    const unsigned long long k = h.keys[i];
+    const unsigned long long k = h.keys[2 * i];
     if (k == EMPTY64) continue;
     const uint32_t o = atomicAdd(counter, 1u);
-    if (o < out_cap) { keys[o] = k; vals[o] = h.vals[i]; }
+    if (o < out_cap) { keys[o] = k; vals[o] = *hash_val(h, (uint32_t)i); }
   }
 }
 

@@ -451,23 +451,21 @@ static int ensure_call_scratch(mpsf_ctx* c, uint64_t n) {
     cudaFree(c->d_hdd);
     c->d_hdd = nullptr;
     c->hcap_dd = 0;
-    CK(cudaMalloc(&c->d_hdd, 12 * c->want_dd));
+    CK(cudaMalloc(&c->d_hdd, 16 * c->want_dd));
     c->hcap_dd = c->want_dd;
   }
   if (c->want_nr != c->hcap_nr) {
     cudaFree(c->d_hnr);
     c->d_hnr = nullptr;
     c->hcap_nr = 0;
-    CK(cudaMalloc(&c->d_hnr, 12 * c->want_nr));
+    CK(cudaMalloc(&c->d_hnr, 16 * c->want_nr));
     c->hcap_nr = c->want_nr;
   }
   Scratch& S = c->S;
   S.hdd.keys = c->d_hdd;
-  S.hdd.vals = reinterpret_cast<uint32_t*>(c->d_hdd + c->hcap_dd);
   S.hdd.mask = (uint32_t)(c->hcap_dd - 1);
   S.hdd.used_slot = C_HASH_DD;
   S.hnr.keys = c->d_hnr;
-  S.hnr.vals = reinterpret_cast<uint32_t*>(c->d_hnr + c->hcap_nr);
   S.hnr.mask = (uint32_t)(c->hcap_nr - 1);
   S.hnr.used_slot = C_HASH_NR;
   S.tiles = c->d_tiles;
@@ -511,8 +509,8 @@ int mpsf_scan(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const mpsf_
   segs.p[k] = c->d_small; segs.words[k] = c->small_empty_bytes / 4; segs.val[k++] = EMPTY32;
   segs.p[k] = c->d_small + c->small_zero_off; segs.words[k] = c->small_zero_bytes / 4; segs.val[k++] = 0;
   segs.p[k] = c->d_tiles; segs.words[k] = 2 * nt; segs.val[k++] = 0;
-  segs.p[k] = c->d_hdd; segs.words[k] = 3 * c->hcap_dd; segs.val[k++] = EMPTY32;
-  segs.p[k] = c->d_hnr; segs.words[k] = 3 * c->hcap_nr; segs.val[k++] = EMPTY32;
+  segs.p[k] = c->d_hdd; segs.words[k] = 4 * c->hcap_dd; segs.val[k++] = EMPTY32;
+  segs.p[k] = c->d_hnr; segs.words[k] = 4 * c->hcap_nr; segs.val[k++] = EMPTY32;
   if (c->W.n_clients) { segs.p[k] = d_counts; segs.words[k] = 2ull * NSCEN * c->W.n_clients; segs.val[k++] = 0; }
   segs.n = k;
   int sms = 0;

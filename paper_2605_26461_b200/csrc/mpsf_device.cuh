@@ -88,8 +88,7 @@ struct World {
 constexpr uint32_t CH_VALID = 1u << 31;
 
 struct Hash {
-  unsigned long long* keys;
-  uint32_t* vals;
+  unsigned long long* keys;   // 16-byte slots: [2s] key, [2s+1] low 32 bits = min value
   uint32_t mask;
   uint32_t used_slot;  // ctrl index counting claimed slots
 };
@@ -244,17 +243,24 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   return x;
 }
 
-// Open addressing, linear probing; value = atomic min.  Returns false on overflow.
+// Open addressing, linear probing over 16-byte slots {u64 key, u32 value, pad}: one load
+// reads key and value together; value = atomic min.  Returns false on overflow.
+__device__ __forceinline__ uint32_t* hash_val(const Hash& h, uint32_t s) {
+  return reinterpret_cast<uint32_t*>(h.keys + 2ull * s + 1);
+}
+
 __device__ __forceinline__ bool hash_min(const Hash& h, uint32_t* ctrl, uint64_t key, uint32_t v) {
   uint32_t s = (uint32_t)mix64(key) & h.mask;
   for (int p = 0; p < HASH_MAX_PROBE; ++p) {
-    unsigned long long k = __ldcg(h.keys + s);
+    const ulonglong2 slot = __ldcg(reinterpret_cast<const ulonglong2*>(h.keys) + s);
+    unsigned long long k = slot.x;
+    uint32_t cur = (uint32_t)slot.y;
     if (k == EMPTY64) {
-      k = atomicCAS(h.keys + s, EMPTY64, (unsigned long long)key);
-      if (k == EMPTY64) { atomicAdd(ctrl + h.used_slot, 1u); k = key; }
+      k = atomicCAS(h.keys + 2ull * s, EMPTY64, (unsigned long long)key);
+      if (k == EMPTY64) { atomicAdd(ctrl + h.used_slot, 1u); k = key; cur = EMPTY32; }
     }
     if (k == key) {
-      if (__ldcg(h.vals + s) > v) atomicMin(h.vals + s, v);
+      if (cur > v) atomicMin(hash_val(h, s), v);
       return true;
     }
     s = (s + 1) & h.mask;
@@ -265,31 +271,33 @@ __device__ __forceinline__ bool hash_min(const Hash& h, uint32_t* ctrl, uint64_t
 __device__ __forceinline__ uint32_t hash_get(const Hash& h, uint64_t key) {
   uint32_t s = (uint32_t)mix64(key) & h.mask;
   for (int p = 0; p < HASH_MAX_PROBE; ++p) {
-    const unsigned long long k = __ldcg(h.keys + s);
-    if (k == key) return __ldcg(h.vals + s);
-    if (k == EMPTY64) return EMPTY32;
+    const ulonglong2 slot = __ldcg(reinterpret_cast<const ulonglong2*>(h.keys) + s);
+    if (slot.x == key) return (uint32_t)slot.y;
+    if (slot.x == EMPTY64) return EMPTY32;
     s = (s + 1) & h.mask;
   }
   return EMPTY32;
 }
 
+// global minimum with a load pre-check (used where nothing filters the calls first)
 __device__ __forceinline__ void min32(uint32_t* g, uint32_t v) {
   if (__ldcg(g) > v) atomicMin(g, v);
 }
 __device__ __forceinline__ void min64(unsigned long long* g, unsigned long long v) {
   if (__ldcg(g) > v) atomicMin(g, v);
 }
-// smem-cached variant: one global atomic per key per block in index order
+// smem-cached variant: the block-local copy filters, the survivors go out as fire-and-forget
+// reductions (RED.MIN, no return value, so no L2 round trip on the critical path)
 __device__ __forceinline__ void min32c(uint32_t* g, uint32_t* c, uint32_t v) {
   if (*c <= v) return;
   if (atomicMin(c, v) <= v) return;
-  min32(g, v);
+  atomicMin(g, v);
 }
 __device__ __forceinline__ void min64c(unsigned long long* g, unsigned long long* c,
                                        unsigned long long v) {
   if (*c <= v) return;
   if (atomicMin(c, v) <= v) return;
-  min64(g, v);
+  atomicMin(g, v);
 }
 
 // dedup key (SURVEY.md Appendix C rule C2)
