@@ -361,16 +361,21 @@ __device__ __forceinline__ void scan_entry(const World& W, const View& v, const 
       } else if (!hash_min(S.hnr, S.ctrl, nr_key(c, 0, r.va >> 12), ok)) {
         atomicOr(S.ctrl + C_OVF, 1u);
       }
-    } else if (r.at.kind != 0) {
-      if (kStaged) min32c(S.ext + r.at.ridx, v.ext + r.at.ridx, ok); else min32(S.ext + r.at.ridx, ok);
+    } else {
+      if (r.at.kind != 0) {
+        if (kStaged) min32c(S.ext + r.at.ridx, v.ext + r.at.ridx, ok); else min32(S.ext + r.at.ridx, ok);
+      }
+      // first eligible record per in-range page: the epoch-1 first-isolation key of a client
+      // released before the drain (trap / dead at start), so that case needs no extra pass
+      if (S.nrall) min32(S.nrall + r.at.slot, ok);
     }
   }
   if (r.kind == 0 && r.repl) {                                       // dedup insert (rule C2)
     const uint32_t val = ((uint32_t)gidx << 3) | r.group;
     bool to_hash = !(r.at.in_range || r.at.guard);
     if (!to_hash && W.dd_groups != 1) {
-      // one slot per (page, group): a fire-and-forget reduction, no round trip
-      atomicMin(S.dd + dd_slot(W, r), val);
+      // one slot per (page, group): min with a load pre-check (hot slots: most records skip)
+      min32(S.dd + dd_slot(W, r), val);
     } else if (!to_hash) {
       uint32_t* slot = S.dd + dd_slot(W, r);
       uint32_t cur = __ldcg(slot);
@@ -516,7 +521,11 @@ __global__ void k_resolve(World W, Scratch S, Params P, mpsf_client_verdict* __r
                    : ((!sa && gr_applied) ? (uint8_t)(ft_gr & 0xFF) : 0xFE);
     }
     verdict[c] = v;
-    if (iso && elig && (rel != REL_NONE || P.m2_us <= P.benign_us)) general = 1;
+    // release-aware pass needed: a client released inside the drain (C3 epochs), a client
+    // released before it when pass 1 kept no per-page keys, or exact M2 minima (m2 <= benign)
+    if (iso && elig &&
+        ((rel != REL_NONE && !(rel == REL_PRE && S.nrall)) || (rel == REL_NONE && P.m2_us <= P.benign_us)))
+      general = 1;
   }
   if (general) atomicOr(&s_general, 1);
   __syncthreads();
@@ -538,11 +547,15 @@ __device__ __forceinline__ uint32_t dedup_rep(const World& W, const Scratch& S, 
   return hash_get(S.hdd, dedup_key(r.c, r.eng, r.s, r.va >> 12));
 }
 
-__device__ __forceinline__ uint32_t nr_lookup(const Scratch& S, const Rec& r, bool epoch1) {
-  if (epoch1) {
+// First isolation-eligible record of r's (client, page, epoch).  A client released before the
+// drain (rel == REL_PRE) has only epoch-1 records, all seeing an empty address space, so its
+// key is the first eligible record of the page: pass 1's nrall / nr0 / epoch-0 hash entries.
+__device__ __forceinline__ uint32_t nr_lookup(const Scratch& S, const Rec& r, bool epoch1, bool pre) {
+  if (epoch1 && !(pre && S.nrall)) {
     if (r.at.in_range || r.at.guard) return __ldcg(S.nr1 + r.at.slot);
     return hash_get(S.hnr, nr_key(r.c, 1, r.va >> 12));
   }
+  if (r.at.in_range) return __ldcg(S.nrall + r.at.slot);
   if (r.at.guard) return __ldcg(S.nr0 + r.at.ridx);
   return hash_get(S.hnr, nr_key(r.c, 0, r.va >> 12));
 }
@@ -557,6 +570,7 @@ __device__ __forceinline__ void general_entry(const World& W, const View& v, con
   const long long rel = v.cst[r.c].rel;
   const uint32_t ok = ok32_of(r.repl, gidx);
   if (rel == REL_NONE && P.m2_us > P.benign_us) return;           // pass-1 minima already exact
+  if (rel == REL_PRE && S.nrall) return;                          // keys from pass 1; fates fixed
   if (r.repl && dedup_rep(W, S, r) != (uint32_t)gidx) return;       // dups excluded (C2)
   const bool epoch1 = rel < (long long)ok;
   const bool no_range = !r.at.in_range || epoch1;
@@ -576,7 +590,7 @@ __device__ __forceinline__ void general_entry(const World& W, const View& v, con
       else min32(giso + 1, ok);
     }
   } else {
-    if (no_range && nr_lookup(S, r, epoch1) != ok) min32(giso + 1, ok);
+    if (no_range && nr_lookup(S, r, epoch1, false) != ok) min32(giso + 1, ok);
   }
 }
 
@@ -687,7 +701,7 @@ __device__ __forceinline__ void finalize_entry(const World& W, const View& v, co
            (cs.flags & CS_KILL_ALL) || rep_ok > cs.kill_tie;
   } else if (!dup) {                      // isolation mechanism (C3)
     const bool epoch1 = cs.rel < (long long)ok;
-    if (!r.at.in_range || epoch1) mech = nr_lookup(S, r, epoch1) == ok ? 1 : 2;
+    if (!r.at.in_range || epoch1) mech = nr_lookup(S, r, epoch1, cs.rel == REL_PRE) == ok ? 1 : 2;
     else if (r.at.kind == 0) mech = 2;
     else mech = __ldcg(S.ext + r.at.ridx) == ok ? 3 : 2;
   }

@@ -26,9 +26,9 @@ struct DevSummary {
 };
 
 struct InitSegs {
-  void* p[8];
-  uint64_t words[8];
-  uint32_t val[8];
+  void* p[10];
+  uint64_t words[10];
+  uint32_t val[10];
   int n;
 };
 
@@ -80,6 +80,7 @@ struct mpsf_ctx {
   // scratch
   uint32_t* d_dd = nullptr;
   uint32_t* d_nr1 = nullptr;
+  uint32_t* d_nrall = nullptr;
   uint64_t dd_cap = 0;
   uint32_t* d_count_part = nullptr;
   uint64_t part_cap = 0;
@@ -216,6 +217,7 @@ void mpsf_destroy(mpsf_ctx* c) {
   cudaFree(c->d_world);
   cudaFree(c->d_dd);
   cudaFree(c->d_nr1);
+  cudaFree(c->d_nrall);
   cudaFree(c->d_count_part);
   cudaFree(c->d_counter);
   cudaFree(c->d_small);
@@ -366,10 +368,12 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   if (!c->d_dd || dd_words > c->dd_cap || np > c->pages_cap) {
     cudaFree(c->d_dd);
     cudaFree(c->d_nr1);
-    c->d_dd = c->d_nr1 = nullptr;
+    cudaFree(c->d_nrall);
+    c->d_dd = c->d_nr1 = c->d_nrall = nullptr;
     c->pages_cap = c->dd_cap = 0;
     CK(cudaMalloc(&c->d_dd, sizeof(uint32_t) * std::max<uint64_t>(dd_words, 1)));
     CK(cudaMalloc(&c->d_nr1, sizeof(uint32_t) * std::max<uint64_t>(np, 1)));
+    CK(cudaMalloc(&c->d_nrall, sizeof(uint32_t) * std::max<uint64_t>(np, 1)));
     c->pages_cap = np;
     c->dd_cap = dd_words;
   }
@@ -411,6 +415,9 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   Scratch& S = c->S;
   S.dd = c->d_dd;
   S.nr1 = c->d_nr1;
+  // per-page first-eligible keys only for dense (small) worlds; large worlds take the
+  // release-aware pass instead when a client is released before the drain
+  S.nrall = W.dd_groups == 5 ? c->d_nrall : nullptr;
   unsigned long long* u64 = reinterpret_cast<unsigned long long*>(s + s_u64);
   S.ft_ce = u64;
   S.ft_sa = u64 + C;
@@ -506,6 +513,9 @@ int mpsf_scan(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const mpsf_
   int k = 0;
   segs.p[k] = c->d_dd; segs.words[k] = c->W.n_pages * c->W.dd_groups; segs.val[k++] = EMPTY32;
   if (p->flags & MPSF_PF_ISOLATION) { segs.p[k] = c->d_nr1; segs.words[k] = c->W.n_pages; segs.val[k++] = EMPTY32; }
+  if ((p->flags & MPSF_PF_ISOLATION) && c->S.nrall) {
+    segs.p[k] = c->S.nrall; segs.words[k] = c->W.n_pages; segs.val[k++] = EMPTY32;
+  }
   segs.p[k] = c->d_small; segs.words[k] = c->small_empty_bytes / 4; segs.val[k++] = EMPTY32;
   segs.p[k] = c->d_small + c->small_zero_off; segs.words[k] = c->small_zero_bytes / 4; segs.val[k++] = 0;
   segs.p[k] = c->d_tiles; segs.words[k] = 2 * nt; segs.val[k++] = 0;
@@ -610,6 +620,7 @@ int mpsf_exchange_buffers(mpsf_ctx* c, int stage, mpsf_xbuf* out, int cap) {
     b[k++] = {s + c->x_u32, c->x_u32_n, 4, MPSF_XOP_MIN};
     if (c->W.dd_groups != 5) return MPSF_E_ARG;   // claimed slots are not combinable: set dense dedup
     b[k++] = {c->d_dd, c->W.n_pages * 5, 4, MPSF_XOP_MIN};
+    if (c->S.nrall) b[k++] = {c->S.nrall, c->W.n_pages, 4, MPSF_XOP_MIN};
   } else if (stage == 2) {
     b[k++] = {s + c->x_giso, c->x_giso_n, 4, MPSF_XOP_MIN};
     b[k++] = {c->d_nr1, c->W.n_pages, 4, MPSF_XOP_MIN};

@@ -97,6 +97,7 @@ struct Scratch {
   uint32_t* dd;        // [n_pages] dense dedup slots: (gidx << 3 | group), EMPTY32
   uint32_t* nr0;       // [n_ranges] guard-page first-isolation key, epoch 0
   uint32_t* nr1;       // [n_pages] first-isolation key per page, epoch 1 (general path)
+  uint32_t* nrall;     // [n_pages] first eligible record per in-range page (dense worlds), or null
   Hash hdd;            // dedup keys of pages outside every range's slot span
   Hash hnr;            // NR keys (client, page, epoch) of such pages
   uint32_t* ext;       // [n_ranges] first isolation-eligible record per external range
