@@ -81,7 +81,7 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 __host__ __device__ inline uint32_t al16(uint64_t x) { return (uint32_t)((x + 15) & ~uint64_t(15)); }
 
 struct Layout {
-  uint32_t tiles, bars, tids, tot, pre;
+  uint32_t tiles, bars, wbars, tids, tot, pre;
   uint32_t pg_base, pg_end, poff, rattr, rrid, skip, crange, cspan, cshift, chan;
   uint32_t c64, iso, r32, counts, cstate, total;
   uint32_t rep_chan;
@@ -92,8 +92,9 @@ struct Layout {
 __host__ __device__ inline Layout make_layout(uint32_t nr, uint32_t nc, uint32_t nch, bool staged, bool fin) {
   Layout L;
   uint32_t o = 0;
-  L.tiles = o; o += NBUF * TILE_BYTES;
+  L.tiles = o; o += 32 * 3 * 1024;        // >= NBUF tiles (finalize) and 32 warps x 3 x 1 KiB chunks
   L.bars = o; o += 4 * 8 * NBUF;          // full, empty, done, pref per buffer
+  L.wbars = o; o += 8 * 32 * 3;           // warp-private stream barriers
   L.tids = o; o += al16(4 * NBUF);
   L.tot = o; o += 8 * 32 * NBUF;          // per buffer, per worker warp: (cancel, dedup) counts
   L.pre = o; o += 8 * 32 * NBUF;          // per buffer, per worker warp: exclusive output offsets
@@ -309,6 +310,63 @@ __device__ __forceinline__ Pipe pipe_init(uint8_t* sm, const Layout& L) {
   return p;
 }
 
+// Warp-private stream for the order-free passes (scan, general): every warp pulls its own
+// 1 KiB chunks (64 entries) with TMA into a 3-deep private ring and refills a slot as soon
+// as its own lanes are done -- no coupling to the slowest warp of the CTA.
+constexpr int WCHUNK = 64;
+constexpr uint32_t WCHUNK_BYTES = WCHUNK * 16;
+constexpr int WDEPTH = 3;
+
+__device__ __forceinline__ void wstream_init(uint8_t* sm, const Layout& L) {
+  if (threadIdx.x == 0) {
+    uint64_t* wb = reinterpret_cast<uint64_t*>(sm + L.wbars);
+    for (int i = 0; i < WARPS * WDEPTH; ++i) mbar_init(wb + i, 1);
+    fence_mbar_init();
+  }
+}
+
+template <typename F>
+__device__ __forceinline__ void warp_stream(uint8_t* sm, const Layout& L, const mpsf_fault_entry* in, uint64_t n,
+                                            F&& fn) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint8_t* wbuf = sm + L.tiles + (size_t)warp * WDEPTH * WCHUNK_BYTES;
+  uint64_t* wbar = reinterpret_cast<uint64_t*>(sm + L.wbars) + warp * WDEPTH;
+  const uint64_t gw = (uint64_t)blockIdx.x * WARPS + warp, GW = (uint64_t)gridDim.x * WARPS;
+  const uint64_t nch = (n + WCHUNK - 1) / WCHUNK;
+  const uint64_t pol = policy_evict_first();
+  auto issue = [&](int b, uint64_t c) {
+    const uint64_t start = c * WCHUNK;
+    const uint64_t cnt = n - start < (uint64_t)WCHUNK ? n - start : (uint64_t)WCHUNK;
+    mbar_expect_tx(wbar + b, (uint32_t)(cnt * 16));
+    bulk_load(wbuf + (size_t)b * WCHUNK_BYTES, in + start, (uint32_t)(cnt * 16), wbar + b, pol);
+  };
+  if (lane == 0) {
+    for (int b = 0; b < WDEPTH; ++b) {
+      const uint64_t c = gw + (uint64_t)b * GW;
+      if (c < nch) issue(b, c);
+    }
+  }
+  __syncwarp();
+  for (uint32_t k = 0;; ++k) {
+    const uint64_t c = gw + (uint64_t)k * GW;
+    if (c >= nch) break;
+    const int b = k % WDEPTH;
+    mbar_wait(wbar + b, (k / WDEPTH) & 1);
+    const uint4* chunk = reinterpret_cast<const uint4*>(wbuf + (size_t)b * WCHUNK_BYTES);
+#pragma unroll
+    for (int e = 0; e < WCHUNK / 32; ++e) {
+      const int li = e * 32 + lane;
+      const uint64_t i = c * WCHUNK + li;
+      if (i < n) fn(chunk[li], i);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      const uint64_t c2 = c + (uint64_t)WDEPTH * GW;
+      if (c2 < nch) issue(b, c2);
+    }
+  }
+}
+
 // Control-warp loop for the statically scheduled passes (tile t = blockIdx + j*grid).
 __device__ __forceinline__ void control_static(const Pipe& p, const mpsf_fault_entry* in, uint64_t n) {
   if ((threadIdx.x & 31) != 0) return;
@@ -403,30 +461,11 @@ __global__ void __launch_bounds__(BLOCK, 1) k_scan(World W, Scratch S, const mps
   extern __shared__ __align__(128) uint8_t smem[];
   const Layout L = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, false);
   const View v = setup<kStaged>(smem, L, W, S, true, false);
-  Pipe p = pipe_init(smem, L);
+  wstream_init(smem, L);
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (warp == 0) {
-    control_static(p, in, n);
-  } else {
-    const int seg = (warp - 1) * WSEG;
-    for (uint32_t j = 0;; ++j) {
-      const int b = j % NBUF;
-      mbar_wait(p.full + b, (j / NBUF) & 1);
-      const uint32_t t = p.tids[b];
-      if (t == TID_NONE) break;
-      const uint4* tile = reinterpret_cast<const uint4*>(p.buf + (size_t)b * TILE_BYTES);
-      const uint64_t start = (uint64_t)t * TILE;
-#pragma unroll 1
-      for (int k = 0; k < EPT; ++k) {
-        const int li = seg + k * 32 + lane;
-        const uint64_t i = start + li;
-        if (i < n) scan_entry<kStaged>(W, v, S, P, tile[li], P.base_index + i, counts);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(p.empty + b);
-    }
-  }
+  warp_stream(smem, L, in, n, [&](uint4 e, uint64_t i) {
+    scan_entry<kStaged>(W, v, S, P, e, P.base_index + i, counts);
+  });
   if (kStaged) {
     __syncthreads();
     uint32_t* part = count_part + (uint64_t)blockIdx.x * NSCEN * W.n_clients;
@@ -601,30 +640,11 @@ __global__ void __launch_bounds__(BLOCK, 1) k_general(World W, Scratch S, const 
   extern __shared__ __align__(128) uint8_t smem[];
   const Layout L = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, true);
   const View v = setup<kStaged>(smem, L, W, S, false, true);
-  Pipe p = pipe_init(smem, L);
+  wstream_init(smem, L);
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (warp == 0) {
-    control_static(p, in, n);
-    return;
-  }
-  const int seg = (warp - 1) * WSEG;
-  for (uint32_t j = 0;; ++j) {
-    const int b = j % NBUF;
-    mbar_wait(p.full + b, (j / NBUF) & 1);
-    const uint32_t t = p.tids[b];
-    if (t == TID_NONE) break;
-    const uint4* tile = reinterpret_cast<const uint4*>(p.buf + (size_t)b * TILE_BYTES);
-    const uint64_t start = (uint64_t)t * TILE;
-#pragma unroll 1
-    for (int k = 0; k < EPT; ++k) {
-      const int li = seg + k * 32 + lane;
-      const uint64_t i = start + li;
-      if (i < n) general_entry<kStaged, kStage>(W, v, S, P, tile[li], P.base_index + i);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(p.empty + b);
-  }
+  warp_stream(smem, L, in, n, [&](uint4 e, uint64_t i) {
+    general_entry<kStaged, kStage>(W, v, S, P, e, P.base_index + i);
+  });
 }
 
 __global__ void k_resolve2(World W, Scratch S, Params P) {
