@@ -235,8 +235,9 @@ __device__ __forceinline__ Rec decode(const World& W, const View& v, const Scrat
     r.s = classify(r.eng, acc, has, r.at.kind, r.at.lifecycle, r.at.migratable, r.at.st);
     r.repl = s_replayable(r.s);
     if (r.eng == 0 && acc != 2) {
-      r.group = (acc == 1 && classify(0, 0, has, r.at.kind, r.at.lifecycle, r.at.migratable, r.at.st) != r.s)
-                    ? 1u : 0u;
+      // an SM write classifies differently from an SM read of the same page exactly when it
+      // takes the access-mismatch branch (faults.py:154-160): ids 1..3 only come from there
+      r.group = (acc == 1 && r.s >= 1 && r.s <= 3) ? 1u : 0u;
     } else {
       r.group = r.eng == 0 ? 2u : (uint32_t)(2 + r.eng);
     }
@@ -367,49 +368,6 @@ __device__ __forceinline__ void warp_stream(uint8_t* sm, const Layout& L, const 
   }
 }
 
-// Same stream, handing each lane its two entries of a chunk together (lane and lane + 32).
-template <typename F>
-__device__ __forceinline__ void warp_stream_pairs(uint8_t* sm, const Layout& L, const mpsf_fault_entry* in,
-                                                  uint64_t n, F&& fn) {
-  static_assert(WCHUNK == 64, "pairs assume 2 entries per lane");
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint8_t* wbuf = sm + L.tiles + (size_t)warp * WDEPTH * WCHUNK_BYTES;
-  uint64_t* wbar = reinterpret_cast<uint64_t*>(sm + L.wbars) + warp * WDEPTH;
-  const uint64_t gw = (uint64_t)blockIdx.x * WARPS + warp, GW = (uint64_t)gridDim.x * WARPS;
-  const uint64_t nch = (n + WCHUNK - 1) / WCHUNK;
-  const uint64_t pol = policy_evict_first();
-  auto issue = [&](int b, uint64_t c) {
-    const uint64_t start = c * WCHUNK;
-    const uint64_t cnt = n - start < (uint64_t)WCHUNK ? n - start : (uint64_t)WCHUNK;
-    mbar_expect_tx(wbar + b, (uint32_t)(cnt * 16));
-    bulk_load(wbuf + (size_t)b * WCHUNK_BYTES, in + start, (uint32_t)(cnt * 16), wbar + b, pol);
-  };
-  if (lane == 0) {
-    for (int b = 0; b < WDEPTH; ++b) {
-      const uint64_t c = gw + (uint64_t)b * GW;
-      if (c < nch) issue(b, c);
-    }
-  }
-  __syncwarp();
-  for (uint32_t k = 0;; ++k) {
-    const uint64_t c = gw + (uint64_t)k * GW;
-    if (c >= nch) break;
-    const int b = k % WDEPTH;
-    mbar_wait(wbar + b, (k / WDEPTH) & 1);
-    const uint4* chunk = reinterpret_cast<const uint4*>(wbuf + (size_t)b * WCHUNK_BYTES);
-    const uint64_t i0 = c * WCHUNK + lane, i1 = i0 + 32;
-    const bool ok0 = i0 < n, ok1 = i1 < n;
-    const uint4 e0 = ok0 ? chunk[lane] : make_uint4(0, 0, 0, 0);
-    const uint4 e1 = ok1 ? chunk[lane + 32] : make_uint4(0, 0, 0, 0);
-    __syncwarp();
-    if (lane == 0) {
-      const uint64_t c2 = c + (uint64_t)WDEPTH * GW;
-      if (c2 < nch) issue(b, c2);                 // both entries are in registers already
-    }
-    fn(e0, i0, ok0, e1, i1, ok1);
-  }
-}
-
 // Control-warp loop for the statically scheduled passes (tile t = blockIdx + j*grid).
 __device__ __forceinline__ void control_static(const Pipe& p, const mpsf_fault_entry* in, uint64_t n) {
   if ((threadIdx.x & 31) != 0) return;
@@ -428,21 +386,9 @@ __device__ __forceinline__ void control_static(const Pipe& p, const mpsf_fault_e
 }
 
 // ---- pass 1 ---------------------------------------------------------------------------------
-// Global (L2) work an entry leaves for after decode: up to two pre-checked minima (dense dedup
-// slot, per-page first-eligible key) and the rare hash / claimed-slot inserts.
-struct ScanOps {
-  uint32_t* a = nullptr;
-  uint32_t av = 0;
-  uint32_t* b = nullptr;
-  uint32_t bv = 0;
-  uint32_t rare_nr = 0, rare_dd = 0;   // rare_dd: 1 claimed slot, 2 hash
-  unsigned long long nr_key = 0, dd_key = 0;
-  uint32_t nr_val = 0, dd_slot = 0, dd_val = 0;
-};
-
 template <bool kStaged>
 __device__ __forceinline__ void scan_entry(const World& W, const View& v, const Scratch& S, const Params& P,
-                                           uint4 e, uint64_t gidx, unsigned long long* counts, ScanOps& ops) {
+                                           uint4 e, uint64_t gidx, unsigned long long* counts) {
   const Rec r = decode<kStaged>(W, v, S, e, gidx);
   if (!r.valid) return;
   const uint32_t c = r.c;
@@ -471,10 +417,8 @@ __device__ __forceinline__ void scan_entry(const World& W, const View& v, const 
     if (!r.at.in_range) {
       if (r.at.guard) {
         if (kStaged) min32c(S.nr0 + r.at.ridx, v.nr0 + r.at.ridx, ok); else min32(S.nr0 + r.at.ridx, ok);
-      } else {
-        ops.rare_nr = 1;
-        ops.nr_key = nr_key(c, 0, r.va >> 12);
-        ops.nr_val = ok;
+      } else if (!hash_min(S.hnr, S.ctrl, nr_key(c, 0, r.va >> 12), ok)) {
+        atomicOr(S.ctrl + C_OVF, 1u);
       }
     } else {
       if (r.at.kind != 0) {
@@ -482,65 +426,33 @@ __device__ __forceinline__ void scan_entry(const World& W, const View& v, const 
       }
       // first eligible record per in-range page: the epoch-1 first-isolation key of a client
       // released before the drain (trap / dead at start), so that case needs no extra pass
-      if (S.nrall) { ops.b = S.nrall + r.at.slot; ops.bv = ok; }
+      if (S.nrall) min32(S.nrall + r.at.slot, ok);
     }
   }
   if (r.kind == 0 && r.repl) {                                       // dedup insert (rule C2)
     const uint32_t val = ((uint32_t)gidx << 3) | r.group;
-    const bool in_world = r.at.in_range || r.at.guard;
-    if (in_world && W.dd_groups != 1) {
-      ops.a = S.dd + dd_slot(W, r);                                  // one slot per (page, group)
-      ops.av = val;
-    } else {
-      ops.rare_dd = in_world ? 1 : 2;                                // claimed slot / hash
-      ops.dd_slot = in_world ? dd_slot(W, r) : 0u;
-      ops.dd_val = val;
-      ops.dd_key = dedup_key(c, r.eng, r.s, r.va >> 12);
-    }
-  }
-}
-
-// The rare, round-trip-heavy inserts: wild-page hash entries and claimed dedup slots.
-__device__ __forceinline__ void scan_rare(const Scratch& S, const ScanOps& o) {
-  if (o.rare_nr && !hash_min(S.hnr, S.ctrl, o.nr_key, o.nr_val)) atomicOr(S.ctrl + C_OVF, 1u);
-  if (!o.rare_dd) return;
-  bool to_hash = o.rare_dd == 2;
-  if (!to_hash) {
-    uint32_t* slot = S.dd + o.dd_slot;
-    const uint32_t group = o.dd_val & 7u;
-    uint32_t cur = __ldcg(slot);
-    while (true) {
-      if (cur == EMPTY32) {
-        const uint32_t prev = atomicCAS(slot, EMPTY32, o.dd_val);
-        if (prev == EMPTY32) break;
-        cur = prev;
-        continue;
+    bool to_hash = !(r.at.in_range || r.at.guard);
+    if (!to_hash && W.dd_groups != 1) {
+      // one slot per (page, group): min with a load pre-check (hot slots: most records skip)
+      min32(S.dd + dd_slot(W, r), val);
+    } else if (!to_hash) {
+      uint32_t* slot = S.dd + dd_slot(W, r);
+      uint32_t cur = __ldcg(slot);
+      while (true) {
+        if (cur == EMPTY32) {
+          const uint32_t prev = atomicCAS(slot, EMPTY32, val);
+          if (prev == EMPTY32) break;
+          cur = prev;
+          continue;
+        }
+        if ((cur & 7u) == r.group) { if (cur > val) atomicMin(slot, val); break; }
+        to_hash = true;
+        break;
       }
-      if ((cur & 7u) == group) { if (cur > o.dd_val) atomicMin(slot, o.dd_val); break; }
-      to_hash = true;
-      break;
     }
+    if (to_hash && !hash_min(S.hdd, S.ctrl, dedup_key(c, r.eng, r.s, r.va >> 12), (uint32_t)gidx))
+      atomicOr(S.ctrl + C_OVF, 1u);
   }
-  if (to_hash && !hash_min(S.hdd, S.ctrl, o.dd_key, o.dd_val >> 3)) atomicOr(S.ctrl + C_OVF, 1u);
-}
-
-// Two entries per lane at once: both decode first, then every L2 pre-check load of both is in
-// flight together before any dependent atomic (the pass is L2-latency bound, not issue bound).
-template <bool kStaged>
-__device__ __forceinline__ void scan_pair(const World& W, const View& v, const Scratch& S, const Params& P,
-                                          uint4 e0, uint64_t g0, bool ok0, uint4 e1, uint64_t g1, bool ok1,
-                                          unsigned long long* counts) {
-  ScanOps o0, o1;
-  if (ok0) scan_entry<kStaged>(W, v, S, P, e0, g0, counts, o0);
-  if (ok1) scan_entry<kStaged>(W, v, S, P, e1, g1, counts, o1);
-  const uint32_t x0a = o0.a ? __ldcg(o0.a) : 0u, x0b = o0.b ? __ldcg(o0.b) : 0u;
-  const uint32_t x1a = o1.a ? __ldcg(o1.a) : 0u, x1b = o1.b ? __ldcg(o1.b) : 0u;
-  scan_rare(S, o0);
-  scan_rare(S, o1);
-  if (o0.a && x0a > o0.av) atomicMin(o0.a, o0.av);
-  if (o0.b && x0b > o0.bv) atomicMin(o0.b, o0.bv);
-  if (o1.a && x1a > o1.av) atomicMin(o1.a, o1.av);
-  if (o1.b && x1b > o1.bv) atomicMin(o1.b, o1.bv);
 }
 
 template <bool kStaged>
@@ -552,13 +464,14 @@ __global__ void __launch_bounds__(BLOCK, 1) k_scan(World W, Scratch S, const mps
   const View v = setup<kStaged>(smem, L, W, S, true, false);
   wstream_init(smem, L);
   __syncthreads();
-  warp_stream_pairs(smem, L, in, n, [&](uint4 e0, uint64_t i0, bool ok0, uint4 e1, uint64_t i1, bool ok1) {
-    scan_pair<kStaged>(W, v, S, P, e0, P.base_index + i0, ok0, e1, P.base_index + i1, ok1, counts);
+  warp_stream(smem, L, in, n, [&](uint4 e, uint64_t i) {
+    scan_entry<kStaged>(W, v, S, P, e, P.base_index + i, counts);
   });
   if (kStaged) {
     __syncthreads();
     uint32_t* part = count_part + (uint64_t)blockIdx.x * NSCEN * W.n_clients;
-    for (uint32_t i = threadIdx.x; i < NSCEN * W.n_clients; i += blockDim.x) part[i] = v.counts[i];
+    // accumulate: a batch may be scanned in several launches (chunked host pipeline)
+    for (uint32_t i = threadIdx.x; i < NSCEN * W.n_clients; i += blockDim.x) part[i] += v.counts[i];
   }
 }
 
@@ -821,23 +734,23 @@ template <bool kStaged>
 __global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const mpsf_fault_entry* __restrict__ in,
                                                        uint64_t n, Params P, mpsf_out_record* __restrict__ out,
                                                        unsigned long long* __restrict__ dkeys,
-                                                       uint32_t* __restrict__ didx, uint32_t* __restrict__ cancel) {
+                                                       uint32_t* __restrict__ didx, uint32_t* __restrict__ cancel,
+                                                       uint32_t tile_lo, uint32_t tile_hi, uint32_t* __restrict__ tctr) {
   extern __shared__ __align__(128) uint8_t smem[];
   if (__ldcg(S.ctrl + C_ERR) != 0) return;
   const Layout L = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, true);
   const View v = setup<kStaged>(smem, L, W, S, false, true);
   Pipe p = pipe_init(smem, L);
   const Globals G = *S.glob;
-  const uint32_t ntiles = (uint32_t)((n + TILE - 1) / TILE);
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (warp == 0) {
-    // control warp: dynamic in-order tile ids, TMA refill, and the look-back of tile j
-    // while the workers already process tile j+1
+    // control warp: dynamic in-order tile ids of [tile_lo, tile_hi), TMA refill, and the
+    // look-back of tile j while the workers already process tile j+1
     auto refill = [&](int b) {
       if (lane == 0) {
-        const uint32_t t = atomicAdd(S.ctrl + C_TILE_FIN, 1u);
-        if (t < ntiles) {
+        const uint32_t t = tile_lo + atomicAdd(tctr, 1u);
+        if (t < tile_hi) {
           p.tids[b] = t;
           fence_proxy_async();
           pipe_issue(p, b, in, n, t);
@@ -1049,7 +962,8 @@ static int scan_t(const World& W, const Scratch& S, const mpsf_fault_entry* in, 
   if ((uint64_t)g > ntiles) g = (int)ntiles;
   k_scan<kStaged><<<g, BLOCK, smem, st>>>(W, S, in, n, P, counts, count_part);
   mk.mark("k_scan");
-  *parts = kStaged ? (uint32_t)g : 0u;
+  // partial rows accumulate across launches and were zeroed by k_init: reduce all of them
+  *parts = kStaged ? count_parts_needed(W) : 0u;
   return ok_or_err();
 }
 
@@ -1075,17 +989,18 @@ static int general_t(const World& W, const Scratch& S, const mpsf_fault_entry* i
 template <bool kStaged>
 static int finalize_t(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
                       mpsf_out_record* out, unsigned long long* dkeys, uint32_t* didx, uint32_t* cancel,
-                      cudaStream_t st, const Marker& mk) {
+                      uint32_t tile_lo, uint32_t tile_hi, uint32_t* tctr, cudaStream_t st, const Marker& mk) {
   set_attrs<kStaged>();
-  if (n == 0) return 0;
+  if (n == 0 || tile_hi <= tile_lo) return 0;
   const uint32_t smem = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, true).total;
-  const uint64_t ntiles = (n + TILE - 1) / TILE;
   int g = grid_for(k_finalize<kStaged>, smem);
-  if ((uint64_t)g > ntiles) g = (int)ntiles;
-  k_finalize<kStaged><<<g, BLOCK, smem, st>>>(W, S, in, n, P, out, dkeys, didx, cancel);
+  if ((uint32_t)g > tile_hi - tile_lo) g = (int)(tile_hi - tile_lo);
+  k_finalize<kStaged><<<g, BLOCK, smem, st>>>(W, S, in, n, P, out, dkeys, didx, cancel, tile_lo, tile_hi, tctr);
   mk.mark("k_finalize");
   return ok_or_err();
 }
+
+uint32_t tile_entries() { return (uint32_t)TILE; }
 
 int launch_scan(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
                 unsigned long long* counts, uint32_t* count_part, cudaStream_t st, const Marker& mk, uint32_t* parts) {
@@ -1117,9 +1032,9 @@ int launch_resolve2(const World& W, const Scratch& S, const Params& P, cudaStrea
 
 int launch_finalize(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
                     mpsf_out_record* out, unsigned long long* dkeys, uint32_t* didx, uint32_t* cancel,
-                    cudaStream_t st, const Marker& mk) {
-  return staged_fits(W) ? finalize_t<true>(W, S, in, n, P, out, dkeys, didx, cancel, st, mk)
-                        : finalize_t<false>(W, S, in, n, P, out, dkeys, didx, cancel, st, mk);
+                    uint32_t tile_lo, uint32_t tile_hi, uint32_t* tctr, cudaStream_t st, const Marker& mk) {
+  return staged_fits(W) ? finalize_t<true>(W, S, in, n, P, out, dkeys, didx, cancel, tile_lo, tile_hi, tctr, st, mk)
+                        : finalize_t<false>(W, S, in, n, P, out, dkeys, didx, cancel, tile_lo, tile_hi, tctr, st, mk);
 }
 
 int launch_hash_export(const Hash& h, uint64_t cap, unsigned long long* keys, uint32_t* vals, uint32_t* counter,

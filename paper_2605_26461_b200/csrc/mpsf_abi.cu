@@ -68,6 +68,11 @@ uint64_t next_pow2(uint64_t x) {
 
 size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// mpsf_process_host splits a batch into at most this many tile-aligned chunks so the
+// host->device copy of chunk k+1 overlaps pass 1 on chunk k, and the device->host copy
+// of chunk k's records overlaps finalize on chunk k+1
+constexpr int kMaxChunks = 8;
+
 }  // namespace
 
 struct mpsf_ctx {
@@ -159,9 +164,12 @@ struct mpsf_ctx {
     return m;
   }
   uint32_t* d_remap_err = nullptr;
-  // host-path buffers
+  uint32_t* d_tctr = nullptr;   // kMaxChunks finalize tile counters (zeroed by k_init)
+  // host-path buffers and the copy streams of the chunked pipeline
   uint8_t* d_io = nullptr;
   size_t io_cap = 0;
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  cudaEvent_t ev_in[kMaxChunks] = {}, ev_fin[kMaxChunks] = {}, ev_fork = nullptr, ev_d2h = nullptr;
 };
 
 #define CK(x)                                \
@@ -201,9 +209,20 @@ int mpsf_create(mpsf_ctx** out, int device) {
       cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming) != cudaSuccess ||
       cudaHostAlloc(reinterpret_cast<void**>(&c->h_sum), sizeof(DevSummary), cudaHostAllocMapped) != cudaSuccess ||
       cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->d_sum), c->h_sum, 0) != cudaSuccess ||
-      cudaMalloc(&c->d_remap_err, sizeof(uint32_t)) != cudaSuccess) {
+      cudaMalloc(&c->d_remap_err, sizeof(uint32_t)) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->h2d_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_d2h, cudaEventDisableTiming) != cudaSuccess) {
     mpsf_destroy(c);
     return MPSF_E_CUDA;
+  }
+  for (int k = 0; k < kMaxChunks; ++k) {
+    if (cudaEventCreateWithFlags(&c->ev_in[k], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_fin[k], cudaEventDisableTiming) != cudaSuccess) {
+      mpsf_destroy(c);
+      return MPSF_E_CUDA;
+    }
   }
   memset(c->h_sum, 0, sizeof(DevSummary));
   *out = c;
@@ -230,6 +249,14 @@ void mpsf_destroy(mpsf_ctx* c) {
   for (cudaEvent_t e : c->pend_events) cudaEventDestroy(e);
   if (c->h_sum) cudaFreeHost(c->h_sum);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
+  for (int k = 0; k < kMaxChunks; ++k) {
+    if (c->ev_in[k]) cudaEventDestroy(c->ev_in[k]);
+    if (c->ev_fin[k]) cudaEventDestroy(c->ev_fin[k]);
+  }
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_d2h) cudaEventDestroy(c->ev_d2h);
+  if (c->h2d_stream) cudaStreamDestroy(c->h2d_stream);
+  if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
 }
@@ -399,6 +426,7 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   c->x_giso = s_giso; c->x_giso_n = 3ull * C;
   const size_t empty_bytes = o;
   const size_t s_ctrl = take(4 * C_NCTRL);
+  const size_t s_tctr = take(4 * kMaxChunks);   // finalize tile counters, one per chunk
   const size_t zero_bytes = o - empty_bytes;
   const size_t s_cst = take(sizeof(CState) * std::max<uint32_t>(C, 1));
   if (o > c->small_cap) {
@@ -434,6 +462,7 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   S.glob = reinterpret_cast<Globals*>(s + s_glob);
   S.err_idx = reinterpret_cast<unsigned long long*>(s + s_err);
   S.ctrl = reinterpret_cast<uint32_t*>(s + s_ctrl);
+  c->d_tctr = reinterpret_cast<uint32_t*>(s + s_tctr);
   S.cstate = reinterpret_cast<CState*>(s + s_cst);
   c->has_world = true;
   return MPSF_OK;
@@ -497,6 +526,10 @@ int mpsf_set_dense_dedup(mpsf_ctx* c, int on) {
 }
 
 // phase 1: clear scratch + k_scan
+static int batch_init(mpsf_ctx* c, uint64_t n, const mpsf_params* p, uint64_t* d_counts, cudaStream_t st);
+static int scan_chunk(mpsf_ctx* c, const mpsf_fault_entry* d_chunk, uint64_t n_chunk, uint64_t chunk_off,
+                      const mpsf_params* p, uint64_t* d_counts, cudaStream_t st);
+
 int mpsf_scan(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const mpsf_params* p, uint64_t* d_counts,
               void* stream) {
   if (!c || !p) return MPSF_E_ARG;
@@ -506,6 +539,14 @@ int mpsf_scan(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const mpsf_
   if (p->base_index + n > MAX_GIDX) return MPSF_E_TOO_LARGE;
   CK(cudaSetDevice(c->device));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int rc = batch_init(c, n, p, d_counts, st);
+  if (!rc) rc = scan_chunk(c, d_in, n, 0, p, d_counts, st);
+  c->last_launches = n ? 2 : 1;
+  return rc;
+}
+
+// clear the per-batch scratch (k_init) and size it for n entries
+static int batch_init(mpsf_ctx* c, uint64_t n, const mpsf_params* p, uint64_t* d_counts, cudaStream_t st) {
   int rc = ensure_call_scratch(c, n);
   if (rc) return rc;
   const uint64_t nt = tiles_for(n);
@@ -522,19 +563,26 @@ int mpsf_scan(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const mpsf_
   segs.p[k] = c->d_hdd; segs.words[k] = 4 * c->hcap_dd; segs.val[k++] = EMPTY32;
   segs.p[k] = c->d_hnr; segs.words[k] = 4 * c->hcap_nr; segs.val[k++] = EMPTY32;
   if (c->W.n_clients) { segs.p[k] = d_counts; segs.words[k] = 2ull * NSCEN * c->W.n_clients; segs.val[k++] = 0; }
+  if (c->part_cap) { segs.p[k] = c->d_count_part; segs.words[k] = c->part_cap; segs.val[k++] = 0; }
   segs.n = k;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   c->mark_begin(st);
-  const Marker mk = c->marker();
   k_init<<<dim3(2 * sms, k), 256, 0, st>>>(segs);
-  mk.mark("k_init");
-  const Params P = to_params(p);
-  if (launch_scan(c->W, c->S, d_in, n, P, reinterpret_cast<unsigned long long*>(d_counts), c->d_count_part, st, mk,
-                  &c->parts))
-    return MPSF_E_CUDA;
+  c->marker().mark("k_init");
   c->phase_n = n;
-  c->last_launches = n ? 2 : 1;
+  CK(cudaGetLastError());
+  return MPSF_OK;
+}
+
+// pass 1 over entries [chunk_off, chunk_off + n_chunk) of the batch (d_chunk points at them)
+static int scan_chunk(mpsf_ctx* c, const mpsf_fault_entry* d_chunk, uint64_t n_chunk, uint64_t chunk_off,
+                      const mpsf_params* p, uint64_t* d_counts, cudaStream_t st) {
+  Params P = to_params(p);
+  P.base_index += chunk_off;
+  if (launch_scan(c->W, c->S, d_chunk, n_chunk, P, reinterpret_cast<unsigned long long*>(d_counts),
+                  c->d_count_part, st, c->marker(), &c->parts))
+    return MPSF_E_CUDA;
   return MPSF_OK;
 }
 
@@ -581,7 +629,7 @@ int mpsf_finalize(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const m
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const Marker mk = c->marker();
   if (launch_finalize(c->W, c->S, d_in, n, to_params(p), d_out, reinterpret_cast<unsigned long long*>(d_dkeys), d_didx,
-                      d_cancel, st, mk))
+                      d_cancel, 0, (uint32_t)tiles_for(n), c->d_tctr, st, mk))
     return MPSF_E_CUDA;
   k_summary<<<1, 1, 0, st>>>(c->S.ctrl, c->S.err_idx, c->d_tiles, tiles_for(n), c->d_sum);
   mk.mark("k_summary");
@@ -752,13 +800,95 @@ int mpsf_process_host(mpsf_ctx* c, const mpsf_fault_entry* h_in, uint64_t n, con
   }
   uint8_t* b = c->d_io;
   cudaStream_t st = c->own_stream;
-  CK(cudaMemcpyAsync(b + o_in, h_in, 16 * n, cudaMemcpyHostToDevice, st));
-  for (int attempt = 0; attempt < 4; ++attempt) {
-    int rc = mpsf_process(c, reinterpret_cast<mpsf_fault_entry*>(b + o_in), n, p,
-                          reinterpret_cast<mpsf_out_record*>(b + o_out),
-                          reinterpret_cast<mpsf_client_verdict*>(b + o_v), reinterpret_cast<uint64_t*>(b + o_cnt),
-                          reinterpret_cast<uint64_t*>(b + o_dk), reinterpret_cast<uint32_t*>(b + o_di),
-                          reinterpret_cast<uint32_t*>(b + o_ca), st);
+  const mpsf_fault_entry* d_in = reinterpret_cast<const mpsf_fault_entry*>(b + o_in);
+  mpsf_out_record* d_out = reinterpret_cast<mpsf_out_record*>(b + o_out);
+  mpsf_client_verdict* d_v = reinterpret_cast<mpsf_client_verdict*>(b + o_v);
+  uint64_t* d_cnt = reinterpret_cast<uint64_t*>(b + o_cnt);
+  unsigned long long* d_dk = reinterpret_cast<unsigned long long*>(b + o_dk);
+  uint32_t* d_di = reinterpret_cast<uint32_t*>(b + o_di);
+  uint32_t* d_ca = reinterpret_cast<uint32_t*>(b + o_ca);
+  if (p->base_index + n > MAX_GIDX) return MPSF_E_TOO_LARGE;
+  // chunk boundaries on finalize-tile multiples: chunk k = tiles [t_lo[k], t_lo[k+1])
+  const uint64_t te = tile_entries(), nt = tiles_for(n);
+  const int nch = n >= (1ull << 20) ? kMaxChunks : n >= (1ull << 18) ? 4 : 1;
+  const uint64_t tpc = (nt + nch - 1) / nch;
+  uint64_t t_lo[kMaxChunks + 1];
+  int chunks = 0;
+  for (uint64_t t = 0; t < nt; t += tpc) t_lo[chunks++] = t;
+  t_lo[chunks] = nt;
+  auto ent = [&](int k) { return std::min<uint64_t>(t_lo[k] * te, n); };
+
+  // attempt 0: pipelined.  H2D chunk k (h2d stream) || pass 1 on chunk k-1 (compute stream);
+  // finalize chunk k (compute) || D2H of chunk k-1's records (d2h stream)
+  CK(cudaEventRecord(c->ev_fork, st));
+  CK(cudaStreamWaitEvent(c->h2d_stream, c->ev_fork, 0));
+  CK(cudaStreamWaitEvent(c->d2h_stream, c->ev_fork, 0));
+  int rc = batch_init(c, n, p, d_cnt, st);
+  if (rc) return rc;
+  int launches = 1;
+  for (int k = 0; k < chunks; ++k) {
+    const uint64_t lo = ent(k), cnt = ent(k + 1) - lo;
+    CK(cudaMemcpyAsync(b + o_in + 16 * lo, h_in + lo, 16 * cnt, cudaMemcpyHostToDevice, c->h2d_stream));
+    CK(cudaEventRecord(c->ev_in[k], c->h2d_stream));
+    CK(cudaStreamWaitEvent(st, c->ev_in[k], 0));
+    if ((rc = scan_chunk(c, d_in + lo, cnt, lo, p, d_cnt, st))) return rc;
+    ++launches;
+  }
+  const Marker mk = c->marker();
+  const Params P = to_params(p);
+  if (launch_resolve(c->W, c->S, P, d_v, c->d_count_part, c->parts, reinterpret_cast<unsigned long long*>(d_cnt),
+                     st, mk))
+    return MPSF_E_CUDA;
+  ++launches;
+  if ((p->flags & MPSF_PF_ISOLATION) && n) {
+    if (launch_general(c->W, c->S, d_in, n, P, 1, st, mk)) return MPSF_E_CUDA;
+    ++launches;
+    if (p->m2_us <= p->benign_us) {
+      if (launch_general(c->W, c->S, d_in, n, P, 2, st, mk)) return MPSF_E_CUDA;
+      ++launches;
+    }
+    if (launch_resolve2(c->W, c->S, P, st, mk)) return MPSF_E_CUDA;
+    ++launches;
+  }
+  for (int k = 0; k < chunks; ++k) {
+    const uint64_t lo = ent(k), cnt = ent(k + 1) - lo;
+    if (launch_finalize(c->W, c->S, d_in, n, P, d_out, d_dk, d_di, d_ca, (uint32_t)t_lo[k], (uint32_t)t_lo[k + 1],
+                        c->d_tctr + k, st, mk))
+      return MPSF_E_CUDA;
+    ++launches;
+    CK(cudaEventRecord(c->ev_fin[k], st));
+    CK(cudaStreamWaitEvent(c->d2h_stream, c->ev_fin[k], 0));
+    CK(cudaMemcpyAsync(h_out + lo, d_out + lo, 8 * cnt, cudaMemcpyDeviceToHost, c->d2h_stream));
+  }
+  k_summary<<<1, 1, 0, st>>>(c->S.ctrl, c->S.err_idx, c->d_tiles, nt, c->d_sum);
+  mk.mark("k_summary");
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(c->ev_done, st));
+  c->pending = true;
+  c->last_n = n;
+  c->last_launches = launches + 1;
+  if (C) {
+    CK(cudaMemcpyAsync(h_verdict, d_v, 4ull * C, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_counts, d_cnt, 8ull * NSCEN * C, cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaEventRecord(c->ev_d2h, c->d2h_stream));
+  CK(cudaStreamWaitEvent(st, c->ev_d2h, 0));
+  if ((rc = mpsf_get_summary(c, summary))) return rc;
+  if (summary->status != MPSF_E_OVERFLOW) {
+    if (summary->status == MPSF_OK) {
+      if (summary->n_dedup) {
+        CK(cudaMemcpyAsync(h_dkeys, d_dk, 8 * summary->n_dedup, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(h_didx, d_di, 4 * summary->n_dedup, cudaMemcpyDeviceToHost, st));
+      }
+      if (summary->n_cancel) CK(cudaMemcpyAsync(h_cancel, d_ca, 4 * summary->n_cancel, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    return MPSF_OK;
+  }
+  // the wild-page hash overflowed (its capacity has grown): re-run on the resident entries
+  CK(cudaStreamSynchronize(st));
+  for (int attempt = 1; attempt < 4; ++attempt) {
+    rc = mpsf_process(c, d_in, n, p, d_out, d_v, d_cnt, reinterpret_cast<uint64_t*>(d_dk), d_di, d_ca, st);
     if (rc) return rc;
     CK(cudaMemcpyAsync(h_out, b + o_out, 8 * n, cudaMemcpyDeviceToHost, st));
     if (C) {

@@ -28,9 +28,12 @@ int launch_resolve(const World& W, const Scratch& S, const Params& P, mpsf_clien
 int launch_general(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
                    int stage, cudaStream_t st, const Marker& mk);
 int launch_resolve2(const World& W, const Scratch& S, const Params& P, cudaStream_t st, const Marker& mk);
+// finalize tiles [tile_lo, tile_hi) of the batch (entries indexed from `in`), dynamic order via
+// the zero-initialised counter tctr
 int launch_finalize(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
                     mpsf_out_record* out, unsigned long long* dkeys, uint32_t* didx, uint32_t* cancel,
-                    cudaStream_t st, const Marker& mk);
+                    uint32_t tile_lo, uint32_t tile_hi, uint32_t* tctr, cudaStream_t st, const Marker& mk);
+uint32_t tile_entries();   // entries per finalize tile (chunk boundaries must be multiples)
 int launch_hash_export(const Hash& h, uint64_t cap, unsigned long long* keys, uint32_t* vals, uint32_t* counter,
                        uint64_t out_cap, cudaStream_t st);
 int launch_hash_merge(const Hash& h, uint32_t* ctrl, const unsigned long long* keys, const uint32_t* vals,
