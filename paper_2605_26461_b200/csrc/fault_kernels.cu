@@ -29,6 +29,10 @@
 #include "mpsf_device.cuh"
 #include "mpsf_kernels.h"
 
+#ifndef MPSF_ABLATE
+#define MPSF_ABLATE 0   // experiment-only switches (tools/ablate.py); 0 in every shipped build
+#endif
+
 namespace mpsf {
 
 // Warp-specialised CTA: warp 0 is the control warp (TMA producer; in the finalize pass also
@@ -83,7 +87,7 @@ __host__ __device__ inline uint32_t al16(uint64_t x) { return (uint32_t)((x + 15
 struct Layout {
   uint32_t tiles, bars, wbars, tids, tot, pre;
   uint32_t pg_base, pg_end, poff, rattr, rrid, skip, crange, cspan, cshift, chan;
-  uint32_t c64, iso, r32, counts, cstate, total;
+  uint32_t c64, iso, r32, counts, used, cstate, total;
   uint32_t rep_chan;
 };
 
@@ -113,6 +117,7 @@ __host__ __device__ inline Layout make_layout(uint32_t nr, uint32_t nc, uint32_t
   L.iso = o; if (staged && !fin) o += al16(3ull * 128 * nc);
   L.r32 = o; if (staged && !fin) o += al16(8ull * nr);
   L.counts = o; if (staged && !fin) o += al16(4ull * NSCEN * nc);
+  L.used = o; if (staged && !fin) o += 16;
   L.cstate = o; if (staged && fin) o += al16(32ull * nc);
   L.total = o;
   return L;
@@ -124,6 +129,7 @@ struct View {
   unsigned long long *ft_ce, *ft_sa, *trap_sa;   // pass-1 caches (or null)
   uint32_t* iso;                                  // [3][C][32] per-lane copies (or null)
   uint32_t *ext, *nr0, *counts;
+  uint32_t* used;                                 // [2] claimed hash slots (dd, nr)
   const CState* cst;
 };
 
@@ -164,6 +170,7 @@ __device__ View setup(uint8_t* sm, const Layout& L, const World& W, const Scratc
   }
   v.ft_ce = v.ft_sa = v.trap_sa = nullptr;
   v.iso = v.ext = v.nr0 = v.counts = nullptr;
+  v.used = S.ctrl + C_HASH_DD;                    // C_HASH_NR follows it
   v.cst = S.cstate;
   if (kStaged && scan) {
     unsigned long long* c64 = reinterpret_cast<unsigned long long*>(sm + L.c64);
@@ -178,6 +185,9 @@ __device__ View setup(uint8_t* sm, const Layout& L, const World& W, const Scratc
     uint32_t* cnt = reinterpret_cast<uint32_t*>(sm + L.counts);
     for (uint32_t i = tid; i < NSCEN * C; i += nb) cnt[i] = 0;
     v.counts = cnt;
+    uint32_t* used = reinterpret_cast<uint32_t*>(sm + L.used);
+    if (tid < 2) used[tid] = 0;
+    v.used = used;
   }
   if (kStaged && fin) {
     CState* cs = reinterpret_cast<CState*>(sm + L.cstate);
@@ -389,15 +399,19 @@ __device__ __forceinline__ void control_static(const Pipe& p, const mpsf_fault_e
 template <bool kStaged>
 __device__ __forceinline__ void scan_entry(const World& W, const View& v, const Scratch& S, const Params& P,
                                            uint4 e, uint64_t gidx, unsigned long long* counts) {
+  if (MPSF_ABLATE & 64) { if (e.x == 0x12345 && e.y == 0x777) atomicOr(S.ctrl + C_ERR, 1u); return; }
   const Rec r = decode<kStaged>(W, v, S, e, gidx);
   if (!r.valid) return;
   const uint32_t c = r.c;
+  if (MPSF_ABLATE & 32) { if (r.s == 99) atomicOr(S.ctrl + C_ERR, 1u); return; }
+  if (!(MPSF_ABLATE & 8)) {
   if (kStaged) atomicAdd(v.counts + c * NSCEN + r.s, 1u);
   else atomicAdd(counts + (uint64_t)c * NSCEN + r.s, 1ull);
+  }
   if (s_trap(r.s)) {
     const unsigned long long t = (gidx << 8) | (unsigned long long)r.s;
     if (!r.sa) min64(S.trap_mps, t);
-    else if (kStaged) min64c(S.trap_sa + c, v.trap_sa + c, t);
+    else if (kStaged) smin64(v.trap_sa + c, t);
     else min64(S.trap_sa + c, t);
     return;
   }
@@ -405,34 +419,36 @@ __device__ __forceinline__ void scan_entry(const World& W, const View& v, const 
   const bool serv = s_serviceable(r.s);
   if (s_parse(r.s) || (!serv && !(P.flags & MPSF_PF_ISOLATION))) {   // fatal report (pipeline.py:168-182)
     const unsigned long long t = ((unsigned long long)ok << 8) | (unsigned long long)r.s;
-    if (r.sa) { if (kStaged) min64c(S.ft_sa + c, v.ft_sa + c, t); else min64(S.ft_sa + c, t); }
-    else if (r.ceng == 1) { if (kStaged) min64c(S.ft_ce + c, v.ft_ce + c, t); else min64(S.ft_ce + c, t); }
+    if (r.sa) { if (kStaged) smin64(v.ft_sa + c, t); else min64(S.ft_sa + c, t); }
+    else if (r.ceng == 1) { if (kStaged) smin64(v.ft_ce + c, t); else min64(S.ft_ce + c, t); }
     else min64(S.ft_gr, t);
   } else if (!serv) {                                                // isolation-eligible (pipeline.py:177-179)
-    // per-client minimum: iso1 unmapped / iso2 managed / iso3 external (per-lane smem copies)
+    // per-client minimum: iso1 unmapped / iso2 managed / iso3 external (per-warp smem copies:
+    // a warp's indices only grow, so each copy takes one atomic per client and mechanism)
     const int m = !r.at.in_range ? 0 : (r.at.kind == 0 ? 1 : 2);
-    uint32_t* g = (m == 0 ? S.iso1 : (m == 1 ? S.iso2 : S.iso3)) + c;
-    if (kStaged) min32c(g, v.iso + ((uint32_t)m * W.n_clients + c) * 32 + (threadIdx.x & 31), ok);
-    else min32(g, ok);
+    if (kStaged) smin32(v.iso + ((uint32_t)m * W.n_clients + c) * 32 + (threadIdx.x >> 5), ok);
+    else min32((m == 0 ? S.iso1 : (m == 1 ? S.iso2 : S.iso3)) + c, ok);
     if (!r.at.in_range) {
       if (r.at.guard) {
-        if (kStaged) min32c(S.nr0 + r.at.ridx, v.nr0 + r.at.ridx, ok); else min32(S.nr0 + r.at.ridx, ok);
-      } else if (!hash_min(S.hnr, S.ctrl, nr_key(c, 0, r.va >> 12), ok)) {
+        if (kStaged) smin32(v.nr0 + r.at.ridx, ok); else min32(S.nr0 + r.at.ridx, ok);
+      } else if (!(MPSF_ABLATE & 1) && !hash_min(S.hnr, v.used + 1, nr_key(c, 0, r.va >> 12), ok)) {
         atomicOr(S.ctrl + C_OVF, 1u);
       }
     } else {
       if (r.at.kind != 0) {
-        if (kStaged) min32c(S.ext + r.at.ridx, v.ext + r.at.ridx, ok); else min32(S.ext + r.at.ridx, ok);
+        if (kStaged) smin32(v.ext + r.at.ridx, ok); else min32(S.ext + r.at.ridx, ok);
       }
       // first eligible record per in-range page: the epoch-1 first-isolation key of a client
       // released before the drain (trap / dead at start), so that case needs no extra pass
-      if (S.nrall) min32(S.nrall + r.at.slot, ok);
+      if (S.nrall && !(MPSF_ABLATE & 2)) min32(S.nrall + r.at.slot, ok);
     }
   }
   if (r.kind == 0 && r.repl) {                                       // dedup insert (rule C2)
     const uint32_t val = ((uint32_t)gidx << 3) | r.group;
     bool to_hash = !(r.at.in_range || r.at.guard);
-    if (!to_hash && W.dd_groups != 1) {
+    if (MPSF_ABLATE & 4) {
+      to_hash = to_hash && !(MPSF_ABLATE & 1);
+    } else if (!to_hash && W.dd_groups != 1) {
       // one slot per (page, group): min with a load pre-check (hot slots: most records skip)
       min32(S.dd + dd_slot(W, r), val);
     } else if (!to_hash) {
@@ -450,9 +466,31 @@ __device__ __forceinline__ void scan_entry(const World& W, const View& v, const 
         break;
       }
     }
-    if (to_hash && !hash_min(S.hdd, S.ctrl, dedup_key(c, r.eng, r.s, r.va >> 12), (uint32_t)gidx))
+    if (MPSF_ABLATE & 1) to_hash = false;
+    if (to_hash && !hash_min(S.hdd, v.used, dedup_key(c, r.eng, r.s, r.va >> 12), (uint32_t)gidx))
       atomicOr(S.ctrl + C_OVF, 1u);
   }
+}
+
+// End of a staged scan block: fold the block-local minima into the global ones (fire-and-forget
+// reductions, one per touched slot).
+__device__ __forceinline__ void flush_minima(const World& W, const Scratch& S, const View& v) {
+  const uint32_t C = W.n_clients, R = W.n_ranges;
+  for (uint32_t i = threadIdx.x; i < 3 * C; i += blockDim.x) {
+    const uint32_t* w = v.iso + i * 32;
+    uint32_t m = EMPTY32;
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) m = min(m, w[k]);
+    uint32_t* g = (i < C ? S.iso1 : (i < 2 * C ? S.iso2 : S.iso3)) + (i % C);
+    if (m != EMPTY32) atomicMin(g, m);
+    const unsigned long long t = v.ft_ce[i];      // c64 = [ft_ce | ft_sa | trap_sa]
+    if (t != EMPTY64) atomicMin(i < C ? S.ft_ce + i : (i < 2 * C ? S.ft_sa + (i - C) : S.trap_sa + (i - 2 * C)), t);
+  }
+  for (uint32_t i = threadIdx.x; i < R; i += blockDim.x) {
+    if (v.ext[i] != EMPTY32) atomicMin(S.ext + i, v.ext[i]);
+    if (v.nr0[i] != EMPTY32) atomicMin(S.nr0 + i, v.nr0[i]);
+  }
+  if (threadIdx.x < 2 && v.used[threadIdx.x]) atomicAdd(S.ctrl + C_HASH_DD + threadIdx.x, v.used[threadIdx.x]);
 }
 
 template <bool kStaged>
@@ -472,6 +510,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_scan(World W, Scratch S, const mps
     uint32_t* part = count_part + (uint64_t)blockIdx.x * NSCEN * W.n_clients;
     // accumulate: a batch may be scanned in several launches (chunked host pipeline)
     for (uint32_t i = threadIdx.x; i < NSCEN * W.n_clients; i += blockDim.x) part[i] += v.counts[i];
+    flush_minima(W, S, v);
   }
 }
 
@@ -621,7 +660,7 @@ __device__ __forceinline__ void general_entry(const World& W, const View& v, con
       min32(giso + 0, ok);
       if (epoch1) {
         if (r.at.in_range || r.at.guard) min32(S.nr1 + r.at.slot, ok);
-        else if (!hash_min(S.hnr, S.ctrl, nr_key(r.c, 1, r.va >> 12), ok)) atomicOr(S.ctrl + C_OVF, 1u);
+        else if (!hash_min(S.hnr, S.ctrl + C_HASH_NR, nr_key(r.c, 1, r.va >> 12), ok)) atomicOr(S.ctrl + C_OVF, 1u);
       }
     } else if (r.at.kind == 0) {
       min32(giso + 1, ok);
@@ -901,7 +940,7 @@ __global__ void k_hash_merge(Hash h, uint32_t* ctrl, const unsigned long long* _
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x) {
     const unsigned long long k = keys[i];
     if (k == EMPTY64) continue;
-    if (!hash_min(h, ctrl, k, vals[i])) atomicOr(ctrl + C_OVF, 1u);
+    if (!hash_min(h, ctrl + h.used_slot, k, vals[i])) atomicOr(ctrl + C_OVF, 1u);
   }
 }
 

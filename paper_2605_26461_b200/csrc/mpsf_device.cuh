@@ -195,7 +195,11 @@ __device__ __forceinline__ Attr attribute_pg(const Tables& T, const uint8_t* __r
     t.slot = T.poff[k] + (page - base);
     t.kind = a & 0xFF; t.lifecycle = (a >> 8) & 0xFF; t.migratable = (a >> 16) & 0xFF;
     const uint32_t ust = a >> 24;
+#if defined(MPSF_ABLATE) && (MPSF_ABLATE & 16)
+    t.st = ust != 0xFF ? ust : (t.slot & 7);
+#else
     t.st = ust != 0xFF ? ust : (uint32_t)page_state[t.slot];
+#endif
   } else if (page == end) {
     t.ridx = (int)k; t.guard = true;
     t.slot = T.poff[k] + (end - T.pg_base[k]);
@@ -250,7 +254,8 @@ __device__ __forceinline__ uint32_t* hash_val(const Hash& h, uint32_t s) {
   return reinterpret_cast<uint32_t*>(h.keys + 2ull * s + 1);
 }
 
-__device__ __forceinline__ bool hash_min(const Hash& h, uint32_t* ctrl, uint64_t key, uint32_t v) {
+// `used` counts claimed slots (a block-local smem counter in the scan, flushed once per block).
+__device__ __forceinline__ bool hash_min(const Hash& h, uint32_t* used, uint64_t key, uint32_t v) {
   uint32_t s = (uint32_t)mix64(key) & h.mask;
   for (int p = 0; p < HASH_MAX_PROBE; ++p) {
     const ulonglong2 slot = __ldcg(reinterpret_cast<const ulonglong2*>(h.keys) + s);
@@ -258,7 +263,7 @@ __device__ __forceinline__ bool hash_min(const Hash& h, uint32_t* ctrl, uint64_t
     uint32_t cur = (uint32_t)slot.y;
     if (k == EMPTY64) {
       k = atomicCAS(h.keys + 2ull * s, EMPTY64, (unsigned long long)key);
-      if (k == EMPTY64) { atomicAdd(ctrl + h.used_slot, 1u); k = key; cur = EMPTY32; }
+      if (k == EMPTY64) { atomicAdd(used, 1u); k = key; cur = EMPTY32; }
     }
     if (k == key) {
       if (cur > v) atomicMin(hash_val(h, s), v);
@@ -287,18 +292,13 @@ __device__ __forceinline__ void min32(uint32_t* g, uint32_t v) {
 __device__ __forceinline__ void min64(unsigned long long* g, unsigned long long v) {
   if (__ldcg(g) > v) atomicMin(g, v);
 }
-// smem-cached variant: the block-local copy filters, the survivors go out as fire-and-forget
-// reductions (RED.MIN, no return value, so no L2 round trip on the critical path)
-__device__ __forceinline__ void min32c(uint32_t* g, uint32_t* c, uint32_t v) {
-  if (*c <= v) return;
-  if (atomicMin(c, v) <= v) return;
-  atomicMin(g, v);
+// block-local minima in shared memory: the scan keeps per-client / per-range minima here and
+// flushes them to global once per block (no same-address global atomics inside the loop)
+__device__ __forceinline__ void smin32(uint32_t* c, uint32_t v) {
+  if (*c > v) atomicMin(c, v);
 }
-__device__ __forceinline__ void min64c(unsigned long long* g, unsigned long long* c,
-                                       unsigned long long v) {
-  if (*c <= v) return;
-  if (atomicMin(c, v) <= v) return;
-  atomicMin(g, v);
+__device__ __forceinline__ void smin64(unsigned long long* c, unsigned long long v) {
+  if (*c > v) atomicMin(c, v);
 }
 
 // dedup key (SURVEY.md Appendix C rule C2)
