@@ -46,6 +46,7 @@ constexpr int TILE = WORKERS * WSEG;       // 1984 entries = 31 KiB
 constexpr int NBUF = 3;
 constexpr uint32_t TILE_BYTES = TILE * 16;
 constexpr uint32_t TID_NONE = 0xFFFFFFFFu;
+constexpr int QCAP = 64;                   // per-warp deferred hash-op stack (scan)
 
 // ---- PTX: mbarrier + bulk async copy (TMA) ---------------------------------------------
 __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -86,6 +87,7 @@ __host__ __device__ inline uint32_t al16(uint64_t x) { return (uint32_t)((x + 15
 
 struct Layout {
   uint32_t tiles, bars, wbars, tids, tot, pre;
+  uint32_t lut, cinfo, queue;
   uint32_t pg_base, pg_end, poff, rattr, rrid, skip, crange, cspan, cshift, chan;
   uint32_t c64, iso, r32, counts, used, cstate, total;
   uint32_t rep_chan;
@@ -96,13 +98,16 @@ struct Layout {
 __host__ __device__ inline Layout make_layout(uint32_t nr, uint32_t nc, uint32_t nch, bool staged, bool fin) {
   Layout L;
   uint32_t o = 0;
-  L.tiles = o; o += 32 * 3 * 1024;        // >= NBUF tiles (finalize) and 32 warps x 3 x 1 KiB chunks
+  L.tiles = o; if (fin) o += NBUF * TILE_BYTES;   // finalize: TMA tile ring
   L.bars = o; o += 4 * 8 * NBUF;          // full, empty, done, pref per buffer
-  L.wbars = o; o += 8 * 32 * 3;           // warp-private stream barriers
+  L.wbars = o;
   L.tids = o; o += al16(4 * NBUF);
   L.tot = o; o += 8 * 32 * NBUF;          // per buffer, per worker warp: (cancel, dedup) counts
   L.pre = o; o += 8 * 32 * NBUF;          // per buffer, per worker warp: exclusive output offsets
   L.rep_chan = (staged && nch <= 256) ? 32u : 0u;
+  L.lut = o; o += 4 * LUT_N;
+  L.cinfo = o; if (staged) o += al16(512ull * nc);
+  L.queue = o; if (!fin) o += WARPS * QCAP * 16;
   L.pg_base = o; if (staged) o += al16(4ull * nr);
   L.pg_end = o; if (staged) o += al16(4ull * nr);
   L.poff = o; if (staged) o += al16(4ull * nr);
@@ -113,7 +118,7 @@ __host__ __device__ inline Layout make_layout(uint32_t nr, uint32_t nc, uint32_t
   L.cspan = o; if (staged) o += al16(128ull * nc);
   L.cshift = o; if (staged) o += al16(128ull * nc);
   L.chan = o; if (staged) o += al16(4ull * nch * (L.rep_chan ? 32 : 1));
-  L.c64 = o; if (staged && !fin) o += al16(24ull * nc);
+  L.c64 = o; if (staged && !fin) o += al16(24ull * nc + 16);
   L.iso = o; if (staged && !fin) o += al16(3ull * 128 * nc);
   L.r32 = o; if (staged && !fin) o += al16(8ull * nr);
   L.counts = o; if (staged && !fin) o += al16(4ull * NSCEN * nc);
@@ -127,6 +132,7 @@ __host__ __device__ inline Layout make_layout(uint32_t nr, uint32_t nc, uint32_t
 struct View {
   Tables T;
   unsigned long long *ft_ce, *ft_sa, *trap_sa;   // pass-1 caches (or null)
+  unsigned long long *ft_gr, *trap_mps;
   uint32_t* iso;                                  // [3][C][32] per-lane copies (or null)
   uint32_t *ext, *nr0, *counts;
   uint32_t* used;                                 // [2] claimed hash slots (dd, nr)
@@ -134,7 +140,8 @@ struct View {
 };
 
 template <bool kStaged>
-__device__ View setup(uint8_t* sm, const Layout& L, const World& W, const Scratch& S, bool scan, bool fin) {
+__device__ View setup(uint8_t* sm, const Layout& L, const World& W, const Scratch& S, bool scan, bool fin,
+                      bool isolation_flag) {
   View v;
   const uint32_t tid = threadIdx.x, nb = blockDim.x;
   const uint32_t R = W.n_ranges, C = W.n_clients;
@@ -160,6 +167,9 @@ __device__ View setup(uint8_t* sm, const Layout& L, const World& W, const Scratc
     uint32_t* cn = reinterpret_cast<uint32_t*>(sm + L.chan);
     const uint32_t rc = L.rep_chan ? 32u : 1u;
     for (uint32_t i = tid; i < rc * W.n_channels; i += nb) cn[i] = __ldg(W.chan + i / rc);
+    uint4* ci = reinterpret_cast<uint4*>(sm + L.cinfo);
+    for (uint32_t i = tid; i < 32 * C; i += nb) ci[i] = __ldg(W.cinfo4 + i / 32);
+    v.T.cinfo = ci;
     v.T.pg_base = pb; v.T.pg_end = pe; v.T.poff = po; v.T.rattr = ra; v.T.rrid = fin ? rr : W.rrid;
     v.T.skip = sk; v.T.crange = cr; v.T.cspan = cs; v.T.cshift = ch; v.T.chan = cn;
     v.T.rep_client = 32; v.T.rep_chan = L.rep_chan;
@@ -167,15 +177,25 @@ __device__ View setup(uint8_t* sm, const Layout& L, const World& W, const Scratc
     v.T.pg_base = W.pg_base; v.T.pg_end = W.pg_end; v.T.poff = W.poff; v.T.rattr = W.rattr; v.T.rrid = W.rrid;
     v.T.skip = W.skip; v.T.crange = W.crange; v.T.cspan = W.cspan; v.T.cshift = W.cshift; v.T.chan = W.chan;
     v.T.rep_client = 0; v.T.rep_chan = 0;
+    v.T.cinfo = W.cinfo4;
+  }
+  {
+    uint32_t* lut = reinterpret_cast<uint32_t*>(sm + L.lut);
+    const bool iso = isolation_flag;
+    for (uint32_t i = tid; i < (uint32_t)LUT_N; i += nb) lut[i] = lut_word((int)i, iso);
+    v.T.lut = lut;
+    v.T.n_channels = W.n_channels;
   }
   v.ft_ce = v.ft_sa = v.trap_sa = nullptr;
+  v.ft_gr = S.ft_gr; v.trap_mps = S.trap_mps;
   v.iso = v.ext = v.nr0 = v.counts = nullptr;
   v.used = S.ctrl + C_HASH_DD;                    // C_HASH_NR follows it
   v.cst = S.cstate;
   if (kStaged && scan) {
     unsigned long long* c64 = reinterpret_cast<unsigned long long*>(sm + L.c64);
-    for (uint32_t i = tid; i < 3 * C; i += nb) c64[i] = EMPTY64;
+    for (uint32_t i = tid; i < 3 * C + 2; i += nb) c64[i] = EMPTY64;
     v.ft_ce = c64; v.ft_sa = c64 + C; v.trap_sa = c64 + 2 * C;
+    v.ft_gr = c64 + 3 * C; v.trap_mps = c64 + 3 * C + 1;
     uint32_t* iso = reinterpret_cast<uint32_t*>(sm + L.iso);
     for (uint32_t i = tid; i < 3 * 32 * C; i += nb) iso[i] = EMPTY32;
     v.iso = iso;
@@ -265,6 +285,93 @@ __device__ __forceinline__ Rec decode(const World& W, const View& v, const Scrat
   return r;
 }
 
+// Rare path of decode_fast: raise the specific entry error (same checks, same order as decode).
+__device__ __noinline__ void entry_error(const Scratch& S, uint32_t cw, bool chok, uint4 e, uint64_t gidx) {
+  const uint32_t w3 = e.w, eng = w3 & 0xFF, acc = (w3 >> 8) & 0xFF, ek = (w3 >> 16) & 0xFF;
+  const uint64_t va = (uint64_t)e.x | ((uint64_t)e.y << 32);
+  if (!chok || !(cw & CH_VALID)) raise_err(S, EB_NO_CHANNEL, gidx);
+  else if (ek == 0 && (eng > 2 || acc > 2)) raise_err(S, EB_BAD_ENTRY, gidx);
+  else if (ek == 0 && eng != ((cw >> 16) & 3u)) raise_err(S, EB_MISMATCH, gidx);
+  else if (ek == 0 && va >= VA_LIMIT) raise_err(S, EB_VA, gidx);
+  else raise_err(S, EB_BAD_ENTRY, gidx);
+}
+
+// Lean decode shared by the passes: channel word, client row, skip-table attribution
+// (MemoryModel.range_at, memory.py:233-237) and one LUT word (faults.classify, faults.py:134-171).
+__device__ __forceinline__ Dec decode_fast(const Tables& T, const uint8_t* __restrict__ page_state,
+                                           const Scratch& S, uint4 e, uint64_t gidx, uint32_t lane) {
+  Dec d;
+  d.f = 0; d.c = 0; d.cw = 0; d.slot = 0; d.ridx = NO_RID; d.inr = false; d.guard = false;
+  d.va = (uint64_t)e.x | ((uint64_t)e.y << 32);
+  const uint32_t w3 = e.w;
+  if (!((w3 >> 24) & MPSF_ENTRY_VALID)) return d;
+  const uint32_t ch = e.z, eng = w3 & 0xFF, acc = (w3 >> 8) & 0xFF, ek = (w3 >> 16) & 0xFF;
+  const bool chok = ch < T.n_channels;
+  const uint32_t cw = chok ? rep_load(T.chan, ch, T.rep_chan, lane) : 0u;
+  const bool k0 = ek == 0;
+  const bool bad = !(cw & CH_VALID) ||
+                   (k0 ? (eng > 2 || acc > 2 || eng != ((cw >> 16) & 3u) || d.va >= VA_LIMIT)
+                       : (ek > 15 || (T.lut[LUT_XK + ek] & LF_BAD)));
+  if (bad) {
+    entry_error(S, cw, chok, e, gidx);
+    return d;
+  }
+  d.c = cw & 0xFFFFu;
+  d.cw = cw;
+  uint32_t idx = LUT_XK + ek;
+  if (k0) {
+    const uint4 ci = T.rep_client ? T.cinfo[d.c * 32 + lane] : T.cinfo[d.c];
+    const uint32_t lo = ci.x & 0xFFFFu, hi = ci.x >> 16;
+    const uint32_t page = (uint32_t)(d.va >> 12);
+    uint32_t rcls = 8, st = 0;
+    if (lo != hi && d.va < VA_TABLE_LIMIT && page >= ci.y) {
+      uint32_t j = (page - ci.y) >> ci.z;
+      j = j < (uint32_t)SKIP_K ? j : (uint32_t)(SKIP_K - 1);
+      uint32_t k = T.skip[d.c * SKIP_K + j];
+      while (k + 1 < hi && T.pg_base[k + 1] <= page) ++k;
+      const uint32_t end = T.pg_end[k], base = T.pg_base[k];
+      d.inr = page < end;
+      d.guard = page == end;
+      d.slot = T.poff[k] + (page - base);
+      if (d.inr || d.guard) d.ridx = k;
+      if (d.inr) {
+        const uint32_t a = T.rattr[k];
+        rcls = (a & 1u) | ((a >> 7) & 2u) | ((a >> 14) & 4u);
+        const uint32_t ust = a >> 24;
+        st = (ust != 0xFF ? ust : (uint32_t)page_state[d.slot]) & 7u;
+      }
+    }
+    idx = ((eng * 3 + acc) * 16 + rcls) * 8 + st;
+  }
+  d.f = T.lut[idx];
+  return d;
+}
+
+// The Rec view of a lean decode (for the passes still written against Rec).
+__device__ __forceinline__ Rec to_rec(const Dec& d, uint4 e) {
+  Rec r;
+  r.valid = d.f != 0;
+  r.va = d.va;
+  r.c = d.c;
+  r.ceng = (int)((d.cw >> 16) & 3u);
+  r.sa = (d.cw >> 18) & 1u;
+  r.eng = (int)(e.w & 0xFF);
+  r.kind = (int)((e.w >> 16) & 0xFF);
+  r.s = (int)(d.f & LF_S);
+  r.repl = (d.f & LF_REPL) != 0;
+  r.group = (d.f >> LF_GROUP_SH) & 7u;
+  r.at.ridx = d.ridx == NO_RID ? -1 : (int)d.ridx;
+  r.at.in_range = d.inr;
+  r.at.guard = d.guard;
+  r.at.slot = d.slot;
+  r.at.st = 0;
+  r.at.kind = ((d.f >> LF_M_SH) & 3u) == 2u ? 1 : 0;
+  r.at.lifecycle = 0;
+  r.at.migratable = 1;
+  r.at.rid = NO_RID;
+  return r;
+}
+
 __device__ __forceinline__ uint32_t ok32_of(bool repl, uint64_t gidx) {
   return (repl ? 0u : 0x80000000u) | (uint32_t)gidx;
 }
@@ -321,60 +428,38 @@ __device__ __forceinline__ Pipe pipe_init(uint8_t* sm, const Layout& L) {
   return p;
 }
 
-// Warp-private stream for the order-free passes (scan, general): every warp pulls its own
-// 1 KiB chunks (64 entries) with TMA into a 3-deep private ring and refills a slot as soon
-// as its own lanes are done -- no coupling to the slowest warp of the CTA.
+// Stream for the order-free passes (scan, general): warp w of the grid owns 64-entry chunks
+// w, w + W, w + 2W, ...; each lane reads its two adjacent entries with one 32-byte
+// non-allocating load (L2 evict-first) and the next chunk's pair is requested before the
+// current one is processed, so a chunk's HBM latency hides behind the previous chunk's work.
 constexpr int WCHUNK = 64;
-constexpr uint32_t WCHUNK_BYTES = WCHUNK * 16;
-constexpr int WDEPTH = 3;
 
-__device__ __forceinline__ void wstream_init(uint8_t* sm, const Layout& L) {
-  if (threadIdx.x == 0) {
-    uint64_t* wb = reinterpret_cast<uint64_t*>(sm + L.wbars);
-    for (int i = 0; i < WARPS * WDEPTH; ++i) mbar_init(wb + i, 1);
-    fence_mbar_init();
+__device__ __forceinline__ void ld_pair(const mpsf_fault_entry* in, uint64_t n, uint64_t i0, bool a32, uint4& a,
+                                        uint4& b) {
+  const uint4* p = reinterpret_cast<const uint4*>(in) + i0;
+  if (a32 && i0 + 1 < n) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+                 : "l"(p));
+  } else {
+    a = i0 < n ? __ldcs(p) : make_uint4(0, 0, 0, 0);
+    b = i0 + 1 < n ? __ldcs(p + 1) : make_uint4(0, 0, 0, 0);
   }
 }
 
 template <typename F>
-__device__ __forceinline__ void warp_stream(uint8_t* sm, const Layout& L, const mpsf_fault_entry* in, uint64_t n,
-                                            F&& fn) {
+__device__ __forceinline__ void ldg_stream(const mpsf_fault_entry* in, uint64_t n, F&& fn) {
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint8_t* wbuf = sm + L.tiles + (size_t)warp * WDEPTH * WCHUNK_BYTES;
-  uint64_t* wbar = reinterpret_cast<uint64_t*>(sm + L.wbars) + warp * WDEPTH;
-  const uint64_t gw = (uint64_t)blockIdx.x * WARPS + warp, GW = (uint64_t)gridDim.x * WARPS;
+  const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp, GW = (uint64_t)gridDim.x * (blockDim.x >> 5);
   const uint64_t nch = (n + WCHUNK - 1) / WCHUNK;
-  const uint64_t pol = policy_evict_first();
-  auto issue = [&](int b, uint64_t c) {
-    const uint64_t start = c * WCHUNK;
-    const uint64_t cnt = n - start < (uint64_t)WCHUNK ? n - start : (uint64_t)WCHUNK;
-    mbar_expect_tx(wbar + b, (uint32_t)(cnt * 16));
-    bulk_load(wbuf + (size_t)b * WCHUNK_BYTES, in + start, (uint32_t)(cnt * 16), wbar + b, pol);
-  };
-  if (lane == 0) {
-    for (int b = 0; b < WDEPTH; ++b) {
-      const uint64_t c = gw + (uint64_t)b * GW;
-      if (c < nch) issue(b, c);
-    }
-  }
-  __syncwarp();
-  for (uint32_t k = 0;; ++k) {
-    const uint64_t c = gw + (uint64_t)k * GW;
-    if (c >= nch) break;
-    const int b = k % WDEPTH;
-    mbar_wait(wbar + b, (k / WDEPTH) & 1);
-    const uint4* chunk = reinterpret_cast<const uint4*>(wbuf + (size_t)b * WCHUNK_BYTES);
-#pragma unroll
-    for (int e = 0; e < WCHUNK / 32; ++e) {
-      const int li = e * 32 + lane;
-      const uint64_t i = c * WCHUNK + li;
-      if (i < n) fn(chunk[li], i);
-    }
-    __syncwarp();
-    if (lane == 0) {
-      const uint64_t c2 = c + (uint64_t)WDEPTH * GW;
-      if (c2 < nch) issue(b, c2);
-    }
+  const bool a32 = ((uintptr_t)in & 31u) == 0;
+  uint4 na = make_uint4(0, 0, 0, 0), nb = na;
+  if (gw < nch) ld_pair(in, n, gw * WCHUNK + 2 * lane, a32, na, nb);
+  for (uint64_t c = gw; c < nch; c += GW) {
+    const uint4 e0 = na, e1 = nb;
+    if (c + GW < nch) ld_pair(in, n, (c + GW) * WCHUNK + 2 * lane, a32, na, nb);
+    const uint64_t i0 = c * WCHUNK + 2 * lane;
+    fn(e0, i0, i0 < n, e1, i0 + 1, i0 + 1 < n);
   }
 }
 
@@ -396,79 +481,127 @@ __device__ __forceinline__ void control_static(const Pipe& p, const mpsf_fault_e
 }
 
 // ---- pass 1 ---------------------------------------------------------------------------------
+// After its block-local part (counts and per-client / per-range minima in shared memory) an
+// entry leaves at most two first-in-group minima on global tables: its dedup key (rule C2,
+// a dense (page, group) slot or a claimed page slot) and the first eligible record of its page
+// (nrall).  Both entries of a lane issue their L2 loads together and resolve afterwards.
+// Wild pages (no range, no guard) go to a per-warp stack of deferred hash operations that is
+// drained 32 at a time, so their CAS round trips never sit on the common path.
+struct QOp { unsigned long long key; uint32_t val, tab; };
+
+struct ScanOut {
+  uint32_t* pa; uint32_t va;     // nrall precheck-min
+  uint32_t* pd; uint32_t vd;     // dedup slot precheck-min / claim
+  bool qn, qd;                   // deferred hash ops: NR key (hnr), dedup key (hdd)
+  unsigned long long kn, kd;
+  uint32_t vn, vdh;
+};
+
 template <bool kStaged>
-__device__ __forceinline__ void scan_entry(const World& W, const View& v, const Scratch& S, const Params& P,
-                                           uint4 e, uint64_t gidx, unsigned long long* counts) {
-  if (MPSF_ABLATE & 64) { if (e.x == 0x12345 && e.y == 0x777) atomicOr(S.ctrl + C_ERR, 1u); return; }
-  const Rec r = decode<kStaged>(W, v, S, e, gidx);
-  if (!r.valid) return;
-  const uint32_t c = r.c;
-  if (MPSF_ABLATE & 32) { if (r.s == 99) atomicOr(S.ctrl + C_ERR, 1u); return; }
-  if (!(MPSF_ABLATE & 8)) {
-  if (kStaged) atomicAdd(v.counts + c * NSCEN + r.s, 1u);
-  else atomicAdd(counts + (uint64_t)c * NSCEN + r.s, 1ull);
-  }
-  if (s_trap(r.s)) {
-    const unsigned long long t = (gidx << 8) | (unsigned long long)r.s;
-    if (!r.sa) min64(S.trap_mps, t);
-    else if (kStaged) smin64(v.trap_sa + c, t);
-    else min64(S.trap_sa + c, t);
+__device__ __forceinline__ void scan_fast(const World& W, const View& v, const Scratch& S, uint4 e, uint64_t gidx,
+                                          unsigned long long* counts, ScanOut& o) {
+  o.pa = nullptr; o.pd = nullptr; o.qn = false; o.qd = false;
+  const uint32_t lane = threadIdx.x & 31;
+  const Dec d = decode_fast(v.T, W.page_state, S, e, gidx, lane);
+  const uint32_t f = d.f;
+  if (!f) return;
+  const uint32_t c = d.c, sid = f & LF_S;
+  if (MPSF_ABLATE & 32) { if (sid == 99) atomicOr(S.ctrl + C_ERR, 1u); return; }
+  if (kStaged) atomicAdd(v.counts + c * NSCEN + sid, 1u);
+  else atomicAdd(counts + (uint64_t)c * NSCEN + sid, 1ull);
+  const bool sa = (d.cw >> 18) & 1u;
+  if (f & LF_TRAP) {
+    const unsigned long long t = (gidx << 8) | (unsigned long long)sid;
+    if (kStaged) smin64(sa ? v.trap_sa + c : v.trap_mps, t);
+    else min64(sa ? S.trap_sa + c : S.trap_mps, t);
     return;
   }
-  const uint32_t ok = ok32_of(r.repl, gidx);
-  const bool serv = s_serviceable(r.s);
-  if (s_parse(r.s) || (!serv && !(P.flags & MPSF_PF_ISOLATION))) {   // fatal report (pipeline.py:168-182)
-    const unsigned long long t = ((unsigned long long)ok << 8) | (unsigned long long)r.s;
-    if (r.sa) { if (kStaged) smin64(v.ft_sa + c, t); else min64(S.ft_sa + c, t); }
-    else if (r.ceng == 1) { if (kStaged) smin64(v.ft_ce + c, t); else min64(S.ft_ce + c, t); }
-    else min64(S.ft_gr, t);
-  } else if (!serv) {                                                // isolation-eligible (pipeline.py:177-179)
+  const uint32_t ok = ((f & LF_REPL) ? 0u : 0x80000000u) | (uint32_t)gidx;
+  if (f & LF_FATAL) {                                                // fatal report (pipeline.py:168-182)
+    const unsigned long long t = ((unsigned long long)ok << 8) | (unsigned long long)sid;
+    const uint32_t ceng = (d.cw >> 16) & 3u;
+    if (kStaged) smin64(sa ? v.ft_sa + c : (ceng == 1 ? v.ft_ce + c : v.ft_gr), t);
+    else min64(sa ? S.ft_sa + c : (ceng == 1 ? S.ft_ce + c : S.ft_gr), t);
+  }
+  const uint32_t page = (uint32_t)(d.va >> 12);
+  if (f & LF_ELIG) {                                                 // isolation-eligible (pipeline.py:177-179)
     // per-client minimum: iso1 unmapped / iso2 managed / iso3 external (per-warp smem copies:
     // a warp's indices only grow, so each copy takes one atomic per client and mechanism)
-    const int m = !r.at.in_range ? 0 : (r.at.kind == 0 ? 1 : 2);
-    if (kStaged) smin32(v.iso + ((uint32_t)m * W.n_clients + c) * 32 + (threadIdx.x >> 5), ok);
+    const uint32_t m = (f >> LF_M_SH) & 3u;
+    if (kStaged) smin32(v.iso + (m * W.n_clients + c) * 32 + (threadIdx.x >> 5), ok);
     else min32((m == 0 ? S.iso1 : (m == 1 ? S.iso2 : S.iso3)) + c, ok);
-    if (!r.at.in_range) {
-      if (r.at.guard) {
-        if (kStaged) smin32(v.nr0 + r.at.ridx, ok); else min32(S.nr0 + r.at.ridx, ok);
-      } else if (!(MPSF_ABLATE & 1) && !hash_min(S.hnr, v.used + 1, nr_key(c, 0, r.va >> 12), ok)) {
-        atomicOr(S.ctrl + C_OVF, 1u);
-      }
+    if (d.guard) {
+      if (kStaged) smin32(v.nr0 + d.ridx, ok); else min32(S.nr0 + d.ridx, ok);
+    } else if (!d.inr) {
+      o.qn = !(MPSF_ABLATE & 1);
+      o.kn = nr_key(c, 0, d.va >> 12);
+      o.vn = ok;
     } else {
-      if (r.at.kind != 0) {
-        if (kStaged) smin32(v.ext + r.at.ridx, ok); else min32(S.ext + r.at.ridx, ok);
-      }
+      if (m == 2) { if (kStaged) smin32(v.ext + d.ridx, ok); else min32(S.ext + d.ridx, ok); }
       // first eligible record per in-range page: the epoch-1 first-isolation key of a client
       // released before the drain (trap / dead at start), so that case needs no extra pass
-      if (S.nrall && !(MPSF_ABLATE & 2)) min32(S.nrall + r.at.slot, ok);
+      if (S.nrall && !(MPSF_ABLATE & 2)) { o.pa = S.nrall + d.slot; o.va = ok; }
     }
   }
-  if (r.kind == 0 && r.repl) {                                       // dedup insert (rule C2)
-    const uint32_t val = ((uint32_t)gidx << 3) | r.group;
-    bool to_hash = !(r.at.in_range || r.at.guard);
-    if (MPSF_ABLATE & 4) {
-      to_hash = to_hash && !(MPSF_ABLATE & 1);
-    } else if (!to_hash && W.dd_groups != 1) {
-      // one slot per (page, group): min with a load pre-check (hot slots: most records skip)
-      min32(S.dd + dd_slot(W, r), val);
-    } else if (!to_hash) {
-      uint32_t* slot = S.dd + dd_slot(W, r);
-      uint32_t cur = __ldcg(slot);
-      while (true) {
-        if (cur == EMPTY32) {
-          const uint32_t prev = atomicCAS(slot, EMPTY32, val);
-          if (prev == EMPTY32) break;
-          cur = prev;
-          continue;
-        }
-        if ((cur & 7u) == r.group) { if (cur > val) atomicMin(slot, val); break; }
-        to_hash = true;
-        break;
-      }
+  if ((f & LF_DD) && !(MPSF_ABLATE & 4)) {                           // dedup insert (rule C2)
+    const uint32_t group = (f >> LF_GROUP_SH) & 7u;
+    o.kd = dedup_key(c, (int)(e.w & 0xFF), (int)sid, d.va >> 12);
+    if (d.inr || d.guard) {
+      o.pd = S.dd + (W.dd_groups == 1 ? d.slot : d.slot * W.dd_groups + group);
+      o.vd = ((uint32_t)gidx << 3) | group;
+    } else {
+      o.qd = !(MPSF_ABLATE & 1);
+      o.vdh = (uint32_t)gidx;
     }
-    if (MPSF_ABLATE & 1) to_hash = false;
-    if (to_hash && !hash_min(S.hdd, v.used, dedup_key(c, r.eng, r.s, r.va >> 12), (uint32_t)gidx))
-      atomicOr(S.ctrl + C_OVF, 1u);
+  }
+  (void)page;
+}
+
+// Claimed-slot dedup (sparse worlds): first claim wins the page for its group; a record of
+// another group of the same page goes to the hash.
+__device__ __forceinline__ void claim_resolve(const Scratch& S, uint32_t* used, uint32_t* slot, uint32_t val,
+                                              uint32_t cur, unsigned long long key) {
+  while (true) {
+    if (cur == EMPTY32) {
+      const uint32_t prev = atomicCAS(slot, EMPTY32, val);
+      if (prev == EMPTY32) return;
+      cur = prev;
+      continue;
+    }
+    if ((cur & 7u) == (val & 7u)) { if (cur > val) atomicMin(slot, val); return; }
+    if (!hash_min(S.hdd, used, key, val >> 3)) atomicOr(S.ctrl + C_OVF, 1u);
+    return;
+  }
+}
+
+// Deferred hash ops: push (warp-collective), drained 32 at a time.
+__device__ __forceinline__ void q_push(QOp* q, uint32_t& cnt, bool has, unsigned long long key, uint32_t val,
+                                       uint32_t tab, const Scratch& S, uint32_t* used) {
+  const uint32_t lane = threadIdx.x & 31;
+  const unsigned m = __ballot_sync(0xFFFFFFFFu, has);
+  if (!m) return;
+  if (has) {
+    QOp x; x.key = key; x.val = val; x.tab = tab;
+    q[cnt + __popc(m & ((1u << lane) - 1u))] = x;
+  }
+  cnt += __popc(m);
+  if (cnt >= 32) {
+    __syncwarp();
+    const QOp x = q[cnt - 32 + lane];
+    const Hash& h = x.tab ? S.hnr : S.hdd;
+    if (!hash_min(h, used + x.tab, x.key, x.val)) atomicOr(S.ctrl + C_OVF, 1u);
+    cnt -= 32;
+    __syncwarp();
+  }
+}
+
+__device__ __forceinline__ void q_drain(QOp* q, uint32_t cnt, const Scratch& S, uint32_t* used) {
+  __syncwarp();
+  const uint32_t lane = threadIdx.x & 31;
+  if (lane < cnt) {
+    const QOp x = q[lane];
+    const Hash& h = x.tab ? S.hnr : S.hdd;
+    if (!hash_min(h, used + x.tab, x.key, x.val)) atomicOr(S.ctrl + C_OVF, 1u);
   }
 }
 
@@ -483,8 +616,12 @@ __device__ __forceinline__ void flush_minima(const World& W, const Scratch& S, c
     for (int k = 0; k < 32; ++k) m = min(m, w[k]);
     uint32_t* g = (i < C ? S.iso1 : (i < 2 * C ? S.iso2 : S.iso3)) + (i % C);
     if (m != EMPTY32) atomicMin(g, m);
-    const unsigned long long t = v.ft_ce[i];      // c64 = [ft_ce | ft_sa | trap_sa]
+    const unsigned long long t = v.ft_ce[i];      // c64 = [ft_ce | ft_sa | trap_sa | ft_gr | trap_mps]
     if (t != EMPTY64) atomicMin(i < C ? S.ft_ce + i : (i < 2 * C ? S.ft_sa + (i - C) : S.trap_sa + (i - 2 * C)), t);
+  }
+  if (threadIdx.x < 2) {
+    const unsigned long long t = v.ft_ce[3 * C + threadIdx.x];
+    if (t != EMPTY64) atomicMin(threadIdx.x ? S.trap_mps : S.ft_gr, t);
   }
   for (uint32_t i = threadIdx.x; i < R; i += blockDim.x) {
     if (v.ext[i] != EMPTY32) atomicMin(S.ext + i, v.ext[i]);
@@ -499,12 +636,36 @@ __global__ void __launch_bounds__(BLOCK, 1) k_scan(World W, Scratch S, const mps
                                                    uint32_t* __restrict__ count_part) {
   extern __shared__ __align__(128) uint8_t smem[];
   const Layout L = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, false);
-  const View v = setup<kStaged>(smem, L, W, S, true, false);
-  wstream_init(smem, L);
+  const View v = setup<kStaged>(smem, L, W, S, true, false, P.flags & MPSF_PF_ISOLATION);
   __syncthreads();
-  warp_stream(smem, L, in, n, [&](uint4 e, uint64_t i) {
-    scan_entry<kStaged>(W, v, S, P, e, P.base_index + i, counts);
+  QOp* q = reinterpret_cast<QOp*>(smem + L.queue) + (threadIdx.x >> 5) * QCAP;
+  uint32_t qn = 0;
+  const bool sparse = W.dd_groups == 1;
+  ldg_stream(in, n, [&](uint4 e0, uint64_t i0, bool ok0, uint4 e1, uint64_t i1, bool ok1) {
+    ScanOut o0, o1;
+    o0.pa = o0.pd = o1.pa = o1.pd = nullptr;
+    o0.qn = o0.qd = o1.qn = o1.qd = false;
+    if (MPSF_ABLATE & 64) { if (e0.x == 0x12345 && e1.y == 0x777) atomicOr(S.ctrl + C_ERR, 1u); return; }
+    if (ok0) scan_fast<kStaged>(W, v, S, e0, P.base_index + i0, counts, o0);
+    if (ok1) scan_fast<kStaged>(W, v, S, e1, P.base_index + i1, counts, o1);
+    // the L2 pre-check loads of both entries in flight together
+    const uint32_t ra0 = o0.pa ? __ldcg(o0.pa) : 0u, rd0 = o0.pd ? __ldcg(o0.pd) : 0u;
+    const uint32_t ra1 = o1.pa ? __ldcg(o1.pa) : 0u, rd1 = o1.pd ? __ldcg(o1.pd) : 0u;
+    if (o0.pa && ra0 > o0.va) atomicMin(o0.pa, o0.va);
+    if (o1.pa && ra1 > o1.va) atomicMin(o1.pa, o1.va);
+    if (!sparse) {
+      if (o0.pd && rd0 > o0.vd) atomicMin(o0.pd, o0.vd);
+      if (o1.pd && rd1 > o1.vd) atomicMin(o1.pd, o1.vd);
+    } else {
+      if (o0.pd) claim_resolve(S, v.used, o0.pd, o0.vd, rd0, o0.kd);
+      if (o1.pd) claim_resolve(S, v.used, o1.pd, o1.vd, rd1, o1.kd);
+    }
+    q_push(q, qn, o0.qn, o0.kn, o0.vn, 1, S, v.used);
+    q_push(q, qn, o0.qd, o0.kd, o0.vdh, 0, S, v.used);
+    q_push(q, qn, o1.qn, o1.kn, o1.vn, 1, S, v.used);
+    q_push(q, qn, o1.qd, o1.kd, o1.vdh, 0, S, v.used);
   });
+  q_drain(q, qn, S, v.used);
   if (kStaged) {
     __syncthreads();
     uint32_t* part = count_part + (uint64_t)blockIdx.x * NSCEN * W.n_clients;
@@ -645,7 +806,7 @@ __device__ __forceinline__ uint32_t nr_lookup(const Scratch& S, const Rec& r, bo
 template <bool kStaged, int kStage>
 __device__ __forceinline__ void general_entry(const World& W, const View& v, const Scratch& S, const Params& P,
                                               uint4 e, uint64_t gidx) {
-  const Rec r = decode<kStaged>(W, v, S, e, gidx);
+  const Rec r = to_rec(decode_fast(v.T, W.page_state, S, e, gidx, threadIdx.x & 31), e);
   if (!r.valid || r.kind != 0 || s_serviceable(r.s)) return;      // eligible translation records only
   const long long rel = v.cst[r.c].rel;
   const uint32_t ok = ok32_of(r.repl, gidx);
@@ -680,11 +841,11 @@ __global__ void __launch_bounds__(BLOCK, 1) k_general(World W, Scratch S, const 
   if (__ldcg(S.ctrl + C_PATH) == 0) return;
   extern __shared__ __align__(128) uint8_t smem[];
   const Layout L = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, true);
-  const View v = setup<kStaged>(smem, L, W, S, false, true);
-  wstream_init(smem, L);
+  const View v = setup<kStaged>(smem, L, W, S, false, true, P.flags & MPSF_PF_ISOLATION);
   __syncthreads();
-  warp_stream(smem, L, in, n, [&](uint4 e, uint64_t i) {
-    general_entry<kStaged, kStage>(W, v, S, P, e, P.base_index + i);
+  ldg_stream(in, n, [&](uint4 e0, uint64_t i0, bool ok0, uint4 e1, uint64_t i1, bool ok1) {
+    if (ok0) general_entry<kStaged, kStage>(W, v, S, P, e0, P.base_index + i0);
+    if (ok1) general_entry<kStaged, kStage>(W, v, S, P, e1, P.base_index + i1);
   });
 }
 
@@ -724,7 +885,7 @@ __device__ __forceinline__ void finalize_entry(const World& W, const View& v, co
                                                unsigned long long& key) {
   o.rid = NO_RID; o.scenario = 0xFF; o.verdict = 0; o.client = 0xFFFF;
   canc = false; rep = false; key = 0;
-  const Rec r = decode<kStaged>(W, v, S, e, gidx);
+  const Rec r = to_rec(decode_fast(v.T, W.page_state, S, e, gidx, threadIdx.x & 31), e);
   if (!r.valid) return;
   const CState cs = v.cst[r.c];
   o.scenario = (uint8_t)r.s;
@@ -778,7 +939,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const
   extern __shared__ __align__(128) uint8_t smem[];
   if (__ldcg(S.ctrl + C_ERR) != 0) return;
   const Layout L = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, true);
-  const View v = setup<kStaged>(smem, L, W, S, false, true);
+  const View v = setup<kStaged>(smem, L, W, S, false, true, P.flags & MPSF_PF_ISOLATION);
   Pipe p = pipe_init(smem, L);
   const Globals G = *S.glob;
   __syncthreads();

@@ -272,6 +272,7 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   for (uint32_t i = 0; i < nr; ++i) {
     const mpsf_range_entry& r = ranges[i];
     if (r.client >= ncl || r.base >= r.end || (r.base & 0xFFF) || (r.end & 0xFFF)) return MPSF_E_WORLD;
+    if (r.kind > 1 || r.lifecycle > 1 || r.migratable > 1) return MPSF_E_WORLD;   // RangeKind / Lifecycle / bool
     if (i > 0) {
       const mpsf_range_entry& p = ranges[i - 1];
       if (p.client > r.client) return MPSF_E_WORLD;
@@ -337,7 +338,8 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   const size_t o_soa = a256(o_cl + sizeof(mpsf_client_entry) * ncl);
   const size_t o_skip = a256(o_soa + 5ull * 4 * nr);
   const size_t o_cinfo = a256(o_skip + 2ull * SKIP_K * ncl);
-  const size_t o_chan = a256(o_cinfo + 3ull * 4 * ncl);
+  const size_t o_cinfo4 = a256(o_cinfo + 3ull * 4 * ncl);
+  const size_t o_chan = a256(o_cinfo4 + 16ull * ncl);
   const size_t total = a256(o_chan + 4ull * nch) + 256;
   cudaFree(c->d_world);
   c->d_world = nullptr;
@@ -363,6 +365,9 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
     CK(cudaMemcpy(cinfo, crange.data(), 4ull * ncl, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(cinfo + ncl, cspan.data(), 4ull * ncl, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(cinfo + 2ull * ncl, cshift.data(), 4ull * ncl, cudaMemcpyHostToDevice));
+    std::vector<uint32_t> c4(4ull * ncl, 0);
+    for (uint32_t i = 0; i < ncl; ++i) { c4[4 * i] = crange[i]; c4[4 * i + 1] = cspan[i]; c4[4 * i + 2] = cshift[i]; }
+    CK(cudaMemcpy(b + o_cinfo4, c4.data(), 16ull * ncl, cudaMemcpyHostToDevice));
   }
   if (nch) CK(cudaMemcpy(b + o_chan, chan.data(), 4ull * nch, cudaMemcpyHostToDevice));
   World& W = c->W;
@@ -380,6 +385,7 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   W.crange = cinfo;
   W.cspan = cinfo + ncl;
   W.cshift = cinfo + 2ull * ncl;
+  W.cinfo4 = reinterpret_cast<const uint4*>(b + o_cinfo4);
   W.chan = reinterpret_cast<const uint32_t*>(b + o_chan);
   W.n_ranges = nr;
   W.n_clients = ncl;

@@ -79,6 +79,7 @@ struct World {
   const uint32_t* cspan;            // [C] first page of the client's span
   const uint32_t* cshift;           // [C] log2 pages per skip slot
   const uint32_t* chan;             // [nch] client | engine << 16 | standalone << 18 | valid << 31
+  const uint4* cinfo4;              // [C] (crange, cspan, cshift, 0): one 16-byte row per client
   uint32_t n_ranges, n_clients, n_channels, world_flags;
   uint64_t n_pages;
   uint32_t has_mps;
@@ -146,6 +147,51 @@ __device__ __forceinline__ int classify(int eng, int acc, bool has, int kind, in
   return oob;                                                 // would-hit fallthrough
 }
 
+// ---- classification LUT ---------------------------------------------------------------------
+// Every decode outcome of an entry maps to one 32-bit word built once per CTA from classify():
+// translation entries index ((eng * 3 + acc) * 16 + rcls) * 8 + st with rcls = kind |
+// lifecycle << 1 | migratable << 2 for an attributed range (8: none, st = 0); the other entry
+// kinds index LUT_XK + kind.  The word carries the scenario id, the dedup group and every
+// predicate the passes branch on, so the per-entry path is one lookup instead of a tree.
+constexpr int LUT_XK = 9 * 16 * 8;
+constexpr int LUT_N = LUT_XK + 16;
+enum : uint32_t {
+  LF_S = 31u,                 // scenario id bits [4:0]
+  LF_GROUP_SH = 5,            // dedup group bits [7:5]
+  LF_REPL = 1u << 8,          // replayable buffer (faults.py:48, pipeline.py:116-123)
+  LF_DD = 1u << 9,            // replayable translation record: dedup candidate (rule C2)
+  LF_SERV = 1u << 10,         // serviceable (benign)
+  LF_ELIG = 1u << 11,         // isolation-eligible (isolation on, not serviceable)
+  LF_FATAL = 1u << 12,        // fatal report (parse-time, or not serviceable with isolation off)
+  LF_TRAP = 1u << 13,         // SM trap (raise_sm_trap, pipeline.py:151-155)
+  LF_BAD = 1u << 14,          // not a known entry kind
+  LF_M_SH = 15,               // bits [16:15]: 0 no range, 1 managed range, 2 external range
+  LF_XKIND = 1u << 17,        // not a translation entry
+  LF_VALID = 1u << 31
+};
+
+__device__ __forceinline__ uint32_t lut_word(int idx, bool isolation) {
+  if (idx >= LUT_XK) {
+    const int k = idx - LUT_XK;
+    if (k >= 1 && k <= 5) return LF_VALID | LF_XKIND | (uint32_t)(23 + k - 1) | LF_REPL | LF_FATAL;
+    if (k >= 8 && k <= 12) return LF_VALID | LF_XKIND | (uint32_t)(18 + k - 8) | LF_TRAP;
+    return LF_VALID | LF_XKIND | LF_BAD;
+  }
+  const int st = idx & 7, rcls = (idx >> 3) & 15, ea = idx >> 7;
+  const int eng = ea / 3, acc = ea % 3;
+  if (rcls > 8) return LF_VALID | LF_BAD;
+  const bool has = rcls < 8;
+  const int kind = rcls & 1, lc = (rcls >> 1) & 1, mig = (rcls >> 2) & 1;
+  const int s = classify(eng, acc, has, kind, lc, mig, has ? (uint32_t)st : 0u);
+  uint32_t group;
+  if (eng == 0 && acc != 2) group = (acc == 1 && s >= 1 && s <= 3) ? 1u : 0u;
+  else group = eng == 0 ? 2u : (uint32_t)(2 + eng);
+  const bool repl = s_replayable(s), serv = s_serviceable(s);
+  const uint32_t m = !has ? 0u : (kind == 0 ? 1u : 2u);
+  return LF_VALID | (uint32_t)s | (group << LF_GROUP_SH) | (repl ? (LF_REPL | LF_DD) : 0u) |
+         (serv ? LF_SERV : (isolation ? LF_ELIG : LF_FATAL)) | (m << LF_M_SH);
+}
+
 struct Attr {
   int ridx;        // range index (in range or owner of the guard page), -1 if wild
   bool in_range;
@@ -163,6 +209,19 @@ struct Tables {
   const uint16_t* skip;
   const uint32_t *crange, *cspan, *cshift, *chan;
   uint32_t rep_client, rep_chan;   // 32 when replicated per lane, else 0
+  const uint4* cinfo;              // [C] or [C][32] rows (crange, cspan, cshift, 0)
+  const uint32_t* lut;             // [LUT_N] classification words (always shared memory)
+  uint32_t n_channels;
+};
+
+// Decoded entry of the lean path (decode_fast).
+struct Dec {
+  uint32_t f;       // LUT word; 0 when the entry is skipped (valid flag clear) or an error was raised
+  uint32_t c, cw;   // client, channel word
+  uint32_t slot;    // page slot (in range or the guard page)
+  uint32_t ridx;    // range index (in range / guard owner), NO_RID when wild
+  bool inr, guard;
+  uint64_t va;
 };
 
 __device__ __forceinline__ uint32_t rep_load(const uint32_t* a, uint32_t i, uint32_t rep, uint32_t lane) {
