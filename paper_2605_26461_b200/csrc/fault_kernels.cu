@@ -86,37 +86,34 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 __host__ __device__ inline uint32_t al16(uint64_t x) { return (uint32_t)((x + 15) & ~uint64_t(15)); }
 
 struct Layout {
-  uint32_t tiles, bars, wbars, tids, tot, pre;
+  uint32_t tiles, bars, tids, tot, pre;
   uint32_t lut, cinfo, queue;
-  uint32_t pg_base, pg_end, poff, rattr, rrid, skip, crange, cspan, cshift, chan;
+  uint32_t pg_base, pg_end, poff, rattr, rrid, skip, chan;
   uint32_t c64, iso, r32, counts, used, cstate, total;
   uint32_t rep_chan;
 };
 
-// kStaged: the interval table (page-granular SoA + skip table, per-client words and the
-// channel table replicated per bank) and the pass-1 caches live in smem
-__host__ __device__ inline Layout make_layout(uint32_t nr, uint32_t nc, uint32_t nch, bool staged, bool fin) {
+// kStaged: the interval table (page-granular SoA + skip tables, the client rows and the
+// channel table replicated per bank) and the pass-1 caches live in smem.  The LUT always does.
+__host__ __device__ inline Layout make_layout(const World& W, bool staged, bool fin) {
+  const uint32_t nr = W.n_ranges + 1, nc = W.n_clients, nch = W.n_channels + 1;
   Layout L;
   uint32_t o = 0;
   L.tiles = o; if (fin) o += NBUF * TILE_BYTES;   // finalize: TMA tile ring
   L.bars = o; o += 4 * 8 * NBUF;          // full, empty, done, pref per buffer
-  L.wbars = o;
   L.tids = o; o += al16(4 * NBUF);
   L.tot = o; o += 8 * 32 * NBUF;          // per buffer, per worker warp: (cancel, dedup) counts
   L.pre = o; o += 8 * 32 * NBUF;          // per buffer, per worker warp: exclusive output offsets
-  L.rep_chan = (staged && nch <= 256) ? 32u : 0u;
+  L.rep_chan = (staged && nch <= 257) ? 32u : 0u;
   L.lut = o; o += 4 * LUT_N;
-  L.cinfo = o; if (staged) o += al16(512ull * nc);
   L.queue = o; if (!fin) o += WARPS * QCAP * 16;
+  L.cinfo = o; if (staged) o += al16(512ull * nc);
   L.pg_base = o; if (staged) o += al16(4ull * nr);
   L.pg_end = o; if (staged) o += al16(4ull * nr);
   L.poff = o; if (staged) o += al16(4ull * nr);
   L.rattr = o; if (staged) o += al16(4ull * nr);
   L.rrid = o; if (staged && fin) o += al16(4ull * nr);
-  L.skip = o; if (staged) o += al16(2ull * SKIP_K * nc);
-  L.crange = o; if (staged) o += al16(128ull * nc);
-  L.cspan = o; if (staged) o += al16(128ull * nc);
-  L.cshift = o; if (staged) o += al16(128ull * nc);
+  L.skip = o; if (staged) o += al16(2ull * (W.n_skip + 1));
   L.chan = o; if (staged) o += al16(4ull * nch * (L.rep_chan ? 32 : 1));
   L.c64 = o; if (staged && !fin) o += al16(24ull * nc + 16);
   L.iso = o; if (staged && !fin) o += al16(3ull * 128 * nc);
@@ -131,9 +128,9 @@ __host__ __device__ inline Layout make_layout(uint32_t nr, uint32_t nc, uint32_t
 // Block-wide view of the world tables (smem when staged, else global) and pass-1 caches.
 struct View {
   Tables T;
-  unsigned long long *ft_ce, *ft_sa, *trap_sa;   // pass-1 caches (or null)
+  unsigned long long *ft_ce, *ft_sa, *trap_sa;   // pass-1 caches (or the global minima)
   unsigned long long *ft_gr, *trap_mps;
-  uint32_t* iso;                                  // [3][C][32] per-lane copies (or null)
+  uint32_t* iso;                                  // [3][C][32] per-warp copies (or null)
   uint32_t *ext, *nr0, *counts;
   uint32_t* used;                                 // [2] claimed hash slots (dd, nr)
   const CState* cst;
@@ -144,51 +141,44 @@ __device__ View setup(uint8_t* sm, const Layout& L, const World& W, const Scratc
                       bool isolation_flag) {
   View v;
   const uint32_t tid = threadIdx.x, nb = blockDim.x;
-  const uint32_t R = W.n_ranges, C = W.n_clients;
+  const uint32_t R1 = W.n_ranges + 1, C = W.n_clients;
   if (kStaged) {
     uint32_t* pb = reinterpret_cast<uint32_t*>(sm + L.pg_base);
     uint32_t* pe = reinterpret_cast<uint32_t*>(sm + L.pg_end);
     uint32_t* po = reinterpret_cast<uint32_t*>(sm + L.poff);
     uint32_t* ra = reinterpret_cast<uint32_t*>(sm + L.rattr);
     uint32_t* rr = reinterpret_cast<uint32_t*>(sm + L.rrid);
-    for (uint32_t i = tid; i < R; i += nb) {
+    for (uint32_t i = tid; i < R1; i += nb) {
       pb[i] = __ldg(W.pg_base + i); pe[i] = __ldg(W.pg_end + i);
       po[i] = __ldg(W.poff + i); ra[i] = __ldg(W.rattr + i);
       if (fin) rr[i] = __ldg(W.rrid + i);
     }
     uint16_t* sk = reinterpret_cast<uint16_t*>(sm + L.skip);
-    for (uint32_t i = tid; i < SKIP_K * C; i += nb) sk[i] = __ldg(W.skip + i);
-    uint32_t* cr = reinterpret_cast<uint32_t*>(sm + L.crange);
-    uint32_t* cs = reinterpret_cast<uint32_t*>(sm + L.cspan);
-    uint32_t* ch = reinterpret_cast<uint32_t*>(sm + L.cshift);
-    for (uint32_t i = tid; i < 32 * C; i += nb) {
-      cr[i] = __ldg(W.crange + i / 32); cs[i] = __ldg(W.cspan + i / 32); ch[i] = __ldg(W.cshift + i / 32);
-    }
+    for (uint32_t i = tid; i <= W.n_skip; i += nb) sk[i] = __ldg(W.skip + i);
     uint32_t* cn = reinterpret_cast<uint32_t*>(sm + L.chan);
     const uint32_t rc = L.rep_chan ? 32u : 1u;
-    for (uint32_t i = tid; i < rc * W.n_channels; i += nb) cn[i] = __ldg(W.chan + i / rc);
+    for (uint32_t i = tid; i < rc * (W.n_channels + 1); i += nb) cn[i] = __ldg(W.chan + i / rc);
     uint4* ci = reinterpret_cast<uint4*>(sm + L.cinfo);
     for (uint32_t i = tid; i < 32 * C; i += nb) ci[i] = __ldg(W.cinfo4 + i / 32);
     v.T.cinfo = ci;
     v.T.pg_base = pb; v.T.pg_end = pe; v.T.poff = po; v.T.rattr = ra; v.T.rrid = fin ? rr : W.rrid;
-    v.T.skip = sk; v.T.crange = cr; v.T.cspan = cs; v.T.cshift = ch; v.T.chan = cn;
+    v.T.skip = sk; v.T.chan = cn;
     v.T.rep_client = 32; v.T.rep_chan = L.rep_chan;
   } else {
     v.T.pg_base = W.pg_base; v.T.pg_end = W.pg_end; v.T.poff = W.poff; v.T.rattr = W.rattr; v.T.rrid = W.rrid;
-    v.T.skip = W.skip; v.T.crange = W.crange; v.T.cspan = W.cspan; v.T.cshift = W.cshift; v.T.chan = W.chan;
+    v.T.skip = W.skip; v.T.chan = W.chan;
     v.T.rep_client = 0; v.T.rep_chan = 0;
     v.T.cinfo = W.cinfo4;
   }
-  {
-    uint32_t* lut = reinterpret_cast<uint32_t*>(sm + L.lut);
-    const bool iso = isolation_flag;
-    for (uint32_t i = tid; i < (uint32_t)LUT_N; i += nb) lut[i] = lut_word((int)i, iso);
-    v.T.lut = lut;
-    v.T.n_channels = W.n_channels;
-  }
-  v.ft_ce = v.ft_sa = v.trap_sa = nullptr;
+  uint32_t* lut = reinterpret_cast<uint32_t*>(sm + L.lut);
+  for (uint32_t i = tid; i < (uint32_t)LUT_N; i += nb) lut[i] = lut_word((int)i, isolation_flag);
+  v.T.lut = lut;
+  v.T.n_channels = W.n_channels;
+  v.T.exact1 = W.exact1;
+  v.ft_ce = S.ft_ce; v.ft_sa = S.ft_sa; v.trap_sa = S.trap_sa;
   v.ft_gr = S.ft_gr; v.trap_mps = S.trap_mps;
-  v.iso = v.ext = v.nr0 = v.counts = nullptr;
+  v.iso = nullptr;
+  v.ext = S.ext; v.nr0 = S.nr0; v.counts = nullptr;
   v.used = S.ctrl + C_HASH_DD;                    // C_HASH_NR follows it
   v.cst = S.cstate;
   if (kStaged && scan) {
@@ -200,8 +190,8 @@ __device__ View setup(uint8_t* sm, const Layout& L, const World& W, const Scratc
     for (uint32_t i = tid; i < 3 * 32 * C; i += nb) iso[i] = EMPTY32;
     v.iso = iso;
     uint32_t* r32 = reinterpret_cast<uint32_t*>(sm + L.r32);
-    for (uint32_t i = tid; i < 2 * R; i += nb) r32[i] = EMPTY32;
-    v.ext = r32; v.nr0 = r32 + R;
+    for (uint32_t i = tid; i < 2 * R1; i += nb) r32[i] = EMPTY32;
+    v.ext = r32; v.nr0 = r32 + R1;
     uint32_t* cnt = reinterpret_cast<uint32_t*>(sm + L.counts);
     for (uint32_t i = tid; i < NSCEN * C; i += nb) cnt[i] = 0;
     v.counts = cnt;
@@ -222,7 +212,66 @@ __device__ __forceinline__ void raise_err(const Scratch& S, uint32_t bit, uint64
   atomicMin(S.err_idx, (unsigned long long)gidx);
 }
 
-// Decoded + classified view of one entry, shared by every pass.
+// Lean decode shared by the passes: channel word, client row, skip-table attribution
+// (MemoryModel.range_at, memory.py:233-237: the unique range of the client with
+// base <= va < end, plus the guard page right after it) and one LUT word
+// (faults.classify, faults.py:134-171).  Entries with the valid flag clear decode to f = 0;
+// malformed entries raise the error bits the host maps onto the reference's exceptions and
+// also give 0: no channel (NoChannelAttribution, errors.py:59-60), engine / access out of
+// range, engine not the channel's (KindMismatch, errors.py:36-37), VA beyond 2^53, unknown
+// entry kind.
+__device__ __forceinline__ Dec decode_fast(const Tables& T, const uint8_t* __restrict__ page_state,
+                                           const Scratch& S, uint4 e, uint64_t gidx, uint32_t lane) {
+  Dec d;
+  d.va = (uint64_t)e.x | ((uint64_t)e.y << 32);
+  const uint32_t w3 = e.w;
+  const uint32_t eng = w3 & 0xFF, acc = (w3 >> 8) & 0xFF, ek = (w3 >> 16) & 0xFF;
+  const bool valid = (w3 >> 24) & MPSF_ENTRY_VALID;
+  const bool chok = e.z < T.n_channels;
+  const uint32_t cw = rep_load(T.chan, chok ? e.z : T.n_channels, T.rep_chan, lane);   // row nch: invalid
+  const uint32_t c = cw & 0xFFFFu, ceng = (cw >> 16) & 3u;
+  const bool k0 = ek == 0;
+  const uint4 ci = T.rep_client ? T.cinfo[c * 32 + lane] : T.cinfo[c];
+  const uint32_t lo = ci.x & 0xFFFFu, hi = ci.x >> 16;
+  const uint32_t page = (uint32_t)(d.va >> 12);
+  const bool look = k0 && lo != hi && d.va < VA_TABLE_LIMIT && page >= ci.y;
+  uint32_t j = (page - ci.y) >> (ci.z & 31u);
+  const uint32_t jmax = ci.z >> 8;
+  j = j < jmax ? j : jmax;
+  uint32_t k = T.skip[ci.w + j];
+  k += (k + 1 < hi && T.pg_base[k + 1] <= page) ? 1u : 0u;
+  if (!T.exact1) {
+    while (k + 1 < hi && T.pg_base[k + 1] <= page) ++k;
+  }
+  const uint32_t end = T.pg_end[k], base = T.pg_base[k];
+  d.inr = look && page < end;
+  d.guard = look && page == end;
+  d.slot = T.poff[k] + (page - base);
+  d.ridx = (d.inr || d.guard) ? k : NO_RID;
+  const uint32_t a = T.rattr[k];
+  const uint32_t ust = a >> 24;
+  uint32_t st = ust;
+  if (d.inr && ust == 0xFF) st = page_state[d.slot];
+  const uint32_t rcls = d.inr ? ((a & 1u) | ((a >> 7) & 2u) | ((a >> 14) & 4u)) : 8u;
+  st = d.inr ? (st & 7u) : 0u;
+  const uint32_t e3 = eng < 3 ? eng : 2u, a3 = acc < 3 ? acc : 2u;
+  const uint32_t idx = k0 ? ((e3 * 3 + a3) * 16 + rcls) * 8 + st : (uint32_t)LUT_XK + (ek < 16 ? ek : 15u);
+  const uint32_t f = T.lut[idx];
+  const bool bad = !(cw & CH_VALID) ||
+                   (k0 ? (eng > 2 || acc > 2 || eng != ceng || d.va >= VA_LIMIT) : (f & LF_BAD) != 0);
+  if (valid && bad) {
+    const uint32_t bit = !(cw & CH_VALID) ? EB_NO_CHANNEL
+                         : (!k0 || eng > 2 || acc > 2) ? EB_BAD_ENTRY
+                         : (eng != ceng ? EB_MISMATCH : EB_VA);
+    raise_err(S, bit, gidx);
+  }
+  d.f = (valid && !bad) ? f : 0u;
+  d.c = c;
+  d.cw = cw;
+  return d;
+}
+
+// Decoded + classified view of one entry (the general and finalize passes).
 struct Rec {
   bool valid;
   uint32_t c;       // client
@@ -230,124 +279,12 @@ struct Rec {
   int eng, kind;
   int s;            // scenario id
   uint64_t va;
-  Attr at;
   bool repl;        // replayable buffer
   uint32_t group;   // dedup group (replayable translation)
   bool sa;          // client is standalone
+  struct { int ridx; bool in_range, guard; uint32_t slot; int kind; } at;
 };
 
-template <bool kStaged>
-__device__ __forceinline__ Rec decode(const World& W, const View& v, const Scratch& S, uint4 e, uint64_t gidx) {
-  Rec r;
-  r.valid = false;
-  r.va = (uint64_t)e.x | ((uint64_t)e.y << 32);
-  const uint32_t w3 = e.w;
-  if (!(w3 >> 24 & MPSF_ENTRY_VALID)) return r;
-  const uint32_t ch = e.z;
-  const uint32_t lane = threadIdx.x & 31;
-  r.eng = (int)(w3 & 0xFF);
-  const int acc = (int)((w3 >> 8) & 0xFF);
-  r.kind = (int)((w3 >> 16) & 0xFF);
-  if (ch >= W.n_channels) { raise_err(S, EB_NO_CHANNEL, gidx); return r; }
-  const uint32_t cw = rep_load(v.T.chan, ch, v.T.rep_chan, lane);
-  if (!(cw & CH_VALID)) { raise_err(S, EB_NO_CHANNEL, gidx); return r; }
-  r.c = cw & 0xFFFFu;
-  r.ceng = (int)((cw >> 16) & 3u);
-  r.sa = (cw >> 18) & 1u;
-  r.group = 0;
-  r.at.ridx = -1; r.at.in_range = false; r.at.guard = false; r.at.rid = NO_RID;
-  if (r.kind == 0) {
-    if (r.eng > 2 || acc > 2) { raise_err(S, EB_BAD_ENTRY, gidx); return r; }
-    if (r.eng != r.ceng) { raise_err(S, EB_MISMATCH, gidx); return r; }
-    if (r.va >= VA_LIMIT) { raise_err(S, EB_VA, gidx); return r; }
-    r.at = attribute_pg(v.T, W.page_state, r.c, r.va, lane);
-    const bool has = r.at.in_range;
-    r.s = classify(r.eng, acc, has, r.at.kind, r.at.lifecycle, r.at.migratable, r.at.st);
-    r.repl = s_replayable(r.s);
-    if (r.eng == 0 && acc != 2) {
-      // an SM write classifies differently from an SM read of the same page exactly when it
-      // takes the access-mismatch branch (faults.py:154-160): ids 1..3 only come from there
-      r.group = (acc == 1 && r.s >= 1 && r.s <= 3) ? 1u : 0u;
-    } else {
-      r.group = r.eng == 0 ? 2u : (uint32_t)(2 + r.eng);
-    }
-  } else if (r.kind >= 1 && r.kind <= 5) {
-    r.s = 23 + r.kind - 1;
-    r.repl = true;
-  } else if (r.kind >= 8 && r.kind <= 12) {
-    r.s = 18 + r.kind - 8;
-    r.repl = false;
-  } else {
-    raise_err(S, EB_BAD_ENTRY, gidx);
-    return r;
-  }
-  r.valid = true;
-  return r;
-}
-
-// Rare path of decode_fast: raise the specific entry error (same checks, same order as decode).
-__device__ __noinline__ void entry_error(const Scratch& S, uint32_t cw, bool chok, uint4 e, uint64_t gidx) {
-  const uint32_t w3 = e.w, eng = w3 & 0xFF, acc = (w3 >> 8) & 0xFF, ek = (w3 >> 16) & 0xFF;
-  const uint64_t va = (uint64_t)e.x | ((uint64_t)e.y << 32);
-  if (!chok || !(cw & CH_VALID)) raise_err(S, EB_NO_CHANNEL, gidx);
-  else if (ek == 0 && (eng > 2 || acc > 2)) raise_err(S, EB_BAD_ENTRY, gidx);
-  else if (ek == 0 && eng != ((cw >> 16) & 3u)) raise_err(S, EB_MISMATCH, gidx);
-  else if (ek == 0 && va >= VA_LIMIT) raise_err(S, EB_VA, gidx);
-  else raise_err(S, EB_BAD_ENTRY, gidx);
-}
-
-// Lean decode shared by the passes: channel word, client row, skip-table attribution
-// (MemoryModel.range_at, memory.py:233-237) and one LUT word (faults.classify, faults.py:134-171).
-__device__ __forceinline__ Dec decode_fast(const Tables& T, const uint8_t* __restrict__ page_state,
-                                           const Scratch& S, uint4 e, uint64_t gidx, uint32_t lane) {
-  Dec d;
-  d.f = 0; d.c = 0; d.cw = 0; d.slot = 0; d.ridx = NO_RID; d.inr = false; d.guard = false;
-  d.va = (uint64_t)e.x | ((uint64_t)e.y << 32);
-  const uint32_t w3 = e.w;
-  if (!((w3 >> 24) & MPSF_ENTRY_VALID)) return d;
-  const uint32_t ch = e.z, eng = w3 & 0xFF, acc = (w3 >> 8) & 0xFF, ek = (w3 >> 16) & 0xFF;
-  const bool chok = ch < T.n_channels;
-  const uint32_t cw = chok ? rep_load(T.chan, ch, T.rep_chan, lane) : 0u;
-  const bool k0 = ek == 0;
-  const bool bad = !(cw & CH_VALID) ||
-                   (k0 ? (eng > 2 || acc > 2 || eng != ((cw >> 16) & 3u) || d.va >= VA_LIMIT)
-                       : (ek > 15 || (T.lut[LUT_XK + ek] & LF_BAD)));
-  if (bad) {
-    entry_error(S, cw, chok, e, gidx);
-    return d;
-  }
-  d.c = cw & 0xFFFFu;
-  d.cw = cw;
-  uint32_t idx = LUT_XK + ek;
-  if (k0) {
-    const uint4 ci = T.rep_client ? T.cinfo[d.c * 32 + lane] : T.cinfo[d.c];
-    const uint32_t lo = ci.x & 0xFFFFu, hi = ci.x >> 16;
-    const uint32_t page = (uint32_t)(d.va >> 12);
-    uint32_t rcls = 8, st = 0;
-    if (lo != hi && d.va < VA_TABLE_LIMIT && page >= ci.y) {
-      uint32_t j = (page - ci.y) >> ci.z;
-      j = j < (uint32_t)SKIP_K ? j : (uint32_t)(SKIP_K - 1);
-      uint32_t k = T.skip[d.c * SKIP_K + j];
-      while (k + 1 < hi && T.pg_base[k + 1] <= page) ++k;
-      const uint32_t end = T.pg_end[k], base = T.pg_base[k];
-      d.inr = page < end;
-      d.guard = page == end;
-      d.slot = T.poff[k] + (page - base);
-      if (d.inr || d.guard) d.ridx = k;
-      if (d.inr) {
-        const uint32_t a = T.rattr[k];
-        rcls = (a & 1u) | ((a >> 7) & 2u) | ((a >> 14) & 4u);
-        const uint32_t ust = a >> 24;
-        st = (ust != 0xFF ? ust : (uint32_t)page_state[d.slot]) & 7u;
-      }
-    }
-    idx = ((eng * 3 + acc) * 16 + rcls) * 8 + st;
-  }
-  d.f = T.lut[idx];
-  return d;
-}
-
-// The Rec view of a lean decode (for the passes still written against Rec).
 __device__ __forceinline__ Rec to_rec(const Dec& d, uint4 e) {
   Rec r;
   r.valid = d.f != 0;
@@ -364,11 +301,7 @@ __device__ __forceinline__ Rec to_rec(const Dec& d, uint4 e) {
   r.at.in_range = d.inr;
   r.at.guard = d.guard;
   r.at.slot = d.slot;
-  r.at.st = 0;
   r.at.kind = ((d.f >> LF_M_SH) & 3u) == 2u ? 1 : 0;
-  r.at.lifecycle = 0;
-  r.at.migratable = 1;
-  r.at.rid = NO_RID;
   return r;
 }
 
@@ -493,68 +426,74 @@ struct ScanOut {
   uint32_t* pa; uint32_t va;     // nrall precheck-min
   uint32_t* pd; uint32_t vd;     // dedup slot precheck-min / claim
   bool qn, qd;                   // deferred hash ops: NR key (hnr), dedup key (hdd)
-  unsigned long long kn, kd;
-  uint32_t vn, vdh;
+  uint32_t c, eng, sid;          // key material (hash ops, claim fallback)
+  uint64_t page;
 };
 
+__device__ __forceinline__ unsigned long long scan_dkey(const ScanOut& o) {
+  return dedup_key(o.c, (int)o.eng, (int)o.sid, o.page);
+}
+
+// Rare part of pass 1: SM traps and fatal reports (parse-time, or isolation off).
 template <bool kStaged>
-__device__ __forceinline__ void scan_fast(const World& W, const View& v, const Scratch& S, uint4 e, uint64_t gidx,
-                                          unsigned long long* counts, ScanOut& o) {
-  o.pa = nullptr; o.pd = nullptr; o.qn = false; o.qd = false;
-  const uint32_t lane = threadIdx.x & 31;
-  const Dec d = decode_fast(v.T, W.page_state, S, e, gidx, lane);
-  const uint32_t f = d.f;
-  if (!f) return;
-  const uint32_t c = d.c, sid = f & LF_S;
-  if (MPSF_ABLATE & 32) { if (sid == 99) atomicOr(S.ctrl + C_ERR, 1u); return; }
-  if (kStaged) atomicAdd(v.counts + c * NSCEN + sid, 1u);
-  else atomicAdd(counts + (uint64_t)c * NSCEN + sid, 1ull);
-  const bool sa = (d.cw >> 18) & 1u;
+__device__ __noinline__ void scan_fatal(const View& v, const Scratch& S, uint32_t f, uint32_t c, uint32_t cw,
+                                        uint64_t gidx) {
+  const uint32_t sid = f & LF_S;
+  const bool sa = (cw >> 18) & 1u;
   if (f & LF_TRAP) {
     const unsigned long long t = (gidx << 8) | (unsigned long long)sid;
     if (kStaged) smin64(sa ? v.trap_sa + c : v.trap_mps, t);
     else min64(sa ? S.trap_sa + c : S.trap_mps, t);
     return;
   }
+  // fatal report (pipeline.py:168-182): keyed by its drain position
   const uint32_t ok = ((f & LF_REPL) ? 0u : 0x80000000u) | (uint32_t)gidx;
-  if (f & LF_FATAL) {                                                // fatal report (pipeline.py:168-182)
-    const unsigned long long t = ((unsigned long long)ok << 8) | (unsigned long long)sid;
-    const uint32_t ceng = (d.cw >> 16) & 3u;
-    if (kStaged) smin64(sa ? v.ft_sa + c : (ceng == 1 ? v.ft_ce + c : v.ft_gr), t);
-    else min64(sa ? S.ft_sa + c : (ceng == 1 ? S.ft_ce + c : S.ft_gr), t);
+  const unsigned long long t = ((unsigned long long)ok << 8) | (unsigned long long)sid;
+  const uint32_t ceng = (cw >> 16) & 3u;
+  if (kStaged) smin64(sa ? v.ft_sa + c : (ceng == 1 ? v.ft_ce + c : v.ft_gr), t);
+  else min64(sa ? S.ft_sa + c : (ceng == 1 ? S.ft_ce + c : S.ft_gr), t);
+}
+
+template <bool kStaged>
+__device__ __forceinline__ void scan_fast(const World& W, const View& v, const Scratch& S, uint4 e, uint64_t gidx,
+                                          unsigned long long* counts, ScanOut& o) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const Dec d = decode_fast(v.T, W.page_state, S, e, gidx, lane);
+  const uint32_t f = d.f, c = d.c, sid = f & LF_S;
+  if (f) {
+    if (kStaged) atomicAdd(v.counts + c * NSCEN + sid, 1u);
+    else atomicAdd(counts + (uint64_t)c * NSCEN + sid, 1ull);
   }
-  const uint32_t page = (uint32_t)(d.va >> 12);
-  if (f & LF_ELIG) {                                                 // isolation-eligible (pipeline.py:177-179)
-    // per-client minimum: iso1 unmapped / iso2 managed / iso3 external (per-warp smem copies:
-    // a warp's indices only grow, so each copy takes one atomic per client and mechanism)
-    const uint32_t m = (f >> LF_M_SH) & 3u;
-    if (kStaged) smin32(v.iso + (m * W.n_clients + c) * 32 + (threadIdx.x >> 5), ok);
-    else min32((m == 0 ? S.iso1 : (m == 1 ? S.iso2 : S.iso3)) + c, ok);
-    if (d.guard) {
-      if (kStaged) smin32(v.nr0 + d.ridx, ok); else min32(S.nr0 + d.ridx, ok);
-    } else if (!d.inr) {
-      o.qn = !(MPSF_ABLATE & 1);
-      o.kn = nr_key(c, 0, d.va >> 12);
-      o.vn = ok;
-    } else {
-      if (m == 2) { if (kStaged) smin32(v.ext + d.ridx, ok); else min32(S.ext + d.ridx, ok); }
-      // first eligible record per in-range page: the epoch-1 first-isolation key of a client
-      // released before the drain (trap / dead at start), so that case needs no extra pass
-      if (S.nrall && !(MPSF_ABLATE & 2)) { o.pa = S.nrall + d.slot; o.va = ok; }
-    }
+  if (f & (LF_TRAP | LF_FATAL)) scan_fatal<kStaged>(v, S, f, c, d.cw, gidx);
+  const uint32_t ok = ((f & LF_REPL) ? 0u : 0x80000000u) | (uint32_t)gidx;
+  // isolation-eligible (pipeline.py:177-179): per-client minimum per mechanism class (iso1
+  // unmapped / iso2 managed / iso3 external; per-warp smem copies: a warp's indices only grow),
+  // first record per guard page (nr0) and per external range (ext)
+  const bool elig = (f & LF_ELIG) && !(f & LF_TRAP);
+  const uint32_t m = (f >> LF_M_SH) & 3u;
+  const bool inw = d.inr || d.guard;
+  const bool rr = elig && (d.guard || (d.inr && m == 2));
+  if (kStaged) {
+    uint32_t* pi = v.iso + (m * W.n_clients + c) * 32 + warp;
+    if (elig && *pi > ok) atomicMin(pi, ok);
+    uint32_t* pr = (d.guard ? v.nr0 : v.ext) + (inw ? d.ridx : 0u);
+    if (rr && *pr > ok) atomicMin(pr, ok);
+  } else {
+    if (elig) min32((m == 0 ? S.iso1 : (m == 1 ? S.iso2 : S.iso3)) + c, ok);
+    if (rr) min32((d.guard ? S.nr0 : S.ext) + d.ridx, ok);
   }
-  if ((f & LF_DD) && !(MPSF_ABLATE & 4)) {                           // dedup insert (rule C2)
-    const uint32_t group = (f >> LF_GROUP_SH) & 7u;
-    o.kd = dedup_key(c, (int)(e.w & 0xFF), (int)sid, d.va >> 12);
-    if (d.inr || d.guard) {
-      o.pd = S.dd + (W.dd_groups == 1 ? d.slot : d.slot * W.dd_groups + group);
-      o.vd = ((uint32_t)gidx << 3) | group;
-    } else {
-      o.qd = !(MPSF_ABLATE & 1);
-      o.vdh = (uint32_t)gidx;
-    }
-  }
-  (void)page;
+  // first eligible record per in-range page: the epoch-1 first-isolation key of a client
+  // released before the drain (trap / dead at start), so that case needs no extra pass
+  o.pa = (elig && d.inr && S.nrall && !(MPSF_ABLATE & 2)) ? S.nrall + d.slot : nullptr;
+  o.va = ok;
+  // dedup insert (rule C2): dense (page, group) slot or claimed page slot; wild pages hash
+  const bool dd = (f & LF_DD) && !(MPSF_ABLATE & 4);
+  const uint32_t group = (f >> LF_GROUP_SH) & 7u;
+  o.pd = (dd && inw) ? S.dd + (W.dd_groups == 1 ? d.slot : d.slot * W.dd_groups + group) : nullptr;
+  o.vd = ((uint32_t)gidx << 3) | group;
+  o.qn = elig && !inw && !(MPSF_ABLATE & 1);
+  o.qd = dd && !inw && !(MPSF_ABLATE & 1);
+  o.c = c; o.eng = e.w & 0xFF; o.sid = sid; o.page = d.va >> 12;
 }
 
 // Claimed-slot dedup (sparse worlds): first claim wins the page for its group; a record of
@@ -635,19 +574,19 @@ __global__ void __launch_bounds__(BLOCK, 1) k_scan(World W, Scratch S, const mps
                                                    uint64_t n, Params P, unsigned long long* __restrict__ counts,
                                                    uint32_t* __restrict__ count_part) {
   extern __shared__ __align__(128) uint8_t smem[];
-  const Layout L = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, false);
+  const Layout L = make_layout(W, kStaged, false);
   const View v = setup<kStaged>(smem, L, W, S, true, false, P.flags & MPSF_PF_ISOLATION);
   __syncthreads();
   QOp* q = reinterpret_cast<QOp*>(smem + L.queue) + (threadIdx.x >> 5) * QCAP;
   uint32_t qn = 0;
   const bool sparse = W.dd_groups == 1;
   ldg_stream(in, n, [&](uint4 e0, uint64_t i0, bool ok0, uint4 e1, uint64_t i1, bool ok1) {
-    ScanOut o0, o1;
-    o0.pa = o0.pd = o1.pa = o1.pd = nullptr;
-    o0.qn = o0.qd = o1.qn = o1.qd = false;
     if (MPSF_ABLATE & 64) { if (e0.x == 0x12345 && e1.y == 0x777) atomicOr(S.ctrl + C_ERR, 1u); return; }
-    if (ok0) scan_fast<kStaged>(W, v, S, e0, P.base_index + i0, counts, o0);
-    if (ok1) scan_fast<kStaged>(W, v, S, e1, P.base_index + i1, counts, o1);
+    ScanOut o0, o1;
+    if (!ok0) e0.w = 0;                       // past the end: decodes as a skipped entry
+    if (!ok1) e1.w = 0;
+    scan_fast<kStaged>(W, v, S, e0, P.base_index + i0, counts, o0);
+    scan_fast<kStaged>(W, v, S, e1, P.base_index + i1, counts, o1);
     // the L2 pre-check loads of both entries in flight together
     const uint32_t ra0 = o0.pa ? __ldcg(o0.pa) : 0u, rd0 = o0.pd ? __ldcg(o0.pd) : 0u;
     const uint32_t ra1 = o1.pa ? __ldcg(o1.pa) : 0u, rd1 = o1.pd ? __ldcg(o1.pd) : 0u;
@@ -657,13 +596,15 @@ __global__ void __launch_bounds__(BLOCK, 1) k_scan(World W, Scratch S, const mps
       if (o0.pd && rd0 > o0.vd) atomicMin(o0.pd, o0.vd);
       if (o1.pd && rd1 > o1.vd) atomicMin(o1.pd, o1.vd);
     } else {
-      if (o0.pd) claim_resolve(S, v.used, o0.pd, o0.vd, rd0, o0.kd);
-      if (o1.pd) claim_resolve(S, v.used, o1.pd, o1.vd, rd1, o1.kd);
+      if (o0.pd) claim_resolve(S, v.used, o0.pd, o0.vd, rd0, scan_dkey(o0));
+      if (o1.pd) claim_resolve(S, v.used, o1.pd, o1.vd, rd1, scan_dkey(o1));
     }
-    q_push(q, qn, o0.qn, o0.kn, o0.vn, 1, S, v.used);
-    q_push(q, qn, o0.qd, o0.kd, o0.vdh, 0, S, v.used);
-    q_push(q, qn, o1.qn, o1.kn, o1.vn, 1, S, v.used);
-    q_push(q, qn, o1.qd, o1.kd, o1.vdh, 0, S, v.used);
+    if (__any_sync(0xFFFFFFFFu, o0.qn || o0.qd || o1.qn || o1.qd)) {
+      q_push(q, qn, o0.qn, nr_key(o0.c, 0, o0.page), o0.va, 1, S, v.used);
+      q_push(q, qn, o0.qd, scan_dkey(o0), (uint32_t)(o0.vd >> 3), 0, S, v.used);
+      q_push(q, qn, o1.qn, nr_key(o1.c, 0, o1.page), o1.va, 1, S, v.used);
+      q_push(q, qn, o1.qd, scan_dkey(o1), (uint32_t)(o1.vd >> 3), 0, S, v.used);
+    }
   });
   q_drain(q, qn, S, v.used);
   if (kStaged) {
@@ -840,7 +781,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_general(World W, Scratch S, const 
                                                       uint64_t n, Params P) {
   if (__ldcg(S.ctrl + C_PATH) == 0) return;
   extern __shared__ __align__(128) uint8_t smem[];
-  const Layout L = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, true);
+  const Layout L = make_layout(W, kStaged, true);
   const View v = setup<kStaged>(smem, L, W, S, false, true, P.flags & MPSF_PF_ISOLATION);
   __syncthreads();
   ldg_stream(in, n, [&](uint4 e0, uint64_t i0, bool ok0, uint4 e1, uint64_t i1, bool ok1) {
@@ -938,7 +879,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const
                                                        uint32_t tile_lo, uint32_t tile_hi, uint32_t* __restrict__ tctr) {
   extern __shared__ __align__(128) uint8_t smem[];
   if (__ldcg(S.ctrl + C_ERR) != 0) return;
-  const Layout L = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, true);
+  const Layout L = make_layout(W, kStaged, true);
   const View v = setup<kStaged>(smem, L, W, S, false, true, P.flags & MPSF_PF_ISOLATION);
   Pipe p = pipe_init(smem, L);
   const Globals G = *S.glob;
@@ -1126,8 +1067,8 @@ static int grid_for(K kernel, size_t smem) {
 }
 
 static bool staged_fits(const World& W) {
-  return make_layout(W.n_ranges, W.n_clients, W.n_channels, true, false).total <= 220 * 1024 &&
-         make_layout(W.n_ranges, W.n_clients, W.n_channels, true, true).total <= 220 * 1024;
+  return make_layout(W, true, false).total <= 220 * 1024 &&
+         make_layout(W, true, true).total <= 220 * 1024;
 }
 
 uint32_t count_parts_needed(const World& W) {
@@ -1155,7 +1096,7 @@ static int scan_t(const World& W, const Scratch& S, const mpsf_fault_entry* in, 
   set_attrs<kStaged>();
   *parts = 0;
   if (n == 0) return 0;
-  const uint32_t smem = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, false).total;
+  const uint32_t smem = make_layout(W, kStaged, false).total;
   const uint64_t ntiles = (n + TILE - 1) / TILE;
   int g = grid_for(k_scan<kStaged>, smem);
   if (kStaged && g > (int)(2 * sm_count())) g = 2 * sm_count();
@@ -1172,7 +1113,7 @@ static int general_t(const World& W, const Scratch& S, const mpsf_fault_entry* i
                      int stage, cudaStream_t st, const Marker& mk) {
   set_attrs<kStaged>();
   if (n == 0) return 0;
-  const uint32_t smem = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, true).total;
+  const uint32_t smem = make_layout(W, kStaged, true).total;
   const uint64_t ntiles = (n + TILE - 1) / TILE;
   int g = grid_for(k_general<kStaged, 1>, smem);
   if ((uint64_t)g > ntiles) g = (int)ntiles;
@@ -1192,7 +1133,7 @@ static int finalize_t(const World& W, const Scratch& S, const mpsf_fault_entry* 
                       uint32_t tile_lo, uint32_t tile_hi, uint32_t* tctr, cudaStream_t st, const Marker& mk) {
   set_attrs<kStaged>();
   if (n == 0 || tile_hi <= tile_lo) return 0;
-  const uint32_t smem = make_layout(W.n_ranges, W.n_clients, W.n_channels, kStaged, true).total;
+  const uint32_t smem = make_layout(W, kStaged, true).total;
   int g = grid_for(k_finalize<kStaged>, smem);
   if ((uint32_t)g > tile_hi - tile_lo) g = (int)(tile_hi - tile_lo);
   k_finalize<kStaged><<<g, BLOCK, smem, st>>>(W, S, in, n, P, out, dkeys, didx, cancel, tile_lo, tile_hi, tctr);

@@ -294,8 +294,8 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   for (uint32_t i = 0; i < nch; ++i)
     if (channels[i].engine > 2) return MPSF_E_WORLD;
   if (nr > 65535) return MPSF_E_WORLD;
-  // page-granular SoA interval table + per-client skip tables (device form, mpsf_device.cuh)
-  std::vector<uint32_t> pg_base(nr), pg_end(nr), poff(nr), rattr(nr), rrid(nr);
+  // page-granular SoA interval table (padded with one sentinel row) + per-client skip tables
+  std::vector<uint32_t> pg_base(nr + 1), pg_end(nr + 1), poff(nr + 1), rattr(nr + 1), rrid(nr + 1);
   for (uint32_t i = 0; i < nr; ++i) {
     const mpsf_range_entry& r = ranges[i];
     if (r.end >= VA_TABLE_LIMIT) return MPSF_E_WORLD;
@@ -306,25 +306,38 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
                ((uint32_t)r.state << 24);
     rrid[i] = r.rid;
   }
-  std::vector<uint16_t> skip((size_t)SKIP_K * ncl, 0);
-  std::vector<uint32_t> crange(ncl), cspan(ncl), cshift(ncl);
+  pg_base[nr] = 0xFFFFFFFFu; pg_end[nr] = 0; poff[nr] = 0; rattr[nr] = 0; rrid[nr] = NO_RID;
+  // skip tables: slot size 2^sh <= the smallest gap between two consecutive bases, so a slot
+  // holds at most one base and attribution is one table read plus at most one step
+  std::vector<uint16_t> skip;
+  std::vector<uint32_t> cinfo(4ull * std::max<uint32_t>(ncl, 1), 0);
+  uint32_t exact1 = 1;
   for (uint32_t cl = 0; cl < ncl; ++cl) {
     const uint32_t lo = off[cl], hi = off[cl + 1];
-    crange[cl] = lo | (hi << 16);
-    if (lo == hi) { cspan[cl] = 0; cshift[cl] = 0; continue; }
+    uint32_t* ci = &cinfo[4ull * cl];
+    ci[0] = lo | (hi << 16);
+    ci[3] = (uint32_t)skip.size();
+    if (lo == hi) continue;
     const uint64_t span_lo = pg_base[lo], span_hi = (uint64_t)pg_end[hi - 1] + 1;
+    uint64_t gap = span_hi - span_lo;
+    for (uint32_t i = lo + 1; i < hi; ++i) gap = std::min<uint64_t>(gap, (uint64_t)pg_base[i] - pg_base[i - 1]);
     uint32_t sh = 0;
-    while (((span_hi - span_lo + (1ull << sh) - 1) >> sh) > (uint64_t)SKIP_K) ++sh;
-    cspan[cl] = (uint32_t)span_lo;
-    cshift[cl] = sh;
+    while ((2ull << sh) <= gap) ++sh;
+    auto slots_for = [&](uint32_t s_) { return (span_hi - span_lo + (1ull << s_) - 1) >> s_; };
+    while (slots_for(sh) > SKIP_MAX) { ++sh; exact1 = 0; }
+    const uint64_t slots = slots_for(sh);
+    ci[1] = (uint32_t)span_lo;
+    ci[2] = sh | ((uint32_t)(slots - 1) << 8);
     uint32_t k = lo;
-    for (int j = 0; j < SKIP_K; ++j) {
-      const uint64_t slot = span_lo + ((uint64_t)j << sh);
-      while (k + 1 < hi && pg_base[k + 1] <= slot) ++k;
-      skip[(size_t)cl * SKIP_K + j] = (uint16_t)k;
+    for (uint64_t j = 0; j < slots; ++j) {
+      const uint64_t st = span_lo + (j << sh);
+      while (k + 1 < hi && pg_base[k + 1] <= st) ++k;
+      skip.push_back((uint16_t)k);
     }
   }
-  std::vector<uint32_t> chan(nch);
+  const uint32_t n_skip = (uint32_t)skip.size();
+  skip.push_back(0);
+  std::vector<uint32_t> chan(nch + 1, 0);
   for (uint32_t i = 0; i < nch; ++i) {
     const uint32_t cl = channels[i].client;
     chan[i] = cl < ncl ? ((cl & 0xFFFFu) | ((uint32_t)channels[i].engine << 16) |
@@ -336,11 +349,10 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   const size_t o_ch = a256(o_ps + np);
   const size_t o_cl = a256(o_ch + sizeof(mpsf_channel_entry) * nch);
   const size_t o_soa = a256(o_cl + sizeof(mpsf_client_entry) * ncl);
-  const size_t o_skip = a256(o_soa + 5ull * 4 * nr);
-  const size_t o_cinfo = a256(o_skip + 2ull * SKIP_K * ncl);
-  const size_t o_cinfo4 = a256(o_cinfo + 3ull * 4 * ncl);
-  const size_t o_chan = a256(o_cinfo4 + 16ull * ncl);
-  const size_t total = a256(o_chan + 4ull * nch) + 256;
+  const size_t o_skip = a256(o_soa + 5ull * 4 * (nr + 1));
+  const size_t o_cinfo4 = a256(o_skip + 2ull * skip.size());
+  const size_t o_chan = a256(o_cinfo4 + 4ull * cinfo.size());
+  const size_t total = a256(o_chan + 4ull * chan.size()) + 256;
   cudaFree(c->d_world);
   c->d_world = nullptr;
   c->has_world = false;
@@ -352,24 +364,15 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   if (nch) CK(cudaMemcpy(b + o_ch, channels, sizeof(mpsf_channel_entry) * nch, cudaMemcpyHostToDevice));
   if (ncl) CK(cudaMemcpy(b + o_cl, clients, sizeof(mpsf_client_entry) * ncl, cudaMemcpyHostToDevice));
   uint32_t* soa = reinterpret_cast<uint32_t*>(b + o_soa);
-  if (nr) {
-    CK(cudaMemcpy(soa, pg_base.data(), 4ull * nr, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(soa + nr, pg_end.data(), 4ull * nr, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(soa + 2ull * nr, poff.data(), 4ull * nr, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(soa + 3ull * nr, rattr.data(), 4ull * nr, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(soa + 4ull * nr, rrid.data(), 4ull * nr, cudaMemcpyHostToDevice));
-  }
-  uint32_t* cinfo = reinterpret_cast<uint32_t*>(b + o_cinfo);
-  if (ncl) {
-    CK(cudaMemcpy(b + o_skip, skip.data(), 2ull * SKIP_K * ncl, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(cinfo, crange.data(), 4ull * ncl, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(cinfo + ncl, cspan.data(), 4ull * ncl, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(cinfo + 2ull * ncl, cshift.data(), 4ull * ncl, cudaMemcpyHostToDevice));
-    std::vector<uint32_t> c4(4ull * ncl, 0);
-    for (uint32_t i = 0; i < ncl; ++i) { c4[4 * i] = crange[i]; c4[4 * i + 1] = cspan[i]; c4[4 * i + 2] = cshift[i]; }
-    CK(cudaMemcpy(b + o_cinfo4, c4.data(), 16ull * ncl, cudaMemcpyHostToDevice));
-  }
-  if (nch) CK(cudaMemcpy(b + o_chan, chan.data(), 4ull * nch, cudaMemcpyHostToDevice));
+  const size_t R1 = nr + 1;
+  CK(cudaMemcpy(soa, pg_base.data(), 4 * R1, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(soa + R1, pg_end.data(), 4 * R1, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(soa + 2 * R1, poff.data(), 4 * R1, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(soa + 3 * R1, rattr.data(), 4 * R1, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(soa + 4 * R1, rrid.data(), 4 * R1, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(b + o_skip, skip.data(), 2ull * skip.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(b + o_cinfo4, cinfo.data(), 4ull * cinfo.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(b + o_chan, chan.data(), 4ull * chan.size(), cudaMemcpyHostToDevice));
   World& W = c->W;
   W.ranges = reinterpret_cast<const mpsf_range_entry*>(b + o_r);
   W.client_off = reinterpret_cast<const uint32_t*>(b + o_off);
@@ -377,16 +380,15 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   W.channels = reinterpret_cast<const mpsf_channel_entry*>(b + o_ch);
   W.clients = reinterpret_cast<const mpsf_client_entry*>(b + o_cl);
   W.pg_base = soa;
-  W.pg_end = soa + nr;
-  W.poff = soa + 2ull * nr;
-  W.rattr = soa + 3ull * nr;
-  W.rrid = soa + 4ull * nr;
+  W.pg_end = soa + R1;
+  W.poff = soa + 2 * R1;
+  W.rattr = soa + 3 * R1;
+  W.rrid = soa + 4 * R1;
   W.skip = reinterpret_cast<const uint16_t*>(b + o_skip);
-  W.crange = cinfo;
-  W.cspan = cinfo + ncl;
-  W.cshift = cinfo + 2ull * ncl;
   W.cinfo4 = reinterpret_cast<const uint4*>(b + o_cinfo4);
   W.chan = reinterpret_cast<const uint32_t*>(b + o_chan);
+  W.n_skip = n_skip;
+  W.exact1 = exact1;
   W.n_ranges = nr;
   W.n_clients = ncl;
   W.n_channels = nch;

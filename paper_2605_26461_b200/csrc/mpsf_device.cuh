@@ -58,32 +58,33 @@ struct Globals {
   uint32_t has_elig;
 };
 
-constexpr int SKIP_K = 64;               // skip-table slots per client
+constexpr uint32_t SKIP_MAX = 256;       // skip-table slots per client (cap)
 constexpr uint64_t VA_TABLE_LIMIT = 1ull << 44;   // interval tables hold 32-bit page numbers
 
 // Device form of the interval table, built by mpsf_upload_world (page-granular SoA so a warp's
-// random lookups touch 4-byte words: no 32-byte-row bank conflicts).
+// random lookups touch 4-byte words: no 32-byte-row bank conflicts).  Per client, a skip table
+// maps (page - span) >> shift to the last range whose base is <= the slot start; the shift is
+// chosen so that a slot holds at most one range base (exact1: attribution takes <= 1 step).
 struct World {
   const mpsf_range_entry* ranges;   // original rows (host order)
   const uint32_t* client_off;
   const uint8_t* page_state;
   const mpsf_channel_entry* channels;
   const mpsf_client_entry* clients;
-  const uint32_t* pg_base;          // [R] base >> 12
-  const uint32_t* pg_end;           // [R] end >> 12
-  const uint32_t* poff;             // [R] first page-state slot
-  const uint32_t* rattr;            // [R] kind | lifecycle << 8 | migratable << 16 | state << 24
-  const uint32_t* rrid;             // [R] reference rid
-  const uint16_t* skip;             // [C][SKIP_K] last range with base <= slot start
-  const uint32_t* crange;           // [C] lo | hi << 16 (range slice)
-  const uint32_t* cspan;            // [C] first page of the client's span
-  const uint32_t* cshift;           // [C] log2 pages per skip slot
-  const uint32_t* chan;             // [nch] client | engine << 16 | standalone << 18 | valid << 31
-  const uint4* cinfo4;              // [C] (crange, cspan, cshift, 0): one 16-byte row per client
+  const uint32_t* pg_base;          // [R + 1] base >> 12 (row R = 0xFFFFFFFF)
+  const uint32_t* pg_end;           // [R + 1] end >> 12
+  const uint32_t* poff;             // [R + 1] first page-state slot
+  const uint32_t* rattr;            // [R + 1] kind | lifecycle << 8 | migratable << 16 | state << 24
+  const uint32_t* rrid;             // [R + 1] reference rid
+  const uint16_t* skip;             // [n_skip + 1] per-client skip tables, concatenated
+  const uint32_t* chan;             // [nch + 1] client | engine << 16 | standalone << 18 | valid << 31
+  const uint4* cinfo4;              // [C] (lo | hi << 16, span, shift | (slots - 1) << 8, skip offset)
   uint32_t n_ranges, n_clients, n_channels, world_flags;
   uint64_t n_pages;
   uint32_t has_mps;
   uint32_t dd_groups;   // 5: one dense dedup slot per (page, group); 1: one claimed slot per page
+  uint32_t n_skip;
+  uint32_t exact1;      // every skip slot holds at most one range base
 };
 
 constexpr uint32_t CH_VALID = 1u << 31;
@@ -192,26 +193,16 @@ __device__ __forceinline__ uint32_t lut_word(int idx, bool isolation) {
          (serv ? LF_SERV : (isolation ? LF_ELIG : LF_FATAL)) | (m << LF_M_SH);
 }
 
-struct Attr {
-  int ridx;        // range index (in range or owner of the guard page), -1 if wild
-  bool in_range;
-  bool guard;      // page is the unmapped guard page right after ranges[ridx]
-  uint32_t slot;   // dense page slot (in_range or guard)
-  uint32_t st;     // page state byte (in_range)
-  int kind, lifecycle, migratable;
-  uint32_t rid;
-};
-
 // Tables a lookup reads (shared memory when staged, else global).  The per-client words and
 // the channel table may be replicated 32x ([i][lane]) so a warp's lookups are bank-conflict free.
 struct Tables {
   const uint32_t *pg_base, *pg_end, *poff, *rattr, *rrid;
   const uint16_t* skip;
-  const uint32_t *crange, *cspan, *cshift, *chan;
+  const uint32_t* chan;
   uint32_t rep_client, rep_chan;   // 32 when replicated per lane, else 0
-  const uint4* cinfo;              // [C] or [C][32] rows (crange, cspan, cshift, 0)
+  const uint4* cinfo;              // [C] or [C][32] client rows (World::cinfo4)
   const uint32_t* lut;             // [LUT_N] classification words (always shared memory)
-  uint32_t n_channels;
+  uint32_t n_channels, exact1;
 };
 
 // Decoded entry of the lean path (decode_fast).
@@ -226,78 +217,6 @@ struct Dec {
 
 __device__ __forceinline__ uint32_t rep_load(const uint32_t* a, uint32_t i, uint32_t rep, uint32_t lane) {
   return rep ? a[i * 32 + lane] : a[i];
-}
-
-// Attribution, restating MemoryModel.range_at (memory.py:233-237): the skip table narrows
-// the client's slice to the range covering the slot start; a short forward walk finishes.
-__device__ __forceinline__ Attr attribute_pg(const Tables& T, const uint8_t* __restrict__ page_state,
-                                             uint32_t c, uint64_t va, uint32_t lane) {
-  Attr t;
-  t.ridx = -1; t.in_range = false; t.guard = false; t.slot = 0; t.st = 0;
-  t.kind = 0; t.lifecycle = 0; t.migratable = 1; t.rid = NO_RID;
-  const uint32_t cr = rep_load(T.crange, c, T.rep_client, lane);
-  const uint32_t lo = cr & 0xFFFFu, hi = cr >> 16;
-  if (lo == hi || va >= VA_TABLE_LIMIT) return t;
-  const uint32_t page = (uint32_t)(va >> 12);
-  const uint32_t span = rep_load(T.cspan, c, T.rep_client, lane);
-  if (page < span) return t;
-  const uint32_t sh = rep_load(T.cshift, c, T.rep_client, lane);
-  uint32_t j = (page - span) >> sh;
-  j = j < (uint32_t)SKIP_K ? j : (uint32_t)(SKIP_K - 1);
-  uint32_t k = T.skip[c * SKIP_K + j];
-  while (k + 1 < hi && T.pg_base[k + 1] <= page) ++k;
-  const uint32_t end = T.pg_end[k];
-  if (page < end) {
-    const uint32_t a = T.rattr[k];
-    const uint32_t base = T.pg_base[k];
-    t.ridx = (int)k; t.in_range = true;
-    t.slot = T.poff[k] + (page - base);
-    t.kind = a & 0xFF; t.lifecycle = (a >> 8) & 0xFF; t.migratable = (a >> 16) & 0xFF;
-    const uint32_t ust = a >> 24;
-#if defined(MPSF_ABLATE) && (MPSF_ABLATE & 16)
-    t.st = ust != 0xFF ? ust : (t.slot & 7);
-#else
-    t.st = ust != 0xFF ? ust : (uint32_t)page_state[t.slot];
-#endif
-  } else if (page == end) {
-    t.ridx = (int)k; t.guard = true;
-    t.slot = T.poff[k] + (end - T.pg_base[k]);
-  }
-  return t;
-}
-
-// Binary search of client's slice [lo, hi) for the last range with base <= va.
-__device__ __forceinline__ Attr attribute(const mpsf_range_entry* __restrict__ R,
-                                          const uint8_t* __restrict__ page_state,
-                                          uint32_t lo, uint32_t hi, uint64_t va) {
-  // branchless: pos converges on the last range with base <= va (if any)
-  uint32_t pos = lo, len = hi - lo;
-  while (len > 1) {
-    const uint32_t half = len >> 1;
-    pos = (R[pos + half].base <= va) ? pos + half : pos;
-    len -= half;
-  }
-  Attr t;
-  t.ridx = -1; t.in_range = false; t.guard = false; t.slot = 0; t.st = 0;
-  t.kind = 0; t.lifecycle = 0; t.migratable = 1; t.rid = NO_RID;
-  if (hi > lo && R[pos].base <= va) {
-    const uint32_t k = pos;
-    const uint64_t base = R[k].base, end = R[k].end;
-    if (va < end) {
-      const uint4 meta = *reinterpret_cast<const uint4*>(&R[k].client);  // client,page_off,kind..state,rid
-      const uint32_t pidx = (uint32_t)((va - base) >> 12);
-      t.ridx = (int)k; t.in_range = true;
-      t.slot = meta.y + pidx;
-      t.kind = meta.z & 0xFF; t.lifecycle = (meta.z >> 8) & 0xFF; t.migratable = (meta.z >> 16) & 0xFF;
-      const uint32_t ust = meta.z >> 24;
-      t.st = ust != 0xFF ? ust : (uint32_t)page_state[t.slot];
-      t.rid = meta.w;
-    } else if (va < end + 4096) {
-      t.ridx = (int)k; t.guard = true;
-      t.slot = R[k].page_off + (uint32_t)((end - base) >> 12);
-    }
-  }
-  return t;
 }
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
