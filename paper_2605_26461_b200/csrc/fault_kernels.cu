@@ -94,9 +94,19 @@ struct Layout {
 };
 
 // kStaged: the interval table (page-granular SoA + skip tables, the client rows and the
-// channel table replicated per bank) and the pass-1 caches live in smem.  The LUT always does.
+// channel table replicated per bank) and the pass-1 caches live in smem at FIXED offsets
+// sized for the FX_* limits, so every table access is an immediate-offset LDS.  Worlds beyond
+// the limits run the global-table variant.  The LUT always lives in smem.
+constexpr uint32_t FX_C = 64, FX_R = 2048, FX_CH = 256, FX_SKIP = 4096;
+
+__host__ __device__ inline bool fits_fixed(const World& W) {
+  return W.n_clients <= FX_C && W.n_ranges + 1 <= FX_R && W.n_channels <= FX_CH && W.n_skip + 1 <= FX_SKIP;
+}
+
 __host__ __device__ inline Layout make_layout(const World& W, bool staged, bool fin) {
-  const uint32_t nr = W.n_ranges + 1, nc = W.n_clients, nch = W.n_channels + 1;
+  const uint32_t nr = staged ? FX_R : W.n_ranges + 1, nc = staged ? FX_C : W.n_clients;
+  const uint32_t nch = staged ? FX_CH + 1 : W.n_channels + 1;
+  const uint32_t nskip = staged ? FX_SKIP : W.n_skip + 1;
   Layout L;
   uint32_t o = 0;
   L.tiles = o; if (fin) o += NBUF * TILE_BYTES;   // finalize: TMA tile ring
@@ -104,7 +114,7 @@ __host__ __device__ inline Layout make_layout(const World& W, bool staged, bool 
   L.tids = o; o += al16(4 * NBUF);
   L.tot = o; o += 8 * 32 * NBUF;          // per buffer, per worker warp: (cancel, dedup) counts
   L.pre = o; o += 8 * 32 * NBUF;          // per buffer, per worker warp: exclusive output offsets
-  L.rep_chan = (staged && nch <= 257) ? 32u : 0u;
+  L.rep_chan = staged ? 32u : 0u;
   L.lut = o; o += 4 * LUT_N;
   L.queue = o; if (!fin) o += WARPS * QCAP * 16;
   L.cinfo = o; if (staged) o += al16(512ull * nc);
@@ -113,7 +123,7 @@ __host__ __device__ inline Layout make_layout(const World& W, bool staged, bool 
   L.poff = o; if (staged) o += al16(4ull * nr);
   L.rattr = o; if (staged) o += al16(4ull * nr);
   L.rrid = o; if (staged && fin) o += al16(4ull * nr);
-  L.skip = o; if (staged) o += al16(2ull * (W.n_skip + 1));
+  L.skip = o; if (staged) o += al16(2ull * nskip);
   L.chan = o; if (staged) o += al16(4ull * nch * (L.rep_chan ? 32 : 1));
   L.c64 = o; if (staged && !fin) o += al16(24ull * nc + 16);
   L.iso = o; if (staged && !fin) o += al16(3ull * 128 * nc);
@@ -1066,9 +1076,11 @@ static int grid_for(K kernel, size_t smem) {
   return per_sm * sm_count();
 }
 
+constexpr int SMEM_MAX = 227 * 1024;
+
 static bool staged_fits(const World& W) {
-  return make_layout(W, true, false).total <= 220 * 1024 &&
-         make_layout(W, true, true).total <= 220 * 1024;
+  return fits_fixed(W) && make_layout(W, true, false).total <= (uint32_t)SMEM_MAX &&
+         make_layout(W, true, true).total <= (uint32_t)SMEM_MAX;
 }
 
 uint32_t count_parts_needed(const World& W) {
@@ -1079,7 +1091,7 @@ template <bool kStaged>
 static void set_attrs() {
   static bool done = false;
   if (done) return;
-  const int mx = 220 * 1024;
+  const int mx = SMEM_MAX;
   cudaFuncSetAttribute(k_scan<kStaged>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(k_general<kStaged, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(k_general<kStaged, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
