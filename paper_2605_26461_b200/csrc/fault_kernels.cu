@@ -35,17 +35,10 @@
 
 namespace mpsf {
 
-// Warp-specialised CTA: warp 0 is the control warp (TMA producer; in the finalize pass also
-// the decoupled look-back, one tile behind the workers), warps 1..31 are workers.
+// Streaming passes: persistent grid of 1024-thread CTAs (one per SM, shared memory holds the
+// world tables); every warp owns 64-entry chunks (two adjacent entries per lane).
 constexpr int BLOCK = 1024;
 constexpr int WARPS = BLOCK / 32;
-constexpr int WORKERS = WARPS - 1;
-constexpr int EPT = 2;                     // entries per worker lane per tile
-constexpr int WSEG = 32 * EPT;             // entries per worker warp per tile
-constexpr int TILE = WORKERS * WSEG;       // 1984 entries = 31 KiB
-constexpr int NBUF = 3;
-constexpr uint32_t TILE_BYTES = TILE * 16;
-constexpr uint32_t TID_NONE = 0xFFFFFFFFu;
 constexpr int QCAP = 64;                   // per-warp deferred hash-op stack (scan)
 
 // ---- PTX: mbarrier + bulk async copy (TMA) ---------------------------------------------
@@ -86,7 +79,6 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 __host__ __device__ inline uint32_t al16(uint64_t x) { return (uint32_t)((x + 15) & ~uint64_t(15)); }
 
 struct Layout {
-  uint32_t tiles, bars, tids, tot, pre;
   uint32_t lut, cinfo, queue;
   uint32_t pg_base, pg_end, poff, rattr, rrid, skip, chan;
   uint32_t c64, iso, r32, counts, used, cstate, total;
@@ -109,11 +101,6 @@ __host__ __device__ inline Layout make_layout(const World& W, bool staged, bool 
   const uint32_t nskip = staged ? FX_SKIP : W.n_skip + 1;
   Layout L;
   uint32_t o = 0;
-  L.tiles = o; if (fin) o += NBUF * TILE_BYTES;   // finalize: TMA tile ring
-  L.bars = o; o += 4 * 8 * NBUF;          // full, empty, done, pref per buffer
-  L.tids = o; o += al16(4 * NBUF);
-  L.tot = o; o += 8 * 32 * NBUF;          // per buffer, per worker warp: (cancel, dedup) counts
-  L.pre = o; o += 8 * 32 * NBUF;          // per buffer, per worker warp: exclusive output offsets
   L.rep_chan = staged ? 32u : 0u;
   L.lut = o; o += 4 * LUT_N;
   L.queue = o; if (!fin) o += WARPS * QCAP * 16;
@@ -323,54 +310,6 @@ __device__ __forceinline__ uint32_t dd_slot(const World& W, const Rec& r) {
   return W.dd_groups == 1 ? r.at.slot : r.at.slot * W.dd_groups + r.group;
 }
 
-// ---- warp-specialised tile pipeline ---------------------------------------------------------
-// full[b]: TMA bytes landed (control arrive.expect_tx + tx count)      -- workers wait
-// empty[b]: every worker warp is done with buffer b (31 arrivals)      -- control waits, refills
-// done[b]/pref[b] (finalize only): worker counts posted / tile offsets known
-struct Pipe {
-  uint8_t* buf;
-  uint64_t *full, *empty, *done, *pref;
-  uint32_t* tids;
-  uint32_t* tot;    // [NBUF][32][2]
-  uint32_t* pre;    // [NBUF][32][2]
-  uint64_t pol;
-};
-
-__device__ __forceinline__ void pipe_issue(const Pipe& p, int b, const mpsf_fault_entry* in, uint64_t n, uint64_t t) {
-  const uint64_t start = t * TILE;
-  const uint64_t cnt = n - start < (uint64_t)TILE ? n - start : (uint64_t)TILE;
-  const uint32_t bytes = (uint32_t)(cnt * 16);
-  mbar_expect_tx(p.full + b, bytes);
-  bulk_load(p.buf + (size_t)b * TILE_BYTES, in + start, bytes, p.full + b, p.pol);
-}
-
-// Buffer b has no more work: complete its full barrier without data (tids[b] = TID_NONE).
-__device__ __forceinline__ void pipe_close(const Pipe& p, int b) {
-  p.tids[b] = TID_NONE;
-  mbar_arrive(p.full + b);
-}
-
-__device__ __forceinline__ Pipe pipe_init(uint8_t* sm, const Layout& L) {
-  Pipe p;
-  p.buf = sm + L.tiles;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.bars);
-  p.full = bars; p.empty = bars + NBUF; p.done = bars + 2 * NBUF; p.pref = bars + 3 * NBUF;
-  p.tids = reinterpret_cast<uint32_t*>(sm + L.tids);
-  p.tot = reinterpret_cast<uint32_t*>(sm + L.tot);
-  p.pre = reinterpret_cast<uint32_t*>(sm + L.pre);
-  if (threadIdx.x == 0) {
-    for (int b = 0; b < NBUF; ++b) {
-      mbar_init(p.full + b, 1);
-      mbar_init(p.empty + b, WORKERS);
-      mbar_init(p.done + b, WORKERS);
-      mbar_init(p.pref + b, 1);
-    }
-    fence_mbar_init();
-  }
-  p.pol = policy_evict_first();
-  return p;
-}
-
 // Stream for the order-free passes (scan, general): warp w of the grid owns 64-entry chunks
 // w, w + W, w + 2W, ...; each lane reads its two adjacent entries with one 32-byte
 // non-allocating load (L2 evict-first) and the next chunk's pair is requested before the
@@ -403,23 +342,6 @@ __device__ __forceinline__ void ldg_stream(const mpsf_fault_entry* in, uint64_t 
     if (c + GW < nch) ld_pair(in, n, (c + GW) * WCHUNK + 2 * lane, a32, na, nb);
     const uint64_t i0 = c * WCHUNK + 2 * lane;
     fn(e0, i0, i0 < n, e1, i0 + 1, i0 + 1 < n);
-  }
-}
-
-// Control-warp loop for the statically scheduled passes (tile t = blockIdx + j*grid).
-__device__ __forceinline__ void control_static(const Pipe& p, const mpsf_fault_entry* in, uint64_t n) {
-  if ((threadIdx.x & 31) != 0) return;
-  const uint64_t ntiles = (n + TILE - 1) / TILE;
-  for (uint32_t j = 0;; ++j) {
-    const int b = j % NBUF;
-    const uint64_t t = blockIdx.x + (uint64_t)j * gridDim.x;
-    if (j >= (uint32_t)NBUF) mbar_wait(p.empty + b, ((j / NBUF) - 1) & 1);
-    if (t >= ntiles) {
-      pipe_close(p, b);
-      return;
-    }
-    p.tids[b] = (uint32_t)t;
-    pipe_issue(p, b, in, n, t);
   }
 }
 
@@ -820,220 +742,274 @@ __global__ void k_resolve2(World W, Scratch S, Params P) {
 }
 
 // ---- pass 2 -----------------------------------------------------------------------------
-// Decoupled look-back descriptor: [63:62] status (0 none, 1 aggregate, 2 prefix),
-// [61:31] dedup count, [30:0] cancel count.
-constexpr unsigned long long LB_AGG = 1ull << 62, LB_PRE = 2ull << 62, LB_VAL = (1ull << 62) - 1;
+// k_finalize writes every OutRecord and, per 64-entry chunk, the bitmasks of cancelled entries
+// and of dedup representatives, and adds the chunk's two counts to its segment counter
+// (SEG_CHUNKS chunks per segment).  k_lists then writes the cancel list and the dedup set in
+// index order: a block per segment sums the counters of the earlier segments for its base and
+// scans its own chunks' popcounts -- no serial look-back between tiles.
+constexpr uint32_t SEG_CHUNKS = 1024;
 
-__device__ __forceinline__ unsigned long long lb_pack(uint32_t nc, uint32_t nd) {
-  return ((unsigned long long)nd << 31) | nc;
+// Pass 2 per entry, in two halves so both entries of a lane issue their L2 lookups together:
+// fin_addr decodes and picks the words the verdict depends on (the dedup slot of its key,
+// the first-isolation word of its (client, page, epoch), its external range's first
+// isolation); fin_resolve turns the loaded words into the OutRecord, the cancel flag and the
+// dedup-set membership.  Wild pages (no range, no guard) look their keys up in the hashes.
+struct FinA {
+  Dec d;
+  CState cs;
+  uint32_t ok;
+  const uint32_t* pd;   // dedup slot word (in-world dedup candidates)
+  const uint32_t* pn;   // first-isolation word (nrall / nr1 / nr0)
+  const uint32_t* pe;   // external range's first isolation (ext)
+  bool hd, hn;          // look up in hdd / hnr instead
+  bool epoch1;
+};
+
+template <bool kStaged>
+__device__ __forceinline__ void fin_addr(const World& W, const View& v, const Scratch& S, uint4 e, uint64_t gidx,
+                                         FinA& a) {
+  a.d = decode_fast(v.T, W.page_state, S, e, gidx, threadIdx.x & 31);
+  const Dec& d = a.d;
+  const uint32_t f = d.f;
+  a.pd = a.pn = a.pe = nullptr;
+  a.hd = a.hn = false;
+  a.epoch1 = false;
+  a.cs = v.cst[d.c];
+  a.ok = ((f & LF_REPL) ? 0u : 0x80000000u) | (uint32_t)gidx;
+  const bool inw = d.inr || d.guard;
+  if (f & LF_DD) {
+    a.pd = inw ? S.dd + (W.dd_groups == 1 ? d.slot : d.slot * W.dd_groups + ((f >> LF_GROUP_SH) & 7u)) : nullptr;
+    a.hd = !inw;
+  }
+  if ((f & LF_ELIG) && !(f & LF_TRAP)) {                           // isolation mechanism inputs (C3)
+    const bool epoch1 = a.cs.rel < (long long)a.ok;
+    a.epoch1 = epoch1;
+    const uint32_t m = (f >> LF_M_SH) & 3u;
+    if (!d.inr || epoch1) {
+      const bool pre = a.cs.rel == REL_PRE;
+      if (epoch1 && !(pre && S.nrall)) {
+        a.pn = inw ? S.nr1 + d.slot : nullptr;
+        a.hn = !inw;
+      } else {
+        a.pn = d.inr ? S.nrall + d.slot : (d.guard ? S.nr0 + d.ridx : nullptr);
+        a.hn = !inw;
+      }
+    } else if (m == 2) {
+      a.pe = S.ext + d.ridx;
+    }
+  }
 }
 
-// Resolves one entry; writes the OutRecord and returns (cancel, rep, dedup key).
 template <bool kStaged>
-__device__ __forceinline__ void finalize_entry(const World& W, const View& v, const Scratch& S, const Params& P,
-                                               const Globals& G, uint4 e, uint64_t gidx,
-                                               mpsf_out_record& o, bool& canc, bool& rep,
-                                               unsigned long long& key) {
-  o.rid = NO_RID; o.scenario = 0xFF; o.verdict = 0; o.client = 0xFFFF;
+__device__ __forceinline__ void fin_resolve(const World& W, const View& v, const Scratch& S, const Globals& G,
+                                            uint4 e, uint64_t gidx, const FinA& a, uint32_t wd, uint32_t wn,
+                                            uint32_t we, unsigned long long& o8, bool& canc, bool& rep,
+                                            unsigned long long& key) {
+  const Dec& d = a.d;
+  const uint32_t f = d.f;
   canc = false; rep = false; key = 0;
-  const Rec r = to_rec(decode_fast(v.T, W.page_state, S, e, gidx, threadIdx.x & 31), e);
-  if (!r.valid) return;
-  const CState cs = v.cst[r.c];
-  o.scenario = (uint8_t)r.s;
-  o.client = (uint16_t)r.c;
-  o.rid = r.at.in_range ? v.T.rrid[r.at.ridx] : NO_RID;
-  if (s_trap(r.s)) {
+  if (!f) {
+    o8 = 0xFFFF000000000000ull | (0xFFull << 32) | NO_RID;     // rid NO_RID, scenario 0xFF, client 0xFFFF
+    return;
+  }
+  const uint32_t sid = f & LF_S, c = d.c;
+  const CState& cs = a.cs;
+  const uint32_t rid = d.inr ? v.T.rrid[d.ridx] : NO_RID;
+  uint32_t verdict;
+  if (f & LF_TRAP) {
     // raise_sm_trap at raise time (pipeline.py:151-155); a second trap on a destroyed
     // TSG is cancelled (the reference raises UnknownTsg)
     if (!(cs.flags & CS_SA)) canc = !(G.gr_alive0 && (uint32_t)gidx == G.trap_mps_idx);
     else canc = !((cs.flags & CS_ALIVE0) && (uint32_t)gidx == cs.trap_sa_idx);
-    o.verdict = canc ? 0x10 : 0;
-    return;
+    verdict = canc ? 0x10u : 0u;
+  } else {
+    const uint32_t outcome = (f & LF_ELIG) ? 2u : ((f & LF_SERV) ? 1u : 3u);
+    const uint32_t ok = a.ok;
+    uint32_t rep_ok = ok;
+    bool dup = false;
+    const uint32_t page_hi = (uint32_t)(d.va >> 12);
+    if (f & LF_DD) {                                               // rule C2: smallest index of the key
+      const uint32_t group = (f >> LF_GROUP_SH) & 7u;
+      key = dedup_key(c, (int)(e.w & 0xFF), (int)sid, d.va >> 12);
+      uint32_t ri;
+      if (!a.hd && wd != EMPTY32 && (wd & 7u) == group) ri = wd >> 3;
+      else ri = hash_get(S.hdd, key);
+      dup = ri != (uint32_t)gidx;
+      rep_ok = ri;                                                 // replayable: ok32 == idx
+      rep = !dup;
+      if (!rep) key = 0;
+    }
+    uint32_t mech = 0;
+    const uint32_t ceng = (d.cw >> 16) & 3u;
+    if (outcome == 3) {                     // fatal: applies iff its TSG still lives (C4)
+      bool applied;
+      if (cs.flags & CS_SA) applied = (cs.flags & CS_ALIVE0) && !(cs.flags & CS_TRAPPED) && rep_ok == cs.ft_sa_ok;
+      else if (ceng == 1) applied = (cs.flags & CS_CE_ALIVE0) && rep_ok == cs.ft_ce_ok && !(cs.rel < (long long)rep_ok);
+      else applied = rep_ok == G.ft_gr_ok;
+      canc = !applied;
+    } else if (outcome == 1) {              // benign completion dropped on a torn channel (C5)
+      canc = cs.rel != REL_NONE || (ceng == 1 && (cs.flags & CS_CE_TORN)) ||
+             (cs.flags & CS_KILL_ALL) || rep_ok > cs.kill_tie;
+    } else if (!dup) {                      // isolation mechanism (C3)
+      if (!d.inr || a.epoch1) {
+        const uint32_t nr = a.hn ? hash_get(S.hnr, nr_key(c, a.epoch1 && !(cs.rel == REL_PRE && S.nrall) ? 1 : 0,
+                                                          d.va >> 12))
+                                 : wn;
+        mech = nr == ok ? 1u : 2u;
+      } else {
+        mech = (a.pe && we == ok) ? 3u : 2u;
+      }
+    }
+    (void)page_hi;
+    verdict = outcome | (mech << 2) | (canc ? 0x10u : 0u) | (dup ? 0x20u : 0u) | ((f & LF_REPL) ? 0x40u : 0u);
   }
-  const bool parse = s_parse(r.s), serv = s_serviceable(r.s);
-  const int outcome = parse ? 3 : (serv ? 1 : ((P.flags & MPSF_PF_ISOLATION) ? 2 : 3));
-  const uint32_t ok = ok32_of(r.repl, gidx);
-  uint32_t rep_ok = ok;
-  bool dup = false;
-  if (r.kind == 0 && r.repl) {
-    const uint32_t ri = dedup_rep(W, S, r);
-    dup = ri != (uint32_t)gidx;
-    rep_ok = ri;                          // replayable: ok32 == idx
-    rep = !dup;
-    if (rep) key = dedup_key(r.c, r.eng, r.s, r.va >> 12);
-  }
-  int mech = 0;
-  if (outcome == 3) {                     // fatal: applies iff its TSG still lives (C4)
-    bool applied;
-    if (cs.flags & CS_SA) applied = (cs.flags & CS_ALIVE0) && !(cs.flags & CS_TRAPPED) && rep_ok == cs.ft_sa_ok;
-    else if (r.ceng == 1) applied = (cs.flags & CS_CE_ALIVE0) && rep_ok == cs.ft_ce_ok && !(cs.rel < (long long)rep_ok);
-    else applied = rep_ok == G.ft_gr_ok;
-    canc = !applied;
-  } else if (outcome == 1) {              // benign completion dropped on a torn channel (C5)
-    canc = cs.rel != REL_NONE || (r.ceng == 1 && (cs.flags & CS_CE_TORN)) ||
-           (cs.flags & CS_KILL_ALL) || rep_ok > cs.kill_tie;
-  } else if (!dup) {                      // isolation mechanism (C3)
-    const bool epoch1 = cs.rel < (long long)ok;
-    if (!r.at.in_range || epoch1) mech = nr_lookup(S, r, epoch1, cs.rel == REL_PRE) == ok ? 1 : 2;
-    else if (r.at.kind == 0) mech = 2;
-    else mech = __ldcg(S.ext + r.at.ridx) == ok ? 3 : 2;
-  }
-  o.verdict = (uint8_t)(outcome | (mech << 2) | (canc ? 0x10 : 0) | (dup ? 0x20 : 0) | (r.repl ? 0x40 : 0));
+  o8 = (unsigned long long)rid | ((unsigned long long)sid << 32) | ((unsigned long long)verdict << 40) |
+       ((unsigned long long)c << 48);
 }
 
+// Spread the 32 bits of x to the even bits of a 64-bit word (bit i -> bit 2i).
+__device__ __forceinline__ unsigned long long spread2(uint32_t x) {
+  unsigned long long v = x;
+  v = (v | (v << 16)) & 0x0000FFFF0000FFFFull;
+  v = (v | (v << 8)) & 0x00FF00FF00FF00FFull;
+  v = (v | (v << 4)) & 0x0F0F0F0F0F0F0F0Full;
+  v = (v | (v << 2)) & 0x3333333333333333ull;
+  v = (v | (v << 1)) & 0x5555555555555555ull;
+  return v;
+}
+
+// Pass 2 over entries [0, n) of `in` (a chunk of the batch starting at batch chunk q_base,
+// global index P.base_index): OutRecords, per-chunk masks, segment counts.
 template <bool kStaged>
 __global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const mpsf_fault_entry* __restrict__ in,
                                                        uint64_t n, Params P, mpsf_out_record* __restrict__ out,
-                                                       unsigned long long* __restrict__ dkeys,
-                                                       uint32_t* __restrict__ didx, uint32_t* __restrict__ cancel,
-                                                       uint32_t tile_lo, uint32_t tile_hi, uint32_t* __restrict__ tctr) {
+                                                       uint64_t q_base) {
   extern __shared__ __align__(128) uint8_t smem[];
   if (__ldcg(S.ctrl + C_ERR) != 0) return;
   const Layout L = make_layout(W, kStaged, true);
   const View v = setup<kStaged>(smem, L, W, S, false, true, P.flags & MPSF_PF_ISOLATION);
-  Pipe p = pipe_init(smem, L);
   const Globals G = *S.glob;
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (warp == 0) {
-    // control warp: dynamic in-order tile ids of [tile_lo, tile_hi), TMA refill, and the
-    // look-back of tile j while the workers already process tile j+1
-    auto refill = [&](int b) {
-      if (lane == 0) {
-        const uint32_t t = tile_lo + atomicAdd(tctr, 1u);
-        if (t < tile_hi) {
-          p.tids[b] = t;
-          fence_proxy_async();
-          pipe_issue(p, b, in, n, t);
-        } else {
-          pipe_close(p, b);
-        }
-      }
-      __syncwarp();
-    };
-    for (int b = 0; b < NBUF; ++b) refill(b);
-    for (uint32_t j = 0;; ++j) {
-      const int b = j % NBUF;
-      const uint32_t t = *reinterpret_cast<volatile uint32_t*>(p.tids + b);
-      if (t == TID_NONE) break;
-      mbar_wait(p.done + b, (j / NBUF) & 1);
-      const uint32_t* tot = p.tot + b * 64;
-      uint32_t c = lane ? tot[2 * lane] : 0u, d = lane ? tot[2 * lane + 1] : 0u;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {          // inclusive warp scan of the worker counts
-        const uint32_t uc = __shfl_up_sync(0xFFFFFFFFu, c, o), ud = __shfl_up_sync(0xFFFFFFFFu, d, o);
-        if (lane >= o) { c += uc; d += ud; }
-      }
-      const uint32_t tc = __shfl_sync(0xFFFFFFFFu, c, 31), td = __shfl_sync(0xFFFFFFFFu, d, 31);
-      const uint32_t ec = c - (lane ? tot[2 * lane] : 0u), ed = d - (lane ? tot[2 * lane + 1] : 0u);
-      // decoupled look-back, 32 predecessors per step
-      volatile unsigned long long* desc = S.tiles;
-      uint32_t pc = 0, pd = 0;
-      if (t == 0) {
-        if (lane == 0) desc[0] = LB_PRE | lb_pack(tc, td);
-      } else {
-        if (lane == 0) desc[t] = LB_AGG | lb_pack(tc, td);
-        int64_t q = (int64_t)t - 1;
-        while (true) {
-          const int64_t idx = q - lane;
-          unsigned long long dsc = 2ull << 62;          // before tile 0: an empty prefix
-          if (idx >= 0) dsc = desc[idx];
-          const unsigned long long st = dsc & ~LB_VAL;
-          const unsigned notready = __ballot_sync(0xFFFFFFFFu, st == 0);
-          const unsigned isp = __ballot_sync(0xFFFFFFFFu, st == LB_PRE);
-          const int firstp = isp ? __ffs(isp) - 1 : 32;
-          const unsigned need = firstp < 32 ? ((2u << firstp) - 1u) : 0xFFFFFFFFu;
-          if (notready & need) {
-            __nanosleep(64);
-            continue;
-          }
-          uint32_t vc = ((need >> lane) & 1u) ? (uint32_t)(dsc & 0x7FFFFFFFull) : 0u;
-          uint32_t vd = ((need >> lane) & 1u) ? (uint32_t)((dsc >> 31) & 0x7FFFFFFFull) : 0u;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            vc += __shfl_xor_sync(0xFFFFFFFFu, vc, o);
-            vd += __shfl_xor_sync(0xFFFFFFFFu, vd, o);
-          }
-          pc += vc;
-          pd += vd;
-          if (firstp < 32) break;
-          q -= 32;
-        }
-        if (lane == 0) desc[t] = LB_PRE | lb_pack(pc + tc, pd + td);
-      }
-      p.pre[b * 64 + 2 * lane] = pc + ec;
-      p.pre[b * 64 + 2 * lane + 1] = pd + ed;
-      __syncwarp();
-      if (lane == 0) mbar_arrive(p.pref + b);
-      // buffer b is refilled once the workers have written tile j's lists out of it
-      if (lane == 0) mbar_wait(p.empty + b, (j / NBUF) & 1);
-      __syncwarp();
-      refill(b);
+  const uint32_t lane = threadIdx.x & 31;
+  ldg_stream(in, n, [&](uint4 e0, uint64_t i0, bool ok0, uint4 e1, uint64_t i1, bool ok1) {
+    if (!ok0) e0.w = 0;                       // past the end: decodes as a skipped entry
+    if (!ok1) e1.w = 0;
+    if (MPSF_ABLATE & 256) { e0.w = 0; e1.w = 0; }
+    FinA a0, a1;
+    fin_addr<kStaged>(W, v, S, e0, P.base_index + i0, a0);
+    fin_addr<kStaged>(W, v, S, e1, P.base_index + i1, a1);
+    const uint32_t wd0 = a0.pd ? __ldcg(a0.pd) : EMPTY32, wn0 = a0.pn ? __ldcg(a0.pn) : EMPTY32;
+    const uint32_t we0 = a0.pe ? __ldcg(a0.pe) : EMPTY32;
+    const uint32_t wd1 = a1.pd ? __ldcg(a1.pd) : EMPTY32, wn1 = a1.pn ? __ldcg(a1.pn) : EMPTY32;
+    const uint32_t we1 = a1.pe ? __ldcg(a1.pe) : EMPTY32;
+    unsigned long long o0, o1, k0, k1;
+    bool c0, c1, r0, r1;
+    fin_resolve<kStaged>(W, v, S, G, e0, P.base_index + i0, a0, wd0, wn0, we0, o0, c0, r0, k0);
+    fin_resolve<kStaged>(W, v, S, G, e1, P.base_index + i1, a1, wd1, wn1, we1, o1, c1, r1, k1);
+    unsigned long long* o = reinterpret_cast<unsigned long long*>(out) + i0;
+    if (ok1 && (((uintptr_t)o & 15u) == 0)) __stcs(reinterpret_cast<ulonglong2*>(o), make_ulonglong2(o0, o1));
+    else {
+      if (ok0) __stcs(o, o0);
+      if (ok1) __stcs(o + 1, o1);
     }
-    return;
-  }
-  // worker warps
-  const unsigned lt_mask = (1u << lane) - 1u;
-  const int seg = (warp - 1) * WSEG;
-  uint64_t prev_start = 0;
-  auto writeout = [&](uint32_t jj, uint64_t start) {
-    const int b = jj % NBUF;
-    mbar_wait(p.pref + b, (jj / NBUF) & 1);
-    const uint4* tile = reinterpret_cast<const uint4*>(p.buf + (size_t)b * TILE_BYTES);
-    const uint32_t bc0 = p.pre[b * 64 + 2 * warp], bd0 = p.pre[b * 64 + 2 * warp + 1];
-#pragma unroll 1
-    for (int k = 0; k < EPT; ++k) {
-      const int li = seg + k * 32 + lane;
-      const uint4 q = tile[li];
-      const uint32_t gidx = (uint32_t)(P.base_index + start + li);
-      if (q.z & 1u) cancel[bc0 + (q.w & 0xFFFFu)] = gidx;
-      if (q.z & 2u) {
-        const uint32_t d = bd0 + (q.w >> 16);
-        dkeys[d] = (unsigned long long)q.x | ((unsigned long long)q.y << 32);
-        didx[d] = gidx;
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(p.empty + b);
-  };
-  uint32_t j = 0;
-  for (;; ++j) {
-    const int b = j % NBUF;
-    mbar_wait(p.full + b, (j / NBUF) & 1);
-    const uint32_t t = p.tids[b];
-    if (t == TID_NONE) break;
-    uint4* tile = reinterpret_cast<uint4*>(p.buf + (size_t)b * TILE_BYTES);
-    const uint64_t start = (uint64_t)t * TILE;
-    uint32_t wc = 0, wd = 0;
-#pragma unroll 1
-    for (int k = 0; k < EPT; ++k) {
-      const int li = seg + k * 32 + lane;
-      const uint64_t i = start + li;
-      mpsf_out_record o;
-      bool canc = false, rep = false;
-      unsigned long long key = 0;
-      if (i < n) {
-        finalize_entry<kStaged>(W, v, S, P, G, tile[li], P.base_index + i, o, canc, rep, key);
-        __stcs(reinterpret_cast<unsigned long long*>(out) + i, *reinterpret_cast<unsigned long long*>(&o));
-      }
-      const unsigned bc = __ballot_sync(0xFFFFFFFFu, canc);
-      const unsigned bd = __ballot_sync(0xFFFFFFFFu, rep);
-      // park the compaction payload in the consumed entry slot
-      tile[li] = make_uint4((uint32_t)key, (uint32_t)(key >> 32), (canc ? 1u : 0u) | (rep ? 2u : 0u),
-                            (wc + __popc(bc & lt_mask)) | ((wd + __popc(bd & lt_mask)) << 16));
-      wc += __popc(bc);
-      wd += __popc(bd);
-    }
+    const uint32_t bc0 = __ballot_sync(0xFFFFFFFFu, ok0 && c0), bc1 = __ballot_sync(0xFFFFFFFFu, ok1 && c1);
+    const uint32_t bd0 = __ballot_sync(0xFFFFFFFFu, ok0 && r0), bd1 = __ballot_sync(0xFFFFFFFFu, ok1 && r1);
     if (lane == 0) {
-      p.tot[b * 64 + 2 * warp] = wc;
-      p.tot[b * 64 + 2 * warp + 1] = wd;
+      const unsigned long long cm = spread2(bc0) | (spread2(bc1) << 1);
+      const unsigned long long dm = spread2(bd0) | (spread2(bd1) << 1);
+      const uint64_t q = q_base + i0 / WCHUNK;
+      S.cmask[q] = make_ulonglong2(cm, dm);
+      if (cm | dm)
+        atomicAdd(S.segcnt + q / SEG_CHUNKS, (unsigned long long)__popcll(cm) | ((unsigned long long)__popcll(dm) << 32));
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(p.done + b);
-    if (j > 0) writeout(j - 1, prev_start);
-    prev_start = start;
+  });
+}
+
+// Cancel list + dedup set in index order.  Block = one segment of SEG_CHUNKS chunks, one
+// thread per chunk: a block-wide scan of the chunks' popcounts gives every chunk its offsets,
+// then each thread writes its own chunk's entries (the L2 merges the short runs).  `in` /
+// `out` / the masks cover the whole batch (nq chunks).
+__global__ void __launch_bounds__(1024, 2) k_lists(Scratch S, const mpsf_fault_entry* __restrict__ in,
+                                                   const mpsf_out_record* __restrict__ out, uint64_t nq,
+                                                   uint64_t base_index, unsigned long long* __restrict__ dkeys,
+                                                   uint32_t* __restrict__ didx, uint32_t* __restrict__ cancel) {
+  static_assert(SEG_CHUNKS == 1024, "one thread per chunk");
+  if (__ldcg(S.ctrl + C_ERR) != 0) return;
+  __shared__ unsigned long long s_base;
+  __shared__ unsigned long long s_w[32];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t seg = blockIdx.x;
+  // base: counts of all earlier segments
+  unsigned long long acc = 0;
+  for (uint64_t i = threadIdx.x; i < seg; i += blockDim.x) acc += __ldcg(S.segcnt + i);
+  if (threadIdx.x == 0) s_base = 0;
+  __syncthreads();
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+  if (lane == 0 && acc) atomicAdd(&s_base, acc);
+  const uint64_t q = seg * SEG_CHUNKS + threadIdx.x;
+  ulonglong2 mk = make_ulonglong2(0, 0);
+  if (q < nq) mk = __ldcg(S.cmask + q);
+  const unsigned long long mine = (unsigned long long)__popcll(mk.x) | ((unsigned long long)__popcll(mk.y) << 32);
+  unsigned long long x = mine;   // inclusive warp scan (both counts packed)
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long u = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if (lane >= o) x += u;
   }
-  if (j > 0) writeout(j - 1, prev_start);
+  if (lane == 31) s_w[warp] = x;
+  __syncthreads();
+  unsigned long long pre = s_base;
+  for (uint32_t w = 0; w < warp; ++w) pre += s_w[w];
+  pre += x - mine;
+  uint64_t pc = pre & 0xFFFFFFFFull, pd = pre >> 32;
+  const uint32_t g0 = (uint32_t)(base_index + q * WCHUNK);
+  for (unsigned long long m = mk.x; m; m &= m - 1) cancel[pc++] = g0 + (uint32_t)__ffsll((long long)m) - 1;
+  // dedup set: key from the entry (engine, page) and its OutRecord (client, scenario); two
+  // representatives per round so their loads overlap
+  unsigned long long m = mk.y;
+  while (m) {
+    const uint32_t b0 = (uint32_t)__ffsll((long long)m) - 1;
+    m &= m - 1;
+    const bool two = m != 0;
+    const uint32_t b1 = two ? (uint32_t)__ffsll((long long)m) - 1 : b0;
+    if (two) m &= m - 1;
+    const uint64_t i0 = q * WCHUNK + b0, i1 = q * WCHUNK + b1;
+    const uint4 e0 = __ldg(reinterpret_cast<const uint4*>(in) + i0);
+    const uint4 e1 = __ldg(reinterpret_cast<const uint4*>(in) + i1);
+    const unsigned long long r0 = __ldg(reinterpret_cast<const unsigned long long*>(out) + i0);
+    const unsigned long long r1 = __ldg(reinterpret_cast<const unsigned long long*>(out) + i1);
+    dkeys[pd] = dedup_key((uint32_t)(r0 >> 48), (int)(e0.w & 0xFF), (int)((r0 >> 32) & 0xFF),
+                          ((uint64_t)e0.x | ((uint64_t)e0.y << 32)) >> 12);
+    didx[pd] = g0 + b0;
+    ++pd;
+    if (two) {
+      dkeys[pd] = dedup_key((uint32_t)(r1 >> 48), (int)(e1.w & 0xFF), (int)((r1 >> 32) & 0xFF),
+                            ((uint64_t)e1.x | ((uint64_t)e1.y << 32)) >> 12);
+      didx[pd] = g0 + b1;
+      ++pd;
+    }
+  }
+}
+
+// Batch summary: error / overflow words and the list lengths (sum of the segment counters).
+__global__ void k_summary(const Scratch S, uint64_t nseg, DevSummary* out) {
+  __shared__ unsigned long long s_tot;
+  if (threadIdx.x == 0) s_tot = 0;
+  __syncthreads();
+  unsigned long long acc = 0;
+  for (uint64_t i = threadIdx.x; i < nseg; i += blockDim.x) acc += __ldcg(S.segcnt + i);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(&s_tot, acc);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C_NCTRL; ++i) out->ctrl[i] = S.ctrl[i];
+    out->err_idx = *S.err_idx;
+    const bool err = S.ctrl[C_ERR] != 0;
+    out->n_cancel = err ? 0 : (s_tot & 0xFFFFFFFFull);
+    out->n_dedup = err ? 0 : (s_tot >> 32);
+  }
 }
 
 // ---- sparse hash exchange (multi-GPU) ------------------------------------------------------
@@ -1101,6 +1077,15 @@ static void set_attrs() {
 
 static int ok_or_err() { return cudaGetLastError() == cudaSuccess ? 0 : -1; }
 
+// at least one 64-entry chunk per warp
+static int clamp_grid(int g, uint64_t n) {
+  const uint64_t per_block = (uint64_t)WCHUNK * WARPS;
+  const uint64_t need = (n + per_block - 1) / per_block;
+  return (uint64_t)g > need ? (int)need : g;
+}
+
+
+
 template <bool kStaged>
 static int scan_t(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
                   unsigned long long* counts, uint32_t* count_part, cudaStream_t st, const Marker& mk,
@@ -1109,10 +1094,9 @@ static int scan_t(const World& W, const Scratch& S, const mpsf_fault_entry* in, 
   *parts = 0;
   if (n == 0) return 0;
   const uint32_t smem = make_layout(W, kStaged, false).total;
-  const uint64_t ntiles = (n + TILE - 1) / TILE;
   int g = grid_for(k_scan<kStaged>, smem);
   if (kStaged && g > (int)(2 * sm_count())) g = 2 * sm_count();
-  if ((uint64_t)g > ntiles) g = (int)ntiles;
+  g = clamp_grid(g, n);
   k_scan<kStaged><<<g, BLOCK, smem, st>>>(W, S, in, n, P, counts, count_part);
   mk.mark("k_scan");
   // partial rows accumulate across launches and were zeroed by k_init: reduce all of them
@@ -1126,9 +1110,7 @@ static int general_t(const World& W, const Scratch& S, const mpsf_fault_entry* i
   set_attrs<kStaged>();
   if (n == 0) return 0;
   const uint32_t smem = make_layout(W, kStaged, true).total;
-  const uint64_t ntiles = (n + TILE - 1) / TILE;
-  int g = grid_for(k_general<kStaged, 1>, smem);
-  if ((uint64_t)g > ntiles) g = (int)ntiles;
+  int g = clamp_grid(grid_for(k_general<kStaged, 1>, smem), n);
   if (stage == 1) {
     k_general<kStaged, 1><<<g, BLOCK, smem, st>>>(W, S, in, n, P);
     mk.mark("k_general1");
@@ -1141,19 +1123,19 @@ static int general_t(const World& W, const Scratch& S, const mpsf_fault_entry* i
 
 template <bool kStaged>
 static int finalize_t(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
-                      mpsf_out_record* out, unsigned long long* dkeys, uint32_t* didx, uint32_t* cancel,
-                      uint32_t tile_lo, uint32_t tile_hi, uint32_t* tctr, cudaStream_t st, const Marker& mk) {
+                      mpsf_out_record* out, uint64_t q_base, cudaStream_t st, const Marker& mk) {
   set_attrs<kStaged>();
-  if (n == 0 || tile_hi <= tile_lo) return 0;
+  if (n == 0) return 0;
   const uint32_t smem = make_layout(W, kStaged, true).total;
-  int g = grid_for(k_finalize<kStaged>, smem);
-  if ((uint32_t)g > tile_hi - tile_lo) g = (int)(tile_hi - tile_lo);
-  k_finalize<kStaged><<<g, BLOCK, smem, st>>>(W, S, in, n, P, out, dkeys, didx, cancel, tile_lo, tile_hi, tctr);
+  const int g = clamp_grid(grid_for(k_finalize<kStaged>, smem), n);
+  k_finalize<kStaged><<<g, BLOCK, smem, st>>>(W, S, in, n, P, out, q_base);
   mk.mark("k_finalize");
   return ok_or_err();
 }
 
-uint32_t tile_entries() { return (uint32_t)TILE; }
+uint32_t chunk_entries() { return (uint32_t)WCHUNK; }
+uint64_t chunks_for(uint64_t n) { return (n + WCHUNK - 1) / WCHUNK; }
+uint64_t segments_for(uint64_t n) { return (chunks_for(n) + SEG_CHUNKS - 1) / SEG_CHUNKS; }
 
 int launch_scan(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
                 unsigned long long* counts, uint32_t* count_part, cudaStream_t st, const Marker& mk, uint32_t* parts) {
@@ -1184,10 +1166,25 @@ int launch_resolve2(const World& W, const Scratch& S, const Params& P, cudaStrea
 }
 
 int launch_finalize(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
-                    mpsf_out_record* out, unsigned long long* dkeys, uint32_t* didx, uint32_t* cancel,
-                    uint32_t tile_lo, uint32_t tile_hi, uint32_t* tctr, cudaStream_t st, const Marker& mk) {
-  return staged_fits(W) ? finalize_t<true>(W, S, in, n, P, out, dkeys, didx, cancel, tile_lo, tile_hi, tctr, st, mk)
-                        : finalize_t<false>(W, S, in, n, P, out, dkeys, didx, cancel, tile_lo, tile_hi, tctr, st, mk);
+                    mpsf_out_record* out, uint64_t q_base, cudaStream_t st, const Marker& mk) {
+  return staged_fits(W) ? finalize_t<true>(W, S, in, n, P, out, q_base, st, mk)
+                        : finalize_t<false>(W, S, in, n, P, out, q_base, st, mk);
+}
+
+int launch_lists(const Scratch& S, const mpsf_fault_entry* in, const mpsf_out_record* out, uint64_t n,
+                 uint64_t base_index, unsigned long long* dkeys, uint32_t* didx, uint32_t* cancel, cudaStream_t st,
+                 const Marker& mk) {
+  const uint64_t nseg = segments_for(n);
+  if (nseg == 0) return 0;
+  k_lists<<<(unsigned)nseg, 1024, 0, st>>>(S, in, out, chunks_for(n), base_index, dkeys, didx, cancel);
+  mk.mark("k_lists");
+  return ok_or_err();
+}
+
+int launch_summary(const Scratch& S, uint64_t n, DevSummary* out, cudaStream_t st, const Marker& mk) {
+  k_summary<<<1, 1024, 0, st>>>(S, segments_for(n), out);
+  mk.mark("k_summary");
+  return ok_or_err();
 }
 
 int launch_hash_export(const Hash& h, uint64_t cap, unsigned long long* keys, uint32_t* vals, uint32_t* counter,
@@ -1203,6 +1200,5 @@ int launch_hash_merge(const Hash& h, uint32_t* ctrl, const unsigned long long* k
   return ok_or_err();
 }
 
-uint64_t tiles_for(uint64_t n) { return (n + TILE - 1) / TILE; }
 
 }  // namespace mpsf

@@ -18,13 +18,6 @@ using namespace mpsf;
 
 namespace {
 
-struct DevSummary {
-  uint32_t ctrl[C_NCTRL];
-  unsigned long long err_idx;
-  unsigned long long n_cancel;
-  unsigned long long n_dedup;
-};
-
 struct InitSegs {
   void* p[10];
   uint64_t words[10];
@@ -44,20 +37,6 @@ __global__ void k_init(InitSegs segs) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < w4; i += stride) p4[i] = v4;
   for (uint64_t i = w4 * 4 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < w; i += stride) p[i] = v;
-}
-
-__global__ void k_summary(const uint32_t* ctrl, const unsigned long long* err_idx,
-                          const unsigned long long* tiles, uint64_t ntiles, DevSummary* out) {
-  for (int i = 0; i < C_NCTRL; ++i) out->ctrl[i] = ctrl[i];
-  out->err_idx = *err_idx;
-  if (ntiles == 0 || ctrl[C_ERR] != 0) {
-    out->n_cancel = 0;
-    out->n_dedup = 0;
-  } else {
-    const unsigned long long d = tiles[ntiles - 1];
-    out->n_cancel = d & 0x7FFFFFFFull;
-    out->n_dedup = (d >> 31) & 0x7FFFFFFFull;
-  }
 }
 
 uint64_t next_pow2(uint64_t x) {
@@ -101,7 +80,7 @@ struct mpsf_ctx {
   uint8_t* d_small = nullptr;
   size_t small_cap = 0;
   size_t small_empty_bytes = 0, small_zero_off = 0, small_zero_bytes = 0;
-  unsigned long long* d_tiles = nullptr;
+  uint8_t* d_masks = nullptr;   // per-chunk masks + segment counters (pass 2)
   uint64_t tiles_cap = 0;
   unsigned long long* d_hdd = nullptr;  // keys then vals
   uint64_t hcap_dd = 0;
@@ -164,7 +143,6 @@ struct mpsf_ctx {
     return m;
   }
   uint32_t* d_remap_err = nullptr;
-  uint32_t* d_tctr = nullptr;   // kMaxChunks finalize tile counters (zeroed by k_init)
   // host-path buffers and the copy streams of the chunked pipeline
   uint8_t* d_io = nullptr;
   size_t io_cap = 0;
@@ -240,7 +218,7 @@ void mpsf_destroy(mpsf_ctx* c) {
   cudaFree(c->d_count_part);
   cudaFree(c->d_counter);
   cudaFree(c->d_small);
-  cudaFree(c->d_tiles);
+  cudaFree(c->d_masks);
   cudaFree(c->d_hdd);
   cudaFree(c->d_hnr);
   cudaFree(c->d_io);
@@ -434,7 +412,6 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   c->x_giso = s_giso; c->x_giso_n = 3ull * C;
   const size_t empty_bytes = o;
   const size_t s_ctrl = take(4 * C_NCTRL);
-  const size_t s_tctr = take(4 * kMaxChunks);   // finalize tile counters, one per chunk
   const size_t zero_bytes = o - empty_bytes;
   const size_t s_cst = take(sizeof(CState) * std::max<uint32_t>(C, 1));
   if (o > c->small_cap) {
@@ -470,21 +447,23 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   S.glob = reinterpret_cast<Globals*>(s + s_glob);
   S.err_idx = reinterpret_cast<unsigned long long*>(s + s_err);
   S.ctrl = reinterpret_cast<uint32_t*>(s + s_ctrl);
-  c->d_tctr = reinterpret_cast<uint32_t*>(s + s_tctr);
   S.cstate = reinterpret_cast<CState*>(s + s_cst);
   c->has_world = true;
   return MPSF_OK;
 }
 
 static int ensure_call_scratch(mpsf_ctx* c, uint64_t n) {
-  const uint64_t nt = tiles_for(n);
-  if (nt > c->tiles_cap) {
-    cudaFree(c->d_tiles);
-    c->d_tiles = nullptr;
+  const uint64_t nq = chunks_for(n), nseg = segments_for(n);
+  const uint64_t mbytes = 16 * std::max<uint64_t>(nq, 1) + 8 * std::max<uint64_t>(nseg, 1);
+  if (mbytes > c->tiles_cap) {
+    cudaFree(c->d_masks);
+    c->d_masks = nullptr;
     c->tiles_cap = 0;
-    CK(cudaMalloc(&c->d_tiles, 8 * std::max<uint64_t>(nt, 1)));
-    c->tiles_cap = nt;
+    CK(cudaMalloc(&c->d_masks, mbytes));
+    c->tiles_cap = mbytes;
   }
+  c->S.cmask = reinterpret_cast<ulonglong2*>(c->d_masks);
+  c->S.segcnt = reinterpret_cast<unsigned long long*>(c->d_masks + 16 * std::max<uint64_t>(nq, 1));
   const uint64_t floor_cap = 1ull << 16;
   if (c->want_dd == 0 || c->last_n != n) {
     const uint64_t guess = next_pow2(std::max<uint64_t>(floor_cap, std::min<uint64_t>(n / 32, 1ull << 24)));
@@ -512,7 +491,6 @@ static int ensure_call_scratch(mpsf_ctx* c, uint64_t n) {
   S.hnr.keys = c->d_hnr;
   S.hnr.mask = (uint32_t)(c->hcap_nr - 1);
   S.hnr.used_slot = C_HASH_NR;
-  S.tiles = c->d_tiles;
   return MPSF_OK;
 }
 
@@ -557,7 +535,6 @@ int mpsf_scan(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const mpsf_
 static int batch_init(mpsf_ctx* c, uint64_t n, const mpsf_params* p, uint64_t* d_counts, cudaStream_t st) {
   int rc = ensure_call_scratch(c, n);
   if (rc) return rc;
-  const uint64_t nt = tiles_for(n);
   InitSegs segs{};
   int k = 0;
   segs.p[k] = c->d_dd; segs.words[k] = c->W.n_pages * c->W.dd_groups; segs.val[k++] = EMPTY32;
@@ -567,7 +544,7 @@ static int batch_init(mpsf_ctx* c, uint64_t n, const mpsf_params* p, uint64_t* d
   }
   segs.p[k] = c->d_small; segs.words[k] = c->small_empty_bytes / 4; segs.val[k++] = EMPTY32;
   segs.p[k] = c->d_small + c->small_zero_off; segs.words[k] = c->small_zero_bytes / 4; segs.val[k++] = 0;
-  segs.p[k] = c->d_tiles; segs.words[k] = 2 * nt; segs.val[k++] = 0;
+  segs.p[k] = c->S.segcnt; segs.words[k] = 2 * segments_for(n); segs.val[k++] = 0;
   segs.p[k] = c->d_hdd; segs.words[k] = 4 * c->hcap_dd; segs.val[k++] = EMPTY32;
   segs.p[k] = c->d_hnr; segs.words[k] = 4 * c->hcap_nr; segs.val[k++] = EMPTY32;
   if (c->W.n_clients) { segs.p[k] = d_counts; segs.words[k] = 2ull * NSCEN * c->W.n_clients; segs.val[k++] = 0; }
@@ -636,16 +613,15 @@ int mpsf_finalize(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const m
   CK(cudaSetDevice(c->device));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const Marker mk = c->marker();
-  if (launch_finalize(c->W, c->S, d_in, n, to_params(p), d_out, reinterpret_cast<unsigned long long*>(d_dkeys), d_didx,
-                      d_cancel, 0, (uint32_t)tiles_for(n), c->d_tctr, st, mk))
+  if (launch_finalize(c->W, c->S, d_in, n, to_params(p), d_out, 0, st, mk)) return MPSF_E_CUDA;
+  if (launch_lists(c->S, d_in, d_out, n, p->base_index, reinterpret_cast<unsigned long long*>(d_dkeys), d_didx,
+                   d_cancel, st, mk))
     return MPSF_E_CUDA;
-  k_summary<<<1, 1, 0, st>>>(c->S.ctrl, c->S.err_idx, c->d_tiles, tiles_for(n), c->d_sum);
-  mk.mark("k_summary");
-  CK(cudaGetLastError());
+  if (launch_summary(c->S, n, c->d_sum, st, mk)) return MPSF_E_CUDA;
   CK(cudaEventRecord(c->ev_done, st));
   c->pending = true;
   c->last_n = n;
-  c->last_launches += n ? 2 : 1;
+  c->last_launches += n ? 3 : 1;
   return MPSF_OK;
 }
 
@@ -816,15 +792,15 @@ int mpsf_process_host(mpsf_ctx* c, const mpsf_fault_entry* h_in, uint64_t n, con
   uint32_t* d_di = reinterpret_cast<uint32_t*>(b + o_di);
   uint32_t* d_ca = reinterpret_cast<uint32_t*>(b + o_ca);
   if (p->base_index + n > MAX_GIDX) return MPSF_E_TOO_LARGE;
-  // chunk boundaries on finalize-tile multiples: chunk k = tiles [t_lo[k], t_lo[k+1])
-  const uint64_t te = tile_entries(), nt = tiles_for(n);
+  // chunk boundaries on 64-entry chunk multiples: host chunk k = entries [e_lo[k], e_lo[k+1])
+  const uint64_t ce = chunk_entries(), nq = chunks_for(n);
   const int nch = n >= (1ull << 20) ? kMaxChunks : n >= (1ull << 18) ? 4 : 1;
-  const uint64_t tpc = (nt + nch - 1) / nch;
-  uint64_t t_lo[kMaxChunks + 1];
+  const uint64_t qpc = (nq + nch - 1) / nch;
+  uint64_t q_lo[kMaxChunks + 1];
   int chunks = 0;
-  for (uint64_t t = 0; t < nt; t += tpc) t_lo[chunks++] = t;
-  t_lo[chunks] = nt;
-  auto ent = [&](int k) { return std::min<uint64_t>(t_lo[k] * te, n); };
+  for (uint64_t q = 0; q < nq; q += qpc) q_lo[chunks++] = q;
+  q_lo[chunks] = nq;
+  auto ent = [&](int k) { return std::min<uint64_t>(q_lo[k] * ce, n); };
 
   // attempt 0: pipelined.  H2D chunk k (h2d stream) || pass 1 on chunk k-1 (compute stream);
   // finalize chunk k (compute) || D2H of chunk k-1's records (d2h stream)
@@ -860,17 +836,17 @@ int mpsf_process_host(mpsf_ctx* c, const mpsf_fault_entry* h_in, uint64_t n, con
   }
   for (int k = 0; k < chunks; ++k) {
     const uint64_t lo = ent(k), cnt = ent(k + 1) - lo;
-    if (launch_finalize(c->W, c->S, d_in, n, P, d_out, d_dk, d_di, d_ca, (uint32_t)t_lo[k], (uint32_t)t_lo[k + 1],
-                        c->d_tctr + k, st, mk))
-      return MPSF_E_CUDA;
+    Params Pk = P;
+    Pk.base_index += lo;
+    if (launch_finalize(c->W, c->S, d_in + lo, cnt, Pk, d_out + lo, q_lo[k], st, mk)) return MPSF_E_CUDA;
     ++launches;
     CK(cudaEventRecord(c->ev_fin[k], st));
     CK(cudaStreamWaitEvent(c->d2h_stream, c->ev_fin[k], 0));
     CK(cudaMemcpyAsync(h_out + lo, d_out + lo, 8 * cnt, cudaMemcpyDeviceToHost, c->d2h_stream));
   }
-  k_summary<<<1, 1, 0, st>>>(c->S.ctrl, c->S.err_idx, c->d_tiles, nt, c->d_sum);
-  mk.mark("k_summary");
-  CK(cudaGetLastError());
+  if (launch_lists(c->S, d_in, d_out, n, p->base_index, d_dk, d_di, d_ca, st, mk)) return MPSF_E_CUDA;
+  if (launch_summary(c->S, n, c->d_sum, st, mk)) return MPSF_E_CUDA;
+  ++launches;
   CK(cudaEventRecord(c->ev_done, st));
   c->pending = true;
   c->last_n = n;

@@ -116,7 +116,16 @@ struct Scratch {
   Globals* glob;
   uint32_t* ctrl;      // [C_NCTRL]
   unsigned long long* err_idx;
-  unsigned long long* tiles;  // look-back descriptors of the finalize pass
+  ulonglong2* cmask;           // [chunks] (cancelled-entry mask, dedup-representative mask)
+  unsigned long long* segcnt;  // [segments] cancel count | dedup count << 32
+};
+
+// What mpsf_get_summary reads back after a batch.
+struct DevSummary {
+  uint32_t ctrl[C_NCTRL];
+  unsigned long long err_idx;
+  unsigned long long n_cancel;
+  unsigned long long n_dedup;
 };
 
 struct Params {

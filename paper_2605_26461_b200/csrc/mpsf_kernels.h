@@ -28,17 +28,21 @@ int launch_resolve(const World& W, const Scratch& S, const Params& P, mpsf_clien
 int launch_general(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
                    int stage, cudaStream_t st, const Marker& mk);
 int launch_resolve2(const World& W, const Scratch& S, const Params& P, cudaStream_t st, const Marker& mk);
-// finalize tiles [tile_lo, tile_hi) of the batch (entries indexed from `in`), dynamic order via
-// the zero-initialised counter tctr
+// pass 2 over entries [0, n) of `in`, a chunk of the batch starting at batch chunk q_base (the
+// chunk's first entry is batch entry 64 * q_base); then, once per batch, the ordered lists
 int launch_finalize(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
-                    mpsf_out_record* out, unsigned long long* dkeys, uint32_t* didx, uint32_t* cancel,
-                    uint32_t tile_lo, uint32_t tile_hi, uint32_t* tctr, cudaStream_t st, const Marker& mk);
-uint32_t tile_entries();   // entries per finalize tile (chunk boundaries must be multiples)
+                    mpsf_out_record* out, uint64_t q_base, cudaStream_t st, const Marker& mk);
+int launch_lists(const Scratch& S, const mpsf_fault_entry* in, const mpsf_out_record* out, uint64_t n,
+                 uint64_t base_index, unsigned long long* dkeys, uint32_t* didx, uint32_t* cancel, cudaStream_t st,
+                 const Marker& mk);
+int launch_summary(const Scratch& S, uint64_t n, DevSummary* out, cudaStream_t st, const Marker& mk);
+uint32_t chunk_entries();   // entries per chunk (host chunk boundaries must be multiples)
+uint64_t chunks_for(uint64_t n);
+uint64_t segments_for(uint64_t n);
 int launch_hash_export(const Hash& h, uint64_t cap, unsigned long long* keys, uint32_t* vals, uint32_t* counter,
                        uint64_t out_cap, cudaStream_t st);
 int launch_hash_merge(const Hash& h, uint32_t* ctrl, const unsigned long long* keys, const uint32_t* vals,
                       uint64_t count, cudaStream_t st);
-uint64_t tiles_for(uint64_t n);
 uint32_t count_parts_needed(const World& W);   // per-block count partial rows k_scan may write
 
 int launch_remap(uint64_t va_base, const uint64_t* phys, uint64_t npages4k, uint32_t gran_log2,
