@@ -748,6 +748,7 @@ __global__ void k_resolve2(World W, Scratch S, Params P) {
 // index order: a block per segment sums the counters of the earlier segments for its base and
 // scans its own chunks' popcounts -- no serial look-back between tiles.
 constexpr uint32_t SEG_CHUNKS = 1024;
+constexpr uint32_t KSTAGE = 8;     // dedup keys staged per chunk by k_finalize (more: k_lists re-derives)
 
 // Pass 2 per entry, in two halves so both entries of a lane issue their L2 lookups together:
 // fin_addr decodes and picks the words the verdict depends on (the dedup slot of its key,
@@ -914,10 +915,17 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const
     }
     const uint32_t bc0 = __ballot_sync(0xFFFFFFFFu, ok0 && c0), bc1 = __ballot_sync(0xFFFFFFFFu, ok1 && c1);
     const uint32_t bd0 = __ballot_sync(0xFFFFFFFFu, ok0 && r0), bd1 = __ballot_sync(0xFFFFFFFFu, ok1 && r1);
+    const uint64_t qq = q_base + i0 / WCHUNK;
+    if (bd0 | bd1) {                          // stage the chunk's first KSTAGE representative keys
+      const uint32_t lt = (1u << lane) - 1u;
+      const uint32_t rk0 = __popc(bd0 & lt) + __popc(bd1 & lt), rk1 = rk0 + (r0 && ok0 ? 1u : 0u);
+      if (ok0 && r0 && rk0 < KSTAGE) S.dstage[qq * KSTAGE + rk0] = k0;
+      if (ok1 && r1 && rk1 < KSTAGE) S.dstage[qq * KSTAGE + rk1] = k1;
+    }
     if (lane == 0) {
       const unsigned long long cm = spread2(bc0) | (spread2(bc1) << 1);
       const unsigned long long dm = spread2(bd0) | (spread2(bd1) << 1);
-      const uint64_t q = q_base + i0 / WCHUNK;
+      const uint64_t q = qq;
       S.cmask[q] = make_ulonglong2(cm, dm);
       if (cm | dm)
         atomicAdd(S.segcnt + q / SEG_CHUNKS, (unsigned long long)__popcll(cm) | ((unsigned long long)__popcll(dm) << 32));
@@ -965,9 +973,16 @@ __global__ void __launch_bounds__(1024, 2) k_lists(Scratch S, const mpsf_fault_e
   uint64_t pc = pre & 0xFFFFFFFFull, pd = pre >> 32;
   const uint32_t g0 = (uint32_t)(base_index + q * WCHUNK);
   for (unsigned long long m = mk.x; m; m &= m - 1) cancel[pc++] = g0 + (uint32_t)__ffsll((long long)m) - 1;
-  // dedup set: key from the entry (engine, page) and its OutRecord (client, scenario); two
-  // representatives per round so their loads overlap
+  // dedup set: the first KSTAGE keys of the chunk were staged by k_finalize; later ones come
+  // from the entry (engine, page) and its OutRecord (client, scenario), two per round
   unsigned long long m = mk.y;
+  for (uint32_t r = 0; m && r < KSTAGE; ++r) {
+    const uint32_t b = (uint32_t)__ffsll((long long)m) - 1;
+    m &= m - 1;
+    dkeys[pd] = __ldcg(S.dstage + q * KSTAGE + r);
+    didx[pd] = g0 + b;
+    ++pd;
+  }
   while (m) {
     const uint32_t b0 = (uint32_t)__ffsll((long long)m) - 1;
     m &= m - 1;
@@ -975,10 +990,10 @@ __global__ void __launch_bounds__(1024, 2) k_lists(Scratch S, const mpsf_fault_e
     const uint32_t b1 = two ? (uint32_t)__ffsll((long long)m) - 1 : b0;
     if (two) m &= m - 1;
     const uint64_t i0 = q * WCHUNK + b0, i1 = q * WCHUNK + b1;
-    const uint4 e0 = __ldg(reinterpret_cast<const uint4*>(in) + i0);
-    const uint4 e1 = __ldg(reinterpret_cast<const uint4*>(in) + i1);
-    const unsigned long long r0 = __ldg(reinterpret_cast<const unsigned long long*>(out) + i0);
-    const unsigned long long r1 = __ldg(reinterpret_cast<const unsigned long long*>(out) + i1);
+    const uint4 e0 = __ldcs(reinterpret_cast<const uint4*>(in) + i0);
+    const uint4 e1 = __ldcs(reinterpret_cast<const uint4*>(in) + i1);
+    const unsigned long long r0 = __ldcs(reinterpret_cast<const unsigned long long*>(out) + i0);
+    const unsigned long long r1 = __ldcs(reinterpret_cast<const unsigned long long*>(out) + i1);
     dkeys[pd] = dedup_key((uint32_t)(r0 >> 48), (int)(e0.w & 0xFF), (int)((r0 >> 32) & 0xFF),
                           ((uint64_t)e0.x | ((uint64_t)e0.y << 32)) >> 12);
     didx[pd] = g0 + b0;

@@ -118,6 +118,7 @@ struct Scratch {
   unsigned long long* err_idx;
   ulonglong2* cmask;           // [chunks] (cancelled-entry mask, dedup-representative mask)
   unsigned long long* segcnt;  // [segments] cancel count | dedup count << 32
+  unsigned long long* dstage;  // [chunks][KSTAGE] first dedup keys of each chunk (k_finalize -> k_lists)
 };
 
 // What mpsf_get_summary reads back after a batch.

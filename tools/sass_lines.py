@@ -1,6 +1,6 @@
 """Per-source-line instruction counts and stall samples from an ncu report (experiment tool).
 
-    python tools/sass_lines.py report.ncu-rep lib.so kernel-mangled-substring [top]
+    python tools/sass_lines.py report.ncu-rep lib.so kernel-mangled-substring [top] [ncu-kernel-regex]
 
 Exports the report's SASS page, disassembles the same kernel from the library with line info
 (nvdisasm -g), maps SASS offsets to (file, line) and aggregates executed warp instructions and
@@ -20,8 +20,11 @@ import tempfile
 def main():
     rep, lib, kname = sys.argv[1], sys.argv[2], sys.argv[3]
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                         capture_output=True, text=True).stdout
+    demangled = sys.argv[5] if len(sys.argv) > 5 else None
+    cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"]
+    if demangled:
+        cmd += ["-k", "regex:" + demangled]
+    out = subprocess.run(cmd, capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr = rows[1]
     ia = hdr.index("Instructions Executed")
