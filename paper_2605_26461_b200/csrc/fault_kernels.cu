@@ -748,7 +748,7 @@ __global__ void k_resolve2(World W, Scratch S, Params P) {
 // index order: a block per segment sums the counters of the earlier segments for its base and
 // scans its own chunks' popcounts -- no serial look-back between tiles.
 constexpr uint32_t SEG_CHUNKS = 1024;
-constexpr uint32_t KSTAGE = 8;     // dedup keys staged per chunk by k_finalize (more: k_lists re-derives)
+constexpr uint32_t KSTAGE = WCHUNK;   // dedup keys staged per chunk by k_finalize, in index order
 
 // Pass 2 per entry, in two halves so both entries of a lane issue their L2 lookups together:
 // fin_addr decodes and picks the words the verdict depends on (the dedup slot of its key,
@@ -868,6 +868,14 @@ __device__ __forceinline__ void fin_resolve(const World& W, const View& v, const
        ((unsigned long long)c << 48);
 }
 
+// Store that asks the L2 to keep the line (evict-last): the staged dedup keys are re-read by
+// k_lists after the finalize stream has passed through the L2.
+__device__ __forceinline__ void st_keep(unsigned long long* p, unsigned long long v) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
+}
+
 // Spread the 32 bits of x to the even bits of a 64-bit word (bit i -> bit 2i).
 __device__ __forceinline__ unsigned long long spread2(uint32_t x) {
   unsigned long long v = x;
@@ -916,11 +924,11 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const
     const uint32_t bc0 = __ballot_sync(0xFFFFFFFFu, ok0 && c0), bc1 = __ballot_sync(0xFFFFFFFFu, ok1 && c1);
     const uint32_t bd0 = __ballot_sync(0xFFFFFFFFu, ok0 && r0), bd1 = __ballot_sync(0xFFFFFFFFu, ok1 && r1);
     const uint64_t qq = q_base + i0 / WCHUNK;
-    if (bd0 | bd1) {                          // stage the chunk's first KSTAGE representative keys
+    if (bd0 | bd1) {                          // stage the chunk's representative keys by rank
       const uint32_t lt = (1u << lane) - 1u;
       const uint32_t rk0 = __popc(bd0 & lt) + __popc(bd1 & lt), rk1 = rk0 + (r0 && ok0 ? 1u : 0u);
-      if (ok0 && r0 && rk0 < KSTAGE) S.dstage[qq * KSTAGE + rk0] = k0;
-      if (ok1 && r1 && rk1 < KSTAGE) S.dstage[qq * KSTAGE + rk1] = k1;
+      if (ok0 && r0) st_keep(S.dstage + qq * KSTAGE + rk0, k0);
+      if (ok1 && r1) st_keep(S.dstage + qq * KSTAGE + rk1, k1);
     }
     if (lane == 0) {
       const unsigned long long cm = spread2(bc0) | (spread2(bc1) << 1);
@@ -945,11 +953,14 @@ __global__ void __launch_bounds__(1024, 2) k_lists(Scratch S, const mpsf_fault_e
   if (__ldcg(S.ctrl + C_ERR) != 0) return;
   __shared__ unsigned long long s_base;
   __shared__ unsigned long long s_w[32];
+  unsigned long long t_start = 0;
+  if (MPSF_ABLATE & 8192) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t seg = blockIdx.x;
   // base: counts of all earlier segments
   unsigned long long acc = 0;
-  for (uint64_t i = threadIdx.x; i < seg; i += blockDim.x) acc += __ldcg(S.segcnt + i);
+  if (!(MPSF_ABLATE & 2048))
+    for (uint64_t i = threadIdx.x; i < seg; i += blockDim.x) acc += __ldcg(S.segcnt + i);
   if (threadIdx.x == 0) s_base = 0;
   __syncthreads();
 #pragma unroll
@@ -970,39 +981,82 @@ __global__ void __launch_bounds__(1024, 2) k_lists(Scratch S, const mpsf_fault_e
   unsigned long long pre = s_base;
   for (uint32_t w = 0; w < warp; ++w) pre += s_w[w];
   pre += x - mine;
-  uint64_t pc = pre & 0xFFFFFFFFull, pd = pre >> 32;
+  const uint64_t pc = pre & 0xFFFFFFFFull;
+  uint64_t pd = pre >> 32;
   const uint32_t g0 = (uint32_t)(base_index + q * WCHUNK);
-  for (unsigned long long m = mk.x; m; m &= m - 1) cancel[pc++] = g0 + (uint32_t)__ffsll((long long)m) - 1;
-  // dedup set: the first KSTAGE keys of the chunk were staged by k_finalize; later ones come
-  // from the entry (engine, page) and its OutRecord (client, scenario), two per round
-  unsigned long long m = mk.y;
-  for (uint32_t r = 0; m && r < KSTAGE; ++r) {
-    const uint32_t b = (uint32_t)__ffsll((long long)m) - 1;
-    m &= m - 1;
-    dkeys[pd] = __ldcg(S.dstage + q * KSTAGE + r);
-    didx[pd] = g0 + b;
-    ++pd;
+  // cancel list: the warp writes its 32 chunks one at a time, lane l the chunk's entries 2l, 2l+1
+  // (consecutive positions: coalesced stores)
+  if (!(MPSF_ABLATE & 512)) {
+    const unsigned long long below = (1ull << (2 * lane)) - 1ull;
+    for (int j = 0; j < 32; ++j) {
+      const unsigned long long cm = __shfl_sync(0xFFFFFFFFu, mk.x, j);
+      if (!cm) continue;
+      const uint64_t cbj = __shfl_sync(0xFFFFFFFFu, pc, j);
+      const uint32_t gj = __shfl_sync(0xFFFFFFFFu, g0, j) + 2 * lane;
+      const uint32_t two = (uint32_t)(cm >> (2 * lane)) & 3u;
+      uint64_t pos = cbj + __popcll(cm & below);
+      if (two & 1u) cancel[pos++] = gj;
+      if (two & 2u) cancel[pos] = gj + 1;
+    }
   }
-  while (m) {
-    const uint32_t b0 = (uint32_t)__ffsll((long long)m) - 1;
-    m &= m - 1;
-    const bool two = m != 0;
-    const uint32_t b1 = two ? (uint32_t)__ffsll((long long)m) - 1 : b0;
-    if (two) m &= m - 1;
-    const uint64_t i0 = q * WCHUNK + b0, i1 = q * WCHUNK + b1;
-    const uint4 e0 = __ldcs(reinterpret_cast<const uint4*>(in) + i0);
-    const uint4 e1 = __ldcs(reinterpret_cast<const uint4*>(in) + i1);
-    const unsigned long long r0 = __ldcs(reinterpret_cast<const unsigned long long*>(out) + i0);
-    const unsigned long long r1 = __ldcs(reinterpret_cast<const unsigned long long*>(out) + i1);
-    dkeys[pd] = dedup_key((uint32_t)(r0 >> 48), (int)(e0.w & 0xFF), (int)((r0 >> 32) & 0xFF),
-                          ((uint64_t)e0.x | ((uint64_t)e0.y << 32)) >> 12);
-    didx[pd] = g0 + b0;
-    ++pd;
-    if (two) {
-      dkeys[pd] = dedup_key((uint32_t)(r1 >> 48), (int)(e1.w & 0xFF), (int)((r1 >> 32) & 0xFF),
-                            ((uint64_t)e1.x | ((uint64_t)e1.y << 32)) >> 12);
-      didx[pd] = g0 + b1;
-      ++pd;
+  // dedup set: the warp's representatives occupy consecutive positions from its first chunk's
+  // offset on; lane l writes flat ranks l, l + 32, ... (coalesced), finding each rank's chunk by
+  // a shuffle search over the chunks' exclusive rep counts.  Keys were staged by k_finalize.
+  {
+    const unsigned long long dm_l = (MPSF_ABLATE & 1024) ? 0ull : mk.y;
+    const uint32_t cnt = (uint32_t)__popcll(dm_l);
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+      if (lane >= o) inc += u;
+    }
+    const uint32_t exc = inc - cnt;
+    const uint32_t R = __shfl_sync(0xFFFFFFFFu, inc, 31);
+    const uint64_t pd0 = __shfl_sync(0xFFFFFFFFu, pd, 0);
+    const uint64_t q0w = q - lane;
+    for (uint32_t r0 = 0; r0 < R; r0 += 128) {
+      unsigned long long key[4];
+      uint32_t gix[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const uint32_t f = r0 + 32 * h + lane;
+        // largest j with exc_j <= f (exc is non-decreasing over lanes)
+        uint32_t j = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const uint32_t e = __shfl_sync(0xFFFFFFFFu, exc, j + step);
+          if (e <= f) j += step;
+        }
+        const uint32_t ej = __shfl_sync(0xFFFFFFFFu, exc, j);
+        const unsigned long long dmj = __shfl_sync(0xFFFFFFFFu, dm_l, j);
+        const uint32_t k = f - ej;
+        const uint32_t lo = (uint32_t)dmj, clo = __popc(lo);
+        const uint32_t bit = k < clo ? __fns(lo, 0, (int)k + 1) : 32 + __fns((uint32_t)(dmj >> 32), 0, (int)(k - clo) + 1);
+        key[h] = f < R ? __ldcg(S.dstage + (q0w + j) * KSTAGE + k) : 0ull;
+        gix[h] = (uint32_t)(base_index + (q0w + j) * WCHUNK) + bit;
+      }
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const uint32_t f = r0 + 32 * h + lane;
+        if (f < R) {
+          dkeys[pd0 + f] = key[h];
+          didx[pd0 + f] = gix[h];
+        }
+      }
+    }
+  }
+  if (MPSF_ABLATE & 8192) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t_end;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      reinterpret_cast<unsigned long long*>(cancel)[(nq + 2) / 2 * 0 + 4 * blockIdx.x + 0] = t_start;
+      reinterpret_cast<unsigned long long*>(cancel)[4 * blockIdx.x + 1] = t_end;
+      reinterpret_cast<unsigned long long*>(cancel)[4 * blockIdx.x + 2] = smid;
+      reinterpret_cast<unsigned long long*>(cancel)[4 * blockIdx.x + 3] = mk.y;
     }
   }
 }
