@@ -541,9 +541,10 @@ __global__ void __launch_bounds__(BLOCK, 1) k_scan(World W, Scratch S, const mps
   q_drain(q, qn, S, v.used);
   if (kStaged) {
     __syncthreads();
-    uint32_t* part = count_part + (uint64_t)blockIdx.x * NSCEN * W.n_clients;
-    // accumulate: a batch may be scanned in several launches (chunked host pipeline)
-    for (uint32_t i = threadIdx.x; i < NSCEN * W.n_clients; i += blockDim.x) part[i] += v.counts[i];
+    // fold the block's (client, scenario) counts into the batch counts (accumulates across the
+    // launches of a chunked batch)
+    for (uint32_t i = threadIdx.x; i < NSCEN * W.n_clients; i += blockDim.x)
+      if (v.counts[i]) atomicAdd(counts + i, (unsigned long long)v.counts[i]);
     flush_minima(W, S, v);
   }
 }
@@ -945,12 +946,25 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const
 // thread per chunk: a block-wide scan of the chunks' popcounts gives every chunk its offsets,
 // then each thread writes its own chunk's entries (the L2 merges the short runs).  `in` /
 // `out` / the masks cover the whole batch (nq chunks).
+__device__ __forceinline__ void write_summary(const Scratch& S, unsigned long long tot, DevSummary* out) {
+  for (int i = 0; i < C_NCTRL; ++i) out->ctrl[i] = __ldcg(S.ctrl + i);
+  out->err_idx = __ldcg(S.err_idx);
+  const bool err = out->ctrl[C_ERR] != 0;
+  out->n_cancel = err ? 0 : (tot & 0xFFFFFFFFull);
+  out->n_dedup = err ? 0 : (tot >> 32);
+}
+
 __global__ void __launch_bounds__(1024, 2) k_lists(Scratch S, const mpsf_fault_entry* __restrict__ in,
                                                    const mpsf_out_record* __restrict__ out, uint64_t nq,
                                                    uint64_t base_index, unsigned long long* __restrict__ dkeys,
-                                                   uint32_t* __restrict__ didx, uint32_t* __restrict__ cancel) {
+                                                   uint32_t* __restrict__ didx, uint32_t* __restrict__ cancel,
+                                                   DevSummary* __restrict__ sum) {
   static_assert(SEG_CHUNKS == 1024, "one thread per chunk");
-  if (__ldcg(S.ctrl + C_ERR) != 0) return;
+  const bool last = blockIdx.x == gridDim.x - 1;
+  if (__ldcg(S.ctrl + C_ERR) != 0) {
+    if (last && threadIdx.x == 0) write_summary(S, 0, sum);
+    return;
+  }
   __shared__ unsigned long long s_base;
   __shared__ unsigned long long s_w[32];
   unsigned long long t_start = 0;
@@ -980,6 +994,7 @@ __global__ void __launch_bounds__(1024, 2) k_lists(Scratch S, const mpsf_fault_e
   __syncthreads();
   unsigned long long pre = s_base;
   for (uint32_t w = 0; w < warp; ++w) pre += s_w[w];
+  if (last && threadIdx.x == blockDim.x - 1) write_summary(S, pre + x, sum);   // batch totals
   pre += x - mine;
   const uint64_t pc = pre & 0xFFFFFFFFull;
   uint64_t pd = pre >> 32;
@@ -1129,7 +1144,8 @@ static bool staged_fits(const World& W) {
 }
 
 uint32_t count_parts_needed(const World& W) {
-  return staged_fits(W) ? (uint32_t)(2 * sm_count()) : 0u;
+  (void)W;
+  return 0u;   // k_scan folds its block counts with atomics
 }
 
 template <bool kStaged>
@@ -1240,19 +1256,18 @@ int launch_finalize(const World& W, const Scratch& S, const mpsf_fault_entry* in
                         : finalize_t<false>(W, S, in, n, P, out, q_base, st, mk);
 }
 
+// cancel list + dedup set + the batch summary (k_summary alone when there is nothing to list)
 int launch_lists(const Scratch& S, const mpsf_fault_entry* in, const mpsf_out_record* out, uint64_t n,
-                 uint64_t base_index, unsigned long long* dkeys, uint32_t* didx, uint32_t* cancel, cudaStream_t st,
-                 const Marker& mk) {
+                 uint64_t base_index, unsigned long long* dkeys, uint32_t* didx, uint32_t* cancel, DevSummary* sum,
+                 cudaStream_t st, const Marker& mk) {
   const uint64_t nseg = segments_for(n);
-  if (nseg == 0) return 0;
-  k_lists<<<(unsigned)nseg, 1024, 0, st>>>(S, in, out, chunks_for(n), base_index, dkeys, didx, cancel);
+  if (nseg == 0) {
+    k_summary<<<1, 1024, 0, st>>>(S, 0, sum);
+    mk.mark("k_summary");
+    return ok_or_err();
+  }
+  k_lists<<<(unsigned)nseg, 1024, 0, st>>>(S, in, out, chunks_for(n), base_index, dkeys, didx, cancel, sum);
   mk.mark("k_lists");
-  return ok_or_err();
-}
-
-int launch_summary(const Scratch& S, uint64_t n, DevSummary* out, cudaStream_t st, const Marker& mk) {
-  k_summary<<<1, 1024, 0, st>>>(S, segments_for(n), out);
-  mk.mark("k_summary");
   return ok_or_err();
 }
 

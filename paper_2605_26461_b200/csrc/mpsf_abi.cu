@@ -616,13 +616,12 @@ int mpsf_finalize(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const m
   const Marker mk = c->marker();
   if (launch_finalize(c->W, c->S, d_in, n, to_params(p), d_out, 0, st, mk)) return MPSF_E_CUDA;
   if (launch_lists(c->S, d_in, d_out, n, p->base_index, reinterpret_cast<unsigned long long*>(d_dkeys), d_didx,
-                   d_cancel, st, mk))
+                   d_cancel, c->d_sum, st, mk))
     return MPSF_E_CUDA;
-  if (launch_summary(c->S, n, c->d_sum, st, mk)) return MPSF_E_CUDA;
   CK(cudaEventRecord(c->ev_done, st));
   c->pending = true;
   c->last_n = n;
-  c->last_launches += n ? 3 : 1;
+  c->last_launches += n ? 2 : 1;
   return MPSF_OK;
 }
 
@@ -845,8 +844,7 @@ int mpsf_process_host(mpsf_ctx* c, const mpsf_fault_entry* h_in, uint64_t n, con
     CK(cudaStreamWaitEvent(c->d2h_stream, c->ev_fin[k], 0));
     CK(cudaMemcpyAsync(h_out + lo, d_out + lo, 8 * cnt, cudaMemcpyDeviceToHost, c->d2h_stream));
   }
-  if (launch_lists(c->S, d_in, d_out, n, p->base_index, d_dk, d_di, d_ca, st, mk)) return MPSF_E_CUDA;
-  if (launch_summary(c->S, n, c->d_sum, st, mk)) return MPSF_E_CUDA;
+  if (launch_lists(c->S, d_in, d_out, n, p->base_index, d_dk, d_di, d_ca, c->d_sum, st, mk)) return MPSF_E_CUDA;
   ++launches;
   CK(cudaEventRecord(c->ev_done, st));
   c->pending = true;

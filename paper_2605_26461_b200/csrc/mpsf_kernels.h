@@ -33,9 +33,8 @@ int launch_resolve2(const World& W, const Scratch& S, const Params& P, cudaStrea
 int launch_finalize(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
                     mpsf_out_record* out, uint64_t q_base, cudaStream_t st, const Marker& mk);
 int launch_lists(const Scratch& S, const mpsf_fault_entry* in, const mpsf_out_record* out, uint64_t n,
-                 uint64_t base_index, unsigned long long* dkeys, uint32_t* didx, uint32_t* cancel, cudaStream_t st,
-                 const Marker& mk);
-int launch_summary(const Scratch& S, uint64_t n, DevSummary* out, cudaStream_t st, const Marker& mk);
+                 uint64_t base_index, unsigned long long* dkeys, uint32_t* didx, uint32_t* cancel, DevSummary* sum,
+                 cudaStream_t st, const Marker& mk);
 uint32_t chunk_entries();   // entries per chunk (host chunk boundaries must be multiples)
 uint64_t chunks_for(uint64_t n);
 uint64_t segments_for(uint64_t n);
