@@ -280,7 +280,7 @@ def run_mine(args):
                        "n_dedup": nd, "n_cancel": nc},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic,
-                         "kernel": "whole mpsf_process step (k_init..k_summary, every launch)",
+                         "kernel": "whole mpsf_process step (k_init..k_lists, every launch)",
                          "alg_bytes_per_step": B, "peak_source": peak_src},
             "kernels": kernels,
             "cpu_baseline": cpu_baseline,
