@@ -79,7 +79,7 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 __host__ __device__ inline uint32_t al16(uint64_t x) { return (uint32_t)((x + 15) & ~uint64_t(15)); }
 
 struct Layout {
-  uint32_t lut, cinfo, queue;
+  uint32_t lut, slut, cinfo, queue;
   uint32_t pg_base, pg_end, poff, rattr, rrid, skip, chan;
   uint32_t c64, iso, r32, counts, used, cstate, total;
   uint32_t rep_chan;
@@ -103,6 +103,7 @@ __host__ __device__ inline Layout make_layout(const World& W, bool staged, bool 
   uint32_t o = 0;
   L.rep_chan = staged ? 32u : 0u;
   L.lut = o; o += 4 * LUT_N;
+  L.slut = o; o += 4 * 32;
   L.queue = o; if (!fin) o += WARPS * QCAP * 16;
   L.cinfo = o; if (staged) o += al16(512ull * nc);
   L.pg_base = o; if (staged) o += al16(4ull * nr);
@@ -345,6 +346,39 @@ __device__ __forceinline__ void ldg_stream(const mpsf_fault_entry* in, uint64_t 
   }
 }
 
+// Flags of a scenario id alone (the pass-1 record keeps the scenario, not the LUT index): the
+// lut_word bits that do not depend on the range or the access.
+__device__ __forceinline__ uint32_t scen_word(int sid, bool isolation) {
+  if (sid >= 28) return 0u;
+  if (sid >= 23) return LF_VALID | LF_XKIND | (uint32_t)sid | LF_REPL | LF_FATAL;
+  if (sid >= 18) return LF_VALID | LF_XKIND | (uint32_t)sid | LF_TRAP;
+  const bool repl = s_replayable(sid), serv = s_serviceable(sid);
+  return LF_VALID | (uint32_t)sid | (repl ? (LF_REPL | LF_DD) : 0u) |
+         (serv ? LF_SERV : (isolation ? LF_ELIG : LF_FATAL));
+}
+
+// The pass-1 record stream: lane l of a warp-chunk reads records 2l, 2l+1 with one 16-byte
+// load, the next chunk's pair requested before the current one is processed.
+template <typename F>
+__device__ __forceinline__ void rec_stream(const unsigned long long* rec, uint64_t n, F&& fn) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp, GW = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  const uint64_t nch = (n + WCHUNK - 1) / WCHUNK;
+  const bool a16 = ((uintptr_t)rec & 15u) == 0;
+  auto ld = [&](uint64_t i0) {
+    if (a16 && i0 + 1 < n) return __ldcs(reinterpret_cast<const ulonglong2*>(rec + i0));
+    return make_ulonglong2(i0 < n ? __ldcs(rec + i0) : 0ull, i0 + 1 < n ? __ldcs(rec + i0 + 1) : 0ull);
+  };
+  ulonglong2 nx = make_ulonglong2(0, 0);
+  if (gw < nch) nx = ld(gw * WCHUNK + 2 * lane);
+  for (uint64_t c = gw; c < nch; c += GW) {
+    const ulonglong2 r = nx;
+    if (c + GW < nch) nx = ld((c + GW) * WCHUNK + 2 * lane);
+    const uint64_t i0 = c * WCHUNK + 2 * lane;
+    fn(r, i0, i0 < n, i0 + 1 < n);
+  }
+}
+
 // ---- pass 1 ---------------------------------------------------------------------------------
 // After its block-local part (counts and per-client / per-range minima in shared memory) an
 // entry leaves at most two first-in-group minima on global tables: its dedup key (rule C2,
@@ -360,7 +394,59 @@ struct ScanOut {
   bool qn, qd;                   // deferred hash ops: NR key (hnr), dedup key (hdd)
   uint32_t c, eng, sid;          // key material (hash ops, claim fallback)
   uint64_t page;
+  unsigned long long rec;        // pass-1 record (fixed-layout worlds)
 };
+
+// ---- pass-1 record (worlds within the FX limits) ----------------------------------------------
+// k_scan leaves every entry's decode in one 8-byte record so pass 2 reads 8 bytes instead of
+// the 16-byte entry and skips the decode:
+//   [4:0] scenario  [10:5] client  [21:11] range index  [23:22] loc (0 skipped, 1 in range,
+//   2 guard page, 3 no range / not a translation)  [25:24] channel engine  [26] standalone
+//   [28:27] mechanism class m  [29] page >= 2^32 (pass 2 re-reads the entry)
+//   [63:32] page slot (in range / guard) or the page number (no range)
+constexpr uint32_t LOC_SKIP = 0, LOC_IN = 1, LOC_GUARD = 2, LOC_NONE = 3;
+
+__device__ __forceinline__ unsigned long long pack_rec(const Dec& d) {
+  if (!d.f) return 0ull;
+  const uint32_t loc = d.inr ? LOC_IN : (d.guard ? LOC_GUARD : LOC_NONE);
+  const uint64_t page = d.va >> 12;
+  const bool inw = d.inr || d.guard;
+  const uint32_t lo = (d.f & LF_S) | ((d.c & 63u) << 5) | ((inw ? d.ridx & 0x7FFu : 0u) << 11) | (loc << 22) |
+                      (((d.cw >> 16) & 3u) << 24) | (((d.cw >> 18) & 1u) << 26) | (((d.f >> LF_M_SH) & 3u) << 27) |
+                      ((!inw && (page >> 32)) ? (1u << 29) : 0u);
+  const uint32_t hi = inw ? d.slot : (uint32_t)page;
+  return (unsigned long long)lo | ((unsigned long long)hi << 32);
+}
+
+// Rebuilds the Dec of a record (the LUT word from the scenario, the page of in-world entries
+// from the range row).  Returns false for a skipped entry.
+__device__ __forceinline__ bool unpack_rec(const View& v, const uint32_t* slut, unsigned long long r,
+                                           const mpsf_fault_entry* in, uint64_t i, Dec& d) {
+  const uint32_t lo = (uint32_t)r, hi = (uint32_t)(r >> 32);
+  const uint32_t loc = (lo >> 22) & 3u;
+  d.f = 0; d.c = 0; d.cw = 0; d.inr = false; d.guard = false; d.ridx = NO_RID; d.slot = 0; d.va = 0;
+  if (loc == LOC_SKIP) return false;
+  const uint32_t sid = lo & 31u, ceng = (lo >> 24) & 3u;
+  d.c = (lo >> 5) & 63u;
+  d.cw = d.c | (ceng << 16) | (((lo >> 26) & 1u) << 18) | CH_VALID;
+  uint32_t group;
+  if (ceng == 0) group = sid == 15 ? 2u : ((sid >= 1 && sid <= 3) ? 1u : 0u);
+  else group = 2u + ceng;
+  d.f = slut[sid] | (((lo >> 27) & 3u) << LF_M_SH) | (group << LF_GROUP_SH);
+  d.inr = loc == LOC_IN;
+  d.guard = loc == LOC_GUARD;
+  if (d.inr || d.guard) {
+    d.ridx = (lo >> 11) & 0x7FFu;
+    d.slot = hi;
+    d.va = (uint64_t)(v.T.pg_base[d.ridx] + (hi - v.T.poff[d.ridx])) << 12;
+  } else if (lo & (1u << 29)) {
+    const uint4 e = __ldcs(reinterpret_cast<const uint4*>(in) + i);   // page beyond 32 bits: re-read
+    d.va = (uint64_t)e.x | ((uint64_t)e.y << 32);
+  } else {
+    d.va = (uint64_t)hi << 12;
+  }
+  return true;
+}
 
 __device__ __forceinline__ unsigned long long scan_dkey(const ScanOut& o) {
   return dedup_key(o.c, (int)o.eng, (int)o.sid, o.page);
@@ -426,6 +512,7 @@ __device__ __forceinline__ void scan_fast(const World& W, const View& v, const S
   o.qn = elig && !inw && !(MPSF_ABLATE & 1);
   o.qd = dd && !inw && !(MPSF_ABLATE & 1);
   o.c = c; o.eng = e.w & 0xFF; o.sid = sid; o.page = d.va >> 12;
+  o.rec = pack_rec(d);
 }
 
 // Claimed-slot dedup (sparse worlds): first claim wins the page for its group; a record of
@@ -519,6 +606,14 @@ __global__ void __launch_bounds__(BLOCK, 1) k_scan(World W, Scratch S, const mps
     if (!ok1) e1.w = 0;
     scan_fast<kStaged>(W, v, S, e0, P.base_index + i0, counts, o0);
     scan_fast<kStaged>(W, v, S, e1, P.base_index + i1, counts, o1);
+    if (kStaged) {                                     // pass-1 records, two per lane (16 bytes)
+      unsigned long long* rp = S.drec + (P.base_index - S.drec_base) + i0;
+      if (ok1 && (((uintptr_t)rp & 15u) == 0)) *reinterpret_cast<ulonglong2*>(rp) = make_ulonglong2(o0.rec, o1.rec);
+      else {
+        if (ok0) rp[0] = o0.rec;
+        if (ok1) rp[1] = o1.rec;
+      }
+    }
     // the L2 pre-check loads of both entries in flight together
     const uint32_t ra0 = o0.pa ? __ldcg(o0.pa) : 0u, rd0 = o0.pd ? __ldcg(o0.pd) : 0u;
     const uint32_t ra1 = o1.pa ? __ldcg(o1.pa) : 0u, rd1 = o1.pd ? __ldcg(o1.pd) : 0u;
@@ -768,9 +863,9 @@ struct FinA {
 };
 
 template <bool kStaged>
-__device__ __forceinline__ void fin_addr(const World& W, const View& v, const Scratch& S, uint4 e, uint64_t gidx,
-                                         FinA& a) {
-  a.d = decode_fast(v.T, W.page_state, S, e, gidx, threadIdx.x & 31);
+__device__ __forceinline__ void fin_addr(const World& W, const View& v, const Scratch& S, const Dec& dd,
+                                         uint64_t gidx, FinA& a) {
+  a.d = dd;
   const Dec& d = a.d;
   const uint32_t f = d.f;
   a.pd = a.pn = a.pe = nullptr;
@@ -804,7 +899,7 @@ __device__ __forceinline__ void fin_addr(const World& W, const View& v, const Sc
 
 template <bool kStaged>
 __device__ __forceinline__ void fin_resolve(const World& W, const View& v, const Scratch& S, const Globals& G,
-                                            uint4 e, uint64_t gidx, const FinA& a, uint32_t wd, uint32_t wn,
+                                            uint64_t gidx, const FinA& a, uint32_t wd, uint32_t wn,
                                             uint32_t we, unsigned long long& o8, bool& canc, bool& rep,
                                             unsigned long long& key) {
   const Dec& d = a.d;
@@ -832,7 +927,7 @@ __device__ __forceinline__ void fin_resolve(const World& W, const View& v, const
     const uint32_t page_hi = (uint32_t)(d.va >> 12);
     if (f & LF_DD) {                                               // rule C2: smallest index of the key
       const uint32_t group = (f >> LF_GROUP_SH) & 7u;
-      key = dedup_key(c, (int)(e.w & 0xFF), (int)sid, d.va >> 12);
+      key = dedup_key(c, (int)((d.cw >> 16) & 3u), (int)sid, d.va >> 12);   // translation: engine == channel's
       uint32_t ri;
       if (!a.hd && wd != EMPTY32 && (wd & 7u) == group) ri = wd >> 3;
       else ri = hash_get(S.hdd, key);
@@ -901,21 +996,22 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const
   const Globals G = *S.glob;
   __syncthreads();
   const uint32_t lane = threadIdx.x & 31;
-  ldg_stream(in, n, [&](uint4 e0, uint64_t i0, bool ok0, uint4 e1, uint64_t i1, bool ok1) {
-    if (!ok0) e0.w = 0;                       // past the end: decodes as a skipped entry
-    if (!ok1) e1.w = 0;
-    if (MPSF_ABLATE & 256) { e0.w = 0; e1.w = 0; }
+  uint32_t* slut = reinterpret_cast<uint32_t*>(smem + L.slut);
+  for (uint32_t k = threadIdx.x; k < 32; k += blockDim.x) slut[k] = scen_word((int)k, P.flags & MPSF_PF_ISOLATION);
+  __syncthreads();
+  auto body = [&](const Dec& d0, const Dec& d1, uint64_t i0, bool ok0, bool ok1) {
+    const uint64_t i1 = i0 + 1;
     FinA a0, a1;
-    fin_addr<kStaged>(W, v, S, e0, P.base_index + i0, a0);
-    fin_addr<kStaged>(W, v, S, e1, P.base_index + i1, a1);
+    fin_addr<kStaged>(W, v, S, d0, P.base_index + i0, a0);
+    fin_addr<kStaged>(W, v, S, d1, P.base_index + i1, a1);
     const uint32_t wd0 = a0.pd ? __ldcg(a0.pd) : EMPTY32, wn0 = a0.pn ? __ldcg(a0.pn) : EMPTY32;
     const uint32_t we0 = a0.pe ? __ldcg(a0.pe) : EMPTY32;
     const uint32_t wd1 = a1.pd ? __ldcg(a1.pd) : EMPTY32, wn1 = a1.pn ? __ldcg(a1.pn) : EMPTY32;
     const uint32_t we1 = a1.pe ? __ldcg(a1.pe) : EMPTY32;
     unsigned long long o0, o1, k0, k1;
     bool c0, c1, r0, r1;
-    fin_resolve<kStaged>(W, v, S, G, e0, P.base_index + i0, a0, wd0, wn0, we0, o0, c0, r0, k0);
-    fin_resolve<kStaged>(W, v, S, G, e1, P.base_index + i1, a1, wd1, wn1, we1, o1, c1, r1, k1);
+    fin_resolve<kStaged>(W, v, S, G, P.base_index + i0, a0, wd0, wn0, we0, o0, c0, r0, k0);
+    fin_resolve<kStaged>(W, v, S, G, P.base_index + i1, a1, wd1, wn1, we1, o1, c1, r1, k1);
     unsigned long long* o = reinterpret_cast<unsigned long long*>(out) + i0;
     if (ok1 && (((uintptr_t)o & 15u) == 0)) __stcs(reinterpret_cast<ulonglong2*>(o), make_ulonglong2(o0, o1));
     else {
@@ -939,7 +1035,25 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const
       if (cm | dm)
         atomicAdd(S.segcnt + q / SEG_CHUNKS, (unsigned long long)__popcll(cm) | ((unsigned long long)__popcll(dm) << 32));
     }
-  });
+  };
+  if (kStaged) {
+    // staged worlds stream the pass-1 records: one 16-byte load = this lane's two records
+    const unsigned long long* rec = S.drec + (P.base_index - S.drec_base);
+    rec_stream(rec, n, [&](ulonglong2 r, uint64_t i0, bool ok0, bool ok1) {
+      Dec d0, d1;
+      unpack_rec(v, slut, ok0 ? r.x : 0ull, in, i0, d0);
+      unpack_rec(v, slut, ok1 ? r.y : 0ull, in, i0 + 1, d1);
+      body(d0, d1, i0, ok0, ok1);
+    });
+  } else {
+    ldg_stream(in, n, [&](uint4 e0, uint64_t i0, bool ok0, uint4 e1, uint64_t i1, bool ok1) {
+      if (!ok0) e0.w = 0;                     // past the end: decodes as a skipped entry
+      if (!ok1) e1.w = 0;
+      const Dec d0 = decode_fast(v.T, W.page_state, S, e0, P.base_index + i0, lane);
+      const Dec d1 = decode_fast(v.T, W.page_state, S, e1, P.base_index + i1, lane);
+      body(d0, d1, i0, ok0, ok1);
+    });
+  }
 }
 
 // Cancel list + dedup set in index order.  Block = one segment of SEG_CHUNKS chunks, one

@@ -81,6 +81,8 @@ struct mpsf_ctx {
   size_t small_cap = 0;
   size_t small_empty_bytes = 0, small_zero_off = 0, small_zero_bytes = 0;
   uint8_t* d_masks = nullptr;   // per-chunk masks + segment counters (pass 2)
+  unsigned long long* d_drec = nullptr;   // pass-1 records (8 B per entry)
+  uint64_t drec_cap = 0;
   uint64_t tiles_cap = 0;
   unsigned long long* d_hdd = nullptr;  // keys then vals
   uint64_t hcap_dd = 0;
@@ -219,6 +221,7 @@ void mpsf_destroy(mpsf_ctx* c) {
   cudaFree(c->d_counter);
   cudaFree(c->d_small);
   cudaFree(c->d_masks);
+  cudaFree(c->d_drec);
   cudaFree(c->d_hdd);
   cudaFree(c->d_hnr);
   cudaFree(c->d_io);
@@ -462,6 +465,14 @@ static int ensure_call_scratch(mpsf_ctx* c, uint64_t n) {
     CK(cudaMalloc(&c->d_masks, mbytes));
     c->tiles_cap = mbytes;
   }
+  if (n > c->drec_cap) {
+    cudaFree(c->d_drec);
+    c->d_drec = nullptr;
+    c->drec_cap = 0;
+    CK(cudaMalloc(&c->d_drec, 8 * std::max<uint64_t>(n, 2)));
+    c->drec_cap = n;
+  }
+  c->S.drec = c->d_drec;
   c->S.cmask = reinterpret_cast<ulonglong2*>(c->d_masks);
   c->S.dstage = reinterpret_cast<unsigned long long*>(c->d_masks + 16 * std::max<uint64_t>(nq, 1));
   c->S.segcnt = c->S.dstage + 64 * std::max<uint64_t>(nq, 1);
@@ -536,6 +547,7 @@ int mpsf_scan(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const mpsf_
 static int batch_init(mpsf_ctx* c, uint64_t n, const mpsf_params* p, uint64_t* d_counts, cudaStream_t st) {
   int rc = ensure_call_scratch(c, n);
   if (rc) return rc;
+  c->S.drec_base = p->base_index;
   InitSegs segs{};
   int k = 0;
   segs.p[k] = c->d_dd; segs.words[k] = c->W.n_pages * c->W.dd_groups; segs.val[k++] = EMPTY32;

@@ -119,6 +119,8 @@ struct Scratch {
   ulonglong2* cmask;           // [chunks] (cancelled-entry mask, dedup-representative mask)
   unsigned long long* segcnt;  // [segments] cancel count | dedup count << 32
   unsigned long long* dstage;  // [chunks][KSTAGE] first dedup keys of each chunk (k_finalize -> k_lists)
+  unsigned long long* drec;    // [n] pass-1 records (fixed-layout worlds), entry drec_base first
+  uint64_t drec_base;          // global index of drec[0] (params.base_index of the batch)
 };
 
 // What mpsf_get_summary reads back after a batch.
