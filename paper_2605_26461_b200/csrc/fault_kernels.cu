@@ -79,7 +79,7 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 __host__ __device__ inline uint32_t al16(uint64_t x) { return (uint32_t)((x + 15) & ~uint64_t(15)); }
 
 struct Layout {
-  uint32_t lut, slut, cinfo, queue;
+  uint32_t lut, slut, fclient, cinfo, queue;
   uint32_t pg_base, pg_end, poff, rattr, rrid, skip, chan;
   uint32_t c64, iso, r32, counts, used, cstate, total;
   uint32_t rep_chan;
@@ -104,6 +104,7 @@ __host__ __device__ inline Layout make_layout(const World& W, bool staged, bool 
   L.rep_chan = staged ? 32u : 0u;
   L.lut = o; o += 4 * LUT_N;
   L.slut = o; o += 4 * 32;
+  L.fclient = o; if (fin) o += al16(32ull * nc);
   L.queue = o; if (!fin) o += WARPS * QCAP * 16;
   L.cinfo = o; if (staged) o += al16(512ull * nc);
   L.pg_base = o; if (staged) o += al16(4ull * nr);
@@ -851,54 +852,78 @@ constexpr uint32_t KSTAGE = WCHUNK;   // dedup keys staged per chunk by k_finali
 // the first-isolation word of its (client, page, epoch), its external range's first
 // isolation); fin_resolve turns the loaded words into the OutRecord, the cancel flag and the
 // dedup-set membership.  Wild pages (no range, no guard) look their keys up in the hashes.
+// Per-client decision table of pass 2, folded once per CTA from CState + Globals so an
+// entry's verdict is a few compares (rules C4-C7 of SURVEY.md Appendix C):
+//   trap records: applied iff idx == trap_ok (a second trap on a destroyed TSG is cancelled)
+//   fatal reports: applied iff the representative's ok32 == ft[channel is CE] (C4)
+//   benign completions: cancelled iff bflags[channel is CE] or ok32 > tie (C5/C6)
+//   isolation: epoch 1 iff rel < ok32 (C3); pre_nrall: epoch-1 keys are pass 1's first-record keys
+struct FinClient {
+  long long rel;
+  uint32_t trap_ok, ft0, ft1, tie;
+  uint32_t bflags;      // bit0: benign always cancelled; bit1: same for a CE channel
+  uint32_t pre_nrall;
+};
+static_assert(sizeof(FinClient) == 32, "FinClient layout");
+
+__device__ __forceinline__ FinClient fin_client(const CState& cs, const Globals& G, bool has_nrall) {
+  FinClient f;
+  f.rel = cs.rel;
+  const bool sa = cs.flags & CS_SA, alive0 = cs.flags & CS_ALIVE0;
+  if (sa) {
+    f.trap_ok = alive0 ? cs.trap_sa_idx : EMPTY32;
+    f.ft0 = (alive0 && !(cs.flags & CS_TRAPPED)) ? cs.ft_sa_ok : EMPTY32;
+    f.ft1 = f.ft0;
+  } else {
+    f.trap_ok = G.gr_alive0 ? G.trap_mps_idx : EMPTY32;
+    f.ft0 = G.ft_gr_ok;
+    f.ft1 = ((cs.flags & CS_CE_ALIVE0) && cs.ft_ce_ok != EMPTY32 && !(cs.rel < (long long)cs.ft_ce_ok))
+                ? cs.ft_ce_ok : EMPTY32;
+  }
+  const bool b0 = cs.rel != REL_NONE || (cs.flags & CS_KILL_ALL);
+  const bool b1 = b0 || (cs.flags & CS_CE_TORN);
+  f.bflags = (b0 ? 1u : 0u) | (b1 ? 2u : 0u);
+  f.tie = cs.kill_tie;
+  f.pre_nrall = (cs.rel == REL_PRE && has_nrall) ? 1u : 0u;
+  return f;
+}
+
+// Pass 2 per entry, in two halves so both entries of a lane issue their L2 lookups together:
+// fin_addr picks the words the verdict depends on (the dedup slot of its key, the
+// first-isolation word of its (client, page, epoch), its external range's first isolation);
+// fin_resolve turns them into the OutRecord, the cancel flag and the dedup-set membership.
 struct FinA {
   Dec d;
-  CState cs;
   uint32_t ok;
   const uint32_t* pd;   // dedup slot word (in-world dedup candidates)
   const uint32_t* pn;   // first-isolation word (nrall / nr1 / nr0)
   const uint32_t* pe;   // external range's first isolation (ext)
-  bool hd, hn;          // look up in hdd / hnr instead
-  bool epoch1;
+  bool needs_nr, e1keys;
 };
 
 template <bool kStaged>
-__device__ __forceinline__ void fin_addr(const World& W, const View& v, const Scratch& S, const Dec& dd,
-                                         uint64_t gidx, FinA& a) {
+__device__ __forceinline__ void fin_addr(const World& W, const View& v, const Scratch& S, const FinClient* fct,
+                                         const Dec& dd, uint64_t gidx, FinA& a) {
   a.d = dd;
   const Dec& d = a.d;
   const uint32_t f = d.f;
-  a.pd = a.pn = a.pe = nullptr;
-  a.hd = a.hn = false;
-  a.epoch1 = false;
-  a.cs = v.cst[d.c];
-  a.ok = ((f & LF_REPL) ? 0u : 0x80000000u) | (uint32_t)gidx;
   const bool inw = d.inr || d.guard;
-  if (f & LF_DD) {
-    a.pd = inw ? S.dd + (W.dd_groups == 1 ? d.slot : d.slot * W.dd_groups + ((f >> LF_GROUP_SH) & 7u)) : nullptr;
-    a.hd = !inw;
-  }
-  if ((f & LF_ELIG) && !(f & LF_TRAP)) {                           // isolation mechanism inputs (C3)
-    const bool epoch1 = a.cs.rel < (long long)a.ok;
-    a.epoch1 = epoch1;
-    const uint32_t m = (f >> LF_M_SH) & 3u;
-    if (!d.inr || epoch1) {
-      const bool pre = a.cs.rel == REL_PRE;
-      if (epoch1 && !(pre && S.nrall)) {
-        a.pn = inw ? S.nr1 + d.slot : nullptr;
-        a.hn = !inw;
-      } else {
-        a.pn = d.inr ? S.nrall + d.slot : (d.guard ? S.nr0 + d.ridx : nullptr);
-        a.hn = !inw;
-      }
-    } else if (m == 2) {
-      a.pe = S.ext + d.ridx;
-    }
-  }
+  a.ok = ((f & LF_REPL) ? 0u : 0x80000000u) | (uint32_t)gidx;
+  a.pd = ((f & LF_DD) && inw)
+             ? S.dd + (W.dd_groups == 1 ? d.slot : d.slot * W.dd_groups + ((f >> LF_GROUP_SH) & 7u)) : nullptr;
+  const bool elig = (f & LF_ELIG) != 0;
+  const long long rel = fct[d.c].rel;
+  const bool epoch1 = rel < (long long)a.ok;
+  a.needs_nr = elig && (!d.inr || epoch1);
+  a.e1keys = epoch1 && !fct[d.c].pre_nrall;
+  const uint32_t* pn = a.e1keys ? (inw ? S.nr1 + d.slot : nullptr)
+                                : (d.inr ? S.nrall + d.slot : (d.guard ? S.nr0 + d.ridx : nullptr));
+  a.pn = a.needs_nr ? pn : nullptr;
+  a.pe = (elig && d.inr && !epoch1 && ((f >> LF_M_SH) & 3u) == 2u) ? S.ext + d.ridx : nullptr;
 }
 
 template <bool kStaged>
-__device__ __forceinline__ void fin_resolve(const World& W, const View& v, const Scratch& S, const Globals& G,
+__device__ __forceinline__ void fin_resolve(const World& W, const View& v, const Scratch& S, const FinClient* fct,
                                             uint64_t gidx, const FinA& a, uint32_t wd, uint32_t wn,
                                             uint32_t we, unsigned long long& o8, bool& canc, bool& rep,
                                             unsigned long long& key) {
@@ -909,57 +934,43 @@ __device__ __forceinline__ void fin_resolve(const World& W, const View& v, const
     o8 = 0xFFFF000000000000ull | (0xFFull << 32) | NO_RID;     // rid NO_RID, scenario 0xFF, client 0xFFFF
     return;
   }
-  const uint32_t sid = f & LF_S, c = d.c;
-  const CState& cs = a.cs;
-  const uint32_t rid = d.inr ? v.T.rrid[d.ridx] : NO_RID;
-  uint32_t verdict;
-  if (f & LF_TRAP) {
-    // raise_sm_trap at raise time (pipeline.py:151-155); a second trap on a destroyed
-    // TSG is cancelled (the reference raises UnknownTsg)
-    if (!(cs.flags & CS_SA)) canc = !(G.gr_alive0 && (uint32_t)gidx == G.trap_mps_idx);
-    else canc = !((cs.flags & CS_ALIVE0) && (uint32_t)gidx == cs.trap_sa_idx);
-    verdict = canc ? 0x10u : 0u;
-  } else {
-    const uint32_t outcome = (f & LF_ELIG) ? 2u : ((f & LF_SERV) ? 1u : 3u);
-    const uint32_t ok = a.ok;
-    uint32_t rep_ok = ok;
-    bool dup = false;
-    const uint32_t page_hi = (uint32_t)(d.va >> 12);
-    if (f & LF_DD) {                                               // rule C2: smallest index of the key
-      const uint32_t group = (f >> LF_GROUP_SH) & 7u;
-      key = dedup_key(c, (int)((d.cw >> 16) & 3u), (int)sid, d.va >> 12);   // translation: engine == channel's
-      uint32_t ri;
-      if (!a.hd && wd != EMPTY32 && (wd & 7u) == group) ri = wd >> 3;
-      else ri = hash_get(S.hdd, key);
-      dup = ri != (uint32_t)gidx;
-      rep_ok = ri;                                                 // replayable: ok32 == idx
-      rep = !dup;
-      if (!rep) key = 0;
-    }
-    uint32_t mech = 0;
-    const uint32_t ceng = (d.cw >> 16) & 3u;
-    if (outcome == 3) {                     // fatal: applies iff its TSG still lives (C4)
-      bool applied;
-      if (cs.flags & CS_SA) applied = (cs.flags & CS_ALIVE0) && !(cs.flags & CS_TRAPPED) && rep_ok == cs.ft_sa_ok;
-      else if (ceng == 1) applied = (cs.flags & CS_CE_ALIVE0) && rep_ok == cs.ft_ce_ok && !(cs.rel < (long long)rep_ok);
-      else applied = rep_ok == G.ft_gr_ok;
-      canc = !applied;
-    } else if (outcome == 1) {              // benign completion dropped on a torn channel (C5)
-      canc = cs.rel != REL_NONE || (ceng == 1 && (cs.flags & CS_CE_TORN)) ||
-             (cs.flags & CS_KILL_ALL) || rep_ok > cs.kill_tie;
-    } else if (!dup) {                      // isolation mechanism (C3)
-      if (!d.inr || a.epoch1) {
-        const uint32_t nr = a.hn ? hash_get(S.hnr, nr_key(c, a.epoch1 && !(cs.rel == REL_PRE && S.nrall) ? 1 : 0,
-                                                          d.va >> 12))
-                                 : wn;
-        mech = nr == ok ? 1u : 2u;
-      } else {
-        mech = (a.pe && we == ok) ? 3u : 2u;
-      }
-    }
-    (void)page_hi;
-    verdict = outcome | (mech << 2) | (canc ? 0x10u : 0u) | (dup ? 0x20u : 0u) | ((f & LF_REPL) ? 0x40u : 0u);
+  const uint32_t sid = f & LF_S, c = d.c, ceng = (d.cw >> 16) & 3u;
+  const FinClient& fc = fct[c];
+  const bool inw = d.inr || d.guard;
+  const uint32_t ok = a.ok;
+  const bool dd = f & LF_DD, trap = f & LF_TRAP, elig = f & LF_ELIG, serv = f & LF_SERV;
+  // rule C2: the smallest index of the entry's dedup key
+  uint32_t rep_ok = ok;
+  bool dup = false;
+  if (dd) {
+    const uint32_t group = (f >> LF_GROUP_SH) & 7u;
+    key = dedup_key(c, (int)ceng, (int)sid, d.va >> 12);      // translation: engine == channel's
+    uint32_t ri = wd >> 3;
+    if (!(inw && wd != EMPTY32 && (wd & 7u) == group))
+      ri = (MPSF_ABLATE & 16384) ? EMPTY32 : hash_get(S.hdd, key);
+    dup = ri != (uint32_t)gidx;
+    rep_ok = ri;                                                 // replayable: ok32 == idx
+    rep = !dup;
+    if (!rep) key = 0;
   }
+  const bool ce = ceng == 1;
+  if (trap) canc = (uint32_t)gidx != fc.trap_ok;
+  else if (serv) canc = ((fc.bflags >> (ce ? 1 : 0)) & 1u) || rep_ok > fc.tie;
+  else if (!elig) canc = rep_ok != (ce ? fc.ft1 : fc.ft0);
+  uint32_t mech = 0;
+  if (elig && !dup) {                                            // isolation mechanism (C3)
+    if (a.needs_nr) {
+      uint32_t nr = wn;
+      if (!inw && !(MPSF_ABLATE & 16384)) nr = hash_get(S.hnr, nr_key(c, a.e1keys ? 1 : 0, d.va >> 12));
+      mech = nr == ok ? 1u : 2u;
+    } else {
+      mech = (a.pe && we == ok) ? 3u : 2u;
+    }
+  }
+  const uint32_t outcome = trap ? 0u : (elig ? 2u : (serv ? 1u : 3u));
+  const uint32_t verdict = outcome | (mech << 2) | (canc ? 0x10u : 0u) | (dup ? 0x20u : 0u) |
+                           ((f & LF_REPL) ? 0x40u : 0u);
+  const uint32_t rid = d.inr ? v.T.rrid[d.ridx] : NO_RID;
   o8 = (unsigned long long)rid | ((unsigned long long)sid << 32) | ((unsigned long long)verdict << 40) |
        ((unsigned long long)c << 48);
 }
@@ -994,6 +1005,8 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const
   const Layout L = make_layout(W, kStaged, true);
   const View v = setup<kStaged>(smem, L, W, S, false, true, P.flags & MPSF_PF_ISOLATION);
   const Globals G = *S.glob;
+  FinClient* fct = reinterpret_cast<FinClient*>(smem + L.fclient);
+  for (uint32_t k = threadIdx.x; k < W.n_clients; k += blockDim.x) fct[k] = fin_client(S.cstate[k], G, S.nrall != nullptr);
   __syncthreads();
   const uint32_t lane = threadIdx.x & 31;
   uint32_t* slut = reinterpret_cast<uint32_t*>(smem + L.slut);
@@ -1002,16 +1015,16 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const
   auto body = [&](const Dec& d0, const Dec& d1, uint64_t i0, bool ok0, bool ok1) {
     const uint64_t i1 = i0 + 1;
     FinA a0, a1;
-    fin_addr<kStaged>(W, v, S, d0, P.base_index + i0, a0);
-    fin_addr<kStaged>(W, v, S, d1, P.base_index + i1, a1);
+    fin_addr<kStaged>(W, v, S, fct, d0, P.base_index + i0, a0);
+    fin_addr<kStaged>(W, v, S, fct, d1, P.base_index + i1, a1);
     const uint32_t wd0 = a0.pd ? __ldcg(a0.pd) : EMPTY32, wn0 = a0.pn ? __ldcg(a0.pn) : EMPTY32;
     const uint32_t we0 = a0.pe ? __ldcg(a0.pe) : EMPTY32;
     const uint32_t wd1 = a1.pd ? __ldcg(a1.pd) : EMPTY32, wn1 = a1.pn ? __ldcg(a1.pn) : EMPTY32;
     const uint32_t we1 = a1.pe ? __ldcg(a1.pe) : EMPTY32;
     unsigned long long o0, o1, k0, k1;
     bool c0, c1, r0, r1;
-    fin_resolve<kStaged>(W, v, S, G, P.base_index + i0, a0, wd0, wn0, we0, o0, c0, r0, k0);
-    fin_resolve<kStaged>(W, v, S, G, P.base_index + i1, a1, wd1, wn1, we1, o1, c1, r1, k1);
+    fin_resolve<kStaged>(W, v, S, fct, P.base_index + i0, a0, wd0, wn0, we0, o0, c0, r0, k0);
+    fin_resolve<kStaged>(W, v, S, fct, P.base_index + i1, a1, wd1, wn1, we1, o1, c1, r1, k1);
     unsigned long long* o = reinterpret_cast<unsigned long long*>(out) + i0;
     if (ok1 && (((uintptr_t)o & 15u) == 0)) __stcs(reinterpret_cast<ulonglong2*>(o), make_ulonglong2(o0, o1));
     else {
@@ -1041,8 +1054,8 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const
     const unsigned long long* rec = S.drec + (P.base_index - S.drec_base);
     rec_stream(rec, n, [&](ulonglong2 r, uint64_t i0, bool ok0, bool ok1) {
       Dec d0, d1;
-      unpack_rec(v, slut, ok0 ? r.x : 0ull, in, i0, d0);
-      unpack_rec(v, slut, ok1 ? r.y : 0ull, in, i0 + 1, d1);
+      unpack_rec(v, slut, (ok0 && !(MPSF_ABLATE & 256)) ? r.x : 0ull, in, i0, d0);
+      unpack_rec(v, slut, (ok1 && !(MPSF_ABLATE & 256)) ? r.y : 0ull, in, i0 + 1, d1);
       body(d0, d1, i0, ok0, ok1);
     });
   } else {
