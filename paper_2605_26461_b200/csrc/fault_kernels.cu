@@ -1034,19 +1034,14 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const
     const uint32_t bc0 = __ballot_sync(0xFFFFFFFFu, ok0 && c0), bc1 = __ballot_sync(0xFFFFFFFFu, ok1 && c1);
     const uint32_t bd0 = __ballot_sync(0xFFFFFFFFu, ok0 && r0), bd1 = __ballot_sync(0xFFFFFFFFu, ok1 && r1);
     const uint64_t qq = q_base + i0 / WCHUNK;
-    if (bd0 | bd1) {                          // stage the chunk's representative keys by rank
-      const uint32_t lt = (1u << lane) - 1u;
-      const uint32_t rk0 = __popc(bd0 & lt) + __popc(bd1 & lt), rk1 = rk0 + (r0 && ok0 ? 1u : 0u);
-      if (ok0 && r0) st_keep(S.dstage + qq * KSTAGE + rk0, k0);
-      if (ok1 && r1) st_keep(S.dstage + qq * KSTAGE + rk1, k1);
-    }
+    // representative keys staged at their entry's position in the chunk
+    if (ok0 && r0) st_keep(S.dstage + qq * KSTAGE + 2 * lane, k0);
+    if (ok1 && r1) st_keep(S.dstage + qq * KSTAGE + 2 * lane + 1, k1);
     if (lane == 0) {
-      const unsigned long long cm = spread2(bc0) | (spread2(bc1) << 1);
-      const unsigned long long dm = spread2(bd0) | (spread2(bd1) << 1);
-      const uint64_t q = qq;
-      S.cmask[q] = make_ulonglong2(cm, dm);
-      if (cm | dm)
-        atomicAdd(S.segcnt + q / SEG_CHUNKS, (unsigned long long)__popcll(cm) | ((unsigned long long)__popcll(dm) << 32));
+      // raw ballots (bit l of .x/.y: entry 2l / 2l + 1 cancelled; .z/.w: representatives)
+      S.cmask[qq] = make_uint4(bc0, bc1, bd0, bd1);
+      const uint32_t nc = __popc(bc0) + __popc(bc1), nd = __popc(bd0) + __popc(bd1);
+      if (nc | nd) atomicAdd(S.segcnt + qq / SEG_CHUNKS, (unsigned long long)nc | ((unsigned long long)nd << 32));
     }
   };
   if (kStaged) {
@@ -1109,7 +1104,10 @@ __global__ void __launch_bounds__(1024, 2) k_lists(Scratch S, const mpsf_fault_e
   if (lane == 0 && acc) atomicAdd(&s_base, acc);
   const uint64_t q = seg * SEG_CHUNKS + threadIdx.x;
   ulonglong2 mk = make_ulonglong2(0, 0);
-  if (q < nq) mk = __ldcg(S.cmask + q);
+  if (q < nq) {
+    const uint4 b = __ldcg(S.cmask + q);
+    mk = make_ulonglong2(spread2(b.x) | (spread2(b.y) << 1), spread2(b.z) | (spread2(b.w) << 1));
+  }
   const unsigned long long mine = (unsigned long long)__popcll(mk.x) | ((unsigned long long)__popcll(mk.y) << 32);
   unsigned long long x = mine;   // inclusive warp scan (both counts packed)
 #pragma unroll
@@ -1175,7 +1173,7 @@ __global__ void __launch_bounds__(1024, 2) k_lists(Scratch S, const mpsf_fault_e
         const uint32_t k = f - ej;
         const uint32_t lo = (uint32_t)dmj, clo = __popc(lo);
         const uint32_t bit = k < clo ? __fns(lo, 0, (int)k + 1) : 32 + __fns((uint32_t)(dmj >> 32), 0, (int)(k - clo) + 1);
-        key[h] = f < R ? __ldcg(S.dstage + (q0w + j) * KSTAGE + k) : 0ull;
+        key[h] = f < R ? __ldcg(S.dstage + (q0w + j) * KSTAGE + bit) : 0ull;
         gix[h] = (uint32_t)(base_index + (q0w + j) * WCHUNK) + bit;
       }
 #pragma unroll

@@ -473,7 +473,7 @@ static int ensure_call_scratch(mpsf_ctx* c, uint64_t n) {
     c->drec_cap = n;
   }
   c->S.drec = c->d_drec;
-  c->S.cmask = reinterpret_cast<ulonglong2*>(c->d_masks);
+  c->S.cmask = reinterpret_cast<uint4*>(c->d_masks);
   c->S.dstage = reinterpret_cast<unsigned long long*>(c->d_masks + 16 * std::max<uint64_t>(nq, 1));
   c->S.segcnt = c->S.dstage + 64 * std::max<uint64_t>(nq, 1);
   const uint64_t floor_cap = 1ull << 16;

@@ -116,7 +116,7 @@ struct Scratch {
   Globals* glob;
   uint32_t* ctrl;      // [C_NCTRL]
   unsigned long long* err_idx;
-  ulonglong2* cmask;           // [chunks] (cancelled-entry mask, dedup-representative mask)
+  uint4* cmask;                // [chunks] ballots: cancelled entries 2l / 2l+1, representatives 2l / 2l+1
   unsigned long long* segcnt;  // [segments] cancel count | dedup count << 32
   unsigned long long* dstage;  // [chunks][KSTAGE] first dedup keys of each chunk (k_finalize -> k_lists)
   unsigned long long* drec;    // [n] pass-1 records (fixed-layout worlds), entry drec_base first
