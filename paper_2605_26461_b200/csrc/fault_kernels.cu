@@ -39,7 +39,7 @@ namespace mpsf {
 // world tables); every warp owns 64-entry chunks (two adjacent entries per lane).
 constexpr int BLOCK = 1024;
 constexpr int WARPS = BLOCK / 32;
-constexpr uint32_t WQ = 64;    // per-warp wild-record buffer of the scan (16-byte records)
+constexpr int QCAP = 64;                   // per-warp deferred hash-op stack (scan)
 
 // ---- PTX: mbarrier + bulk async copy (TMA) ---------------------------------------------
 __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -104,8 +104,8 @@ __host__ __device__ inline Layout make_layout(const World& W, bool staged, bool 
   L.rep_chan = staged ? 32u : 0u;
   L.lut = o; o += 4 * LUT_N;
   L.slut = o; o += 4 * 32;
-  L.fclient = o; if (fin && staged) o += al16(32ull * nc);
-  L.queue = o; if (!fin) o += WARPS * WQ * 16;
+  L.fclient = o; if (fin) o += al16(32ull * nc);
+  L.queue = o; if (!fin) o += WARPS * QCAP * 16;
   L.cinfo = o; if (staged) o += al16(512ull * nc);
   L.pg_base = o; if (staged) o += al16(4ull * nr);
   L.pg_end = o; if (staged) o += al16(4ull * nr);
@@ -385,21 +385,14 @@ __device__ __forceinline__ void rec_stream(const unsigned long long* rec, uint64
 // entry leaves at most two first-in-group minima on global tables: its dedup key (rule C2,
 // a dense (page, group) slot or a claimed page slot) and the first eligible record of its page
 // (nrall).  Both entries of a lane issue their L2 loads together and resolve afterwards.
-// Wild pages (no range, no guard): their hash-table work is taken off the streaming passes --
-// the scan appends their index to a wild list, k_wild inserts their keys (after the scan) and
-// finalizes their records (after k_finalize), so no hash round trip sits on the common path.
-
-// An entry whose keys live in the wild-page hashes (C2 dedup keys and
-// C3 first-isolation keys of pages outside every range's slot span).
-__device__ __forceinline__ bool is_wild(const Dec& d) {
-  return d.f && !(d.f & LF_XKIND) && !(d.inr || d.guard) && (d.f & (LF_ELIG | LF_DD));
-}
+// Wild pages (no range, no guard) go to a per-warp stack of deferred hash operations that is
+// drained 32 at a time, so their CAS round trips never sit on the common path.
+struct QOp { unsigned long long key; uint32_t val, tab; };
 
 struct ScanOut {
   uint32_t* pa; uint32_t va;     // nrall precheck-min
   uint32_t* pd; uint32_t vd;     // dedup slot precheck-min / claim
-  bool wild;                     // keys in the wild-page hashes (k_wild)
-  uint32_t cw;                   // channel word
+  bool qn, qd;                   // deferred hash ops: NR key (hnr), dedup key (hdd)
   uint32_t c, eng, sid;          // key material (hash ops, claim fallback)
   uint64_t page;
   unsigned long long rec;        // pass-1 record (fixed-layout worlds)
@@ -517,8 +510,8 @@ __device__ __forceinline__ void scan_fast(const World& W, const View& v, const S
   const uint32_t group = (f >> LF_GROUP_SH) & 7u;
   o.pd = (dd && inw) ? S.dd + (W.dd_groups == 1 ? d.slot : d.slot * W.dd_groups + group) : nullptr;
   o.vd = ((uint32_t)gidx << 3) | group;
-  o.wild = is_wild(d) && !(MPSF_ABLATE & 1);
-  o.cw = d.cw;
+  o.qn = elig && !inw && !(MPSF_ABLATE & 1);
+  o.qd = dd && !inw && !(MPSF_ABLATE & 1);
   o.c = c; o.eng = e.w & 0xFF; o.sid = sid; o.page = d.va >> 12;
   o.rec = pack_rec(d);
 }
@@ -540,34 +533,34 @@ __device__ __forceinline__ void claim_resolve(const Scratch& S, uint32_t* used, 
   }
 }
 
-// Wild-record buffer: lanes with a wild entry append its record {global index, client |
-// scenario << 16 | channel engine << 21 | standalone << 23, page} (warp-collective); a nearly
-// full buffer goes to the global wild list with one atomic per flush.
-__device__ __forceinline__ uint4 wild_rec(const ScanOut& o, uint32_t gidx, uint32_t cw) {
-  return make_uint4(gidx, o.c | (o.sid << 16) | (((cw >> 16) & 3u) << 21) | (((cw >> 18) & 1u) << 23),
-                    (uint32_t)o.page, (uint32_t)(o.page >> 32));
-}
-
-__device__ __forceinline__ void w_flush(uint4* q, uint32_t cnt, const Scratch& S) {
-  __syncwarp();
-  if (!cnt) return;
-  const uint32_t lane = threadIdx.x & 31;
-  uint32_t base = 0;
-  if (lane == 0) base = atomicAdd(S.ctrl + C_WILD, cnt);
-  base = __shfl_sync(0xFFFFFFFFu, base, 0);
-  for (uint32_t k = lane; k < cnt; k += 32) S.wild[base + k] = q[k];
-  __syncwarp();
-}
-
-__device__ __forceinline__ void w_push(uint4* q, uint32_t& cnt, bool has, uint4 rec, const Scratch& S) {
+// Deferred hash ops: push (warp-collective), drained 32 at a time.
+__device__ __forceinline__ void q_push(QOp* q, uint32_t& cnt, bool has, unsigned long long key, uint32_t val,
+                                       uint32_t tab, const Scratch& S, uint32_t* used) {
   const uint32_t lane = threadIdx.x & 31;
   const unsigned m = __ballot_sync(0xFFFFFFFFu, has);
   if (!m) return;
-  if (has) q[cnt + __popc(m & ((1u << lane) - 1u))] = rec;
+  if (has) {
+    QOp x; x.key = key; x.val = val; x.tab = tab;
+    q[cnt + __popc(m & ((1u << lane) - 1u))] = x;
+  }
   cnt += __popc(m);
-  if (cnt > WQ - 32) {
-    w_flush(q, cnt, S);
-    cnt = 0;
+  if (cnt >= 32) {
+    __syncwarp();
+    const QOp x = q[cnt - 32 + lane];
+    const Hash& h = x.tab ? S.hnr : S.hdd;
+    if (!hash_min(h, used + x.tab, x.key, x.val)) atomicOr(S.ctrl + C_OVF, 1u);
+    cnt -= 32;
+    __syncwarp();
+  }
+}
+
+__device__ __forceinline__ void q_drain(QOp* q, uint32_t cnt, const Scratch& S, uint32_t* used) {
+  __syncwarp();
+  const uint32_t lane = threadIdx.x & 31;
+  if (lane < cnt) {
+    const QOp x = q[lane];
+    const Hash& h = x.tab ? S.hnr : S.hdd;
+    if (!hash_min(h, used + x.tab, x.key, x.val)) atomicOr(S.ctrl + C_OVF, 1u);
   }
 }
 
@@ -596,7 +589,6 @@ __device__ __forceinline__ void flush_minima(const World& W, const Scratch& S, c
   if (threadIdx.x < 2 && v.used[threadIdx.x]) atomicAdd(S.ctrl + C_HASH_DD + threadIdx.x, v.used[threadIdx.x]);
 }
 
-
 template <bool kStaged>
 __global__ void __launch_bounds__(BLOCK, 1) k_scan(World W, Scratch S, const mpsf_fault_entry* __restrict__ in,
                                                    uint64_t n, Params P, unsigned long long* __restrict__ counts,
@@ -605,7 +597,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_scan(World W, Scratch S, const mps
   const Layout L = make_layout(W, kStaged, false);
   const View v = setup<kStaged>(smem, L, W, S, true, false, P.flags & MPSF_PF_ISOLATION);
   __syncthreads();
-  uint4* q = reinterpret_cast<uint4*>(smem + L.queue) + (threadIdx.x >> 5) * WQ;
+  QOp* q = reinterpret_cast<QOp*>(smem + L.queue) + (threadIdx.x >> 5) * QCAP;
   uint32_t qn = 0;
   const bool sparse = W.dd_groups == 1;
   ldg_stream(in, n, [&](uint4 e0, uint64_t i0, bool ok0, uint4 e1, uint64_t i1, bool ok1) {
@@ -635,12 +627,14 @@ __global__ void __launch_bounds__(BLOCK, 1) k_scan(World W, Scratch S, const mps
       if (o0.pd) claim_resolve(S, v.used, o0.pd, o0.vd, rd0, scan_dkey(o0));
       if (o1.pd) claim_resolve(S, v.used, o1.pd, o1.vd, rd1, scan_dkey(o1));
     }
-    if (__any_sync(0xFFFFFFFFu, o0.wild || o1.wild)) {
-      w_push(q, qn, o0.wild, wild_rec(o0, (uint32_t)(P.base_index + i0), o0.cw), S);
-      w_push(q, qn, o1.wild, wild_rec(o1, (uint32_t)(P.base_index + i1), o1.cw), S);
+    if (__any_sync(0xFFFFFFFFu, o0.qn || o0.qd || o1.qn || o1.qd)) {
+      q_push(q, qn, o0.qn, nr_key(o0.c, 0, o0.page), o0.va, 1, S, v.used);
+      q_push(q, qn, o0.qd, scan_dkey(o0), (uint32_t)(o0.vd >> 3), 0, S, v.used);
+      q_push(q, qn, o1.qn, nr_key(o1.c, 0, o1.page), o1.va, 1, S, v.used);
+      q_push(q, qn, o1.qd, scan_dkey(o1), (uint32_t)(o1.vd >> 3), 0, S, v.used);
     }
   });
-  w_flush(q, qn, S);
+  q_drain(q, qn, S, v.used);
   if (kStaged) {
     __syncthreads();
     // fold the block's (client, scenario) counts into the batch counts (accumulates across the
@@ -752,10 +746,6 @@ __global__ void k_resolve(World W, Scratch S, Params P, mpsf_client_verdict* __r
     G->gr_alive0 = gr_alive0;
     S.ctrl[C_PATH] = s_general;
   }
-  __syncthreads();
-  const Globals Gv = *G;
-  for (uint32_t c = threadIdx.x; c < W.n_clients; c += blockDim.x)
-    S.fclient[c] = fin_client(S.cstate[c], Gv, S.nrall != nullptr);
 }
 
 // ---- general path (rule C3 epochs) ----------------------------------------------------------
@@ -845,7 +835,6 @@ __global__ void k_resolve2(World W, Scratch S, Params P) {
     cs.kill_tie = tie;
     cs.flags = (cs.flags & ~CS_KILL_ALL) | (kill_all ? CS_KILL_ALL : 0u);
     S.cstate[c] = cs;
-    S.fclient[c] = fin_client(cs, *S.glob, S.nrall != nullptr);
   }
 }
 
@@ -857,6 +846,47 @@ __global__ void k_resolve2(World W, Scratch S, Params P) {
 // scans its own chunks' popcounts -- no serial look-back between tiles.
 constexpr uint32_t SEG_CHUNKS = 1024;
 constexpr uint32_t KSTAGE = WCHUNK;   // dedup keys staged per chunk by k_finalize, in index order
+
+// Pass 2 per entry, in two halves so both entries of a lane issue their L2 lookups together:
+// fin_addr decodes and picks the words the verdict depends on (the dedup slot of its key,
+// the first-isolation word of its (client, page, epoch), its external range's first
+// isolation); fin_resolve turns the loaded words into the OutRecord, the cancel flag and the
+// dedup-set membership.  Wild pages (no range, no guard) look their keys up in the hashes.
+// Per-client decision table of pass 2, folded once per CTA from CState + Globals so an
+// entry's verdict is a few compares (rules C4-C7 of SURVEY.md Appendix C):
+//   trap records: applied iff idx == trap_ok (a second trap on a destroyed TSG is cancelled)
+//   fatal reports: applied iff the representative's ok32 == ft[channel is CE] (C4)
+//   benign completions: cancelled iff bflags[channel is CE] or ok32 > tie (C5/C6)
+//   isolation: epoch 1 iff rel < ok32 (C3); pre_nrall: epoch-1 keys are pass 1's first-record keys
+struct FinClient {
+  long long rel;
+  uint32_t trap_ok, ft0, ft1, tie;
+  uint32_t bflags;      // bit0: benign always cancelled; bit1: same for a CE channel
+  uint32_t pre_nrall;
+};
+static_assert(sizeof(FinClient) == 32, "FinClient layout");
+
+__device__ __forceinline__ FinClient fin_client(const CState& cs, const Globals& G, bool has_nrall) {
+  FinClient f;
+  f.rel = cs.rel;
+  const bool sa = cs.flags & CS_SA, alive0 = cs.flags & CS_ALIVE0;
+  if (sa) {
+    f.trap_ok = alive0 ? cs.trap_sa_idx : EMPTY32;
+    f.ft0 = (alive0 && !(cs.flags & CS_TRAPPED)) ? cs.ft_sa_ok : EMPTY32;
+    f.ft1 = f.ft0;
+  } else {
+    f.trap_ok = G.gr_alive0 ? G.trap_mps_idx : EMPTY32;
+    f.ft0 = G.ft_gr_ok;
+    f.ft1 = ((cs.flags & CS_CE_ALIVE0) && cs.ft_ce_ok != EMPTY32 && !(cs.rel < (long long)cs.ft_ce_ok))
+                ? cs.ft_ce_ok : EMPTY32;
+  }
+  const bool b0 = cs.rel != REL_NONE || (cs.flags & CS_KILL_ALL);
+  const bool b1 = b0 || (cs.flags & CS_CE_TORN);
+  f.bflags = (b0 ? 1u : 0u) | (b1 ? 2u : 0u);
+  f.tie = cs.kill_tie;
+  f.pre_nrall = (cs.rel == REL_PRE && has_nrall) ? 1u : 0u;
+  return f;
+}
 
 // Pass 2 per entry, in two halves so both entries of a lane issue their L2 lookups together:
 // fin_addr picks the words the verdict depends on (the dedup slot of its key, the
@@ -892,9 +922,7 @@ __device__ __forceinline__ void fin_addr(const World& W, const View& v, const Sc
   a.pe = (elig && d.inr && !epoch1 && ((f >> LF_M_SH) & 3u) == 2u) ? S.ext + d.ridx : nullptr;
 }
 
-// kWild: the entry is a wild-page one (k_wild), its keys are looked up in the hashes; the
-// streaming pass leaves such entries to k_wild (placeholder record, no list bits).
-template <bool kStaged, bool kWild = false>
+template <bool kStaged>
 __device__ __forceinline__ void fin_resolve(const World& W, const View& v, const Scratch& S, const FinClient* fct,
                                             uint64_t gidx, const FinA& a, uint32_t wd, uint32_t wn,
                                             uint32_t we, unsigned long long& o8, bool& canc, bool& rep,
@@ -902,7 +930,7 @@ __device__ __forceinline__ void fin_resolve(const World& W, const View& v, const
   const Dec& d = a.d;
   const uint32_t f = d.f;
   canc = false; rep = false; key = 0;
-  if (!f || (!kWild && is_wild(d))) {
+  if (!f) {
     o8 = 0xFFFF000000000000ull | (0xFFull << 32) | NO_RID;     // rid NO_RID, scenario 0xFF, client 0xFFFF
     return;
   }
@@ -919,7 +947,7 @@ __device__ __forceinline__ void fin_resolve(const World& W, const View& v, const
     key = dedup_key(c, (int)ceng, (int)sid, d.va >> 12);      // translation: engine == channel's
     uint32_t ri = wd >> 3;
     if (!(inw && wd != EMPTY32 && (wd & 7u) == group))
-      ri = hash_get(S.hdd, key);                               // wild page / claimed by another group
+      ri = (MPSF_ABLATE & 16384) ? EMPTY32 : hash_get(S.hdd, key);
     dup = ri != (uint32_t)gidx;
     rep_ok = ri;                                                 // replayable: ok32 == idx
     rep = !dup;
@@ -933,7 +961,7 @@ __device__ __forceinline__ void fin_resolve(const World& W, const View& v, const
   if (elig && !dup) {                                            // isolation mechanism (C3)
     if (a.needs_nr) {
       uint32_t nr = wn;
-      if (kWild && !inw) nr = hash_get(S.hnr, nr_key(c, a.e1keys ? 1 : 0, d.va >> 12));
+      if (!inw && !(MPSF_ABLATE & 16384)) nr = hash_get(S.hnr, nr_key(c, a.e1keys ? 1 : 0, d.va >> 12));
       mech = nr == ok ? 1u : 2u;
     } else {
       mech = (a.pe && we == ok) ? 3u : 2u;
@@ -977,11 +1005,8 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const
   const Layout L = make_layout(W, kStaged, true);
   const View v = setup<kStaged>(smem, L, W, S, false, true, P.flags & MPSF_PF_ISOLATION);
   const Globals G = *S.glob;
-  // the client decision table: staged copy (fixed-layout worlds) or the global one
-  FinClient* fct = kStaged ? reinterpret_cast<FinClient*>(smem + L.fclient) : S.fclient;
-  if (kStaged)
-    for (uint32_t k = threadIdx.x; k < W.n_clients; k += blockDim.x) fct[k] = S.fclient[k];
-  (void)G;
+  FinClient* fct = reinterpret_cast<FinClient*>(smem + L.fclient);
+  for (uint32_t k = threadIdx.x; k < W.n_clients; k += blockDim.x) fct[k] = fin_client(S.cstate[k], G, S.nrall != nullptr);
   __syncthreads();
   const uint32_t lane = threadIdx.x & 31;
   uint32_t* slut = reinterpret_cast<uint32_t*>(smem + L.slut);
@@ -1036,71 +1061,6 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const
       const Dec d1 = decode_fast(v.T, W.page_state, S, e1, P.base_index + i1, lane);
       body(d0, d1, i0, ok0, ok1);
     });
-  }
-}
-
-// ---- wild-page entries ---------------------------------------------------------------------
-// A small grid over the wild list (ctrl[C_WILD] entries of the batch whose first entry is
-// batch_base): kPhase 0 inserts their keys (after the scan), kPhase 1 writes their records and
-// list bits (after k_finalize, entries of [lo, hi) only -- the chunked host pipeline).
-template <int kPhase>
-__global__ void __launch_bounds__(256) k_wild(World W, Scratch S, uint64_t batch_base, uint64_t lo, uint64_t hi,
-                                              Params P, mpsf_out_record* __restrict__ out) {
-  __shared__ uint32_t s_slut[32];
-  __shared__ uint32_t s_used[2];
-  const uint32_t cnt = __ldcg(S.ctrl + C_WILD);
-  if (__ldcg(S.ctrl + C_ERR) != 0 || cnt == 0) return;
-  const bool iso = P.flags & MPSF_PF_ISOLATION;
-  if (threadIdx.x < 32) s_slut[threadIdx.x] = scen_word((int)threadIdx.x, iso);
-  if (threadIdx.x < 2) s_used[threadIdx.x] = 0;
-  __syncthreads();
-  View v;
-  v.T.rrid = W.rrid;
-  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
-    const uint4 wr = __ldcg(S.wild + k);
-    const uint32_t g = wr.x;
-    const uint64_t i = (uint64_t)g - batch_base;
-    if (i < lo || i >= hi) continue;
-    // the wild entry's decode from its record (no range: mechanism class 0)
-    Dec d;
-    const uint32_t sid = (wr.y >> 16) & 31u, ceng = (wr.y >> 21) & 3u;
-    d.c = wr.y & 0xFFFFu;
-    d.cw = d.c | (ceng << 16) | (((wr.y >> 23) & 1u) << 18) | CH_VALID;
-    const uint32_t group = ceng == 0 ? (sid == 15 ? 2u : ((sid >= 1 && sid <= 3) ? 1u : 0u)) : 2u + ceng;
-    d.f = s_slut[sid] | (group << LF_GROUP_SH);
-    d.inr = false; d.guard = false; d.ridx = NO_RID; d.slot = 0;
-    const uint64_t page = (uint64_t)wr.z | ((uint64_t)wr.w << 32);
-    d.va = page << 12;
-    if (kPhase == 0) {
-      const uint32_t ok = ((d.f & LF_REPL) ? 0u : 0x80000000u) | g;
-      if (d.f & LF_ELIG) {
-        if (!hash_min(S.hnr, s_used + 1, nr_key(d.c, 0, page), ok)) atomicOr(S.ctrl + C_OVF, 1u);
-      }
-      if (d.f & LF_DD) {
-        if (!hash_min(S.hdd, s_used, dedup_key(d.c, (int)ceng, (int)sid, page), g)) atomicOr(S.ctrl + C_OVF, 1u);
-      }
-    } else {
-      FinA a;
-      fin_addr<false>(W, v, S, S.fclient, d, g, a);
-      unsigned long long o8, key;
-      bool canc, rep;
-      fin_resolve<false, true>(W, v, S, S.fclient, g, a, EMPTY32, EMPTY32, EMPTY32, o8, canc, rep, key);
-      reinterpret_cast<unsigned long long*>(out)[i] = o8;
-      const uint64_t q = i / WCHUNK;
-      const uint32_t p = (uint32_t)(i % WCHUNK), bit = 1u << (p >> 1);
-      uint32_t* mw = reinterpret_cast<uint32_t*>(S.cmask + q);
-      if (canc) atomicOr(mw + (p & 1u), bit);
-      if (rep) {
-        S.dstage[q * KSTAGE + p] = key;
-        atomicOr(mw + 2 + (p & 1u), bit);
-      }
-      if (canc || rep)
-        atomicAdd(S.segcnt + q / SEG_CHUNKS, (canc ? 1ull : 0ull) | (rep ? (1ull << 32) : 0ull));
-    }
-  }
-  if (kPhase == 0) {
-    __syncthreads();
-    if (threadIdx.x < 2 && s_used[threadIdx.x]) atomicAdd(S.ctrl + C_HASH_DD + threadIdx.x, s_used[threadIdx.x]);
   }
 }
 
@@ -1433,21 +1393,6 @@ int launch_lists(const Scratch& S, const mpsf_fault_entry* in, const mpsf_out_re
   }
   k_lists<<<(unsigned)nseg, 1024, 0, st>>>(S, in, out, chunks_for(n), base_index, dkeys, didx, cancel, sum);
   mk.mark("k_lists");
-  return ok_or_err();
-}
-
-int launch_wild(const World& W, const Scratch& S, const mpsf_fault_entry* in_batch, uint64_t batch_base,
-                int phase, uint64_t lo, uint64_t hi, const Params& P, mpsf_out_record* out_batch, cudaStream_t st,
-                const Marker& mk) {
-  (void)in_batch;
-  const int g = 8 * sm_count();
-  if (phase == 0) {
-    k_wild<0><<<g, 256, 0, st>>>(W, S, batch_base, lo, hi, P, out_batch);
-    mk.mark("k_wild_scan");
-  } else {
-    k_wild<1><<<g, 256, 0, st>>>(W, S, batch_base, lo, hi, P, out_batch);
-    mk.mark("k_wild_fin");
-  }
   return ok_or_err();
 }
 

@@ -83,8 +83,6 @@ struct mpsf_ctx {
   uint8_t* d_masks = nullptr;   // per-chunk masks + segment counters (pass 2)
   unsigned long long* d_drec = nullptr;   // pass-1 records (8 B per entry)
   uint64_t drec_cap = 0;
-  uint4* d_wild = nullptr;                // wild-page entry records (16 B)
-  uint64_t wild_cap = 0;
   uint64_t tiles_cap = 0;
   unsigned long long* d_hdd = nullptr;  // keys then vals
   uint64_t hcap_dd = 0;
@@ -224,7 +222,6 @@ void mpsf_destroy(mpsf_ctx* c) {
   cudaFree(c->d_small);
   cudaFree(c->d_masks);
   cudaFree(c->d_drec);
-  cudaFree(c->d_wild);
   cudaFree(c->d_hdd);
   cudaFree(c->d_hnr);
   cudaFree(c->d_io);
@@ -420,7 +417,6 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   const size_t s_ctrl = take(4 * C_NCTRL);
   const size_t zero_bytes = o - empty_bytes;
   const size_t s_cst = take(sizeof(CState) * std::max<uint32_t>(C, 1));
-  const size_t s_fcl = take(sizeof(FinClient) * std::max<uint32_t>(C, 1));
   if (o > c->small_cap) {
     cudaFree(c->d_small);
     c->d_small = nullptr;
@@ -455,7 +451,6 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   S.err_idx = reinterpret_cast<unsigned long long*>(s + s_err);
   S.ctrl = reinterpret_cast<uint32_t*>(s + s_ctrl);
   S.cstate = reinterpret_cast<CState*>(s + s_cst);
-  S.fclient = reinterpret_cast<FinClient*>(s + s_fcl);
   c->has_world = true;
   return MPSF_OK;
 }
@@ -478,14 +473,6 @@ static int ensure_call_scratch(mpsf_ctx* c, uint64_t n) {
     c->drec_cap = n;
   }
   c->S.drec = c->d_drec;
-  if (n > c->wild_cap) {
-    cudaFree(c->d_wild);
-    c->d_wild = nullptr;
-    c->wild_cap = 0;
-    CK(cudaMalloc(&c->d_wild, 16 * std::max<uint64_t>(n, 1)));
-    c->wild_cap = n;
-  }
-  c->S.wild = c->d_wild;
   c->S.cmask = reinterpret_cast<uint4*>(c->d_masks);
   c->S.dstage = reinterpret_cast<unsigned long long*>(c->d_masks + 16 * std::max<uint64_t>(nq, 1));
   c->S.segcnt = c->S.dstage + 64 * std::max<uint64_t>(nq, 1);
@@ -552,9 +539,7 @@ int mpsf_scan(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const mpsf_
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int rc = batch_init(c, n, p, d_counts, st);
   if (!rc) rc = scan_chunk(c, d_in, n, 0, p, d_counts, st);
-  if (!rc && n && launch_wild(c->W, c->S, d_in, p->base_index, 0, 0, n, to_params(p), nullptr, st, c->marker()))
-    rc = MPSF_E_CUDA;
-  c->last_launches = n ? 3 : 1;
+  c->last_launches = n ? 2 : 1;
   return rc;
 }
 
@@ -642,14 +627,13 @@ int mpsf_finalize(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const m
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const Marker mk = c->marker();
   if (launch_finalize(c->W, c->S, d_in, n, to_params(p), d_out, 0, st, mk)) return MPSF_E_CUDA;
-  if (n && launch_wild(c->W, c->S, d_in, p->base_index, 1, 0, n, to_params(p), d_out, st, mk)) return MPSF_E_CUDA;
   if (launch_lists(c->S, d_in, d_out, n, p->base_index, reinterpret_cast<unsigned long long*>(d_dkeys), d_didx,
                    d_cancel, c->d_sum, st, mk))
     return MPSF_E_CUDA;
   CK(cudaEventRecord(c->ev_done, st));
   c->pending = true;
   c->last_n = n;
-  c->last_launches += n ? 3 : 1;
+  c->last_launches += n ? 2 : 1;
   return MPSF_OK;
 }
 
@@ -848,8 +832,6 @@ int mpsf_process_host(mpsf_ctx* c, const mpsf_fault_entry* h_in, uint64_t n, con
   }
   const Marker mk = c->marker();
   const Params P = to_params(p);
-  if (n && launch_wild(c->W, c->S, d_in, p->base_index, 0, 0, n, P, nullptr, st, mk)) return MPSF_E_CUDA;
-  ++launches;
   if (launch_resolve(c->W, c->S, P, d_v, c->d_count_part, c->parts, reinterpret_cast<unsigned long long*>(d_cnt),
                      st, mk))
     return MPSF_E_CUDA;
@@ -869,8 +851,7 @@ int mpsf_process_host(mpsf_ctx* c, const mpsf_fault_entry* h_in, uint64_t n, con
     Params Pk = P;
     Pk.base_index += lo;
     if (launch_finalize(c->W, c->S, d_in + lo, cnt, Pk, d_out + lo, q_lo[k], st, mk)) return MPSF_E_CUDA;
-    if (launch_wild(c->W, c->S, d_in, p->base_index, 1, lo, lo + cnt, P, d_out, st, mk)) return MPSF_E_CUDA;
-    launches += 2;
+    ++launches;
     CK(cudaEventRecord(c->ev_fin[k], st));
     CK(cudaStreamWaitEvent(c->d2h_stream, c->ev_fin[k], 0));
     CK(cudaMemcpyAsync(h_out + lo, d_out + lo, 8 * cnt, cudaMemcpyDeviceToHost, c->d2h_stream));

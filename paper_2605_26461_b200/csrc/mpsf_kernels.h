@@ -35,11 +35,6 @@ int launch_finalize(const World& W, const Scratch& S, const mpsf_fault_entry* in
 int launch_lists(const Scratch& S, const mpsf_fault_entry* in, const mpsf_out_record* out, uint64_t n,
                  uint64_t base_index, unsigned long long* dkeys, uint32_t* didx, uint32_t* cancel, DevSummary* sum,
                  cudaStream_t st, const Marker& mk);
-// wild-page entries (the list k_scan builds): phase 0 inserts their hash keys (after the scan),
-// phase 1 writes their records and list bits for batch entries [lo, hi) (after k_finalize)
-int launch_wild(const World& W, const Scratch& S, const mpsf_fault_entry* in_batch, uint64_t batch_base,
-                int phase, uint64_t lo, uint64_t hi, const Params& P, mpsf_out_record* out_batch, cudaStream_t st,
-                const Marker& mk);
 uint32_t chunk_entries();   // entries per chunk (host chunk boundaries must be multiples)
 uint64_t chunks_for(uint64_t n);
 uint64_t segments_for(uint64_t n);

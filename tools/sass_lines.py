@@ -22,10 +22,16 @@ def main():
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
     demangled = sys.argv[5] if len(sys.argv) > 5 else None
     cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"]
-    if demangled:
-        cmd += ["-k", "regex:" + demangled]
     out = subprocess.run(cmd, capture_output=True, text=True).stdout
-    rows = list(csv.reader(io.StringIO(out)))
+    # one section per profiled launch: keep the first one whose kernel name matches
+    sections = [sec for sec in out.split('"Kernel Name"')[1:]]
+    pick = sections[0]
+    if demangled:
+        for sec in sections:
+            if re.search(demangled, sec.splitlines()[0]):
+                pick = sec
+                break
+    rows = list(csv.reader(io.StringIO('"Kernel Name"' + pick)))
     hdr = rows[1]
     ia = hdr.index("Instructions Executed")
     isamp = hdr.index("Warp Stall Sampling (All Samples)")
