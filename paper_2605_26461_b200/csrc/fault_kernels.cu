@@ -844,7 +844,7 @@ __global__ void k_resolve2(World W, Scratch S, Params P) {
 // (SEG_CHUNKS chunks per segment).  k_lists then writes the cancel list and the dedup set in
 // index order: a block per segment sums the counters of the earlier segments for its base and
 // scans its own chunks' popcounts -- no serial look-back between tiles.
-constexpr uint32_t SEG_CHUNKS = 1024;
+constexpr uint32_t SEG_CHUNKS = 256;
 constexpr uint32_t KSTAGE = WCHUNK;   // dedup keys staged per chunk by k_finalize, in index order
 
 // Pass 2 per entry, in two halves so both entries of a lane issue their L2 lookups together:
@@ -1076,12 +1076,12 @@ __device__ __forceinline__ void write_summary(const Scratch& S, unsigned long lo
   out->n_dedup = err ? 0 : (tot >> 32);
 }
 
-__global__ void __launch_bounds__(1024, 2) k_lists(Scratch S, const mpsf_fault_entry* __restrict__ in,
+__global__ void __launch_bounds__(SEG_CHUNKS) k_lists(Scratch S, const mpsf_fault_entry* __restrict__ in,
                                                    const mpsf_out_record* __restrict__ out, uint64_t nq,
                                                    uint64_t base_index, unsigned long long* __restrict__ dkeys,
                                                    uint32_t* __restrict__ didx, uint32_t* __restrict__ cancel,
                                                    DevSummary* __restrict__ sum) {
-  static_assert(SEG_CHUNKS == 1024, "one thread per chunk");
+  static_assert(SEG_CHUNKS % 32 == 0 && SEG_CHUNKS <= 1024, "one thread per chunk");
   const bool last = blockIdx.x == gridDim.x - 1;
   if (__ldcg(S.ctrl + C_ERR) != 0) {
     if (last && threadIdx.x == 0) write_summary(S, 0, sum);
@@ -1391,7 +1391,7 @@ int launch_lists(const Scratch& S, const mpsf_fault_entry* in, const mpsf_out_re
     mk.mark("k_summary");
     return ok_or_err();
   }
-  k_lists<<<(unsigned)nseg, 1024, 0, st>>>(S, in, out, chunks_for(n), base_index, dkeys, didx, cancel, sum);
+  k_lists<<<(unsigned)nseg, SEG_CHUNKS, 0, st>>>(S, in, out, chunks_for(n), base_index, dkeys, didx, cancel, sum);
   mk.mark("k_lists");
   return ok_or_err();
 }
