@@ -104,7 +104,7 @@ __host__ __device__ inline Layout make_layout(const World& W, bool staged, bool 
   L.rep_chan = staged ? 32u : 0u;
   L.lut = o; o += 4 * LUT_N;
   L.slut = o; o += 4 * 32;
-  L.fclient = o; if (fin) o += al16(32ull * nc);
+  L.fclient = o; if (fin && staged) o += al16(32ull * nc);
   L.queue = o; if (!fin) o += WARPS * QCAP * 16;
   L.cinfo = o; if (staged) o += al16(512ull * nc);
   L.pg_base = o; if (staged) o += al16(4ull * nr);
@@ -589,14 +589,12 @@ __device__ __forceinline__ void flush_minima(const World& W, const Scratch& S, c
   if (threadIdx.x < 2 && v.used[threadIdx.x]) atomicAdd(S.ctrl + C_HASH_DD + threadIdx.x, v.used[threadIdx.x]);
 }
 
+// Pass 1 over entries [0, n) of `in` (global index P.base_index + i) by the calling CTA of a
+// persistent grid: stream, flush the block-local minima and counts.
 template <bool kStaged>
-__global__ void __launch_bounds__(BLOCK, 1) k_scan(World W, Scratch S, const mpsf_fault_entry* __restrict__ in,
-                                                   uint64_t n, Params P, unsigned long long* __restrict__ counts,
-                                                   uint32_t* __restrict__ count_part) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  const Layout L = make_layout(W, kStaged, false);
-  const View v = setup<kStaged>(smem, L, W, S, true, false, P.flags & MPSF_PF_ISOLATION);
-  __syncthreads();
+__device__ __forceinline__ void scan_phase(const World& W, const Scratch& S, const View& v, const Layout& L,
+                                           uint8_t* smem, const mpsf_fault_entry* __restrict__ in, uint64_t n,
+                                           const Params& P, unsigned long long* __restrict__ counts) {
   QOp* q = reinterpret_cast<QOp*>(smem + L.queue) + (threadIdx.x >> 5) * QCAP;
   uint32_t qn = 0;
   const bool sparse = W.dd_groups == 1;
@@ -645,6 +643,18 @@ __global__ void __launch_bounds__(BLOCK, 1) k_scan(World W, Scratch S, const mps
   }
 }
 
+template <bool kStaged>
+__global__ void __launch_bounds__(BLOCK, 1) k_scan(World W, Scratch S, const mpsf_fault_entry* __restrict__ in,
+                                                   uint64_t n, Params P, unsigned long long* __restrict__ counts,
+                                                   uint32_t* __restrict__ count_part) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const Layout L = make_layout(W, kStaged, false);
+  const View v = setup<kStaged>(smem, L, W, S, true, false, P.flags & MPSF_PF_ISOLATION);
+  __syncthreads();
+  scan_phase<kStaged>(W, S, v, L, smem, in, n, P, counts);
+  (void)count_part;
+}
+
 // ---- per-client resolution ------------------------------------------------------------------
 // Rules C4-C7 of SURVEY.md Appendix C (C9 "ROUND 1" + fate).  Block 0; blocks 1.. reduce counts.
 __device__ inline void kill_thresholds(const Params& P, uint32_t m1, uint32_t m2, uint32_t m3,
@@ -662,27 +672,18 @@ __device__ inline void kill_thresholds(const Params& P, uint32_t m1, uint32_t m2
   }
 }
 
-__global__ void k_resolve(World W, Scratch S, Params P, mpsf_client_verdict* __restrict__ verdict,
-                          const uint32_t* __restrict__ count_part, uint32_t n_parts,
-                          unsigned long long* __restrict__ counts) {
-  if (blockIdx.x > 0) {
-    // counts: bins x parts partial sums (parts == 0 when counts went straight to global)
-    const uint32_t bins = NSCEN * W.n_clients;
-    for (uint32_t b = (blockIdx.x - 1) * blockDim.x + threadIdx.x; b < bins; b += (gridDim.x - 1) * blockDim.x) {
-      unsigned long long s = 0;
-      for (uint32_t q = 0; q < n_parts; ++q) s += __ldcg(count_part + (uint64_t)q * bins + b);
-      if (n_parts) counts[b] = s;
-    }
-    return;
-  }
-  __shared__ int s_general;
-  if (threadIdx.x == 0) s_general = 0;
+// Rules C4-C7 (C9 "ROUND 1" + fate) for every client, by the calling block: the client states go
+// to cs (global or the CTA's shared copy), the shared scalars to gl; with `outputs` the block
+// also writes the per-client verdicts, the global copies and the path word.  Returns whether
+// the release-aware (general) path is needed -- the same on every block that calls it.
+__device__ __forceinline__ bool resolve_phase(const World& W, const Scratch& S, const Params& P, CState* cs_out,
+                                              Globals* gl, mpsf_client_verdict* __restrict__ verdict,
+                                              bool outputs, int* s_general) {
+  if (threadIdx.x == 0) *s_general = 0;
   __syncthreads();
-  if (__ldcg(S.ctrl + C_ERR) != 0) return;
   const bool iso = P.flags & MPSF_PF_ISOLATION;
-  Globals* G = S.glob;
   const bool gr_alive0 = W.has_mps && !(W.world_flags & MPSF_WF_GR_DEAD);
-  const unsigned long long trap_mps = *S.trap_mps, ft_gr = *S.ft_gr;
+  const unsigned long long trap_mps = __ldcg(S.trap_mps), ft_gr = __ldcg(S.ft_gr);
   const bool trapped_mps = gr_alive0 && trap_mps != EMPTY64;
   const bool gr_applied = gr_alive0 && !trapped_mps && ft_gr != EMPTY64;
   const long long gr_rel = (!gr_alive0 || trapped_mps) ? REL_PRE
@@ -693,7 +694,7 @@ __global__ void k_resolve(World W, Scratch S, Params P, mpsf_client_verdict* __r
     const bool sa = ce.mode == 1;
     const bool alive0 = ce.flags & 1;
     const bool ce_alive0 = !sa && alive0 && !(ce.flags & 2);
-    const unsigned long long tsa = S.trap_sa[c], fsa = S.ft_sa[c], fce = S.ft_ce[c];
+    const unsigned long long tsa = __ldcg(S.trap_sa + c), fsa = __ldcg(S.ft_sa + c), fce = __ldcg(S.ft_ce + c);
     const bool trapped = sa ? (alive0 && tsa != EMPTY64) : trapped_mps;
     const bool sa_applied = sa && alive0 && !trapped && fsa != EMPTY64;
     long long rel;
@@ -701,7 +702,7 @@ __global__ void k_resolve(World W, Scratch S, Params P, mpsf_client_verdict* __r
     else if (sa) rel = trapped ? REL_PRE : (sa_applied ? (long long)(fsa >> 8) : REL_NONE);
     else rel = gr_rel;
     const bool ce_applied = ce_alive0 && fce != EMPTY64 && !(rel < (long long)(fce >> 8));
-    const uint32_t i1 = S.iso1[c], i2 = S.iso2[c], i3 = S.iso3[c];
+    const uint32_t i1 = __ldcg(S.iso1 + c), i2 = __ldcg(S.iso2 + c), i3 = __ldcg(S.iso3 + c);
     const bool elig = (i1 & i2 & i3) != EMPTY32;
     CState cs;
     cs.rel = rel;
@@ -716,36 +717,60 @@ __global__ void k_resolve(World W, Scratch S, Params P, mpsf_client_verdict* __r
                ((!sa && (!ce_alive0 || ce_applied)) ? CS_CE_TORN : 0u) | (kill_all ? CS_KILL_ALL : 0u) |
                (trapped ? CS_TRAPPED : 0u) | (elig ? CS_ELIG : 0u);
     cs.pad = 0;
-    S.cstate[c] = cs;
-    mpsf_client_verdict v;
-    v.flags = 0;
-    if (alive0) {
-      if (trapped) { v.state = 1; v.reason = 2; v.notifier = (uint8_t)((sa ? tsa : trap_mps) & 0xFF); }
-      else if (!sa && gr_applied) { v.state = 1; v.reason = 2; v.notifier = (uint8_t)(ft_gr & 0xFF); }
-      else if (sa_applied) { v.state = 1; v.reason = 2; v.notifier = (uint8_t)(fsa & 0xFF); }
-      else if (elig) { v.state = 1; v.reason = 1; v.notifier = ce_applied ? (uint8_t)(fce & 0xFF) : 0xFF; }
-      else if (ce_applied) { v.state = 0; v.reason = 0; v.notifier = (uint8_t)(fce & 0xFF); }
-      else { v.state = 0; v.reason = 0; v.notifier = 0xFF; }
-    } else {
-      v.state = 1; v.reason = 3;
-      v.notifier = (!sa && trapped_mps) ? (uint8_t)(trap_mps & 0xFF)
-                   : ((!sa && gr_applied) ? (uint8_t)(ft_gr & 0xFF) : 0xFE);
+    cs_out[c] = cs;
+    if (outputs) {
+      if (cs_out != S.cstate) S.cstate[c] = cs;
+      mpsf_client_verdict v;
+      v.flags = 0;
+      if (alive0) {
+        if (trapped) { v.state = 1; v.reason = 2; v.notifier = (uint8_t)((sa ? tsa : trap_mps) & 0xFF); }
+        else if (!sa && gr_applied) { v.state = 1; v.reason = 2; v.notifier = (uint8_t)(ft_gr & 0xFF); }
+        else if (sa_applied) { v.state = 1; v.reason = 2; v.notifier = (uint8_t)(fsa & 0xFF); }
+        else if (elig) { v.state = 1; v.reason = 1; v.notifier = ce_applied ? (uint8_t)(fce & 0xFF) : 0xFF; }
+        else if (ce_applied) { v.state = 0; v.reason = 0; v.notifier = (uint8_t)(fce & 0xFF); }
+        else { v.state = 0; v.reason = 0; v.notifier = 0xFF; }
+      } else {
+        v.state = 1; v.reason = 3;
+        v.notifier = (!sa && trapped_mps) ? (uint8_t)(trap_mps & 0xFF)
+                     : ((!sa && gr_applied) ? (uint8_t)(ft_gr & 0xFF) : 0xFE);
+      }
+      verdict[c] = v;
     }
-    verdict[c] = v;
     // release-aware pass needed: a client released inside the drain (C3 epochs), a client
     // released before it when pass 1 kept no per-page keys, or exact M2 minima (m2 <= benign)
     if (iso && elig &&
         ((rel != REL_NONE && !(rel == REL_PRE && S.nrall)) || (rel == REL_NONE && P.m2_us <= P.benign_us)))
       general = 1;
   }
-  if (general) atomicOr(&s_general, 1);
+  if (general) atomicOr(s_general, 1);
   __syncthreads();
   if (threadIdx.x == 0) {
-    G->ft_gr_ok = gr_applied ? (uint32_t)(ft_gr >> 8) : EMPTY32;
-    G->trap_mps_idx = trapped_mps ? (uint32_t)(trap_mps >> 8) : EMPTY32;
-    G->gr_alive0 = gr_alive0;
-    S.ctrl[C_PATH] = s_general;
+    Globals g;
+    g.ft_gr_ok = gr_applied ? (uint32_t)(ft_gr >> 8) : EMPTY32;
+    g.trap_mps_idx = trapped_mps ? (uint32_t)(trap_mps >> 8) : EMPTY32;
+    g.gr_alive0 = gr_alive0;
+    g.has_elig = 0;
+    *gl = g;
+    if (outputs) {
+      if (gl != S.glob) *S.glob = g;
+      S.ctrl[C_PATH] = *s_general;
+    }
   }
+  __syncthreads();
+  if (outputs)   // the global decision table (worlds beyond the fixed layout read it in pass 2)
+    for (uint32_t c = threadIdx.x; c < W.n_clients; c += blockDim.x)
+      S.fclient[c] = fin_client(cs_out[c], *gl, S.nrall != nullptr);
+  return *s_general != 0;
+}
+
+__global__ void k_resolve(World W, Scratch S, Params P, mpsf_client_verdict* __restrict__ verdict,
+                          const uint32_t* __restrict__ count_part, uint32_t n_parts,
+                          unsigned long long* __restrict__ counts) {
+  (void)count_part; (void)n_parts; (void)counts;
+  if (blockIdx.x > 0) return;
+  __shared__ int s_general;
+  if (__ldcg(S.ctrl + C_ERR) != 0) return;
+  resolve_phase(W, S, P, S.cstate, S.glob, verdict, true, &s_general);
 }
 
 // ---- general path (rule C3 epochs) ----------------------------------------------------------
@@ -806,6 +831,15 @@ __device__ __forceinline__ void general_entry(const World& W, const View& v, con
 }
 
 template <bool kStaged, int kStage>
+__device__ __forceinline__ void general_phase(const World& W, const Scratch& S, const View& v,
+                                              const mpsf_fault_entry* __restrict__ in, uint64_t n, const Params& P) {
+  ldg_stream(in, n, [&](uint4 e0, uint64_t i0, bool ok0, uint4 e1, uint64_t i1, bool ok1) {
+    if (ok0) general_entry<kStaged, kStage>(W, v, S, P, e0, P.base_index + i0);
+    if (ok1) general_entry<kStaged, kStage>(W, v, S, P, e1, P.base_index + i1);
+  });
+}
+
+template <bool kStaged, int kStage>
 __global__ void __launch_bounds__(BLOCK, 1) k_general(World W, Scratch S, const mpsf_fault_entry* __restrict__ in,
                                                       uint64_t n, Params P) {
   if (__ldcg(S.ctrl + C_PATH) == 0) return;
@@ -813,29 +847,34 @@ __global__ void __launch_bounds__(BLOCK, 1) k_general(World W, Scratch S, const 
   const Layout L = make_layout(W, kStaged, true);
   const View v = setup<kStaged>(smem, L, W, S, false, true, P.flags & MPSF_PF_ISOLATION);
   __syncthreads();
-  ldg_stream(in, n, [&](uint4 e0, uint64_t i0, bool ok0, uint4 e1, uint64_t i1, bool ok1) {
-    if (ok0) general_entry<kStaged, kStage>(W, v, S, P, e0, P.base_index + i0);
-    if (ok1) general_entry<kStaged, kStage>(W, v, S, P, e1, P.base_index + i1);
-  });
+  general_phase<kStaged, kStage>(W, S, v, in, n, P);
 }
 
-__global__ void k_resolve2(World W, Scratch S, Params P) {
-  if (__ldcg(S.ctrl + C_PATH) == 0) return;
+// Kill thresholds from the exact minima of the general path (cs: global or the CTA's copy).
+__device__ __forceinline__ void resolve2_phase(const World& W, const Scratch& S, const Params& P, CState* cs_arr) {
   for (uint32_t c = threadIdx.x; c < W.n_clients; c += blockDim.x) {
-    CState cs = S.cstate[c];
+    CState cs = cs_arr[c];
     if (cs.rel == REL_NONE && P.m2_us > P.benign_us) continue;     // pass-1 minima are exact
     bool kill_all;
     uint32_t tie;
-    uint32_t g0 = S.giso[3 * c], g1 = S.giso[3 * c + 1], g2 = S.giso[3 * c + 2];
+    uint32_t g0 = __ldcg(S.giso + 3 * c), g1 = __ldcg(S.giso + 3 * c + 1), g2 = __ldcg(S.giso + 3 * c + 2);
     if (cs.rel == REL_NONE) {                 // only M2 needed recomputing: keep exact M1 / M3
-      g0 = S.iso1[c];
-      g2 = S.iso3[c];
+      g0 = __ldcg(S.iso1 + c);
+      g2 = __ldcg(S.iso3 + c);
     }
     kill_thresholds(P, g0, g1, g2, true, kill_all, tie);
     cs.kill_tie = tie;
     cs.flags = (cs.flags & ~CS_KILL_ALL) | (kill_all ? CS_KILL_ALL : 0u);
-    S.cstate[c] = cs;
+    cs_arr[c] = cs;
   }
+}
+
+__global__ void k_resolve2(World W, Scratch S, Params P) {
+  if (__ldcg(S.ctrl + C_PATH) == 0) return;
+  resolve2_phase(W, S, P, S.cstate);
+  __syncthreads();
+  for (uint32_t c = threadIdx.x; c < W.n_clients; c += blockDim.x)
+    S.fclient[c] = fin_client(S.cstate[c], *S.glob, S.nrall != nullptr);
 }
 
 // ---- pass 2 -----------------------------------------------------------------------------
@@ -852,42 +891,6 @@ constexpr uint32_t KSTAGE = WCHUNK;   // dedup keys staged per chunk by k_finali
 // the first-isolation word of its (client, page, epoch), its external range's first
 // isolation); fin_resolve turns the loaded words into the OutRecord, the cancel flag and the
 // dedup-set membership.  Wild pages (no range, no guard) look their keys up in the hashes.
-// Per-client decision table of pass 2, folded once per CTA from CState + Globals so an
-// entry's verdict is a few compares (rules C4-C7 of SURVEY.md Appendix C):
-//   trap records: applied iff idx == trap_ok (a second trap on a destroyed TSG is cancelled)
-//   fatal reports: applied iff the representative's ok32 == ft[channel is CE] (C4)
-//   benign completions: cancelled iff bflags[channel is CE] or ok32 > tie (C5/C6)
-//   isolation: epoch 1 iff rel < ok32 (C3); pre_nrall: epoch-1 keys are pass 1's first-record keys
-struct FinClient {
-  long long rel;
-  uint32_t trap_ok, ft0, ft1, tie;
-  uint32_t bflags;      // bit0: benign always cancelled; bit1: same for a CE channel
-  uint32_t pre_nrall;
-};
-static_assert(sizeof(FinClient) == 32, "FinClient layout");
-
-__device__ __forceinline__ FinClient fin_client(const CState& cs, const Globals& G, bool has_nrall) {
-  FinClient f;
-  f.rel = cs.rel;
-  const bool sa = cs.flags & CS_SA, alive0 = cs.flags & CS_ALIVE0;
-  if (sa) {
-    f.trap_ok = alive0 ? cs.trap_sa_idx : EMPTY32;
-    f.ft0 = (alive0 && !(cs.flags & CS_TRAPPED)) ? cs.ft_sa_ok : EMPTY32;
-    f.ft1 = f.ft0;
-  } else {
-    f.trap_ok = G.gr_alive0 ? G.trap_mps_idx : EMPTY32;
-    f.ft0 = G.ft_gr_ok;
-    f.ft1 = ((cs.flags & CS_CE_ALIVE0) && cs.ft_ce_ok != EMPTY32 && !(cs.rel < (long long)cs.ft_ce_ok))
-                ? cs.ft_ce_ok : EMPTY32;
-  }
-  const bool b0 = cs.rel != REL_NONE || (cs.flags & CS_KILL_ALL);
-  const bool b1 = b0 || (cs.flags & CS_CE_TORN);
-  f.bflags = (b0 ? 1u : 0u) | (b1 ? 2u : 0u);
-  f.tie = cs.kill_tie;
-  f.pre_nrall = (cs.rel == REL_PRE && has_nrall) ? 1u : 0u;
-  return f;
-}
-
 // Pass 2 per entry, in two halves so both entries of a lane issue their L2 lookups together:
 // fin_addr picks the words the verdict depends on (the dedup slot of its key, the
 // first-isolation word of its (client, page, epoch), its external range's first isolation);
@@ -994,24 +997,14 @@ __device__ __forceinline__ unsigned long long spread2(uint32_t x) {
   return v;
 }
 
-// Pass 2 over entries [0, n) of `in` (a chunk of the batch starting at batch chunk q_base,
-// global index P.base_index): OutRecords, per-chunk masks, segment counts.
+// Pass 2 (OutRecords, per-chunk masks, segment counts) by the calling CTA of a persistent grid over entries [0, n) of `in` (batch chunk q_base
+// on): fct / slut are the CTA's client decision table and scenario flags (shared memory).
 template <bool kStaged>
-__global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const mpsf_fault_entry* __restrict__ in,
-                                                       uint64_t n, Params P, mpsf_out_record* __restrict__ out,
-                                                       uint64_t q_base) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  if (__ldcg(S.ctrl + C_ERR) != 0) return;
-  const Layout L = make_layout(W, kStaged, true);
-  const View v = setup<kStaged>(smem, L, W, S, false, true, P.flags & MPSF_PF_ISOLATION);
-  const Globals G = *S.glob;
-  FinClient* fct = reinterpret_cast<FinClient*>(smem + L.fclient);
-  for (uint32_t k = threadIdx.x; k < W.n_clients; k += blockDim.x) fct[k] = fin_client(S.cstate[k], G, S.nrall != nullptr);
-  __syncthreads();
+__device__ __forceinline__ void finalize_phase(const World& W, const Scratch& S, const View& v,
+                                               const FinClient* fct, const uint32_t* slut,
+                                               const mpsf_fault_entry* __restrict__ in, uint64_t n, const Params& P,
+                                               mpsf_out_record* __restrict__ out, uint64_t q_base) {
   const uint32_t lane = threadIdx.x & 31;
-  uint32_t* slut = reinterpret_cast<uint32_t*>(smem + L.slut);
-  for (uint32_t k = threadIdx.x; k < 32; k += blockDim.x) slut[k] = scen_word((int)k, P.flags & MPSF_PF_ISOLATION);
-  __syncthreads();
   auto body = [&](const Dec& d0, const Dec& d1, uint64_t i0, bool ok0, bool ok1) {
     const uint64_t i1 = i0 + 1;
     FinA a0, a1;
@@ -1062,6 +1055,32 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const
       body(d0, d1, i0, ok0, ok1);
     });
   }
+}
+
+// The CTA's copies of the client decision table and the scenario flags.
+__device__ __forceinline__ void fin_tables(const World& W, const Scratch& S, const Params& P, const CState* cs,
+                                           const Globals& G, FinClient* fct, uint32_t* slut) {
+  if (fct)
+    for (uint32_t k = threadIdx.x; k < W.n_clients; k += blockDim.x) fct[k] = fin_client(cs[k], G, S.nrall != nullptr);
+  for (uint32_t k = threadIdx.x; k < 32; k += blockDim.x) slut[k] = scen_word((int)k, P.flags & MPSF_PF_ISOLATION);
+}
+
+template <bool kStaged>
+__global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const mpsf_fault_entry* __restrict__ in,
+                                                       uint64_t n, Params P, mpsf_out_record* __restrict__ out,
+                                                       uint64_t q_base) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  if (__ldcg(S.ctrl + C_ERR) != 0) return;
+  const Layout L = make_layout(W, kStaged, true);
+  const View v = setup<kStaged>(smem, L, W, S, false, true, P.flags & MPSF_PF_ISOLATION);
+  // the client decision table: the CTA's copy (fixed-layout worlds) or the global one k_resolve /
+  // k_resolve2 wrote (any number of clients)
+  FinClient* fct = kStaged ? reinterpret_cast<FinClient*>(smem + L.fclient) : S.fclient;
+  uint32_t* slut = reinterpret_cast<uint32_t*>(smem + L.slut);
+  if (kStaged) fin_tables(W, S, P, S.cstate, *S.glob, fct, slut);
+  else fin_tables(W, S, P, S.cstate, *S.glob, nullptr, slut);
+  __syncthreads();
+  finalize_phase<kStaged>(W, S, v, fct, slut, in, n, P, out, q_base);
 }
 
 // Cancel list + dedup set in index order.  Block = one segment of SEG_CHUNKS chunks, one

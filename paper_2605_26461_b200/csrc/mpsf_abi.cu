@@ -417,6 +417,7 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   const size_t s_ctrl = take(4 * C_NCTRL);
   const size_t zero_bytes = o - empty_bytes;
   const size_t s_cst = take(sizeof(CState) * std::max<uint32_t>(C, 1));
+  const size_t s_fcl = take(sizeof(FinClient) * std::max<uint32_t>(C, 1));
   if (o > c->small_cap) {
     cudaFree(c->d_small);
     c->d_small = nullptr;
@@ -451,6 +452,7 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   S.err_idx = reinterpret_cast<unsigned long long*>(s + s_err);
   S.ctrl = reinterpret_cast<uint32_t*>(s + s_ctrl);
   S.cstate = reinterpret_cast<CState*>(s + s_cst);
+  S.fclient = reinterpret_cast<FinClient*>(s + s_fcl);
   c->has_world = true;
   return MPSF_OK;
 }

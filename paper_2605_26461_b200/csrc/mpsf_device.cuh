@@ -58,6 +58,42 @@ struct Globals {
   uint32_t has_elig;
 };
 
+// Per-client decision table of pass 2, folded from CState + Globals so an
+// entry's verdict is a few compares (rules C4-C7 of SURVEY.md Appendix C):
+//   trap records: applied iff idx == trap_ok (a second trap on a destroyed TSG is cancelled)
+//   fatal reports: applied iff the representative's ok32 == ft[channel is CE] (C4)
+//   benign completions: cancelled iff bflags[channel is CE] or ok32 > tie (C5/C6)
+//   isolation: epoch 1 iff rel < ok32 (C3); pre_nrall: epoch-1 keys are pass 1's first-record keys
+struct FinClient {
+  long long rel;
+  uint32_t trap_ok, ft0, ft1, tie;
+  uint32_t bflags;      // bit0: benign always cancelled; bit1: same for a CE channel
+  uint32_t pre_nrall;
+};
+static_assert(sizeof(FinClient) == 32, "FinClient layout");
+
+__device__ __forceinline__ FinClient fin_client(const CState& cs, const Globals& G, bool has_nrall) {
+  FinClient f;
+  f.rel = cs.rel;
+  const bool sa = cs.flags & CS_SA, alive0 = cs.flags & CS_ALIVE0;
+  if (sa) {
+    f.trap_ok = alive0 ? cs.trap_sa_idx : EMPTY32;
+    f.ft0 = (alive0 && !(cs.flags & CS_TRAPPED)) ? cs.ft_sa_ok : EMPTY32;
+    f.ft1 = f.ft0;
+  } else {
+    f.trap_ok = G.gr_alive0 ? G.trap_mps_idx : EMPTY32;
+    f.ft0 = G.ft_gr_ok;
+    f.ft1 = ((cs.flags & CS_CE_ALIVE0) && cs.ft_ce_ok != EMPTY32 && !(cs.rel < (long long)cs.ft_ce_ok))
+                ? cs.ft_ce_ok : EMPTY32;
+  }
+  const bool b0 = cs.rel != REL_NONE || (cs.flags & CS_KILL_ALL);
+  const bool b1 = b0 || (cs.flags & CS_CE_TORN);
+  f.bflags = (b0 ? 1u : 0u) | (b1 ? 2u : 0u);
+  f.tie = cs.kill_tie;
+  f.pre_nrall = (cs.rel == REL_PRE && has_nrall) ? 1u : 0u;
+  return f;
+}
+
 constexpr uint32_t SKIP_MAX = 256;       // skip-table slots per client (cap)
 constexpr uint64_t VA_TABLE_LIMIT = 1ull << 44;   // interval tables hold 32-bit page numbers
 
@@ -113,6 +149,7 @@ struct Scratch {
   uint32_t* iso3;      // [C] external-range eligible (M3 candidates)
   uint32_t* giso;      // [3*C] exact per-mechanism minima, general path
   CState* cstate;      // [C]
+  FinClient* fclient;  // [C] pass-2 decision table (k_resolve / k_resolve2)
   Globals* glob;
   uint32_t* ctrl;      // [C_NCTRL]
   unsigned long long* err_idx;
