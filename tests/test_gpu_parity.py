@@ -53,6 +53,22 @@ def run_both(eng, w, entries, p):
     return got, want
 
 
+def run_device(eng, w, entries, p, dense_dedup=False):
+    """The device-resident form (mpsf_process on device buffers, no host chunking); with
+    dense_dedup the world keeps one dedup slot per (page, group) whatever its size."""
+    import torch
+    eng.set_dense_dedup(dense_dedup)
+    eng.upload_world(w)
+    try:
+        n = len(entries)
+        raw = entries.view(np.uint8).copy() if n else np.zeros(16, np.uint8)
+        d_in = torch.from_numpy(raw).cuda()
+        bufs = DeviceBuffers(n, w.n_clients)
+        return eng.process_resident(d_in, n, bp(p), bufs)
+    finally:
+        eng.set_dense_dedup(False)
+
+
 # -- golden fixtures from the reference ---------------------------------------------------
 
 def test_classify_golden_c1(eng):
@@ -108,6 +124,42 @@ def test_random_batches_vs_oracle(eng, seed):
         entries = RW.random_batch(rnd, w, rnd.randint(1, 64))
         got, want = run_both(eng, w, entries, p)
         assert_same(got, want, (seed, it))
+
+
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("dense", [False, True])
+def test_random_batches_device_form_vs_oracle(eng, seed, dense):
+    rnd = random.Random(5000 + seed)
+    for it in range(80):
+        w = RW.random_world(rnd, dead_p=0.15 if seed % 2 else 0.0)
+        p = RW.random_params(rnd)
+        entries = RW.random_batch(rnd, w, rnd.randint(1, 300))
+        got = run_device(eng, w, entries, p, dense)
+        want = so.process_batch(w, entries, p)
+        assert_same(got, want, (seed, it, dense))
+
+
+@pytest.mark.parametrize("dense", [False, True])
+def test_large_random_batch_device_form_vs_oracle(eng, dense):
+    rnd = random.Random(91)
+    for it in range(4):
+        w = RW.random_world(rnd, max_mps=6, max_sa=3)
+        p = RW.random_params(rnd)
+        entries = RW.random_batch(rnd, w, 30_000, parse_p=0.001, trap_p=0.0005, pool=12)
+        got = run_device(eng, w, entries, p, dense)
+        want = so.process_batch(w, entries, p)
+        assert_same(got, want, (it, dense))
+
+
+def test_config2b_and_storm_device_form_vs_oracle(eng):
+    w, trace = synth.make_config("c2b", n=100_000)
+    assert_same(run_device(eng, w, trace, so.Params(isolation=True)),
+                so.process_batch(w, trace, so.Params(isolation=True)), "c2b")
+    w, _ = synth.build_synthetic_world(6, 64, 3)
+    trace = synth.generate_storm(w, 80_000, 8_000, 3)
+    for iso in (True, False):
+        assert_same(run_device(eng, w, trace, so.Params(isolation=iso)),
+                    so.process_batch(w, trace, so.Params(isolation=iso)), ("storm", iso))
 
 
 def test_large_random_batch_vs_oracle(eng):

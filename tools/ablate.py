@@ -62,7 +62,14 @@ def one(wl, lib, reps):
     for _ in range(reps):
         eng.process_device(d_in, n, p, bufs)
     prof = eng.profile()
-    return {k: round(v[1] / max(v[0], 1), 4) for k, v in prof.items()}
+    res = {k: round(v[1] / max(v[0], 1), 4) for k, v in prof.items()}
+    if "k_batch" in res:
+        import ctypes
+        ts = (ctypes.c_uint64 * 8)()
+        eng.lib.mpsf_debug_phase_times(ctypes.cast(ts, ctypes.c_void_p))
+        names = ["clear", "scan", "resolve", "finalize", "lists"]
+        res["phases_us"] = {names[k]: round((ts[k + 1] - ts[k]) / 1e3, 1) for k in range(5)}
+    return res
 
 
 def main():
