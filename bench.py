@@ -217,8 +217,9 @@ def run_mine(args):
     achieved = B / (ms_step / 1e3) / 1e9
     kernels = {}
     for name, (cnt, ms) in sorted(prof.items()):
+        # the path's algorithmic bytes attributed to the kernel that moves them
         kb = {"k_scan": 16 * n, "k_general1": 16 * n, "k_general2": 16 * n,
-              "k_finalize": 16 * n + 8 * n + 12 * nd + 4 * nc}.get(name)
+              "k_finalize": 8 * n, "k_lists": 12 * nd + 4 * nc}.get(name)
         per = ms / max(cnt, 1)
         kernels[name] = {"ms": round(per, 5), "share": round(ms / max(total_ms, 1e-9), 4)}
         if kb:
