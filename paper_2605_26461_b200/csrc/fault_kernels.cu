@@ -198,13 +198,14 @@ __device__ View setup(uint8_t* sm, const Layout& L, const World& W, const Scratc
     if (tid < 2) used[tid] = 0;
     v.used = used;
   }
-  if (kStaged && fin) {
-    CState* cs = reinterpret_cast<CState*>(sm + L.cstate);
-    for (uint32_t i = tid; i < C; i += nb) cs[i] = S.cstate[i];
-    v.cst = cs;
-  }
   return v;
 }
+
+// Programmatic dependent launch: a kernel launched with programmatic stream serialization may
+// start while its predecessor drains -- it stages its world tables first, then waits here for
+// the predecessor's results (griddepcontrol.wait); pdl_trigger lets the successor start early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 __device__ __forceinline__ void raise_err(const Scratch& S, uint32_t bit, uint64_t gidx) {
   atomicOr(S.ctrl + C_ERR, bit);
@@ -648,9 +649,11 @@ __global__ void __launch_bounds__(BLOCK, 1) k_scan(World W, Scratch S, const mps
                                                    uint64_t n, Params P, unsigned long long* __restrict__ counts,
                                                    uint32_t* __restrict__ count_part) {
   extern __shared__ __align__(128) uint8_t smem[];
+  pdl_trigger();
   const Layout L = make_layout(W, kStaged, false);
   const View v = setup<kStaged>(smem, L, W, S, true, false, P.flags & MPSF_PF_ISOLATION);
   __syncthreads();
+  pdl_wait();
   scan_phase<kStaged>(W, S, v, L, smem, in, n, P, counts);
   (void)count_part;
 }
@@ -767,6 +770,8 @@ __global__ void k_resolve(World W, Scratch S, Params P, mpsf_client_verdict* __r
                           const uint32_t* __restrict__ count_part, uint32_t n_parts,
                           unsigned long long* __restrict__ counts) {
   (void)count_part; (void)n_parts; (void)counts;
+  pdl_wait();
+  pdl_trigger();
   if (blockIdx.x > 0) return;
   __shared__ int s_general;
   if (__ldcg(S.ctrl + C_ERR) != 0) return;
@@ -842,10 +847,17 @@ __device__ __forceinline__ void general_phase(const World& W, const Scratch& S, 
 template <bool kStaged, int kStage>
 __global__ void __launch_bounds__(BLOCK, 1) k_general(World W, Scratch S, const mpsf_fault_entry* __restrict__ in,
                                                       uint64_t n, Params P) {
+  pdl_trigger();
+  pdl_wait();
   if (__ldcg(S.ctrl + C_PATH) == 0) return;
   extern __shared__ __align__(128) uint8_t smem[];
   const Layout L = make_layout(W, kStaged, true);
-  const View v = setup<kStaged>(smem, L, W, S, false, true, P.flags & MPSF_PF_ISOLATION);
+  View v = setup<kStaged>(smem, L, W, S, false, true, P.flags & MPSF_PF_ISOLATION);
+  if (kStaged) {                                 // the client states k_resolve wrote
+    CState* cs = reinterpret_cast<CState*>(smem + L.cstate);
+    for (uint32_t i = threadIdx.x; i < W.n_clients; i += blockDim.x) cs[i] = S.cstate[i];
+    v.cst = cs;
+  }
   __syncthreads();
   general_phase<kStaged, kStage>(W, S, v, in, n, P);
 }
@@ -870,6 +882,8 @@ __device__ __forceinline__ void resolve2_phase(const World& W, const Scratch& S,
 }
 
 __global__ void k_resolve2(World W, Scratch S, Params P) {
+  pdl_wait();
+  pdl_trigger();
   if (__ldcg(S.ctrl + C_PATH) == 0) return;
   resolve2_phase(W, S, P, S.cstate);
   __syncthreads();
@@ -1070,9 +1084,11 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const
                                                        uint64_t n, Params P, mpsf_out_record* __restrict__ out,
                                                        uint64_t q_base) {
   extern __shared__ __align__(128) uint8_t smem[];
-  if (__ldcg(S.ctrl + C_ERR) != 0) return;
+  pdl_trigger();
   const Layout L = make_layout(W, kStaged, true);
   const View v = setup<kStaged>(smem, L, W, S, false, true, P.flags & MPSF_PF_ISOLATION);
+  pdl_wait();
+  if (__ldcg(S.ctrl + C_ERR) != 0) return;
   // the client decision table: the CTA's copy (fixed-layout worlds) or the global one k_resolve /
   // k_resolve2 wrote (any number of clients)
   FinClient* fct = kStaged ? reinterpret_cast<FinClient*>(smem + L.fclient) : S.fclient;
@@ -1101,6 +1117,7 @@ __global__ void __launch_bounds__(SEG_CHUNKS) k_lists(Scratch S, const mpsf_faul
                                                    uint32_t* __restrict__ didx, uint32_t* __restrict__ cancel,
                                                    DevSummary* __restrict__ sum) {
   static_assert(SEG_CHUNKS % 32 == 0 && SEG_CHUNKS <= 1024, "one thread per chunk");
+  pdl_wait();
   const bool last = blockIdx.x == gridDim.x - 1;
   if (__ldcg(S.ctrl + C_ERR) != 0) {
     if (last && threadIdx.x == 0) write_summary(S, 0, sum);
@@ -1222,6 +1239,7 @@ __global__ void __launch_bounds__(SEG_CHUNKS) k_lists(Scratch S, const mpsf_faul
 
 // Batch summary: error / overflow words and the list lengths (sum of the segment counters).
 __global__ void k_summary(const Scratch S, uint64_t nseg, DevSummary* out) {
+  pdl_wait();
   __shared__ unsigned long long s_tot;
   if (threadIdx.x == 0) s_tot = 0;
   __syncthreads();
@@ -1306,6 +1324,23 @@ static void set_attrs() {
 
 static int ok_or_err() { return cudaGetLastError() == cudaSuccess ? 0 : -1; }
 
+// Launch with programmatic stream serialization (the kernel may start while the previous one
+// on the stream drains; it waits with griddepcontrol.wait before reading its inputs).
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 // at least one 64-entry chunk per warp
 static int clamp_grid(int g, uint64_t n) {
   const uint64_t per_block = (uint64_t)WCHUNK * WARPS;
@@ -1326,7 +1361,7 @@ static int scan_t(const World& W, const Scratch& S, const mpsf_fault_entry* in, 
   int g = grid_for(k_scan<kStaged>, smem);
   if (kStaged && g > (int)(2 * sm_count())) g = 2 * sm_count();
   g = clamp_grid(g, n);
-  k_scan<kStaged><<<g, BLOCK, smem, st>>>(W, S, in, n, P, counts, count_part);
+  launch_pdl(k_scan<kStaged>, dim3(g), dim3(BLOCK), smem, st, W, S, in, n, P, counts, count_part);
   mk.mark("k_scan");
   // partial rows accumulate across launches and were zeroed by k_init: reduce all of them
   *parts = kStaged ? count_parts_needed(W) : 0u;
@@ -1341,10 +1376,10 @@ static int general_t(const World& W, const Scratch& S, const mpsf_fault_entry* i
   const uint32_t smem = make_layout(W, kStaged, true).total;
   int g = clamp_grid(grid_for(k_general<kStaged, 1>, smem), n);
   if (stage == 1) {
-    k_general<kStaged, 1><<<g, BLOCK, smem, st>>>(W, S, in, n, P);
+    launch_pdl(k_general<kStaged, 1>, dim3(g), dim3(BLOCK), smem, st, W, S, in, n, P);
     mk.mark("k_general1");
   } else {
-    k_general<kStaged, 2><<<g, BLOCK, smem, st>>>(W, S, in, n, P);
+    launch_pdl(k_general<kStaged, 2>, dim3(g), dim3(BLOCK), smem, st, W, S, in, n, P);
     mk.mark("k_general2");
   }
   return ok_or_err();
@@ -1357,7 +1392,7 @@ static int finalize_t(const World& W, const Scratch& S, const mpsf_fault_entry* 
   if (n == 0) return 0;
   const uint32_t smem = make_layout(W, kStaged, true).total;
   const int g = clamp_grid(grid_for(k_finalize<kStaged>, smem), n);
-  k_finalize<kStaged><<<g, BLOCK, smem, st>>>(W, S, in, n, P, out, q_base);
+  launch_pdl(k_finalize<kStaged>, dim3(g), dim3(BLOCK), smem, st, W, S, in, n, P, out, q_base);
   mk.mark("k_finalize");
   return ok_or_err();
 }
@@ -1377,7 +1412,7 @@ int launch_resolve(const World& W, const Scratch& S, const Params& P, mpsf_clien
                    const Marker& mk) {
   const uint32_t bins = NSCEN * W.n_clients;
   const uint32_t rblocks = 1 + (parts ? (bins + 255) / 256 : 0);
-  k_resolve<<<rblocks, 256, 0, st>>>(W, S, P, verdict, count_part, parts, counts);
+  launch_pdl(k_resolve, dim3(rblocks), dim3(256), 0, st, W, S, P, verdict, count_part, parts, counts);
   mk.mark("k_resolve");
   return ok_or_err();
 }
@@ -1389,7 +1424,7 @@ int launch_general(const World& W, const Scratch& S, const mpsf_fault_entry* in,
 }
 
 int launch_resolve2(const World& W, const Scratch& S, const Params& P, cudaStream_t st, const Marker& mk) {
-  k_resolve2<<<1, 256, 0, st>>>(W, S, P);
+  launch_pdl(k_resolve2, dim3(1), dim3(256), 0, st, W, S, P);
   mk.mark("k_resolve2");
   return ok_or_err();
 }
@@ -1406,11 +1441,12 @@ int launch_lists(const Scratch& S, const mpsf_fault_entry* in, const mpsf_out_re
                  cudaStream_t st, const Marker& mk) {
   const uint64_t nseg = segments_for(n);
   if (nseg == 0) {
-    k_summary<<<1, 1024, 0, st>>>(S, 0, sum);
+    launch_pdl(k_summary, dim3(1), dim3(1024), 0, st, S, (uint64_t)0, sum);
     mk.mark("k_summary");
     return ok_or_err();
   }
-  k_lists<<<(unsigned)nseg, SEG_CHUNKS, 0, st>>>(S, in, out, chunks_for(n), base_index, dkeys, didx, cancel, sum);
+  launch_pdl(k_lists, dim3((unsigned)nseg), dim3(SEG_CHUNKS), 0, st, S, in, out, chunks_for(n), base_index, dkeys,
+             didx, cancel, sum);
   mk.mark("k_lists");
   return ok_or_err();
 }
