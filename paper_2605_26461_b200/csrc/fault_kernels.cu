@@ -207,6 +207,23 @@ __device__ View setup(uint8_t* sm, const Layout& L, const World& W, const Scratc
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Branch-free conditional reductions (one predicated RED, no divergent block): the hot per-entry
+// minima and counters.  The address must be valid whatever p is.
+__device__ __forceinline__ void red_add_s(bool p, uint32_t* a) {
+  asm volatile("{.reg .pred q; setp.ne.u32 q, %0, 0; @q red.shared.add.u32 [%1], 1;}" ::"r"((uint32_t)p),
+               "r"((uint32_t)__cvta_generic_to_shared(a)) : "memory");
+}
+__device__ __forceinline__ void min_s_if(bool p, uint32_t* a, uint32_t v) {   // shared: load, compare, reduce
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(a);
+  asm volatile("{.reg .pred q, r; .reg .u32 cur; ld.shared.u32 cur, [%1]; setp.ne.u32 q, %0, 0;"
+               " setp.gt.and.u32 r, cur, %2, q; @r red.shared.min.u32 [%1], %2;}" ::"r"((uint32_t)p), "r"(sa), "r"(v)
+               : "memory");
+}
+__device__ __forceinline__ void min_g_if(bool p, uint32_t cur, uint32_t* a, uint32_t v) {   // global, pre-loaded
+  asm volatile("{.reg .pred q, r; setp.ne.u32 q, %0, 0; setp.gt.and.u32 r, %1, %2, q; @r red.relaxed.gpu.global.min.u32 [%3], %2;}"
+               ::"r"((uint32_t)p), "r"(cur), "r"(v), "l"(a) : "memory");
+}
+
 __device__ __forceinline__ void raise_err(const Scratch& S, uint32_t bit, uint64_t gidx) {
   atomicOr(S.ctrl + C_ERR, bit);
   atomicMin(S.err_idx, (unsigned long long)gidx);
@@ -480,10 +497,8 @@ __device__ __forceinline__ void scan_fast(const World& W, const View& v, const S
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const Dec d = decode_fast(v.T, W.page_state, S, e, gidx, lane);
   const uint32_t f = d.f, c = d.c, sid = f & LF_S;
-  if (f) {
-    if (kStaged) atomicAdd(v.counts + c * NSCEN + sid, 1u);
-    else atomicAdd(counts + (uint64_t)c * NSCEN + sid, 1ull);
-  }
+  if (kStaged) red_add_s(f != 0, v.counts + (f ? c * NSCEN + sid : 0u));
+  else if (f) atomicAdd(counts + (uint64_t)c * NSCEN + sid, 1ull);
   if (f & (LF_TRAP | LF_FATAL)) scan_fatal<kStaged>(v, S, f, c, d.cw, gidx);
   const uint32_t ok = ((f & LF_REPL) ? 0u : 0x80000000u) | (uint32_t)gidx;
   // isolation-eligible (pipeline.py:177-179): per-client minimum per mechanism class (iso1
@@ -495,9 +510,9 @@ __device__ __forceinline__ void scan_fast(const World& W, const View& v, const S
   const bool rr = elig && (d.guard || (d.inr && m == 2));
   if (kStaged) {
     uint32_t* pi = v.iso + (m * W.n_clients + c) * 32 + warp;
-    if (elig && *pi > ok) atomicMin(pi, ok);
+    min_s_if(elig, pi, ok);
     uint32_t* pr = (d.guard ? v.nr0 : v.ext) + (inw ? d.ridx : 0u);
-    if (rr && *pr > ok) atomicMin(pr, ok);
+    min_s_if(rr, pr, ok);
   } else {
     if (elig) min32((m == 0 ? S.iso1 : (m == 1 ? S.iso2 : S.iso3)) + c, ok);
     if (rr) min32((d.guard ? S.nr0 : S.ext) + d.ridx, ok);
@@ -617,11 +632,11 @@ __device__ __forceinline__ void scan_phase(const World& W, const Scratch& S, con
     // the L2 pre-check loads of both entries in flight together
     const uint32_t ra0 = o0.pa ? __ldcg(o0.pa) : 0u, rd0 = o0.pd ? __ldcg(o0.pd) : 0u;
     const uint32_t ra1 = o1.pa ? __ldcg(o1.pa) : 0u, rd1 = o1.pd ? __ldcg(o1.pd) : 0u;
-    if (o0.pa && ra0 > o0.va) atomicMin(o0.pa, o0.va);
-    if (o1.pa && ra1 > o1.va) atomicMin(o1.pa, o1.va);
+    min_g_if(o0.pa != nullptr, ra0, o0.pa, o0.va);
+    min_g_if(o1.pa != nullptr, ra1, o1.pa, o1.va);
     if (!sparse) {
-      if (o0.pd && rd0 > o0.vd) atomicMin(o0.pd, o0.vd);
-      if (o1.pd && rd1 > o1.vd) atomicMin(o1.pd, o1.vd);
+      min_g_if(o0.pd != nullptr, rd0, o0.pd, o0.vd);
+      min_g_if(o1.pd != nullptr, rd1, o1.pd, o1.vd);
     } else {
       if (o0.pd) claim_resolve(S, v.used, o0.pd, o0.vd, rd0, scan_dkey(o0));
       if (o1.pd) claim_resolve(S, v.used, o1.pd, o1.vd, rd1, scan_dkey(o1));
