@@ -67,6 +67,9 @@ SIGNATURES = {
     "mpsf_process_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(Params),
                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                     C.c_void_p, C.POINTER(Summary)]),
+    "mpsf_submit_host": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.POINTER(Params), C.c_void_p,
+                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "mpsf_collect_host": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(Summary)]),
     "mpsf_remap": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_uint32,
                              C.c_void_p, C.c_void_p]),
     "mpsf_remap_blocks": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p,

@@ -1466,6 +1466,35 @@ int launch_lists(const Scratch& S, const mpsf_fault_entry* in, const mpsf_out_re
   return ok_or_err();
 }
 
+// The lists of a batch straight into (device-mapped) pinned host buffers; the lengths are read
+// from the segment counters on the device, so the host never waits for them.
+__global__ void k_copyout(Scratch S, uint64_t nseg, const unsigned long long* __restrict__ d_dk,
+                          const uint32_t* __restrict__ d_di, const uint32_t* __restrict__ d_ca,
+                          unsigned long long* h_dk, uint32_t* h_di, uint32_t* h_ca) {
+  pdl_wait();
+  __shared__ unsigned long long s_tot;
+  if (threadIdx.x == 0) s_tot = 0;
+  __syncthreads();
+  if (__ldcg(S.ctrl + C_ERR) != 0) return;
+  unsigned long long acc = 0;
+  for (uint64_t i = threadIdx.x; i < nseg; i += blockDim.x) acc += __ldcg(S.segcnt + i);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(&s_tot, acc);
+  __syncthreads();
+  const uint64_t nc = s_tot & 0xFFFFFFFFull, nd = s_tot >> 32;
+  const uint64_t T = (uint64_t)gridDim.x * blockDim.x, t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (uint64_t i = t; i < nd; i += T) { h_dk[i] = __ldcs(d_dk + i); h_di[i] = __ldcs(d_di + i); }
+  for (uint64_t i = t; i < nc; i += T) h_ca[i] = __ldcs(d_ca + i);
+}
+
+int launch_copyout(const Scratch& S, uint64_t n, const unsigned long long* d_dk, const uint32_t* d_di,
+                   const uint32_t* d_ca, unsigned long long* h_dk, uint32_t* h_di, uint32_t* h_ca, cudaStream_t st) {
+  launch_pdl(k_copyout, dim3(2 * sm_count()), dim3(512), 0, st, S, segments_for(n), d_dk, d_di, d_ca, h_dk, h_di,
+             h_ca);
+  return ok_or_err();
+}
+
 int launch_hash_export(const Hash& h, uint64_t cap, unsigned long long* keys, uint32_t* vals, uint32_t* counter,
                        uint64_t out_cap, cudaStream_t st) {
   k_hash_export<<<2 * sm_count(), 256, 0, st>>>(h, cap, keys, vals, counter, out_cap);

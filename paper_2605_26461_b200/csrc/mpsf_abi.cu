@@ -54,6 +54,28 @@ constexpr int kMaxChunks = 8;
 
 }  // namespace
 
+constexpr int kSlots = 2;
+
+// One in-flight batch of the asynchronous host-buffer form.
+struct HostSlot {
+  uint8_t* d_io = nullptr;
+  size_t io_cap = 0;
+  size_t o_in = 0, o_out = 0, o_v = 0, o_cnt = 0, o_dk = 0, o_di = 0, o_ca = 0;
+  DevSummary* h_sum = nullptr;     // mapped pinned
+  DevSummary* d_sum = nullptr;
+  cudaEvent_t ev_done = nullptr;   // every output of the slot's batch is on the host
+  bool busy = false, lists_copied = false;
+  uint64_t n = 0;
+  mpsf_params p{};
+  const mpsf_fault_entry* h_in = nullptr;
+  mpsf_out_record* h_out = nullptr;
+  mpsf_client_verdict* h_verdict = nullptr;
+  uint64_t* h_counts = nullptr;
+  uint64_t* h_dkeys = nullptr;
+  uint32_t* h_didx = nullptr;
+  uint32_t* h_cancel = nullptr;
+};
+
 struct mpsf_ctx {
   int device = 0;
   cudaStream_t own_stream = nullptr;
@@ -146,8 +168,7 @@ struct mpsf_ctx {
   }
   uint32_t* d_remap_err = nullptr;
   // host-path buffers and the copy streams of the chunked pipeline
-  uint8_t* d_io = nullptr;
-  size_t io_cap = 0;
+  HostSlot slots[kSlots];
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
   cudaEvent_t ev_in[kMaxChunks] = {}, ev_fin[kMaxChunks] = {}, ev_fork = nullptr, ev_d2h = nullptr;
 };
@@ -157,7 +178,69 @@ struct mpsf_ctx {
     if ((x) != cudaSuccess) return MPSF_E_CUDA; \
   } while (0)
 
+static void fill_summary(mpsf_ctx* c, const DevSummary& d, mpsf_summary* out) {
+  memset(out, 0, sizeof(*out));
+  const uint32_t err = d.ctrl[C_ERR];
+  if (err & EB_NO_CHANNEL) out->status = MPSF_E_NO_CHANNEL;
+  else if (err & EB_BAD_ENTRY) out->status = MPSF_E_BAD_ENTRY;
+  else if (err & EB_MISMATCH) out->status = MPSF_E_ENGINE_MISMATCH;
+  else if (err & EB_VA) out->status = MPSF_E_VA_RANGE;
+  else if (d.ctrl[C_OVF]) out->status = MPSF_E_OVERFLOW;
+  else out->status = MPSF_OK;
+  out->path = d.ctrl[C_PATH];
+  out->n_dedup = d.n_dedup;
+  out->n_cancel = d.n_cancel;
+  out->error_index = d.err_idx;
+  out->hash_used = (uint64_t)d.ctrl[C_HASH_DD] + d.ctrl[C_HASH_NR];
+  // adapt the wild-page hash tables for the next call
+  if (out->status == MPSF_E_OVERFLOW) {
+    if (d.ctrl[C_HASH_DD] * 2ull >= c->hcap_dd / 2) c->want_dd = c->hcap_dd * 4;
+    if (d.ctrl[C_HASH_NR] * 2ull >= c->hcap_nr / 2) c->want_nr = c->hcap_nr * 4;
+    if (c->want_dd == c->hcap_dd && c->want_nr == c->hcap_nr) { c->want_dd *= 4; c->want_nr *= 4; }
+  } else if (out->status == MPSF_OK) {
+    c->want_dd = next_pow2(std::max<uint64_t>(1ull << 16, 4ull * d.ctrl[C_HASH_DD]));
+    c->want_nr = next_pow2(std::max<uint64_t>(1ull << 16, 4ull * d.ctrl[C_HASH_NR]));
+  }
+}
+
+static int slot_buffers(mpsf_ctx* c, HostSlot& h, uint64_t n) {
+  const uint32_t C = c->W.n_clients;
+  h.o_in = 0;
+  h.o_out = a256(16 * n);
+  h.o_v = h.o_out + a256(8 * n);
+  h.o_cnt = h.o_v + a256(4ull * C + 4);
+  h.o_dk = h.o_cnt + a256(8ull * NSCEN * C + 8);
+  h.o_di = h.o_dk + a256(8 * n);
+  h.o_ca = h.o_di + a256(4 * n);
+  const size_t total = h.o_ca + a256(4 * n + 4);
+  if (total > h.io_cap) {
+    if (h.ev_done) cudaEventSynchronize(h.ev_done);
+    cudaFree(h.d_io);
+    h.d_io = nullptr;
+    h.io_cap = 0;
+    CK(cudaMalloc(&h.d_io, total));
+    h.io_cap = total;
+  }
+  if (!h.h_sum) {
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&h.h_sum), sizeof(DevSummary), cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h.d_sum), h.h_sum, 0));
+    CK(cudaEventCreateWithFlags(&h.ev_done, cudaEventDisableTiming));
+  }
+  return MPSF_OK;
+}
+
+template <typename T>
+static T* device_view(T* host) {      // the device address of pinned host memory, or null
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, host) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return (at.type == cudaMemoryTypeHost && at.devicePointer) ? reinterpret_cast<T*>(at.devicePointer) : nullptr;
+}
+
 extern "C" {
+
 
 int mpsf_version(void) { return MPSF_ABI_VERSION; }
 
@@ -224,7 +307,11 @@ void mpsf_destroy(mpsf_ctx* c) {
   cudaFree(c->d_drec);
   cudaFree(c->d_hdd);
   cudaFree(c->d_hnr);
-  cudaFree(c->d_io);
+  for (int k = 0; k < kSlots; ++k) {
+    cudaFree(c->slots[k].d_io);
+    if (c->slots[k].h_sum) cudaFreeHost(c->slots[k].h_sum);
+    if (c->slots[k].ev_done) cudaEventDestroy(c->slots[k].ev_done);
+  }
   cudaFree(c->d_remap_err);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : c->pend_events) cudaEventDestroy(e);
@@ -713,31 +800,10 @@ int mpsf_get_summary(mpsf_ctx* c, mpsf_summary* out) {
     CK(cudaEventSynchronize(c->ev_done));
     c->pending = false;
   }
-  const DevSummary& d = *c->h_sum;
-  memset(out, 0, sizeof(*out));
-  const uint32_t err = d.ctrl[C_ERR];
-  if (err & EB_NO_CHANNEL) out->status = MPSF_E_NO_CHANNEL;
-  else if (err & EB_BAD_ENTRY) out->status = MPSF_E_BAD_ENTRY;
-  else if (err & EB_MISMATCH) out->status = MPSF_E_ENGINE_MISMATCH;
-  else if (err & EB_VA) out->status = MPSF_E_VA_RANGE;
-  else if (d.ctrl[C_OVF]) out->status = MPSF_E_OVERFLOW;
-  else out->status = MPSF_OK;
-  out->path = d.ctrl[C_PATH];
-  out->n_dedup = d.n_dedup;
-  out->n_cancel = d.n_cancel;
-  out->error_index = d.err_idx;
-  out->hash_used = (uint64_t)d.ctrl[C_HASH_DD] + d.ctrl[C_HASH_NR];
-  // adapt the wild-page hash tables for the next call
-  if (out->status == MPSF_E_OVERFLOW) {
-    if (d.ctrl[C_HASH_DD] * 2ull >= c->hcap_dd / 2) c->want_dd = c->hcap_dd * 4;
-    if (d.ctrl[C_HASH_NR] * 2ull >= c->hcap_nr / 2) c->want_nr = c->hcap_nr * 4;
-    if (c->want_dd == c->hcap_dd && c->want_nr == c->hcap_nr) { c->want_dd *= 4; c->want_nr *= 4; }
-  } else if (out->status == MPSF_OK) {
-    c->want_dd = next_pow2(std::max<uint64_t>(1ull << 16, 4ull * d.ctrl[C_HASH_DD]));
-    c->want_nr = next_pow2(std::max<uint64_t>(1ull << 16, 4ull * d.ctrl[C_HASH_NR]));
-  }
+  fill_summary(c, *c->h_sum, out);
   return MPSF_OK;
 }
+
 
 int mpsf_last_launches(mpsf_ctx* c) { return c ? c->last_launches : 0; }
 
@@ -778,55 +844,57 @@ int mpsf_get_profile(mpsf_ctx* c, mpsf_kernel_time* out, int cap) {
   return cap ? i : (int)c->acc.size();
 }
 
-int mpsf_process_host(mpsf_ctx* c, const mpsf_fault_entry* h_in, uint64_t n, const mpsf_params* p,
-                      mpsf_out_record* h_out, mpsf_client_verdict* h_verdict, uint64_t* h_counts,
-                      uint64_t* h_dkeys, uint32_t* h_didx, uint32_t* h_cancel, mpsf_summary* summary) {
-  if (!c || !p || !summary) return MPSF_E_ARG;
+// ---- host-buffer form: asynchronous two-slot pipeline -----------------------------------------
+// A slot owns the device copies of one batch's input and outputs and its mapped summary.
+// mpsf_submit_host enqueues: H2D of the entries in chunks (h2d stream) overlapping pass 1, the
+// resolution, pass 2 in chunks with the D2H of each chunk's records (d2h stream) behind it, the
+// lists, and the D2H of verdicts / counts / lists -- the lists copied by a kernel straight into
+// the caller's host buffers when they are device-accessible (pinned), so nothing waits for the
+// list lengths.  Batches run in submission order on the compute stream (the scratch is shared);
+// with two slots the H2D of batch k+1 overlaps the passes and the D2H of batch k.
+int mpsf_submit_host(mpsf_ctx* c, int slot, const mpsf_fault_entry* h_in, uint64_t n, const mpsf_params* p,
+                     mpsf_out_record* h_out, mpsf_client_verdict* h_verdict, uint64_t* h_counts,
+                     uint64_t* h_dkeys, uint32_t* h_didx, uint32_t* h_cancel) {
+  if (!c || !p || slot < 0 || slot >= kSlots) return MPSF_E_ARG;
   if (!c->has_world) return MPSF_E_NO_WORLD;
   if (n && (!h_in || !h_out || !h_dkeys || !h_didx || !h_cancel)) return MPSF_E_ARG;
-  CK(cudaSetDevice(c->device));
-  const uint32_t C = c->W.n_clients;
-  const size_t o_in = 0, o_out = a256(16 * n), o_v = o_out + a256(8 * n), o_cnt = o_v + a256(4ull * C + 4);
-  const size_t o_dk = o_cnt + a256(8ull * NSCEN * C + 8), o_di = o_dk + a256(8 * n), o_ca = o_di + a256(4 * n);
-  const size_t total = o_ca + a256(4 * n + 4);
-  if (total > c->io_cap) {
-    cudaFree(c->d_io);
-    c->d_io = nullptr;
-    c->io_cap = 0;
-    CK(cudaMalloc(&c->d_io, total));
-    c->io_cap = total;
-  }
-  uint8_t* b = c->d_io;
-  cudaStream_t st = c->own_stream;
-  const mpsf_fault_entry* d_in = reinterpret_cast<const mpsf_fault_entry*>(b + o_in);
-  mpsf_out_record* d_out = reinterpret_cast<mpsf_out_record*>(b + o_out);
-  mpsf_client_verdict* d_v = reinterpret_cast<mpsf_client_verdict*>(b + o_v);
-  uint64_t* d_cnt = reinterpret_cast<uint64_t*>(b + o_cnt);
-  unsigned long long* d_dk = reinterpret_cast<unsigned long long*>(b + o_dk);
-  uint32_t* d_di = reinterpret_cast<uint32_t*>(b + o_di);
-  uint32_t* d_ca = reinterpret_cast<uint32_t*>(b + o_ca);
+  if (c->W.n_clients && (!h_verdict || !h_counts)) return MPSF_E_ARG;
   if (p->base_index + n > MAX_GIDX) return MPSF_E_TOO_LARGE;
+  HostSlot& h = c->slots[slot];
+  if (h.busy) return MPSF_E_ARG;                   // collect it first
+  CK(cudaSetDevice(c->device));
+  int rc = slot_buffers(c, h, n);
+  if (rc) return rc;
+  h.n = n; h.p = *p; h.h_in = h_in; h.h_out = h_out; h.h_verdict = h_verdict; h.h_counts = h_counts;
+  h.h_dkeys = h_dkeys; h.h_didx = h_didx; h.h_cancel = h_cancel;
+  const uint32_t C = c->W.n_clients;
+  uint8_t* b = h.d_io;
+  cudaStream_t st = c->own_stream;
+  const mpsf_fault_entry* d_in = reinterpret_cast<const mpsf_fault_entry*>(b + h.o_in);
+  mpsf_out_record* d_out = reinterpret_cast<mpsf_out_record*>(b + h.o_out);
+  mpsf_client_verdict* d_v = reinterpret_cast<mpsf_client_verdict*>(b + h.o_v);
+  uint64_t* d_cnt = reinterpret_cast<uint64_t*>(b + h.o_cnt);
+  unsigned long long* d_dk = reinterpret_cast<unsigned long long*>(b + h.o_dk);
+  uint32_t* d_di = reinterpret_cast<uint32_t*>(b + h.o_di);
+  uint32_t* d_ca = reinterpret_cast<uint32_t*>(b + h.o_ca);
   // chunk boundaries on 64-entry chunk multiples: host chunk k = entries [e_lo[k], e_lo[k+1])
   const uint64_t ce = chunk_entries(), nq = chunks_for(n);
   const int nch = n >= (1ull << 20) ? kMaxChunks : n >= (1ull << 18) ? 4 : 1;
-  const uint64_t qpc = (nq + nch - 1) / nch;
+  const uint64_t qpc = std::max<uint64_t>(1, (nq + nch - 1) / nch);
   uint64_t q_lo[kMaxChunks + 1];
   int chunks = 0;
   for (uint64_t q = 0; q < nq; q += qpc) q_lo[chunks++] = q;
   q_lo[chunks] = nq;
   auto ent = [&](int k) { return std::min<uint64_t>(q_lo[k] * ce, n); };
-
-  // attempt 0: pipelined.  H2D chunk k (h2d stream) || pass 1 on chunk k-1 (compute stream);
-  // finalize chunk k (compute) || D2H of chunk k-1's records (d2h stream)
-  CK(cudaEventRecord(c->ev_fork, st));
-  CK(cudaStreamWaitEvent(c->h2d_stream, c->ev_fork, 0));
-  CK(cudaStreamWaitEvent(c->d2h_stream, c->ev_fork, 0));
-  int rc = batch_init(c, n, p, d_cnt, st);
+  // the slot's previous batch must have landed before its device buffers are overwritten
+  CK(cudaStreamWaitEvent(c->h2d_stream, h.ev_done, 0));
+  CK(cudaStreamWaitEvent(c->d2h_stream, h.ev_done, 0));
+  rc = batch_init(c, n, p, d_cnt, st);
   if (rc) return rc;
   int launches = 1;
   for (int k = 0; k < chunks; ++k) {
     const uint64_t lo = ent(k), cnt = ent(k + 1) - lo;
-    CK(cudaMemcpyAsync(b + o_in + 16 * lo, h_in + lo, 16 * cnt, cudaMemcpyHostToDevice, c->h2d_stream));
+    CK(cudaMemcpyAsync(b + h.o_in + 16 * lo, h_in + lo, 16 * cnt, cudaMemcpyHostToDevice, c->h2d_stream));
     CK(cudaEventRecord(c->ev_in[k], c->h2d_stream));
     CK(cudaStreamWaitEvent(st, c->ev_in[k], 0));
     if ((rc = scan_chunk(c, d_in + lo, cnt, lo, p, d_cnt, st))) return rc;
@@ -858,53 +926,93 @@ int mpsf_process_host(mpsf_ctx* c, const mpsf_fault_entry* h_in, uint64_t n, con
     CK(cudaStreamWaitEvent(c->d2h_stream, c->ev_fin[k], 0));
     CK(cudaMemcpyAsync(h_out + lo, d_out + lo, 8 * cnt, cudaMemcpyDeviceToHost, c->d2h_stream));
   }
-  if (launch_lists(c->S, d_in, d_out, n, p->base_index, d_dk, d_di, d_ca, c->d_sum, st, mk)) return MPSF_E_CUDA;
+  if (launch_lists(c->S, d_in, d_out, n, p->base_index, d_dk, d_di, d_ca, h.d_sum, st, mk)) return MPSF_E_CUDA;
   ++launches;
-  CK(cudaEventRecord(c->ev_done, st));
-  c->pending = true;
-  c->last_n = n;
-  c->last_launches = launches + 1;
   if (C) {
     CK(cudaMemcpyAsync(h_verdict, d_v, 4ull * C, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(h_counts, d_cnt, 8ull * NSCEN * C, cudaMemcpyDeviceToHost, st));
   }
-  CK(cudaEventRecord(c->ev_d2h, c->d2h_stream));
-  CK(cudaStreamWaitEvent(st, c->ev_d2h, 0));
-  if ((rc = mpsf_get_summary(c, summary))) return rc;
-  if (summary->status != MPSF_E_OVERFLOW) {
-    if (summary->status == MPSF_OK) {
+  // the lists: straight into pinned host buffers by a copy kernel (lengths stay on the device)
+  unsigned long long* hv_dk = device_view(reinterpret_cast<unsigned long long*>(h_dkeys));
+  uint32_t* hv_di = device_view(h_didx);
+  uint32_t* hv_ca = device_view(h_cancel);
+  h.lists_copied = n && hv_dk && hv_di && hv_ca;
+  if (h.lists_copied) {
+    if (launch_copyout(c->S, n, d_dk, d_di, d_ca, hv_dk, hv_di, hv_ca, st)) return MPSF_E_CUDA;
+    ++launches;
+  }
+  CK(cudaEventRecord(c->ev_fork, st));
+  CK(cudaStreamWaitEvent(c->d2h_stream, c->ev_fork, 0));
+  CK(cudaEventRecord(h.ev_done, c->d2h_stream));
+  CK(cudaStreamWaitEvent(st, h.ev_done, 0));       // the next batch's scratch use follows this one
+  h.busy = true;
+  c->last_n = n;
+  c->last_launches = launches + 1;
+  return MPSF_OK;
+}
+
+int mpsf_collect_host(mpsf_ctx* c, int slot, mpsf_summary* summary) {
+  if (!c || !summary || slot < 0 || slot >= kSlots) return MPSF_E_ARG;
+  HostSlot& h = c->slots[slot];
+  if (!h.busy) return MPSF_E_ARG;
+  CK(cudaSetDevice(c->device));
+  CK(cudaEventSynchronize(h.ev_done));
+  h.busy = false;
+  fill_summary(c, *h.h_sum, summary);
+  const uint64_t n = h.n;
+  uint8_t* b = h.d_io;
+  cudaStream_t st = c->own_stream;
+  if (summary->status == MPSF_OK) {
+    if (!h.lists_copied) {
       if (summary->n_dedup) {
-        CK(cudaMemcpyAsync(h_dkeys, d_dk, 8 * summary->n_dedup, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(h_didx, d_di, 4 * summary->n_dedup, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(h.h_dkeys, b + h.o_dk, 8 * summary->n_dedup, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(h.h_didx, b + h.o_di, 4 * summary->n_dedup, cudaMemcpyDeviceToHost, st));
       }
-      if (summary->n_cancel) CK(cudaMemcpyAsync(h_cancel, d_ca, 4 * summary->n_cancel, cudaMemcpyDeviceToHost, st));
+      if (summary->n_cancel)
+        CK(cudaMemcpyAsync(h.h_cancel, b + h.o_ca, 4 * summary->n_cancel, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
     }
-    CK(cudaStreamSynchronize(st));
     return MPSF_OK;
   }
+  if (summary->status != MPSF_E_OVERFLOW) return MPSF_OK;
   // the wild-page hash overflowed (its capacity has grown): re-run on the resident entries
-  CK(cudaStreamSynchronize(st));
+  const uint32_t C = c->W.n_clients;
+  const mpsf_fault_entry* d_in = reinterpret_cast<const mpsf_fault_entry*>(b + h.o_in);
   for (int attempt = 1; attempt < 4; ++attempt) {
-    rc = mpsf_process(c, d_in, n, p, d_out, d_v, d_cnt, reinterpret_cast<uint64_t*>(d_dk), d_di, d_ca, st);
+    int rc = mpsf_process(c, d_in, n, &h.p, reinterpret_cast<mpsf_out_record*>(b + h.o_out),
+                          reinterpret_cast<mpsf_client_verdict*>(b + h.o_v), reinterpret_cast<uint64_t*>(b + h.o_cnt),
+                          reinterpret_cast<uint64_t*>(b + h.o_dk), reinterpret_cast<uint32_t*>(b + h.o_di),
+                          reinterpret_cast<uint32_t*>(b + h.o_ca), st);
     if (rc) return rc;
-    CK(cudaMemcpyAsync(h_out, b + o_out, 8 * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h.h_out, b + h.o_out, 8 * n, cudaMemcpyDeviceToHost, st));
     if (C) {
-      CK(cudaMemcpyAsync(h_verdict, b + o_v, 4ull * C, cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(h_counts, b + o_cnt, 8ull * NSCEN * C, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(h.h_verdict, b + h.o_v, 4ull * C, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(h.h_counts, b + h.o_cnt, 8ull * NSCEN * C, cudaMemcpyDeviceToHost, st));
     }
     rc = mpsf_get_summary(c, summary);
     if (rc) return rc;
     if (summary->status == MPSF_E_OVERFLOW) continue;
     if (summary->status != MPSF_OK) return MPSF_OK;
     if (summary->n_dedup) {
-      CK(cudaMemcpyAsync(h_dkeys, b + o_dk, 8 * summary->n_dedup, cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(h_didx, b + o_di, 4 * summary->n_dedup, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(h.h_dkeys, b + h.o_dk, 8 * summary->n_dedup, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(h.h_didx, b + h.o_di, 4 * summary->n_dedup, cudaMemcpyDeviceToHost, st));
     }
-    if (summary->n_cancel) CK(cudaMemcpyAsync(h_cancel, b + o_ca, 4 * summary->n_cancel, cudaMemcpyDeviceToHost, st));
+    if (summary->n_cancel) CK(cudaMemcpyAsync(h.h_cancel, b + h.o_ca, 4 * summary->n_cancel, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return MPSF_OK;
   }
   return MPSF_OK;
+}
+
+int mpsf_process_host(mpsf_ctx* c, const mpsf_fault_entry* h_in, uint64_t n, const mpsf_params* p,
+                      mpsf_out_record* h_out, mpsf_client_verdict* h_verdict, uint64_t* h_counts,
+                      uint64_t* h_dkeys, uint32_t* h_didx, uint32_t* h_cancel, mpsf_summary* summary) {
+  if (!c || !summary) return MPSF_E_ARG;
+  for (int s = 0; s < kSlots; ++s)
+    if (c->slots[s].busy) return MPSF_E_ARG;      // not while batches are in flight
+  int rc = mpsf_submit_host(c, 0, h_in, n, p, h_out, h_verdict, h_counts, h_dkeys, h_didx, h_cancel);
+  if (rc) return rc;
+  return mpsf_collect_host(c, 0, summary);
 }
 
 int mpsf_remap(mpsf_ctx* c, uint64_t va_base, const uint64_t* d_phys, uint64_t npages4k, uint32_t gran_log2,

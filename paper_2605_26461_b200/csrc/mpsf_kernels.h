@@ -35,6 +35,8 @@ int launch_finalize(const World& W, const Scratch& S, const mpsf_fault_entry* in
 int launch_lists(const Scratch& S, const mpsf_fault_entry* in, const mpsf_out_record* out, uint64_t n,
                  uint64_t base_index, unsigned long long* dkeys, uint32_t* didx, uint32_t* cancel, DevSummary* sum,
                  cudaStream_t st, const Marker& mk);
+int launch_copyout(const Scratch& S, uint64_t n, const unsigned long long* d_dk, const uint32_t* d_di,
+                   const uint32_t* d_ca, unsigned long long* h_dk, uint32_t* h_di, uint32_t* h_ca, cudaStream_t st);
 uint32_t chunk_entries();   // entries per chunk (host chunk boundaries must be multiples)
 uint64_t chunks_for(uint64_t n);
 uint64_t segments_for(uint64_t n);

@@ -197,6 +197,35 @@ class FaultEngine:
                            out_bufs["counts"][:Cn], out_bufs["dkeys"][:s.n_dedup],
                            out_bufs["didx"][:s.n_dedup], out_bufs["cancel"][:s.n_cancel], int(s.path))
 
+    # -- asynchronous host-buffer form (two slots, pipelined batches) -------------------------
+    def submit(self, entries: np.ndarray, params: BatchParams, out_bufs: dict, slot: int) -> None:
+        """``mpsf_submit_host``: enqueue one batch into slot 0/1 and return.  ``entries`` and
+        ``out_bufs`` (``alloc_host_outputs``; pinned for device-written lists) must stay alive
+        until :meth:`collect`."""
+        entries = np.ascontiguousarray(entries, dtype=ENTRY_DTYPE)
+        p = params.to_c()
+        rc = self.lib.mpsf_submit_host(self.ctx, slot, entries.ctypes.data, len(entries), C.byref(p),
+                                       out_bufs["out"].ctypes.data, out_bufs["verdict"].ctypes.data,
+                                       out_bufs["counts"].ctypes.data, out_bufs["dkeys"].ctypes.data,
+                                       out_bufs["didx"].ctypes.data, out_bufs["cancel"].ctypes.data)
+        self._check(rc)
+        if not hasattr(self, "_inflight"):
+            self._inflight = {}
+        self._inflight[slot] = (entries, out_bufs, len(entries))
+
+    def collect(self, slot: int) -> BatchResult:
+        """``mpsf_collect_host``: wait for slot ``slot`` and return its results."""
+        entries, out_bufs, n = self._inflight.pop(slot)
+        s = _lib.Summary()
+        self._check(self.lib.mpsf_collect_host(self.ctx, slot, C.byref(s)))
+        if s.status:
+            raise_for(s.status, self.lib.mpsf_strerror(s.status).decode(), int(s.error_index))
+        Cn = self.world.n_clients
+        del entries
+        return BatchResult(out_bufs["out"][:n], out_bufs["verdict"][:Cn], out_bufs["counts"][:Cn],
+                           out_bufs["dkeys"][:s.n_dedup], out_bufs["didx"][:s.n_dedup],
+                           out_bufs["cancel"][:s.n_cancel], int(s.path))
+
     # -- recovery remap -------------------------------------------------------------------------
     def remap_device(self, va_base: int, d_phys, npages4k: int, gran_log2: int, d_out, stream=None) -> None:
         import torch

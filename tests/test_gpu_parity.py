@@ -230,6 +230,31 @@ def test_device_resident_matches_host_form(eng):
     assert_same(dev, host)
 
 
+@pytest.mark.parametrize("pinned", [True, False])
+def test_pipelined_host_batches_vs_oracle(eng, pinned):
+    """mpsf_submit_host / mpsf_collect_host: two slots in flight, batches of different sizes and
+    worlds-compatible parameters; every batch equals its oracle result."""
+    from paper_2605_26461_b200.engine import alloc_host_outputs
+    w, trace = synth.make_config("c2b", n=300_000)
+    eng.upload_world(w)
+    cuts = [(0, 120_000), (120_000, 130_000), (130_000, 300_000), (5_000, 250_000)]
+    params = [so.Params(isolation=True), so.Params(isolation=False), so.Params(isolation=True),
+              so.Params(isolation=True, m2_us=100)]
+    pending = {}
+    for k, ((lo, hi), p) in enumerate(zip(cuts, params)):
+        slot = k % 2
+        if slot in pending:
+            got = eng.collect(slot)
+            want = pending.pop(slot)
+            assert_same(got, want, ("slot", slot))
+        part = trace[lo:hi]
+        bufs = alloc_host_outputs(len(part), w.n_clients, pinned=pinned)
+        eng.submit(part, bp(p), bufs, slot)
+        pending[slot] = so.process_batch(w, part, p)
+    for slot, want in pending.items():
+        assert_same(eng.collect(slot), want, ("slot", slot))
+
+
 # -- edge cases ------------------------------------------------------------------------------
 
 def test_empty_and_invalid_batches(eng):
