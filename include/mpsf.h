@@ -170,6 +170,27 @@ int mpsf_submit_host(mpsf_ctx* ctx, int slot, const mpsf_fault_entry* h_entries,
                      uint32_t* h_dedup_idx, uint32_t* h_cancel);
 int mpsf_collect_host(mpsf_ctx* ctx, int slot, mpsf_summary* summary);
 
+/* ---- batched translation: MemoryModel.resolve_va (memory.py:339-364) over an access stream ----
+ * The step before the fault path: each access (a kind-0 entry: va, access,
+ * engine, channel) is translated in stream order against the uploaded page tables plus the
+ * one mutation translation makes -- a PREFETCH into a managed range populates its page
+ * (populate_page, memory.py:368-380), so later accesses to that page see it GPU-resident.
+ * Outputs: d_hit[n] (1 Hit, 0 Miss, 0xFF entry skipped), the misses in order as fault-buffer
+ * entries d_faults[] (the seeds mpsf_process consumes) with their indices d_fault_idx[], and
+ * d_pop_idx[] = the prefetches that populated a page.  Entry errors as mpsf_process.  Do not
+ * interleave with the phase calls of an unfinished mpsf_process batch (shared scratch). */
+typedef struct {
+  int32_t status;
+  uint32_t pad;
+  uint64_t n_miss;        /* fault entries written                                          */
+  uint64_t n_populated;   /* pages populated by prefetches                                  */
+  uint64_t error_index;
+} mpsf_translate_summary;
+int mpsf_translate(mpsf_ctx* ctx, const mpsf_fault_entry* d_accesses, uint64_t n, uint64_t base_index,
+                   uint8_t* d_hit, mpsf_fault_entry* d_faults, uint32_t* d_fault_idx, uint32_t* d_pop_idx,
+                   void* stream);
+int mpsf_get_translate_summary(mpsf_ctx* ctx, mpsf_translate_summary* out);
+
 /* Number of kernel launches the last mpsf_process / mpsf_remap enqueued. */
 int mpsf_last_launches(mpsf_ctx* ctx);
 

@@ -414,3 +414,103 @@ def remap_blocks(va_base: int, phys_pages, block_ids) -> np.ndarray:
     for j, b in enumerate(block_ids):
         out[j] = (va_base + (int(b) << K.PAGE_SHIFT), int(phys[int(b)]))
     return out
+
+
+# -- batched translation (the step before the fault path) ---------------
+
+@dataclass
+class TranslateResult:
+    hit: np.ndarray          # uint8[n]: 1 Hit, 0 Miss, 0xFF skipped (valid flag clear)
+    fault_idx: np.ndarray    # uint32[]: the misses, in access order (their seeds become fault entries)
+    pop_idx: np.ndarray      # uint32[]: prefetches that populated a page (populate_page), in order
+
+
+def translate_batch(w: FlatWorld, entries: np.ndarray, base_index: int = 0) -> TranslateResult:
+    """``MemoryModel.resolve_va`` (memory.py:339-364) over an access stream, one access at a
+    time in stream order, on the batch-start page tables plus the only mutation translation
+    itself makes: a PREFETCH into a managed range populates its page (``populate_page``,
+    memory.py:368-380: residency -> GPU, protection unchanged), so later accesses to that
+    page see it GPU-resident.  Entries are the 16-byte fault-entry format with kind 0 (the
+    would-be seed: va, access, engine, channel); the same entry errors as ``decode``."""
+    n = len(entries)
+    hit = np.full(n, 0xFF, np.uint8)
+    faults, pops = [], []
+    populated = set()                  # (ridx, page) made GPU-resident in this batch
+    nch = len(w.channels)
+    r = w.ranges
+    for i in range(n):
+        e = entries[i]
+        if not (int(e["flags"]) & K.ENTRY_FLAG_VALID):
+            continue
+        ch = int(e["channel"])
+        if ch >= nch or int(w.channels["client"][ch]) >= w.n_clients:
+            raise OracleError(ERR_BAD_CHANNEL, f"entry {i}: channel {ch} has no client")
+        c, ceng = int(w.channels["client"][ch]), int(w.channels["engine"][ch])
+        kind, eng, acc, va = int(e["kind"]), int(e["engine"]), int(e["access"]), int(e["va"])
+        if kind != K.KIND_TRANSLATION or eng > 2 or acc > 2:
+            raise OracleError(ERR_BAD_ENTRY, f"entry {i}: not a translation access")
+        if eng != ceng:
+            raise OracleError(ERR_ENGINE_MISMATCH, f"entry {i}: engine != channel engine")
+        if va >= (1 << 53):
+            raise OracleError(ERR_VA_RANGE, f"entry {i}: va >= 2^53")
+        ridx = range_at(w, c, va)
+        ok = False
+        if acc == K.ACC_PREFETCH:                                  # memory.py:344-349
+            if ridx >= 0 and int(r["kind"][ridx]) == K.RK_MANAGED:
+                page = (va - int(r["base"][ridx])) >> K.PAGE_SHIFT
+                res = page_state_at(w, ridx, va) & 0x3
+                if res != K.RES_GPU and (ridx, page) not in populated:
+                    populated.add((ridx, page))
+                    pops.append(base_index + i)
+                ok = True
+        elif ridx >= 0 and int(r["lifecycle"][ridx]) != K.LC_ZOMBIE:   # 350-353
+            page = (va - int(r["base"][ridx])) >> K.PAGE_SHIFT
+            st = page_state_at(w, ridx, va)
+            res, ro = st & 0x3, bool(st & K.PS_RO)
+            if (ridx, page) in populated:
+                res = K.RES_GPU
+            if not (not int(r["migratable"][ridx]) and res == K.RES_CPU) and \
+                    not (acc == K.ACC_WRITE and ro) and res == K.RES_GPU:   # 355-361
+                ok = True
+        hit[i] = 1 if ok else 0
+        if not ok:
+            faults.append(base_index + i)
+    return TranslateResult(hit, np.array(faults, np.uint32), np.array(pops, np.uint32))
+
+
+def translate_batch_np(w: FlatWorld, entries: np.ndarray, base_index: int = 0) -> TranslateResult:
+    """The same result as ``translate_batch`` for large streams (numpy, no per-entry loop):
+    the only in-batch dependency is "was this page populated by an earlier prefetch", i.e. the
+    first prefetch index per (range, page).  Assumes well-formed entries (no error checks)."""
+    n = len(entries)
+    valid = (entries["flags"] & K.ENTRY_FLAG_VALID) != 0
+    ch = entries["channel"].astype(np.int64)
+    client = w.channels["client"][ch].astype(np.uint64)
+    va = entries["va"].astype(np.uint64)
+    acc = entries["access"].astype(np.int64)
+    r = w.ranges
+    keys = (r["client"].astype(np.uint64) << np.uint64(40)) | (r["base"] >> np.uint64(12))
+    page = va >> np.uint64(12)
+    pos = np.searchsorted(keys, (client << np.uint64(40)) | page, side="right").astype(np.int64) - 1
+    p = np.where(pos >= 0, pos, 0)
+    has = (pos >= 0) & (r["client"][p] == client) & (page < (r["end"][p] >> np.uint64(12)))
+    slot = (r["page_off"][p].astype(np.int64) + (page - (r["base"][p] >> np.uint64(12))).astype(np.int64))
+    slot = np.where(has, slot, 0)
+    st = np.where(has, w.page_state[slot], 0).astype(np.int64)
+    res, ro = st & 3, (st & K.PS_RO) != 0
+    managed = has & (r["kind"][p] == K.RK_MANAGED)
+    pref = acc == K.ACC_PREFETCH
+    idx = np.arange(n, dtype=np.int64)
+    pf_first = np.full(len(w.page_state) + 1, np.iinfo(np.int64).max, np.int64)
+    sel = valid & pref & managed
+    np.minimum.at(pf_first, slot[sel], idx[sel])
+    populated_before = has & (pf_first[slot] < idx)
+    res_eff = np.where(populated_before, K.RES_GPU, res)
+    live = has & (r["lifecycle"][p] == K.LC_LIVE)
+    nonmig = (r["migratable"][p] == 0) & (res_eff == K.RES_CPU)
+    am = (acc == K.ACC_WRITE) & ro
+    ok = np.where(pref, managed, live & ~nonmig & ~am & (res_eff == K.RES_GPU))
+    hit = np.where(valid, ok.astype(np.uint8), np.uint8(0xFF)).astype(np.uint8)
+    pop = valid & pref & managed & (pf_first[slot] == idx) & (res != K.RES_GPU)
+    return TranslateResult(hit, (np.nonzero(valid & ~ok)[0] + base_index).astype(np.uint32),
+                           (np.nonzero(pop)[0] + base_index).astype(np.uint32))

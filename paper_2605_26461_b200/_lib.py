@@ -53,6 +53,11 @@ class Summary(C.Structure):
                 ("n_cancel", C.c_uint64), ("error_index", C.c_uint64), ("hash_used", C.c_uint64)]
 
 
+class TranslateSummary(C.Structure):
+    _fields_ = [("status", C.c_int32), ("pad", C.c_uint32), ("n_miss", C.c_uint64),
+                ("n_populated", C.c_uint64), ("error_index", C.c_uint64)]
+
+
 SIGNATURES = {
     "mpsf_version": (C.c_int, []),
     "mpsf_strerror": (C.c_char_p, [C.c_int]),
@@ -70,6 +75,9 @@ SIGNATURES = {
     "mpsf_submit_host": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.POINTER(Params), C.c_void_p,
                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "mpsf_collect_host": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(Summary)]),
+    "mpsf_translate": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
+                                 C.c_void_p, C.c_void_p, C.c_void_p]),
+    "mpsf_get_translate_summary": (C.c_int, [C.c_void_p, C.POINTER(TranslateSummary)]),
     "mpsf_remap": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_uint32,
                              C.c_void_p, C.c_void_p]),
     "mpsf_remap_blocks": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p,

@@ -75,6 +75,33 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
+// ---- batched translation LUT (MemoryModel.resolve_va, memory.py:339-364) --------------------
+// The same index space as lut_word; the word says what an access decides on the batch-start
+// page state: TR_HIT, TR_HIT_POP (the outcome once an earlier PREFETCH populated the page),
+// TR_PF (a PREFETCH into a managed range: Hit, populates the page, memory.py:344-349) and TR_POP
+// (... and the page was not GPU-resident, so populate_page changes it, memory.py:368-380).
+enum : uint32_t { TR_HIT = 1u, TR_HIT_POP = 2u, TR_PF = 4u, TR_POP = 8u };
+
+__device__ __forceinline__ uint32_t tr_word(int idx) {
+  if (idx >= LUT_XK) return LF_VALID | LF_XKIND | LF_BAD;     // translation streams: kind 0 only
+  const int st = idx & 7, rcls = (idx >> 3) & 15, ea = idx >> 7;
+  const int acc = ea % 3;
+  if (rcls > 8) return LF_VALID | LF_BAD;
+  const bool has = rcls < 8;
+  const int kind = rcls & 1, lc = (rcls >> 1) & 1, mig = (rcls >> 2) & 1;
+  const int res = st & 3;
+  const bool ro = (st & 4) != 0;
+  uint32_t w = 0;
+  if (acc == 2) {                                   // PREFETCH: Hit iff a managed range
+    if (has && kind == 0) w = TR_HIT | TR_HIT_POP | TR_PF | (res != 2 ? TR_POP : 0u);
+  } else if (has && lc == 0) {                      // zombie / no range: Miss
+    const bool am = acc == 1 && ro;
+    if (!(!mig && res == 1) && !am && res == 2) w |= TR_HIT;
+    if (!am) w |= TR_HIT_POP;                       // populated: GPU-resident, protection kept
+  }
+  return LF_VALID | w;
+}
+
 // ---- shared-memory layout ---------------------------------------------------------------
 __host__ __device__ inline uint32_t al16(uint64_t x) { return (uint32_t)((x + 15) & ~uint64_t(15)); }
 
@@ -137,7 +164,7 @@ struct View {
 
 template <bool kStaged>
 __device__ View setup(uint8_t* sm, const Layout& L, const World& W, const Scratch& S, bool scan, bool fin,
-                      bool isolation_flag) {
+                      bool isolation_flag, bool translation = false) {
   View v;
   const uint32_t tid = threadIdx.x, nb = blockDim.x;
   const uint32_t R1 = W.n_ranges + 1, C = W.n_clients;
@@ -170,7 +197,8 @@ __device__ View setup(uint8_t* sm, const Layout& L, const World& W, const Scratc
     v.T.cinfo = W.cinfo4;
   }
   uint32_t* lut = reinterpret_cast<uint32_t*>(sm + L.lut);
-  for (uint32_t i = tid; i < (uint32_t)LUT_N; i += nb) lut[i] = lut_word((int)i, isolation_flag);
+  for (uint32_t i = tid; i < (uint32_t)LUT_N; i += nb)
+    lut[i] = translation ? tr_word((int)i) : lut_word((int)i, isolation_flag);
   v.T.lut = lut;
   v.T.n_channels = W.n_channels;
   v.T.exact1 = W.exact1;
@@ -1273,6 +1301,139 @@ __global__ void k_summary(const Scratch S, uint64_t nseg, DevSummary* out) {
   }
 }
 
+// ---- batched translation kernels ------------------------------------------------------------
+// T1: the first PREFETCH index per managed page (the only in-batch dependency of resolve_va).
+template <bool kStaged>
+__global__ void __launch_bounds__(BLOCK, 1) k_tr_prefetch(World W, Scratch S, const mpsf_fault_entry* __restrict__ in,
+                                                          uint64_t n, Params P) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  pdl_trigger();
+  const Layout L = make_layout(W, kStaged, true);
+  const View v = setup<kStaged>(smem, L, W, S, false, true, false, true);
+  __syncthreads();
+  pdl_wait();
+  const uint32_t lane = threadIdx.x & 31;
+  ldg_stream(in, n, [&](uint4 e0, uint64_t i0, bool ok0, uint4 e1, uint64_t i1, bool ok1) {
+    if (!ok0) e0.w = 0;
+    if (!ok1) e1.w = 0;
+    const Dec d0 = decode_fast(v.T, W.page_state, S, e0, P.base_index + i0, lane);
+    const Dec d1 = decode_fast(v.T, W.page_state, S, e1, P.base_index + i1, lane);
+    if ((d0.f & TR_PF) && d0.inr) min32(S.pf + d0.slot, (uint32_t)(P.base_index + i0));
+    if ((d1.f & TR_PF) && d1.inr) min32(S.pf + d1.slot, (uint32_t)(P.base_index + i1));
+  });
+}
+
+// T2: Hit / Miss per access (the page state an earlier prefetch left), per-chunk ballots of
+// the misses (.x/.y) and of the populating prefetches (.z/.w), segment counters.
+template <bool kStaged>
+__global__ void __launch_bounds__(BLOCK, 1) k_tr_classify(World W, Scratch S, const mpsf_fault_entry* __restrict__ in,
+                                                          uint64_t n, Params P, uint8_t* __restrict__ hit) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  pdl_trigger();
+  const Layout L = make_layout(W, kStaged, true);
+  const View v = setup<kStaged>(smem, L, W, S, false, true, false, true);
+  __syncthreads();
+  pdl_wait();
+  if (__ldcg(S.ctrl + C_ERR) != 0) return;
+  const uint32_t lane = threadIdx.x & 31;
+  ldg_stream(in, n, [&](uint4 e0, uint64_t i0, bool ok0, uint4 e1, uint64_t i1, bool ok1) {
+    if (!ok0) e0.w = 0;
+    if (!ok1) e1.w = 0;
+    const uint32_t g0 = (uint32_t)(P.base_index + i0), g1 = (uint32_t)(P.base_index + i1);
+    const Dec d0 = decode_fast(v.T, W.page_state, S, e0, g0, lane);
+    const Dec d1 = decode_fast(v.T, W.page_state, S, e1, g1, lane);
+    const uint32_t pf0 = d0.inr ? __ldcg(S.pf + d0.slot) : EMPTY32;
+    const uint32_t pf1 = d1.inr ? __ldcg(S.pf + d1.slot) : EMPTY32;
+    const bool h0 = (d0.f & (pf0 < g0 ? TR_HIT_POP : TR_HIT)) != 0;
+    const bool h1 = (d1.f & (pf1 < g1 ? TR_HIT_POP : TR_HIT)) != 0;
+    const bool m0 = d0.f && !h0, m1 = d1.f && !h1;
+    const bool p0 = (d0.f & TR_POP) && pf0 == g0, p1 = (d1.f & TR_POP) && pf1 == g1;
+    const uint32_t b0 = d0.f ? (h0 ? 1u : 0u) : 0xFFu, b1 = d1.f ? (h1 ? 1u : 0u) : 0xFFu;
+    uint8_t* hp = hit + i0;
+    if (ok1 && (((uintptr_t)hp & 1u) == 0)) *reinterpret_cast<uint16_t*>(hp) = (uint16_t)(b0 | (b1 << 8));
+    else {
+      if (ok0) hp[0] = (uint8_t)b0;
+      if (ok1) hp[1] = (uint8_t)b1;
+    }
+    const uint32_t bm0 = __ballot_sync(0xFFFFFFFFu, ok0 && m0), bm1 = __ballot_sync(0xFFFFFFFFu, ok1 && m1);
+    const uint32_t bp0 = __ballot_sync(0xFFFFFFFFu, ok0 && p0), bp1 = __ballot_sync(0xFFFFFFFFu, ok1 && p1);
+    if (lane == 0) {
+      const uint64_t q = i0 / WCHUNK;
+      S.cmask[q] = make_uint4(bm0, bm1, bp0, bp1);
+      const uint32_t nm = __popc(bm0) + __popc(bm1), np_ = __popc(bp0) + __popc(bp1);
+      if (nm | np_) atomicAdd(S.segcnt + q / SEG_CHUNKS, (unsigned long long)nm | ((unsigned long long)np_ << 32));
+    }
+  });
+}
+
+// T3: the misses in access order as fault-buffer entries (+ their indices), the populating
+// prefetches' indices; one SEG_CHUNKS-thread block per segment (as k_lists).
+__global__ void __launch_bounds__(SEG_CHUNKS) k_tr_lists(Scratch S, const mpsf_fault_entry* __restrict__ in,
+                                                      uint64_t nq, uint64_t base_index,
+                                                      mpsf_fault_entry* __restrict__ faults,
+                                                      uint32_t* __restrict__ fault_idx, uint32_t* __restrict__ pop_idx,
+                                                      DevSummary* __restrict__ sum) {
+  pdl_wait();
+  const bool last = blockIdx.x == gridDim.x - 1;
+  if (__ldcg(S.ctrl + C_ERR) != 0) {
+    if (last && threadIdx.x == 0) write_summary(S, 0, sum);
+    return;
+  }
+  __shared__ unsigned long long s_base;
+  __shared__ unsigned long long s_w[32];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t seg = blockIdx.x;
+  unsigned long long acc = 0;
+  for (uint64_t i = threadIdx.x; i < seg; i += blockDim.x) acc += __ldcg(S.segcnt + i);
+  if (threadIdx.x == 0) s_base = 0;
+  __syncthreads();
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+  if (lane == 0 && acc) atomicAdd(&s_base, acc);
+  const uint64_t q = seg * SEG_CHUNKS + threadIdx.x;
+  ulonglong2 mk = make_ulonglong2(0, 0);
+  if (q < nq) {
+    const uint4 b = __ldcg(S.cmask + q);
+    mk = make_ulonglong2(spread2(b.x) | (spread2(b.y) << 1), spread2(b.z) | (spread2(b.w) << 1));
+  }
+  const unsigned long long mine = (unsigned long long)__popcll(mk.x) | ((unsigned long long)__popcll(mk.y) << 32);
+  unsigned long long x = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long u = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if (lane >= o) x += u;
+  }
+  if (lane == 31) s_w[warp] = x;
+  __syncthreads();
+  unsigned long long pre = s_base;
+  for (uint32_t w = 0; w < warp; ++w) pre += s_w[w];
+  if (last && threadIdx.x == blockDim.x - 1) write_summary(S, pre + x, sum);
+  pre += x - mine;
+  const uint64_t pm = pre & 0xFFFFFFFFull, pp = pre >> 32;
+  const uint32_t g0 = (uint32_t)(base_index + q * WCHUNK);
+  const unsigned long long below = (1ull << (2 * lane)) - 1ull;
+  for (int j = 0; j < 32; ++j) {                    // warp-cooperative, coalesced
+    const unsigned long long mm = __shfl_sync(0xFFFFFFFFu, mk.x, j), pm2 = __shfl_sync(0xFFFFFFFFu, mk.y, j);
+    if (!(mm | pm2)) continue;
+    const uint64_t bj = __shfl_sync(0xFFFFFFFFu, pm, j), pj = __shfl_sync(0xFFFFFFFFu, pp, j);
+    const uint32_t gj = __shfl_sync(0xFFFFFFFFu, g0, j) + 2 * lane;
+    const uint64_t qj = q - lane + j;
+    const uint32_t two = (uint32_t)(mm >> (2 * lane)) & 3u, twp = (uint32_t)(pm2 >> (2 * lane)) & 3u;
+    uint64_t pos = bj + __popcll(mm & below);
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      if (two & (1u << t)) {
+        fault_idx[pos] = gj + t;
+        reinterpret_cast<uint4*>(faults)[pos] = __ldcs(reinterpret_cast<const uint4*>(in) + qj * WCHUNK + 2 * lane + t);
+        ++pos;
+      }
+    }
+    uint64_t ppos = pj + __popcll(pm2 & below);
+    if (twp & 1u) pop_idx[ppos++] = gj;
+    if (twp & 2u) pop_idx[ppos] = gj + 1;
+  }
+}
+
 // ---- sparse hash exchange (multi-GPU) ------------------------------------------------------
 __global__ void k_hash_export(Hash h, uint64_t cap, unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals,
                               uint32_t* __restrict__ counter, uint64_t out_cap) {
@@ -1493,6 +1654,40 @@ int launch_copyout(const Scratch& S, uint64_t n, const unsigned long long* d_dk,
   launch_pdl(k_copyout, dim3(2 * sm_count()), dim3(512), 0, st, S, segments_for(n), d_dk, d_di, d_ca, h_dk, h_di,
              h_ca);
   return ok_or_err();
+}
+
+template <bool kStaged>
+static int translate_t(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
+                       uint8_t* hit, mpsf_fault_entry* faults, uint32_t* fault_idx, uint32_t* pop_idx,
+                       DevSummary* sum, cudaStream_t st, const Marker& mk) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_tr_prefetch<kStaged>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
+    cudaFuncSetAttribute(k_tr_classify<kStaged>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
+    attr = true;
+  }
+  const uint32_t smem = make_layout(W, kStaged, true).total;
+  const int g = clamp_grid(grid_for(k_tr_classify<kStaged>, smem), n);
+  launch_pdl(k_tr_prefetch<kStaged>, dim3(g), dim3(BLOCK), smem, st, W, S, in, n, P);
+  mk.mark("k_tr_prefetch");
+  launch_pdl(k_tr_classify<kStaged>, dim3(g), dim3(BLOCK), smem, st, W, S, in, n, P, hit);
+  mk.mark("k_tr_classify");
+  const uint64_t nseg = segments_for(n);
+  launch_pdl(k_tr_lists, dim3((unsigned)nseg), dim3(SEG_CHUNKS), 0, st, S, in, chunks_for(n), (uint64_t)P.base_index,
+             faults, fault_idx, pop_idx, sum);
+  mk.mark("k_tr_lists");
+  return ok_or_err();
+}
+
+int launch_translate(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
+                     uint8_t* hit, mpsf_fault_entry* faults, uint32_t* fault_idx, uint32_t* pop_idx, DevSummary* sum,
+                     cudaStream_t st, const Marker& mk) {
+  if (n == 0) {
+    launch_pdl(k_summary, dim3(1), dim3(1024), 0, st, S, (uint64_t)0, sum);
+    return ok_or_err();
+  }
+  return staged_fits(W) ? translate_t<true>(W, S, in, n, P, hit, faults, fault_idx, pop_idx, sum, st, mk)
+                        : translate_t<false>(W, S, in, n, P, hit, faults, fault_idx, pop_idx, sum, st, mk);
 }
 
 int launch_hash_export(const Hash& h, uint64_t cap, unsigned long long* keys, uint32_t* vals, uint32_t* counter,

@@ -86,6 +86,7 @@ struct mpsf_ctx {
   // scratch
   uint32_t* d_dd = nullptr;
   uint32_t* d_nr1 = nullptr;
+  uint32_t* d_pf = nullptr;     // first PREFETCH per page (batched translation)
   uint32_t* d_nrall = nullptr;
   uint64_t dd_cap = 0;
   uint32_t* d_count_part = nullptr;
@@ -304,6 +305,7 @@ void mpsf_destroy(mpsf_ctx* c) {
   cudaFree(c->d_counter);
   cudaFree(c->d_small);
   cudaFree(c->d_masks);
+  cudaFree(c->d_pf);
   cudaFree(c->d_drec);
   cudaFree(c->d_hdd);
   cudaFree(c->d_hnr);
@@ -476,6 +478,9 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
     c->pages_cap = c->dd_cap = 0;
     CK(cudaMalloc(&c->d_dd, sizeof(uint32_t) * std::max<uint64_t>(dd_words, 1)));
     CK(cudaMalloc(&c->d_nr1, sizeof(uint32_t) * std::max<uint64_t>(np, 1)));
+    cudaFree(c->d_pf);
+    c->d_pf = nullptr;
+    CK(cudaMalloc(&c->d_pf, sizeof(uint32_t) * std::max<uint64_t>(np, 1)));
     CK(cudaMalloc(&c->d_nrall, sizeof(uint32_t) * std::max<uint64_t>(np, 1)));
     c->pages_cap = np;
     c->dd_cap = dd_words;
@@ -519,6 +524,7 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   Scratch& S = c->S;
   S.dd = c->d_dd;
   S.nr1 = c->d_nr1;
+  S.pf = c->d_pf;
   // per-page first-eligible keys only for dense (small) worlds; large worlds take the
   // release-aware pass instead when a client is released before the drain
   S.nrall = W.dd_groups == 5 ? c->d_nrall : nullptr;
@@ -740,6 +746,53 @@ int mpsf_process(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const mp
   }
   if (!rc) rc = mpsf_finalize(c, d_in, n, p, d_out, d_dkeys, d_didx, d_cancel, stream);
   return rc;
+}
+
+int mpsf_translate(mpsf_ctx* c, const mpsf_fault_entry* d_acc, uint64_t n, uint64_t base_index, uint8_t* d_hit,
+                   mpsf_fault_entry* d_faults, uint32_t* d_fault_idx, uint32_t* d_pop_idx, void* stream) {
+  if (!c) return MPSF_E_ARG;
+  if (!c->has_world) return MPSF_E_NO_WORLD;
+  if (n && (!d_acc || !d_hit || !d_faults || !d_fault_idx || !d_pop_idx)) return MPSF_E_ARG;
+  if (base_index + n > MAX_GIDX) return MPSF_E_TOO_LARGE;
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int rc = ensure_call_scratch(c, n);
+  if (rc) return rc;
+  InitSegs segs{};
+  int k = 0;
+  segs.p[k] = c->d_pf; segs.words[k] = c->W.n_pages; segs.val[k++] = EMPTY32;
+  segs.p[k] = c->d_small; segs.words[k] = c->small_empty_bytes / 4; segs.val[k++] = EMPTY32;
+  segs.p[k] = c->d_small + c->small_zero_off; segs.words[k] = c->small_zero_bytes / 4; segs.val[k++] = 0;
+  segs.p[k] = c->S.segcnt; segs.words[k] = 2 * segments_for(n); segs.val[k++] = 0;
+  segs.n = k;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  c->mark_begin(st);
+  k_init<<<dim3(2 * sms, k), 256, 0, st>>>(segs);
+  c->marker().mark("k_init");
+  mpsf_params p{};
+  p.base_index = base_index;
+  if (launch_translate(c->W, c->S, d_acc, n, to_params(&p), d_hit, d_faults, d_fault_idx, d_pop_idx, c->d_sum, st,
+                       c->marker()))
+    return MPSF_E_CUDA;
+  CK(cudaEventRecord(c->ev_done, st));
+  c->pending = true;
+  c->last_n = n;
+  c->last_launches = n ? 4 : 2;
+  return MPSF_OK;
+}
+
+int mpsf_get_translate_summary(mpsf_ctx* c, mpsf_translate_summary* out) {
+  if (!c || !out) return MPSF_E_ARG;
+  mpsf_summary s;
+  const int rc = mpsf_get_summary(c, &s);
+  if (rc) return rc;
+  memset(out, 0, sizeof(*out));
+  out->status = s.status;
+  out->n_miss = s.n_cancel;
+  out->n_populated = s.n_dedup;
+  out->error_index = s.error_index;
+  return MPSF_OK;
 }
 
 int mpsf_exchange_buffers(mpsf_ctx* c, int stage, mpsf_xbuf* out, int cap) {

@@ -136,6 +136,7 @@ struct Scratch {
   uint32_t* nr0;       // [n_ranges] guard-page first-isolation key, epoch 0
   uint32_t* nr1;       // [n_pages] first-isolation key per page, epoch 1 (general path)
   uint32_t* nrall;     // [n_pages] first eligible record per in-range page (dense worlds), or null
+  uint32_t* pf;        // [n_pages] first PREFETCH per managed page (batched translation)
   Hash hdd;            // dedup keys of pages outside every range's slot span
   Hash hnr;            // NR keys (client, page, epoch) of such pages
   uint32_t* ext;       // [n_ranges] first isolation-eligible record per external range

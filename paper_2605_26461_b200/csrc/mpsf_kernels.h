@@ -37,6 +37,11 @@ int launch_lists(const Scratch& S, const mpsf_fault_entry* in, const mpsf_out_re
                  cudaStream_t st, const Marker& mk);
 int launch_copyout(const Scratch& S, uint64_t n, const unsigned long long* d_dk, const uint32_t* d_di,
                    const uint32_t* d_ca, unsigned long long* h_dk, uint32_t* h_di, uint32_t* h_ca, cudaStream_t st);
+// batched translation (MemoryModel.resolve_va over an access stream): hit bytes, the misses as
+// fault entries in order, the populating prefetches; summary n_cancel = misses, n_dedup = pops
+int launch_translate(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
+                     uint8_t* hit, mpsf_fault_entry* faults, uint32_t* fault_idx, uint32_t* pop_idx, DevSummary* sum,
+                     cudaStream_t st, const Marker& mk);
 uint32_t chunk_entries();   // entries per chunk (host chunk boundaries must be multiples)
 uint64_t chunks_for(uint64_t n);
 uint64_t segments_for(uint64_t n);

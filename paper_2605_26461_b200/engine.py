@@ -197,6 +197,47 @@ class FaultEngine:
                            out_bufs["counts"][:Cn], out_bufs["dkeys"][:s.n_dedup],
                            out_bufs["didx"][:s.n_dedup], out_bufs["cancel"][:s.n_cancel], int(s.path))
 
+    # -- batched translation (resolve_va over an access stream) -------------------------------
+    def translate_device(self, d_acc, n: int, d_hit, d_faults, d_fault_idx, d_pop_idx, base_index: int = 0,
+                         stream=None) -> None:
+        """``mpsf_translate`` on device buffers (torch tensors); see :meth:`translate_summary`."""
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        rc = self.lib.mpsf_translate(self.ctx, d_acc.data_ptr(), n, base_index, d_hit.data_ptr(),
+                                     d_faults.data_ptr(), d_fault_idx.data_ptr(), d_pop_idx.data_ptr(),
+                                     C.c_void_p(stream.cuda_stream))
+        self._check(rc)
+
+    def translate_summary(self) -> _lib.TranslateSummary:
+        s = _lib.TranslateSummary()
+        self._check(self.lib.mpsf_get_translate_summary(self.ctx, C.byref(s)))
+        if s.status:
+            raise_for(s.status, self.lib.mpsf_strerror(s.status).decode(), int(s.error_index))
+        return s
+
+    def translate(self, accesses: np.ndarray, base_index: int = 0):
+        """Host form: returns (hit u8[n], fault entries in order, their indices, populating
+        prefetch indices) -- the outputs of ``MemoryModel.resolve_va`` per access."""
+        import torch
+        accesses = np.ascontiguousarray(accesses, dtype=ENTRY_DTYPE)
+        n = len(accesses)
+        dev = torch.device("cuda", self.device)
+        raw = accesses.view(np.uint8) if n else np.zeros(16, np.uint8)
+        d_acc = torch.from_numpy(raw.copy()).to(dev)
+        d_hit = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+        d_faults = torch.empty(max(16 * n, 16), dtype=torch.uint8, device=dev)
+        d_fi = torch.empty(max(4 * n, 4), dtype=torch.uint8, device=dev)
+        d_pi = torch.empty(max(4 * n, 4), dtype=torch.uint8, device=dev)
+        self.translate_device(d_acc, n, d_hit, d_faults, d_fi, d_pi, base_index)
+        s = self.translate_summary()
+        nm, npop = int(s.n_miss), int(s.n_populated)
+        hit = d_hit[:n].cpu().numpy()
+        faults = d_faults[:16 * nm].cpu().numpy().view(ENTRY_DTYPE)
+        fi = d_fi[:4 * nm].cpu().numpy().view(np.uint32)
+        pi = d_pi[:4 * npop].cpu().numpy().view(np.uint32)
+        return hit, faults, fi, pi
+
     # -- asynchronous host-buffer form (two slots, pipelined batches) -------------------------
     def submit(self, entries: np.ndarray, params: BatchParams, out_bufs: dict, slot: int) -> None:
         """``mpsf_submit_host``: enqueue one batch into slot 0/1 and return.  ``entries`` and

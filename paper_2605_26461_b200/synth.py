@@ -199,6 +199,28 @@ def generate_trace(w: FlatWorld, spec: TraceSpec) -> np.ndarray:
     return out
 
 
+def generate_access_stream(w: FlatWorld, n: int, seed: int, wild_frac: float = 0.02,
+                           prefetch: float = 0.10) -> np.ndarray:
+    """An access stream for the batched translation (``MemoryModel.resolve_va``,
+    memory.py:339-364): the trace recipe without the would-hit rejection, so hits and misses
+    mix, with ``prefetch`` of the accesses PREFETCHes (they populate managed pages for the
+    accesses after them)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    lk = _Lookup(w)
+    client, va, engine, _ = _draw(lk, rng, n, wild_frac)
+    u = rng.random(n)
+    access = np.where(u < prefetch, K.ACC_PREFETCH, np.where(u < prefetch + (1 - prefetch) * 0.47, K.ACC_WRITE,
+                                                            K.ACC_READ)).astype(np.uint8)
+    out = np.zeros(n, ENTRY_DTYPE)
+    out["va"] = va
+    out["channel"] = client * 3 + engine
+    out["engine"] = engine
+    out["access"] = access
+    out["kind"] = K.KIND_TRANSLATION
+    out["flags"] = K.ENTRY_FLAG_VALID
+    return out
+
+
 def generate_storm(w: FlatWorld, n: int, unique: int, seed: int,
                    wild_frac: float = 0.02, device=None):
     """Config 3: ``unique`` distinct (client, page) pairs, each with one fixed
