@@ -296,6 +296,8 @@ def run_mine(args):
         extra["storm_c3"] = bench_storm(args, eng, hbm_peak, flush)
     if not args.no_remap:
         extra["remap_c4"] = bench_remap(args, eng, hbm_peak, flush)
+    if not args.no_storm and ws == 1:
+        extra["translate_f2"] = bench_translate(args, eng, hbm_peak, flush, w)
 
     if rank == 0:
         line = {
@@ -359,6 +361,49 @@ def bench_storm(args, eng, hbm_peak, flush):
                          "frac": ach / hbm_peak, "alg_bytes_per_step": B},
             "kernels": {k: round(v[1] / max(v[0], 1), 5) for k, v in sorted(prof.items())},
             "n_dedup": nd, "n_cancel": nc, "dedup_exact": bool(ok)}
+
+
+def bench_translate(args, eng, hbm_peak, flush, w):
+    """MemoryModel.resolve_va over a 10^7-access stream on the c2 world
+    (hits and misses mixed, 10 % prefetches), device-resident; checked against the oracle."""
+    import torch
+    from paper_2605_26461_b200 import synth
+    from oracle.seq_oracle import translate_batch_np
+    n = 10_000_000 if args.n is None else args.n
+    acc = synth.generate_access_stream(w, n, seed=11)
+    eng.upload_world(w)
+    dev = torch.device("cuda")
+    d_acc = torch.from_numpy(acc.view(np.uint8)).to(dev)
+    d_hit = torch.empty(n, dtype=torch.uint8, device=dev)
+    d_f = torch.empty(16 * n, dtype=torch.uint8, device=dev)
+    d_fi = torch.empty(4 * n, dtype=torch.uint8, device=dev)
+    d_pi = torch.empty(4 * n, dtype=torch.uint8, device=dev)
+    for _ in range(3):
+        eng.translate_device(d_acc, n, d_hit, d_f, d_fi, d_pi)
+    s = eng.translate_summary()
+    want = translate_batch_np(w, acc)
+    nm, npop = int(s.n_miss), int(s.n_populated)
+    exact = (np.array_equal(d_hit.cpu().numpy(), want.hit) and
+             np.array_equal(d_fi[:4 * nm].cpu().numpy().view(np.uint32), want.fault_idx) and
+             np.array_equal(d_pi[:4 * npop].cpu().numpy().view(np.uint32), want.pop_idx))
+    steps = max(5, min(args.steps, 20))
+    tot = 0.0
+    for _ in range(steps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        eng.translate_device(d_acc, n, d_hit, d_f, d_fi, d_pi)
+        b.record()
+        b.synchronize()
+        tot += a.elapsed_time(b)
+    ms = tot / steps
+    B = 16 * n + n + 20 * nm + 4 * npop          # accesses read, hit bytes, fault entries + indices
+    return {"workload": f"{n} accesses (resolve_va) on the c2 world, 10 % prefetches, 2 % wild",
+            "value": n / (ms / 1e3), "unit": "accesses/s", "ms_per_step": ms, "steps": steps,
+            "n_miss": nm, "n_populated": npop, "bit_exact_vs_oracle": bool(exact),
+            "roofline": {"bound": "hbm", "achieved": B / (ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": B / (ms / 1e3) / 1e9 / hbm_peak, "alg_bytes": B}}
 
 
 def bench_remap(args, eng, hbm_peak, flush):
