@@ -514,3 +514,54 @@ def translate_batch_np(w: FlatWorld, entries: np.ndarray, base_index: int = 0) -
     pop = valid & pref & managed & (pf_first[slot] == idx) & (res != K.RES_GPU)
     return TranslateResult(hit, (np.nonzero(valid & ~ok)[0] + base_index).astype(np.uint32),
                            (np.nonzero(pop)[0] + base_index).astype(np.uint32))
+
+
+# -- snapshot delta fold (the step after the remap) ----------------------
+
+@dataclass
+class FoldResult:
+    order: np.ndarray        # uint32[R']: request ids in first-appearance order (dict order)
+    blk_off: np.ndarray      # uint64[R'+1]: CSR offsets into blocks
+    blocks: np.ndarray       # uint32[]: each request's KV block ids, deltas concatenated in seq order
+    tok_off: np.ndarray      # uint64[R'+1]
+    tokens: np.ndarray       # uint32[]
+    progress: np.ndarray     # uint32[R']: the last snapshot's progress
+    done: np.ndarray         # uint8[R']: any snapshot done
+    last_seq: int            # last consumed sequence number
+
+
+NO_REQ = 0xFFFFFFFF
+
+
+def fold_snapshots(req, seq, nblk, ntok, progress, done, blocks, tokens) -> FoldResult:
+    """``StandbyInstance.fold`` (recovery.py:83-92) over consumed snapshots in order: per
+    request (dict insertion order = first appearance) the block-id and token deltas are
+    appended, progress is the last snapshot's, done is sticky; a snapshot without a request id
+    (``NO_REQ``) only advances ``last_consumed_seq``.  Snapshot i's deltas are
+    ``blocks[sum(nblk[:i]) : sum(nblk[:i+1])]`` (same for tokens)."""
+    folded = {}
+    bo = to = 0
+    last = 0
+    for i in range(len(req)):
+        b = blocks[bo:bo + int(nblk[i])]
+        t = tokens[to:to + int(ntok[i])]
+        bo += int(nblk[i])
+        to += int(ntok[i])
+        last = int(seq[i])
+        r = int(req[i])
+        if r == NO_REQ:
+            continue
+        e = folded.setdefault(r, [[], [], 0, False])
+        e[0].extend(int(x) for x in b)
+        e[1].extend(int(x) for x in t)
+        e[2] = int(progress[i])
+        e[3] = e[3] or bool(done[i])
+    order = np.array(list(folded), np.uint32)
+    bl = [folded[r][0] for r in folded]
+    tl = [folded[r][1] for r in folded]
+    return FoldResult(order, np.concatenate([[0], np.cumsum([len(x) for x in bl])]).astype(np.uint64),
+                      np.array([x for l in bl for x in l], np.uint32),
+                      np.concatenate([[0], np.cumsum([len(x) for x in tl])]).astype(np.uint64),
+                      np.array([x for l in tl for x in l], np.uint32),
+                      np.array([folded[r][2] for r in folded], np.uint32),
+                      np.array([folded[r][3] for r in folded], np.uint8), last)

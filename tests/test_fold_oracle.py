@@ -1,0 +1,59 @@
+"""Pin the snapshot-fold oracle (``seq_oracle.fold_snapshots``) against the reference's own
+``StandbyInstance.fold`` (recovery.py:83-92) on random consumed-snapshot sequences.  Skips when
+the reference is not importable (the GPU box)."""
+
+import random
+
+import numpy as np
+import pytest
+
+from oracle import seq_oracle as so
+from tests import refharness as H
+
+pytestmark = pytest.mark.skipif(not H.reference_available(), reason="reference not present")
+
+
+def random_snapshots(rnd, n_req, n_snap):
+    snaps = []
+    for i in range(n_snap):
+        r = rnd.randrange(n_req) if rnd.random() > 0.1 else None
+        snaps.append(dict(req=r, seq=i + 1, blocks=[rnd.randrange(1 << 20) for _ in range(rnd.randrange(0, 5))],
+                          tokens=[rnd.randrange(50000) for _ in range(rnd.randrange(0, 9))],
+                          progress=rnd.randrange(1000), done=rnd.random() < 0.1))
+    return snaps
+
+
+def to_arrays(snaps):
+    req = np.array([so.NO_REQ if s["req"] is None else s["req"] for s in snaps], np.uint32)
+    seq = np.array([s["seq"] for s in snaps], np.uint64)
+    nblk = np.array([len(s["blocks"]) for s in snaps], np.uint32)
+    ntok = np.array([len(s["tokens"]) for s in snaps], np.uint32)
+    prog = np.array([s["progress"] for s in snaps], np.uint32)
+    done = np.array([s["done"] for s in snaps], np.uint8)
+    blocks = np.array([b for s in snaps for b in s["blocks"]], np.uint32)
+    tokens = np.array([t for s in snaps for t in s["tokens"]], np.uint32)
+    return req, seq, nblk, ntok, prog, done, blocks, tokens
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_fold_oracle_matches_standby_fold(seed):
+    H.import_reference()
+    from mpssim.recovery import ForwardSnapshot, StandbyInstance
+    rnd = random.Random(70 + seed)
+    for it in range(40):
+        snaps = random_snapshots(rnd, rnd.randint(1, 12), rnd.randint(0, 80))
+        st = StandbyInstance("p", 1, 2)
+        for s in snaps:
+            st.fold(ForwardSnapshot(request_id="" if s["req"] is None else f"r{s['req']}", seq=s["seq"],
+                                    kv_block_ids_delta=list(s["blocks"]), token_delta=list(s["tokens"]),
+                                    progress=s["progress"], done=s["done"]))
+        got = so.fold_snapshots(*to_arrays(snaps))
+        assert [f"r{r}" for r in got.order] == list(st.folded)
+        for k, rid in enumerate(st.folded):
+            f = st.folded[rid]
+            b0, b1 = int(got.blk_off[k]), int(got.blk_off[k + 1])
+            t0, t1 = int(got.tok_off[k]), int(got.tok_off[k + 1])
+            assert got.blocks[b0:b1].tolist() == f.block_ids
+            assert got.tokens[t0:t1].tolist() == f.tokens
+            assert int(got.progress[k]) == f.progress and bool(got.done[k]) == f.done
+        assert got.last_seq == st.last_consumed_seq
