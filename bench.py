@@ -298,6 +298,7 @@ def run_mine(args):
         extra["remap_c4"] = bench_remap(args, eng, hbm_peak, flush)
     if not args.no_storm and ws == 1:
         extra["translate_f2"] = bench_translate(args, eng, hbm_peak, flush, w)
+        extra["fold_f3"] = bench_fold(args, eng, hbm_peak, flush)
 
     if rank == 0:
         line = {
@@ -402,6 +403,61 @@ def bench_translate(args, eng, hbm_peak, flush, w):
     return {"workload": f"{n} accesses (resolve_va) on the c2 world, 10 % prefetches, 2 % wild",
             "value": n / (ms / 1e3), "unit": "accesses/s", "ms_per_step": ms, "steps": steps,
             "n_miss": nm, "n_populated": npop, "bit_exact_vs_oracle": bool(exact),
+            "roofline": {"bound": "hbm", "achieved": B / (ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": B / (ms / 1e3) / 1e9 / hbm_peak, "alg_bytes": B}}
+
+
+def bench_fold(args, eng, hbm_peak, flush):
+    """StandbyInstance.fold over a 4 M-snapshot ring drain (100 k
+    requests, decode-step deltas: 1-4 tokens, a KV block every ~4th snapshot, 5 % liveness-only),
+    device-resident; checked against the oracle's vectorized fold."""
+    import torch
+    from oracle.seq_oracle import NO_REQ, fold_snapshots_np
+    from paper_2605_26461_b200.engine import alloc_fold_outputs
+    S, R = 4_000_000, 100_000
+    rng = np.random.default_rng(21)
+    req = rng.integers(0, R, S, dtype=np.uint32)
+    req[rng.random(S) < 0.05] = NO_REQ
+    seq = np.arange(1, S + 1, dtype=np.uint64)
+    ntok = rng.integers(1, 5, S, dtype=np.uint32)
+    nblk = (rng.random(S) < 0.25).astype(np.uint32)
+    prog = rng.integers(0, 1 << 20, S, dtype=np.uint32)
+    done = (rng.random(S) < 0.01).astype(np.uint8)
+    blocks = rng.integers(0, 1 << 24, int(nblk.sum()), dtype=np.uint32)
+    tokens = rng.integers(0, 50000, int(ntok.sum()), dtype=np.uint32)
+    dev = torch.device("cuda")
+    up = lambda a: torch.from_numpy(a.view(np.uint8).copy()).to(dev)  # noqa: E731
+    d = [up(req), up(nblk), up(ntok), up(prog), up(done), up(blocks), up(tokens)]
+    out = alloc_fold_outputs(S, len(blocks), len(tokens))
+    for _ in range(3):
+        s = eng.fold_device(S, R, *d, out)
+    want = fold_snapshots_np(req, seq, nblk, ntok, prog, done, blocks, tokens)
+    r, nb, nt = int(s.n_requests), int(s.n_blocks), int(s.n_tokens)
+    exact = (r == len(want.order) and
+             np.array_equal(out["order"][:4 * r].cpu().numpy().view(np.uint32), want.order) and
+             np.array_equal(out["blk_off"][:8 * (r + 1)].cpu().numpy().view(np.uint64), want.blk_off) and
+             np.array_equal(out["blocks"][:4 * nb].cpu().numpy().view(np.uint32), want.blocks) and
+             np.array_equal(out["tokens"][:4 * nt].cpu().numpy().view(np.uint32), want.tokens) and
+             np.array_equal(out["progress"][:4 * r].cpu().numpy().view(np.uint32), want.progress) and
+             np.array_equal(out["done"][:r].cpu().numpy(), want.done))
+    steps = max(5, min(args.steps, 20))
+    tot = 0.0
+    for _ in range(steps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        eng.fold_device(S, R, *d, out)     # includes the summary read (a stream sync)
+        b.record()
+        b.synchronize()
+        tot += a.elapsed_time(b)
+    ms = tot / steps
+    # snapshot SoA read (17 B) + payload read and written + per-request outputs (order,
+    # offsets, progress, done = 25 B)
+    B = 17 * S + 8 * (nb + nt) + 25 * r
+    return {"workload": f"{S} snapshots, {R} requests, decode-step deltas (fold)",
+            "value": S / (ms / 1e3), "unit": "snapshots/s", "ms_per_step": ms, "steps": steps,
+            "n_requests": r, "n_blocks": nb, "n_tokens": nt, "bit_exact_vs_oracle": bool(exact),
             "roofline": {"bound": "hbm", "achieved": B / (ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                          "frac": B / (ms / 1e3) / 1e9 / hbm_peak, "alg_bytes": B}}
 

@@ -191,6 +191,34 @@ int mpsf_translate(mpsf_ctx* ctx, const mpsf_fault_entry* d_accesses, uint64_t n
                    void* stream);
 int mpsf_get_translate_summary(mpsf_ctx* ctx, mpsf_translate_summary* out);
 
+/* ---- snapshot delta fold: StandbyInstance.fold (recovery.py:83-92) over a batch ----
+ * The step after the recovery remap.  n_snap ForwardSnapshots
+ * (recovery.py:30-41) in consume order, as device arrays: d_req[i] the request id (< n_req_ids)
+ * or 0xFFFFFFFF for a liveness-only snapshot; d_nblk[i] / d_ntok[i] the lengths of its
+ * KV-block and token deltas, concatenated in consume order in d_blocks / d_tokens;
+ * d_progress[i]; d_done[i] (0/1).  Output per request, in first-appearance order (the
+ * fold dict's insertion order): d_order[k] its id, the CSR offsets d_blk_off[k..k+1] /
+ * d_tok_off[k..k+1] into d_blocks_out / d_tokens_out (the deltas appended in consume order),
+ * d_progress_out[k] (the last snapshot's), d_done_out[k] (sticky OR).  Capacities: n_snap
+ * for the per-request arrays, n_snap+1 for the offsets, the input totals for the payloads.
+ * last_consumed_seq is the last snapshot's seq (the caller holds it).  A request id >= n_req_ids
+ * returns MPSF_E_BAD_ENTRY with the first such snapshot in error_index (its snapshot is not
+ * folded).  Synchronous on `stream` (the summary needs the counts). */
+typedef struct {
+  int32_t status;
+  uint32_t pad;
+  uint64_t n_requests;
+  uint64_t n_blocks;
+  uint64_t n_tokens;
+  uint64_t error_index;
+} mpsf_fold_summary;
+int mpsf_fold(mpsf_ctx* ctx, uint64_t n_snap, uint32_t n_req_ids, const uint32_t* d_req,
+              const uint32_t* d_nblk, const uint32_t* d_ntok, const uint32_t* d_progress,
+              const uint8_t* d_done, const uint32_t* d_blocks, const uint32_t* d_tokens,
+              uint32_t* d_order, uint64_t* d_blk_off, uint32_t* d_blocks_out, uint64_t* d_tok_off,
+              uint32_t* d_tokens_out, uint32_t* d_progress_out, uint8_t* d_done_out,
+              mpsf_fold_summary* summary, void* stream);
+
 /* Number of kernel launches the last mpsf_process / mpsf_remap enqueued. */
 int mpsf_last_launches(mpsf_ctx* ctx);
 

@@ -565,3 +565,47 @@ def fold_snapshots(req, seq, nblk, ntok, progress, done, blocks, tokens) -> Fold
                       np.array([x for l in tl for x in l], np.uint32),
                       np.array([folded[r][2] for r in folded], np.uint32),
                       np.array([folded[r][3] for r in folded], np.uint8), last)
+
+
+def _seg_gather(src, starts, lens):
+    """Concatenate src[starts[k] : starts[k]+lens[k]] over k (vectorized)."""
+    lens = np.asarray(lens, np.int64)
+    tot = int(lens.sum())
+    if tot == 0:
+        return np.zeros(0, src.dtype)
+    excl = np.cumsum(lens) - lens
+    return src[np.repeat(np.asarray(starts, np.int64) - excl, lens) + np.arange(tot)]
+
+
+def fold_snapshots_np(req, seq, nblk, ntok, progress, done, blocks, tokens) -> FoldResult:
+    """Vectorized ``fold_snapshots`` for large batches (the same result; checked against the
+    loop form in tests/test_fold_oracle.py): requests ranked by first appearance, snapshots
+    stably grouped by rank, deltas gathered by segment."""
+    req = np.asarray(req, np.uint32)
+    nblk = np.asarray(nblk, np.int64)
+    ntok = np.asarray(ntok, np.int64)
+    blocks = np.asarray(blocks, np.uint32)
+    tokens = np.asarray(tokens, np.uint32)
+    idx = np.nonzero(req != NO_REQ)[0]
+    r = req[idx]
+    uniq, first = np.unique(r, return_index=True)
+    pos = np.argsort(first, kind="stable")
+    order = uniq[pos].astype(np.uint32)
+    rank_u = np.empty(len(uniq), np.int64)
+    rank_u[pos] = np.arange(len(uniq))
+    rk = rank_u[np.searchsorted(uniq, r)]
+    o = np.argsort(rk, kind="stable")
+    perm, rks = idx[o], rk[o]
+    bstart = np.cumsum(nblk) - nblk
+    tstart = np.cumsum(ntok) - ntok
+    R = len(order)
+    bc = np.bincount(rks, weights=nblk[perm], minlength=R).astype(np.int64) if R else np.zeros(0, np.int64)
+    tc = np.bincount(rks, weights=ntok[perm], minlength=R).astype(np.int64) if R else np.zeros(0, np.int64)
+    ends = np.cumsum(np.bincount(rks, minlength=R)) - 1 if R else np.zeros(0, np.int64)
+    dn = np.bincount(rks, weights=np.asarray(done)[perm] != 0, minlength=R) if R else np.zeros(0)
+    return FoldResult(order, np.concatenate([[0], np.cumsum(bc)]).astype(np.uint64),
+                      _seg_gather(blocks, bstart[perm], nblk[perm]).astype(np.uint32),
+                      np.concatenate([[0], np.cumsum(tc)]).astype(np.uint64),
+                      _seg_gather(tokens, tstart[perm], ntok[perm]).astype(np.uint32),
+                      np.asarray(progress, np.uint32)[perm[ends]] if R else np.zeros(0, np.uint32),
+                      (dn > 0).astype(np.uint8), int(seq[-1]) if len(req) else 0)

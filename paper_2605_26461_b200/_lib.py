@@ -53,6 +53,11 @@ class Summary(C.Structure):
                 ("n_cancel", C.c_uint64), ("error_index", C.c_uint64), ("hash_used", C.c_uint64)]
 
 
+class FoldSummary(C.Structure):
+    _fields_ = [("status", C.c_int32), ("pad", C.c_uint32), ("n_requests", C.c_uint64),
+                ("n_blocks", C.c_uint64), ("n_tokens", C.c_uint64), ("error_index", C.c_uint64)]
+
+
 class TranslateSummary(C.Structure):
     _fields_ = [("status", C.c_int32), ("pad", C.c_uint32), ("n_miss", C.c_uint64),
                 ("n_populated", C.c_uint64), ("error_index", C.c_uint64)]
@@ -80,6 +85,8 @@ SIGNATURES = {
     "mpsf_get_translate_summary": (C.c_int, [C.c_void_p, C.POINTER(TranslateSummary)]),
     "mpsf_remap": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_uint32,
                              C.c_void_p, C.c_void_p]),
+    "mpsf_fold": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32] + [C.c_void_p] * 14
+                  + [C.POINTER(FoldSummary), C.c_void_p]),
     "mpsf_remap_blocks": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p,
                                     C.c_uint64, C.c_void_p, C.c_void_p]),
     "mpsf_last_launches": (C.c_int, [C.c_void_p]),

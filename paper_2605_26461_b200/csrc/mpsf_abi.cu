@@ -168,6 +168,8 @@ struct mpsf_ctx {
     return m;
   }
   uint32_t* d_remap_err = nullptr;
+  uint8_t* d_fold = nullptr;    // snapshot-fold scratch (grown on demand)
+  size_t fold_cap = 0;
   // host-path buffers and the copy streams of the chunked pipeline
   HostSlot slots[kSlots];
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
@@ -315,6 +317,7 @@ void mpsf_destroy(mpsf_ctx* c) {
     if (c->slots[k].ev_done) cudaEventDestroy(c->slots[k].ev_done);
   }
   cudaFree(c->d_remap_err);
+  cudaFree(c->d_fold);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : c->pend_events) cudaEventDestroy(e);
   if (c->h_sum) cudaFreeHost(c->h_sum);
@@ -1093,6 +1096,46 @@ int mpsf_remap_blocks(mpsf_ctx* c, uint64_t va_base, const uint64_t* d_phys, uin
   CK(cudaStreamSynchronize(st));
   c->last_launches = nblocks ? 1 : 0;
   return err ? MPSF_E_ARG : MPSF_OK;
+}
+
+int mpsf_fold(mpsf_ctx* c, uint64_t n_snap, uint32_t n_req_ids, const uint32_t* d_req, const uint32_t* d_nblk,
+              const uint32_t* d_ntok, const uint32_t* d_progress, const uint8_t* d_done, const uint32_t* d_blocks,
+              const uint32_t* d_tokens, uint32_t* d_order, uint64_t* d_blk_off, uint32_t* d_blocks_out,
+              uint64_t* d_tok_off, uint32_t* d_tokens_out, uint32_t* d_progress_out, uint8_t* d_done_out,
+              mpsf_fold_summary* summary, void* stream) {
+  if (!c || !summary) return MPSF_E_ARG;
+  if (n_snap >= (1ull << 31) - 1) return MPSF_E_TOO_LARGE;
+  if (n_snap && (!d_req || !d_nblk || !d_ntok || !d_progress || !d_done || !d_order || !d_blk_off ||
+                 !d_tok_off || !d_progress_out || !d_done_out))
+    return MPSF_E_ARG;
+  *summary = mpsf_fold_summary{};
+  summary->error_index = ~0ull;
+  if (!n_snap) return MPSF_OK;
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t need = fold_scratch_bytes(n_snap, n_req_ids ? n_req_ids : 1);
+  if (need > c->fold_cap) {
+    CK(cudaStreamSynchronize(st));
+    cudaFree(c->d_fold);
+    c->d_fold = nullptr;
+    c->fold_cap = 0;
+    CK(cudaMalloc(&c->d_fold, need));
+    c->fold_cap = need;
+  }
+  FoldTotals tot{};
+  c->mark_begin(st);
+  if (launch_fold(c->d_fold, c->fold_cap, (uint32_t)n_snap, n_req_ids ? n_req_ids : 1, d_req, d_nblk, d_ntok,
+                  d_progress, d_done, d_blocks, d_tokens, d_order, d_blk_off, d_blocks_out, d_tok_off, d_tokens_out,
+                  d_progress_out, d_done_out, &tot, st))
+    return MPSF_E_CUDA;
+  c->marker().mark("k_fold");
+  c->last_launches = 7;   // own kernels; the CUB scans and the radix sort add theirs
+  summary->n_requests = tot.n_requests;
+  summary->n_blocks = tot.n_blocks;
+  summary->n_tokens = tot.n_tokens;
+  summary->error_index = tot.error_index;
+  summary->status = tot.error_index == ~0ull ? MPSF_OK : MPSF_E_BAD_ENTRY;
+  return summary->status;
 }
 
 }  // extern "C"

@@ -56,4 +56,14 @@ int launch_remap(uint64_t va_base, const uint64_t* phys, uint64_t npages4k, uint
 int launch_remap_blocks(uint64_t va_base, const uint64_t* phys, uint64_t npages4k,
                         const uint32_t* blocks, uint64_t nblocks, mpsf_remap_entry* out,
                         uint32_t* err_flag, cudaStream_t st);
+// snapshot delta fold (StandbyInstance.fold over a batch of snapshots); synchronous on st
+struct FoldTotals {
+  uint64_t n_requests, n_blocks, n_tokens, error_index;
+};
+size_t fold_scratch_bytes(uint64_t S, uint64_t R);
+int launch_fold(uint8_t* scratch, size_t scratch_bytes, uint32_t S, uint32_t R, const uint32_t* req,
+                const uint32_t* nblk, const uint32_t* ntok, const uint32_t* progress, const uint8_t* done,
+                const uint32_t* blocks, const uint32_t* tokens, uint32_t* order, uint64_t* blk_off,
+                uint32_t* blocks_out, uint64_t* tok_off, uint32_t* tokens_out, uint32_t* prog_out,
+                uint8_t* done_out, FoldTotals* tot, cudaStream_t st);
 }  // namespace mpsf

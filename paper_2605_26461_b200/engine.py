@@ -300,6 +300,74 @@ class FaultEngine:
                                                C.c_void_p(stream.cuda_stream)))
         return d_out[:16 * len(blocks)].cpu().numpy().view(REMAP_DTYPE)
 
+    # -- snapshot delta fold (StandbyInstance.fold, recovery.py:83-92) -------------------------
+    def fold_device(self, n_snap: int, n_req_ids: int, d_req, d_nblk, d_ntok, d_progress, d_done, d_blocks,
+                    d_tokens, out: dict, stream=None) -> _lib.FoldSummary:
+        """``mpsf_fold`` on device tensors; ``out`` holds ``alloc_fold_outputs`` tensors."""
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        s = _lib.FoldSummary()
+        rc = self.lib.mpsf_fold(self.ctx, n_snap, n_req_ids, d_req.data_ptr(), d_nblk.data_ptr(),
+                                d_ntok.data_ptr(), d_progress.data_ptr(), d_done.data_ptr(), d_blocks.data_ptr(),
+                                d_tokens.data_ptr(), out["order"].data_ptr(), out["blk_off"].data_ptr(),
+                                out["blocks"].data_ptr(), out["tok_off"].data_ptr(), out["tokens"].data_ptr(),
+                                out["progress"].data_ptr(), out["done"].data_ptr(), C.byref(s),
+                                C.c_void_p(stream.cuda_stream))
+        if rc:
+            raise_for(rc, self.lib.mpsf_strerror(rc).decode(), int(s.error_index))
+        return s
+
+    def fold(self, req, seq, nblk, ntok, progress, done, blocks, tokens, n_req_ids: int | None = None) -> "Folded":
+        """Host form: the fold of ``len(req)`` consumed snapshots (SoA, consume order; request id
+        0xFFFFFFFF = liveness-only).  Returns :class:`Folded` (requests in first-appearance
+        order, CSR deltas, last progress, sticky done, last consumed seq)."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        req = np.ascontiguousarray(req, dtype=np.uint32)
+        S = len(req)
+        if n_req_ids is None:
+            live = req[req != 0xFFFFFFFF]
+            n_req_ids = int(live.max()) + 1 if len(live) else 1
+
+        def up(a, dt):
+            a = np.ascontiguousarray(a, dtype=dt)
+            return torch.from_numpy(a.view(np.uint8).copy() if len(a) else np.zeros(4, np.uint8)).to(dev)
+        d = [up(req, np.uint32), up(nblk, np.uint32), up(ntok, np.uint32), up(progress, np.uint32),
+             up(done, np.uint8), up(blocks, np.uint32), up(tokens, np.uint32)]
+        out = alloc_fold_outputs(S, len(blocks), len(tokens), self.device)
+        s = self.fold_device(S, n_req_ids, *d, out)
+        r, nb, nt = int(s.n_requests), int(s.n_blocks), int(s.n_tokens)
+        u32 = lambda t, k: t[:4 * k].cpu().numpy().view(np.uint32)  # noqa: E731
+        u64 = lambda t, k: t[:8 * k].cpu().numpy().view(np.uint64)  # noqa: E731
+        return Folded(order=u32(out["order"], r), blk_off=u64(out["blk_off"], r + 1) if r else np.zeros(1, np.uint64),
+                      blocks=u32(out["blocks"], nb), tok_off=u64(out["tok_off"], r + 1) if r else np.zeros(1, np.uint64),
+                      tokens=u32(out["tokens"], nt), progress=u32(out["progress"], r),
+                      done=out["done"][:r].cpu().numpy().copy(), last_seq=int(seq[-1]) if S else 0)
+
+
+@dataclass
+class Folded:
+    """Result of :meth:`FaultEngine.fold` -- ``StandbyInstance`` state after ``fold``: the
+    ``folded`` dict as CSR (rows in insertion order) plus ``last_consumed_seq``."""
+    order: np.ndarray
+    blk_off: np.ndarray
+    blocks: np.ndarray
+    tok_off: np.ndarray
+    tokens: np.ndarray
+    progress: np.ndarray
+    done: np.ndarray
+    last_seq: int
+
+
+def alloc_fold_outputs(n_snap: int, n_blocks: int, n_tokens: int, device: int = 0) -> dict:
+    """Device output tensors (raw bytes) for ``FaultEngine.fold_device``."""
+    import torch
+    dev = torch.device("cuda", device)
+    b = lambda n: torch.empty(max(n, 8), dtype=torch.uint8, device=dev)  # noqa: E731
+    return dict(order=b(4 * n_snap), blk_off=b(8 * (n_snap + 1)), blocks=b(4 * n_blocks),
+                tok_off=b(8 * (n_snap + 1)), tokens=b(4 * n_tokens), progress=b(4 * n_snap), done=b(n_snap))
+
 
 def alloc_host_outputs(n: int, n_clients: int, pinned: bool = False) -> dict:
     """Host result buffers for ``FaultEngine.process`` (optionally page-locked)."""

@@ -57,3 +57,19 @@ def test_fold_oracle_matches_standby_fold(seed):
             assert got.tokens[t0:t1].tolist() == f.tokens
             assert int(got.progress[k]) == f.progress and bool(got.done[k]) == f.done
         assert got.last_seq == st.last_consumed_seq
+
+
+def _same(a, b):
+    for f in ("order", "blk_off", "blocks", "tok_off", "tokens", "progress", "done"):
+        x, y = getattr(a, f), getattr(b, f)
+        assert x.dtype == y.dtype and np.array_equal(x, y), f
+    assert a.last_seq == b.last_seq
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_fold_np_matches_loop(seed):
+    rnd = random.Random(900 + seed)
+    for it in range(30):
+        snaps = random_snapshots(rnd, rnd.randint(1, 40), rnd.randint(0, 300))
+        a = to_arrays(snaps)
+        _same(so.fold_snapshots_np(*a), so.fold_snapshots(*a))

@@ -1,0 +1,103 @@
+"""Snapshot delta fold on the GPU (mpsf_fold) against the oracle's
+``fold_snapshots`` (pinned against the reference ``StandbyInstance.fold`` in
+tests/test_fold_oracle.py), and the fold chained into the live-KV remap
+(``complete_wake``, recovery.py:310-363).  Bit-exact."""
+
+import numpy as np
+import pytest
+
+from paper_2605_26461_b200.engine import FaultEngine
+from paper_2605_26461_b200.errors import EntryError
+
+from oracle import seq_oracle as so
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def eng():
+    e = FaultEngine(0)
+    yield e
+    e.close()
+
+
+def snapshots(rng, n_req, n_snap, max_blk=4, max_tok=8, liveness=0.1):
+    req = rng.integers(0, n_req, n_snap, dtype=np.uint32)
+    req[rng.random(n_snap) < liveness] = so.NO_REQ
+    seq = np.arange(1, n_snap + 1, dtype=np.uint64) * 3
+    nblk = rng.integers(0, max_blk + 1, n_snap, dtype=np.uint32)
+    ntok = rng.integers(0, max_tok + 1, n_snap, dtype=np.uint32)
+    prog = rng.integers(0, 1 << 20, n_snap, dtype=np.uint32)
+    done = (rng.random(n_snap) < 0.05).astype(np.uint8)
+    blocks = rng.integers(0, 1 << 24, int(nblk.sum()), dtype=np.uint32)
+    tokens = rng.integers(0, 50000, int(ntok.sum()), dtype=np.uint32)
+    return req, seq, nblk, ntok, prog, done, blocks, tokens
+
+
+def check(got, want):
+    assert np.array_equal(got.order, want.order)
+    assert np.array_equal(got.blk_off, want.blk_off)
+    assert np.array_equal(got.blocks, want.blocks)
+    assert np.array_equal(got.tok_off, want.tok_off)
+    assert np.array_equal(got.tokens, want.tokens)
+    assert np.array_equal(got.progress, want.progress)
+    assert np.array_equal(got.done, want.done)
+    assert got.last_seq == want.last_seq
+
+
+@pytest.mark.parametrize("n_req,n_snap", [(1, 1), (1, 50), (7, 300), (200, 5000), (5000, 20000),
+                                          (100_000, 200_000)])
+def test_fold_vs_oracle(eng, n_req, n_snap):
+    rng = np.random.default_rng(n_req * 7 + n_snap)
+    a = snapshots(rng, n_req, n_snap)
+    check(eng.fold(*a, n_req_ids=n_req), so.fold_snapshots(*a))
+
+
+def test_fold_edge_cases(eng):
+    rng = np.random.default_rng(5)
+    # empty
+    a = snapshots(rng, 3, 0)
+    check(eng.fold(*a), so.fold_snapshots(*a))
+    # liveness only: nothing folded, seq still advances
+    a = snapshots(rng, 3, 40, liveness=1.0)
+    check(eng.fold(*a, n_req_ids=3), so.fold_snapshots(*a))
+    # empty deltas everywhere
+    a = snapshots(rng, 9, 500, max_blk=0, max_tok=0)
+    check(eng.fold(*a, n_req_ids=9), so.fold_snapshots(*a))
+    # one request with long deltas (warp copy loops > 32)
+    a = snapshots(rng, 1, 64, max_blk=300, max_tok=1000)
+    check(eng.fold(*a, n_req_ids=1), so.fold_snapshots(*a))
+    # sparse ids: a large id space, few requests
+    a = list(snapshots(rng, 5, 1000))
+    ids = np.array([3, 77, 1 << 20, 9, 123456], np.uint32)
+    live = a[0] != so.NO_REQ
+    a[0] = a[0].copy()
+    a[0][live] = ids[a[0][live]]
+    check(eng.fold(*a, n_req_ids=(1 << 20) + 1), so.fold_snapshots(*a))
+
+
+def test_fold_bad_request_id(eng):
+    rng = np.random.default_rng(9)
+    a = list(snapshots(rng, 10, 100, liveness=0.0))
+    a[0] = a[0].copy()
+    a[0][37] = 10
+    a[0][80] = 11
+    with pytest.raises(EntryError) as ei:
+        eng.fold(*a, n_req_ids=10)
+    assert ei.value.index == 37
+
+
+def test_fold_then_remap_blocks(eng):
+    """complete_wake: the folded block table of every live request remapped onto the
+    standby's physical pages -- the fold output feeds mpsf_remap_blocks directly."""
+    rng = np.random.default_rng(11)
+    npages = 1 << 16
+    phys = rng.integers(1, 1 << 40, npages, dtype=np.uint64)
+    a = list(snapshots(rng, 300, 4000))
+    a[6] = rng.integers(0, npages, len(a[6]), dtype=np.uint32)
+    got = eng.fold(*a, n_req_ids=300)
+    want = so.fold_snapshots(*a)
+    check(got, want)
+    va = 0x7F00_0000_0000
+    t = eng.remap_blocks(va, phys, got.blocks)
+    assert np.array_equal(t, so.remap_blocks(va, phys, want.blocks))
