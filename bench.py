@@ -430,7 +430,7 @@ def bench_fold(args, eng, hbm_peak, flush):
     d = [up(req), up(nblk), up(ntok), up(prog), up(done), up(blocks), up(tokens)]
     out = alloc_fold_outputs(S, len(blocks), len(tokens))
     for _ in range(3):
-        s = eng.fold_device(S, R, *d, out)
+        s = eng.fold_device(S, R, *d[:6], len(blocks), d[6], len(tokens), out)
     want = fold_snapshots_np(req, seq, nblk, ntok, prog, done, blocks, tokens)
     r, nb, nt = int(s.n_requests), int(s.n_blocks), int(s.n_tokens)
     exact = (r == len(want.order) and
@@ -447,7 +447,7 @@ def bench_fold(args, eng, hbm_peak, flush):
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record()
-        eng.fold_device(S, R, *d, out)     # includes the summary read (a stream sync)
+        eng.fold_device(S, R, *d[:6], len(blocks), d[6], len(tokens), out)     # includes the summary read (a stream sync)
         b.record()
         b.synchronize()
         tot += a.elapsed_time(b)

@@ -200,7 +200,8 @@ int mpsf_get_translate_summary(mpsf_ctx* ctx, mpsf_translate_summary* out);
  * fold dict's insertion order): d_order[k] its id, the CSR offsets d_blk_off[k..k+1] /
  * d_tok_off[k..k+1] into d_blocks_out / d_tokens_out (the deltas appended in consume order),
  * d_progress_out[k] (the last snapshot's), d_done_out[k] (sticky OR).  Capacities: n_snap
- * for the per-request arrays, n_snap+1 for the offsets, the input totals for the payloads.
+ * for the per-request arrays, n_snap+1 for the offsets, n_blocks / n_tokens (the payload
+ * lengths, each < 2^32) for the payloads.  Deltas reaching past the payloads: MPSF_E_ARG.
  * last_consumed_seq is the last snapshot's seq (the caller holds it).  A request id >= n_req_ids
  * returns MPSF_E_BAD_ENTRY with the first such snapshot in error_index (its snapshot is not
  * folded).  Synchronous on `stream` (the summary needs the counts). */
@@ -214,8 +215,8 @@ typedef struct {
 } mpsf_fold_summary;
 int mpsf_fold(mpsf_ctx* ctx, uint64_t n_snap, uint32_t n_req_ids, const uint32_t* d_req,
               const uint32_t* d_nblk, const uint32_t* d_ntok, const uint32_t* d_progress,
-              const uint8_t* d_done, const uint32_t* d_blocks, const uint32_t* d_tokens,
-              uint32_t* d_order, uint64_t* d_blk_off, uint32_t* d_blocks_out, uint64_t* d_tok_off,
+              const uint8_t* d_done, const uint32_t* d_blocks, uint64_t n_blocks,
+              const uint32_t* d_tokens, uint64_t n_tokens, uint32_t* d_order, uint64_t* d_blk_off, uint32_t* d_blocks_out, uint64_t* d_tok_off,
               uint32_t* d_tokens_out, uint32_t* d_progress_out, uint8_t* d_done_out,
               mpsf_fold_summary* summary, void* stream);
 

@@ -1100,11 +1100,12 @@ int mpsf_remap_blocks(mpsf_ctx* c, uint64_t va_base, const uint64_t* d_phys, uin
 
 int mpsf_fold(mpsf_ctx* c, uint64_t n_snap, uint32_t n_req_ids, const uint32_t* d_req, const uint32_t* d_nblk,
               const uint32_t* d_ntok, const uint32_t* d_progress, const uint8_t* d_done, const uint32_t* d_blocks,
-              const uint32_t* d_tokens, uint32_t* d_order, uint64_t* d_blk_off, uint32_t* d_blocks_out,
+              uint64_t n_blocks, const uint32_t* d_tokens, uint64_t n_tokens, uint32_t* d_order, uint64_t* d_blk_off, uint32_t* d_blocks_out,
               uint64_t* d_tok_off, uint32_t* d_tokens_out, uint32_t* d_progress_out, uint8_t* d_done_out,
               mpsf_fold_summary* summary, void* stream) {
   if (!c || !summary) return MPSF_E_ARG;
-  if (n_snap >= (1ull << 31) - 1) return MPSF_E_TOO_LARGE;
+  if (n_snap >= (1ull << 31) - 1 || n_blocks >= (1ull << 32) || n_tokens >= (1ull << 32)) return MPSF_E_TOO_LARGE;
+  if ((n_blocks && (!d_blocks || !d_blocks_out)) || (n_tokens && (!d_tokens || !d_tokens_out))) return MPSF_E_ARG;
   if (n_snap && (!d_req || !d_nblk || !d_ntok || !d_progress || !d_done || !d_order || !d_blk_off ||
                  !d_tok_off || !d_progress_out || !d_done_out))
     return MPSF_E_ARG;
@@ -1125,16 +1126,16 @@ int mpsf_fold(mpsf_ctx* c, uint64_t n_snap, uint32_t n_req_ids, const uint32_t* 
   FoldTotals tot{};
   c->mark_begin(st);
   if (launch_fold(c->d_fold, c->fold_cap, (uint32_t)n_snap, n_req_ids ? n_req_ids : 1, d_req, d_nblk, d_ntok,
-                  d_progress, d_done, d_blocks, d_tokens, d_order, d_blk_off, d_blocks_out, d_tok_off, d_tokens_out,
+                  d_progress, d_done, d_blocks, n_blocks, d_tokens, n_tokens, d_order, d_blk_off, d_blocks_out, d_tok_off, d_tokens_out,
                   d_progress_out, d_done_out, &tot, st))
     return MPSF_E_CUDA;
   c->marker().mark("k_fold");
-  c->last_launches = 7;   // own kernels; the CUB scans and the radix sort add theirs
+  c->last_launches = 4;   // own kernels; the CUB scans and the radix sort add theirs
   summary->n_requests = tot.n_requests;
   summary->n_blocks = tot.n_blocks;
   summary->n_tokens = tot.n_tokens;
   summary->error_index = tot.error_index;
-  summary->status = tot.error_index == ~0ull ? MPSF_OK : MPSF_E_BAD_ENTRY;
+  summary->status = tot.error_index != ~0ull ? MPSF_E_BAD_ENTRY : tot.overrun ? MPSF_E_ARG : MPSF_OK;
   return summary->status;
 }
 

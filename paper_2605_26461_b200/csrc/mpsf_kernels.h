@@ -59,11 +59,12 @@ int launch_remap_blocks(uint64_t va_base, const uint64_t* phys, uint64_t npages4
 // snapshot delta fold (StandbyInstance.fold over a batch of snapshots); synchronous on st
 struct FoldTotals {
   uint64_t n_requests, n_blocks, n_tokens, error_index;
+  uint32_t overrun;   // the delta lengths reach past the payload arrays
 };
 size_t fold_scratch_bytes(uint64_t S, uint64_t R);
 int launch_fold(uint8_t* scratch, size_t scratch_bytes, uint32_t S, uint32_t R, const uint32_t* req,
                 const uint32_t* nblk, const uint32_t* ntok, const uint32_t* progress, const uint8_t* done,
-                const uint32_t* blocks, const uint32_t* tokens, uint32_t* order, uint64_t* blk_off,
-                uint32_t* blocks_out, uint64_t* tok_off, uint32_t* tokens_out, uint32_t* prog_out,
-                uint8_t* done_out, FoldTotals* tot, cudaStream_t st);
+                const uint32_t* blocks, uint64_t n_blocks_in, const uint32_t* tokens, uint64_t n_tokens_in,
+                uint32_t* order, uint64_t* blk_off, uint32_t* blocks_out, uint64_t* tok_off, uint32_t* tokens_out,
+                uint32_t* prog_out, uint8_t* done_out, FoldTotals* tot, cudaStream_t st);
 }  // namespace mpsf

@@ -302,7 +302,7 @@ class FaultEngine:
 
     # -- snapshot delta fold (StandbyInstance.fold, recovery.py:83-92) -------------------------
     def fold_device(self, n_snap: int, n_req_ids: int, d_req, d_nblk, d_ntok, d_progress, d_done, d_blocks,
-                    d_tokens, out: dict, stream=None) -> _lib.FoldSummary:
+                    n_blocks: int, d_tokens, n_tokens: int, out: dict, stream=None) -> _lib.FoldSummary:
         """``mpsf_fold`` on device tensors; ``out`` holds ``alloc_fold_outputs`` tensors."""
         import torch
         if stream is None:
@@ -310,7 +310,7 @@ class FaultEngine:
         s = _lib.FoldSummary()
         rc = self.lib.mpsf_fold(self.ctx, n_snap, n_req_ids, d_req.data_ptr(), d_nblk.data_ptr(),
                                 d_ntok.data_ptr(), d_progress.data_ptr(), d_done.data_ptr(), d_blocks.data_ptr(),
-                                d_tokens.data_ptr(), out["order"].data_ptr(), out["blk_off"].data_ptr(),
+                                n_blocks, d_tokens.data_ptr(), n_tokens, out["order"].data_ptr(), out["blk_off"].data_ptr(),
                                 out["blocks"].data_ptr(), out["tok_off"].data_ptr(), out["tokens"].data_ptr(),
                                 out["progress"].data_ptr(), out["done"].data_ptr(), C.byref(s),
                                 C.c_void_p(stream.cuda_stream))
@@ -336,7 +336,7 @@ class FaultEngine:
         d = [up(req, np.uint32), up(nblk, np.uint32), up(ntok, np.uint32), up(progress, np.uint32),
              up(done, np.uint8), up(blocks, np.uint32), up(tokens, np.uint32)]
         out = alloc_fold_outputs(S, len(blocks), len(tokens), self.device)
-        s = self.fold_device(S, n_req_ids, *d, out)
+        s = self.fold_device(S, n_req_ids, *d[:6], len(blocks), d[6], len(tokens), out)
         r, nb, nt = int(s.n_requests), int(s.n_blocks), int(s.n_tokens)
         u32 = lambda t, k: t[:4 * k].cpu().numpy().view(np.uint32)  # noqa: E731
         u64 = lambda t, k: t[:8 * k].cpu().numpy().view(np.uint64)  # noqa: E731

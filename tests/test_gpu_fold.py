@@ -101,3 +101,14 @@ def test_fold_then_remap_blocks(eng):
     va = 0x7F00_0000_0000
     t = eng.remap_blocks(va, phys, got.blocks)
     assert np.array_equal(t, so.remap_blocks(va, phys, want.blocks))
+
+
+def test_fold_delta_overrun_rejected(eng):
+    """Delta lengths that reach past the payload arrays are an argument error, not a read past
+    the buffer."""
+    from paper_2605_26461_b200.errors import SimError
+    rng = np.random.default_rng(13)
+    a = list(snapshots(rng, 4, 50, liveness=0.0))
+    a[6] = a[6][:-3]                      # three block ids short
+    with pytest.raises(SimError):
+        eng.fold(*a, n_req_ids=4)
