@@ -332,6 +332,17 @@ def run_mine(args):
         dist.destroy_process_group()
 
 
+def rewarm(fn, ms=200.0):
+    """Run ``fn`` back to back for ~``ms`` of wall time right before a timed loop: the extras run
+    after seconds of CPU-side oracle checks, and an idle GPU's clocks take that long to ramp."""
+    import time
+    import torch
+    t0 = time.perf_counter()
+    while (time.perf_counter() - t0) * 1e3 < ms:
+        fn()
+        torch.cuda.synchronize()
+
+
 def bench_storm(args, eng, hbm_peak, flush):
     import torch
     from paper_2605_26461_b200 import synth
@@ -387,7 +398,8 @@ def bench_translate(args, eng, hbm_peak, flush, w):
     exact = (np.array_equal(d_hit.cpu().numpy(), want.hit) and
              np.array_equal(d_fi[:4 * nm].cpu().numpy().view(np.uint32), want.fault_idx) and
              np.array_equal(d_pi[:4 * npop].cpu().numpy().view(np.uint32), want.pop_idx))
-    steps = max(5, min(args.steps, 20))
+    steps = max(20, min(args.steps, 50))
+    rewarm(lambda: eng.translate_device(d_acc, n, d_hit, d_f, d_fi, d_pi))
     tot = 0.0
     for _ in range(steps):
         flush.zero_()
@@ -440,7 +452,8 @@ def bench_fold(args, eng, hbm_peak, flush):
              np.array_equal(out["tokens"][:4 * nt].cpu().numpy().view(np.uint32), want.tokens) and
              np.array_equal(out["progress"][:4 * r].cpu().numpy().view(np.uint32), want.progress) and
              np.array_equal(out["done"][:r].cpu().numpy(), want.done))
-    steps = max(5, min(args.steps, 20))
+    steps = max(20, min(args.steps, 50))
+    rewarm(lambda: eng.fold_device(S, R, *d[:6], len(blocks), d[6], len(tokens), out))
     tot = 0.0
     for _ in range(steps):
         flush.zero_()
@@ -476,8 +489,9 @@ def bench_remap(args, eng, hbm_peak, flush):
         for _ in range(3):
             eng.remap_device(0x7F00_0000_0000, phys, npages, gran, d_out)
         torch.cuda.synchronize()
+        steps = max(20, min(args.steps, 50))
+        rewarm(lambda: eng.remap_device(0x7F00_0000_0000, phys, npages, gran, d_out))
         eng.set_profiling(True)
-        steps = max(5, min(args.steps, 50))
         tot = 0.0
         for _ in range(steps):
             flush.zero_()

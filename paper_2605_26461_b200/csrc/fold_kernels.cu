@@ -8,22 +8,24 @@
 // Batch form: S snapshots in consume order as SoA (request id or NO_REQ, delta lengths,
 // progress, done) plus the concatenated deltas.  The fold is a stable group-by with
 // variable-length payloads:
-//   k_fold_stats   per request id: first snapshot (atomicMin), sticky done (atomicOr)
-//   head scan      a snapshot is its request's head iff it is the request's first; the heads'
-//                  exclusive scan (fed by an iterator, nothing materialised) ranks the
-//                  requests in first-appearance order -> k_fold_rank, k_fold_keys
-//   sort           snapshot indices by request rank, stable (CUB onesweep radix sort, only
-//                  the bits min(R, S) needs; liveness-only snapshots sort last)
-//   offset scans   one u64 scan packs (blocks | tokens << 32): source offsets in consume
-//                  order, destination offsets in sorted order
-//   k_fold_copy    thread per sorted snapshot: its deltas to their destination; group starts
-//                  write the request's order / CSR offsets, group ends its progress / done,
-//                  the last live position the totals
+//   k_fold_stats   per request id: first / last snapshot (atomicMin/Max), sticky done (atomicOr)
+//   head scan      heads (a request's first snapshot) counted in consume order, fed by an
+//                  iterator: ranks the requests in first-appearance order
+//   k_fold_rank    per head: rank, order, last progress, done, request count
+//   src scan       (blocks | tokens << 32) in consume order: each snapshot's source offsets
+//   sort           snapshot indices by request rank, stable (CUB onesweep radix sort over
+//                  only the bits min(R, S) needs; liveness-only snapshots sort last)
+//   dst scan       packed lengths in sorted order, scattered back to consume order through a
+//                  permutation output iterator: each snapshot's destination offsets
+//   k_fold_copy    thread per snapshot in consume order (coalesced reads of the SoA, the
+//                  offsets and the payload): its deltas to their destination; heads write
+//                  their request's CSR start, the last live snapshot in fold order the ends
 // CUB supplies the scans and the radix sort (library primitives, like cuBLAS for a GEMM).
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/permutation_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
 
 #include "mpsf_kernels.h"
@@ -38,9 +40,13 @@ struct FoldDev {            // device-side totals, read back once
   uint32_t overrun;         // deltas reach past the payload arrays
 };
 
+__device__ __forceinline__ unsigned long long pack_len(uint32_t nb, uint32_t nt) {
+  return (unsigned long long)nb | ((unsigned long long)nt << 32);
+}
+
 __global__ void k_fold_stats(uint32_t S, uint32_t R, const uint32_t* __restrict__ req,
                              const uint8_t* __restrict__ done, uint32_t* __restrict__ first,
-                             uint32_t* __restrict__ rdone, FoldDev* __restrict__ dev) {
+                             uint32_t* __restrict__ last, uint32_t* __restrict__ rdone, FoldDev* __restrict__ dev) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= S) return;
   const uint32_t r = req[i];
@@ -50,6 +56,7 @@ __global__ void k_fold_stats(uint32_t S, uint32_t R, const uint32_t* __restrict_
     return;
   }
   atomicMin(first + r, i);
+  atomicMax(last + r, i);
   if (done[i]) atomicOr(rdone + r, 1u);
 }
 
@@ -63,15 +70,13 @@ struct HeadFlag {           // snapshot i is its request's first
   }
 };
 
-struct PackLen {            // (blocks | tokens << 32) of snapshot i, consume order
+struct PackLen {            // packed lengths of snapshot i, consume order (every snapshot)
   const uint32_t* nblk;
   const uint32_t* ntok;
-  __device__ unsigned long long operator()(uint32_t i) const {
-    return (unsigned long long)nblk[i] | ((unsigned long long)ntok[i] << 32);
-  }
+  __device__ unsigned long long operator()(uint32_t i) const { return pack_len(nblk[i], ntok[i]); }
 };
 
-struct PackLenSorted {      // the same at sorted position p (liveness-only snapshots: 0)
+struct PackLenSorted {      // packed lengths at sorted position p (liveness-only snapshots: 0)
   const uint32_t* sidx;
   const uint32_t* skey;
   const uint32_t* nblk;
@@ -80,18 +85,29 @@ struct PackLenSorted {      // the same at sorted position p (liveness-only snap
   __device__ unsigned long long operator()(uint32_t p) const {
     if (skey[p] >= live_bound) return 0ull;
     const uint32_t i = sidx[p];
-    return (unsigned long long)nblk[i] | ((unsigned long long)ntok[i] << 32);
+    return pack_len(nblk[i], ntok[i]);
   }
 };
 
-// heads: rank[r] = head_pos[i]
+// heads: rank, the request's order entry, its last progress and sticky done; the count
 __global__ void k_fold_rank(uint32_t S, uint32_t R, const uint32_t* __restrict__ req,
-                            const uint32_t* __restrict__ first, const uint32_t* __restrict__ head_pos,
-                            uint32_t* __restrict__ rank) {
+                            const uint32_t* __restrict__ first, const uint32_t* __restrict__ last,
+                            const uint32_t* __restrict__ rdone, const uint32_t* __restrict__ progress,
+                            const uint32_t* __restrict__ head_pos, uint32_t* __restrict__ rank,
+                            uint32_t* __restrict__ order, uint32_t* __restrict__ prog_out,
+                            uint8_t* __restrict__ done_out, FoldDev* __restrict__ dev) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= S) return;
   const uint32_t r = req[i];
-  if (r < R && first[r] == i) rank[r] = head_pos[i];
+  const bool head = r < R && first[r] == i;
+  if (head) {
+    const uint32_t k = head_pos[i];
+    rank[r] = k;
+    order[k] = r;
+    prog_out[k] = progress[last[r]];
+    done_out[k] = rdone[r] ? 1 : 0;
+  }
+  if (i == S - 1) dev->n_requests = head_pos[i] + (head ? 1u : 0u);
 }
 
 // sort keys: the request's rank; liveness-only (and rejected) snapshots key past every rank
@@ -105,26 +121,23 @@ __global__ void k_fold_keys(uint32_t S, uint32_t R, uint32_t live_bound, const u
   idx[i] = i;
 }
 
-__global__ void k_fold_copy(uint32_t S, uint32_t live_bound, const uint32_t* __restrict__ sidx,
-                            const uint32_t* __restrict__ skey, const uint32_t* __restrict__ req,
+// thread per snapshot in consume order: coalesced reads of the SoA, offsets and payload
+__global__ void k_fold_copy(uint32_t S, uint32_t R, const uint32_t* __restrict__ req,
                             const uint32_t* __restrict__ nblk, const uint32_t* __restrict__ ntok,
-                            const uint32_t* __restrict__ progress, const uint32_t* __restrict__ rdone,
-                            const unsigned long long* __restrict__ src, const unsigned long long* __restrict__ dst,
-                            const uint32_t* __restrict__ blocks, const uint32_t* __restrict__ tokens,
-                            unsigned long long n_blocks_in, unsigned long long n_tokens_in,
-                            uint32_t* __restrict__ order, unsigned long long* __restrict__ blk_off,
+                            const uint32_t* __restrict__ first, const uint32_t* __restrict__ last,
+                            const uint32_t* __restrict__ rank, const unsigned long long* __restrict__ src,
+                            const unsigned long long* __restrict__ dst, const uint32_t* __restrict__ blocks,
+                            const uint32_t* __restrict__ tokens, unsigned long long n_blocks_in,
+                            unsigned long long n_tokens_in, unsigned long long* __restrict__ blk_off,
                             unsigned long long* __restrict__ tok_off, uint32_t* __restrict__ blocks_out,
-                            uint32_t* __restrict__ tokens_out, uint32_t* __restrict__ prog_out,
-                            uint8_t* __restrict__ done_out, FoldDev* __restrict__ dev) {
-  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= S) return;
-  const uint32_t k = skey[p];
-  if (k >= live_bound) return;
-  const uint32_t i = sidx[p];
-  const unsigned long long d = dst[p], s = src[i];
-  const uint32_t db = (uint32_t)d, dt = (uint32_t)(d >> 32), sb = (uint32_t)s, st = (uint32_t)(s >> 32);
-  const uint32_t nb = nblk[i], nt = ntok[i];
+                            uint32_t* __restrict__ tokens_out, FoldDev* __restrict__ dev) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= S) return;
   const uint32_t r = req[i];
+  if (r >= R) return;                        // liveness-only / rejected
+  const unsigned long long s = src[i], d = dst[i];
+  const uint32_t sb = (uint32_t)s, st = (uint32_t)(s >> 32), db = (uint32_t)d, dt = (uint32_t)(d >> 32);
+  const uint32_t nb = nblk[i], nt = ntok[i];
   if ((unsigned long long)sb + nb > n_blocks_in || (unsigned long long)st + nt > n_tokens_in ||
       (unsigned long long)db + nb > n_blocks_in || (unsigned long long)dt + nt > n_tokens_in) {
     atomicOr(&dev->overrun, 1u);
@@ -132,22 +145,19 @@ __global__ void k_fold_copy(uint32_t S, uint32_t live_bound, const uint32_t* __r
     for (uint32_t j = 0; j < nb; ++j) blocks_out[db + j] = blocks[sb + j];
     for (uint32_t j = 0; j < nt; ++j) tokens_out[dt + j] = tokens[st + j];
   }
-  if (p == 0 || skey[p - 1] != k) {          // group start: the request's row
-    order[k] = r;
-    blk_off[k] = db;
-    tok_off[k] = dt;
-  }
-  const bool last_live = p + 1 == S || skey[p + 1] >= live_bound;
-  if (last_live || skey[p + 1] != k) {       // group end: last progress, sticky done
-    prog_out[k] = progress[i];
-    done_out[k] = rdone[r] ? 1 : 0;
-  }
-  if (last_live) {                           // the CSR ends and the totals
-    blk_off[k + 1] = (unsigned long long)db + nb;
-    tok_off[k + 1] = (unsigned long long)dt + nt;
-    dev->n_requests = k + 1ull;
-    dev->n_blocks = (unsigned long long)db + nb;
-    dev->n_tokens = (unsigned long long)dt + nt;
+  const bool head = first[r] == i, tail = last[r] == i;
+  if (head || tail) {
+    const uint32_t k = rank[r];
+    if (head) {                              // the request's CSR start
+      blk_off[k] = db;
+      tok_off[k] = dt;
+    }
+    if (tail && k + 1ull == dev->n_requests) {   // the last live snapshot in fold order: the CSR ends
+      blk_off[k + 1] = (unsigned long long)db + nb;
+      tok_off[k + 1] = (unsigned long long)dt + nt;
+      dev->n_blocks = (unsigned long long)db + nb;
+      dev->n_tokens = (unsigned long long)dt + nt;
+    }
   }
 }
 
@@ -161,18 +171,19 @@ static int key_bits(uint32_t live_bound) {   // bits for keys in [0, live_bound]
 
 // scratch layout for S snapshots and R request ids
 size_t fold_scratch_bytes(uint64_t S, uint64_t R) {
-  size_t o = al256(sizeof(FoldDev)) + al256(4 * R) * 3;   // dev, first, rdone, rank
+  size_t o = al256(sizeof(FoldDev)) + al256(4 * R) * 4;   // dev, first, last, rdone, rank
   o += al256(4 * S) * 5;                                   // head_pos, key, idx, skey, sidx
   o += al256(8 * S) * 2;                                   // src, dst
   size_t cub_bytes = 0, t = 0;
   thrust::counting_iterator<uint32_t> c0(0);
+  cub::DeviceScan::ExclusiveSum(nullptr, t, thrust::make_transform_iterator(c0, HeadFlag{}), (uint32_t*)nullptr,
+                                (int)S);
+  cub_bytes = t > cub_bytes ? t : cub_bytes;
   cub::DeviceScan::ExclusiveSum(nullptr, t, thrust::make_transform_iterator(c0, PackLen{}),
                                 (unsigned long long*)nullptr, (int)S);
   cub_bytes = t > cub_bytes ? t : cub_bytes;
   cub::DeviceScan::ExclusiveSum(nullptr, t, thrust::make_transform_iterator(c0, PackLenSorted{}),
-                                (unsigned long long*)nullptr, (int)S);
-  cub_bytes = t > cub_bytes ? t : cub_bytes;
-  cub::DeviceScan::ExclusiveSum(nullptr, t, thrust::make_transform_iterator(c0, HeadFlag{}), (uint32_t*)nullptr,
+                                thrust::make_permutation_iterator((unsigned long long*)nullptr, (const uint32_t*)nullptr),
                                 (int)S);
   cub_bytes = t > cub_bytes ? t : cub_bytes;
   cub::DeviceRadixSort::SortPairs(nullptr, t, (const uint32_t*)nullptr, (uint32_t*)nullptr,
@@ -190,6 +201,7 @@ int launch_fold(uint8_t* scratch, size_t scratch_bytes, uint32_t S, uint32_t R, 
   auto take = [&](size_t bytes) { uint8_t* r = p; p += al256(bytes); return r; };
   FoldDev* dev = reinterpret_cast<FoldDev*>(take(sizeof(FoldDev)));
   uint32_t* first = reinterpret_cast<uint32_t*>(take(4ull * R));
+  uint32_t* last = reinterpret_cast<uint32_t*>(take(4ull * R));
   uint32_t* rdone = reinterpret_cast<uint32_t*>(take(4ull * R));
   uint32_t* rank = reinterpret_cast<uint32_t*>(take(4ull * R));
   uint32_t* head_pos = reinterpret_cast<uint32_t*>(take(4ull * S));
@@ -203,19 +215,19 @@ int launch_fold(uint8_t* scratch, size_t scratch_bytes, uint32_t S, uint32_t R, 
   const size_t cub_bytes = scratch_bytes - (size_t)(p - scratch);
   const uint32_t live_bound = R < S ? R : S;   // ranks < min(R, S)
   const FoldDev init{0, 0, 0, NO_REQ, 0};
-  // dev, first (0xFF..), rdone (0) are contiguous: two memsets and one small copy
   if (cudaMemcpyAsync(dev, &init, sizeof(init), cudaMemcpyHostToDevice, st) != cudaSuccess ||
       cudaMemsetAsync(first, 0xFF, 4ull * R, st) != cudaSuccess ||
-      cudaMemsetAsync(rdone, 0, 4ull * R, st) != cudaSuccess)
+      cudaMemsetAsync(last, 0, 4ull * R, st) != cudaSuccess || cudaMemsetAsync(rdone, 0, 4ull * R, st) != cudaSuccess)
     return -1;
   const uint32_t b = 256, g = (S + b - 1) / b;
-  k_fold_stats<<<g, b, 0, st>>>(S, R, req, done, first, rdone, dev);
+  k_fold_stats<<<g, b, 0, st>>>(S, R, req, done, first, last, rdone, dev);
   thrust::counting_iterator<uint32_t> c0(0);
   size_t t = cub_bytes;
   if (cub::DeviceScan::ExclusiveSum(cub_tmp, t, thrust::make_transform_iterator(c0, HeadFlag{req, first, R}),
                                     head_pos, (int)S, st) != cudaSuccess)
     return -1;
-  k_fold_rank<<<g, b, 0, st>>>(S, R, req, first, head_pos, rank);
+  k_fold_rank<<<g, b, 0, st>>>(S, R, req, first, last, rdone, progress, head_pos, rank, order, prog_out, done_out,
+                               dev);
   k_fold_keys<<<g, b, 0, st>>>(S, R, live_bound, req, rank, key, idx);
   t = cub_bytes;
   if (cub::DeviceRadixSort::SortPairs(cub_tmp, t, key, skey, idx, sidx, (int)S, 0, key_bits(live_bound), st) !=
@@ -227,14 +239,12 @@ int launch_fold(uint8_t* scratch, size_t scratch_bytes, uint32_t S, uint32_t R, 
     return -1;
   t = cub_bytes;
   if (cub::DeviceScan::ExclusiveSum(
-          cub_tmp, t, thrust::make_transform_iterator(c0, PackLenSorted{sidx, skey, nblk, ntok, live_bound}), dst,
-          (int)S, st) != cudaSuccess)
+          cub_tmp, t, thrust::make_transform_iterator(c0, PackLenSorted{sidx, skey, nblk, ntok, live_bound}),
+          thrust::make_permutation_iterator(dst, sidx), (int)S, st) != cudaSuccess)
     return -1;
-  k_fold_copy<<<g, b, 0, st>>>(S, live_bound, sidx, skey, req, nblk, ntok, progress, rdone, src, dst, blocks,
-                               tokens, n_blocks_in, n_tokens_in, order,
-                               reinterpret_cast<unsigned long long*>(blk_off),
-                               reinterpret_cast<unsigned long long*>(tok_off), blocks_out, tokens_out, prog_out,
-                               done_out, dev);
+  k_fold_copy<<<g, b, 0, st>>>(S, R, req, nblk, ntok, first, last, rank, src, dst, blocks, tokens, n_blocks_in,
+                               n_tokens_in, reinterpret_cast<unsigned long long*>(blk_off),
+                               reinterpret_cast<unsigned long long*>(tok_off), blocks_out, tokens_out, dev);
   FoldDev h{};
   if (cudaMemcpyAsync(&h, dev, sizeof(h), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
       cudaStreamSynchronize(st) != cudaSuccess)

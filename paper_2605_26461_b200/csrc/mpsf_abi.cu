@@ -1111,9 +1111,13 @@ int mpsf_fold(mpsf_ctx* c, uint64_t n_snap, uint32_t n_req_ids, const uint32_t* 
     return MPSF_E_ARG;
   *summary = mpsf_fold_summary{};
   summary->error_index = ~0ull;
-  if (!n_snap) return MPSF_OK;
   CK(cudaSetDevice(c->device));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (!n_snap) {   // nothing folded: the CSR is the single zero offset
+    if (d_blk_off) CK(cudaMemsetAsync(d_blk_off, 0, 8, st));
+    if (d_tok_off) CK(cudaMemsetAsync(d_tok_off, 0, 8, st));
+    return MPSF_OK;
+  }
   const size_t need = fold_scratch_bytes(n_snap, n_req_ids ? n_req_ids : 1);
   if (need > c->fold_cap) {
     CK(cudaStreamSynchronize(st));
