@@ -267,6 +267,7 @@ def run_mine(args):
             ts.append(time.perf_counter() - t0)
         t_e2e = max_over_ranks(ws, statistics.median(ts))
         e2e_mode = "one batch at a time (mpsf_process_host)"
+        t_single, t_pipe = t_e2e, None
         if ws == 1:
             # a stream of batches through the asynchronous form: two slots in flight, so the
             # H2D of batch k+1 overlaps the passes and the D2H of batch k
@@ -289,7 +290,9 @@ def run_mine(args):
         e2e = {"value": ws * n / t_e2e, "unit": "entries/s", "h2d_bytes_per_step": 16 * n,
                "d2h_bytes_per_step": d2h, "ms_per_step": round(t_e2e * 1e3, 3),
                "api": f"{e2e_mode}, pinned host buffers" if ws == 1 else
-                      "H2D + sharded phase API + NCCL exchanges + D2H"}
+                      "H2D + sharded phase API + NCCL exchanges + D2H",
+               "single_batch_ms": round(t_single * 1e3, 3),
+               "stream_ms_per_batch": None if t_pipe is None else round(t_pipe * 1e3, 3)}
 
     extra = {}
     if not args.no_storm and ws == 1:

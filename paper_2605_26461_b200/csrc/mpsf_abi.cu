@@ -1000,7 +1000,8 @@ int mpsf_submit_host(mpsf_ctx* c, int slot, const mpsf_fault_entry* h_in, uint64
   CK(cudaEventRecord(c->ev_fork, st));
   CK(cudaStreamWaitEvent(c->d2h_stream, c->ev_fork, 0));
   CK(cudaEventRecord(h.ev_done, c->d2h_stream));
-  CK(cudaStreamWaitEvent(st, h.ev_done, 0));       // the next batch's scratch use follows this one
+  // No compute-stream wait on this batch's D2H: the copies read only this slot's buffers, and
+  // the slot's next batch overwrites them only after its H2D, which waits for h.ev_done.
   h.busy = true;
   c->last_n = n;
   c->last_launches = launches + 1;
