@@ -220,6 +220,15 @@ int mpsf_fold(mpsf_ctx* ctx, uint64_t n_snap, uint32_t n_req_ids, const uint32_t
               uint32_t* d_tokens_out, uint32_t* d_progress_out, uint8_t* d_done_out,
               mpsf_fold_summary* summary, void* stream);
 
+/* ---- KV pool restore: BlockPool.reserve (workload.py:77-80) of folded block ids ----
+ * complete_wake reserves every folded request's blocks in the standby's pool
+ * (recovery.py:356-357).  d_reserved[total_blocks] = 1 for every id in d_block_ids[n] (ids >=
+ * total_blocks are not pool blocks and mark nothing) -- the valid mask of the live-KV remap;
+ * d_free[total_blocks] = the unreserved ids ascending (the pool heap's pop order), *n_free
+ * of them.  Synchronous on `stream`. */
+int mpsf_kv_reserve(mpsf_ctx* ctx, uint32_t total_blocks, const uint32_t* d_block_ids, uint64_t n,
+                    uint8_t* d_reserved, uint32_t* d_free, uint64_t* n_free, void* stream);
+
 /* Number of kernel launches the last mpsf_process / mpsf_remap enqueued. */
 int mpsf_last_launches(mpsf_ctx* ctx);
 

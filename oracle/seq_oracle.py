@@ -416,6 +416,15 @@ def remap_blocks(va_base: int, phys_pages, block_ids) -> np.ndarray:
     return out
 
 
+def kv_reserve(total_blocks: int, block_ids):
+    """``BlockPool(total).reserve(block_ids)`` (workload.py:77-80): the reserved mask over the
+    pool's ids and the free ids in pop order (the heap pops smallest first)."""
+    taken = set(int(b) for b in block_ids)
+    reserved = np.array([1 if b in taken else 0 for b in range(total_blocks)], np.uint8)
+    free = np.array([b for b in range(total_blocks) if b not in taken], np.uint32)
+    return reserved, free
+
+
 # -- batched translation (SURVEY.md §8(f) rank 2: the step before the fault path) ---------------
 
 @dataclass

@@ -87,6 +87,8 @@ SIGNATURES = {
                              C.c_void_p, C.c_void_p]),
     "mpsf_fold": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32] + [C.c_void_p] * 6 + [C.c_uint64, C.c_void_p]
                   + [C.c_uint64] + [C.c_void_p] * 7 + [C.POINTER(FoldSummary), C.c_void_p]),
+    "mpsf_kv_reserve": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p,
+                                  C.POINTER(C.c_uint64), C.c_void_p]),
     "mpsf_remap_blocks": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p,
                                     C.c_uint64, C.c_void_p, C.c_void_p]),
     "mpsf_last_launches": (C.c_int, [C.c_void_p]),

@@ -24,6 +24,8 @@
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <algorithm>
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/permutation_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
@@ -261,6 +263,53 @@ int launch_fold(uint8_t* scratch, size_t scratch_bytes, uint32_t S, uint32_t R, 
   tot->n_tokens = h.n_tokens;
   tot->error_index = h.err == NO_REQ ? ~0ull : h.err;
   tot->overrun = h.overrun;
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+// ---- KV pool restore: BlockPool.reserve (workload.py:77-80) of the folded block ids ----------
+// complete_wake reserves every folded request's block ids in the standby's pool
+// (recovery.py:356-357); the pool's free list is then the unreserved ids, popped smallest
+// first.  Output: the reserved mask (the remap's valid mask over KV pages) and the free ids
+// ascending (the heap's pop order).  Ids >= total are not pool blocks: they mark nothing.
+
+__global__ void k_kv_mark(const uint32_t* __restrict__ blocks, uint64_t nb, uint32_t total,
+                          uint8_t* __restrict__ reserved) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nb; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = __ldcs(blocks + j);
+    if (b < total) reserved[b] = 1;
+  }
+}
+
+struct IsFree {
+  const uint8_t* reserved;
+  __device__ bool operator()(uint32_t b) const { return reserved[b] == 0; }
+};
+
+size_t kv_reserve_scratch_bytes(uint32_t total) {
+  size_t t = 0;
+  thrust::counting_iterator<uint32_t> c0(0);
+  cub::DeviceSelect::If(nullptr, t, c0, (uint32_t*)nullptr, (unsigned long long*)nullptr, (int64_t)total, IsFree{});
+  return al256(8) + al256(t) + 256;
+}
+
+int launch_kv_reserve(uint8_t* scratch, size_t scratch_bytes, uint32_t total, const uint32_t* blocks, uint64_t nb,
+                      uint8_t* reserved, uint32_t* free_ids, uint64_t* n_free, cudaStream_t st) {
+  unsigned long long* d_nsel = reinterpret_cast<unsigned long long*>(scratch);
+  uint8_t* cub_tmp = scratch + al256(8);
+  size_t t = scratch_bytes - al256(8);
+  if (cudaMemsetAsync(reserved, 0, total, st) != cudaSuccess) return -1;
+  if (nb) {
+    const uint64_t g = std::min<uint64_t>((nb + 255) / 256, 148ull * 16);
+    k_kv_mark<<<(uint32_t)g, 256, 0, st>>>(blocks, nb, total, reserved);
+  }
+  thrust::counting_iterator<uint32_t> c0(0);
+  if (cub::DeviceSelect::If(cub_tmp, t, c0, free_ids, d_nsel, (int64_t)total, IsFree{reserved}, st) != cudaSuccess)
+    return -1;
+  unsigned long long h = 0;
+  if (cudaMemcpyAsync(&h, d_nsel, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return -1;
+  *n_free = h;
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

@@ -1144,4 +1144,28 @@ int mpsf_fold(mpsf_ctx* c, uint64_t n_snap, uint32_t n_req_ids, const uint32_t* 
   return summary->status;
 }
 
+int mpsf_kv_reserve(mpsf_ctx* c, uint32_t total_blocks, const uint32_t* d_block_ids, uint64_t n,
+                    uint8_t* d_reserved, uint32_t* d_free, uint64_t* n_free, void* stream) {
+  if (!c || !n_free || (n && !d_block_ids) || (total_blocks && (!d_reserved || !d_free))) return MPSF_E_ARG;
+  *n_free = 0;
+  if (!total_blocks) return MPSF_OK;
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t need = kv_reserve_scratch_bytes(total_blocks);
+  if (need > c->fold_cap) {
+    CK(cudaStreamSynchronize(st));
+    cudaFree(c->d_fold);
+    c->d_fold = nullptr;
+    c->fold_cap = 0;
+    CK(cudaMalloc(&c->d_fold, need));
+    c->fold_cap = need;
+  }
+  c->mark_begin(st);
+  if (launch_kv_reserve(c->d_fold, c->fold_cap, total_blocks, d_block_ids, n, d_reserved, d_free, n_free, st))
+    return MPSF_E_CUDA;
+  c->marker().mark("k_kv_reserve");
+  c->last_launches = n ? 1 : 0;   // own kernel; CUB's select adds its own
+  return MPSF_OK;
+}
+
 }  // extern "C"

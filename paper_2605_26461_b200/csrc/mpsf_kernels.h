@@ -67,4 +67,8 @@ int launch_fold(uint8_t* scratch, size_t scratch_bytes, uint32_t S, uint32_t R, 
                 const uint32_t* blocks, uint64_t n_blocks_in, const uint32_t* tokens, uint64_t n_tokens_in,
                 uint32_t* order, uint64_t* blk_off, uint32_t* blocks_out, uint64_t* tok_off, uint32_t* tokens_out,
                 uint32_t* prog_out, uint8_t* done_out, FoldTotals* tot, cudaStream_t st);
+// KV pool restore (BlockPool.reserve of folded block ids): reserved mask + free ids ascending
+size_t kv_reserve_scratch_bytes(uint32_t total);
+int launch_kv_reserve(uint8_t* scratch, size_t scratch_bytes, uint32_t total, const uint32_t* blocks, uint64_t nb,
+                      uint8_t* reserved, uint32_t* free_ids, uint64_t* n_free, cudaStream_t st);
 }  // namespace mpsf

@@ -345,6 +345,29 @@ class FaultEngine:
                       tokens=u32(out["tokens"], nt), progress=u32(out["progress"], r),
                       done=out["done"][:r].cpu().numpy().copy(), last_seq=int(seq[-1]) if S else 0)
 
+    def kv_reserve_device(self, total_blocks: int, d_blocks, n: int, d_reserved, d_free, stream=None) -> int:
+        """``mpsf_kv_reserve`` on device tensors; returns the number of free ids."""
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        nf = C.c_uint64(0)
+        self._check(self.lib.mpsf_kv_reserve(self.ctx, total_blocks, d_blocks.data_ptr() if n else None, n,
+                                             d_reserved.data_ptr(), d_free.data_ptr(), C.byref(nf),
+                                             C.c_void_p(stream.cuda_stream)))
+        return int(nf.value)
+
+    def kv_reserve(self, total_blocks: int, block_ids):
+        """``BlockPool(total_blocks).reserve(block_ids)``: (reserved mask u8[total], free ids
+        ascending -- the pool's pop order)."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        ids = np.ascontiguousarray(block_ids, dtype=np.uint32)
+        d_b = torch.from_numpy(ids.view(np.uint8).copy() if len(ids) else np.zeros(4, np.uint8)).to(dev)
+        d_r = torch.empty(max(total_blocks, 1), dtype=torch.uint8, device=dev)
+        d_f = torch.empty(max(4 * total_blocks, 4), dtype=torch.uint8, device=dev)
+        nf = self.kv_reserve_device(total_blocks, d_b, len(ids), d_r, d_f)
+        return d_r[:total_blocks].cpu().numpy(), d_f[:4 * nf].cpu().numpy().view(np.uint32)
+
 
 @dataclass
 class Folded:

@@ -73,3 +73,20 @@ def test_fold_np_matches_loop(seed):
         snaps = random_snapshots(rnd, rnd.randint(1, 40), rnd.randint(0, 300))
         a = to_arrays(snaps)
         _same(so.fold_snapshots_np(*a), so.fold_snapshots(*a))
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_kv_reserve_oracle_matches_block_pool(seed):
+    """``seq_oracle.kv_reserve`` against the reference ``BlockPool.reserve`` + pops."""
+    H.import_reference()
+    from mpssim.workload import BlockPool
+    rnd = random.Random(300 + seed)
+    for it in range(30):
+        total = rnd.randint(0, 300)
+        ids = [rnd.randrange(total + 20) for _ in range(rnd.randint(0, 2 * total + 1))]
+        pool = BlockPool(total)
+        pool.reserve(ids)
+        pops = [pool.allocate() for _ in range(pool.free_count)]
+        reserved, free = so.kv_reserve(total, ids)
+        assert free.tolist() == pops
+        assert reserved.tolist() == [1 if b in set(ids) else 0 for b in range(total)]

@@ -112,3 +112,33 @@ def test_fold_delta_overrun_rejected(eng):
     a[6] = a[6][:-3]                      # three block ids short
     with pytest.raises(SimError):
         eng.fold(*a, n_req_ids=4)
+
+
+@pytest.mark.parametrize("total,n", [(0, 0), (1, 0), (1, 1), (64, 10), (1000, 5000), (1 << 20, 300_000)])
+def test_kv_reserve_vs_oracle(eng, total, n):
+    rng = np.random.default_rng(total + n)
+    ids = rng.integers(0, total + 50, n, dtype=np.uint32) if n else np.zeros(0, np.uint32)
+    reserved, free = eng.kv_reserve(total, ids)
+    want_r, want_f = so.kv_reserve(total, ids) if total <= 5000 else _kv_reserve_np(total, ids)
+    assert np.array_equal(reserved, want_r)
+    assert np.array_equal(free, want_f)
+
+
+def _kv_reserve_np(total, ids):
+    r = np.zeros(total, np.uint8)
+    ids = ids[ids < total]
+    r[ids] = 1
+    return r, np.nonzero(r == 0)[0].astype(np.uint32)
+
+
+def test_fold_then_kv_reserve(eng):
+    """complete_wake: every folded request's blocks reserved in the standby's pool."""
+    rng = np.random.default_rng(17)
+    a = list(snapshots(rng, 50, 2000))
+    total = 4096
+    a[6] = rng.integers(0, total, len(a[6]), dtype=np.uint32)
+    got = eng.fold(*a, n_req_ids=50)
+    reserved, free = eng.kv_reserve(total, got.blocks)
+    want = so.fold_snapshots(*a)
+    want_r, want_f = so.kv_reserve(total, want.blocks)
+    assert np.array_equal(reserved, want_r) and np.array_equal(free, want_f)
