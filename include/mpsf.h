@@ -229,6 +229,32 @@ int mpsf_fold(mpsf_ctx* ctx, uint64_t n_snap, uint32_t n_req_ids, const uint32_t
 int mpsf_kv_reserve(mpsf_ctx* ctx, uint32_t total_blocks, const uint32_t* d_block_ids, uint64_t n,
                     uint8_t* d_reserved, uint32_t* d_free, uint64_t* n_free, void* stream);
 
+/* ---- Trace-line rendering of a processed batch (host only) ----
+ * Trace.render_record (kernel.py:127-132) lines for `n` entries and the OutRecords
+ * mpsf_process produced for them: MPSF_RENDER_TOP = the top half per entry in index (raise)
+ * order (fault_raised, shadow_copy; pipeline.py:113-143), MPSF_RENDER_DRAIN = the bottom half
+ * in drain order as the batch verdicts apply (bh_service, parse_fatal, tlb_invalidate,
+ * fatal_report, isolate_begin; pipeline.py:160-183, 224-230, 296-298).  SM traps and skipped
+ * entries render nothing.  Writes at most `cap` bytes of '\n'-terminated lines into buf and
+ * returns the total length (> cap, or buf NULL: nothing written, call again with that
+ * capacity), or a negative MPSF_E_* code.  Needs no device. */
+#define MPSF_RENDER_TOP 1u
+#define MPSF_RENDER_DRAIN 2u
+typedef struct {
+  uint64_t t_drain;                  /* world.clock.now at the drain                        */
+  const uint64_t* t_raise;           /* per-entry raise time (top half), NULL: t_drain       */
+  uint32_t m1_us, m2_us, m3_us;      /* SimParams mechanism latencies (isolate_begin)        */
+  uint32_t parts;                    /* MPSF_RENDER_TOP | MPSF_RENDER_DRAIN                  */
+  const char* const* channel_names;  /* reference channel ids ("c1.sm"), by channel index    */
+  uint32_t n_channels;
+  uint32_t n_clients;
+  const char* const* client_names;   /* reference pids ("c1"), by client index               */
+  uint32_t threads;                  /* host threads (0: all)                                */
+  uint32_t pad;
+} mpsf_render_params;
+int64_t mpsf_render_trace(const mpsf_fault_entry* entries, const mpsf_out_record* out, uint64_t n,
+                          const mpsf_render_params* params, char* buf, uint64_t cap);
+
 /* Number of kernel launches the last mpsf_process / mpsf_remap enqueued. */
 int mpsf_last_launches(mpsf_ctx* ctx);
 

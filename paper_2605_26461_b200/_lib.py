@@ -58,6 +58,13 @@ class FoldSummary(C.Structure):
                 ("n_blocks", C.c_uint64), ("n_tokens", C.c_uint64), ("error_index", C.c_uint64)]
 
 
+class RenderParams(C.Structure):
+    _fields_ = [("t_drain", C.c_uint64), ("t_raise", C.c_void_p), ("m1_us", C.c_uint32), ("m2_us", C.c_uint32),
+                ("m3_us", C.c_uint32), ("parts", C.c_uint32), ("channel_names", C.POINTER(C.c_char_p)),
+                ("n_channels", C.c_uint32), ("n_clients", C.c_uint32), ("client_names", C.POINTER(C.c_char_p)),
+                ("threads", C.c_uint32), ("pad", C.c_uint32)]
+
+
 class TranslateSummary(C.Structure):
     _fields_ = [("status", C.c_int32), ("pad", C.c_uint32), ("n_miss", C.c_uint64),
                 ("n_populated", C.c_uint64), ("error_index", C.c_uint64)]
@@ -89,6 +96,8 @@ SIGNATURES = {
                   + [C.c_uint64] + [C.c_void_p] * 7 + [C.POINTER(FoldSummary), C.c_void_p]),
     "mpsf_kv_reserve": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p,
                                   C.POINTER(C.c_uint64), C.c_void_p]),
+    "mpsf_render_trace": (C.c_int64, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(RenderParams), C.c_void_p,
+                                      C.c_uint64]),
     "mpsf_remap_blocks": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p,
                                     C.c_uint64, C.c_void_p, C.c_void_p]),
     "mpsf_last_launches": (C.c_int, [C.c_void_p]),

@@ -17,7 +17,8 @@ OUT = os.path.join(ROOT, "build", "ablate")
 def build(masks, extra=()):
     import glob
     os.makedirs(OUT, exist_ok=True)
-    srcs = sorted(glob.glob(os.path.join(ROOT, "paper_2605_26461_b200", "csrc", "*.cu")))
+    srcs = sorted(glob.glob(os.path.join(ROOT, "paper_2605_26461_b200", "csrc", "*.cu")) +
+                  glob.glob(os.path.join(ROOT, "paper_2605_26461_b200", "csrc", "*.cpp")))
     procs = []
     for m in masks:
         lib = os.path.join(OUT, f"libmpsf_{m}.so")
