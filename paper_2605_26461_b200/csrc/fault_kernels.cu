@@ -266,7 +266,7 @@ __device__ __forceinline__ void raise_err(const Scratch& S, uint32_t bit, uint64
 // range, engine not the channel's (KindMismatch, errors.py:36-37), VA beyond 2^53, unknown
 // entry kind.
 __device__ __forceinline__ Dec decode_fast(const Tables& T, const uint8_t* __restrict__ page_state,
-                                           const Scratch& S, uint4 e, uint64_t gidx, uint32_t lane) {
+                                           const Scratch& S, uint4 e, uint32_t gidx, uint32_t lane) {
   Dec d;
   d.va = (uint64_t)e.x | ((uint64_t)e.y << 32);
   const uint32_t w3 = e.w;
@@ -364,7 +364,7 @@ __device__ __forceinline__ uint32_t dd_slot(const World& W, const Rec& r) {
 // current one is processed, so a chunk's HBM latency hides behind the previous chunk's work.
 constexpr int WCHUNK = 64;
 
-__device__ __forceinline__ void ld_pair(const mpsf_fault_entry* in, uint64_t n, uint64_t i0, bool a32, uint4& a,
+__device__ __forceinline__ void ld_pair(const mpsf_fault_entry* in, uint32_t n, uint32_t i0, bool a32, uint4& a,
                                         uint4& b) {
   const uint4* p = reinterpret_cast<const uint4*>(in) + i0;
   if (a32 && i0 + 1 < n) {
@@ -378,17 +378,19 @@ __device__ __forceinline__ void ld_pair(const mpsf_fault_entry* in, uint64_t n, 
 }
 
 template <typename F>
-__device__ __forceinline__ void ldg_stream(const mpsf_fault_entry* in, uint64_t n, F&& fn) {
+__device__ __forceinline__ void ldg_stream(const mpsf_fault_entry* in, uint64_t n64, F&& fn) {
+  // batch indices stay below MAX_GIDX (2^29): chunk and entry indices are 32-bit
+  const uint32_t n = (uint32_t)n64;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp, GW = (uint64_t)gridDim.x * (blockDim.x >> 5);
-  const uint64_t nch = (n + WCHUNK - 1) / WCHUNK;
+  const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + warp, GW = gridDim.x * (blockDim.x >> 5);
+  const uint32_t nch = (n + WCHUNK - 1) / WCHUNK;
   const bool a32 = ((uintptr_t)in & 31u) == 0;
   uint4 na = make_uint4(0, 0, 0, 0), nb = na;
   if (gw < nch) ld_pair(in, n, gw * WCHUNK + 2 * lane, a32, na, nb);
-  for (uint64_t c = gw; c < nch; c += GW) {
+  for (uint32_t c = gw; c < nch; c += GW) {
     const uint4 e0 = na, e1 = nb;
     if (c + GW < nch) ld_pair(in, n, (c + GW) * WCHUNK + 2 * lane, a32, na, nb);
-    const uint64_t i0 = c * WCHUNK + 2 * lane;
+    const uint32_t i0 = c * WCHUNK + 2 * lane;
     fn(e0, i0, i0 < n, e1, i0 + 1, i0 + 1 < n);
   }
 }
@@ -407,21 +409,22 @@ __device__ __forceinline__ uint32_t scen_word(int sid, bool isolation) {
 // The pass-1 record stream: lane l of a warp-chunk reads records 2l, 2l+1 with one 16-byte
 // load, the next chunk's pair requested before the current one is processed.
 template <typename F>
-__device__ __forceinline__ void rec_stream(const unsigned long long* rec, uint64_t n, F&& fn) {
+__device__ __forceinline__ void rec_stream(const unsigned long long* rec, uint64_t n64, F&& fn) {
+  const uint32_t n = (uint32_t)n64;   // < MAX_GIDX
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp, GW = (uint64_t)gridDim.x * (blockDim.x >> 5);
-  const uint64_t nch = (n + WCHUNK - 1) / WCHUNK;
+  const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + warp, GW = gridDim.x * (blockDim.x >> 5);
+  const uint32_t nch = (n + WCHUNK - 1) / WCHUNK;
   const bool a16 = ((uintptr_t)rec & 15u) == 0;
-  auto ld = [&](uint64_t i0) {
+  auto ld = [&](uint32_t i0) {
     if (a16 && i0 + 1 < n) return __ldcs(reinterpret_cast<const ulonglong2*>(rec + i0));
     return make_ulonglong2(i0 < n ? __ldcs(rec + i0) : 0ull, i0 + 1 < n ? __ldcs(rec + i0 + 1) : 0ull);
   };
   ulonglong2 nx = make_ulonglong2(0, 0);
   if (gw < nch) nx = ld(gw * WCHUNK + 2 * lane);
-  for (uint64_t c = gw; c < nch; c += GW) {
+  for (uint32_t c = gw; c < nch; c += GW) {
     const ulonglong2 r = nx;
     if (c + GW < nch) nx = ld((c + GW) * WCHUNK + 2 * lane);
-    const uint64_t i0 = c * WCHUNK + 2 * lane;
+    const uint32_t i0 = c * WCHUNK + 2 * lane;
     fn(r, i0, i0 < n, i0 + 1 < n);
   }
 }
@@ -520,7 +523,7 @@ __device__ __noinline__ void scan_fatal(const View& v, const Scratch& S, uint32_
 }
 
 template <bool kStaged>
-__device__ __forceinline__ void scan_fast(const World& W, const View& v, const Scratch& S, uint4 e, uint64_t gidx,
+__device__ __forceinline__ void scan_fast(const World& W, const View& v, const Scratch& S, uint4 e, uint32_t gidx,
                                           unsigned long long* counts, ScanOut& o) {
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const Dec d = decode_fast(v.T, W.page_state, S, e, gidx, lane);
@@ -642,15 +645,17 @@ __device__ __forceinline__ void scan_phase(const World& W, const Scratch& S, con
   QOp* q = reinterpret_cast<QOp*>(smem + L.queue) + (threadIdx.x >> 5) * QCAP;
   uint32_t qn = 0;
   const bool sparse = W.dd_groups == 1;
-  ldg_stream(in, n, [&](uint4 e0, uint64_t i0, bool ok0, uint4 e1, uint64_t i1, bool ok1) {
+  const uint32_t base = (uint32_t)P.base_index;                          // < MAX_GIDX
+  unsigned long long* const drec = kStaged ? S.drec + (P.base_index - S.drec_base) : nullptr;
+  ldg_stream(in, n, [&](uint4 e0, uint32_t i0, bool ok0, uint4 e1, uint32_t i1, bool ok1) {
     if (MPSF_ABLATE & 64) { if (e0.x == 0x12345 && e1.y == 0x777) atomicOr(S.ctrl + C_ERR, 1u); return; }
     ScanOut o0, o1;
     if (!ok0) e0.w = 0;                       // past the end: decodes as a skipped entry
     if (!ok1) e1.w = 0;
-    scan_fast<kStaged>(W, v, S, e0, P.base_index + i0, counts, o0);
-    scan_fast<kStaged>(W, v, S, e1, P.base_index + i1, counts, o1);
+    scan_fast<kStaged>(W, v, S, e0, base + i0, counts, o0);
+    scan_fast<kStaged>(W, v, S, e1, base + i1, counts, o1);
     if (kStaged) {                                     // pass-1 records, two per lane (16 bytes)
-      unsigned long long* rp = S.drec + (P.base_index - S.drec_base) + i0;
+      unsigned long long* rp = drec + i0;
       if (ok1 && (((uintptr_t)rp & 15u) == 0)) *reinterpret_cast<ulonglong2*>(rp) = make_ulonglong2(o0.rec, o1.rec);
       else {
         if (ok0) rp[0] = o0.rec;
@@ -963,7 +968,7 @@ struct FinA {
 
 template <bool kStaged>
 __device__ __forceinline__ void fin_addr(const World& W, const View& v, const Scratch& S, const FinClient* fct,
-                                         const Dec& dd, uint64_t gidx, FinA& a) {
+                                         const Dec& dd, uint32_t gidx, FinA& a) {
   a.d = dd;
   const Dec& d = a.d;
   const uint32_t f = d.f;
@@ -984,7 +989,7 @@ __device__ __forceinline__ void fin_addr(const World& W, const View& v, const Sc
 
 template <bool kStaged>
 __device__ __forceinline__ void fin_resolve(const World& W, const View& v, const Scratch& S, const FinClient* fct,
-                                            uint64_t gidx, const FinA& a, uint32_t wd, uint32_t wn,
+                                            uint32_t gidx, const FinA& a, uint32_t wd, uint32_t wn,
                                             uint32_t we, unsigned long long& o8, bool& canc, bool& rep,
                                             unsigned long long& key) {
   const Dec& d = a.d;
@@ -1062,19 +1067,20 @@ __device__ __forceinline__ void finalize_phase(const World& W, const Scratch& S,
                                                const mpsf_fault_entry* __restrict__ in, uint64_t n, const Params& P,
                                                mpsf_out_record* __restrict__ out, uint64_t q_base) {
   const uint32_t lane = threadIdx.x & 31;
-  auto body = [&](const Dec& d0, const Dec& d1, uint64_t i0, bool ok0, bool ok1) {
-    const uint64_t i1 = i0 + 1;
+  const uint32_t base = (uint32_t)P.base_index;   // < MAX_GIDX
+  auto body = [&](const Dec& d0, const Dec& d1, uint32_t i0, bool ok0, bool ok1) {
+    const uint32_t i1 = i0 + 1;
     FinA a0, a1;
-    fin_addr<kStaged>(W, v, S, fct, d0, P.base_index + i0, a0);
-    fin_addr<kStaged>(W, v, S, fct, d1, P.base_index + i1, a1);
+    fin_addr<kStaged>(W, v, S, fct, d0, base + i0, a0);
+    fin_addr<kStaged>(W, v, S, fct, d1, base + i1, a1);
     const uint32_t wd0 = a0.pd ? __ldcg(a0.pd) : EMPTY32, wn0 = a0.pn ? __ldcg(a0.pn) : EMPTY32;
     const uint32_t we0 = a0.pe ? __ldcg(a0.pe) : EMPTY32;
     const uint32_t wd1 = a1.pd ? __ldcg(a1.pd) : EMPTY32, wn1 = a1.pn ? __ldcg(a1.pn) : EMPTY32;
     const uint32_t we1 = a1.pe ? __ldcg(a1.pe) : EMPTY32;
     unsigned long long o0, o1, k0, k1;
     bool c0, c1, r0, r1;
-    fin_resolve<kStaged>(W, v, S, fct, P.base_index + i0, a0, wd0, wn0, we0, o0, c0, r0, k0);
-    fin_resolve<kStaged>(W, v, S, fct, P.base_index + i1, a1, wd1, wn1, we1, o1, c1, r1, k1);
+    fin_resolve<kStaged>(W, v, S, fct, base + i0, a0, wd0, wn0, we0, o0, c0, r0, k0);
+    fin_resolve<kStaged>(W, v, S, fct, base + i1, a1, wd1, wn1, we1, o1, c1, r1, k1);
     unsigned long long* o = reinterpret_cast<unsigned long long*>(out) + i0;
     if (ok1 && (((uintptr_t)o & 15u) == 0)) __stcs(reinterpret_cast<ulonglong2*>(o), make_ulonglong2(o0, o1));
     else {
@@ -1097,18 +1103,18 @@ __device__ __forceinline__ void finalize_phase(const World& W, const Scratch& S,
   if (kStaged) {
     // staged worlds stream the pass-1 records: one 16-byte load = this lane's two records
     const unsigned long long* rec = S.drec + (P.base_index - S.drec_base);
-    rec_stream(rec, n, [&](ulonglong2 r, uint64_t i0, bool ok0, bool ok1) {
+    rec_stream(rec, n, [&](ulonglong2 r, uint32_t i0, bool ok0, bool ok1) {
       Dec d0, d1;
       unpack_rec(v, slut, (ok0 && !(MPSF_ABLATE & 256)) ? r.x : 0ull, in, i0, d0);
       unpack_rec(v, slut, (ok1 && !(MPSF_ABLATE & 256)) ? r.y : 0ull, in, i0 + 1, d1);
       body(d0, d1, i0, ok0, ok1);
     });
   } else {
-    ldg_stream(in, n, [&](uint4 e0, uint64_t i0, bool ok0, uint4 e1, uint64_t i1, bool ok1) {
+    ldg_stream(in, n, [&](uint4 e0, uint32_t i0, bool ok0, uint4 e1, uint32_t i1, bool ok1) {
       if (!ok0) e0.w = 0;                     // past the end: decodes as a skipped entry
       if (!ok1) e1.w = 0;
-      const Dec d0 = decode_fast(v.T, W.page_state, S, e0, P.base_index + i0, lane);
-      const Dec d1 = decode_fast(v.T, W.page_state, S, e1, P.base_index + i1, lane);
+      const Dec d0 = decode_fast(v.T, W.page_state, S, e0, base + i0, lane);
+      const Dec d1 = decode_fast(v.T, W.page_state, S, e1, base + i1, lane);
       body(d0, d1, i0, ok0, ok1);
     });
   }
