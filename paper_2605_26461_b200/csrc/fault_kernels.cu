@@ -1309,24 +1309,70 @@ __global__ void k_summary(const Scratch S, uint64_t nseg, DevSummary* out) {
 
 // ---- batched translation kernels ------------------------------------------------------------
 // T1: the first PREFETCH index per managed page (the only in-batch dependency of resolve_va).
+// Only PREFETCH translations matter here (~1 in 10 accesses), so a warp stacks its candidates
+// (entry + index) in shared memory and decodes them 32 at a time: one decode per 32 prefetches
+// instead of one per access.  (Malformed entries are reported by k_tr_classify, which decodes
+// every access.)  Without room for the stacks (use_q false) every access is decoded.
+constexpr uint32_t PFQ = 96;                       // per-warp stack: < 32 kept + 64 per chunk
+constexpr uint32_t PFQ_BYTES = WARPS * PFQ * 20;   // uint4 entry + u32 index
+
 template <bool kStaged>
 __global__ void __launch_bounds__(BLOCK, 1) k_tr_prefetch(World W, Scratch S, const mpsf_fault_entry* __restrict__ in,
-                                                          uint64_t n, Params P) {
+                                                          uint64_t n, Params P, uint32_t use_q) {
   extern __shared__ __align__(128) uint8_t smem[];
   pdl_trigger();
   const Layout L = make_layout(W, kStaged, true);
   const View v = setup<kStaged>(smem, L, W, S, false, true, false, true);
   __syncthreads();
   pdl_wait();
-  const uint32_t lane = threadIdx.x & 31;
-  ldg_stream(in, n, [&](uint4 e0, uint64_t i0, bool ok0, uint4 e1, uint64_t i1, bool ok1) {
-    if (!ok0) e0.w = 0;
-    if (!ok1) e1.w = 0;
-    const Dec d0 = decode_fast(v.T, W.page_state, S, e0, P.base_index + i0, lane);
-    const Dec d1 = decode_fast(v.T, W.page_state, S, e1, P.base_index + i1, lane);
-    if ((d0.f & TR_PF) && d0.inr) min32(S.pf + d0.slot, (uint32_t)(P.base_index + i0));
-    if ((d1.f & TR_PF) && d1.inr) min32(S.pf + d1.slot, (uint32_t)(P.base_index + i1));
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t base = (uint32_t)P.base_index;
+  if (!use_q) {
+    ldg_stream(in, n, [&](uint4 e0, uint32_t i0, bool ok0, uint4 e1, uint32_t i1, bool ok1) {
+      if (!ok0) e0.w = 0;
+      if (!ok1) e1.w = 0;
+      const Dec d0 = decode_fast(v.T, W.page_state, S, e0, base + i0, lane);
+      const Dec d1 = decode_fast(v.T, W.page_state, S, e1, base + i1, lane);
+      if ((d0.f & TR_PF) && d0.inr) min32(S.pf + d0.slot, base + i0);
+      if ((d1.f & TR_PF) && d1.inr) min32(S.pf + d1.slot, base + i1);
+    });
+    return;
+  }
+  uint4* qe = reinterpret_cast<uint4*>(smem + L.total) + warp * PFQ;
+  uint32_t* qi = reinterpret_cast<uint32_t*>(smem + L.total + WARPS * PFQ * 16) + warp * PFQ;
+  uint32_t qn = 0;
+  auto drain = [&](uint32_t k) {   // decode stack entries [qn - k, qn) by lanes 0..k-1
+    __syncwarp();
+    if (lane < k) {
+      const uint32_t g = qi[qn - k + lane];
+      const Dec d = decode_fast(v.T, W.page_state, S, qe[qn - k + lane], g, lane);
+      if ((d.f & TR_PF) && d.inr) min32(S.pf + d.slot, g);
+    }
+    qn -= k;
+    __syncwarp();
+  };
+  const uint32_t lt = (1u << lane) - 1u;
+  ldg_stream(in, n, [&](uint4 e0, uint32_t i0, bool ok0, uint4 e1, uint32_t i1, bool ok1) {
+    // candidates: valid translation entries with access PREFETCH
+    const bool c0 = ok0 && (e0.w & 0x01FFFF00u) == (0x01000000u | (2u << 8));
+    const bool c1 = ok1 && (e1.w & 0x01FFFF00u) == (0x01000000u | (2u << 8));
+    const uint32_t b0 = __ballot_sync(0xFFFFFFFFu, c0), b1 = __ballot_sync(0xFFFFFFFFu, c1);
+    if (!(b0 | b1)) return;
+    if (c0) {
+      const uint32_t p = qn + __popc(b0 & lt);
+      qe[p] = e0;
+      qi[p] = base + i0;
+    }
+    qn += __popc(b0);
+    if (c1) {
+      const uint32_t p = qn + __popc(b1 & lt);
+      qe[p] = e1;
+      qi[p] = base + i1;
+    }
+    qn += __popc(b1);
+    while (qn >= 32) drain(32);
   });
+  if (qn) drain(qn);
 }
 
 // T2: Hit / Miss per access (the page state an earlier prefetch left), per-chunk ballots of
@@ -1674,7 +1720,9 @@ static int translate_t(const World& W, const Scratch& S, const mpsf_fault_entry*
   }
   const uint32_t smem = make_layout(W, kStaged, true).total;
   const int g = clamp_grid(grid_for(k_tr_classify<kStaged>, smem), n);
-  launch_pdl(k_tr_prefetch<kStaged>, dim3(g), dim3(BLOCK), smem, st, W, S, in, n, P);
+  const uint32_t use_q = smem + PFQ_BYTES <= (uint32_t)SMEM_MAX ? 1u : 0u;
+  launch_pdl(k_tr_prefetch<kStaged>, dim3(g), dim3(BLOCK), smem + (use_q ? PFQ_BYTES : 0u), st, W, S, in, n, P,
+             use_q);
   mk.mark("k_tr_prefetch");
   launch_pdl(k_tr_classify<kStaged>, dim3(g), dim3(BLOCK), smem, st, W, S, in, n, P, hit);
   mk.mark("k_tr_classify");
