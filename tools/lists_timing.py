@@ -15,10 +15,16 @@ bufs = DeviceBuffers(n, w.n_clients)
 for _ in range(3):
     eng.process_device(d_in, n, BatchParams(isolation=True), bufs)
 torch.cuda.synchronize()
-t = bufs.cancel[:8 * 4 * 160].cpu().numpy().view(np.uint64).reshape(-1, 4)[:153]
+nseg = -(-(-(-n // 64)) // 256)
+t = bufs.cancel[:8 * 4 * nseg].cpu().numpy().view(np.uint64).reshape(-1, 4)[:nseg]
 t0 = t[:, 0].min()
 st, en = (t[:, 0] - t0) / 1e3, (t[:, 1] - t0) / 1e3
 order = np.argsort(-(en - st))
 for b in order[:12]:
     print(f"block {b:4d} sm {t[b,2]:4d} start {st[b]:8.2f} end {en[b]:8.2f} dur {en[b]-st[b]:8.2f} us")
 print("median dur", np.median(en - st), "max end", en.max(), "starts spread", st.max())
+dd = bufs.dedup_idx if hasattr(bufs, "dedup_idx") else None
+res = eng.process(trace, BatchParams(isolation=True))
+seg = np.asarray(res.dedup_idx, np.int64) // (64 * 256)
+cnt = np.bincount(seg, minlength=nseg)
+print("reps per segment: first 8", cnt[:8].tolist(), "max", cnt.max(), "median", int(np.median(cnt)), "total", cnt.sum())
