@@ -331,9 +331,7 @@ def run_mine(args):
             "metric": METRIC, "value": value, "unit": "entries/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": f"{args.workload}: 48 MPS clients x 32 ranges x 16 pages, "
-                                   f"{n} entries/GPU, translation misses + parse-time (1e-4) + SM traps (1e-5), "
-                                   f"isolation on (BASELINE configs[1])",
+            "config": {"workload": workload_name(args.workload, n),
                        "entries_per_gpu": n, "clients": w.n_clients, "ranges": int(len(w.ranges)),
                        "l2_flush": "256 MiB write between timed steps, outside the per-step CUDA events",
                        "parallelism": f"shard{ws}", "path": "general" if summ.path else "fast",
@@ -548,6 +546,20 @@ def bench_remap(args, eng, hbm_peak, flush):
 
 # ------------------------------------------------------------------------------------------
 
+def workload_name(wl: str, n: int) -> str:
+    """The `config.workload` both arms report (same text, so the driver's ratio compares like
+    with like)."""
+    from paper_2605_26461_b200 import synth
+    c = synth.CONFIGS[wl]
+    mix = "translation misses"
+    if c.get("parse_frac"):
+        mix += f" + parse-time ({c['parse_frac']:g})"
+    if c.get("trap_frac"):
+        mix += f" + SM traps ({c['trap_frac']:g})"
+    return (f"{wl}: {c['clients']} MPS clients x 32 ranges x {c['pages']} pages, {n} entries/GPU, {mix}, "
+            f"isolation on")
+
+
 def run_reference(args):
     """The reference's CPU implementation of the path (its restatement oracle/mpsf_oracle.c;
     the reference itself is pure Python and absent on the GPU box) on the host cores."""
@@ -578,7 +590,8 @@ def run_reference(args):
     line = {"metric": METRIC, "value": value, "unit": "entries/s", "impl": "reference", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": args.workload, "entries_per_step": sample},
+            "config": {"workload": workload_name(args.workload, n), "entries_per_gpu": n,
+                       "entries_per_step": sample},
             "cpu_baseline": {"value": value, "unit": "entries/s", "cores": threads, "kind": "port", "sample": smp},
             "e2e": {"value": value, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
