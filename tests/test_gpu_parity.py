@@ -299,3 +299,41 @@ def test_remap_granularities_vs_oracle(eng, gran):
     got = eng.remap(0x7F00_0000_0000, phys, gran)
     want = so.remap_table(0x7F00_0000_0000, phys, gran)
     assert np.array_equal(got, want)
+
+
+def test_maximum_batch_size_properties(eng):
+    """A batch of exactly MAX_GIDX = 2^29 entries (the largest the global index / drain key
+    encoding allows), device-resident: size-independent properties of the storm (exactly
+    `u` representatives, every other entry a duplicate, ordered lists, counts summing to n),
+    and one entry more is refused with MPSF_E_TOO_LARGE before any work."""
+    import torch
+    from paper_2605_26461_b200.errors import SimError
+    n, u = 1 << 29, 10_000_000
+    w, _ = synth.build_synthetic_world(48, 8192, 3)
+    d_in = synth.generate_storm(w, n, u, 3, device="cuda")
+    eng.upload_world(w)
+    bufs = DeviceBuffers(n, w.n_clients)
+    p = BatchParams(isolation=True)
+    for _ in range(4):
+        eng.process_device(d_in, n, p, bufs)
+        try:
+            s = eng.summary()
+            break
+        except Exception as exc:   # hash overflow: the table grew, run again
+            assert type(exc).__name__ == "HashOverflow"
+    assert int(s.n_dedup) == u
+    out = bufs.out[:8 * n].view(torch.int64)
+    verdict = (out >> 40) & 0xFF
+    assert int(((verdict & K.V_DUP) != 0).sum()) == n - u
+    didx = bufs.didx[:4 * u].view(torch.int32).to(torch.int64)
+    assert bool((didx[1:] > didx[:-1]).all())
+    nc = int(s.n_cancel)
+    if nc > 1:
+        ca = bufs.cancel[:4 * nc].view(torch.int32).to(torch.int64)
+        assert bool((ca[1:] > ca[:-1]).all())
+    counts = bufs.counts[:8 * K.N_SCENARIOS * w.n_clients].view(torch.int64)
+    assert int(counts.sum()) == n
+    with pytest.raises(SimError):
+        eng.process_device(d_in, n + 1, p, bufs)
+    del d_in, bufs, out, verdict, didx
+    torch.cuda.empty_cache()
