@@ -324,6 +324,9 @@ def run_mine(args):
         extra["remap_c4"] = bench_remap(args, eng, hbm_peak, flush)
     if not args.no_storm and ws == 1:
         extra["translate_f2"] = bench_translate(args, eng, hbm_peak, flush, w)
+    elif args.sharded_translate:
+        # opt-in: the multi-GPU form of the translation extra (NCCL between the phases)
+        extra["translate_f2_sharded"] = bench_translate_sharded(args, eng, hbm_peak, flush, w, ws, rank)
         extra["fold_f3"] = bench_fold(args, eng, hbm_peak, flush)
 
     if rank == 0:
@@ -438,6 +441,57 @@ def bench_translate(args, eng, hbm_peak, flush, w):
             "n_miss": nm, "n_populated": npop, "bit_exact_vs_oracle": bool(exact),
             "roofline": {"bound": "hbm", "achieved": B / (ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                          "frac": B / (ms / 1e3) / 1e9 / hbm_peak, "alg_bytes": B}}
+
+
+def bench_translate_sharded(args, eng, hbm_peak, flush, w, ws, rank):
+    """The batched translation over N GPUs (weak scaling): rank r translates its own 10^7
+    accesses at global indices r*10^7.., the ranks MIN-combine the first-PREFETCH page table
+    over NCCL between the two phases (parallel.ShardedTranslate); max over ranks of the
+    per-rank device time.  Each rank checks its shard against the oracle's two phases with the
+    same combined table."""
+    import torch
+    import torch.distributed as dist
+    from paper_2605_26461_b200 import synth
+    from paper_2605_26461_b200.parallel import GpuTranslateShard, ShardedTranslate, allreduce_min_unsigned
+    from oracle.seq_oracle import translate_finish_np, translate_prefetch_np
+    n = 10_000_000 if args.n is None else args.n
+    acc = synth.generate_access_stream(w, n, seed=11 + rank)
+    eng.upload_world(w)
+    d_acc = torch.from_numpy(acc.view(np.uint8)).cuda()
+    shard = GpuTranslateShard(eng, d_acc, n, rank * n)
+    st = ShardedTranslate(shard)
+    got = st.translate()
+    pf = torch.from_numpy(translate_prefetch_np(w, acc, rank * n)).cuda()
+    allreduce_min_unsigned(pf)
+    want = translate_finish_np(w, acc, rank * n, pf.cpu().numpy())
+    ok = (np.array_equal(got["hit"], want.hit) and np.array_equal(got["fault_idx"], want.fault_idx)
+          and np.array_equal(got["pop_idx"], want.pop_idx))
+    ok_all = torch.tensor([1 if ok else 0], dtype=torch.int32, device="cuda")
+    dist.all_reduce(ok_all, op=dist.ReduceOp.MIN)
+    steps = max(20, min(args.steps, 50))
+
+    def one():
+        shard.prefetch()
+        for t, _ in shard.exchange(4):
+            allreduce_min_unsigned(t)
+        eng._check(eng.lib.mpsf_translate_finish(eng.ctx, d_acc.data_ptr(), n, rank * n, shard.hit.data_ptr(),
+                                                 shard.faults.data_ptr(), shard.fi.data_ptr(), shard.pi.data_ptr(),
+                                                 shard.sp))
+    rewarm(one)
+    barrier(ws)
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        one()
+    b.record()
+    b.synchronize()
+    ms = max_over_ranks(ws, a.elapsed_time(b) / steps)
+    return {"workload": f"{n} accesses per GPU (resolve_va) on the c2 world, sharded over {ws} GPUs, one NCCL MIN "
+                        f"of the first-PREFETCH page table between the phases",
+            "value": ws * n / (ms / 1e3), "unit": "accesses/s", "ms_per_step": ms, "steps": steps,
+            "scaling": "weak", "bit_exact_vs_oracle": bool(int(ok_all.item()))}
 
 
 def bench_fold(args, eng, hbm_peak, flush):
@@ -602,6 +656,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--sharded-translate", action="store_true",
+                    help="with --gpus N > 1: also time the sharded batched translation (NCCL MIN between phases)")
     ap.add_argument("--impl", default="mine", choices=("mine", "reference"))
     ap.add_argument("--workload", default="c2b", choices=("c1", "c2a", "c2b"))
     ap.add_argument("--n", type=int, default=None)

@@ -190,6 +190,16 @@ int mpsf_translate(mpsf_ctx* ctx, const mpsf_fault_entry* d_accesses, uint64_t n
                    uint8_t* d_hit, mpsf_fault_entry* d_faults, uint32_t* d_fault_idx, uint32_t* d_pop_idx,
                    void* stream);
 int mpsf_get_translate_summary(mpsf_ctx* ctx, mpsf_translate_summary* out);
+/* The same as two phases, for sharded streams (one process per GPU, contiguous index ranges
+ * base_index .. base_index+n): mpsf_translate_prefetch records the first PREFETCH per
+ * managed page (global indices) in the table mpsf_exchange_buffers(ctx, 4, ...) exposes;
+ * after the shards combine it with a MIN, mpsf_translate_finish classifies and compacts this
+ * shard (same n / base_index).  mpsf_translate = prefetch + finish. */
+int mpsf_translate_prefetch(mpsf_ctx* ctx, const mpsf_fault_entry* d_accesses, uint64_t n, uint64_t base_index,
+                            void* stream);
+int mpsf_translate_finish(mpsf_ctx* ctx, const mpsf_fault_entry* d_accesses, uint64_t n, uint64_t base_index,
+                          uint8_t* d_hit, mpsf_fault_entry* d_faults, uint32_t* d_fault_idx, uint32_t* d_pop_idx,
+                          void* stream);
 
 /* ---- snapshot delta fold: StandbyInstance.fold (recovery.py:83-92) over a batch ----
  * The step after the recovery remap.  n_snap ForwardSnapshots
@@ -297,7 +307,8 @@ typedef struct {
   uint32_t elem_bytes;  /* 4 or 8 (unsigned)                                */
   uint32_t op;          /* MPSF_XOP_MIN / MPSF_XOP_SUM                      */
 } mpsf_xbuf;
-/* stage 1: after mpsf_scan; 2: after mpsf_general(stage 1); 3: after stage 2 */
+/* stage 1: after mpsf_scan; 2: after mpsf_general(stage 1); 3: after stage 2;
+ * 4: after mpsf_translate_prefetch (the first-PREFETCH page table, MIN) */
 int mpsf_exchange_buffers(mpsf_ctx* ctx, int stage, mpsf_xbuf* out, int cap);
 /* which: 0 dedup hash, 1 first-isolation (NR) hash.  Export compacts the non-empty slots
  * (returns the count, waits on the stream); merge inserts keys with atomic-min values. */

@@ -487,11 +487,7 @@ def translate_batch(w: FlatWorld, entries: np.ndarray, base_index: int = 0) -> T
     return TranslateResult(hit, np.array(faults, np.uint32), np.array(pops, np.uint32))
 
 
-def translate_batch_np(w: FlatWorld, entries: np.ndarray, base_index: int = 0) -> TranslateResult:
-    """The same result as ``translate_batch`` for large streams (numpy, no per-entry loop):
-    the only in-batch dependency is "was this page populated by an earlier prefetch", i.e. the
-    first prefetch index per (range, page).  Assumes well-formed entries (no error checks)."""
-    n = len(entries)
+def _translate_attr(w: FlatWorld, entries: np.ndarray):
     valid = (entries["flags"] & K.ENTRY_FLAG_VALID) != 0
     ch = entries["channel"].astype(np.int64)
     client = w.channels["client"][ch].astype(np.uint64)
@@ -505,14 +501,31 @@ def translate_batch_np(w: FlatWorld, entries: np.ndarray, base_index: int = 0) -
     has = (pos >= 0) & (r["client"][p] == client) & (page < (r["end"][p] >> np.uint64(12)))
     slot = (r["page_off"][p].astype(np.int64) + (page - (r["base"][p] >> np.uint64(12))).astype(np.int64))
     slot = np.where(has, slot, 0)
+    managed = has & (r["kind"][p] == K.RK_MANAGED)
+    return valid, acc, p, has, slot, managed
+
+
+def translate_prefetch_np(w: FlatWorld, entries: np.ndarray, base_index: int = 0) -> np.ndarray:
+    """Phase 1 of ``translate_batch_np`` for a shard at global index ``base_index``: the first
+    PREFETCH index per managed page slot (global indices; int64 max where none).  Shards of a
+    stream combine these with an elementwise MIN."""
+    valid, acc, _, _, slot, managed = _translate_attr(w, entries)
+    pf_first = np.full(len(w.page_state) + 1, np.iinfo(np.int64).max, np.int64)
+    sel = valid & (acc == K.ACC_PREFETCH) & managed
+    idx = np.arange(len(entries), dtype=np.int64) + base_index
+    np.minimum.at(pf_first, slot[sel], idx[sel])
+    return pf_first
+
+
+def translate_finish_np(w: FlatWorld, entries: np.ndarray, base_index: int, pf_first: np.ndarray) -> TranslateResult:
+    """Phase 2: hit / miss of the shard's accesses given the (combined) first-prefetch table."""
+    n = len(entries)
+    valid, acc, p, has, slot, managed = _translate_attr(w, entries)
+    r = w.ranges
     st = np.where(has, w.page_state[slot], 0).astype(np.int64)
     res, ro = st & 3, (st & K.PS_RO) != 0
-    managed = has & (r["kind"][p] == K.RK_MANAGED)
     pref = acc == K.ACC_PREFETCH
-    idx = np.arange(n, dtype=np.int64)
-    pf_first = np.full(len(w.page_state) + 1, np.iinfo(np.int64).max, np.int64)
-    sel = valid & pref & managed
-    np.minimum.at(pf_first, slot[sel], idx[sel])
+    idx = np.arange(n, dtype=np.int64) + base_index
     populated_before = has & (pf_first[slot] < idx)
     res_eff = np.where(populated_before, K.RES_GPU, res)
     live = has & (r["lifecycle"][p] == K.LC_LIVE)
@@ -523,6 +536,13 @@ def translate_batch_np(w: FlatWorld, entries: np.ndarray, base_index: int = 0) -
     pop = valid & pref & managed & (pf_first[slot] == idx) & (res != K.RES_GPU)
     return TranslateResult(hit, (np.nonzero(valid & ~ok)[0] + base_index).astype(np.uint32),
                            (np.nonzero(pop)[0] + base_index).astype(np.uint32))
+
+
+def translate_batch_np(w: FlatWorld, entries: np.ndarray, base_index: int = 0) -> TranslateResult:
+    """The same result as ``translate_batch`` for large streams (numpy, no per-entry loop):
+    the only in-batch dependency is "was this page populated by an earlier prefetch", i.e. the
+    first prefetch index per (range, page).  Assumes well-formed entries (no error checks)."""
+    return translate_finish_np(w, entries, base_index, translate_prefetch_np(w, entries, base_index))
 
 
 # -- snapshot delta fold (SURVEY.md §8(f) rank 3: the step after the remap) ----------------------

@@ -89,6 +89,9 @@ SIGNATURES = {
     "mpsf_collect_host": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(Summary)]),
     "mpsf_translate": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_void_p, C.c_void_p]),
+    "mpsf_translate_prefetch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p]),
+    "mpsf_translate_finish": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.c_void_p, C.c_void_p]),
     "mpsf_get_translate_summary": (C.c_int, [C.c_void_p, C.POINTER(TranslateSummary)]),
     "mpsf_remap": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_uint32,
                              C.c_void_p, C.c_void_p]),

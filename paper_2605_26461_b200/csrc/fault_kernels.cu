@@ -1709,21 +1709,35 @@ int launch_copyout(const Scratch& S, uint64_t n, const unsigned long long* d_dk,
 }
 
 template <bool kStaged>
-static int translate_t(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
-                       uint8_t* hit, mpsf_fault_entry* faults, uint32_t* fault_idx, uint32_t* pop_idx,
-                       DevSummary* sum, cudaStream_t st, const Marker& mk) {
+static void translate_attrs() {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_tr_prefetch<kStaged>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
     cudaFuncSetAttribute(k_tr_classify<kStaged>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
     attr = true;
   }
+}
+
+template <bool kStaged>
+static int translate_prefetch_t(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n,
+                                const Params& P, cudaStream_t st, const Marker& mk) {
+  translate_attrs<kStaged>();
   const uint32_t smem = make_layout(W, kStaged, true).total;
   const int g = clamp_grid(grid_for(k_tr_classify<kStaged>, smem), n);
   const uint32_t use_q = smem + PFQ_BYTES <= (uint32_t)SMEM_MAX ? 1u : 0u;
   launch_pdl(k_tr_prefetch<kStaged>, dim3(g), dim3(BLOCK), smem + (use_q ? PFQ_BYTES : 0u), st, W, S, in, n, P,
              use_q);
   mk.mark("k_tr_prefetch");
+  return ok_or_err();
+}
+
+template <bool kStaged>
+static int translate_finish_t(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n,
+                              const Params& P, uint8_t* hit, mpsf_fault_entry* faults, uint32_t* fault_idx,
+                              uint32_t* pop_idx, DevSummary* sum, cudaStream_t st, const Marker& mk) {
+  translate_attrs<kStaged>();
+  const uint32_t smem = make_layout(W, kStaged, true).total;
+  const int g = clamp_grid(grid_for(k_tr_classify<kStaged>, smem), n);
   launch_pdl(k_tr_classify<kStaged>, dim3(g), dim3(BLOCK), smem, st, W, S, in, n, P, hit);
   mk.mark("k_tr_classify");
   const uint64_t nseg = segments_for(n);
@@ -1733,15 +1747,32 @@ static int translate_t(const World& W, const Scratch& S, const mpsf_fault_entry*
   return ok_or_err();
 }
 
-int launch_translate(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
-                     uint8_t* hit, mpsf_fault_entry* faults, uint32_t* fault_idx, uint32_t* pop_idx, DevSummary* sum,
-                     cudaStream_t st, const Marker& mk) {
+// Phase 1 of a batched translation: the first PREFETCH per managed page (S.pf, global
+// indices -- shards combine it with a MIN before phase 2).
+int launch_translate_prefetch(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n,
+                              const Params& P, cudaStream_t st, const Marker& mk) {
+  if (n == 0) return 0;
+  return staged_fits(W) ? translate_prefetch_t<true>(W, S, in, n, P, st, mk)
+                        : translate_prefetch_t<false>(W, S, in, n, P, st, mk);
+}
+
+// Phase 2: hit / miss per access against S.pf, the ordered miss and population lists.
+int launch_translate_finish(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n,
+                            const Params& P, uint8_t* hit, mpsf_fault_entry* faults, uint32_t* fault_idx,
+                            uint32_t* pop_idx, DevSummary* sum, cudaStream_t st, const Marker& mk) {
   if (n == 0) {
     launch_pdl(k_summary, dim3(1), dim3(1024), 0, st, S, (uint64_t)0, sum);
     return ok_or_err();
   }
-  return staged_fits(W) ? translate_t<true>(W, S, in, n, P, hit, faults, fault_idx, pop_idx, sum, st, mk)
-                        : translate_t<false>(W, S, in, n, P, hit, faults, fault_idx, pop_idx, sum, st, mk);
+  return staged_fits(W) ? translate_finish_t<true>(W, S, in, n, P, hit, faults, fault_idx, pop_idx, sum, st, mk)
+                        : translate_finish_t<false>(W, S, in, n, P, hit, faults, fault_idx, pop_idx, sum, st, mk);
+}
+
+int launch_translate(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
+                     uint8_t* hit, mpsf_fault_entry* faults, uint32_t* fault_idx, uint32_t* pop_idx, DevSummary* sum,
+                     cudaStream_t st, const Marker& mk) {
+  if (launch_translate_prefetch(W, S, in, n, P, st, mk)) return -1;
+  return launch_translate_finish(W, S, in, n, P, hit, faults, fault_idx, pop_idx, sum, st, mk);
 }
 
 int launch_hash_export(const Hash& h, uint64_t cap, unsigned long long* keys, uint32_t* vals, uint32_t* counter,

@@ -751,11 +751,11 @@ int mpsf_process(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const mp
   return rc;
 }
 
-int mpsf_translate(mpsf_ctx* c, const mpsf_fault_entry* d_acc, uint64_t n, uint64_t base_index, uint8_t* d_hit,
-                   mpsf_fault_entry* d_faults, uint32_t* d_fault_idx, uint32_t* d_pop_idx, void* stream) {
+int mpsf_translate_prefetch(mpsf_ctx* c, const mpsf_fault_entry* d_acc, uint64_t n, uint64_t base_index,
+                            void* stream) {
   if (!c) return MPSF_E_ARG;
   if (!c->has_world) return MPSF_E_NO_WORLD;
-  if (n && (!d_acc || !d_hit || !d_faults || !d_fault_idx || !d_pop_idx)) return MPSF_E_ARG;
+  if (n && !d_acc) return MPSF_E_ARG;
   if (base_index + n > MAX_GIDX) return MPSF_E_TOO_LARGE;
   CK(cudaSetDevice(c->device));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -775,14 +775,41 @@ int mpsf_translate(mpsf_ctx* c, const mpsf_fault_entry* d_acc, uint64_t n, uint6
   c->marker().mark("k_init");
   mpsf_params p{};
   p.base_index = base_index;
-  if (launch_translate(c->W, c->S, d_acc, n, to_params(&p), d_hit, d_faults, d_fault_idx, d_pop_idx, c->d_sum, st,
-                       c->marker()))
+  if (launch_translate_prefetch(c->W, c->S, d_acc, n, to_params(&p), st, c->marker())) return MPSF_E_CUDA;
+  c->phase_n = n;
+  c->last_launches = n ? 2 : 1;
+  return MPSF_OK;
+}
+
+int mpsf_translate_finish(mpsf_ctx* c, const mpsf_fault_entry* d_acc, uint64_t n, uint64_t base_index,
+                          uint8_t* d_hit, mpsf_fault_entry* d_faults, uint32_t* d_fault_idx, uint32_t* d_pop_idx,
+                          void* stream) {
+  if (!c) return MPSF_E_ARG;
+  if (!c->has_world) return MPSF_E_NO_WORLD;
+  if (n && (!d_acc || !d_hit || !d_faults || !d_fault_idx || !d_pop_idx)) return MPSF_E_ARG;
+  if (base_index + n > MAX_GIDX) return MPSF_E_TOO_LARGE;
+  if (n != c->phase_n) return MPSF_E_ARG;        // the batch mpsf_translate_prefetch started
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  mpsf_params p{};
+  p.base_index = base_index;
+  if (launch_translate_finish(c->W, c->S, d_acc, n, to_params(&p), d_hit, d_faults, d_fault_idx, d_pop_idx,
+                              c->d_sum, st, c->marker()))
     return MPSF_E_CUDA;
   CK(cudaEventRecord(c->ev_done, st));
   c->pending = true;
   c->last_n = n;
-  c->last_launches = n ? 4 : 2;
+  c->last_launches += n ? 2 : 1;
   return MPSF_OK;
+}
+
+int mpsf_translate(mpsf_ctx* c, const mpsf_fault_entry* d_acc, uint64_t n, uint64_t base_index, uint8_t* d_hit,
+                   mpsf_fault_entry* d_faults, uint32_t* d_fault_idx, uint32_t* d_pop_idx, void* stream) {
+  if (!c) return MPSF_E_ARG;
+  if (n && (!d_acc || !d_hit || !d_faults || !d_fault_idx || !d_pop_idx)) return MPSF_E_ARG;
+  int rc = mpsf_translate_prefetch(c, d_acc, n, base_index, stream);
+  if (rc) return rc;
+  return mpsf_translate_finish(c, d_acc, n, base_index, d_hit, d_faults, d_fault_idx, d_pop_idx, stream);
 }
 
 int mpsf_get_translate_summary(mpsf_ctx* c, mpsf_translate_summary* out) {
@@ -815,6 +842,8 @@ int mpsf_exchange_buffers(mpsf_ctx* c, int stage, mpsf_xbuf* out, int cap) {
     b[k++] = {c->d_nr1, c->W.n_pages, 4, MPSF_XOP_MIN};
   } else if (stage == 3) {
     b[k++] = {s + c->x_giso, c->x_giso_n, 4, MPSF_XOP_MIN};
+  } else if (stage == 4) {                        // translation: first PREFETCH per page
+    b[k++] = {c->d_pf, c->W.n_pages, 4, MPSF_XOP_MIN};
   } else {
     return MPSF_E_ARG;
   }

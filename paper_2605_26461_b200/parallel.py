@@ -260,6 +260,80 @@ class GpuShard:
         return self.bufs.fetch(self.n, self.eng.world.n_clients, int(s.n_dedup), int(s.n_cancel), int(s.path))
 
 
+# -- sharded batched translation (MemoryModel.resolve_va over a stream) --
+
+class ShardedTranslate:
+    """One rank's contiguous range of an access stream.  The only cross-access dependency of
+    ``resolve_va`` over a stream is "did an earlier PREFETCH populate this page", so after
+    phase 1 the ranks MIN-combine the first-PREFETCH page table (global indices) and each rank
+    classifies its range; the concatenated per-rank results equal the single-GPU result."""
+
+    def __init__(self, adapter, group=None):
+        self.a = adapter
+        self.group = group
+
+    def translate(self):
+        self.a.prefetch()
+        for t, op in self.a.exchange(4):
+            allreduce_min_unsigned(t, self.group)
+        return self.a.finish()
+
+
+class LocalTranslateGroup:
+    """The same over several shards held by one process (elementwise MIN across buffers)."""
+
+    def __init__(self, adapters):
+        self.ads = adapters
+
+    def translate(self):
+        import torch
+        for a in self.ads:
+            a.prefetch()
+        tabs = [a.exchange(4)[0][0] for a in self.ads]
+        flip = -(1 << 31)
+        acc = tabs[0] ^ flip
+        for t in tabs[1:]:
+            acc = torch.minimum(acc, t.to(acc.device) ^ flip)
+        acc = acc ^ flip
+        for t in tabs:
+            t.copy_(acc.to(t.device))
+        return [a.finish() for a in self.ads]
+
+
+class GpuTranslateShard:
+    """Adapter: ``mpsf_translate_prefetch`` / exchange stage 4 / ``mpsf_translate_finish`` for
+    one shard (accesses ``d_acc[0:n]`` at global index ``base``)."""
+
+    def __init__(self, eng: FaultEngine, d_acc, n: int, base: int):
+        import torch
+        self.eng, self.d_acc, self.n, self.base = eng, d_acc, n, base
+        self.lib, self.ctx = eng.lib, eng.ctx
+        self.sp = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        dev = d_acc.device
+        self.hit = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+        self.faults = torch.empty(max(16 * n, 16), dtype=torch.uint8, device=dev)
+        self.fi = torch.empty(max(4 * n, 4), dtype=torch.uint8, device=dev)
+        self.pi = torch.empty(max(4 * n, 4), dtype=torch.uint8, device=dev)
+
+    def prefetch(self):
+        self.eng._check(self.lib.mpsf_translate_prefetch(self.ctx, self.d_acc.data_ptr(), self.n, self.base, self.sp))
+
+    def exchange(self, stage):
+        arr = (_lib.XBuf * 4)()
+        k = self.lib.mpsf_exchange_buffers(self.ctx, stage, C.cast(arr, C.c_void_p), 4)
+        self.eng._check(min(k, 0))
+        return [(device_view(arr[i].ptr, arr[i].count, arr[i].elem_bytes), "min") for i in range(k)]
+
+    def finish(self):
+        self.eng._check(self.lib.mpsf_translate_finish(self.ctx, self.d_acc.data_ptr(), self.n, self.base,
+                                                       self.hit.data_ptr(), self.faults.data_ptr(),
+                                                       self.fi.data_ptr(), self.pi.data_ptr(), self.sp))
+        s = self.eng.translate_summary()
+        nm, npop = int(s.n_miss), int(s.n_populated)
+        return dict(hit=self.hit[:self.n].cpu().numpy(), fault_idx=self.fi[:4 * nm].cpu().numpy().view(np.uint32),
+                    pop_idx=self.pi[:4 * npop].cpu().numpy().view(np.uint32))
+
+
 def combine_verdicts_nccl(verdict: np.ndarray) -> np.ndarray:
     """Elementwise MAX of per-shard client fates (used only by the replica fallback)."""
     import torch

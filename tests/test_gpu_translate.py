@@ -88,3 +88,34 @@ def test_translate_errors_and_empty(eng):
     e[1]["kind"] = 8                                              # a trap record is not an access
     with pytest.raises(EntryError):
         eng.translate(e)
+
+
+@pytest.mark.parametrize("nshards", [2, 3])
+def test_sharded_translation_vs_whole_stream(nshards):
+    """The two-phase API (mpsf_translate_prefetch, exchange stage 4, mpsf_translate_finish)
+    over contiguous shards, one context each, the first-PREFETCH tables MIN-combined:
+    concatenated results equal the whole-stream oracle bit for bit."""
+    import torch
+    from paper_2605_26461_b200.parallel import GpuTranslateShard, LocalTranslateGroup
+    rnd = random.Random(60 + nshards)
+    for it in range(6):
+        w, _ = synth.build_synthetic_world(rnd.choice((6, 48)), rnd.choice((16, 64)), 1 + it % 3)
+        acc = synth.generate_access_stream(w, rnd.randint(1000, 300_000), seed=it, prefetch=rnd.choice((0.1, 0.4)))
+        n = len(acc)
+        cut = [n * r // nshards for r in range(nshards + 1)]
+        engs, ads = [], []
+        for r in range(nshards):
+            e = FaultEngine(0)
+            e.upload_world(w)
+            sh = acc[cut[r]:cut[r + 1]]
+            d = torch.from_numpy(sh.view(np.uint8).copy()).cuda() if len(sh) else torch.empty(16, dtype=torch.uint8,
+                                                                                                device="cuda")
+            ads.append(GpuTranslateShard(e, d, len(sh), cut[r]))
+            engs.append(e)
+        parts = LocalTranslateGroup(ads).translate()
+        for e in engs:
+            e.close()
+        want = so.translate_batch_np(w, acc)
+        assert np.array_equal(np.concatenate([p["hit"] for p in parts]), want.hit), it
+        assert np.array_equal(np.concatenate([p["fault_idx"] for p in parts]), want.fault_idx), it
+        assert np.array_equal(np.concatenate([p["pop_idx"] for p in parts]), want.pop_idx), it

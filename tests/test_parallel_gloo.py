@@ -142,3 +142,67 @@ def test_sharded_gloo_equals_sequential_oracle(ws):
     for seed in seeds:
         w, entries, bp = make_case(seed)
         check_against_oracle(w, entries, bp, [per_rank[r][seed] for r in range(ws)])
+
+
+# -- sharded batched translation (one MIN exchange of the first-PREFETCH page table) ----------
+
+class OracleTranslateShard:
+    """CPU adapter with the surface of parallel.GpuTranslateShard (the oracle's two phases)."""
+
+    def __init__(self, w, acc, base):
+        self.w, self.acc, self.base = w, acc, base
+
+    def prefetch(self):
+        self.pf = so.translate_prefetch_np(self.w, self.acc, self.base)
+
+    def exchange(self, stage):
+        assert stage == 4
+        return [(torch.from_numpy(self.pf), "min")]
+
+    def finish(self):
+        r = so.translate_finish_np(self.w, self.acc, self.base, self.pf)
+        return dict(hit=r.hit, fault_idx=r.fault_idx, pop_idx=r.pop_idx)
+
+
+def translate_case(seed):
+    from paper_2605_26461_b200 import synth
+    rnd = random.Random(seed)
+    w, _ = synth.build_synthetic_world(rnd.choice((4, 6)), rnd.choice((16, 64)), 1 + seed % 3)
+    acc = synth.generate_access_stream(w, rnd.randint(1, 3000), seed=seed, prefetch=rnd.choice((0.1, 0.4)))
+    return w, acc
+
+
+def _translate_worker(rank, ws, port, seeds, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    import pickle
+    from paper_2605_26461_b200.parallel import ShardedTranslate
+    results = {}
+    for seed in seeds:
+        w, acc = translate_case(seed)
+        n = len(acc)
+        cut = [n * r // ws for r in range(ws + 1)]
+        results[seed] = ShardedTranslate(OracleTranslateShard(w, acc[cut[rank]:cut[rank + 1]], cut[rank])).translate()
+    with open(os.path.join(outdir, f"t{rank}.pkl"), "wb") as f:
+        pickle.dump(results, f)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ws", [2, 3])
+def test_sharded_translation_gloo_equals_whole_stream(ws):
+    """Concatenated per-rank hits / misses / populations == the whole stream translated at once
+    (and that equals the access-by-access oracle, tests/test_translate_oracle.py)."""
+    import pickle
+    seeds = list(range(200, 230))
+    with tempfile.TemporaryDirectory() as d:
+        mp.start_processes(_translate_worker, args=(ws, _free_port(), seeds, d), nprocs=ws, start_method="fork")
+        per_rank = [pickle.load(open(os.path.join(d, f"t{r}.pkl"), "rb")) for r in range(ws)]
+    for seed in seeds:
+        w, acc = translate_case(seed)
+        want = so.translate_batch(w, acc)
+        parts = [per_rank[r][seed] for r in range(ws)]
+        assert np.array_equal(np.concatenate([p["hit"] for p in parts]), want.hit), seed
+        assert np.array_equal(np.concatenate([p["fault_idx"] for p in parts]), want.fault_idx), seed
+        assert np.array_equal(np.concatenate([p["pop_idx"] for p in parts]), want.pop_idx), seed
