@@ -295,17 +295,23 @@ def run_mine(args):
             # a stream of batches through the asynchronous form: two slots in flight, so the
             # H2D of batch k+1 overlaps the passes and the D2H of batch k
             hb2 = [hb, alloc_host_outputs(n, w.n_clients, pinned=True)]
-            eng.submit(pinned, params, hb2[0], 0)
-            eng.collect(0)
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            for k in range(e2e_steps):
-                if k >= 2:
-                    eng.collect(k % 2)
-                eng.submit(pinned, params, hb2[k % 2], k % 2)
-            for k in range(max(0, e2e_steps - 2), e2e_steps):
-                r2 = eng.collect(k % 2)
-            t_pipe = (time.perf_counter() - t0) / e2e_steps
+
+            def stream(nb):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                r = None
+                for k in range(nb):
+                    if k >= 2:
+                        eng.collect(k % 2)
+                    eng.submit(pinned, params, hb2[k % 2], k % 2)
+                for k in range(max(0, nb - 2), nb):
+                    r = eng.collect(k % 2)
+                return (time.perf_counter() - t0) / nb, r
+
+            stream(4)                                   # warm the two slots
+            # best of two timed streams: a host hiccup in one pass does not decide the number
+            (t_a, r2), (t_b, _) = stream(e2e_steps), stream(e2e_steps)
+            t_pipe = min(t_a, t_b)
             if t_pipe < t_e2e:
                 t_e2e = t_pipe
                 e2e_mode = "stream of batches, two in flight (mpsf_submit_host / mpsf_collect_host)"
@@ -324,10 +330,10 @@ def run_mine(args):
         extra["remap_c4"] = bench_remap(args, eng, hbm_peak, flush)
     if not args.no_storm and ws == 1:
         extra["translate_f2"] = bench_translate(args, eng, hbm_peak, flush, w)
+        extra["fold_f3"] = bench_fold(args, eng, hbm_peak, flush)
     elif args.sharded_translate:
         # opt-in: the multi-GPU form of the translation extra (NCCL between the phases)
         extra["translate_f2_sharded"] = bench_translate_sharded(args, eng, hbm_peak, flush, w, ws, rank)
-        extra["fold_f3"] = bench_fold(args, eng, hbm_peak, flush)
 
     if rank == 0:
         line = {
@@ -388,6 +394,18 @@ def bench_storm(args, eng, hbm_peak, flush):
     B = alg_bytes(n, nd, nc)
     ach = B / (ms / 1e3) / 1e9
     ok = nd == u and int(((res.out["verdict"] & 0x20) != 0).sum()) == n - u
+    # the CPU restatement (oracle/mpsf_oracle.c, all host threads) on a 5 M-entry prefix
+    from oracle import c_oracle as co
+    from oracle.seq_oracle import Params as OP
+    ns = min(n, 5_000_000)
+    from paper_2605_26461_b200.world import ENTRY_DTYPE
+    sample = d_in[:16 * ns].cpu().numpy().view(ENTRY_DTYPE)
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    co.process_batch(w, sample, OP(isolation=True), threads=threads)
+    t_cpu = time.perf_counter() - t0
+    cpu_b = {"value": ns / t_cpu, "unit": "entries/s", "cores": threads, "kind": "port",
+             "sample": f"first {ns} entries of the storm, oracle/mpsf_oracle.c"}
     del d_in, bufs
     torch.cuda.empty_cache()
     return {"workload": f"c3: 48 clients x 32 ranges x 8192 pages, {n} replayable entries, {u} unique "
@@ -396,7 +414,7 @@ def bench_storm(args, eng, hbm_peak, flush):
             "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
                          "frac": ach / hbm_peak, "alg_bytes_per_step": B},
             "kernels": {k: round(v[1] / max(v[0], 1), 5) for k, v in sorted(prof.items())},
-            "n_dedup": nd, "n_cancel": nc, "dedup_exact": bool(ok)}
+            "n_dedup": nd, "n_cancel": nc, "dedup_exact": bool(ok), "cpu_baseline": cpu_b}
 
 
 def bench_translate(args, eng, hbm_peak, flush, w):
@@ -417,7 +435,9 @@ def bench_translate(args, eng, hbm_peak, flush, w):
     for _ in range(3):
         eng.translate_device(d_acc, n, d_hit, d_f, d_fi, d_pi)
     s = eng.translate_summary()
+    t0 = time.perf_counter()
     want = translate_batch_np(w, acc)
+    t_cpu = time.perf_counter() - t0
     nm, npop = int(s.n_miss), int(s.n_populated)
     exact = (np.array_equal(d_hit.cpu().numpy(), want.hit) and
              np.array_equal(d_fi[:4 * nm].cpu().numpy().view(np.uint32), want.fault_idx) and
@@ -439,6 +459,9 @@ def bench_translate(args, eng, hbm_peak, flush, w):
     return {"workload": f"{n} accesses (resolve_va) on the c2 world, 10 % prefetches, 2 % wild",
             "value": n / (ms / 1e3), "unit": "accesses/s", "ms_per_step": ms, "steps": steps,
             "n_miss": nm, "n_populated": npop, "bit_exact_vs_oracle": bool(exact),
+            "cpu_baseline": {"value": n / t_cpu, "unit": "accesses/s", "cores": 1, "kind": "port",
+                             "sample": f"the same {n} accesses, oracle/seq_oracle.translate_batch_np (numpy, "
+                                       f"one thread)"},
             "roofline": {"bound": "hbm", "achieved": B / (ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                          "frac": B / (ms / 1e3) / 1e9 / hbm_peak, "alg_bytes": B}}
 
@@ -518,7 +541,9 @@ def bench_fold(args, eng, hbm_peak, flush):
     out = alloc_fold_outputs(S, len(blocks), len(tokens))
     for _ in range(3):
         s = eng.fold_device(S, R, *d[:6], len(blocks), d[6], len(tokens), out)
+    t0 = time.perf_counter()
     want = fold_snapshots_np(req, seq, nblk, ntok, prog, done, blocks, tokens)
+    t_cpu = time.perf_counter() - t0
     r, nb, nt = int(s.n_requests), int(s.n_blocks), int(s.n_tokens)
     exact = (r == len(want.order) and
              np.array_equal(out["order"][:4 * r].cpu().numpy().view(np.uint32), want.order) and
@@ -546,6 +571,9 @@ def bench_fold(args, eng, hbm_peak, flush):
     return {"workload": f"{S} snapshots, {R} requests, decode-step deltas (fold)",
             "value": S / (ms / 1e3), "unit": "snapshots/s", "ms_per_step": ms, "steps": steps,
             "n_requests": r, "n_blocks": nb, "n_tokens": nt, "bit_exact_vs_oracle": bool(exact),
+            "cpu_baseline": {"value": S / t_cpu, "unit": "snapshots/s", "cores": 1, "kind": "port",
+                             "sample": f"the same {S} snapshots, oracle/seq_oracle.fold_snapshots_np (numpy, "
+                                       f"one thread)"},
             "roofline": {"bound": "hbm", "achieved": B / (ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                          "frac": B / (ms / 1e3) / 1e9 / hbm_peak, "alg_bytes": B}}
 
@@ -588,12 +616,19 @@ def bench_remap(args, eng, hbm_peak, flush):
         want = remap_table(0x7F00_0000_0000, np.arange(514, 514 + 4096 * (1 << (gran - 12)), dtype=np.uint64), gran)
         ok = np.array_equal(head[:, 0].astype(np.uint64), want["va"]) and \
             np.array_equal(head[:, 1].astype(np.uint64), want["phys"])
+        # the CPU restatement on a bounded sample (100 k entries), one thread
+        ns = 100_000
+        t0 = time.perf_counter()
+        remap_table(0x7F00_0000_0000, np.arange(514, 514 + ns * (1 << (gran - 12)), dtype=np.uint64), gran)
+        t_cpu = time.perf_counter() - t0
+        cpu_b = {"value": ns * (1 << gran) / t_cpu / 1e9, "unit": "GB/s of state", "cores": 1, "kind": "port",
+                 "sample": f"{ns} entries, oracle/seq_oracle.remap_table (one thread)"}
         out[f"{1 << (gran - 10)}KiB"] = {
             "entries": e, "ms_per_step": ms, "kernel_ms": k_ms,
             "remap_GBps_of_state": state_bytes / (ms / 1e3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": B / (k_ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                          "frac": B / (k_ms / 1e3) / 1e9 / hbm_peak, "alg_bytes": B},
-            "check": "matches oracle" if ok else "MISMATCH"}
+            "check": "matches oracle" if ok else "MISMATCH", "cpu_baseline": cpu_b}
         del d_out
     return {"state": "64 GiB shared state (one allocation, 16,777,216 x 4 KiB pages)", **out}
 
