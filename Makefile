@@ -2,7 +2,7 @@
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -lineinfo -std=c++17 $(ARCH) -Xcompiler -fPIC,-O3 -Iinclude -Xptxas -v
-SRC := $(wildcard paper_2605_26461_b200/csrc/*.cu)
+SRC := $(wildcard paper_2605_26461_b200/csrc/*.cu paper_2605_26461_b200/csrc/*.cpp)
 HDR := $(wildcard paper_2605_26461_b200/csrc/*.cuh paper_2605_26461_b200/csrc/*.h) include/mpsf.h
 
 all: paper_2605_26461_b200/libmpsf.so
