@@ -953,10 +953,6 @@ constexpr uint32_t KSTAGE = WCHUNK;   // dedup keys staged per chunk by k_finali
 // the first-isolation word of its (client, page, epoch), its external range's first
 // isolation); fin_resolve turns the loaded words into the OutRecord, the cancel flag and the
 // dedup-set membership.  Wild pages (no range, no guard) look their keys up in the hashes.
-// Pass 2 per entry, in two halves so both entries of a lane issue their L2 lookups together:
-// fin_addr picks the words the verdict depends on (the dedup slot of its key, the
-// first-isolation word of its (client, page, epoch), its external range's first isolation);
-// fin_resolve turns them into the OutRecord, the cancel flag and the dedup-set membership.
 struct FinA {
   Dec d;
   uint32_t ok;
