@@ -37,7 +37,10 @@ namespace mpsf {
 
 // Streaming passes: persistent grid of 1024-thread CTAs (one per SM, shared memory holds the
 // world tables); every warp owns 64-entry chunks (two adjacent entries per lane).
-constexpr int BLOCK = 1024;
+#ifndef MPSF_BLOCK
+#define MPSF_BLOCK 1024   // threads per persistent CTA (experiments override)
+#endif
+constexpr int BLOCK = MPSF_BLOCK;
 constexpr int WARPS = BLOCK / 32;
 constexpr int QCAP = 64;                   // per-warp deferred hash-op stack (scan)
 
