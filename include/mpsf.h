@@ -212,7 +212,7 @@ int mpsf_translate_finish(mpsf_ctx* ctx, const mpsf_fault_entry* d_accesses, uin
  * d_progress_out[k] (the last snapshot's), d_done_out[k] (sticky OR).  Capacities: n_snap
  * for the per-request arrays, n_snap+1 for the offsets, n_blocks / n_tokens (the payload
  * lengths, each < 2^32) for the payloads.  Deltas reaching past the payloads: MPSF_E_ARG.
- * last_consumed_seq is the last snapshot's seq (the caller holds it).  A request id >= n_req_ids
+ * last_consumed_seq is the last snapshot's seq (the caller holds it); n_req_ids <= 2^30.  A request id >= n_req_ids
  * returns MPSF_E_BAD_ENTRY with the first such snapshot in error_index (its snapshot is not
  * folded).  Synchronous on `stream` (the summary needs the counts). */
 typedef struct {

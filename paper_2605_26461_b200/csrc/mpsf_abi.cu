@@ -1134,7 +1134,8 @@ int mpsf_fold(mpsf_ctx* c, uint64_t n_snap, uint32_t n_req_ids, const uint32_t* 
               uint64_t* d_tok_off, uint32_t* d_tokens_out, uint32_t* d_progress_out, uint8_t* d_done_out,
               mpsf_fold_summary* summary, void* stream) {
   if (!c || !summary) return MPSF_E_ARG;
-  if (n_snap >= (1ull << 31) - 1 || n_blocks >= (1ull << 32) || n_tokens >= (1ull << 32)) return MPSF_E_TOO_LARGE;
+  if (n_snap >= (1ull << 31) - 1 || n_blocks >= (1ull << 32) || n_tokens >= (1ull << 32) || n_req_ids > (1u << 30))
+    return MPSF_E_TOO_LARGE;   // (the id space sizes four u32 tables of scratch)
   if ((n_blocks && (!d_blocks || !d_blocks_out)) || (n_tokens && (!d_tokens || !d_tokens_out))) return MPSF_E_ARG;
   if (n_snap && (!d_req || !d_nblk || !d_ntok || !d_progress || !d_done || !d_order || !d_blk_off ||
                  !d_tok_off || !d_progress_out || !d_done_out))

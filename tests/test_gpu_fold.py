@@ -142,3 +142,11 @@ def test_fold_then_kv_reserve(eng):
     want = so.fold_snapshots(*a)
     want_r, want_f = so.kv_reserve(total, want.blocks)
     assert np.array_equal(reserved, want_r) and np.array_equal(free, want_f)
+
+
+def test_fold_id_space_limit(eng):
+    from paper_2605_26461_b200.errors import SimError
+    rng = np.random.default_rng(1)
+    a = snapshots(rng, 4, 10, liveness=0.0)
+    with pytest.raises(SimError):
+        eng.fold(*a, n_req_ids=(1 << 30) + 1)
