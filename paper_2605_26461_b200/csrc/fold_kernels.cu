@@ -46,20 +46,35 @@ __device__ __forceinline__ unsigned long long pack_len(uint32_t nb, uint32_t nt)
   return (unsigned long long)nb | ((unsigned long long)nt << 32);
 }
 
+// The gather kernels (rank, keys) and the stats take FI snapshots per thread (block-strided, so every load stays
+// coalesced) and issue all of their loads before the dependent gathers / atomics: one
+// snapshot per thread left them latency-bound at 10-20 % issue activity.
+constexpr int FI = 4;
+__device__ __forceinline__ uint32_t fi_index(int u) { return blockIdx.x * (blockDim.x * FI) + u * blockDim.x + threadIdx.x; }
+
 __global__ void k_fold_stats(uint32_t S, uint32_t R, const uint32_t* __restrict__ req,
                              const uint8_t* __restrict__ done, uint32_t* __restrict__ first,
                              uint32_t* __restrict__ last, uint32_t* __restrict__ rdone, FoldDev* __restrict__ dev) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= S) return;
-  const uint32_t r = req[i];
-  if (r == NO_REQ) return;
-  if (r >= R) {   // request id outside the caller's id space: reported, not folded
-    atomicMin(&dev->err, i);
-    return;
+  uint32_t r[FI];
+  uint8_t dn[FI];
+#pragma unroll
+  for (int u = 0; u < FI; ++u) {
+    const uint32_t i = fi_index(u);
+    r[u] = i < S ? req[i] : NO_REQ;
+    dn[u] = i < S ? done[i] : 0;
   }
-  atomicMin(first + r, i);
-  atomicMax(last + r, i);
-  if (done[i]) atomicOr(rdone + r, 1u);
+#pragma unroll
+  for (int u = 0; u < FI; ++u) {
+    const uint32_t i = fi_index(u);
+    if (r[u] == NO_REQ) continue;
+    if (r[u] >= R) {   // request id outside the caller's id space: reported, not folded
+      atomicMin(&dev->err, i);
+      continue;
+    }
+    atomicMin(first + r[u], i);
+    atomicMax(last + r[u], i);
+    if (dn[u]) atomicOr(rdone + r[u], 1u);
+  }
 }
 
 struct HeadFlag {           // snapshot i is its request's first
@@ -98,29 +113,50 @@ __global__ void k_fold_rank(uint32_t S, uint32_t R, const uint32_t* __restrict__
                             const uint32_t* __restrict__ head_pos, uint32_t* __restrict__ rank,
                             uint32_t* __restrict__ order, uint32_t* __restrict__ prog_out,
                             uint8_t* __restrict__ done_out, FoldDev* __restrict__ dev) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= S) return;
-  const uint32_t r = req[i];
-  const bool head = r < R && first[r] == i;
-  if (head) {
-    const uint32_t k = head_pos[i];
-    rank[r] = k;
-    order[k] = r;
-    prog_out[k] = progress[last[r]];
-    done_out[k] = rdone[r] ? 1 : 0;
+  uint32_t r[FI], f[FI];
+#pragma unroll
+  for (int u = 0; u < FI; ++u) {
+    const uint32_t i = fi_index(u);
+    r[u] = i < S ? req[i] : NO_REQ;
   }
-  if (i == S - 1) dev->n_requests = head_pos[i] + (head ? 1u : 0u);
+#pragma unroll
+  for (int u = 0; u < FI; ++u) f[u] = r[u] < R ? first[r[u]] : NO_REQ;
+#pragma unroll
+  for (int u = 0; u < FI; ++u) {
+    const uint32_t i = fi_index(u);
+    if (i >= S) break;
+    const bool head = r[u] < R && f[u] == i;
+    if (head) {
+      const uint32_t k = head_pos[i];
+      rank[r[u]] = k;
+      order[k] = r[u];
+      prog_out[k] = progress[last[r[u]]];
+      done_out[k] = rdone[r[u]] ? 1 : 0;
+    }
+    if (i == S - 1) dev->n_requests = head_pos[i] + (head ? 1u : 0u);
+  }
 }
 
 // sort keys: the request's rank; liveness-only (and rejected) snapshots key past every rank
 __global__ void k_fold_keys(uint32_t S, uint32_t R, uint32_t live_bound, const uint32_t* __restrict__ req,
                             const uint32_t* __restrict__ rank, uint32_t* __restrict__ key,
                             uint32_t* __restrict__ idx) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= S) return;
-  const uint32_t r = req[i];
-  key[i] = r < R ? rank[r] : live_bound;
-  idx[i] = i;
+  uint32_t r[FI], k[FI];
+#pragma unroll
+  for (int u = 0; u < FI; ++u) {
+    const uint32_t i = fi_index(u);
+    r[u] = i < S ? req[i] : NO_REQ;
+  }
+#pragma unroll
+  for (int u = 0; u < FI; ++u) k[u] = r[u] < R ? rank[r[u]] : live_bound;
+#pragma unroll
+  for (int u = 0; u < FI; ++u) {
+    const uint32_t i = fi_index(u);
+    if (i < S) {
+      key[i] = k[u];
+      idx[i] = i;
+    }
+  }
 }
 
 // thread per snapshot in consume order: coalesced reads of the SoA, offsets and payload
@@ -221,7 +257,7 @@ int launch_fold(uint8_t* scratch, size_t scratch_bytes, uint32_t S, uint32_t R, 
       cudaMemsetAsync(first, 0xFF, 4ull * R, st) != cudaSuccess ||
       cudaMemsetAsync(last, 0, 4ull * R, st) != cudaSuccess || cudaMemsetAsync(rdone, 0, 4ull * R, st) != cudaSuccess)
     return -1;
-  const uint32_t b = 256, g = (S + b - 1) / b;
+  const uint32_t b = 256, g = (S + b * FI - 1) / (b * FI);
   k_fold_stats<<<g, b, 0, st>>>(S, R, req, done, first, last, rdone, dev);
   thrust::counting_iterator<uint32_t> c0(0);
   size_t t = cub_bytes;
@@ -244,7 +280,7 @@ int launch_fold(uint8_t* scratch, size_t scratch_bytes, uint32_t S, uint32_t R, 
           cub_tmp, t, thrust::make_transform_iterator(c0, PackLenSorted{sidx, skey, nblk, ntok, live_bound}),
           thrust::make_permutation_iterator(dst, sidx), (int)S, st) != cudaSuccess)
     return -1;
-  k_fold_copy<<<g, b, 0, st>>>(S, R, req, nblk, ntok, first, last, rank, src, dst, blocks, tokens, n_blocks_in,
+  k_fold_copy<<<(S + b - 1) / b, b, 0, st>>>(S, R, req, nblk, ntok, first, last, rank, src, dst, blocks, tokens, n_blocks_in,
                                n_tokens_in, reinterpret_cast<unsigned long long*>(blk_off),
                                reinterpret_cast<unsigned long long*>(tok_off), blocks_out, tokens_out, dev);
   FoldDev h{};
