@@ -25,18 +25,21 @@ struct InitSegs {
   int n;
 };
 
+// Clears / fills the per-batch scratch: every thread of a 1-D grid strides over each segment
+// in turn (16-byte stores), so the large segments (hash tables, dedup slots) get the whole
+// grid rather than a slice of it.
 __global__ void k_init(InitSegs segs) {
-  const int s = blockIdx.y;
-  if (s >= segs.n) return;
-  uint32_t* p = reinterpret_cast<uint32_t*>(segs.p[s]);
-  const uint64_t w = segs.words[s];
-  const uint32_t v = segs.val[s];
-  const uint64_t w4 = w / 4;
-  uint4* p4 = reinterpret_cast<uint4*>(p);
-  const uint4 v4 = make_uint4(v, v, v, v);
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < w4; i += stride) p4[i] = v4;
-  for (uint64_t i = w4 * 4 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < w; i += stride) p[i] = v;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (uint64_t)gridDim.x * blockDim.x;
+  for (int s = 0; s < segs.n; ++s) {
+    uint32_t* p = reinterpret_cast<uint32_t*>(segs.p[s]);
+    const uint64_t w = segs.words[s];
+    const uint32_t v = segs.val[s];
+    const uint64_t w4 = w / 4;
+    uint4* p4 = reinterpret_cast<uint4*>(p);
+    const uint4 v4 = make_uint4(v, v, v, v);
+    for (uint64_t i = tid; i < w4; i += stride) p4[i] = v4;
+    for (uint64_t i = w4 * 4 + tid; i < w; i += stride) p[i] = v;
+  }
 }
 
 uint64_t next_pow2(uint64_t x) {
@@ -664,7 +667,7 @@ static int batch_init(mpsf_ctx* c, uint64_t n, const mpsf_params* p, uint64_t* d
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   c->mark_begin(st);
-  k_init<<<dim3(2 * sms, k), 256, 0, st>>>(segs);
+  k_init<<<dim3(8 * sms), 256, 0, st>>>(segs);
   c->marker().mark("k_init");
   c->phase_n = n;
   CK(cudaGetLastError());
@@ -771,7 +774,7 @@ int mpsf_translate_prefetch(mpsf_ctx* c, const mpsf_fault_entry* d_acc, uint64_t
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   c->mark_begin(st);
-  k_init<<<dim3(2 * sms, k), 256, 0, st>>>(segs);
+  k_init<<<dim3(8 * sms), 256, 0, st>>>(segs);
   c->marker().mark("k_init");
   mpsf_params p{};
   p.base_index = base_index;
