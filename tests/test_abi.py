@@ -58,3 +58,19 @@ def test_library_is_built_for_sm100a_only():
         return
     assert "sm_100a" in out.stdout
     assert "sm_90" not in out.stdout
+
+
+def test_plain_c_consumer_links_and_runs(tmp_path):
+    """The boundary is a C ABI: a C program compiled against include/mpsf.h links libmpsf.so
+    and calls the host-only entry points (version, strerror, trace rendering)."""
+    import subprocess
+    lib = _lib.LIB_PATH
+    exe = str(tmp_path / "abi_smoke")
+    subprocess.run(["gcc", "-O2", "-I", os.path.join(ROOT, "include"), os.path.join(ROOT, "tests", "c", "abi_smoke.c"),
+                    lib, "-Wl,-rpath," + os.path.dirname(lib), "-o", exe], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True)
+    assert out.returncode == 0, (out.returncode, out.stderr)
+    lines = out.stdout.splitlines()
+    assert lines[0] == "t=42 who=c1.sm kind=fault_raised scenario=mmu.oob.sm va=4096 access=write engine=sm"
+    assert "t=42 who=uvm kind=isolate_begin mechanism=M1 scenario=mmu.oob.sm pid=c1 latency_us=131" in lines
+    assert "t=42 who=uvm kind=parse_fatal scenario=parse.channel_state" in lines
