@@ -337,3 +337,36 @@ def test_maximum_batch_size_properties(eng):
         eng.process_device(d_in, n + 1, p, bufs)
     del d_in, bufs, out, verdict, didx
     torch.cuda.empty_cache()
+
+
+def test_wild_page_hash_overflow_retries_exactly(eng):
+    """More distinct wild-page keys than the first hash sizing expects: the batch reports
+    MPSF_E_OVERFLOW, the tables grow and the rerun is exact (host form, asynchronous form and
+    device form)."""
+    from oracle import c_oracle as co
+    from paper_2605_26461_b200.engine import alloc_host_outputs
+    w, _ = synth.build_synthetic_world(4, 16, 1)
+    n = 300_000
+    e = np.zeros(n, ENTRY_DTYPE)
+    e["va"] = (np.uint64(1) << np.uint64(34)) + (np.arange(n, dtype=np.uint64) << np.uint64(12))   # no range
+    e["channel"] = (np.arange(n) % w.n_clients) * 3          # SM channels
+    e["engine"] = K.ENG_SM
+    e["access"] = K.ACC_READ
+    e["flags"] = K.ENTRY_FLAG_VALID
+    p = so.Params(isolation=True)
+    want = co.process_batch(w, e, p)
+    fresh = FaultEngine(0)                                   # fresh context: first sizing from n
+    try:
+        fresh.upload_world(w)
+        assert_same(fresh.process(e, bp(p)), want, "host")
+        fresh2 = FaultEngine(0)
+        try:
+            fresh2.upload_world(w)
+            bufs = alloc_host_outputs(n, w.n_clients, pinned=True)
+            fresh2.submit(e, bp(p), bufs, 0)
+            assert_same(fresh2.collect(0), want, "async")
+        finally:
+            fresh2.close()
+    finally:
+        fresh.close()
+    assert_same(run_device(eng, w, e, p), want, "device")
