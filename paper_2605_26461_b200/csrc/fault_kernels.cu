@@ -656,7 +656,11 @@ __device__ __forceinline__ void scan_phase(const World& W, const Scratch& S, con
     if (!ok0) e0.w = 0;                       // past the end: decodes as a skipped entry
     if (!ok1) e1.w = 0;
     scan_fast<kStaged>(W, v, S, e0, base + i0, counts, o0);
+    // entry 0's L2 pre-check loads go out before entry 1 is decoded, entry 1's right after:
+    // the decode of entry 1 and the record store cover entry 0's L2 round trip
+    const uint32_t ra0 = o0.pa ? __ldcg(o0.pa) : 0u, rd0 = o0.pd ? __ldcg(o0.pd) : 0u;
     scan_fast<kStaged>(W, v, S, e1, base + i1, counts, o1);
+    const uint32_t ra1 = o1.pa ? __ldcg(o1.pa) : 0u, rd1 = o1.pd ? __ldcg(o1.pd) : 0u;
     if (kStaged) {                                     // pass-1 records, two per lane (16 bytes)
       unsigned long long* rp = drec + i0;
       if (ok1 && (((uintptr_t)rp & 15u) == 0)) *reinterpret_cast<ulonglong2*>(rp) = make_ulonglong2(o0.rec, o1.rec);
@@ -665,9 +669,6 @@ __device__ __forceinline__ void scan_phase(const World& W, const Scratch& S, con
         if (ok1) rp[1] = o1.rec;
       }
     }
-    // the L2 pre-check loads of both entries in flight together
-    const uint32_t ra0 = o0.pa ? __ldcg(o0.pa) : 0u, rd0 = o0.pd ? __ldcg(o0.pd) : 0u;
-    const uint32_t ra1 = o1.pa ? __ldcg(o1.pa) : 0u, rd1 = o1.pd ? __ldcg(o1.pd) : 0u;
     min_g_if(o0.pa != nullptr, ra0, o0.pa, o0.va);
     min_g_if(o1.pa != nullptr, ra1, o1.pa, o1.va);
     if (!sparse) {
