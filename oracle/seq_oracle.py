@@ -638,3 +638,14 @@ def fold_snapshots_np(req, seq, nblk, ntok, progress, done, blocks, tokens) -> F
                       _seg_gather(tokens, tstart[perm], ntok[perm]).astype(np.uint32),
                       np.asarray(progress, np.uint32)[perm[ends]] if R else np.zeros(0, np.uint32),
                       (dn > 0).astype(np.uint8), int(seq[-1]) if len(req) else 0)
+
+
+def fold_as_snapshots(f: FoldResult):
+    """A fold result as one snapshot per folded request (first-appearance order), so that folds
+    of contiguous ranges of a stream compose: fold(A ++ B) == fold(snaps(fold(A)) ++
+    snaps(fold(B))) -- the merge step of a sharded fold."""
+    r = len(f.order)
+    nblk = np.diff(f.blk_off).astype(np.uint32) if r else np.zeros(0, np.uint32)
+    ntok = np.diff(f.tok_off).astype(np.uint32) if r else np.zeros(0, np.uint32)
+    return (np.asarray(f.order, np.uint32), np.zeros(r, np.uint64), nblk, ntok, np.asarray(f.progress, np.uint32),
+            np.asarray(f.done, np.uint8), np.asarray(f.blocks, np.uint32), np.asarray(f.tokens, np.uint32))

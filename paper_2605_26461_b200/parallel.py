@@ -334,6 +334,60 @@ class GpuTranslateShard:
                     pop_idx=self.pi[:4 * npop].cpu().numpy().view(np.uint32))
 
 
+# -- sharded snapshot fold (StandbyInstance.fold over a consumed stream) --
+
+def allgather_cat(t, group=None):
+    """All-gather a 1-D tensor of per-rank length; returns the concatenation in rank order."""
+    import torch
+    dist = _dist()
+    ws = dist.get_world_size(group)
+    cnt = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
+    cnts = [torch.zeros_like(cnt) for _ in range(ws)]
+    dist.all_gather(cnts, cnt, group=group)
+    sizes = [int(c.item()) for c in cnts]
+    m = max(sizes)
+    if m == 0:
+        return t[:0]
+    pad = torch.zeros(m, dtype=t.dtype, device=t.device)
+    pad[:t.numel()] = t
+    out = [torch.empty_like(pad) for _ in range(ws)]
+    dist.all_gather(out, pad, group=group)
+    return torch.cat([out[r][:sizes[r]] for r in range(ws)])
+
+
+class ShardedFold:
+    """Each rank folds a contiguous range of the consumed snapshot stream; the folds compose
+    (fold(A ++ B) == fold(snapshots(fold(A)) ++ snapshots(fold(B))), one snapshot per folded
+    request), so the ranks all-gather their folds as snapshots and fold once more.  Every
+    rank ends with the whole stream's fold.  ``fold_fn(req, seq, nblk, ntok, progress, done,
+    blocks, tokens, n_req_ids)`` returns an object with order / blk_off / blocks / tok_off /
+    tokens / progress / done / last_seq (``FaultEngine.fold`` on GPUs, the oracle on CPU)."""
+
+    def __init__(self, fold_fn, device="cpu", group=None):
+        self.fold_fn, self.device, self.group = fold_fn, device, group
+
+    def fold(self, req, seq, nblk, ntok, progress, done, blocks, tokens, n_req_ids):
+        import torch
+        local = self.fold_fn(req, seq, nblk, ntok, progress, done, blocks, tokens, n_req_ids)
+        r = len(local.order)
+        cols = [np.asarray(local.order, np.uint32),
+                (np.diff(local.blk_off) if r else np.zeros(0)).astype(np.uint32),
+                (np.diff(local.tok_off) if r else np.zeros(0)).astype(np.uint32),
+                np.asarray(local.progress, np.uint32), np.asarray(local.done, np.uint8).astype(np.uint32),
+                np.asarray(local.blocks, np.uint32), np.asarray(local.tokens, np.uint32)]
+        # int64 carriers (gloo and NCCL both gather them; values are < 2^32)
+        g = [allgather_cat(torch.from_numpy(c.astype(np.int64)).to(self.device), self.group).cpu().numpy()
+             for c in cols]
+        last = torch.tensor([int(local.last_seq) if len(req) else -1], dtype=torch.int64, device=self.device)
+        _dist().all_reduce(last, op=_dist().ReduceOp.MAX, group=self.group)
+        m = len(g[0])
+        merged = self.fold_fn(g[0].astype(np.uint32), np.zeros(m, np.uint64), g[1].astype(np.uint32),
+                              g[2].astype(np.uint32), g[3].astype(np.uint32), g[4].astype(np.uint8),
+                              g[5].astype(np.uint32), g[6].astype(np.uint32), n_req_ids)
+        merged.last_seq = max(int(last.item()), 0)
+        return merged
+
+
 def combine_verdicts_nccl(verdict: np.ndarray) -> np.ndarray:
     """Elementwise MAX of per-shard client fates (used only by the replica fallback)."""
     import torch

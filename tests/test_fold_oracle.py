@@ -90,3 +90,28 @@ def test_kv_reserve_oracle_matches_block_pool(seed):
         reserved, free = so.kv_reserve(total, ids)
         assert free.tolist() == pops
         assert reserved.tolist() == [1 if b in set(ids) else 0 for b in range(total)]
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_fold_composes_over_contiguous_ranges(seed):
+    """fold(A ++ B ++ ...) == fold(snapshots(fold(A)) ++ snapshots(fold(B)) ++ ...): the merge
+    step of the sharded fold (parallel.ShardedFold)."""
+    rnd = random.Random(1200 + seed)
+    for it in range(30):
+        snaps = random_snapshots(rnd, rnd.randint(1, 20), rnd.randint(0, 200))
+        a = to_arrays(snaps)
+        n = len(a[0])
+        k = rnd.randint(1, 4)
+        cuts = sorted([0, n] + [rnd.randint(0, n) for _ in range(k - 1)])
+        parts = []
+        for lo, hi in zip(cuts[:-1], cuts[1:]):
+            bo = int(a[2][:lo].sum()), int(a[2][:hi].sum())
+            to = int(a[3][:lo].sum()), int(a[3][:hi].sum())
+            sub = (a[0][lo:hi], a[1][lo:hi], a[2][lo:hi], a[3][lo:hi], a[4][lo:hi], a[5][lo:hi],
+                   a[6][bo[0]:bo[1]], a[7][to[0]:to[1]])
+            parts.append(so.fold_as_snapshots(so.fold_snapshots_np(*sub)))
+        merged = tuple(np.concatenate([p[j] for p in parts]) if parts else np.zeros(0) for j in range(8))
+        got = so.fold_snapshots_np(*merged)
+        want = so.fold_snapshots_np(*a)
+        for f in ("order", "blk_off", "blocks", "tok_off", "tokens", "progress", "done"):
+            assert np.array_equal(getattr(got, f), getattr(want, f)), (seed, it, f)

@@ -150,3 +150,26 @@ def test_fold_id_space_limit(eng):
     a = snapshots(rng, 4, 10, liveness=0.0)
     with pytest.raises(SimError):
         eng.fold(*a, n_req_ids=(1 << 30) + 1)
+
+
+@pytest.mark.parametrize("nshards", [2, 4])
+def test_sharded_fold_merge_on_gpu(eng, nshards):
+    """The sharded fold's two GPU steps on one device: each contiguous range folded, the
+    per-range folds (as one snapshot per request) concatenated and folded again == the whole
+    stream's fold (parallel.ShardedFold does the same with an all-gather between them)."""
+    rng = np.random.default_rng(40 + nshards)
+    a = snapshots(rng, 500, 20_000)
+    n = len(a[0])
+    cut = [n * r // nshards for r in range(nshards + 1)]
+    parts = []
+    for lo, hi in zip(cut[:-1], cut[1:]):
+        bo = int(a[2][:lo].sum()), int(a[2][:hi].sum())
+        to = int(a[3][:lo].sum()), int(a[3][:hi].sum())
+        sub = (a[0][lo:hi], a[1][lo:hi], a[2][lo:hi], a[3][lo:hi], a[4][lo:hi], a[5][lo:hi],
+               a[6][bo[0]:bo[1]], a[7][to[0]:to[1]])
+        parts.append(so.fold_as_snapshots(eng.fold(*sub, n_req_ids=500)))
+    merged = tuple(np.concatenate([p[j] for p in parts]) for j in range(8))
+    got = eng.fold(*merged, n_req_ids=500)
+    want = so.fold_snapshots(*a)
+    for f in ("order", "blk_off", "blocks", "tok_off", "tokens", "progress", "done"):
+        assert np.array_equal(getattr(got, f), getattr(want, f)), f

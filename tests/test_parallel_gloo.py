@@ -206,3 +206,66 @@ def test_sharded_translation_gloo_equals_whole_stream(ws):
         assert np.array_equal(np.concatenate([p["hit"] for p in parts]), want.hit), seed
         assert np.array_equal(np.concatenate([p["fault_idx"] for p in parts]), want.fault_idx), seed
         assert np.array_equal(np.concatenate([p["pop_idx"] for p in parts]), want.pop_idx), seed
+
+
+# -- sharded snapshot fold (all-gather of the per-rank folds, then one merge fold) -------------
+
+def fold_case(seed):
+    rnd = np.random.default_rng(seed)
+    S = int(rnd.integers(0, 400))
+    R = int(rnd.integers(1, 30))
+    req = rnd.integers(0, R, S, dtype=np.uint32)
+    req[rnd.random(S) < 0.1] = so.NO_REQ
+    seq = np.arange(1, S + 1, dtype=np.uint64)
+    nblk = rnd.integers(0, 4, S, dtype=np.uint32)
+    ntok = rnd.integers(0, 6, S, dtype=np.uint32)
+    prog = rnd.integers(0, 1000, S, dtype=np.uint32)
+    done = (rnd.random(S) < 0.1).astype(np.uint8)
+    blocks = rnd.integers(0, 1 << 20, int(nblk.sum()), dtype=np.uint32)
+    tokens = rnd.integers(0, 50000, int(ntok.sum()), dtype=np.uint32)
+    return (req, seq, nblk, ntok, prog, done, blocks, tokens), R
+
+
+def shard_of(a, lo, hi):
+    bo = int(a[2][:lo].sum()), int(a[2][:hi].sum())
+    to = int(a[3][:lo].sum()), int(a[3][:hi].sum())
+    return (a[0][lo:hi], a[1][lo:hi], a[2][lo:hi], a[3][lo:hi], a[4][lo:hi], a[5][lo:hi],
+            a[6][bo[0]:bo[1]], a[7][to[0]:to[1]])
+
+
+def _fold_worker(rank, ws, port, seeds, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    import pickle
+    from paper_2605_26461_b200.parallel import ShardedFold
+    sf = ShardedFold(lambda *a: so.fold_snapshots_np(*a[:8]))
+    results = {}
+    for seed in seeds:
+        a, R = fold_case(seed)
+        n = len(a[0])
+        cut = [n * r // ws for r in range(ws + 1)]
+        f = sf.fold(*shard_of(a, cut[rank], cut[rank + 1]), R)
+        results[seed] = {k: getattr(f, k) for k in ("order", "blk_off", "blocks", "tok_off", "tokens", "progress",
+                                                    "done", "last_seq")}
+    with open(os.path.join(outdir, f"f{rank}.pkl"), "wb") as fh:
+        pickle.dump(results, fh)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ws", [2, 3])
+def test_sharded_fold_gloo_equals_whole_stream(ws):
+    import pickle
+    seeds = list(range(300, 340))
+    with tempfile.TemporaryDirectory() as d:
+        mp.start_processes(_fold_worker, args=(ws, _free_port(), seeds, d), nprocs=ws, start_method="fork")
+        per_rank = [pickle.load(open(os.path.join(d, f"f{r}.pkl"), "rb")) for r in range(ws)]
+    for seed in seeds:
+        a, R = fold_case(seed)
+        want = so.fold_snapshots(*a)
+        for r in range(ws):
+            got = per_rank[r][seed]
+            for k in ("order", "blk_off", "blocks", "tok_off", "tokens", "progress", "done"):
+                assert np.array_equal(got[k], getattr(want, k)), (seed, r, k)
+            assert got["last_seq"] == want.last_seq, seed
