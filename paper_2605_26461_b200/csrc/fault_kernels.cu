@@ -1152,12 +1152,24 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const
 // thread per chunk: a block-wide scan of the chunks' popcounts gives every chunk its offsets,
 // then each thread writes its own chunk's entries (the L2 merges the short runs).  `in` /
 // `out` / the masks cover the whole batch (nq chunks).
+// The summary usually lives in mapped pinned host memory: one thread gathers it in registers
+// and writes it with 16-byte stores (no read-back of host memory -- each one is a PCIe round
+// trip).
 __device__ __forceinline__ void write_summary(const Scratch& S, unsigned long long tot, DevSummary* out) {
-  for (int i = 0; i < C_NCTRL; ++i) out->ctrl[i] = __ldcg(S.ctrl + i);
-  out->err_idx = __ldcg(S.err_idx);
-  const bool err = out->ctrl[C_ERR] != 0;
-  out->n_cancel = err ? 0 : (tot & 0xFFFFFFFFull);
-  out->n_dedup = err ? 0 : (tot >> 32);
+  if (MPSF_ABLATE & 32768) return;
+  static_assert(sizeof(DevSummary) == 4 * C_NCTRL + 24 && C_NCTRL % 4 == 0, "summary layout");
+  uint32_t c[C_NCTRL];
+#pragma unroll
+  for (int i = 0; i < C_NCTRL; ++i) c[i] = __ldcg(S.ctrl + i);
+  const unsigned long long e = __ldcg(S.err_idx);
+  const bool err = c[C_ERR] != 0;
+  uint4* o4 = reinterpret_cast<uint4*>(out);
+#pragma unroll
+  for (int i = 0; i < C_NCTRL / 4; ++i) o4[i] = make_uint4(c[4 * i], c[4 * i + 1], c[4 * i + 2], c[4 * i + 3]);
+  unsigned long long* t = reinterpret_cast<unsigned long long*>(out->ctrl + C_NCTRL);
+  t[0] = e;
+  t[1] = err ? 0ull : (tot & 0xFFFFFFFFull);
+  t[2] = err ? 0ull : (tot >> 32);
 }
 
 __global__ void __launch_bounds__(SEG_CHUNKS) k_lists(Scratch S, const mpsf_fault_entry* __restrict__ in,
@@ -1298,13 +1310,7 @@ __global__ void k_summary(const Scratch S, uint64_t nseg, DevSummary* out) {
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
   if ((threadIdx.x & 31) == 0 && acc) atomicAdd(&s_tot, acc);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < C_NCTRL; ++i) out->ctrl[i] = S.ctrl[i];
-    out->err_idx = *S.err_idx;
-    const bool err = S.ctrl[C_ERR] != 0;
-    out->n_cancel = err ? 0 : (s_tot & 0xFFFFFFFFull);
-    out->n_dedup = err ? 0 : (s_tot >> 32);
-  }
+  if (threadIdx.x == 0) write_summary(S, s_tot, out);
 }
 
 // ---- batched translation kernels ------------------------------------------------------------
@@ -1563,7 +1569,7 @@ static void launch_pdl(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStr
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[0].val.programmaticStreamSerializationAllowed = (MPSF_ABLATE & 65536) ? 0 : 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, k, args...);
