@@ -951,6 +951,9 @@ __global__ void k_resolve2(World W, Scratch S, Params P) {
 // scans its own chunks' popcounts -- no serial look-back between tiles.
 constexpr uint32_t SEG_CHUNKS = 256;
 constexpr uint32_t KSTAGE = WCHUNK;   // dedup keys staged per chunk by k_finalize, in index order
+#ifndef LIST_KEYS
+#define LIST_KEYS 8                    // dedup keys in flight per lane in k_lists
+#endif
 
 // Pass 2 per entry, in two halves so both entries of a lane issue their L2 lookups together:
 // fin_addr decodes and picks the words the verdict depends on (the dedup slot of its key,
@@ -1237,10 +1240,13 @@ __global__ void __launch_bounds__(SEG_CHUNKS) k_lists(Scratch S, const mpsf_faul
     }
   }
   // dedup set: the warp's representatives occupy consecutive positions from its first chunk's
-  // offset on; lane l writes flat ranks l, l + 32, ... (coalesced), finding each rank's chunk by
-  // a shuffle search over the chunks' exclusive rep counts.  Keys were staged by k_finalize.
+  // offset on.  Each lane lists its chunk's representatives (chunk << 6 | entry) at their flat
+  // ranks in a per-warp shared table, then lane l writes ranks l, l + 32, ... (coalesced) with
+  // one table read each.  Keys were staged by k_finalize.
   {
-    const unsigned long long dm_l = (MPSF_ABLATE & 1024) ? 0ull : mk.y;
+    __shared__ uint16_t s_code[SEG_CHUNKS / 32][32 * WCHUNK];   // per warp: its 32 chunks
+    uint16_t* code = s_code[warp];
+    unsigned long long dm_l = (MPSF_ABLATE & 1024) ? 0ull : mk.y;
     const uint32_t cnt = (uint32_t)__popcll(dm_l);
     uint32_t inc = cnt;
 #pragma unroll
@@ -1248,33 +1254,25 @@ __global__ void __launch_bounds__(SEG_CHUNKS) k_lists(Scratch S, const mpsf_faul
       const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, inc, o);
       if (lane >= o) inc += u;
     }
-    const uint32_t exc = inc - cnt;
     const uint32_t R = __shfl_sync(0xFFFFFFFFu, inc, 31);
     const uint64_t pd0 = __shfl_sync(0xFFFFFFFFu, pd, 0);
     const uint64_t q0w = q - lane;
-    for (uint32_t r0 = 0; r0 < R; r0 += 128) {
-      unsigned long long key[4];
-      uint32_t gix[4];
+    for (uint32_t pos = inc - cnt; dm_l; dm_l &= dm_l - 1)
+      code[pos++] = (uint16_t)((lane << 6) | (uint32_t)(__ffsll((long long)dm_l) - 1));
+    __syncwarp();
+    for (uint32_t r0 = 0; r0 < R; r0 += 32 * LIST_KEYS) {
+      unsigned long long key[LIST_KEYS];
+      uint32_t gix[LIST_KEYS];
 #pragma unroll
-      for (int h = 0; h < 4; ++h) {
+      for (int h = 0; h < LIST_KEYS; ++h) {
         const uint32_t f = r0 + 32 * h + lane;
-        // largest j with exc_j <= f (exc is non-decreasing over lanes)
-        uint32_t j = 0;
-#pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-          const uint32_t e = __shfl_sync(0xFFFFFFFFu, exc, j + step);
-          if (e <= f) j += step;
-        }
-        const uint32_t ej = __shfl_sync(0xFFFFFFFFu, exc, j);
-        const unsigned long long dmj = __shfl_sync(0xFFFFFFFFu, dm_l, j);
-        const uint32_t k = f - ej;
-        const uint32_t lo = (uint32_t)dmj, clo = __popc(lo);
-        const uint32_t bit = k < clo ? __fns(lo, 0, (int)k + 1) : 32 + __fns((uint32_t)(dmj >> 32), 0, (int)(k - clo) + 1);
-        key[h] = f < R ? __ldcg(S.dstage + (q0w + j) * KSTAGE + bit) : 0ull;
-        gix[h] = (uint32_t)(base_index + (q0w + j) * WCHUNK) + bit;
+        const uint32_t c = f < R ? code[f] : 0u;
+        const uint64_t qj = q0w + (c >> 6);
+        key[h] = f < R ? __ldcg(S.dstage + qj * KSTAGE + (c & 63u)) : 0ull;
+        gix[h] = (uint32_t)(base_index + qj * WCHUNK) + (c & 63u);
       }
 #pragma unroll
-      for (int h = 0; h < 4; ++h) {
+      for (int h = 0; h < LIST_KEYS; ++h) {
         const uint32_t f = r0 + 32 * h + lane;
         if (f < R) {
           dkeys[pd0 + f] = key[h];
