@@ -119,3 +119,19 @@ def test_sharded_translation_vs_whole_stream(nshards):
         assert np.array_equal(np.concatenate([p["hit"] for p in parts]), want.hit), it
         assert np.array_equal(np.concatenate([p["fault_idx"] for p in parts]), want.fault_idx), it
         assert np.array_equal(np.concatenate([p["pop_idx"] for p in parts]), want.pop_idx), it
+
+
+def test_translate_phase_misuse(eng):
+    """mpsf_translate_finish must follow mpsf_translate_prefetch of the same batch size."""
+    import torch
+    from paper_2605_26461_b200.errors import SimError
+    from paper_2605_26461_b200.parallel import GpuTranslateShard
+    w, _ = synth.build_synthetic_world(4, 16, 1)
+    eng.upload_world(w)
+    acc = synth.generate_access_stream(w, 1000, seed=3)
+    d = torch.from_numpy(acc.view(np.uint8).copy()).cuda()
+    sh = GpuTranslateShard(eng, d, 1000, 0)
+    sh.prefetch()
+    sh.n = 999                                                   # a different batch than the prefetch's
+    with pytest.raises(SimError):
+        sh.finish()
