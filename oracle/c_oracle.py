@@ -22,7 +22,7 @@ _lib = None
 
 def build() -> str:
     root = os.path.dirname(HERE)
-    subprocess.run(["gcc", "-O3", "-march=native", "-fPIC", "-shared", "-pthread", "-I",
+    subprocess.run(["gcc", "-O3", "-march=x86-64-v3", "-fPIC", "-shared", "-pthread", "-I",
                     os.path.join(root, "include"), "-o", LIB, os.path.join(HERE, "mpsf_oracle.c")],
                    check=True)
     return LIB
