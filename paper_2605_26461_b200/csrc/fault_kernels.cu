@@ -7,22 +7,27 @@
 // computed with the parallel recipe C9 of SURVEY.md Appendix C -- every cross-record
 // dependency is a first-in-group minimum over the drain key:
 //
-//   k_scan      pass 1: decode, attribute (binary search of the smem interval table),
-//               classify (smem LUT of faults.classify), per-block (client, scenario) counts,
-//               group minima (fatal TSG teardowns, traps, first isolation per external
-//               range / unmapped page / client, first record per dedup key)
+//   k_init      clear the per-batch scratch (dedup slots, minima, hash tables, counters)
+//   k_scan      pass 1: decode (channel word, skip-table attribution in the smem interval
+//               table, one smem LUT word = faults.classify), per-block (client, scenario)
+//               counts, group minima (fatal TSG teardowns, traps, first isolation per
+//               external range / guard page / client, first record per dedup key; wild
+//               pages through L2 hash tables), and an 8-byte pass-1 record per entry
 //   k_resolve   block 0: per-client release keys, kill thresholds, fates, fast/general
-//               path; blocks 1..: reduce the per-block count partials
+//               path, the per-client decision table
 //   k_general   [general path: a client with isolation-eligible records is released
 //               inside the batch, or m2 <= benign] release-aware first-isolation keys
 //               (rule C3 epochs) and exact per-client mechanism minima
 //   k_resolve2  [general path] kill thresholds from the exact minima
-//   k_finalize  pass 2: dup / mechanism / cancel per entry, the 8-byte OutRecord, and the
-//               cancel list + dedup set compacted in index order (decoupled look-back)
+//   k_finalize  pass 2 over the records: dup / mechanism / cancel per entry, the 8-byte
+//               OutRecord, per-chunk ballot masks and segment counters, staged dedup keys
+//   k_lists     the cancel list and the dedup set in index order (block per segment)
 //
-// Every pass streams the entries with TMA bulk copies (cp.async.bulk, L2 evict-first)
-// into a double-buffered shared-memory tile, completion tracked by mbarriers, so the
-// per-entry loop is a small rolled loop over shared memory while the next tile lands.
+// The streaming passes are persistent grids of 1024-thread CTAs with the world tables at
+// fixed shared-memory offsets; each lane reads two adjacent entries with one 32-byte
+// non-allocating load (or two 8-byte records with one 16-byte load) and requests the next
+// chunk before working on the current one.  Kernel boundaries use programmatic dependent
+// launch.  DESIGN.md §4 has the measured bound of each.
 #include <cuda_runtime.h>
 #include <stdint.h>
 

@@ -2,8 +2,9 @@
 //
 // Reference semantics restated here (paths relative to the reference's pkg/src/mpssim/):
 //   classify()   -- faults.classify, faults.py:134-171 (priority order 145-171)
-//   attribute()  -- MemoryModel.range_at, memory.py:233-237, as a binary search over the
-//                   (client, base)-sorted interval table instead of a linear scan
+//   range_at     -- MemoryModel.range_at, memory.py:233-237: the (client, base)-sorted,
+//                   page-granular interval table plus per-client skip tables (World below),
+//                   used by decode_fast in fault_kernels.cu instead of a linear scan
 //   scenario predicates -- the 28-row table faults.py:79-108 (ids = list position)
 #pragma once
 
