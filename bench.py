@@ -103,8 +103,15 @@ def setup_dist(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # test hook: MPSF_BENCH_ONE_GPU=1 runs every rank on cuda:0 over gloo (exercises the
+        # multi-rank path on a single-GPU box; NCCL refuses two ranks on one device)
+        if os.environ.get("MPSF_BENCH_ONE_GPU") == "1":
+            local = 0
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         if torch.cuda.is_available():
             torch.cuda.set_device(local)

@@ -94,7 +94,22 @@ class ShardedFaultPath:
         ks, vs = allgather_ragged(keys, vals, self.group)
         self.a.hash_merge(which, ks, vs)
 
-    def process(self, params: BatchParams):
+    def process(self, params: BatchParams, max_attempts: int = 6):
+        """One sharded batch.  A wild-page hash table that fills up on any rank -- in its own
+        inserts or in the merge of the other ranks' keys -- makes every rank run the batch
+        again (the full tables have grown); the ranks agree on that with a MAX all-reduce."""
+        import torch
+        from .errors import HashOverflow
+        for _ in range(max_attempts):
+            res = self._once(params)
+            ovf = torch.tensor([1 if res is None else 0], dtype=torch.int32, device=self.a.counts_tensor().device)
+            if _dist().is_initialized():
+                _dist().all_reduce(ovf, op=_dist().ReduceOp.MAX, group=self.group)
+            if int(ovf.item()) == 0:
+                return res
+        raise HashOverflow("wild-page hash tables kept overflowing")
+
+    def _once(self, params: BatchParams):
         a = self.a
         a.scan(params)
         self._combine(1)
@@ -147,7 +162,15 @@ class LocalShardGroup:
         for a in self.ads:
             a.hash_merge(which, ks, vs)
 
-    def process(self, params_list):
+    def process(self, params_list, max_attempts: int = 6):
+        from .errors import HashOverflow
+        for _ in range(max_attempts):
+            res = self._once(params_list)
+            if all(r is not None for r in res):
+                return res
+        raise HashOverflow("wild-page hash tables kept overflowing")
+
+    def _once(self, params_list):
         for a, p in zip(self.ads, params_list):
             a.scan(p)
         self._combine(1)
@@ -256,7 +279,12 @@ class GpuShard:
         return self.bufs.counts[:8 * K.N_SCENARIOS * self.eng.world.n_clients].view(__import__("torch").int64)
 
     def result(self):
-        s = self.eng.summary()
+        """The shard's results, or None when its hash tables overflowed (they have grown)."""
+        from .errors import HashOverflow
+        try:
+            s = self.eng.summary()
+        except HashOverflow:
+            return None
         return self.bufs.fetch(self.n, self.eng.world.n_clients, int(s.n_dedup), int(s.n_cancel), int(s.path))
 
 
