@@ -11,6 +11,7 @@ import torch
 from paper_2605_26461_b200 import synth
 from paper_2605_26461_b200.engine import BatchParams, DeviceBuffers, FaultEngine
 from paper_2605_26461_b200.parallel import GpuShard, LocalShardGroup
+from paper_2605_26461_b200.world import ENTRY_DTYPE
 
 from oracle import c_oracle as co
 from oracle import seq_oracle as so
@@ -75,3 +76,18 @@ def test_sharded_storm_slice():
     trace = synth.generate_storm(w, 200_000, 20_000, 3)
     bp = BatchParams(isolation=True)
     check(w, trace, bp, run_sharded(w, trace, bp, 2))
+
+
+@pytest.mark.parametrize("nshards", [2, 3])
+def test_sharded_wild_hash_overflow_reruns(nshards):
+    """Distinct wild-page keys beyond the first hash sizing, split over shards: the merge of
+    the other shards' keys overflows the tables, every shard reruns the batch with grown
+    tables, and the result is exact."""
+    w, _ = synth.build_synthetic_world(4, 16, 1)
+    n = 240_000
+    e = np.zeros(n, ENTRY_DTYPE)
+    e["va"] = (np.uint64(1) << np.uint64(34)) + (np.arange(n, dtype=np.uint64) << np.uint64(12))
+    e["channel"] = (np.arange(n) % w.n_clients) * 3
+    e["flags"] = 1
+    bp = BatchParams(isolation=True)
+    check(w, e, bp, run_sharded(w, e, bp, nshards))
