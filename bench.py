@@ -301,27 +301,29 @@ def run_mine(args):
         if ws == 1:
             # a stream of batches through the asynchronous form: two slots in flight, so the
             # H2D of batch k+1 overlaps the passes and the D2H of batch k
-            hb2 = [hb, alloc_host_outputs(n, w.n_clients, pinned=True)]
+            # (three slots: the H2D of batch k+3 waits only for batch k's copies to land)
+            NS = 3
+            hb2 = [hb] + [alloc_host_outputs(n, w.n_clients, pinned=True) for _ in range(NS - 1)]
 
             def stream(nb):
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
                 r = None
                 for k in range(nb):
-                    if k >= 2:
-                        eng.collect(k % 2)
-                    eng.submit(pinned, params, hb2[k % 2], k % 2)
-                for k in range(max(0, nb - 2), nb):
-                    r = eng.collect(k % 2)
+                    if k >= NS:
+                        eng.collect(k % NS)
+                    eng.submit(pinned, params, hb2[k % NS], k % NS)
+                for k in range(max(0, nb - NS), nb):
+                    r = eng.collect(k % NS)
                 return (time.perf_counter() - t0) / nb, r
 
-            stream(4)                                   # warm the two slots
+            stream(2 * NS)                              # warm the slots
             # best of two timed streams: a host hiccup in one pass does not decide the number
-            (t_a, r2), (t_b, _) = stream(e2e_steps), stream(e2e_steps)
+            (t_a, r2), (t_b, _) = stream(max(e2e_steps, 2 * NS)), stream(max(e2e_steps, 2 * NS))
             t_pipe = min(t_a, t_b)
             if t_pipe < t_e2e:
                 t_e2e = t_pipe
-                e2e_mode = "stream of batches, two in flight (mpsf_submit_host / mpsf_collect_host)"
+                e2e_mode = "stream of batches, three in flight (mpsf_submit_host / mpsf_collect_host)"
         d2h = 8 * n + 4 * w.n_clients + 8 * 28 * w.n_clients + 12 * len(r2.dedup_keys) + 4 * len(r2.cancel)
         e2e = {"value": ws * n / t_e2e, "unit": "entries/s", "h2d_bytes_per_step": 16 * n,
                "d2h_bytes_per_step": d2h, "ms_per_step": round(t_e2e * 1e3, 3),

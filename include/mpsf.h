@@ -158,12 +158,13 @@ int mpsf_remap_blocks(mpsf_ctx* ctx, uint64_t va_base, const uint64_t* d_phys_pa
                       mpsf_remap_entry* d_out, void* stream);
 
 /* Asynchronous host-buffer form (the same work as mpsf_process_host): mpsf_submit_host
- * enqueues one batch into slot 0 or 1 and returns; mpsf_collect_host waits for that slot and
+ * enqueues one batch into slot 0 .. MPSF_HOST_SLOTS-1 and returns; mpsf_collect_host waits for that slot and
  * reports it (and re-runs the batch if the wild-page hash overflowed).  Batches execute in
  * submission order; the H2D of one overlaps the passes and the D2H of the other.  Output
  * buffers must stay valid until collected; with pinned (device-accessible) list buffers the
  * lists are written by the device without a host round trip.  mpsf_process_host = submit
  * (slot 0) + collect. */
+#define MPSF_HOST_SLOTS 3   /* batches the asynchronous host form can hold in flight */
 int mpsf_submit_host(mpsf_ctx* ctx, int slot, const mpsf_fault_entry* h_entries, uint64_t n,
                      const mpsf_params* params, mpsf_out_record* h_out,
                      mpsf_client_verdict* h_verdict, uint64_t* h_counts, uint64_t* h_dedup_keys,

@@ -57,7 +57,7 @@ constexpr int kMaxChunks = 8;
 
 }  // namespace
 
-constexpr int kSlots = 2;
+constexpr int kSlots = MPSF_HOST_SLOTS;
 
 // One in-flight batch of the asynchronous host-buffer form.
 struct HostSlot {
