@@ -342,7 +342,7 @@ __device__ __forceinline__ void ld_pair(const mpsf_fault_entry* in, uint32_t n, 
                                         uint4& b) {
   const uint4* p = reinterpret_cast<const uint4*>(in) + i0;
   if (a32 && i0 + 1 < n) {
-    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+    asm("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
                  : "l"(p));
   } else {
@@ -1018,7 +1018,7 @@ __device__ __forceinline__ void fin_resolve(const World& W, const View& v, const
 // k_lists after the finalize stream has passed through the L2.
 __device__ __forceinline__ void st_keep(unsigned long long* p, unsigned long long v) {
   uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));   // pure: hoisted / shared
   asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
 }
 
