@@ -96,11 +96,36 @@ def alg_bytes(n, n_dedup, n_cancel):
 
 # ------------------------------------------------------------------------------------------
 
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch(args) -> int:
+    """``--gpus N`` (N > 1) without a torchrun environment: re-exec this script under
+    ``torch.distributed.run`` with N ranks on this node (rendezvous on 127.0.0.1); rank 0 prints
+    the JSON line to the inherited stdout."""
+    # torchrun's own parser takes abbreviations of its options (``--n`` would match ``--nnodes``):
+    # hand the script its options in their unabbreviated spellings
+    fwd = ["--entries" if a == "--n" else a for a in sys.argv[1:]]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *fwd]
+    print("+ " + " ".join(cmd), file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
 def setup_dist(args):
     import torch
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws} (launch with torchrun "
+                         f"--nproc-per-node {args.gpus}, or without torchrun to self-launch)")
     if ws > 1:
         import torch.distributed as dist
         # test hook: MPSF_BENCH_ONE_GPU=1 runs every rank on cuda:0 over gloo (exercises the
@@ -110,6 +135,8 @@ def setup_dist(args):
             torch.cuda.set_device(0)
             dist.init_process_group("gloo")
         else:
+            if torch.cuda.device_count() < ws:
+                raise SystemExit(f"bench.py: {ws} ranks but {torch.cuda.device_count()} visible GPUs")
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
@@ -132,6 +159,42 @@ def max_over_ranks(ws, x):
     t = torch.tensor([x], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def gather_arrays(ws, arr, dev):
+    """All-gather one numpy array of per-rank length (any dtype); the rank-ordered list."""
+    import torch
+    import torch.distributed as dist
+    raw = np.ascontiguousarray(arr).view(np.uint8).reshape(-1)
+    t = torch.from_numpy(raw.copy()).to(dev) if raw.size else torch.zeros(0, dtype=torch.uint8, device=dev)
+    cnt = torch.tensor([t.numel()], dtype=torch.int64, device=dev)
+    cnts = [torch.zeros_like(cnt) for _ in range(ws)]
+    dist.all_gather(cnts, cnt)
+    sizes = [int(c.item()) for c in cnts]
+    m = max(sizes)
+    pad = torch.zeros(max(m, 1), dtype=torch.uint8, device=dev)
+    pad[:t.numel()] = t
+    outs = [torch.empty_like(pad) for _ in range(ws)]
+    dist.all_gather(outs, pad)
+    return [outs[r][:sizes[r]].cpu().numpy().view(arr.dtype) for r in range(ws)]
+
+
+def check_gathered(ws, rank, dev, w, traces, res, threads, label):
+    """Rank 0: the concatenated per-rank outputs of a sharded batch against the C oracle on the
+    whole (global-index) trace; every rank must hold the same per-client fates and counts."""
+    from oracle import c_oracle as co
+    from oracle.seq_oracle import Params as OP
+    parts = {f: gather_arrays(ws, getattr(res, f), dev) for f in
+             ("out", "verdict", "counts", "dedup_keys", "dedup_idx", "cancel")}
+    if rank != 0:
+        return None
+    want = co.process_batch(w, np.concatenate(traces), OP(isolation=True), threads=threads)
+    same = all(np.array_equal(np.concatenate(parts[f]), getattr(want, f))
+               for f in ("out", "dedup_keys", "dedup_idx", "cancel"))
+    same = same and all(np.array_equal(v, want.verdict.reshape(-1)) for v in parts["verdict"])
+    same = same and all(np.array_equal(c, want.counts.reshape(-1)) for c in parts["counts"])
+    return (f"bit-exact vs C oracle ({label}, {ws} shards concatenated)" if same
+            else f"MISMATCH vs C oracle ({label})")
 
 
 def time_resident(eng, d_in, n, params, bufs, steps, flush, step_fn=None):
@@ -169,6 +232,32 @@ def time_resident(eng, d_in, n, params, bufs, steps, flush, step_fn=None):
     return total, s, prof
 
 
+def reference_cpu_path(cfg, trace, device_out=None, n_prefix=100_000):
+    """The reference's OWN per-entry path (channel_to_pid + faults.classify, pipeline.py:103-104,
+    faults.py:134-171) over a prefix of the trace, on 1 core and on every host core, when the
+    reference is installed (baseline/_ref, tools/install_reference.sh).  With the device's
+    OutRecords it also checks the device scenario of every entry of the prefix against it."""
+    try:
+        from oracle import refpath
+        if not refpath.reference_available():
+            return {"unavailable": "reference package not installed (tools/install_reference.sh)"}
+        from paper_2605_26461_b200 import constants as K
+        cores = os.cpu_count() or 1
+        pre = trace[:n_prefix]
+        r = refpath.reference_classify(cfg["clients"], cfg["pages"], cfg["seed"], pre, procs=cores)
+        d = {"value_1core": r["n"] / r["t1"], "value_all_cores": (r["n"] / r["tN"]) if r["tN"] else None,
+             "unit": "entries/s", "cores": cores, "kind": "reference",
+             "sample": f"first {len(pre)} entries ({r['n']} translation entries): mpssim channel_to_pid + "
+                       f"faults.classify, 1 core and {cores} forked workers"}
+        if device_out is not None:
+            names = [s.sid for s in K.SCENARIOS]
+            got = [names[x] for x in device_out["scenario"][:len(pre)][r["mask"]]]
+            d["device_scenarios_match_reference"] = got == r["sids"]
+        return d
+    except Exception as exc:        # the baseline is reported, never the thing measured
+        return {"unavailable": f"{type(exc).__name__}: {exc}"}
+
+
 def run_mine(args):
     import torch
     from paper_2605_26461_b200 import synth
@@ -181,41 +270,52 @@ def run_mine(args):
     hbm_peak, peak_src = peaks()
     cfg = synth.CONFIGS[args.workload]
     n = cfg["n"] if args.n is None else args.n
+    threads = os.cpu_count() or 1
     w, _ = synth.build_synthetic_world(cfg["clients"], cfg["pages"], cfg["seed"])
-    # each rank's shard of the globally indexed trace: same generator, per-rank seed
-    spec = synth.TraceSpec(n=n, seed=cfg["seed"] + 1000 * rank,
-                           parse_frac=cfg.get("parse_frac", 0.0), trap_frac=cfg.get("trap_frac", 0.0))
-    trace = synth.generate_trace(w, spec)
+
+    def rank_trace(r):
+        # weak scaling: rank r owns its own n-entry trace at global indices r*n .. (same
+        # generator, per-rank seed; rank 0's trace is the 1-GPU headline trace)
+        return synth.generate_trace(w, synth.TraceSpec(n=n, seed=cfg["seed"] + 1000 * r,
+                                                       parse_frac=cfg.get("parse_frac", 0.0),
+                                                       trap_frac=cfg.get("trap_frac", 0.0)))
+    trace = rank_trace(rank)
     params = BatchParams(isolation=True, base_index=rank * n)
     eng = FaultEngine(local)
     if ws > 1:
-        eng.set_dense_dedup(True)          # dedup slots are combined with an all-reduce MIN
+        eng.set_dense_dedup(True)          # dedup slots are MIN-combined across ranks
     eng.upload_world(w)
     d_in = torch.from_numpy(trace.view(np.uint8)).to(dev)
     bufs = DeviceBuffers(n, w.n_clients, local)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     sharded = ShardedFaultPath(GpuShard(eng, d_in, n, bufs)) if ws > 1 else None
-    step_fn = (lambda: sharded.process(params)) if ws > 1 else None
+    # sharded steps leave the outputs in HBM (no D2H inside the device-resident number)
+    step_fn = (lambda: sharded.process(params, fetch=False)) if ws > 1 else None
 
     # warm-up (also sizes the wild-page hash tables) and a bit-exact check vs the C oracle
     for _ in range(max(args.warmup, 3)):
         res = sharded.process(params) if ws > 1 else eng.process_resident(d_in, n, params, bufs)
     parity = None
     cpu_baseline = None
-    if rank == 0 and ws == 1 and not args.no_check:
-        from oracle import c_oracle as co
-        from oracle.seq_oracle import Params as OP
-        threads = os.cpu_count() or 1
-        t0 = time.perf_counter()
-        want = co.process_batch(w, trace, OP(isolation=True), base_index=rank * n, threads=threads)
-        t_cpu = time.perf_counter() - t0
-        same = all(np.array_equal(getattr(res, f), getattr(want, f)) for f in
-                   ("out", "verdict", "counts", "dedup_keys", "dedup_idx", "cancel"))
-        parity = "bit-exact vs C oracle (full trace)" if same else "MISMATCH vs C oracle"
+    ref_path = None
+    if not args.no_check:
         if ws == 1:
+            from oracle import c_oracle as co
+            from oracle.seq_oracle import Params as OP
+            t0 = time.perf_counter()
+            want = co.process_batch(w, trace, OP(isolation=True), threads=threads)
+            t_cpu = time.perf_counter() - t0
+            same = all(np.array_equal(getattr(res, f), getattr(want, f)) for f in
+                       ("out", "verdict", "counts", "dedup_keys", "dedup_idx", "cancel"))
+            parity = "bit-exact vs C oracle (full trace)" if same else "MISMATCH vs C oracle"
             cpu_baseline = {"value": n / t_cpu, "unit": "entries/s", "cores": threads, "kind": "port",
                             "sample": f"full {args.workload} trace ({n} entries), oracle/mpsf_oracle.c "
                                       f"(pthreads decode + sequential drain), 1 run"}
+            if not args.no_ref_path:
+                ref_path = reference_cpu_path(cfg, trace, res.out)
+        else:
+            traces = [rank_trace(r) for r in range(ws)] if rank == 0 else None
+            parity = check_gathered(ws, rank, dev, w, traces, res, threads, f"{ws} x {n} entries, weak")
     launches = eng.last_launches()
 
     barrier(ws)
@@ -270,9 +370,6 @@ def run_mine(args):
                     "frac": achieved / hbm_peak, "traffic": step_roof["traffic"], "kernel": step_roof["what"],
                     "peak_source": peak_src}
 
-    # per-client fates are identical on every rank after the exchanges
-    combined = res.verdict if ws > 1 else None
-
     # end to end through the C ABI with pinned host buffers
     e2e = None
     if not args.no_e2e:
@@ -299,9 +396,8 @@ def run_mine(args):
         e2e_mode = "one batch at a time (mpsf_process_host)"
         t_single, t_pipe = t_e2e, None
         if ws == 1:
-            # a stream of batches through the asynchronous form: two slots in flight, so the
+            # a stream of batches through the asynchronous form: three slots in flight, so the
             # H2D of batch k+1 overlaps the passes and the D2H of batch k
-            # (three slots: the H2D of batch k+3 waits only for batch k's copies to land)
             NS = 3
             hb2 = [hb] + [alloc_host_outputs(n, w.n_clients, pinned=True) for _ in range(NS - 1)]
 
@@ -328,13 +424,15 @@ def run_mine(args):
         e2e = {"value": ws * n / t_e2e, "unit": "entries/s", "h2d_bytes_per_step": 16 * n,
                "d2h_bytes_per_step": d2h, "ms_per_step": round(t_e2e * 1e3, 3),
                "api": f"{e2e_mode}, pinned host buffers" if ws == 1 else
-                      "H2D + sharded phase API + NCCL exchanges + D2H",
+                      "H2D + sharded phase API + NCCL exchanges + D2H (per rank; bytes per rank)",
                "single_batch_ms": round(t_single * 1e3, 3),
                "stream_ms_per_batch": None if t_pipe is None else round(t_pipe * 1e3, 3)}
 
     extra = {}
-    if not args.no_storm and ws == 1:
-        extra["storm_c3"] = bench_storm(args, eng, hbm_peak, flush)
+    if ws > 1 and not args.no_strong:
+        extra["strong_c5"] = bench_strong(args, eng, w, cfg, ws, rank, local, flush, threads)
+    if not args.no_storm:
+        extra["storm_c3"] = bench_storm(args, eng, hbm_peak, flush, ws, rank, local, threads)
     if not args.no_remap:
         extra["remap_c4"] = bench_remap(args, eng, hbm_peak, flush)
     if not args.no_storm and ws == 1:
@@ -357,18 +455,55 @@ def run_mine(args):
             "roofline": dom_roof,
             "kernels": kernels,
             "cpu_baseline": cpu_baseline,
+            "reference_cpu_path": ref_path,
             "e2e": e2e,
             "gpu_launches": launches * args.steps,
             "clocks": clk.summary(),
             "parity": parity,
             "extra": extra,
         }
-        if combined is not None:
-            line["combined_clients_terminated"] = int((combined["state"] == 1).sum())
+        if ws > 1:
+            line["combined_clients_terminated"] = int((res.verdict["state"] == 1).sum())
         print(json.dumps(line), flush=True)
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def bench_strong(args, eng, w, cfg, ws, rank, local, flush, threads):
+    """Config 5 (BASELINE.json configs[4]): the 10^7-entry config-2b trace of the 1-GPU headline
+    split over the N GPUs by contiguous entry range (strong scaling), per-client verdicts and
+    group minima combined over NCCL; the concatenated shards are checked against the C oracle on
+    the whole trace (= the 1-GPU result)."""
+    import torch
+    from paper_2605_26461_b200 import synth
+    from paper_2605_26461_b200.engine import BatchParams, DeviceBuffers
+    from paper_2605_26461_b200.parallel import GpuShard, ShardedFaultPath
+    dev = torch.device("cuda", local)
+    N = cfg["n"] if args.n is None else args.n
+    full = synth.generate_trace(w, synth.TraceSpec(n=N, seed=cfg["seed"], parse_frac=cfg.get("parse_frac", 0.0),
+                                                   trap_frac=cfg.get("trap_frac", 0.0)))
+    cut = [N * r // ws for r in range(ws + 1)]
+    sh = full[cut[rank]:cut[rank + 1]]
+    n = len(sh)
+    d_in = torch.from_numpy(sh.view(np.uint8).copy()).to(dev)
+    bufs = DeviceBuffers(n, w.n_clients, local)
+    p = BatchParams(isolation=True, base_index=cut[rank])
+    path = ShardedFaultPath(GpuShard(eng, d_in, n, bufs))
+    for _ in range(3):
+        res = path.process(p)
+    parity = None
+    if not args.no_check:
+        parity = check_gathered(ws, rank, dev, w, [full[cut[r]:cut[r + 1]] for r in range(ws)], res, threads,
+                                f"c5: {N} entries split {ws} ways")
+    steps = max(3, min(args.steps, 10))
+    barrier(ws)
+    total, s, prof = time_resident(eng, d_in, n, p, bufs, steps, flush, lambda: path.process(p, fetch=False))
+    ms = max_over_ranks(ws, total / steps)
+    return {"workload": f"c5: the {N}-entry c2b trace split over {ws} GPUs (contiguous entry ranges), NCCL "
+                        f"exchanges of the group minima, sparse exchange of page-sized tables",
+            "value": N / (ms / 1e3), "unit": "entries/s", "ms_per_step": ms, "steps": steps, "scaling": "strong",
+            "parity": parity, "kernels": {k: round(v[1] / max(v[0], 1), 5) for k, v in sorted(prof.items())}}
 
 
 def rewarm(fn, ms=200.0):
@@ -382,48 +517,91 @@ def rewarm(fn, ms=200.0):
         torch.cuda.synchronize()
 
 
-def bench_storm(args, eng, hbm_peak, flush):
+def bench_storm(args, eng, hbm_peak, flush, ws=1, rank=0, local=0, threads=1):
+    """Config 3: the 10^8-entry replayable storm (90 % duplicate pages) on the 48 x 32 x 8192
+    world -- 12.6 M page slots, so one GPU takes the claimed-slot dedup layout.  The whole
+    batch is checked against the C oracle (all six outputs), which is also the CPU baseline.
+    At N > 1 the batch is split over the GPUs (strong scaling: 2^29 global indices cap weak
+    scaling of 10^8-entry shards at five GPUs) with the dense layout and the sparse exchange of
+    the page-sized tables."""
     import torch
     from paper_2605_26461_b200 import synth
     from paper_2605_26461_b200.engine import BatchParams, DeviceBuffers
-    cfg = synth.CONFIGS["c3"]
-    n = cfg["n"] if args.storm_n is None else args.storm_n
-    u = max(1, n // 10)
-    w, _ = synth.build_synthetic_world(cfg["clients"], cfg["pages"], cfg["seed"])
-    d_in = synth.generate_storm(w, n, u, cfg["seed"], device="cuda")
-    eng.upload_world(w)
-    bufs = DeviceBuffers(n, w.n_clients)
-    params = BatchParams(isolation=True)
-    for _ in range(3):
-        res = eng.process_resident(d_in, n, params, bufs)
-    steps = max(3, min(args.steps, 10))
-    total, s, prof = time_resident(eng, d_in, n, params, bufs, steps, flush)
-    ms = total / steps
-    nd, nc = int(s.n_dedup), int(s.n_cancel)
-    B = alg_bytes(n, nd, nc)
-    ach = B / (ms / 1e3) / 1e9
-    ok = nd == u and int(((res.out["verdict"] & 0x20) != 0).sum()) == n - u
-    # the CPU restatement (oracle/mpsf_oracle.c, all host threads) on a 5 M-entry prefix
-    from oracle import c_oracle as co
-    from oracle.seq_oracle import Params as OP
-    ns = min(n, 5_000_000)
+    from paper_2605_26461_b200.parallel import GpuShard, ShardedFaultPath
     from paper_2605_26461_b200.world import ENTRY_DTYPE
-    sample = d_in[:16 * ns].cpu().numpy().view(ENTRY_DTYPE)
-    threads = os.cpu_count() or 1
-    t0 = time.perf_counter()
-    co.process_batch(w, sample, OP(isolation=True), threads=threads)
-    t_cpu = time.perf_counter() - t0
-    cpu_b = {"value": ns / t_cpu, "unit": "entries/s", "cores": threads, "kind": "port",
-             "sample": f"first {ns} entries of the storm, oracle/mpsf_oracle.c"}
-    del d_in, bufs
+    cfg = synth.CONFIGS["c3"]
+    N = cfg["n"] if args.storm_n is None else args.storm_n
+    u = max(1, N // 10)
+    dev = torch.device("cuda", local)
+    w, _ = synth.build_synthetic_world(cfg["clients"], cfg["pages"], cfg["seed"])
+    full = synth.generate_storm(w, N, u, cfg["seed"], device=dev)       # uint8[16 N] in HBM
+    cut = [N * r // ws for r in range(ws + 1)]
+    n = cut[rank + 1] - cut[rank]
+    d_in = full[16 * cut[rank]:16 * cut[rank + 1]] if ws > 1 else full
+    eng.set_dedup_layout("dense" if ws > 1 else "auto")
+    eng.upload_world(w)
+    eng.set_dedup_layout("auto")
+    bufs = DeviceBuffers(n, w.n_clients, local)
+    params = BatchParams(isolation=True, base_index=cut[rank])
+    path = ShardedFaultPath(GpuShard(eng, d_in, n, bufs)) if ws > 1 else None
+    step_fn = (lambda: path.process(params, fetch=False)) if ws > 1 else None
+    for _ in range(3):
+        res = path.process(params) if ws > 1 else eng.process_resident(d_in, n, params, bufs)
+    steps = max(3, min(args.steps, 10))
+    barrier(ws)
+    total, s, prof = time_resident(eng, d_in, n, params, bufs, steps, flush, step_fn)
+    ms = max_over_ranks(ws, total / steps)
+    nd, nc = int(s.n_dedup), int(s.n_cancel)
+    # the whole batch against the C oracle (all host threads): parity and the CPU baseline
+    parity, cpu_b = None, None
+    if not args.no_check:
+        host = full.cpu().numpy().view(ENTRY_DTYPE) if rank == 0 else None
+        if ws > 1:
+            from oracle import c_oracle as co
+            from oracle.seq_oracle import Params as OP
+            parts = {f: gather_arrays(ws, getattr(res, f), dev) for f in
+                     ("out", "verdict", "counts", "dedup_keys", "dedup_idx", "cancel")}
+            if rank == 0:
+                t0 = time.perf_counter()
+                want = co.process_batch(w, host, OP(isolation=True), threads=threads)
+                t_cpu = time.perf_counter() - t0
+                got = {f: np.concatenate(v) for f, v in parts.items() if f not in ("verdict", "counts")}
+                got["verdict"], got["counts"] = parts["verdict"][0], parts["counts"][0].reshape(want.counts.shape)
+                ok = all(np.array_equal(got[f], getattr(want, f)) for f in got)
+        else:
+            from oracle import c_oracle as co
+            from oracle.seq_oracle import Params as OP
+            t0 = time.perf_counter()
+            want = co.process_batch(w, host, OP(isolation=True), threads=threads)
+            t_cpu = time.perf_counter() - t0
+            ok = all(np.array_equal(getattr(res, f), getattr(want, f)) for f in
+                     ("out", "verdict", "counts", "dedup_keys", "dedup_idx", "cancel"))
+        if rank == 0:
+            parity = (f"bit-exact vs C oracle (all {N} entries, six outputs)" if ok
+                      else "MISMATCH vs C oracle")
+            cpu_b = {"value": N / t_cpu, "unit": "entries/s", "cores": threads, "kind": "port",
+                     "sample": f"the whole {N}-entry storm, oracle/mpsf_oracle.c (pthreads decode + sequential "
+                               f"drain), 1 run"}
+            del host, want
+    if ws > 1:          # batch totals (each shard lists its own range)
+        import torch.distributed as dist
+        t = torch.tensor([nd, nc], dtype=torch.int64, device=dev)
+        dist.all_reduce(t)
+        nd, nc = int(t[0].item()), int(t[1].item())
+    B = alg_bytes(N, nd, nc)
+    ach = B / (ms / 1e3) / 1e9
+    dup_ok = nd == u
+    del d_in, full, bufs, res
     torch.cuda.empty_cache()
-    return {"workload": f"c3: 48 clients x 32 ranges x 8192 pages, {n} replayable entries, {u} unique "
-                        f"(client,page) pairs, 90% duplicates, isolation on",
-            "value": n / (ms / 1e3), "unit": "entries/s", "ms_per_step": ms, "steps": steps,
+    return {"workload": f"c3: 48 clients x 32 ranges x 8192 pages, {N} replayable entries, {u} unique "
+                        f"(client,page) pairs, 90% duplicates, isolation on"
+                        + (f", split over {ws} GPUs (strong scaling)" if ws > 1 else ""),
+            "value": N / (ms / 1e3), "unit": "entries/s", "ms_per_step": ms, "steps": steps,
+            "scaling": "strong" if ws > 1 else None,
             "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
                          "frac": ach / hbm_peak, "alg_bytes_per_step": B},
             "kernels": {k: round(v[1] / max(v[0], 1), 5) for k, v in sorted(prof.items())},
-            "n_dedup": nd, "n_cancel": nc, "dedup_exact": bool(ok), "cpu_baseline": cpu_b}
+            "n_dedup": nd, "n_cancel": nc, "dedup_count_exact": dup_ok, "parity": parity, "cpu_baseline": cpu_b}
 
 
 def bench_translate(args, eng, hbm_peak, flush, w):
@@ -659,8 +837,13 @@ def workload_name(wl: str, n: int) -> str:
 
 
 def run_reference(args):
-    """The reference's CPU implementation of the path (its restatement oracle/mpsf_oracle.c;
-    the reference itself is pure Python and absent on the GPU box) on the host cores."""
+    """The reference arm: the reference's CPU implementation of the path on the host cores, on
+    the same workload as this arm's line.  The reference is pure Python whose bottom half cannot
+    run a 10^7-entry batch (it raises on duplicate pages and on a second fatal record, SURVEY.md
+    [P2]), so each step runs its restatement ``oracle/mpsf_oracle.c`` over the WHOLE trace on
+    every host thread (pinned bit-exact to the reference by tests/test_c_oracle.py and
+    tests/test_oracle_vs_reference.py); when the reference is installed (baseline/_ref) its own
+    top half -- channel_to_pid + faults.classify -- is timed beside it on a prefix."""
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -670,28 +853,39 @@ def run_reference(args):
     from paper_2605_26461_b200 import synth
     cfg = synth.CONFIGS[args.workload]
     n = cfg["n"] if args.n is None else args.n
-    sample = min(n, 2_000_000)
     w, _ = synth.build_synthetic_world(cfg["clients"], cfg["pages"], cfg["seed"])
     trace = synth.generate_trace(w, synth.TraceSpec(n=n, seed=cfg["seed"], parse_frac=cfg.get("parse_frac", 0.0),
-                                                    trap_frac=cfg.get("trap_frac", 0.0)))[:sample]
+                                                    trap_frac=cfg.get("trap_frac", 0.0)))
     threads = os.cpu_count() or 1
-    for _ in range(args.warmup):
+    steps, warmup = args.steps, args.warmup
+    # bounded run: the whole trace per step; steps capped so the arm ends within a few minutes
+    t0 = time.perf_counter()
+    co.process_batch(w, trace, OP(isolation=True), threads=threads)
+    t_one = time.perf_counter() - t0
+    budget = 150.0
+    if t_one * (steps + warmup) > budget:
+        steps = max(3, int(budget / t_one) - 1)
+        warmup = 1
+    for _ in range(warmup - 1):
         co.process_batch(w, trace, OP(isolation=True), threads=threads)
     ts = []
-    for _ in range(args.steps):
+    for _ in range(steps):
         t0 = time.perf_counter()
         co.process_batch(w, trace, OP(isolation=True), threads=threads)
         ts.append(time.perf_counter() - t0)
     ms = 1e3 * sum(ts) / len(ts)
-    value = sample / (ms / 1e3)
-    smp = f"first {sample} entries of the {args.workload} trace per step, oracle/mpsf_oracle.c, {threads} threads"
-    line = {"metric": METRIC, "value": value, "unit": "entries/s", "impl": "reference", "n_gpus": ws,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+    value = n / (ms / 1e3)
+    smp = f"the whole {args.workload} trace ({n} entries) per step, oracle/mpsf_oracle.c, {threads} threads"
+    line = {"metric": METRIC, "value": value, "unit": "entries/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": steps, "warmup": warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": workload_name(args.workload, n), "entries_per_gpu": n,
-                       "entries_per_step": sample},
+                       "entries_per_step": n},
             "cpu_baseline": {"value": value, "unit": "entries/s", "cores": threads, "kind": "port", "sample": smp},
+            "reference_cpu_path": None if args.no_ref_path else reference_cpu_path(cfg, trace),
             "e2e": {"value": value, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if steps != args.steps:
+        line["steps_capped"] = f"{args.steps} requested; {steps} whole-trace steps fit the time budget"
     print(json.dumps(line), flush=True)
 
 
@@ -704,17 +898,27 @@ def main():
                     help="with --gpus N > 1: also time the sharded batched translation (NCCL MIN between phases)")
     ap.add_argument("--impl", default="mine", choices=("mine", "reference"))
     ap.add_argument("--workload", default="c2b", choices=("c1", "c2a", "c2b"))
-    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--entries", "--n", dest="n", type=int, default=None, help="entries per GPU (default: the config's)")
     ap.add_argument("--storm-n", type=int, default=None)
     ap.add_argument("--no-storm", action="store_true")
     ap.add_argument("--no-remap", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--no-strong", action="store_true", help="N > 1: skip the strong-scaling config-5 extra")
+    ap.add_argument("--no-ref-path", action="store_true", help="skip timing the reference's own classify")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
+    elif os.environ.get("MPSF_BENCH_LAUNCH_PROBE") == "1":
+        # test hook (tests/test_bench_launch.py): report the rank layout and stop before any CUDA work
+        print(json.dumps({"probe": True, "rank": int(os.environ.get("RANK", "0")),
+                          "world_size": int(os.environ.get("WORLD_SIZE", "1")),
+                          "local_rank": int(os.environ.get("LOCAL_RANK", "0")),
+                          "master_addr": os.environ.get("MASTER_ADDR")}), flush=True)
     else:
         run_mine(args)
 

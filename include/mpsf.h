@@ -288,7 +288,10 @@ int mpsf_get_profile(mpsf_ctx* ctx, mpsf_kernel_time* out, int cap);
  * general stages follow (exchange stage 2 after stage 1, stage 3 after stage 2); finally
  * mpsf_finalize writes this shard's outputs.  Because every cross-entry dependency is a
  * group minimum, the concatenated per-rank outputs equal a single-GPU run bit for bit. */
-int mpsf_set_dense_dedup(mpsf_ctx* ctx, int on);   /* before upload: one dedup slot per (page, group) */
+/* Dedup-slot layout, before upload: on > 0 one dense slot per (page, group) (sharded runs);
+ * on < 0 one claimed slot per page, other groups through the hash, no per-page first-eligible
+ * keys (the layout large worlds get; forcing it lets small worlds test that path); 0 by size. */
+int mpsf_set_dense_dedup(mpsf_ctx* ctx, int on);
 int mpsf_scan(mpsf_ctx* ctx, const mpsf_fault_entry* d_entries, uint64_t n, const mpsf_params* params,
               uint64_t* d_counts, void* stream);
 int mpsf_resolve(mpsf_ctx* ctx, const mpsf_params* params, mpsf_client_verdict* d_verdict,
@@ -317,6 +320,16 @@ int64_t mpsf_hash_export(mpsf_ctx* ctx, int which, uint64_t* d_keys, uint32_t* d
                          void* stream);
 int mpsf_hash_merge(mpsf_ctx* ctx, int which, const uint64_t* d_keys, const uint32_t* d_vals,
                     uint64_t count, void* stream);
+
+/* Sparse form of a MIN exchange buffer of 4-byte words (the page-sized dedup slots and
+ * first-eligible keys of a large world are mostly empty): export compacts the words that are
+ * not 0xFFFFFFFF into (index, value) pairs (returns the count, MPSF_E_OVERFLOW beyond cap;
+ * waits on the stream); merge applies pairs gathered from the other ranks with an atomic MIN.
+ * Export + all-gather + merge on every rank == a MIN all-reduce of the buffer. */
+int64_t mpsf_sparse_export(mpsf_ctx* ctx, const uint32_t* d_buf, uint64_t count, uint32_t* d_idx, uint32_t* d_val,
+                           uint64_t cap, void* stream);
+int mpsf_sparse_merge(mpsf_ctx* ctx, uint32_t* d_buf, uint64_t count, const uint32_t* d_idx, const uint32_t* d_val,
+                      uint64_t n, void* stream);
 
 #ifdef __cplusplus
 }

@@ -1684,6 +1684,53 @@ int launch_copyout(const Scratch& S, uint64_t n, const unsigned long long* d_dk,
   return ok_or_err();
 }
 
+// ---- sparse exchange of page-sized minima tables (multi-GPU round 1b) ---------------------
+// The dense dedup slots / first-eligible page keys of a large world are mostly EMPTY: a rank
+// compacts its non-empty words to (index, value) pairs (warp-aggregated append), the ranks
+// all-gather the pairs and each merges the others' with an atomic MIN -- the same minima as a
+// dense all-reduce, moving O(keys) instead of O(pages) bytes.
+__global__ void k_sparse_export(const uint32_t* __restrict__ buf, uint64_t count, uint32_t* __restrict__ idx,
+                                uint32_t* __restrict__ val, uint32_t* __restrict__ counter, uint64_t cap) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x; i0 < count; i0 += stride) {
+    const uint64_t i = i0 + threadIdx.x;
+    const uint32_t v = i < count ? __ldcs(buf + i) : EMPTY32;
+    const bool has = v != EMPTY32;
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, has);
+    if (!m) continue;
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(counter, (uint32_t)__popc(m));
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    if (has) {
+      const uint64_t o = base + __popc(m & ((1u << lane) - 1u));
+      if (o < cap) { idx[o] = (uint32_t)i; val[o] = v; }
+    }
+  }
+}
+
+__global__ void k_sparse_merge(uint32_t* __restrict__ buf, uint64_t count, const uint32_t* __restrict__ idx,
+                               const uint32_t* __restrict__ val, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = idx[i];
+    if (k < count) min32(buf + k, val[i]);
+  }
+}
+
+int launch_sparse_export(const uint32_t* buf, uint64_t count, uint32_t* idx, uint32_t* val, uint32_t* counter,
+                         uint64_t cap, cudaStream_t st) {
+  if (count == 0) return 0;
+  k_sparse_export<<<4 * sm_count(), 512, 0, st>>>(buf, count, idx, val, counter, cap);
+  return ok_or_err();
+}
+
+int launch_sparse_merge(uint32_t* buf, uint64_t count, const uint32_t* idx, const uint32_t* val, uint64_t n,
+                        cudaStream_t st) {
+  if (n == 0) return 0;
+  k_sparse_merge<<<4 * sm_count(), 512, 0, st>>>(buf, count, idx, val, n);
+  return ok_or_err();
+}
+
 template <bool kStaged>
 static void translate_attrs() {
   static bool attr = false;

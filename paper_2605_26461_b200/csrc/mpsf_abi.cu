@@ -94,7 +94,7 @@ struct mpsf_ctx {
   uint64_t dd_cap = 0;
   uint32_t* d_count_part = nullptr;
   uint64_t part_cap = 0;
-  bool dense_dedup = false;
+  int dedup_mode = 0;            // 1 dense slots, -1 claimed slots (large-world layout), 0 by size
   // exchange-group offsets inside d_small
   size_t x_u64 = 0, x_u32 = 0, x_giso = 0;
   uint64_t x_u64_n = 0, x_u32_n = 0, x_giso_n = 0;
@@ -121,6 +121,7 @@ struct mpsf_ctx {
   DevSummary* d_sum = nullptr;
   cudaEvent_t ev_done = nullptr;
   bool pending = false;
+  bool pending_fault = true;      // the pending summary is a fault-path batch (not a translation)
   uint64_t last_n = 0;
   int last_launches = 0;
   // per-kernel profiling (events recorded after every launch)
@@ -184,7 +185,9 @@ struct mpsf_ctx {
     if ((x) != cudaSuccess) return MPSF_E_CUDA; \
   } while (0)
 
-static void fill_summary(mpsf_ctx* c, const DevSummary& d, mpsf_summary* out) {
+// `fault`: a fault-path batch (translation summaries carry no hash counts and must not size
+// the wild-page tables)
+static void fill_summary(mpsf_ctx* c, const DevSummary& d, mpsf_summary* out, bool fault) {
   memset(out, 0, sizeof(*out));
   const uint32_t err = d.ctrl[C_ERR];
   if (err & EB_NO_CHANNEL) out->status = MPSF_E_NO_CHANNEL;
@@ -199,6 +202,7 @@ static void fill_summary(mpsf_ctx* c, const DevSummary& d, mpsf_summary* out) {
   out->error_index = d.err_idx;
   out->hash_used = (uint64_t)d.ctrl[C_HASH_DD] + d.ctrl[C_HASH_NR];
   // adapt the wild-page hash tables for the next call
+  if (!fault) return;
   if (out->status == MPSF_E_OVERFLOW) {
     if (d.ctrl[C_HASH_DD] * 2ull >= c->hcap_dd / 2) c->want_dd = c->hcap_dd * 4;
     if (d.ctrl[C_HASH_NR] * 2ull >= c->hcap_nr / 2) c->want_nr = c->hcap_nr * 4;
@@ -473,7 +477,9 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   W.has_mps = has_mps;
   // dedup slots: one per (page, group) while that stays small (L2-resident), else one
   // claimed slot per page with overflow to the hash table
-  W.dd_groups = (c->dense_dedup || np * 5 * 4 <= (64ull << 20)) ? 5 : 1;
+  // (mpsf_set_dense_dedup forces either layout: dense for sharded runs, claimed slots to test the
+  // large-world path on small worlds)
+  W.dd_groups = c->dedup_mode > 0 ? 5 : c->dedup_mode < 0 ? 1 : (np * 5 * 4 <= (64ull << 20)) ? 5 : 1;
   // page-sized scratch
   const uint64_t dd_words = np * W.dd_groups;
   if (!c->d_dd || dd_words > c->dd_cap || np > c->pages_cap) {
@@ -620,7 +626,7 @@ static Params to_params(const mpsf_params* p) {
 
 int mpsf_set_dense_dedup(mpsf_ctx* c, int on) {
   if (!c) return MPSF_E_ARG;
-  c->dense_dedup = on != 0;
+  c->dedup_mode = on > 0 ? 1 : on < 0 ? -1 : 0;
   return MPSF_OK;
 }
 
@@ -733,6 +739,7 @@ int mpsf_finalize(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const m
     return MPSF_E_CUDA;
   CK(cudaEventRecord(c->ev_done, st));
   c->pending = true;
+  c->pending_fault = true;
   c->last_n = n;
   c->last_launches += n ? 2 : 1;
   return MPSF_OK;
@@ -801,6 +808,7 @@ int mpsf_translate_finish(mpsf_ctx* c, const mpsf_fault_entry* d_acc, uint64_t n
     return MPSF_E_CUDA;
   CK(cudaEventRecord(c->ev_done, st));
   c->pending = true;
+  c->pending_fault = false;
   c->last_n = n;
   c->last_launches += n ? 2 : 1;
   return MPSF_OK;
@@ -881,6 +889,28 @@ int mpsf_hash_merge(mpsf_ctx* c, int which, const uint64_t* d_keys, const uint32
   return MPSF_OK;
 }
 
+int64_t mpsf_sparse_export(mpsf_ctx* c, const uint32_t* d_buf, uint64_t count, uint32_t* d_idx, uint32_t* d_val,
+                           uint64_t cap, void* stream) {
+  if (!c || (count && !d_buf) || (cap && (!d_idx || !d_val)) || count > 0xFFFFFFFFull) return MPSF_E_ARG;
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (!c->d_counter) CK(cudaMalloc(&c->d_counter, 4));
+  CK(cudaMemsetAsync(c->d_counter, 0, 4, st));
+  if (launch_sparse_export(d_buf, count, d_idx, d_val, c->d_counter, cap, st)) return MPSF_E_CUDA;
+  uint32_t cnt = 0;
+  CK(cudaMemcpyAsync(&cnt, c->d_counter, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return cnt > cap ? MPSF_E_OVERFLOW : (int64_t)cnt;
+}
+
+int mpsf_sparse_merge(mpsf_ctx* c, uint32_t* d_buf, uint64_t count, const uint32_t* d_idx, const uint32_t* d_val,
+                      uint64_t n, void* stream) {
+  if (!c || (count && !d_buf) || (n && (!d_idx || !d_val))) return MPSF_E_ARG;
+  CK(cudaSetDevice(c->device));
+  if (launch_sparse_merge(d_buf, count, d_idx, d_val, n, reinterpret_cast<cudaStream_t>(stream))) return MPSF_E_CUDA;
+  return MPSF_OK;
+}
+
 int mpsf_get_summary(mpsf_ctx* c, mpsf_summary* out) {
   if (!c || !out) return MPSF_E_ARG;
   CK(cudaSetDevice(c->device));
@@ -888,7 +918,7 @@ int mpsf_get_summary(mpsf_ctx* c, mpsf_summary* out) {
     CK(cudaEventSynchronize(c->ev_done));
     c->pending = false;
   }
-  fill_summary(c, *c->h_sum, out);
+  fill_summary(c, *c->h_sum, out, c->pending_fault);
   return MPSF_OK;
 }
 
@@ -1047,7 +1077,7 @@ int mpsf_collect_host(mpsf_ctx* c, int slot, mpsf_summary* summary) {
   CK(cudaSetDevice(c->device));
   CK(cudaEventSynchronize(h.ev_done));
   h.busy = false;
-  fill_summary(c, *h.h_sum, summary);
+  fill_summary(c, *h.h_sum, summary, true);
   const uint64_t n = h.n;
   uint8_t* b = h.d_io;
   cudaStream_t st = c->own_stream;

@@ -54,6 +54,11 @@ int launch_hash_export(const Hash& h, uint64_t cap, unsigned long long* keys, ui
                        uint64_t out_cap, cudaStream_t st);
 int launch_hash_merge(const Hash& h, uint32_t* ctrl, const unsigned long long* keys, const uint32_t* vals,
                       uint64_t count, cudaStream_t st);
+// sparse exchange of a u32 minima table: compact the non-EMPTY words / MIN-merge (index, value) pairs
+int launch_sparse_export(const uint32_t* buf, uint64_t count, uint32_t* idx, uint32_t* val, uint32_t* counter,
+                         uint64_t cap, cudaStream_t st);
+int launch_sparse_merge(uint32_t* buf, uint64_t count, const uint32_t* idx, const uint32_t* val, uint64_t n,
+                        cudaStream_t st);
 uint32_t count_parts_needed(const World& W);   // per-block count partial rows k_scan may write
 
 int launch_remap(uint64_t va_base, const uint64_t* phys, uint64_t npages4k, uint32_t gran_log2,

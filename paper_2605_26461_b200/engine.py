@@ -111,9 +111,15 @@ class FaultEngine:
 
     # -- world ---------------------------------------------------------------------------
     def set_dense_dedup(self, on: bool = True) -> None:
-        """One dedup slot per (page, group) regardless of world size (required for sharded
-        runs, whose dedup slots are combined with an all-reduce MIN).  Call before upload."""
-        self._check(self.lib.mpsf_set_dense_dedup(self.ctx, 1 if on else 0))
+        """One dedup slot per (page, group) regardless of world size.  Call before upload."""
+        self.set_dedup_layout("dense" if on else "auto")
+
+    def set_dedup_layout(self, layout: str = "auto") -> None:
+        """Dedup-slot layout of the next upload: "dense" (one slot per (page, group)),
+        "sparse" (one claimed slot per page, other groups through the hash table, no per-page
+        first-eligible keys -- what worlds over ~3.3 M pages get), or "auto" (by size)."""
+        mode = {"auto": 0, "dense": 1, "sparse": -1}[layout]
+        self._check(self.lib.mpsf_set_dense_dedup(self.ctx, mode))
 
     def upload_world(self, w: FlatWorld) -> None:
         """``mpsf_upload_world``: the interval table, page states, channels, clients."""

@@ -7,8 +7,11 @@ a sum, or a max of flags, so the shards only need:
 
 1. after pass 1 (``mpsf_scan``): all-reduce MIN of the dense group minima (fatal TSG
    teardowns, traps, first isolation per external range / guard page / client) and of the
-   dense dedup slots, plus a sparse merge (all-gather + atomic-min insert) of the two
-   wild-page hash tables;
+   dedup slots, plus a sparse merge (all-gather + atomic-min insert) of the two wild-page
+   hash tables.  Page-sized tables (dedup slots, first-eligible page keys) go dense only
+   while small; beyond ``SPARSE_MIN_BYTES`` each rank compacts its non-empty words to
+   (index, value) pairs, the ranks all-gather them and MIN-merge (SURVEY.md §8(e) round 1b:
+   O(keys) bytes, not O(pages) -- 252 MB of dedup slots per batch on the config-3 world);
 2. with isolation on, after the release-aware stage (``mpsf_general`` 1): MIN of the exact
    per-client mechanism minima and of the epoch-1 first-isolation slots, sparse NR merge;
    after stage 2 (only when m2 <= benign): MIN of the per-client M2 minima;
@@ -23,12 +26,35 @@ the CPU tests; unsigned MIN is done on signed views with the sign bit flipped.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 
 from . import _lib
 from .engine import BatchParams, DeviceBuffers, FaultEngine
-from .world import VERDICT_DTYPE
+from .errors import E_BAD_ENTRY, E_MISMATCH, E_NO_CHANNEL, E_OVERFLOW, E_VA, raise_for
+
+# 4-byte MIN buffers larger than this are exchanged as compacted (index, value) pairs
+# (MPSF_SPARSE_X=always|never overrides, for tests)
+SPARSE_MIN_BYTES = 4 << 20
+
+# entry errors in the priority mpsf_get_summary reports them (the device ORs the error bits of
+# every bad entry and reports the highest-priority code with the smallest offending index)
+_ERR_PRIO = {E_NO_CHANNEL: 4, E_BAD_ENTRY: 3, E_MISMATCH: 2, E_VA: 1}
+_PRIO_ERR = {v: k for k, v in _ERR_PRIO.items()}
+_ERR_MSG = {E_NO_CHANNEL: "fault entry channel has no client attribution",
+            E_BAD_ENTRY: "malformed fault entry (engine/access/kind)",
+            E_MISMATCH: "fault entry engine differs from its channel's engine",
+            E_VA: "fault VA >= 2^53"}
+
+
+def use_sparse(t) -> bool:
+    mode = os.environ.get("MPSF_SPARSE_X", "auto")
+    if mode == "always":
+        return t.element_size() == 4
+    if mode == "never":
+        return False
+    return t.element_size() == 4 and t.numel() * 4 > SPARSE_MIN_BYTES
 
 
 def _dist():
@@ -84,7 +110,11 @@ class ShardedFaultPath:
 
     def _combine(self, stage):
         for t, op in self.a.exchange(stage):
-            if op == "min":
+            if op == "min" and use_sparse(t):
+                idx, val = self.a.sparse_export(t)
+                gi, gv = allgather_ragged(idx, val, self.group)
+                self.a.sparse_merge(t, gi, gv)
+            elif op == "min":
                 allreduce_min_unsigned(t, self.group)
             else:
                 allreduce_sum(t, self.group)
@@ -94,19 +124,39 @@ class ShardedFaultPath:
         ks, vs = allgather_ragged(keys, vals, self.group)
         self.a.hash_merge(which, ks, vs)
 
-    def process(self, params: BatchParams, max_attempts: int = 6):
+    def _agree(self, status: int, error_index: int):
+        """Every rank's batch status -> the one the whole batch has: the highest-priority entry
+        error of any rank with the smallest global offending index (what one GPU reports), else
+        overflow if any rank overflowed, else ok.  One MAX and one MIN all-reduce."""
+        import torch
+        dev = self.a.counts_tensor().device
+        flags = torch.tensor([1 if status == E_OVERFLOW else 0, _ERR_PRIO.get(status, 0)], dtype=torch.int64,
+                             device=dev)
+        idx = torch.tensor([error_index if status in _ERR_PRIO else (1 << 62)], dtype=torch.int64, device=dev)
+        if _dist().is_initialized():
+            _dist().all_reduce(flags, op=_dist().ReduceOp.MAX, group=self.group)
+        prio = int(flags[1].item())
+        if prio:
+            if _dist().is_initialized():     # the smallest bad entry of any kind on any rank
+                _dist().all_reduce(idx, op=_dist().ReduceOp.MIN, group=self.group)
+            return _PRIO_ERR[prio], int(idx.item())
+        return (E_OVERFLOW if int(flags[0].item()) else 0), -1
+
+    def process(self, params: BatchParams, max_attempts: int = 6, fetch: bool = True):
         """One sharded batch.  A wild-page hash table that fills up on any rank -- in its own
         inserts or in the merge of the other ranks' keys -- makes every rank run the batch
-        again (the full tables have grown); the ranks agree on that with a MAX all-reduce."""
-        import torch
+        again (the full tables have grown).  An entry error on any rank raises the same
+        exception on every rank (no rank is left waiting in a collective).  ``fetch=False``
+        leaves this shard's outputs in device memory (returns None)."""
         from .errors import HashOverflow
         for _ in range(max_attempts):
-            res = self._once(params)
-            ovf = torch.tensor([1 if res is None else 0], dtype=torch.int32, device=self.a.counts_tensor().device)
-            if _dist().is_initialized():
-                _dist().all_reduce(ovf, op=_dist().ReduceOp.MAX, group=self.group)
-            if int(ovf.item()) == 0:
-                return res
+            self._once(params)
+            status, eidx = self._agree(*self.a.status())
+            if status == E_OVERFLOW:
+                continue
+            if status:
+                raise_for(status, _ERR_MSG[status], eidx)
+            return self.a.result() if fetch else None
         raise HashOverflow("wild-page hash tables kept overflowing")
 
     def _once(self, params: BatchParams):
@@ -126,7 +176,6 @@ class ShardedFaultPath:
             a.resolve2(params)
         a.finalize(params)
         allreduce_sum(a.counts_tensor(), self.group)
-        return a.result()
 
 
 class LocalShardGroup:
@@ -165,9 +214,15 @@ class LocalShardGroup:
     def process(self, params_list, max_attempts: int = 6):
         from .errors import HashOverflow
         for _ in range(max_attempts):
-            res = self._once(params_list)
-            if all(r is not None for r in res):
-                return res
+            self._once(params_list)
+            st = [a.status() for a in self.ads]
+            errs = [(_ERR_PRIO[c], i) for c, i in st if c in _ERR_PRIO]
+            if errs:
+                code = _PRIO_ERR[max(p for p, _ in errs)]
+                raise_for(code, _ERR_MSG[code], min(i for _, i in errs))
+            if any(c == E_OVERFLOW for c, _ in st):
+                continue
+            return [a.result() for a in self.ads]
         raise HashOverflow("wild-page hash tables kept overflowing")
 
     def _once(self, params_list):
@@ -196,7 +251,6 @@ class LocalShardGroup:
         tot = sum(a.counts_tensor().clone() for a in self.ads)
         for a in self.ads:
             a.counts_tensor().copy_(tot)
-        return [a.result() for a in self.ads]
 
 
 class _CAI:
@@ -257,6 +311,26 @@ class GpuShard:
         self.eng._check(self.lib.mpsf_hash_merge(self.ctx, which, keys.data_ptr(), vals.data_ptr(),
                                                  keys.numel(), self.sp))
 
+    def sparse_export(self, t):
+        """Non-empty words of a 4-byte MIN exchange buffer as (index, value) int32 tensors."""
+        import torch
+        cap = max(1 << 16, t.numel() // 8)
+        while True:
+            idx = torch.empty(cap, dtype=torch.int32, device=t.device)
+            val = torch.empty(cap, dtype=torch.int32, device=t.device)
+            k = self.lib.mpsf_sparse_export(self.ctx, t.data_ptr(), t.numel(), idx.data_ptr(), val.data_ptr(),
+                                            cap, self.sp)
+            if k >= 0:
+                return idx[:k], val[:k]
+            if k != E_OVERFLOW:
+                self.eng._check(int(k))
+            cap = t.numel()
+
+    def sparse_merge(self, t, idx, val):
+        idx, val = idx.contiguous(), val.contiguous()
+        self.eng._check(self.lib.mpsf_sparse_merge(self.ctx, t.data_ptr(), t.numel(), idx.data_ptr(),
+                                                   val.data_ptr(), idx.numel(), self.sp))
+
     def resolve(self, params):
         self.eng._check(self.lib.mpsf_resolve(self.ctx, self._p(params), self.bufs.verdict.data_ptr(),
                                               self.bufs.counts.data_ptr(), self.sp))
@@ -278,13 +352,16 @@ class GpuShard:
         from . import constants as K
         return self.bufs.counts[:8 * K.N_SCENARIOS * self.eng.world.n_clients].view(__import__("torch").int64)
 
+    def status(self):
+        """(status, global index of the first bad entry) of this shard's batch, not raised."""
+        s = _lib.Summary()
+        self.eng._check(self.lib.mpsf_get_summary(self.ctx, C.byref(s)))
+        self._summary = s
+        return int(s.status), int(s.error_index)
+
     def result(self):
-        """The shard's results, or None when its hash tables overflowed (they have grown)."""
-        from .errors import HashOverflow
-        try:
-            s = self.eng.summary()
-        except HashOverflow:
-            return None
+        """The shard's results (after :meth:`status` reported the batch ok)."""
+        s = self._summary
         return self.bufs.fetch(self.n, self.eng.world.n_clients, int(s.n_dedup), int(s.n_cancel), int(s.path))
 
 
@@ -391,7 +468,9 @@ class ShardedFold:
     blocks, tokens, n_req_ids)`` returns an object with order / blk_off / blocks / tok_off /
     tokens / progress / done / last_seq (``FaultEngine.fold`` on GPUs, the oracle on CPU)."""
 
-    def __init__(self, fold_fn, device="cpu", group=None):
+    def __init__(self, fold_fn, device=None, group=None):
+        if device is None:      # the process group's own device (NCCL needs CUDA tensors)
+            device = "cuda" if _dist().get_backend(group) == "nccl" else "cpu"
         self.fold_fn, self.device, self.group = fold_fn, device, group
 
     def fold(self, req, seq, nblk, ntok, progress, done, blocks, tokens, n_req_ids):
@@ -406,20 +485,19 @@ class ShardedFold:
         # int64 carriers (gloo and NCCL both gather them; values are < 2^32)
         g = [allgather_cat(torch.from_numpy(c.astype(np.int64)).to(self.device), self.group).cpu().numpy()
              for c in cols]
-        last = torch.tensor([int(local.last_seq) if len(req) else -1], dtype=torch.int64, device=self.device)
-        _dist().all_reduce(last, op=_dist().ReduceOp.MAX, group=self.group)
+        # last_consumed_seq = the seq of the last consumed snapshot of the whole stream: the
+        # last one of the highest rank that consumed any (recovery.py:83-92 advances it for every
+        # snapshot, monotone or not)
+        ws = _dist().get_world_size(self.group)
+        mine = torch.tensor([_dist().get_rank(self.group) if len(req) else -1, int(local.last_seq) if len(req) else 0],
+                            dtype=torch.int64, device=self.device)
+        allp = [torch.zeros_like(mine) for _ in range(ws)]
+        _dist().all_gather(allp, mine, group=self.group)
+        owners = [(int(p[0].item()), int(p[1].item())) for p in allp if int(p[0].item()) >= 0]
+        last_seq = max(owners)[1] if owners else 0
         m = len(g[0])
         merged = self.fold_fn(g[0].astype(np.uint32), np.zeros(m, np.uint64), g[1].astype(np.uint32),
                               g[2].astype(np.uint32), g[3].astype(np.uint32), g[4].astype(np.uint8),
                               g[5].astype(np.uint32), g[6].astype(np.uint32), n_req_ids)
-        merged.last_seq = max(int(last.item()), 0)
+        merged.last_seq = last_seq
         return merged
-
-
-def combine_verdicts_nccl(verdict: np.ndarray) -> np.ndarray:
-    """Elementwise MAX of per-shard client fates (used only by the replica fallback)."""
-    import torch
-    dist = _dist()
-    t = torch.from_numpy(verdict.view(np.uint8).astype(np.int32)).cuda()
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return t.to(torch.uint8).cpu().numpy().view(VERDICT_DTYPE)

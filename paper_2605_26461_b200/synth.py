@@ -317,6 +317,42 @@ def _expand_storm_torch(client, va, engine, access, n, seed, device):
     return out.view(torch.uint8).reshape(-1)
 
 
+def generate_mixed_storm(w: FlatWorld, n: int, seed: int, cross_frac: float = 0.1,
+                         specials: tuple = ()) -> np.ndarray:
+    """A large-world parity trace: half a config-3 storm (replayable duplicates), the config-2
+    recipe (every scenario class, wild pages, guard pages), and ``cross_frac`` of entries that
+    hit a storm page again from the same client with another (engine, access) -- SM read/write
+    and PREFETCH from every engine -- so one page carries several dedup groups (in the
+    claimed-slot layout the later groups go through the hash table).  ``specials`` =
+    ((position in [0, 1), kind, client), ...) places parse-time (kind 1..5) or SM-trap (8..12)
+    entries at fixed positions of the shuffled trace.  Synthetic worlds only (channel =
+    3 * client + engine)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    n_storm = n // 2
+    n_cross = int(n * cross_frac)
+    n_tr = n - n_storm - n_cross
+    storm = generate_storm(w, n_storm, max(1, n_storm // 10), seed)
+    tr = generate_trace(w, TraceSpec(n=n_tr, seed=seed + 1))
+    src = storm[rng.integers(0, n_storm, n_cross)]
+    combos = np.array([(K.ENG_SM, K.ACC_READ), (K.ENG_SM, K.ACC_WRITE), (K.ENG_SM, K.ACC_PREFETCH),
+                       (K.ENG_CE, K.ACC_PREFETCH), (K.ENG_PBDMA, K.ACC_PREFETCH), (K.ENG_CE, K.ACC_WRITE)],
+                      np.uint8)
+    pick = combos[rng.integers(0, len(combos), n_cross)]
+    cross = np.zeros(n_cross, ENTRY_DTYPE)
+    client = src["channel"] // 3
+    cross["va"] = (src["va"] & ~np.uint64(0xFFF)) | rng.integers(0, 4096, n_cross).astype(np.uint64)
+    cross["engine"] = pick[:, 0]
+    cross["access"] = pick[:, 1]
+    cross["channel"] = client * 3 + pick[:, 0]
+    cross["kind"] = K.KIND_TRANSLATION
+    cross["flags"] = K.ENTRY_FLAG_VALID
+    out = np.concatenate([storm, tr, cross])[rng.permutation(n)]
+    for pos, kind, c in specials:
+        i = min(n - 1, int(pos * n))
+        out[i] = (0, 3 * c + K.ENG_SM, K.ENG_SM, K.ACC_READ, kind, K.ENTRY_FLAG_VALID)
+    return out
+
+
 # -- config table (BASELINE.json "configs") -------------------------------------------
 
 CONFIGS = {

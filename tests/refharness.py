@@ -17,19 +17,9 @@ import sys
 
 import numpy as np
 
-REF_SRC = os.environ.get("MPSSIM_REF", "/root/reference/pkg/src")
-
-
-def reference_available() -> bool:
-    return os.path.isdir(os.path.join(REF_SRC, "mpssim"))
-
-
-def import_reference():
-    if REF_SRC not in sys.path:
-        sys.path.insert(0, REF_SRC)
-    import mpssim  # noqa: F401
-    from mpssim import faults, machine, pipeline  # noqa: F401
-    return mpssim
+# where the reference (and its tests) are: $MPSSIM_REF, /root/reference/pkg/src, or the
+# baseline/_ref install that travels to the GPU box (oracle/refpath.py)
+from oracle.refpath import REF_SRC, REF_TESTS, import_reference, reference_available  # noqa: E402,F401
 
 
 ENGINES = ("sm", "ce", "pbdma")

@@ -53,11 +53,15 @@ def run_both(eng, w, entries, p):
     return got, want
 
 
-def run_device(eng, w, entries, p, dense_dedup=False):
-    """The device-resident form (mpsf_process on device buffers, no host chunking); with
-    dense_dedup the world keeps one dedup slot per (page, group) whatever its size."""
+def run_device(eng, w, entries, p, layout="auto"):
+    """The device-resident form (mpsf_process on device buffers, no host chunking); ``layout``
+    forces the dedup-slot layout: "dense" one slot per (page, group) whatever the world size,
+    "sparse" the large-world layout (claimed page slots + hash for other groups, no per-page
+    first-eligible keys, so a client released before the drain takes the general path)."""
     import torch
-    eng.set_dense_dedup(dense_dedup)
+    if layout is True or layout is False:
+        layout = "dense" if layout else "auto"
+    eng.set_dedup_layout(layout)
     eng.upload_world(w)
     try:
         n = len(entries)
@@ -66,7 +70,7 @@ def run_device(eng, w, entries, p, dense_dedup=False):
         bufs = DeviceBuffers(n, w.n_clients)
         return eng.process_resident(d_in, n, bp(p), bufs)
     finally:
-        eng.set_dense_dedup(False)
+        eng.set_dedup_layout("auto")
 
 
 # -- golden fixtures from the reference ---------------------------------------------------
@@ -80,7 +84,17 @@ def test_classify_golden_c1(eng):
     assert np.array_equal(res.out["rid"], z["rid"])
 
 
-def test_reference_batches_golden(eng):
+@pytest.fixture
+def layout_eng(eng, request):
+    """The engine with the dedup-slot layout of the test's ``layout`` parameter."""
+    eng.set_dedup_layout(request.param)
+    yield eng
+    eng.set_dedup_layout("auto")
+
+
+@pytest.mark.parametrize("layout_eng", ["auto", "sparse"], indirect=True)
+def test_reference_batches_golden(layout_eng):
+    eng = layout_eng
     n = 0
     for flat, entries, p, expect in G.batches():
         eng.upload_world(flat)
@@ -90,7 +104,9 @@ def test_reference_batches_golden(eng):
     assert n == 400
 
 
-def test_truth_table_golden(eng):
+@pytest.mark.parametrize("layout_eng", ["auto", "sparse"], indirect=True)
+def test_truth_table_golden(layout_eng):
+    eng = layout_eng
     for row, flat, entries in G.truth_table():
         eng.upload_world(flat)
         res = eng.process(entries, BatchParams(isolation=row["isolation"]))
@@ -127,7 +143,7 @@ def test_random_batches_vs_oracle(eng, seed):
 
 
 @pytest.mark.parametrize("seed", range(4))
-@pytest.mark.parametrize("dense", [False, True])
+@pytest.mark.parametrize("dense", ["auto", "dense", "sparse"])
 def test_random_batches_device_form_vs_oracle(eng, seed, dense):
     rnd = random.Random(5000 + seed)
     for it in range(80):
@@ -139,7 +155,7 @@ def test_random_batches_device_form_vs_oracle(eng, seed, dense):
         assert_same(got, want, (seed, it, dense))
 
 
-@pytest.mark.parametrize("dense", [False, True])
+@pytest.mark.parametrize("dense", ["auto", "dense", "sparse"])
 def test_large_random_batch_device_form_vs_oracle(eng, dense):
     rnd = random.Random(91)
     for it in range(4):

@@ -91,3 +91,37 @@ def test_sharded_wild_hash_overflow_reruns(nshards):
     e["flags"] = 1
     bp = BatchParams(isolation=True)
     check(w, e, bp, run_sharded(w, e, bp, nshards))
+
+
+def test_sparse_export_merge_equals_min():
+    """mpsf_sparse_export / mpsf_sparse_merge: compaction of the non-empty words and the MIN
+    merge of another rank's pairs equal an elementwise unsigned MIN of the two buffers."""
+    import torch
+    from paper_2605_26461_b200.engine import FaultEngine
+    from paper_2605_26461_b200.parallel import GpuShard
+    eng = FaultEngine(0)
+    rng = np.random.default_rng(5)
+    n = 3_000_001
+    a = np.full(n, 0xFFFFFFFF, np.uint32)
+    b = a.copy()
+    ia, ib = rng.choice(n, 200_000, replace=False), rng.choice(n, 150_000, replace=False)
+    a[ia] = rng.integers(0, 1 << 31, len(ia))
+    b[ib] = rng.integers(0, 1 << 32, len(ib), dtype=np.uint64).astype(np.uint32) & 0xFFFFFFFE
+    ta = torch.from_numpy(a.view(np.int32).copy()).cuda()
+    tb = torch.from_numpy(b.view(np.int32).copy()).cuda()
+
+    class _Sh(GpuShard):
+        def __init__(self, e):
+            self.eng, self.lib, self.ctx = e, e.lib, e.ctx
+            import ctypes as C
+            self.sp = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    sh = _Sh(eng)
+    idx, val = sh.sparse_export(tb)
+    got_i = idx.cpu().numpy().astype(np.int64)
+    order = np.argsort(got_i)
+    assert np.array_equal(got_i[order], np.sort(ib))
+    assert np.array_equal(val.cpu().numpy().view(np.uint32)[order], b[np.sort(ib)])
+    sh.sparse_merge(ta, idx, val)
+    torch.cuda.synchronize()
+    assert np.array_equal(ta.cpu().numpy().view(np.uint32), np.minimum(a, b))
+    eng.close()

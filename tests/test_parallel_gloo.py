@@ -64,6 +64,20 @@ class C9Shard:
     def counts_tensor(self):
         return torch.from_numpy(self.e.counts.view(np.int64))
 
+    def sparse_export(self, t):
+        """CPU stand-in of mpsf_sparse_export: the non-empty words as (index, value)."""
+        idx = torch.nonzero(t != -1).flatten()
+        return idx.to(torch.int32), t[idx].clone()
+
+    def sparse_merge(self, t, idx, val):
+        flip = -(1 << 31)
+        cur = (t ^ flip).clone()
+        cur.scatter_reduce_(0, idx.long(), val ^ flip, reduce="amin")
+        t.copy_(cur ^ flip)
+
+    def status(self):
+        return 0, -1
+
     def result(self):
         return dict(out=self.out, dk=self.dk, di=self.di, ca=self.ca, verdict=self.verdict,
                     counts=self.e.counts.reshape(-1, K.N_SCENARIOS).copy())
@@ -105,9 +119,10 @@ def test_c9_mirror_single_shard_equals_sequential_oracle(monkeypatch):
         check_against_oracle(w, entries, bp, [res])
 
 
-def _worker(rank, ws, port, seeds, outdir):
+def _worker(rank, ws, port, seeds, outdir, sparse="auto"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    os.environ["MPSF_SPARSE_X"] = sparse
     dist.init_process_group("gloo", rank=rank, world_size=ws)
     import pickle
     results = {}
@@ -132,16 +147,67 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("ws", [2, 3])
-def test_sharded_gloo_equals_sequential_oracle(ws):
+@pytest.mark.parametrize("ws,sparse", [(2, "auto"), (3, "auto"), (2, "always")])
+def test_sharded_gloo_equals_sequential_oracle(ws, sparse):
+    """Dense all-reduce of every exchange buffer, and (``always``) the sparse form of the
+    page-sized ones: compacted (index, value) pairs all-gathered and MIN-merged."""
     import pickle
     seeds = list(range(1000, 1060))
     with tempfile.TemporaryDirectory() as d:
-        mp.start_processes(_worker, args=(ws, _free_port(), seeds, d), nprocs=ws, start_method="fork")
+        mp.start_processes(_worker, args=(ws, _free_port(), seeds, d, sparse), nprocs=ws, start_method="fork")
         per_rank = [pickle.load(open(os.path.join(d, f"r{r}.pkl"), "rb")) for r in range(ws)]
     for seed in seeds:
         w, entries, bp = make_case(seed)
         check_against_oracle(w, entries, bp, [per_rank[r][seed] for r in range(ws)])
+
+
+class _BadShard(C9Shard):
+    """A shard whose batch reports an entry error (what GpuShard.status() returns after the
+    device flagged a bad entry in this rank's range)."""
+
+    def __init__(self, w, entries, base, err):
+        super().__init__(w, entries, base)
+        self.err = err
+
+    def status(self):
+        return self.err
+
+
+def _err_worker(rank, ws, port, errs, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    from paper_2605_26461_b200.errors import SimError
+    w, entries, bp = make_case(1003)
+    cut = [len(entries) * r // ws for r in range(ws + 1)]
+    shard = _BadShard(w, entries[cut[rank]:cut[rank + 1]], cut[rank], errs[rank])
+    got = None
+    try:
+        ShardedFaultPath(shard).process(bp)
+    except SimError as exc:
+        got = (type(exc).__name__, getattr(exc, "index", None), str(exc))
+    with open(os.path.join(outdir, f"e{rank}.txt"), "w") as f:
+        f.write(repr(got))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("errs,want", [
+    # one rank has a bad entry: every rank raises it (nobody waits in a collective)
+    ([(0, -1), (-3, 17), (0, -1)], ("NoChannelAttribution", 17)),
+    # two kinds on two ranks: the highest-priority code, the smallest index of any bad entry
+    ([(-6, 5), (-4, 40), (0, -1)], ("EntryError", 5)),
+])
+def test_sharded_entry_error_raises_on_every_rank(errs, want):
+    ws = len(errs)
+    with tempfile.TemporaryDirectory() as d:
+        mp.start_processes(_err_worker, args=(ws, _free_port(), errs, d), nprocs=ws, start_method="fork")
+        got = [eval(open(os.path.join(d, f"e{r}.txt")).read()) for r in range(ws)]
+    for g in got:
+        assert g is not None and g[0] == want[0], got
+        assert str(want[1]) in g[2], got
+    if want[0] == "EntryError":
+        assert all(g[1] == want[1] and "-4" in g[2] for g in got), got    # E_BAD_ENTRY outranks E_VA
 
 
 # -- sharded batched translation (one MIN exchange of the first-PREFETCH page table) ----------

@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def test_reference_suite_passes_with_batch_bottom_half():
     env = dict(os.environ, PYTHONPATH=os.pathsep.join([ROOT, H.REF_SRC]))
-    tests_dir = os.path.join(os.path.dirname(H.REF_SRC), "tests")
+    tests_dir = H.REF_TESTS
     r = subprocess.run([sys.executable, "-m", "pytest", tests_dir, "-q", "-p", "no:cacheprovider",
                         "-p", "tests.shim_plugin"], cwd=ROOT, env=env, capture_output=True, text=True,
                        timeout=900)
