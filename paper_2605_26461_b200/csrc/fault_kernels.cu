@@ -34,9 +34,6 @@
 #include "mpsf_device.cuh"
 #include "mpsf_kernels.h"
 
-#ifndef MPSF_ABLATE
-#define MPSF_ABLATE 0   // experiment-only switches (tools/ablate.py); 0 in every shipped build
-#endif
 
 namespace mpsf {
 
@@ -525,15 +522,15 @@ __device__ __forceinline__ void scan_fast(const World& W, const View& v, const S
   }
   // first eligible record per in-range page: the epoch-1 first-isolation key of a client
   // released before the drain (trap / dead at start), so that case needs no extra pass
-  o.pa = (elig && d.inr && S.nrall && !(MPSF_ABLATE & 2)) ? S.nrall + d.slot : nullptr;
+  o.pa = (elig && d.inr && S.nrall) ? S.nrall + d.slot : nullptr;
   o.va = ok;
   // dedup insert (rule C2): dense (page, group) slot or claimed page slot; wild pages hash
-  const bool dd = (f & LF_DD) && !(MPSF_ABLATE & 4);
+  const bool dd = (f & LF_DD) != 0;
   const uint32_t group = (f >> LF_GROUP_SH) & 7u;
   o.pd = (dd && inw) ? S.dd + (W.dd_groups == 1 ? d.slot : d.slot * W.dd_groups + group) : nullptr;
   o.vd = ((uint32_t)gidx << 3) | group;
-  o.qn = elig && !inw && !(MPSF_ABLATE & 1);
-  o.qd = dd && !inw && !(MPSF_ABLATE & 1);
+  o.qn = elig && !inw;
+  o.qd = dd && !inw;
   o.c = c; o.eng = e.w & 0xFF; o.sid = sid; o.page = d.va >> 12;
   o.rec = pack_rec(d);
 }
@@ -623,7 +620,6 @@ __device__ __forceinline__ void scan_phase(const World& W, const Scratch& S, con
   const uint32_t base = (uint32_t)P.base_index;                          // < MAX_GIDX
   unsigned long long* const drec = kStaged ? S.drec + (P.base_index - S.drec_base) : nullptr;
   ldg_stream(in, n, [&](uint4 e0, uint32_t i0, bool ok0, uint4 e1, uint32_t i1, bool ok1) {
-    if (MPSF_ABLATE & 64) { if (e0.x == 0x12345 && e1.y == 0x777) atomicOr(S.ctrl + C_ERR, 1u); return; }
     ScanOut o0, o1;
     if (!ok0) e0.w = 0;                       // past the end: decodes as a skipped entry
     if (!ok1) e1.w = 0;
@@ -635,10 +631,11 @@ __device__ __forceinline__ void scan_phase(const World& W, const Scratch& S, con
     const uint32_t ra1 = o1.pa ? __ldcg(o1.pa) : 0u, rd1 = o1.pd ? __ldcg(o1.pd) : 0u;
     if (kStaged) {                                     // pass-1 records, two per lane (16 bytes)
       unsigned long long* rp = drec + i0;
-      if (ok1 && (((uintptr_t)rp & 15u) == 0)) *reinterpret_cast<ulonglong2*>(rp) = make_ulonglong2(o0.rec, o1.rec);
+      // streaming stores (evict-first): the records must not push the dedup slots out of the L2
+      if (ok1 && (((uintptr_t)rp & 15u) == 0)) __stcs(reinterpret_cast<ulonglong2*>(rp), make_ulonglong2(o0.rec, o1.rec));
       else {
-        if (ok0) rp[0] = o0.rec;
-        if (ok1) rp[1] = o1.rec;
+        if (ok0) __stcs(rp, o0.rec);
+        if (ok1) __stcs(rp + 1, o1.rec);
       }
     }
     min_g_if(o0.pa != nullptr, ra0, o0.pa, o0.va);
@@ -670,8 +667,7 @@ __device__ __forceinline__ void scan_phase(const World& W, const Scratch& S, con
 
 template <bool kStaged>
 __global__ void __launch_bounds__(BLOCK, 1) k_scan(World W, Scratch S, const mpsf_fault_entry* __restrict__ in,
-                                                   uint64_t n, Params P, unsigned long long* __restrict__ counts,
-                                                   uint32_t* __restrict__ count_part) {
+                                                   uint64_t n, Params P, unsigned long long* __restrict__ counts) {
   extern __shared__ __align__(128) uint8_t smem[];
   pdl_trigger();
   const Layout L = make_layout(W, kStaged, false);
@@ -679,7 +675,6 @@ __global__ void __launch_bounds__(BLOCK, 1) k_scan(World W, Scratch S, const mps
   __syncthreads();
   pdl_wait();
   scan_phase<kStaged>(W, S, v, L, smem, in, n, P, counts);
-  (void)count_part;
 }
 
 // ---- per-client resolution ------------------------------------------------------------------
@@ -790,10 +785,7 @@ __device__ __forceinline__ bool resolve_phase(const World& W, const Scratch& S, 
   return *s_general != 0;
 }
 
-__global__ void k_resolve(World W, Scratch S, Params P, mpsf_client_verdict* __restrict__ verdict,
-                          const uint32_t* __restrict__ count_part, uint32_t n_parts,
-                          unsigned long long* __restrict__ counts) {
-  (void)count_part; (void)n_parts; (void)counts;
+__global__ void k_resolve(World W, Scratch S, Params P, mpsf_client_verdict* __restrict__ verdict) {
   pdl_wait();
   pdl_trigger();
   if (blockIdx.x > 0) return;
@@ -987,7 +979,7 @@ __device__ __forceinline__ void fin_resolve(const World& W, const View& v, const
     key = dedup_key(c, (int)ceng, (int)sid, d.va >> 12);      // translation: engine == channel's
     uint32_t ri = wd >> 3;
     if (!(inw && wd != EMPTY32 && (wd & 7u) == group))
-      ri = (MPSF_ABLATE & 16384) ? EMPTY32 : hash_get(S.hdd, key);
+      ri = hash_get(S.hdd, key);
     dup = ri != (uint32_t)gidx;
     rep_ok = ri;                                                 // replayable: ok32 == idx
     rep = !dup;
@@ -1001,7 +993,7 @@ __device__ __forceinline__ void fin_resolve(const World& W, const View& v, const
   if (elig && !dup) {                                            // isolation mechanism (C3)
     if (a.needs_nr) {
       uint32_t nr = wn;
-      if (!inw && !(MPSF_ABLATE & 16384)) nr = hash_get(S.hnr, nr_key(c, a.e1keys ? 1 : 0, d.va >> 12));
+      if (!inw) nr = hash_get(S.hnr, nr_key(c, a.e1keys ? 1 : 0, d.va >> 12));
       mech = nr == ok ? 1u : 2u;
     } else {
       mech = (a.pe && we == ok) ? 3u : 2u;
@@ -1015,13 +1007,9 @@ __device__ __forceinline__ void fin_resolve(const World& W, const View& v, const
        ((unsigned long long)c << 48);
 }
 
-// Store that asks the L2 to keep the line (evict-last): the staged dedup keys are re-read by
-// k_lists after the finalize stream has passed through the L2.
-__device__ __forceinline__ void st_keep(unsigned long long* p, unsigned long long v) {
-  uint64_t pol;
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));   // pure: hoisted / shared
-  asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
-}
+// Staged dedup key (re-read by k_lists): an L2-allocating store with the default policy (an
+// evict-last policy here pinned up to 80 MB of keys at config 3 and pushed the dedup slots out).
+__device__ __forceinline__ void st_keep(unsigned long long* p, unsigned long long v) { __stcg(p, v); }
 
 // Spread the 32 bits of x to the even bits of a 64-bit word (bit i -> bit 2i).
 __device__ __forceinline__ unsigned long long spread2(uint32_t x) {
@@ -1080,8 +1068,8 @@ __device__ __forceinline__ void finalize_phase(const World& W, const Scratch& S,
     const unsigned long long* rec = S.drec + (P.base_index - S.drec_base);
     rec_stream(rec, n, [&](ulonglong2 r, uint32_t i0, bool ok0, bool ok1) {
       Dec d0, d1;
-      unpack_rec(v, slut, (ok0 && !(MPSF_ABLATE & 256)) ? r.x : 0ull, in, i0, d0);
-      unpack_rec(v, slut, (ok1 && !(MPSF_ABLATE & 256)) ? r.y : 0ull, in, i0 + 1, d1);
+      unpack_rec(v, slut, ok0 ? r.x : 0ull, in, i0, d0);
+      unpack_rec(v, slut, ok1 ? r.y : 0ull, in, i0 + 1, d1);
       body(d0, d1, i0, ok0, ok1);
     });
   } else {
@@ -1131,7 +1119,6 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize(World W, Scratch S, const
 // and writes it with 16-byte stores (no read-back of host memory -- each one is a PCIe round
 // trip).
 __device__ __forceinline__ void write_summary(const Scratch& S, unsigned long long tot, DevSummary* out) {
-  if (MPSF_ABLATE & 32768) return;
   static_assert(sizeof(DevSummary) == 4 * C_NCTRL + 24 && C_NCTRL % 4 == 0, "summary layout");
   uint32_t c[C_NCTRL];
 #pragma unroll
@@ -1161,14 +1148,11 @@ __global__ void __launch_bounds__(SEG_CHUNKS) k_lists(Scratch S, const mpsf_faul
   }
   __shared__ unsigned long long s_base;
   __shared__ unsigned long long s_w[32];
-  unsigned long long t_start = 0;
-  if (MPSF_ABLATE & 8192) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t seg = blockIdx.x;
   // base: counts of all earlier segments
   unsigned long long acc = 0;
-  if (!(MPSF_ABLATE & 2048))
-    for (uint64_t i = threadIdx.x; i < seg; i += blockDim.x) acc += __ldcg(S.segcnt + i);
+  for (uint64_t i = threadIdx.x; i < seg; i += blockDim.x) acc += __ldcg(S.segcnt + i);
   if (threadIdx.x == 0) s_base = 0;
   __syncthreads();
 #pragma unroll
@@ -1198,7 +1182,7 @@ __global__ void __launch_bounds__(SEG_CHUNKS) k_lists(Scratch S, const mpsf_faul
   const uint32_t g0 = (uint32_t)(base_index + q * WCHUNK);
   // cancel list: the warp writes its 32 chunks one at a time, lane l the chunk's entries 2l, 2l+1
   // (consecutive positions: coalesced stores)
-  if (!(MPSF_ABLATE & 512)) {
+  {
     const unsigned long long below = (1ull << (2 * lane)) - 1ull;
     for (int j = 0; j < 32; ++j) {
       const unsigned long long cm = __shfl_sync(0xFFFFFFFFu, mk.x, j);
@@ -1218,7 +1202,7 @@ __global__ void __launch_bounds__(SEG_CHUNKS) k_lists(Scratch S, const mpsf_faul
   {
     __shared__ uint16_t s_code[SEG_CHUNKS / 32][32 * WCHUNK];   // per warp: its 32 chunks
     uint16_t* code = s_code[warp];
-    unsigned long long dm_l = (MPSF_ABLATE & 1024) ? 0ull : mk.y;
+    unsigned long long dm_l = mk.y;
     const uint32_t cnt = (uint32_t)__popcll(dm_l);
     uint32_t inc = cnt;
 #pragma unroll
@@ -1253,19 +1237,6 @@ __global__ void __launch_bounds__(SEG_CHUNKS) k_lists(Scratch S, const mpsf_faul
       }
     }
   }
-  if (MPSF_ABLATE & 8192) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned long long t_end;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
-      uint32_t smid;
-      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      reinterpret_cast<unsigned long long*>(cancel)[(nq + 2) / 2 * 0 + 4 * blockIdx.x + 0] = t_start;
-      reinterpret_cast<unsigned long long*>(cancel)[4 * blockIdx.x + 1] = t_end;
-      reinterpret_cast<unsigned long long*>(cancel)[4 * blockIdx.x + 2] = smid;
-      reinterpret_cast<unsigned long long*>(cancel)[4 * blockIdx.x + 3] = mk.y;
-    }
-  }
 }
 
 // Batch summary: error / overflow words and the list lengths (sum of the segment counters).
@@ -1282,6 +1253,8 @@ __global__ void k_summary(const Scratch S, uint64_t nseg, DevSummary* out) {
   __syncthreads();
   if (threadIdx.x == 0) write_summary(S, s_tot, out);
 }
+
+#include "fx_passes.cuh"
 
 // ---- batched translation kernels ------------------------------------------------------------
 // T1: the first PREFETCH index per managed page (the only in-batch dependency of resolve_va).
@@ -1509,10 +1482,8 @@ static bool staged_fits(const World& W) {
          make_layout(W, true, true).total <= (uint32_t)SMEM_MAX;
 }
 
-uint32_t count_parts_needed(const World& W) {
-  (void)W;
-  return 0u;   // k_scan folds its block counts with atomics
-}
+// the row-table passes (fx_passes.cuh): fixed layout and at most one range base per skip slot
+static bool fx_fits(const World& W) { return staged_fits(W) && W.exact1 && W.n_skip + 1 <= FX_SKIP; }
 
 template <bool kStaged>
 static void set_attrs() {
@@ -1523,6 +1494,8 @@ static void set_attrs() {
   cudaFuncSetAttribute(k_general<kStaged, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(k_general<kStaged, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(k_finalize<kStaged>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(fx::k_scan_fx, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(fx::k_finalize_fx, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   done = true;
 }
 
@@ -1539,7 +1512,7 @@ static void launch_pdl(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStr
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = (MPSF_ABLATE & 65536) ? 0 : 1;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, k, args...);
@@ -1556,19 +1529,21 @@ static int clamp_grid(int g, uint64_t n) {
 
 template <bool kStaged>
 static int scan_t(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
-                  unsigned long long* counts, uint32_t* count_part, cudaStream_t st, const Marker& mk,
-                  uint32_t* parts) {
+                  unsigned long long* counts, cudaStream_t st, const Marker& mk) {
   set_attrs<kStaged>();
-  *parts = 0;
   if (n == 0) return 0;
+  if (kStaged && fx_fits(W)) {
+    const int g = clamp_grid(grid_for(fx::k_scan_fx, fx::SCAN_BYTES), n);
+    launch_pdl(fx::k_scan_fx, dim3(g), dim3(BLOCK), fx::SCAN_BYTES, st, W, S, in, n, P, counts);
+    mk.mark("k_scan");
+    return ok_or_err();
+  }
   const uint32_t smem = make_layout(W, kStaged, false).total;
   int g = grid_for(k_scan<kStaged>, smem);
   if (kStaged && g > (int)(2 * sm_count())) g = 2 * sm_count();
   g = clamp_grid(g, n);
-  launch_pdl(k_scan<kStaged>, dim3(g), dim3(BLOCK), smem, st, W, S, in, n, P, counts, count_part);
+  launch_pdl(k_scan<kStaged>, dim3(g), dim3(BLOCK), smem, st, W, S, in, n, P, counts);
   mk.mark("k_scan");
-  // partial rows accumulate across launches and were zeroed by k_init: reduce all of them
-  *parts = kStaged ? count_parts_needed(W) : 0u;
   return ok_or_err();
 }
 
@@ -1594,6 +1569,12 @@ static int finalize_t(const World& W, const Scratch& S, const mpsf_fault_entry* 
                       mpsf_out_record* out, uint64_t q_base, cudaStream_t st, const Marker& mk) {
   set_attrs<kStaged>();
   if (n == 0) return 0;
+  if (kStaged && fx_fits(W)) {
+    const int g = clamp_grid(grid_for(fx::k_finalize_fx, fx::FIN_BYTES), n);
+    launch_pdl(fx::k_finalize_fx, dim3(g), dim3(BLOCK), fx::FIN_BYTES, st, W, S, n, P, out, q_base);
+    mk.mark("k_finalize");
+    return ok_or_err();
+  }
   const uint32_t smem = make_layout(W, kStaged, true).total;
   const int g = clamp_grid(grid_for(k_finalize<kStaged>, smem), n);
   launch_pdl(k_finalize<kStaged>, dim3(g), dim3(BLOCK), smem, st, W, S, in, n, P, out, q_base);
@@ -1606,17 +1587,14 @@ uint64_t chunks_for(uint64_t n) { return (n + WCHUNK - 1) / WCHUNK; }
 uint64_t segments_for(uint64_t n) { return (chunks_for(n) + SEG_CHUNKS - 1) / SEG_CHUNKS; }
 
 int launch_scan(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
-                unsigned long long* counts, uint32_t* count_part, cudaStream_t st, const Marker& mk, uint32_t* parts) {
-  return staged_fits(W) ? scan_t<true>(W, S, in, n, P, counts, count_part, st, mk, parts)
-                        : scan_t<false>(W, S, in, n, P, counts, count_part, st, mk, parts);
+                unsigned long long* counts, cudaStream_t st, const Marker& mk) {
+  return staged_fits(W) ? scan_t<true>(W, S, in, n, P, counts, st, mk)
+                        : scan_t<false>(W, S, in, n, P, counts, st, mk);
 }
 
 int launch_resolve(const World& W, const Scratch& S, const Params& P, mpsf_client_verdict* verdict,
-                   const uint32_t* count_part, uint32_t parts, unsigned long long* counts, cudaStream_t st,
-                   const Marker& mk) {
-  const uint32_t bins = NSCEN * W.n_clients;
-  const uint32_t rblocks = 1 + (parts ? (bins + 255) / 256 : 0);
-  launch_pdl(k_resolve, dim3(rblocks), dim3(256), 0, st, W, S, P, verdict, count_part, parts, counts);
+                   cudaStream_t st, const Marker& mk) {
+  launch_pdl(k_resolve, dim3(1), dim3(256), 0, st, W, S, P, verdict);
   mk.mark("k_resolve");
   return ok_or_err();
 }

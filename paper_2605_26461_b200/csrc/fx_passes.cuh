@@ -1,0 +1,513 @@
+// Streaming passes for worlds within the fixed shared-memory layout (the common case: every
+// BASELINE config).  Included by fault_kernels.cu after its helpers.
+//
+// Same computation as scan_fast / finalize_phase (rules C0-C9 of SURVEY.md Appendix C; the
+// reference semantics they restate are cited there), laid out for instruction count -- both
+// passes are issue-bound -- rather than generality:
+//  * the world tables are rows read with one shared load per step: channel row (client word,
+//    skip-table span / shift / offset) replicated 8x so a quarter-warp's 16-byte loads never
+//    share a bank group; skip slot {range at the slot start, base of the next range inside the
+//    slot}; range row {base, end, page-state slot, attributes}.  Attribution
+//    (MemoryModel.range_at, memory.py:233-237) is three dependent loads, no loop, no compare
+//    against a second row;
+//  * one classification LUT indexed by (min(engine, 3), min(access, 3), range class, page state)
+//    also rejects bad engine / access values;
+//  * the pass-1 record carries exactly what pass 2 indexes with (scenario, dedup group,
+//    mechanism class, location, channel engine, client, range index | page high bits, page slot |
+//    page low bits) plus one "known duplicate" bit: pass 1 already saw a smaller index on the
+//    entry's dedup slot, so pass 2 needs no dedup lookup for it unless its cancel flag depends on
+//    the representative's index.
+namespace fx {
+
+constexpr uint32_t NCH = FX_CH + 1;            // channel rows (the last: invalid channel)
+constexpr uint32_t CH_COPIES = 8;              // replicas of a channel row (one per quarter-warp lane)
+constexpr uint32_t LUT2_XK = 16 * 16 * 8;      // [min(eng,3) * 4 + min(acc,3)][range class][state]
+constexpr uint32_t LUT2_N = LUT2_XK + 16;      // + the non-translation kinds
+
+__host__ __device__ constexpr uint32_t a16(uint32_t x) { return (x + 15u) & ~15u; }
+
+// shared-memory layout (fixed offsets: every table access is an immediate-offset load)
+constexpr uint32_t O_LUT = 0;
+constexpr uint32_t O_SLUT = a16(O_LUT + 4 * LUT2_N);
+constexpr uint32_t O_CHAN = a16(O_SLUT + 4 * 32);
+constexpr uint32_t O_SKIP = O_CHAN + NCH * CH_COPIES * 16;
+constexpr uint32_t O_ROWS = O_SKIP + FX_SKIP * 8;
+constexpr uint32_t O_PASS = O_ROWS + FX_R * 16;
+// pass 1
+constexpr uint32_t O_QUEUE = O_PASS;
+constexpr uint32_t O_C64 = O_QUEUE + WARPS * QCAP * 16;
+constexpr uint32_t O_ISO = a16(O_C64 + 8 * (3 * FX_C + 2));
+constexpr uint32_t O_R32 = O_ISO + 4 * 3 * FX_C * 32;
+constexpr uint32_t O_CNT = O_R32 + 4 * 2 * FX_R;
+constexpr uint32_t O_USED = O_CNT + 4 * NSCEN * FX_C;
+constexpr uint32_t SCAN_BYTES = O_USED + 16;
+// pass 2
+constexpr uint32_t O_FCL = O_PASS;
+constexpr uint32_t O_RRID = O_FCL + 32 * FX_C;
+constexpr uint32_t O_EXT = O_RRID + 4 * FX_R;
+constexpr uint32_t O_NR0 = O_EXT + 4 * FX_R;
+constexpr uint32_t O_SLOWQ = O_NR0 + 4 * FX_R;
+constexpr uint32_t FIN_BYTES = O_SLOWQ + WARPS * 96 * 16;
+static_assert(SCAN_BYTES <= 227 * 1024 && FIN_BYTES <= 227 * 1024, "fixed layout exceeds shared memory");
+
+__device__ __forceinline__ uint32_t lut2_word(uint32_t idx, bool isolation) {
+  if (idx >= LUT2_XK) return lut_word((int)(LUT_XK + (idx - LUT2_XK)), isolation);
+  const uint32_t st = idx & 7, rcls = (idx >> 3) & 15, ea = idx >> 7;
+  const uint32_t e = ea >> 2, a = ea & 3;
+  if (e > 2 || a > 2) return LF_VALID | LF_BAD;
+  return lut_word((int)(((e * 3 + a) * 16 + rcls) * 8 + st), isolation);
+}
+
+// World tables into shared memory (both passes).
+__device__ __forceinline__ void stage_tables(uint8_t* sm, const World& W, bool isolation) {
+  const uint32_t tid = threadIdx.x, nb = blockDim.x;
+  uint32_t* lut = reinterpret_cast<uint32_t*>(sm + O_LUT);
+  for (uint32_t i = tid; i < LUT2_N; i += nb) lut[i] = lut2_word(i, isolation);
+  uint32_t* slut = reinterpret_cast<uint32_t*>(sm + O_SLUT);
+  if (tid < 32) slut[tid] = scen_word((int)tid, isolation);
+  uint4* ch = reinterpret_cast<uint4*>(sm + O_CHAN);
+  const uint32_t nch1 = W.n_channels + 1;
+  for (uint32_t i = tid; i < nch1 * CH_COPIES; i += nb) ch[i] = __ldg(W.chan4 + i / CH_COPIES);
+  uint2* sk = reinterpret_cast<uint2*>(sm + O_SKIP);
+  for (uint32_t i = tid; i <= W.n_skip; i += nb) sk[i] = __ldg(W.skip2 + i);
+  uint4* rows = reinterpret_cast<uint4*>(sm + O_ROWS);
+  for (uint32_t i = tid; i <= W.n_ranges; i += nb) rows[i] = __ldg(W.row4 + i);
+}
+
+// Decoded entry.  f = LUT word (0: skipped or malformed -- the error bits are raised here).
+struct D {
+  uint32_t f, cw, page, slot, k;
+  bool inr, grd;
+};
+
+__device__ __forceinline__ D decode(const uint8_t* sm, const uint8_t* __restrict__ ps, uint32_t nch, uint32_t copy16,
+                                    const Scratch& S, uint4 e, uint32_t gidx) {
+  D d;
+  const uint32_t w3 = e.w, ek = (w3 >> 16) & 0xFFu;
+  const uint32_t ch = min(e.z, nch);
+  const uint4 cr = *reinterpret_cast<const uint4*>(sm + O_CHAN + ch * (CH_COPIES * 16) + copy16);
+  d.page = __funnelshift_r(e.x, e.y, 12);
+  const uint32_t j = min((d.page - cr.y) >> cr.z, cr.w >> 16);
+  const uint2 sk = reinterpret_cast<const uint2*>(sm + O_SKIP)[(cr.w & 0xFFFFu) + j];
+  d.k = sk.x + (d.page >= sk.y ? 1u : 0u);
+  const uint4 row = reinterpret_cast<const uint4*>(sm + O_ROWS)[d.k];
+  // translation entries below 2^44 - 4 KiB look their range up (no range reaches higher)
+  const bool look = ek == 0 && e.y < 0x1000u && d.page != 0xFFFFFFFFu;
+  d.inr = look && d.page >= row.x && d.page < row.y;
+  d.grd = look && d.page == row.y;
+  d.slot = row.z + (d.page - row.x);
+  uint32_t st = row.w & 7u;
+  if (d.inr && (row.w & ROW_PERPAGE)) st = ps[d.slot] & 7u;
+  const uint32_t eng = w3 & 0xFFu, acc = (w3 >> 8) & 0xFFu;
+  const uint32_t ea = min(eng, 3u) * 4 + min(acc, 3u);
+  const uint32_t idx = ek == 0 ? ea * 128 + (d.inr ? ((row.w >> 1) & 0x78u) + st : 64u) : LUT2_XK + min(ek, 15u);
+  const uint32_t f = reinterpret_cast<const uint32_t*>(sm + O_LUT)[idx];
+  d.cw = cr.x;
+  const uint32_t ceng = (cr.x >> 16) & 3u;
+  const bool bad = !(cr.x & CH_VALID) || (f & LF_BAD) || (ek == 0 && (eng != ceng || e.y >= (1u << 21)));
+  const bool valid = (w3 >> 24) & MPSF_ENTRY_VALID;
+  if (valid && bad) {
+    const uint32_t bit = !(cr.x & CH_VALID) ? EB_NO_CHANNEL
+                         : (f & LF_BAD) ? EB_BAD_ENTRY : (eng != ceng ? EB_MISMATCH : EB_VA);
+    raise_err(S, bit, gidx);
+  }
+  d.f = (valid && !bad) ? f : 0u;
+  return d;
+}
+
+// pass-1 record: lo = scenario [4:0] | dedup group [7:5] | mechanism class [9:8] | location
+// [11:10] (LOC_*) | channel engine [13:12] | client [19:14] | range index, or page bits 32.. of a
+// wild page, [30:20] | known duplicate [31];  hi = page-state slot (in range / guard) or page
+// bits 0..31
+constexpr uint32_t R_KDUP = 1u << 31;
+
+// Pass 1 over [0, n) (global index P.base_index + i).
+__device__ __forceinline__ void scan_body(const World& W, const Scratch& S, uint8_t* sm,
+                                          const mpsf_fault_entry* __restrict__ in, uint64_t n, const Params& P) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t copy16 = (lane & (CH_COPIES - 1)) * 16;
+  const uint32_t C = W.n_clients, nch = W.n_channels;
+  const uint32_t base = (uint32_t)P.base_index;
+  const bool sparse = W.dd_groups == 1;
+  uint32_t* counts = reinterpret_cast<uint32_t*>(sm + O_CNT);
+  uint32_t* iso = reinterpret_cast<uint32_t*>(sm + O_ISO) + warp;
+  uint32_t* r32 = reinterpret_cast<uint32_t*>(sm + O_R32);
+  uint32_t* used = reinterpret_cast<uint32_t*>(sm + O_USED);
+  unsigned long long* c64 = reinterpret_cast<unsigned long long*>(sm + O_C64);
+  QOp* q = reinterpret_cast<QOp*>(sm + O_QUEUE) + warp * QCAP;
+  uint32_t qn = 0;
+  unsigned long long* const drec = S.drec + (P.base_index - S.drec_base);
+  const uint8_t* __restrict__ ps = W.page_state;
+
+  struct O {
+    uint32_t* pd; uint32_t vd;     // dedup slot and its value
+    uint32_t* pa; uint32_t va;     // first eligible record of the page (dense worlds)
+    bool qn, qd;
+    uint32_t lo, hi;               // record
+    uint32_t ok;
+    uint64_t page;                 // the entry's page (dedup / NR keys)
+  };
+  // the per-entry work up to the global pre-check loads
+  auto first = [&](uint4 e, uint32_t gidx, O& o) {
+    const D d = decode(sm, ps, nch, copy16, S, e, gidx);
+    const uint32_t f = d.f, c = d.cw & 0xFFFFu, sid = f & LF_S;
+    red_add_s(f != 0, counts + (f ? c * NSCEN + sid : 0u));
+    if (f & (LF_TRAP | LF_FATAL)) {                    // rare: traps and fatal reports
+      const bool sa = (d.cw >> 18) & 1u;
+      const uint32_t ceng = (d.cw >> 16) & 3u;
+      if (f & LF_TRAP) {
+        smin64(sa ? c64 + 2 * C + c : c64 + 3 * C + 1, ((unsigned long long)gidx << 8) | sid);
+      } else {
+        const uint32_t okf = ((f & LF_REPL) ? 0u : 0x80000000u) | gidx;
+        smin64(sa ? c64 + C + c : (ceng == 1 ? c64 + c : c64 + 3 * C), ((unsigned long long)okf << 8) | sid);
+      }
+    }
+    o.ok = ((f & LF_REPL) ? 0u : 0x80000000u) | gidx;
+    const bool elig = (f & LF_ELIG) != 0;
+    const uint32_t m = (f >> LF_M_SH) & 3u;
+    const bool inw = d.inr || d.grd;
+    min_s_if(elig, iso + (m * C + c) * 32, o.ok);
+    min_s_if(elig && (d.grd || (d.inr && m == 2)), r32 + (d.grd ? FX_R : 0u) + d.k, o.ok);
+    o.pa = (elig && d.inr && S.nrall) ? S.nrall + d.slot : nullptr;
+    o.va = o.ok;
+    const bool dd = (f & LF_DD) != 0;
+    const uint32_t group = (f >> LF_GROUP_SH) & 7u;
+    o.pd = (dd && inw) ? S.dd + (sparse ? d.slot : d.slot * 5 + group) : nullptr;
+    o.vd = (gidx << 3) | group;
+    o.qn = elig && !inw;
+    o.qd = dd && !inw;
+    const uint32_t loc = f ? (d.inr ? LOC_IN : (d.grd ? LOC_GUARD : LOC_NONE)) : LOC_SKIP;
+    const uint32_t pagehi = (e.y >> 12) & 0x7FFu;
+    o.lo = (f & 0xFFu) | ((f >> (LF_M_SH - 8)) & 0x300u) | (loc << 10) | ((d.cw >> 4) & 0x3000u) | ((c & 63u) << 14) |
+           ((inw ? d.k : pagehi) << 20);
+    o.hi = inw ? d.slot : d.page;
+    o.page = (uint64_t)d.page | ((uint64_t)pagehi << 32);
+  };
+  auto key_of = [&](const O& o) {     // the entry's dedup key
+    const uint32_t c = (o.lo >> 14) & 63u, ceng = (o.lo >> 12) & 3u, sid = o.lo & 31u;
+    return dedup_key(c, (int)ceng, (int)sid, o.page);
+  };
+  auto nrkey_of = [&](const O& o) { return nr_key((o.lo >> 14) & 63u, 0, o.page); };
+
+  ldg_stream(in, n, [&](uint4 e0, uint32_t i0, bool ok0, uint4 e1, uint32_t i1, bool ok1) {
+    if (!ok0) e0.w = 0;
+    if (!ok1) e1.w = 0;
+    O o0, o1;
+    first(e0, base + i0, o0);
+    const uint32_t ra0 = o0.pa ? __ldcg(o0.pa) : 0u, rd0 = o0.pd ? __ldcg(o0.pd) : EMPTY32;
+    first(e1, base + i1, o1);
+    const uint32_t ra1 = o1.pa ? __ldcg(o1.pa) : 0u, rd1 = o1.pd ? __ldcg(o1.pd) : EMPTY32;
+    // a smaller index of the same key already in the slot: a duplicate whatever comes later
+    if (rd0 != EMPTY32 && (rd0 & 7u) == (o0.vd & 7u) && rd0 < o0.vd) o0.lo |= R_KDUP;
+    if (rd1 != EMPTY32 && (rd1 & 7u) == (o1.vd & 7u) && rd1 < o1.vd) o1.lo |= R_KDUP;
+    unsigned long long* rp = drec + i0;
+    const unsigned long long r0 = (unsigned long long)o0.lo | ((unsigned long long)o0.hi << 32);
+    const unsigned long long r1 = (unsigned long long)o1.lo | ((unsigned long long)o1.hi << 32);
+    if (ok1 && (((uintptr_t)rp & 15u) == 0)) __stcs(reinterpret_cast<ulonglong2*>(rp), make_ulonglong2(r0, r1));
+    else {
+      if (ok0) __stcs(rp, r0);
+      if (ok1) __stcs(rp + 1, r1);
+    }
+    min_g_if(o0.pa != nullptr, ra0, o0.pa, o0.va);
+    min_g_if(o1.pa != nullptr, ra1, o1.pa, o1.va);
+    if (!sparse) {
+      min_g_if(o0.pd != nullptr, rd0, o0.pd, o0.vd);
+      min_g_if(o1.pd != nullptr, rd1, o1.pd, o1.vd);
+    } else {
+      if (o0.pd && !(o0.lo & R_KDUP)) claim_resolve(S, used, o0.pd, o0.vd, rd0, key_of(o0));
+      if (o1.pd && !(o1.lo & R_KDUP)) claim_resolve(S, used, o1.pd, o1.vd, rd1, key_of(o1));
+    }
+    if (__any_sync(0xFFFFFFFFu, o0.qn || o0.qd || o1.qn || o1.qd)) {
+      q_push(q, qn, o0.qn, nrkey_of(o0), o0.va, 1, S, used);
+      q_push(q, qn, o0.qd, key_of(o0), o0.vd >> 3, 0, S, used);
+      q_push(q, qn, o1.qn, nrkey_of(o1), o1.va, 1, S, used);
+      q_push(q, qn, o1.qd, key_of(o1), o1.vd >> 3, 0, S, used);
+    }
+  });
+  q_drain(q, qn, S, used);
+}
+
+__global__ void __launch_bounds__(BLOCK, 1) k_scan_fx(World W, Scratch S, const mpsf_fault_entry* __restrict__ in,
+                                                      uint64_t n, Params P, unsigned long long* __restrict__ counts) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  pdl_trigger();
+  const uint32_t tid = threadIdx.x, nb = blockDim.x, C = W.n_clients, R1 = W.n_ranges + 1;
+  stage_tables(sm, W, P.flags & MPSF_PF_ISOLATION);
+  unsigned long long* c64 = reinterpret_cast<unsigned long long*>(sm + O_C64);
+  for (uint32_t i = tid; i < 3 * C + 2; i += nb) c64[i] = EMPTY64;
+  uint32_t* iso = reinterpret_cast<uint32_t*>(sm + O_ISO);
+  for (uint32_t i = tid; i < 3 * 32 * C; i += nb) iso[i] = EMPTY32;
+  uint32_t* r32 = reinterpret_cast<uint32_t*>(sm + O_R32);
+  for (uint32_t i = tid; i < R1; i += nb) { r32[i] = EMPTY32; r32[FX_R + i] = EMPTY32; }
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(sm + O_CNT);
+  for (uint32_t i = tid; i < NSCEN * C; i += nb) cnt[i] = 0;
+  uint32_t* used = reinterpret_cast<uint32_t*>(sm + O_USED);
+  if (tid < 2) used[tid] = 0;
+  __syncthreads();
+  pdl_wait();
+  scan_body(W, S, sm, in, n, P);
+  __syncthreads();
+  for (uint32_t i = tid; i < NSCEN * C; i += nb)
+    if (cnt[i]) atomicAdd(counts + i, (unsigned long long)cnt[i]);
+  // fold the block-local minima into the global ones (same slots as flush_minima)
+  for (uint32_t i = tid; i < 3 * C; i += nb) {
+    const uint32_t* w = iso + i * 32;
+    uint32_t m = EMPTY32;
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) m = min(m, w[k]);
+    uint32_t* g = (i < C ? S.iso1 : (i < 2 * C ? S.iso2 : S.iso3)) + (i % C);
+    if (m != EMPTY32) atomicMin(g, m);
+    const unsigned long long t = c64[i];
+    if (t != EMPTY64) atomicMin(i < C ? S.ft_ce + i : (i < 2 * C ? S.ft_sa + (i - C) : S.trap_sa + (i - 2 * C)), t);
+  }
+  if (tid < 2) {
+    const unsigned long long t = c64[3 * C + tid];
+    if (t != EMPTY64) atomicMin(tid ? S.trap_mps : S.ft_gr, t);
+  }
+  for (uint32_t i = tid; i < W.n_ranges; i += nb) {
+    if (r32[i] != EMPTY32) atomicMin(S.ext + i, r32[i]);
+    if (r32[FX_R + i] != EMPTY32) atomicMin(S.nr0 + i, r32[FX_R + i]);
+  }
+  if (tid < 2 && used[tid]) atomicAdd(S.ctrl + C_HASH_DD + tid, used[tid]);
+}
+
+// ---- pass 2 ----------------------------------------------------------------------------------
+// Per entry: the OutRecord from the record, the client's decision row and at most two loads (its
+// dedup slot, its first-isolation word).  The common path has no data-dependent branch: every
+// candidate value is computed and selected (a rare path inside a warp's 64 entries would make
+// the whole warp execute it).  Entries that need a wild-page hash lookup (no range and no guard
+// page, or a claimed page slot held by another dedup group) are queued per warp and resolved 32
+// at a time; their mask bits are OR-ed into the chunk masks afterwards.
+constexpr uint32_t SQ_CAP = 96;   // per-warp slow queue: < 32 kept + 64 per chunk
+
+// decision word per scenario id (slot 31: skipped entry)
+constexpr uint32_t S2_DD = 1u << 8, S2_SERV = 1u << 9, S2_ELIG = 1u << 10, S2_FATAL = 1u << 11,
+                   S2_TRAP = 1u << 12, S2_NONREPL = 1u << 31;   // [6:0] static verdict bits
+
+__device__ __forceinline__ uint32_t slut2_word(uint32_t sid, bool isolation) {
+  const uint32_t f = scen_word((int)sid, isolation);
+  if (!f) return 0u;
+  const bool trap = f & LF_TRAP, elig = f & LF_ELIG, serv = f & LF_SERV;
+  const uint32_t outcome = trap ? 0u : (elig ? 2u : (serv ? 1u : 3u));
+  return outcome | ((f & LF_REPL) ? 0x40u : 0u) | ((f & LF_DD) ? S2_DD : 0u) | (serv ? S2_SERV : 0u) |
+         (elig ? S2_ELIG : 0u) | ((!trap && !elig && !serv) ? S2_FATAL : 0u) | (trap ? S2_TRAP : 0u) |
+         ((f & LF_REPL) ? 0u : S2_NONREPL);
+}
+
+// per-client decision row (32 B): epoch-1 threshold, applied trap, applied fatal reports, kill tie,
+// flags (bit0: benign always cancelled, bit1: same on a CE channel, bit2: epoch-1 keys are pass 1's)
+struct Fc2 {
+  uint32_t rel_lt, trap_ok, ft0, ft1;
+  uint32_t tie, flags, pad0, pad1;
+};
+
+__device__ __forceinline__ Fc2 fc2_of(const FinClient& f) {
+  Fc2 r;
+  // epoch 1 iff rel < ok32 (ok32 < 2^32 - 1):  ok32 >= rel + 1, with rel = REL_PRE -> 0, REL_NONE -> ~0
+  r.rel_lt = f.rel < 0 ? 0u : (f.rel >= (long long)0xFFFFFFFEll ? 0xFFFFFFFFu : (uint32_t)f.rel + 1u);
+  r.trap_ok = f.trap_ok; r.ft0 = f.ft0; r.ft1 = f.ft1; r.tie = f.tie;
+  r.flags = (f.bflags & 3u) | (f.pre_nrall ? 4u : 0u);
+  r.pad0 = r.pad1 = 0;
+  return r;
+}
+
+__device__ __forceinline__ uint32_t ldcg_if(bool p, const uint32_t* a, uint32_t dflt) {
+  uint32_t v;
+  asm("{.reg .pred q; setp.ne.u32 q, %2, 0; mov.b32 %0, %3; @q ld.global.cg.u32 %0, [%1];}"
+      : "=r"(v) : "l"(a), "r"((uint32_t)p), "r"(dflt));
+  return v;
+}
+
+__global__ void __launch_bounds__(BLOCK, 1) k_finalize_fx(World W, Scratch S, uint64_t n, Params P,
+                                                          mpsf_out_record* __restrict__ out, uint64_t q_base) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  pdl_trigger();
+  const uint32_t tid = threadIdx.x, nb = blockDim.x;
+  const bool isolation = P.flags & MPSF_PF_ISOLATION;
+  stage_tables(sm, W, isolation);
+  uint32_t* slut2 = reinterpret_cast<uint32_t*>(sm + O_SLUT);      // (the pass-1 scenario words are not needed)
+  if (tid < 32) slut2[tid] = tid == 31 ? 0u : slut2_word(tid, isolation);
+  uint32_t* rrid = reinterpret_cast<uint32_t*>(sm + O_RRID);
+  for (uint32_t i = tid; i < FX_R; i += nb) rrid[i] = i <= W.n_ranges ? __ldg(W.rrid + i) : NO_RID;
+  pdl_wait();
+  if (__ldcg(S.ctrl + C_ERR) != 0) return;
+  Fc2* fcl = reinterpret_cast<Fc2*>(sm + O_FCL);
+  for (uint32_t k = tid; k < W.n_clients; k += nb) fcl[k] = fc2_of(fin_client(S.cstate[k], *S.glob, S.nrall != nullptr));
+  uint32_t* ext = reinterpret_cast<uint32_t*>(sm + O_EXT);
+  uint32_t* nr0 = reinterpret_cast<uint32_t*>(sm + O_NR0);
+  for (uint32_t i = tid; i < FX_R; i += nb) {
+    ext[i] = i < W.n_ranges ? __ldcg(S.ext + i) : EMPTY32;
+    nr0[i] = i < W.n_ranges ? __ldcg(S.nr0 + i) : EMPTY32;
+  }
+  __syncthreads();
+  const uint4* rows = reinterpret_cast<const uint4*>(sm + O_ROWS);
+  const uint32_t lane = tid & 31, warp = tid >> 5;
+  const uint32_t base = (uint32_t)P.base_index;
+  const uint32_t G = W.dd_groups, gmask = W.dd_groups == 1 ? 0u : 7u;
+  uint4* sq = reinterpret_cast<uint4*>(sm + O_SLOWQ) + warp * SQ_CAP;   // {lo, hi, batch index, dd word}
+  uint32_t sqn = 0;
+
+  // the general resolution of one queued entry (hash lookups allowed), by one lane
+  auto slow_one = [&](uint4 q) {
+    const uint32_t lo = q.x, hi = q.y, i = q.z, wd = q.w, gidx = base + i;
+    const uint32_t sid = lo & 31u, c = (lo >> 14) & 63u, ceng = (lo >> 12) & 3u, k = (lo >> 20) & 0x7FFu;
+    const uint32_t loc = (lo >> 10) & 3u, grp = (lo >> 5) & 7u, m = (lo >> 8) & 3u;
+    const bool inr = loc == LOC_IN, inw = inr || loc == LOC_GUARD;
+    const uint32_t sw = slut2[sid];
+    const Fc2 fc = fcl[c];
+    const uint32_t ok = gidx | (sw & S2_NONREPL);
+    const bool ep1 = ok >= fc.rel_lt, elig = sw & S2_ELIG, dd = sw & S2_DD;
+    const uint64_t page = inw ? (uint64_t)(rows[k].x + (hi - rows[k].z)) : ((uint64_t)hi | ((uint64_t)k << 32));
+    unsigned long long key = dd ? dedup_key(c, (int)ceng, (int)sid, page) : 0ull;
+    uint32_t ri = ok;
+    if (dd) ri = (inw && wd != EMPTY32 && (wd & 7u) == grp) ? (wd >> 3) : hash_get(S.hdd, key);
+    const bool dup = dd && ri != gidx;
+    const uint32_t rep_ok = dd ? ri : ok;
+    const bool ce = ceng == 1;
+    bool canc = false;
+    if (sw & S2_TRAP) canc = gidx != fc.trap_ok;
+    else if (sw & S2_SERV) canc = ((fc.flags >> (ce ? 1 : 0)) & 1u) || rep_ok > fc.tie;
+    else if (sw & S2_FATAL) canc = rep_ok != (ce ? fc.ft1 : fc.ft0);
+    uint32_t mech = 0;
+    if (elig && !dup) {
+      const bool e1 = ep1 && !(fc.flags & 4u);
+      if (!inr || ep1) {
+        uint32_t nr;
+        if (!inw) nr = hash_get(S.hnr, nr_key(c, e1 ? 1 : 0, page));
+        else if (e1) nr = __ldcg(S.nr1 + hi);
+        else nr = inr ? __ldcg(S.nrall + hi) : nr0[k];
+        mech = nr == ok ? 1u : 2u;
+      } else {
+        mech = (m == 2 && ext[k] == ok) ? 3u : 2u;
+      }
+    }
+    const uint32_t verdict = (sw & 0x7Fu) | (mech << 2) | (canc ? 0x10u : 0u) | (dup ? 0x20u : 0u);
+    const uint32_t rid = inr ? rrid[k] : NO_RID;
+    __stcs(reinterpret_cast<unsigned long long*>(out) + i, (unsigned long long)rid | ((unsigned long long)sid << 32) |
+           ((unsigned long long)verdict << 40) | ((unsigned long long)c << 48));
+    const uint64_t qq = q_base + i / WCHUNK;
+    const uint32_t w = i % WCHUNK, bit = 1u << (w >> 1);
+    uint32_t* mw = reinterpret_cast<uint32_t*>(S.cmask + qq);
+    const bool rep = dd && !dup;
+    if (canc) atomicOr(mw + (w & 1u), bit);
+    if (rep) {
+      atomicOr(mw + 2 + (w & 1u), bit);
+      st_keep(S.dstage + qq * KSTAGE + w, key);
+    }
+    if (canc || rep) atomicAdd(S.segcnt + qq / SEG_CHUNKS, (canc ? 1ull : 0ull) | (rep ? (1ull << 32) : 0ull));
+  };
+  auto slow_drain = [&](uint32_t k) {   // queue entries [sqn - k, sqn) by lanes 0..k-1
+    __syncwarp();
+    if (lane < k) slow_one(sq[sqn - k + lane]);
+    sqn -= k;
+    __syncwarp();
+  };
+
+  // the common path of one entry: load addresses first (A), outcome after the loads (B)
+  struct A {
+    uint32_t lo, hi, sw, ok, k;
+    uint32_t flags;        // bit0 rep_free, bit1 want_rep, bit2 needs_nr, bit3 pe, bit4 slow, bit5 p_dd
+    uint32_t fcw[6];
+    const uint32_t *pd, *pn;
+    bool p_dd, p_nr;
+    uint32_t smv;
+  };
+  auto addr = [&](uint32_t lo, uint32_t hi, uint32_t gidx, A& a) {
+    a.lo = lo; a.hi = hi;
+    const uint32_t loc = (lo >> 10) & 3u, sid = lo & 31u;
+    a.sw = slut2[loc ? sid : 31u];
+    const uint32_t sw = a.sw, c = (lo >> 14) & 63u;
+    a.k = (lo >> 20) & 0x7FFu;
+    const uint4 f0 = *reinterpret_cast<const uint4*>(fcl + c);
+    const uint2 f1 = *reinterpret_cast<const uint2*>(&fcl[c].tie);
+    a.fcw[0] = f0.x; a.fcw[1] = f0.y; a.fcw[2] = f0.z; a.fcw[3] = f0.w; a.fcw[4] = f1.x; a.fcw[5] = f1.y;
+    a.ok = gidx | (sw & S2_NONREPL);
+    const bool ep1 = a.ok >= f0.x;
+    const bool inr = loc == LOC_IN, grd = loc == LOC_GUARD, inw = inr | grd, wild = loc == LOC_NONE;
+    const bool kd = (lo & R_KDUP) != 0;
+    const bool elig = (sw & S2_ELIG) != 0, dd = (sw & S2_DD) != 0, serv = (sw & S2_SERV) != 0;
+    const bool rep_free = kd & (elig | (serv & (f1.x == EMPTY32)));
+    const bool want_rep = dd & !rep_free;
+    const bool needs_nr = elig & !kd & (!inr | ep1);
+    const bool e1 = ep1 & !(f1.y & 4u);
+    const bool pe = elig & !kd & inr & !ep1 & (((lo >> 8) & 3u) == 2u);
+    const bool slow = wild & (want_rep | needs_nr);
+    a.p_dd = want_rep & inw;
+    a.pd = S.dd + (hi * G + (((lo >> 5) & 7u) & gmask));
+    a.p_nr = needs_nr & (e1 ? inw : inr);
+    a.pn = (e1 ? S.nr1 : S.nrall) + hi;
+    a.smv = (pe ? ext : nr0)[a.k];
+    a.flags = (rep_free ? 1u : 0u) | (want_rep ? 2u : 0u) | (needs_nr ? 4u : 0u) | (pe ? 8u : 0u) | (slow ? 16u : 0u);
+  };
+  auto fin = [&](A& a, uint32_t wd, uint32_t wn, uint32_t gidx, unsigned long long& o8, bool& canc, bool& rep,
+                 unsigned long long& key) {
+    const uint32_t lo = a.lo, hi = a.hi, sw = a.sw, k = a.k;
+    const uint32_t sid = lo & 31u, c = (lo >> 14) & 63u, ceng = (lo >> 12) & 3u, loc = (lo >> 10) & 3u;
+    const bool dd = (sw & S2_DD) != 0, elig = (sw & S2_ELIG) != 0;
+    const bool rep_free = a.flags & 1u, needs_nr = a.flags & 4u, pe = a.flags & 8u;
+    // a claimed page slot held by another dedup group: the key is in the hash (slow path)
+    if (a.p_dd && (wd == EMPTY32 || (wd & 7u) != ((lo >> 5) & 7u))) a.flags |= 16u;
+    const uint32_t ri = wd >> 3;
+    const bool dup = dd & (rep_free | (ri != gidx));
+    const uint32_t rep_ok = (dd & !rep_free) ? ri : a.ok;
+    const uint32_t ce = ceng == 1 ? 1u : 0u;
+    const bool c_trap = gidx != a.fcw[1];
+    const bool c_serv = ((a.fcw[5] >> ce) & 1u) | (rep_ok > a.fcw[4]);
+    const bool c_fat = rep_ok != (ce ? a.fcw[3] : a.fcw[2]);
+    canc = ((sw & S2_TRAP) && c_trap) | ((sw & S2_SERV) && c_serv) | ((sw & S2_FATAL) && c_fat);
+    const bool hit = wn == a.ok;
+    const uint32_t mech = (elig & !dup) ? (needs_nr ? (hit ? 1u : 2u) : ((pe & hit) ? 3u : 2u)) : 0u;
+    const uint32_t verdict = (sw & 0x7Fu) | (mech << 2) | (canc ? 0x10u : 0u) | (dup ? 0x20u : 0u);
+    const uint32_t rid = loc == LOC_IN ? rrid[k] : NO_RID;
+    o8 = sw ? ((unsigned long long)rid | ((unsigned long long)sid << 32) | ((unsigned long long)verdict << 40) |
+               ((unsigned long long)c << 48))
+            : (0xFFFF000000000000ull | (0xFFull << 32) | NO_RID);
+    rep = dd & !dup;
+    const uint4 row = rows[k];
+    key = dedup_key(c, (int)ceng, (int)sid, (uint64_t)(row.x + (hi - row.z)));
+    if (a.flags & 16u) { canc = false; rep = false; }        // resolved by the slow path
+  };
+
+  const unsigned long long* rec = S.drec + (P.base_index - S.drec_base);
+  const uint32_t below = (1u << lane) - 1u;
+  rec_stream(rec, n, [&](ulonglong2 r, uint32_t i0, bool ok0, bool ok1) {
+    A a0, a1;
+    addr(ok0 ? (uint32_t)r.x : 0u, (uint32_t)(r.x >> 32), base + i0, a0);
+    addr(ok1 ? (uint32_t)r.y : 0u, (uint32_t)(r.y >> 32), base + i0 + 1, a1);
+    const uint32_t wd0 = ldcg_if(a0.p_dd, a0.pd, EMPTY32), wn0 = ldcg_if(a0.p_nr, a0.pn, a0.smv);
+    const uint32_t wd1 = ldcg_if(a1.p_dd, a1.pd, EMPTY32), wn1 = ldcg_if(a1.p_nr, a1.pn, a1.smv);
+    unsigned long long o0, o1, k0, k1;
+    bool c0, c1, p0, p1;
+    fin(a0, wd0, wn0, base + i0, o0, c0, p0, k0);
+    fin(a1, wd1, wn1, base + i0 + 1, o1, c1, p1, k1);
+    unsigned long long* o = reinterpret_cast<unsigned long long*>(out) + i0;
+    if (ok1 && (((uintptr_t)o & 15u) == 0)) __stcs(reinterpret_cast<ulonglong2*>(o), make_ulonglong2(o0, o1));
+    else {
+      if (ok0) __stcs(o, o0);
+      if (ok1) __stcs(o + 1, o1);
+    }
+    const uint32_t bc0 = __ballot_sync(0xFFFFFFFFu, ok0 && c0), bc1 = __ballot_sync(0xFFFFFFFFu, ok1 && c1);
+    const uint32_t bd0 = __ballot_sync(0xFFFFFFFFu, ok0 && p0), bd1 = __ballot_sync(0xFFFFFFFFu, ok1 && p1);
+    const uint64_t qq = q_base + i0 / WCHUNK;
+    if (ok0 && p0) st_keep(S.dstage + qq * KSTAGE + 2 * lane, k0);
+    if (ok1 && p1) st_keep(S.dstage + qq * KSTAGE + 2 * lane + 1, k1);
+    if (lane == 0) {
+      S.cmask[qq] = make_uint4(bc0, bc1, bd0, bd1);
+      const uint32_t nc = __popc(bc0) + __popc(bc1), nd = __popc(bd0) + __popc(bd1);
+      if (nc | nd) atomicAdd(S.segcnt + qq / SEG_CHUNKS, (unsigned long long)nc | ((unsigned long long)nd << 32));
+    }
+    // entries needing a hash lookup: queued, resolved 32 at a time (after this chunk's mask store)
+    const bool s0 = ok0 && (a0.flags & 16u), s1 = ok1 && (a1.flags & 16u);
+    const uint32_t b0 = __ballot_sync(0xFFFFFFFFu, s0), b1 = __ballot_sync(0xFFFFFFFFu, s1);
+    if (b0 | b1) {
+      if (s0) sq[sqn + __popc(b0 & below)] = make_uint4(a0.lo, a0.hi, i0, wd0);
+      sqn += __popc(b0);
+      if (s1) sq[sqn + __popc(b1 & below)] = make_uint4(a1.lo, a1.hi, i0 + 1, wd1);
+      sqn += __popc(b1);
+      while (sqn >= 32) slow_drain(32);
+    }
+  });
+  if (sqn) slow_drain(sqn);
+}
+
+}  // namespace fx

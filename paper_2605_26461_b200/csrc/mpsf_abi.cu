@@ -4,6 +4,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <stdio.h>
 
 #include <algorithm>
 #include <map>
@@ -92,14 +93,11 @@ struct mpsf_ctx {
   uint32_t* d_pf = nullptr;     // first PREFETCH per page (batched translation)
   uint32_t* d_nrall = nullptr;
   uint64_t dd_cap = 0;
-  uint32_t* d_count_part = nullptr;
-  uint64_t part_cap = 0;
   int dedup_mode = 0;            // 1 dense slots, -1 claimed slots (large-world layout), 0 by size
   // exchange-group offsets inside d_small
   size_t x_u64 = 0, x_u32 = 0, x_giso = 0;
   uint64_t x_u64_n = 0, x_u32_n = 0, x_giso_n = 0;
   // state carried between phase calls
-  uint32_t parts = 0;
   uint64_t phase_n = 0;
   uint32_t* d_counter = nullptr;
   uint64_t pages_cap = 0;
@@ -310,7 +308,6 @@ void mpsf_destroy(mpsf_ctx* c) {
   cudaFree(c->d_dd);
   cudaFree(c->d_nr1);
   cudaFree(c->d_nrall);
-  cudaFree(c->d_count_part);
   cudaFree(c->d_counter);
   cudaFree(c->d_small);
   cudaFree(c->d_masks);
@@ -378,7 +375,7 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   std::vector<uint32_t> pg_base(nr + 1), pg_end(nr + 1), poff(nr + 1), rattr(nr + 1), rrid(nr + 1);
   for (uint32_t i = 0; i < nr; ++i) {
     const mpsf_range_entry& r = ranges[i];
-    if (r.end >= VA_TABLE_LIMIT) return MPSF_E_WORLD;
+    if (r.end > VA_TABLE_LIMIT) return MPSF_E_WORLD;
     pg_base[i] = (uint32_t)(r.base >> 12);
     pg_end[i] = (uint32_t)(r.end >> 12);
     poff[i] = r.page_off;
@@ -424,6 +421,45 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
                           ((uint32_t)(clients[cl].mode & 1) << 18) | CH_VALID)
                        : 0u;
   }
+  // row form for the streaming passes (mpsf_device.cuh World::chan4 / skip2 / row4)
+  std::vector<uint32_t> chan4(4ull * (nch + 1), 0), skip2(2ull * (skip.size()), 0), row4(4ull * (nr + 1), 0);
+  for (uint32_t i = 0; i <= nch; ++i) {
+    uint32_t* o = &chan4[4ull * i];
+    o[0] = chan[i];
+    o[3] = n_skip;                                    // no ranges: the sentinel slot, jmax 0
+    if (i < nch && (chan[i] & CH_VALID)) {
+      const uint32_t* ci = &cinfo[4ull * (chan[i] & 0xFFFFu)];
+      if ((ci[0] & 0xFFFFu) != (ci[0] >> 16)) {
+        o[1] = ci[1];
+        o[2] = ci[2] & 31u;
+        o[3] = ci[3] | ((ci[2] >> 8) << 16);
+      }
+    }
+  }
+  for (uint32_t cl = 0; cl < ncl; ++cl) {
+    const uint32_t* ci = &cinfo[4ull * cl];
+    const uint32_t lo = ci[0] & 0xFFFFu, hi = ci[0] >> 16;
+    if (lo == hi) continue;
+    const uint32_t sh = ci[2] & 31u, slots = (ci[2] >> 8) + 1;
+    for (uint32_t j = 0; j < slots; ++j) {
+      const uint32_t k = skip[ci[3] + j];
+      const uint64_t end_slot = (uint64_t)ci[1] + ((uint64_t)(j + 1) << sh);
+      skip2[2ull * (ci[3] + j)] = k;
+      skip2[2ull * (ci[3] + j) + 1] = (k + 1 < hi && pg_base[k + 1] < end_slot) ? pg_base[k + 1] : 0xFFFFFFFFu;
+    }
+  }
+  skip2[2ull * n_skip] = nr;                          // sentinel slot -> sentinel row
+  skip2[2ull * n_skip + 1] = 0xFFFFFFFFu;
+  for (uint32_t i = 0; i < nr; ++i) {
+    const mpsf_range_entry& r = ranges[i];
+    row4[4ull * i] = pg_base[i];
+    row4[4ull * i + 1] = pg_end[i];
+    row4[4ull * i + 2] = r.page_off;
+    row4[4ull * i + 3] = (r.state == 0xFF ? ROW_PERPAGE : (uint32_t)(r.state & 7u)) |
+                         (((uint32_t)r.kind | ((uint32_t)r.lifecycle << 1) | ((uint32_t)r.migratable << 2)) << 4);
+  }
+  row4[4ull * nr] = 0xFFFFFFFFu;                      // sentinel: no page is in it or its guard
+  row4[4ull * nr + 1] = 0xFFFFFFFFu;
   const size_t o_r = 0, o_off = a256(o_r + sizeof(mpsf_range_entry) * nr);
   const size_t o_ps = a256(o_off + sizeof(uint32_t) * (ncl + 1));
   const size_t o_ch = a256(o_ps + np);
@@ -432,7 +468,10 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   const size_t o_skip = a256(o_soa + 5ull * 4 * (nr + 1));
   const size_t o_cinfo4 = a256(o_skip + 2ull * skip.size());
   const size_t o_chan = a256(o_cinfo4 + 4ull * cinfo.size());
-  const size_t total = a256(o_chan + 4ull * chan.size()) + 256;
+  const size_t o_chan4 = a256(o_chan + 4ull * chan.size());
+  const size_t o_skip2 = a256(o_chan4 + 4ull * chan4.size());
+  const size_t o_row4 = a256(o_skip2 + 4ull * skip2.size());
+  const size_t total = a256(o_row4 + 4ull * row4.size()) + 256;
   cudaFree(c->d_world);
   c->d_world = nullptr;
   c->has_world = false;
@@ -453,6 +492,9 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   CK(cudaMemcpy(b + o_skip, skip.data(), 2ull * skip.size(), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(b + o_cinfo4, cinfo.data(), 4ull * cinfo.size(), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(b + o_chan, chan.data(), 4ull * chan.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(b + o_chan4, chan4.data(), 4ull * chan4.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(b + o_skip2, skip2.data(), 4ull * skip2.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(b + o_row4, row4.data(), 4ull * row4.size(), cudaMemcpyHostToDevice));
   World& W = c->W;
   W.ranges = reinterpret_cast<const mpsf_range_entry*>(b + o_r);
   W.client_off = reinterpret_cast<const uint32_t*>(b + o_off);
@@ -467,6 +509,9 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
   W.skip = reinterpret_cast<const uint16_t*>(b + o_skip);
   W.cinfo4 = reinterpret_cast<const uint4*>(b + o_cinfo4);
   W.chan = reinterpret_cast<const uint32_t*>(b + o_chan);
+  W.chan4 = reinterpret_cast<const uint4*>(b + o_chan4);
+  W.skip2 = reinterpret_cast<const uint2*>(b + o_skip2);
+  W.row4 = reinterpret_cast<const uint4*>(b + o_row4);
   W.n_skip = n_skip;
   W.exact1 = exact1;
   W.n_ranges = nr;
@@ -496,14 +541,6 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
     CK(cudaMalloc(&c->d_nrall, sizeof(uint32_t) * std::max<uint64_t>(np, 1)));
     c->pages_cap = np;
     c->dd_cap = dd_words;
-  }
-  const uint64_t part_words = (uint64_t)count_parts_needed(W) * NSCEN * ncl;
-  if (part_words > c->part_cap) {
-    cudaFree(c->d_count_part);
-    c->d_count_part = nullptr;
-    c->part_cap = 0;
-    CK(cudaMalloc(&c->d_count_part, 4 * part_words));
-    c->part_cap = part_words;
   }
   // small scratch: [EMPTY-init][ZERO-init][uninit]
   const uint32_t C = ncl, R = nr;
@@ -668,7 +705,6 @@ static int batch_init(mpsf_ctx* c, uint64_t n, const mpsf_params* p, uint64_t* d
   segs.p[k] = c->d_hdd; segs.words[k] = 4 * c->hcap_dd; segs.val[k++] = EMPTY32;
   segs.p[k] = c->d_hnr; segs.words[k] = 4 * c->hcap_nr; segs.val[k++] = EMPTY32;
   if (c->W.n_clients) { segs.p[k] = d_counts; segs.words[k] = 2ull * NSCEN * c->W.n_clients; segs.val[k++] = 0; }
-  if (c->part_cap) { segs.p[k] = c->d_count_part; segs.words[k] = c->part_cap; segs.val[k++] = 0; }
   segs.n = k;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
@@ -686,7 +722,7 @@ static int scan_chunk(mpsf_ctx* c, const mpsf_fault_entry* d_chunk, uint64_t n_c
   Params P = to_params(p);
   P.base_index += chunk_off;
   if (launch_scan(c->W, c->S, d_chunk, n_chunk, P, reinterpret_cast<unsigned long long*>(d_counts),
-                  c->d_count_part, st, c->marker(), &c->parts))
+                  st, c->marker()))
     return MPSF_E_CUDA;
   return MPSF_OK;
 }
@@ -696,9 +732,7 @@ int mpsf_resolve(mpsf_ctx* c, const mpsf_params* p, mpsf_client_verdict* d_verdi
   if (!c || !p) return MPSF_E_ARG;
   if (c->W.n_clients && (!d_verdict || !d_counts)) return MPSF_E_ARG;
   CK(cudaSetDevice(c->device));
-  if (launch_resolve(c->W, c->S, to_params(p), d_verdict, c->d_count_part, c->parts,
-                     reinterpret_cast<unsigned long long*>(d_counts), reinterpret_cast<cudaStream_t>(stream),
-                     c->marker()))
+  if (launch_resolve(c->W, c->S, to_params(p), d_verdict, reinterpret_cast<cudaStream_t>(stream), c->marker()))
     return MPSF_E_CUDA;
   c->last_launches += 1;
   return MPSF_OK;
@@ -1020,8 +1054,7 @@ int mpsf_submit_host(mpsf_ctx* c, int slot, const mpsf_fault_entry* h_in, uint64
   }
   const Marker mk = c->marker();
   const Params P = to_params(p);
-  if (launch_resolve(c->W, c->S, P, d_v, c->d_count_part, c->parts, reinterpret_cast<unsigned long long*>(d_cnt),
-                     st, mk))
+  if (launch_resolve(c->W, c->S, P, d_v, st, mk))
     return MPSF_E_CUDA;
   ++launches;
   if ((p->flags & MPSF_PF_ISOLATION) && n) {

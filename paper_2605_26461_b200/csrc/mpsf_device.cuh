@@ -96,7 +96,7 @@ __device__ __forceinline__ FinClient fin_client(const CState& cs, const Globals&
 }
 
 constexpr uint32_t SKIP_MAX = 256;       // skip-table slots per client (cap)
-constexpr uint64_t VA_TABLE_LIMIT = 1ull << 44;   // interval tables hold 32-bit page numbers
+constexpr uint64_t VA_TABLE_LIMIT = (1ull << 44) - 8192;   // range ends: guard page numbers stay below 2^32 - 1
 
 // Device form of the interval table, built by mpsf_upload_world (page-granular SoA so a warp's
 // random lookups touch 4-byte words: no 32-byte-row bank conflicts).  Per client, a skip table
@@ -122,7 +122,15 @@ struct World {
   uint32_t dd_groups;   // 5: one dense dedup slot per (page, group); 1: one claimed slot per page
   uint32_t n_skip;
   uint32_t exact1;      // every skip slot holds at most one range base
+  // row form of the same tables for the streaming passes (one 16- or 8-byte shared load per step):
+  const uint4* chan4;   // [nch + 1] {channel word, client span start page, skip shift, skip offset | jmax << 16}
+  const uint2* skip2;   // [n_skip + 1] {range index at the slot start, base page of the next range if it
+                        //  starts inside the slot else 0xFFFFFFFF}
+  const uint4* row4;    // [R + 1] {base page, end page, first page-state slot, attr}; attr = uniform state
+                        //  [2:0] | per-page state [3] | range class (kind | zombie << 1 | migratable << 2) << 4
 };
+
+constexpr uint32_t ROW_PERPAGE = 8u;
 
 constexpr uint32_t CH_VALID = 1u << 31;
 

@@ -18,13 +18,11 @@ struct Marker {
   }
 };
 
-// pass 1; *parts = number of per-block count partial rows written (0: counts went to global)
+// pass 1 (counts accumulate across the launches of a chunked batch; k_init zeroes them)
 int launch_scan(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
-                unsigned long long* counts, uint32_t* count_part, cudaStream_t st, const Marker& mk,
-                uint32_t* parts);
+                unsigned long long* counts, cudaStream_t st, const Marker& mk);
 int launch_resolve(const World& W, const Scratch& S, const Params& P, mpsf_client_verdict* verdict,
-                   const uint32_t* count_part, uint32_t parts, unsigned long long* counts, cudaStream_t st,
-                   const Marker& mk);
+                   cudaStream_t st, const Marker& mk);
 int launch_general(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
                    int stage, cudaStream_t st, const Marker& mk);
 int launch_resolve2(const World& W, const Scratch& S, const Params& P, cudaStream_t st, const Marker& mk);
@@ -59,7 +57,6 @@ int launch_sparse_export(const uint32_t* buf, uint64_t count, uint32_t* idx, uin
                          uint64_t cap, cudaStream_t st);
 int launch_sparse_merge(uint32_t* buf, uint64_t count, const uint32_t* idx, const uint32_t* val, uint64_t n,
                         cudaStream_t st);
-uint32_t count_parts_needed(const World& W);   // per-block count partial rows k_scan may write
 
 int launch_remap(uint64_t va_base, const uint64_t* phys, uint64_t npages4k, uint32_t gran_log2,
                  mpsf_remap_entry* out, cudaStream_t st);
