@@ -1483,7 +1483,9 @@ static bool staged_fits(const World& W) {
 }
 
 // the row-table passes (fx_passes.cuh): fixed layout and at most one range base per skip slot
-static bool fx_fits(const World& W) { return staged_fits(W) && W.exact1 && W.n_skip + 1 <= FX_SKIP; }
+static bool fx_fits(const World& W) {
+  return staged_fits(W) && W.exact1 && W.n_skip + 1 <= FX_SKIP && W.n_pages < (1ull << 30);
+}
 
 template <bool kStaged>
 static void set_attrs() {

@@ -40,7 +40,8 @@ constexpr uint32_t O_ISO = a16(O_C64 + 8 * (3 * FX_C + 2));
 constexpr uint32_t O_R32 = O_ISO + 4 * 3 * FX_C * 32;
 constexpr uint32_t O_CNT = O_R32 + 4 * 2 * FX_R;
 constexpr uint32_t O_USED = O_CNT + 4 * NSCEN * FX_C;
-constexpr uint32_t SCAN_BYTES = O_USED + 16;
+constexpr uint32_t O_QCNT = O_USED + 16;
+constexpr uint32_t SCAN_BYTES = O_QCNT + 4 * WARPS;
 // pass 2
 constexpr uint32_t O_FCL = O_PASS;
 constexpr uint32_t O_RRID = O_FCL + 32 * FX_C;
@@ -52,10 +53,17 @@ static_assert(SCAN_BYTES <= 227 * 1024 && FIN_BYTES <= 227 * 1024, "fixed layout
 
 __device__ __forceinline__ uint32_t lut2_word(uint32_t idx, bool isolation) {
   if (idx >= LUT2_XK) return lut_word((int)(LUT_XK + (idx - LUT2_XK)), isolation);
-  const uint32_t st = idx & 7, rcls = (idx >> 3) & 15, ea = idx >> 7;
-  const uint32_t e = ea >> 2, a = ea & 3;
+  const uint32_t st = idx & 7, rcls = (idx >> 3) & 15, e = idx >> 9, a = (idx >> 7) & 3;
   if (e > 2 || a > 2) return LF_VALID | LF_BAD;
   return lut_word((int)(((e * 3 + a) * 16 + rcls) * 8 + st), isolation);
+}
+
+// predicated L2 load (no branch): dflt when p is false
+__device__ __forceinline__ uint32_t ldcg_if(bool p, const uint32_t* a, uint32_t dflt) {
+  uint32_t v;
+  asm("{.reg .pred q; setp.ne.u32 q, %2, 0; mov.b32 %0, %3; @q ld.global.cg.u32 %0, [%1];}"
+      : "=r"(v) : "l"(a), "r"((uint32_t)p), "r"(dflt));
+  return v;
 }
 
 // World tables into shared memory (both passes).
@@ -92,26 +100,29 @@ __device__ __forceinline__ D decode(const uint8_t* sm, const uint8_t* __restrict
   d.k = sk.x + (d.page >= sk.y ? 1u : 0u);
   const uint4 row = reinterpret_cast<const uint4*>(sm + O_ROWS)[d.k];
   // translation entries below 2^44 - 4 KiB look their range up (no range reaches higher)
-  const bool look = ek == 0 && e.y < 0x1000u && d.page != 0xFFFFFFFFu;
-  d.inr = look && d.page >= row.x && d.page < row.y;
-  d.grd = look && d.page == row.y;
+  const bool look = (ek == 0) & (e.y < 0x1000u) & (d.page != 0xFFFFFFFFu);
+  d.inr = look & (d.page >= row.x) & (d.page < row.y);
+  d.grd = look & (d.page == row.y);
   d.slot = row.z + (d.page - row.x);
-  uint32_t st = row.w & 7u;
-  if (d.inr && (row.w & ROW_PERPAGE)) st = ps[d.slot] & 7u;
-  const uint32_t eng = w3 & 0xFFu, acc = (w3 >> 8) & 0xFFu;
-  const uint32_t ea = min(eng, 3u) * 4 + min(acc, 3u);
-  const uint32_t idx = ek == 0 ? ea * 128 + (d.inr ? ((row.w >> 1) & 0x78u) + st : 64u) : LUT2_XK + min(ek, 15u);
+  const bool pp = d.inr & ((row.w & ROW_PERPAGE) != 0);
+  const uint32_t pst = pp ? ps[d.slot] : row.w;                 // per-page state byte, else the uniform one
+  // LUT index: [engine][access][range class][state] (engine / access 3 -> a BAD word), or the kind
+  const uint32_t ea = ((w3 & 3u) << 9) | ((w3 & 0x300u) >> 1);
+  const uint32_t t = d.inr ? ((row.w & 0x38u) | (pst & 7u)) : 64u;
+  const uint32_t idx = ek == 0 ? ea + t : LUT2_XK + min(ek, 15u);
   const uint32_t f = reinterpret_cast<const uint32_t*>(sm + O_LUT)[idx];
   d.cw = cr.x;
-  const uint32_t ceng = (cr.x >> 16) & 3u;
-  const bool bad = !(cr.x & CH_VALID) || (f & LF_BAD) || (ek == 0 && (eng != ceng || e.y >= (1u << 21)));
+  const uint32_t eng = w3 & 0xFFu, ceng = (cr.x >> 16) & 3u;
+  const bool tbad = (ek == 0) & (((w3 & 0xFCFCu) != 0) | (eng != ceng) | (e.y >= (1u << 21)));
+  const bool bad = !(cr.x & CH_VALID) | ((f & LF_BAD) != 0) | tbad;
   const bool valid = (w3 >> 24) & MPSF_ENTRY_VALID;
-  if (valid && bad) {
+  if (valid && bad) {                                             // malformed entry (never in a valid trace)
     const uint32_t bit = !(cr.x & CH_VALID) ? EB_NO_CHANNEL
-                         : (f & LF_BAD) ? EB_BAD_ENTRY : (eng != ceng ? EB_MISMATCH : EB_VA);
+                         : (((f & LF_BAD) != 0) | ((ek == 0) & ((w3 & 0xFCFCu) != 0))) ? EB_BAD_ENTRY
+                         : (eng != ceng ? EB_MISMATCH : EB_VA);
     raise_err(S, bit, gidx);
   }
-  d.f = (valid && !bad) ? f : 0u;
+  d.f = (valid & !bad) ? f : 0u;
   return d;
 }
 
@@ -121,7 +132,21 @@ __device__ __forceinline__ D decode(const uint8_t* sm, const uint8_t* __restrict
 // bits 0..31
 constexpr uint32_t R_KDUP = 1u << 31;
 
-// Pass 1 over [0, n) (global index P.base_index + i).
+// Pass 1 over [0, n) (global index P.base_index + i).  As pass 2, the common path has no
+// data-dependent branch: the block-local minima and counts are predicated shared-memory
+// reductions, the global pre-check loads and minima predicated accesses; the work a warp would
+// otherwise serialise on -- wild-page hash inserts and claimed-slot CAS claims -- goes to the
+// per-warp queue, drained 32 operations at a time.  Traps and fatal reports (rare) keep a branch.
+__device__ __forceinline__ void q_exec(const Scratch& S, uint32_t* used, const QOp& x) {
+  const uint32_t t = x.tab & 3u;
+  if (t == 2) {                                  // claimed-slot dedup (sparse worlds)
+    uint32_t* slot = S.dd + (x.tab >> 2);
+    claim_resolve(S, used, slot, x.val, __ldcg(slot), x.key);
+  } else if (!hash_min(t ? S.hnr : S.hdd, used + t, x.key, x.val)) {
+    atomicOr(S.ctrl + C_OVF, 1u);
+  }
+}
+
 __device__ __forceinline__ void scan_body(const World& W, const Scratch& S, uint8_t* sm,
                                           const mpsf_fault_entry* __restrict__ in, uint64_t n, const Params& P) {
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -129,27 +154,42 @@ __device__ __forceinline__ void scan_body(const World& W, const Scratch& S, uint
   const uint32_t C = W.n_clients, nch = W.n_channels;
   const uint32_t base = (uint32_t)P.base_index;
   const bool sparse = W.dd_groups == 1;
+  const uint32_t G = W.dd_groups, gmask = sparse ? 0u : 7u;
   uint32_t* counts = reinterpret_cast<uint32_t*>(sm + O_CNT);
   uint32_t* iso = reinterpret_cast<uint32_t*>(sm + O_ISO) + warp;
   uint32_t* r32 = reinterpret_cast<uint32_t*>(sm + O_R32);
   uint32_t* used = reinterpret_cast<uint32_t*>(sm + O_USED);
   unsigned long long* c64 = reinterpret_cast<unsigned long long*>(sm + O_C64);
   QOp* q = reinterpret_cast<QOp*>(sm + O_QUEUE) + warp * QCAP;
-  uint32_t qn = 0;
   unsigned long long* const drec = S.drec + (P.base_index - S.drec_base);
   const uint8_t* __restrict__ ps = W.page_state;
-
+  uint32_t* const nrall = S.nrall;
   struct O {
     uint32_t* pd; uint32_t vd;     // dedup slot and its value
-    uint32_t* pa; uint32_t va;     // first eligible record of the page (dense worlds)
-    bool qn, qd;
-    uint32_t lo, hi;               // record
+    uint32_t* pa;                  // first eligible record of the page (dense worlds)
     uint32_t ok;
-    uint64_t page;                 // the entry's page (dedup / NR keys)
+    bool p_dd, p_a, qn, qd;        // predicates: dedup slot, nrall; wild NR / dedup hash ops
+    uint32_t lo, hi;               // record
+    uint64_t page;
   };
-  // the per-entry work up to the global pre-check loads
-  auto first = [&](uint4 e, uint32_t gidx, O& o) {
-    const D d = decode(sm, ps, nch, copy16, S, e, gidx);
+  // per entry, in two halves: (a) decode and the addresses of the global pre-check loads (both
+  // entries' loads are issued before either entry's shared-memory work, which covers them);
+  // (b) counts, block-local minima, the record
+  auto first = [&](uint4 e, uint32_t gidx, O& o, D& d) {
+    d = decode(sm, ps, nch, copy16, S, e, gidx);
+    const uint32_t f = d.f;
+    o.ok = ((f & LF_REPL) ? 0u : 0x80000000u) | gidx;
+    const bool elig = (f & LF_ELIG) != 0;
+    const bool inw = d.inr | d.grd;
+    o.p_a = elig & d.inr & (nrall != nullptr);
+    o.pa = nrall + d.slot;
+    const bool dd = (f & LF_DD) != 0;
+    const uint32_t group = (f >> LF_GROUP_SH) & 7u;
+    o.p_dd = dd & inw;
+    o.pd = S.dd + (d.slot * G + (group & gmask));
+    o.vd = (gidx << 3) | group;
+  };
+  auto second = [&](uint4 e, uint32_t gidx, O& o, const D& d) {
     const uint32_t f = d.f, c = d.cw & 0xFFFFu, sid = f & LF_S;
     red_add_s(f != 0, counts + (f ? c * NSCEN + sid : 0u));
     if (f & (LF_TRAP | LF_FATAL)) {                    // rare: traps and fatal reports
@@ -158,24 +198,17 @@ __device__ __forceinline__ void scan_body(const World& W, const Scratch& S, uint
       if (f & LF_TRAP) {
         smin64(sa ? c64 + 2 * C + c : c64 + 3 * C + 1, ((unsigned long long)gidx << 8) | sid);
       } else {
-        const uint32_t okf = ((f & LF_REPL) ? 0u : 0x80000000u) | gidx;
-        smin64(sa ? c64 + C + c : (ceng == 1 ? c64 + c : c64 + 3 * C), ((unsigned long long)okf << 8) | sid);
+        smin64(sa ? c64 + C + c : (ceng == 1 ? c64 + c : c64 + 3 * C), ((unsigned long long)o.ok << 8) | sid);
       }
     }
-    o.ok = ((f & LF_REPL) ? 0u : 0x80000000u) | gidx;
     const bool elig = (f & LF_ELIG) != 0;
     const uint32_t m = (f >> LF_M_SH) & 3u;
-    const bool inw = d.inr || d.grd;
+    const bool inw = d.inr | d.grd;
     min_s_if(elig, iso + (m * C + c) * 32, o.ok);
-    min_s_if(elig && (d.grd || (d.inr && m == 2)), r32 + (d.grd ? FX_R : 0u) + d.k, o.ok);
-    o.pa = (elig && d.inr && S.nrall) ? S.nrall + d.slot : nullptr;
-    o.va = o.ok;
+    min_s_if(elig & (d.grd | (d.inr & (m == 2))), r32 + (d.grd ? FX_R : 0u) + d.k, o.ok);
     const bool dd = (f & LF_DD) != 0;
-    const uint32_t group = (f >> LF_GROUP_SH) & 7u;
-    o.pd = (dd && inw) ? S.dd + (sparse ? d.slot : d.slot * 5 + group) : nullptr;
-    o.vd = (gidx << 3) | group;
-    o.qn = elig && !inw;
-    o.qd = dd && !inw;
+    o.qn = elig & !inw;
+    o.qd = dd & !inw;
     const uint32_t loc = f ? (d.inr ? LOC_IN : (d.grd ? LOC_GUARD : LOC_NONE)) : LOC_SKIP;
     const uint32_t pagehi = (e.y >> 12) & 0x7FFu;
     o.lo = (f & 0xFFu) | ((f >> (LF_M_SH - 8)) & 0x300u) | (loc << 10) | ((d.cw >> 4) & 0x3000u) | ((c & 63u) << 14) |
@@ -184,47 +217,71 @@ __device__ __forceinline__ void scan_body(const World& W, const Scratch& S, uint
     o.page = (uint64_t)d.page | ((uint64_t)pagehi << 32);
   };
   auto key_of = [&](const O& o) {     // the entry's dedup key
-    const uint32_t c = (o.lo >> 14) & 63u, ceng = (o.lo >> 12) & 3u, sid = o.lo & 31u;
-    return dedup_key(c, (int)ceng, (int)sid, o.page);
+    return dedup_key((o.lo >> 14) & 63u, (int)((o.lo >> 12) & 3u), (int)(o.lo & 31u), o.page);
   };
-  auto nrkey_of = [&](const O& o) { return nr_key((o.lo >> 14) & 63u, 0, o.page); };
-
+  // wild-page hash operations: appended to the warp's queue by the lanes that have them (a
+  // shared counter, no ballot), executed 32 at a time by the whole warp
+  uint32_t* qc = reinterpret_cast<uint32_t*>(sm + O_QCNT) + warp;
+  if (lane == 0) *qc = 0;
+  __syncwarp();
+  auto push = [&](unsigned long long key, uint32_t val, uint32_t tab) {
+    QOp x; x.key = key; x.val = val; x.tab = tab;
+    const uint32_t pos = atomicAdd(qc, 1u);
+    if (pos < QCAP) q[pos] = x;
+    else q_exec(S, used, x);                      // queue full (a chunk of wild pages): now
+  };
   ldg_stream(in, n, [&](uint4 e0, uint32_t i0, bool ok0, uint4 e1, uint32_t i1, bool ok1) {
     if (!ok0) e0.w = 0;
     if (!ok1) e1.w = 0;
     O o0, o1;
-    first(e0, base + i0, o0);
-    const uint32_t ra0 = o0.pa ? __ldcg(o0.pa) : 0u, rd0 = o0.pd ? __ldcg(o0.pd) : EMPTY32;
-    first(e1, base + i1, o1);
-    const uint32_t ra1 = o1.pa ? __ldcg(o1.pa) : 0u, rd1 = o1.pd ? __ldcg(o1.pd) : EMPTY32;
+    D d0, d1;
+    first(e0, base + i0, o0, d0);
+    const uint32_t ra0 = ldcg_if(o0.p_a, o0.pa, 0u), rd0 = ldcg_if(o0.p_dd, o0.pd, EMPTY32);
+    first(e1, base + i1, o1, d1);
+    const uint32_t ra1 = ldcg_if(o1.p_a, o1.pa, 0u), rd1 = ldcg_if(o1.p_dd, o1.pd, EMPTY32);
+    second(e0, base + i0, o0, d0);
+    second(e1, base + i1, o1, d1);
     // a smaller index of the same key already in the slot: a duplicate whatever comes later
-    if (rd0 != EMPTY32 && (rd0 & 7u) == (o0.vd & 7u) && rd0 < o0.vd) o0.lo |= R_KDUP;
-    if (rd1 != EMPTY32 && (rd1 & 7u) == (o1.vd & 7u) && rd1 < o1.vd) o1.lo |= R_KDUP;
+    const bool kd0 = (rd0 != EMPTY32) & ((rd0 & 7u) == (o0.vd & 7u)) & (rd0 < o0.vd);
+    const bool kd1 = (rd1 != EMPTY32) & ((rd1 & 7u) == (o1.vd & 7u)) & (rd1 < o1.vd);
+    const uint32_t lo0 = o0.lo | (kd0 ? R_KDUP : 0u), lo1 = o1.lo | (kd1 ? R_KDUP : 0u);
     unsigned long long* rp = drec + i0;
-    const unsigned long long r0 = (unsigned long long)o0.lo | ((unsigned long long)o0.hi << 32);
-    const unsigned long long r1 = (unsigned long long)o1.lo | ((unsigned long long)o1.hi << 32);
+    const unsigned long long r0 = (unsigned long long)lo0 | ((unsigned long long)o0.hi << 32);
+    const unsigned long long r1 = (unsigned long long)lo1 | ((unsigned long long)o1.hi << 32);
     if (ok1 && (((uintptr_t)rp & 15u) == 0)) __stcs(reinterpret_cast<ulonglong2*>(rp), make_ulonglong2(r0, r1));
     else {
       if (ok0) __stcs(rp, r0);
       if (ok1) __stcs(rp + 1, r1);
     }
-    min_g_if(o0.pa != nullptr, ra0, o0.pa, o0.va);
-    min_g_if(o1.pa != nullptr, ra1, o1.pa, o1.va);
-    if (!sparse) {
-      min_g_if(o0.pd != nullptr, rd0, o0.pd, o0.vd);
-      min_g_if(o1.pd != nullptr, rd1, o1.pd, o1.vd);
-    } else {
-      if (o0.pd && !(o0.lo & R_KDUP)) claim_resolve(S, used, o0.pd, o0.vd, rd0, key_of(o0));
-      if (o1.pd && !(o1.lo & R_KDUP)) claim_resolve(S, used, o1.pd, o1.vd, rd1, key_of(o1));
+    min_g_if(o0.p_a, ra0, o0.pa, o0.ok);
+    min_g_if(o1.p_a, ra1, o1.pa, o1.ok);
+    // dense slots: a predicated atomic MIN; claimed slots: claim (CAS), or MIN, or the hash
+    min_g_if(o0.p_dd & !sparse & !kd0, rd0, o0.pd, o0.vd);
+    min_g_if(o1.p_dd & !sparse & !kd1, rd1, o1.pd, o1.vd);
+    const bool cl0 = o0.p_dd & sparse & !kd0, cl1 = o1.p_dd & sparse & !kd1;
+    if (cl0) claim_resolve(S, used, o0.pd, o0.vd, rd0, key_of(o0));
+    if (cl1) claim_resolve(S, used, o1.pd, o1.vd, rd1, key_of(o1));
+    if (o0.qn | o0.qd | o1.qn | o1.qd) {
+      if (o0.qn) push(nr_key((o0.lo >> 14) & 63u, 0, o0.page), o0.ok, 1);
+      if (o0.qd) push(key_of(o0), o0.vd >> 3, 0);
+      if (o1.qn) push(nr_key((o1.lo >> 14) & 63u, 0, o1.page), o1.ok, 1);
+      if (o1.qd) push(key_of(o1), o1.vd >> 3, 0);
     }
-    if (__any_sync(0xFFFFFFFFu, o0.qn || o0.qd || o1.qn || o1.qd)) {
-      q_push(q, qn, o0.qn, nrkey_of(o0), o0.va, 1, S, used);
-      q_push(q, qn, o0.qd, key_of(o0), o0.vd >> 3, 0, S, used);
-      q_push(q, qn, o1.qn, nrkey_of(o1), o1.va, 1, S, used);
-      q_push(q, qn, o1.qd, key_of(o1), o1.vd >> 3, 0, S, used);
+    __syncwarp();
+    uint32_t qn = min(*qc, (uint32_t)QCAP);
+    if (qn >= 32) {
+      do {
+        q_exec(S, used, q[qn - 32 + lane]);
+        qn -= 32;
+      } while (qn >= 32);
+      __syncwarp();
+      if (lane == 0) *qc = qn;
+      __syncwarp();
     }
   });
-  q_drain(q, qn, S, used);
+  __syncwarp();
+  const uint32_t qn = min(*qc, (uint32_t)QCAP);
+  if (lane < qn) q_exec(S, used, q[lane]);
 }
 
 __global__ void __launch_bounds__(BLOCK, 1) k_scan_fx(World W, Scratch S, const mpsf_fault_entry* __restrict__ in,
@@ -309,13 +366,6 @@ __device__ __forceinline__ Fc2 fc2_of(const FinClient& f) {
   r.flags = (f.bflags & 3u) | (f.pre_nrall ? 4u : 0u);
   r.pad0 = r.pad1 = 0;
   return r;
-}
-
-__device__ __forceinline__ uint32_t ldcg_if(bool p, const uint32_t* a, uint32_t dflt) {
-  uint32_t v;
-  asm("{.reg .pred q; setp.ne.u32 q, %2, 0; mov.b32 %0, %3; @q ld.global.cg.u32 %0, [%1];}"
-      : "=r"(v) : "l"(a), "r"((uint32_t)p), "r"(dflt));
-  return v;
 }
 
 __global__ void __launch_bounds__(BLOCK, 1) k_finalize_fx(World W, Scratch S, uint64_t n, Params P,

@@ -456,7 +456,7 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
     row4[4ull * i + 1] = pg_end[i];
     row4[4ull * i + 2] = r.page_off;
     row4[4ull * i + 3] = (r.state == 0xFF ? ROW_PERPAGE : (uint32_t)(r.state & 7u)) |
-                         (((uint32_t)r.kind | ((uint32_t)r.lifecycle << 1) | ((uint32_t)r.migratable << 2)) << 4);
+                         (((uint32_t)r.kind | ((uint32_t)r.lifecycle << 1) | ((uint32_t)r.migratable << 2)) << 3);
   }
   row4[4ull * nr] = 0xFFFFFFFFu;                      // sentinel: no page is in it or its guard
   row4[4ull * nr + 1] = 0xFFFFFFFFu;

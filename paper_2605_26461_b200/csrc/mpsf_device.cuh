@@ -127,10 +127,10 @@ struct World {
   const uint2* skip2;   // [n_skip + 1] {range index at the slot start, base page of the next range if it
                         //  starts inside the slot else 0xFFFFFFFF}
   const uint4* row4;    // [R + 1] {base page, end page, first page-state slot, attr}; attr = uniform state
-                        //  [2:0] | per-page state [3] | range class (kind | zombie << 1 | migratable << 2) << 4
+                        //  [2:0] | range class (kind | zombie << 1 | migratable << 2) [5:3] | per-page state [7]
 };
 
-constexpr uint32_t ROW_PERPAGE = 8u;
+constexpr uint32_t ROW_PERPAGE = 0x80u;
 
 constexpr uint32_t CH_VALID = 1u << 31;
 

@@ -1,6 +1,9 @@
 """pytest plugin: run the REFERENCE's own test suite with ``mpssim.pipeline.service_bottom_half``
 replaced by the batch drop-in (``paper_2605_26461_b200.shim``).  The engine behind it is the
-C oracle here (CPU container); on a GPU box the same shim takes a ``FaultEngine``."""
+C oracle by default (CPU container); with ``MPSF_SHIM_ENGINE=gpu`` it is the device path
+(``FaultEngine(0)``, libmpsf.so on cuda:0) -- the drop-in as a user would install it."""
+
+import os
 
 import numpy as np
 
@@ -21,9 +24,25 @@ class OracleEngine:
             m2_us=params.m2_us, m3_us=params.m3_us))
 
 
+class CountingEngine:
+    """The device engine, counting the batches it processes."""
+
+    def __init__(self):
+        from paper_2605_26461_b200.engine import FaultEngine
+        self.eng = FaultEngine(0)
+
+    def upload_world(self, flat):
+        self.eng.upload_world(flat)
+
+    def process(self, entries, params):
+        CALLS["n"] += 1
+        CALLS["records"] += len(entries)
+        return self.eng.process(entries, params)
+
+
 def pytest_configure(config):
     from paper_2605_26461_b200 import shim
-    shim.install(OracleEngine())
+    shim.install(CountingEngine() if os.environ.get("MPSF_SHIM_ENGINE") == "gpu" else OracleEngine())
 
 
 def pytest_sessionfinish(session, exitstatus):
