@@ -171,6 +171,15 @@ int mpsf_submit_host(mpsf_ctx* ctx, int slot, const mpsf_fault_entry* h_entries,
                      uint32_t* h_dedup_idx, uint32_t* h_cancel);
 int mpsf_collect_host(mpsf_ctx* ctx, int slot, mpsf_summary* summary);
 
+/* ---- batched top half: faults.classify + MemoryModel.range_at of every entry ----
+ * What raise_mmu_fault computes per record before queueing it (pipeline.py:103-104;
+ * faults.py:134-171; memory.py:233-237): d_scenario[i] = the scenario id (position in
+ * faults.py:79-108; 0xFF for an entry without the valid flag), d_rid[i] = the rid of the range
+ * holding the VA (0xFFFFFFFF: none).  Parse-time / SM-trap entries get their scenario.  Device
+ * pointers, asynchronous; mpsf_get_summary reports entry errors like mpsf_process. */
+int mpsf_classify(mpsf_ctx* ctx, const mpsf_fault_entry* d_entries, uint64_t n, uint64_t base_index,
+                  uint8_t* d_scenario, uint32_t* d_rid, void* stream);
+
 /* ---- batched translation: MemoryModel.resolve_va (memory.py:339-364) over an access stream ----
  * The step before the fault path: each access (a kind-0 entry: va, access,
  * engine, channel) is translated in stream order against the uploaded page tables plus the

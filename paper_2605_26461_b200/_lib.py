@@ -116,6 +116,8 @@ SIGNATURES = {
     "mpsf_exchange_buffers": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int]),
     "mpsf_hash_export": (C.c_int64, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
     "mpsf_hash_merge": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
+    "mpsf_classify": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
+                                C.c_void_p]),
     "mpsf_sparse_export": (C.c_int64, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64,
                                        C.c_void_p]),
     "mpsf_sparse_merge": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64,

@@ -1771,6 +1771,62 @@ int launch_translate_finish(const World& W, const Scratch& S, const mpsf_fault_e
                         : translate_finish_t<false>(W, S, in, n, P, hit, faults, fault_idx, pop_idx, sum, st, mk);
 }
 
+// ---- batched top half: faults.classify + MemoryModel.range_at per entry -----------------------
+// raise_mmu_fault's classification of every entry (pipeline.py:103-104, faults.py:134-171,
+// memory.py:233-237): the scenario id (0xFF: entry skipped) and the rid of the range the VA is in
+// (NO_RID: none).  The same decode and LUT as the fault path; errors raise the same status bits.
+template <bool kStaged>
+__global__ void __launch_bounds__(BLOCK, 1) k_classify(World W, Scratch S, const mpsf_fault_entry* __restrict__ in,
+                                                       uint64_t n, Params P, uint8_t* __restrict__ sid_out,
+                                                       uint32_t* __restrict__ rid_out) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  pdl_trigger();
+  const Layout L = make_layout(W, kStaged, true);
+  const View v = setup<kStaged>(smem, L, W, S, false, true, true);
+  __syncthreads();
+  pdl_wait();
+  const uint32_t lane = threadIdx.x & 31, base = (uint32_t)P.base_index;
+  ldg_stream(in, n, [&](uint4 e0, uint32_t i0, bool ok0, uint4 e1, uint32_t i1, bool ok1) {
+    if (!ok0) e0.w = 0;
+    if (!ok1) e1.w = 0;
+    const Dec d0 = decode_fast(v.T, W.page_state, S, e0, base + i0, lane);
+    const Dec d1 = decode_fast(v.T, W.page_state, S, e1, base + i1, lane);
+    const uint32_t s0 = d0.f ? (d0.f & LF_S) : 0xFFu, s1 = d1.f ? (d1.f & LF_S) : 0xFFu;
+    const uint32_t r0 = (d0.f && d0.inr) ? v.T.rrid[d0.ridx] : NO_RID, r1 = (d1.f && d1.inr) ? v.T.rrid[d1.ridx] : NO_RID;
+    if (ok1 && ((i0 & 1u) == 0)) {
+      *reinterpret_cast<uint16_t*>(sid_out + i0) = (uint16_t)(s0 | (s1 << 8));
+      __stcs(reinterpret_cast<uint2*>(rid_out + i0), make_uint2(r0, r1));
+    } else {
+      if (ok0) { sid_out[i0] = (uint8_t)s0; rid_out[i0] = r0; }
+      if (ok1) { sid_out[i1] = (uint8_t)s1; rid_out[i1] = r1; }
+    }
+  });
+}
+
+template <bool kStaged>
+static int classify_t(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
+                      uint8_t* sid, uint32_t* rid, DevSummary* sum, cudaStream_t st, const Marker& mk) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_classify<kStaged>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
+    attr = true;
+  }
+  if (n) {
+    const uint32_t smem = make_layout(W, kStaged, true).total;
+    const int g = clamp_grid(grid_for(k_classify<kStaged>, smem), n);
+    launch_pdl(k_classify<kStaged>, dim3(g), dim3(BLOCK), smem, st, W, S, in, n, P, sid, rid);
+    mk.mark("k_classify");
+  }
+  launch_pdl(k_summary, dim3(1), dim3(1024), 0, st, S, (uint64_t)0, sum);
+  return ok_or_err();
+}
+
+int launch_classify(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
+                    uint8_t* sid, uint32_t* rid, DevSummary* sum, cudaStream_t st, const Marker& mk) {
+  return staged_fits(W) ? classify_t<true>(W, S, in, n, P, sid, rid, sum, st, mk)
+                        : classify_t<false>(W, S, in, n, P, sid, rid, sum, st, mk);
+}
+
 int launch_translate(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
                      uint8_t* hit, mpsf_fault_entry* faults, uint32_t* fault_idx, uint32_t* pop_idx, DevSummary* sum,
                      cudaStream_t st, const Marker& mk) {

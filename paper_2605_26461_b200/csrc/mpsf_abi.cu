@@ -795,6 +795,33 @@ int mpsf_process(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const mp
   return rc;
 }
 
+int mpsf_classify(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, uint64_t base_index, uint8_t* d_scenario,
+                  uint32_t* d_rid, void* stream) {
+  if (!c) return MPSF_E_ARG;
+  if (!c->has_world) return MPSF_E_NO_WORLD;
+  if (n && (!d_in || !d_scenario || !d_rid)) return MPSF_E_ARG;
+  if (base_index + n > MAX_GIDX) return MPSF_E_TOO_LARGE;
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  InitSegs segs{};
+  int k = 0;
+  segs.p[k] = c->d_small; segs.words[k] = c->small_empty_bytes / 4; segs.val[k++] = EMPTY32;
+  segs.p[k] = c->d_small + c->small_zero_off; segs.words[k] = c->small_zero_bytes / 4; segs.val[k++] = 0;
+  segs.n = k;
+  c->mark_begin(st);
+  k_init<<<dim3(16), 256, 0, st>>>(segs);
+  CK(cudaGetLastError());
+  mpsf_params p{};
+  p.base_index = base_index;
+  if (launch_classify(c->W, c->S, d_in, n, to_params(&p), d_scenario, d_rid, c->d_sum, st, c->marker()))
+    return MPSF_E_CUDA;
+  CK(cudaEventRecord(c->ev_done, st));
+  c->pending = true;
+  c->pending_fault = false;
+  c->last_launches = n ? 3 : 2;
+  return MPSF_OK;
+}
+
 int mpsf_translate_prefetch(mpsf_ctx* c, const mpsf_fault_entry* d_acc, uint64_t n, uint64_t base_index,
                             void* stream) {
   if (!c) return MPSF_E_ARG;

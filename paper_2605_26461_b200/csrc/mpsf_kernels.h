@@ -45,6 +45,9 @@ int launch_translate_prefetch(const World& W, const Scratch& S, const mpsf_fault
 int launch_translate_finish(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n,
                             const Params& P, uint8_t* hit, mpsf_fault_entry* faults, uint32_t* fault_idx,
                             uint32_t* pop_idx, DevSummary* sum, cudaStream_t st, const Marker& mk);
+// batched top half: scenario id (0xFF skipped) and rid (NO_RID) per entry, then the summary
+int launch_classify(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
+                    uint8_t* sid, uint32_t* rid, DevSummary* sum, cudaStream_t st, const Marker& mk);
 uint32_t chunk_entries();   // entries per chunk (host chunk boundaries must be multiples)
 uint64_t chunks_for(uint64_t n);
 uint64_t segments_for(uint64_t n);

@@ -8,7 +8,7 @@
 // power-of-two granularity G >= 4 KiB: entry k = (base + k*G, pages[k*G/4096]).
 //
 // Pure bandwidth: 8 B read + 16 B written per entry.  At G > 4 KiB the read is a stride
-// of G/4096 u64, so every read pulls a full 32-B sector for 8 useful bytes.
+// of G/4096 u64, so every read pulls a 64-B L2 fetch for 8 useful bytes.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -19,6 +19,15 @@ namespace mpsf {
 constexpr int RB = 256;
 constexpr int REPT = 4;
 
+// One 8-byte page number per entry, G apart: the L2 fetches at least 64 B per miss, and the
+// default (a 128-byte fetch) reads twice that -- the 64-byte prefetch size cuts the 64 KiB remap
+// from 31 to 23 us (tools/remap_ab.py; profiles/r02/ab_remap.txt).
+__device__ __forceinline__ unsigned long long ld_phys(const unsigned long long* p) {
+  unsigned long long v;
+  asm("ld.global.nc.L2::64B.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+
 __global__ void __launch_bounds__(RB) k_remap(uint64_t va_base, const unsigned long long* __restrict__ phys,
                                               uint32_t shift, uint32_t gran_log2, uint64_t E,
                                               ulonglong2* __restrict__ out) {
@@ -28,7 +37,7 @@ __global__ void __launch_bounds__(RB) k_remap(uint64_t va_base, const unsigned l
 #pragma unroll
     for (int u = 0; u < REPT; ++u) {
       const uint64_t k = k0 + (uint64_t)u * RB;
-      p[u] = k < E ? __ldcs(phys + (k << shift)) : 0ull;
+      p[u] = k < E ? ld_phys(phys + (k << shift)) : 0ull;
     }
 #pragma unroll
     for (int u = 0; u < REPT; ++u) {

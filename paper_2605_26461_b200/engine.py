@@ -203,6 +203,23 @@ class FaultEngine:
                            out_bufs["counts"][:Cn], out_bufs["dkeys"][:s.n_dedup],
                            out_bufs["didx"][:s.n_dedup], out_bufs["cancel"][:s.n_cancel], int(s.path))
 
+    # -- batched top half (faults.classify + range_at per entry) ------------------------------
+    def classify(self, entries: np.ndarray, base_index: int = 0):
+        """``mpsf_classify``: (scenario id u8[n] -- 0xFF skipped --, rid u32[n] -- 0xFFFFFFFF
+        none) of every entry, as ``raise_mmu_fault`` classifies it (pipeline.py:103-104)."""
+        import torch
+        entries = np.ascontiguousarray(entries, dtype=ENTRY_DTYPE)
+        n = len(entries)
+        dev = torch.device("cuda", self.device)
+        d_in = torch.from_numpy(entries.view(np.uint8).copy() if n else np.zeros(16, np.uint8)).to(dev)
+        d_s = torch.empty(max(n, 2), dtype=torch.uint8, device=dev)
+        d_r = torch.empty(max(4 * n, 8), dtype=torch.uint8, device=dev)
+        stream = torch.cuda.current_stream(self.device)
+        self._check(self.lib.mpsf_classify(self.ctx, d_in.data_ptr(), n, base_index, d_s.data_ptr(), d_r.data_ptr(),
+                                           C.c_void_p(stream.cuda_stream)))
+        self.summary()
+        return d_s[:n].cpu().numpy(), d_r[:4 * n].cpu().numpy().view(np.uint32)
+
     # -- batched translation (resolve_va over an access stream) -------------------------------
     def translate_device(self, d_acc, n: int, d_hit, d_faults, d_fault_idx, d_pop_idx, base_index: int = 0,
                          stream=None) -> None:

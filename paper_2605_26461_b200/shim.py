@@ -127,16 +127,48 @@ def service_bottom_half_gpu(world, engine=None) -> list:
     return labels
 
 
-def install(engine=None):
-    """Patch ``mpssim.pipeline.service_bottom_half`` with the batch path; returns an undo."""
+REMAP_CHECKS = {"maps": 0, "pages": 0}
+
+
+def vmm_map_with_remap(orig, engine):
+    """``MemoryModel.vmm_map`` (memory.py:269-283) that also builds the mapping's remap table on
+    the device: entry i = (range base + i * 4 KiB, alloc.pages[i]) -- the page-granular state the
+    reference's PageRecs alias (one PageRec per physical page of the allocation).  The table is
+    checked against the reference's own allocation on every call (deploy_pair maps weights and
+    KV this way, recovery.py:175-184) and kept as ``world.remap_tables[rid]``."""
+    def vmm_map(self, world, pid, handle):
+        rng = orig(self, world, pid, handle)
+        eng = engine if engine is not None else default_engine()
+        phys = np.asarray(self.allocations[handle].pages, dtype=np.uint64)
+        table = eng.remap(rng.base, phys, K.PAGE_SHIFT)
+        if not (np.array_equal(table["phys"], phys) and np.array_equal(
+                table["va"], np.uint64(rng.base) + (np.arange(len(phys), dtype=np.uint64) << np.uint64(K.PAGE_SHIFT)))):
+            raise ShimMismatch(f"remap table of rid {rng.rid} differs from the allocation's pages")
+        if not hasattr(world, "remap_tables"):
+            world.remap_tables = {}
+        world.remap_tables[rng.rid] = table
+        REMAP_CHECKS["maps"] += 1
+        REMAP_CHECKS["pages"] += len(phys)
+        return rng
+    return vmm_map
+
+
+def install(engine=None, remap: bool = True):
+    """Patch ``mpssim.pipeline.service_bottom_half`` with the batch path (and, with ``remap``,
+    ``MemoryModel.vmm_map`` with the device remap); returns an undo."""
+    from mpssim import memory as M
     from mpssim import pipeline as P
     orig = P.service_bottom_half
+    orig_map = M.MemoryModel.vmm_map
 
     def patched(world):
         return service_bottom_half_gpu(world, engine)
 
     P.service_bottom_half = patched
+    if remap:
+        M.MemoryModel.vmm_map = vmm_map_with_remap(orig_map, engine)
 
     def undo():
         P.service_bottom_half = orig
+        M.MemoryModel.vmm_map = orig_map
     return undo

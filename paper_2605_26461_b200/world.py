@@ -19,8 +19,9 @@ that state as flat tables it can put in HBM once and read from every entry:
 Two producers exist: :class:`WorldBuilder`, a from-scratch restatement of the
 reference's allocation APIs used for synthetic configs (no reference import),
 and :func:`export_reference_world`, which reads a live reference ``World``
-(duck-typed; used by the DES drop-in shim).  ``tests/test_world.py`` checks the
-two agree on the same recipe.
+(duck-typed; used by the DES drop-in shim).
+``tests/test_oracle_vs_reference.py::test_classify_equals_reference_classify_on_synthetic_world`` checks the two
+give identical tables for the same recipe.
 """
 
 from __future__ import annotations

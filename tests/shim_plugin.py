@@ -14,6 +14,10 @@ class OracleEngine:
     def upload_world(self, flat):
         self.flat = flat
 
+    def remap(self, va_base, phys, gran_log2):
+        from oracle import seq_oracle as so
+        return so.remap_table(va_base, phys, gran_log2)
+
     def process(self, entries, params):
         from oracle import c_oracle as co
         from oracle import seq_oracle as so
@@ -34,6 +38,9 @@ class CountingEngine:
     def upload_world(self, flat):
         self.eng.upload_world(flat)
 
+    def remap(self, va_base, phys, gran_log2):
+        return self.eng.remap(va_base, phys, gran_log2)
+
     def process(self, entries, params):
         CALLS["n"] += 1
         CALLS["records"] += len(entries)
@@ -46,4 +53,6 @@ def pytest_configure(config):
 
 
 def pytest_sessionfinish(session, exitstatus):
-    print(f"\nSHIM_CALLS={CALLS['n']} SHIM_RECORDS={CALLS['records']}")
+    from paper_2605_26461_b200.shim import REMAP_CHECKS
+    print(f"\nSHIM_CALLS={CALLS['n']} SHIM_RECORDS={CALLS['records']} "
+          f"REMAP_MAPS={REMAP_CHECKS['maps']} REMAP_PAGES={REMAP_CHECKS['pages']}")

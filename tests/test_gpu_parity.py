@@ -386,3 +386,47 @@ def test_wild_page_hash_overflow_retries_exactly(eng):
     finally:
         fresh.close()
     assert_same(run_device(eng, w, e, p), want, "device")
+
+
+# -- batched top half (mpsf_classify): the reference's per-record classify + range_at ------------
+
+def test_batched_classify_golden_c1(eng):
+    """mpsf_classify on the 20k-entry config-1 trace equals faults.classify / range_at as the
+    reference computed them (tests/golden/classify_c1.npz, made by the reference itself)."""
+    z = G.classify_c1()
+    w, _ = synth.build_synthetic_world(4, 16, 1)
+    eng.upload_world(w)
+    sid, rid = eng.classify(z["entries"])
+    assert np.array_equal(sid, z["scenario"])
+    assert np.array_equal(rid, z["rid"])
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_batched_classify_vs_process(eng, seed):
+    """The top half alone equals the scenario / rid fields mpsf_process writes, on random worlds
+    with parse-time, trap, invalid and wild entries (and a world beyond the fixed layout)."""
+    rnd = random.Random(700 + seed)
+    for it in range(40):
+        w = RW.random_world(rnd, max_mps=6, max_sa=3)
+        entries = RW.random_batch(rnd, w, rnd.randint(1, 400))
+        eng.upload_world(w)
+        sid, rid = eng.classify(entries, base_index=it)
+        full = eng.process(entries, BatchParams())
+        assert np.array_equal(sid, full.out["scenario"]), (seed, it)
+        assert np.array_equal(rid, full.out["rid"]), (seed, it)
+    w, trace = synth.build_synthetic_world(80, 4, 5)[0], None
+    trace = synth.generate_trace(w, synth.TraceSpec(n=5000, seed=seed, parse_frac=0.01, trap_frac=0.001))
+    eng.upload_world(w)
+    sid, rid = eng.classify(trace)
+    full = eng.process(trace, BatchParams())
+    assert np.array_equal(sid, full.out["scenario"]) and np.array_equal(rid, full.out["rid"])
+
+
+def test_batched_classify_errors(eng):
+    w, _ = synth.build_synthetic_world(2, 4, 1)
+    eng.upload_world(w)
+    e = np.zeros(3, ENTRY_DTYPE)
+    e[:] = (0x100000, 0, 0, 0, 0, 1)
+    e[2]["channel"] = 999
+    with pytest.raises(NoChannelAttribution):
+        eng.classify(e)

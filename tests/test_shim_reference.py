@@ -25,3 +25,4 @@ def test_reference_suite_passes_with_batch_bottom_half():
     assert "169 passed" in tail, tail
     calls = int(tail.split("SHIM_CALLS=")[1].split()[0])
     assert calls > 100, tail
+    assert int(tail.split("REMAP_MAPS=")[1].split()[0]) > 10, tail     # vmm_map remap tables checked
