@@ -132,6 +132,36 @@ __device__ __forceinline__ D decode(const uint8_t* sm, const uint8_t* __restrict
 // bits 0..31
 constexpr uint32_t R_KDUP = 1u << 31;
 
+// entries per lane per step of pass 1 (4 measured: k_scan 1.27 -> 1.87-2.24 ms at config 3 for
+// 512-1024-thread CTAs -- register spills / fewer warps; profiles/r02/ab_entries_per_lane.txt)
+constexpr int EPL = 2;
+
+// Entry stream of pass 1: warp w of the grid owns steps w, w + W, ... of 32 * EPL entries; lane l
+// reads its EPL adjacent entries (32-byte non-allocating loads), the next step's requested before
+// the current one is processed.
+template <int N, typename F>
+__device__ __forceinline__ void stream_n(const mpsf_fault_entry* in, uint64_t n64, F&& fn) {
+  constexpr uint32_t CH = 32 * N;
+  const uint32_t n = (uint32_t)n64;   // < MAX_GIDX
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + warp, GW = gridDim.x * (blockDim.x >> 5);
+  const uint32_t nch = (n + CH - 1) / CH;
+  const bool a32 = ((uintptr_t)in & 31u) == 0;
+  uint4 nx[N];
+  auto load = [&](uint32_t c) {
+#pragma unroll
+    for (int u = 0; u < N; u += 2) ld_pair(in, n, c * CH + N * lane + u, a32, nx[u], nx[u + 1]);
+  };
+  if (gw < nch) load(gw);
+  for (uint32_t c = gw; c < nch; c += GW) {
+    uint4 e[N];
+#pragma unroll
+    for (int u = 0; u < N; ++u) e[u] = nx[u];
+    if (c + GW < nch) load(c + GW);
+    fn(e, c * CH + N * lane);
+  }
+}
+
 // Pass 1 over [0, n) (global index P.base_index + i).  As pass 2, the common path has no
 // data-dependent branch: the block-local minima and counts are predicated shared-memory
 // reductions, the global pre-check loads and minima predicated accesses; the work a warp would
@@ -156,7 +186,9 @@ __device__ __forceinline__ void scan_body(const World& W, const Scratch& S, uint
   const bool sparse = W.dd_groups == 1;
   const uint32_t G = W.dd_groups, gmask = sparse ? 0u : 7u;
   uint32_t* counts = reinterpret_cast<uint32_t*>(sm + O_CNT);
-  uint32_t* iso = reinterpret_cast<uint32_t*>(sm + O_ISO) + warp;
+  // per-warp copies of the per-(mechanism class, client) minima, one row per warp: a warp's lanes
+  // spread over the banks (a column-per-warp layout put every lane of a warp on one bank)
+  uint32_t* iso = reinterpret_cast<uint32_t*>(sm + O_ISO) + warp * (3 * FX_C);
   uint32_t* r32 = reinterpret_cast<uint32_t*>(sm + O_R32);
   uint32_t* used = reinterpret_cast<uint32_t*>(sm + O_USED);
   unsigned long long* c64 = reinterpret_cast<unsigned long long*>(sm + O_C64);
@@ -204,7 +236,7 @@ __device__ __forceinline__ void scan_body(const World& W, const Scratch& S, uint
     const bool elig = (f & LF_ELIG) != 0;
     const uint32_t m = (f >> LF_M_SH) & 3u;
     const bool inw = d.inr | d.grd;
-    min_s_if(elig, iso + (m * C + c) * 32, o.ok);
+    min_s_if(elig, iso + (m * C + c), o.ok);
     min_s_if(elig & (d.grd | (d.inr & (m == 2))), r32 + (d.grd ? FX_R : 0u) + d.k, o.ok);
     const bool dd = (f & LF_DD) != 0;
     o.qn = elig & !inw;
@@ -230,42 +262,53 @@ __device__ __forceinline__ void scan_body(const World& W, const Scratch& S, uint
     if (pos < QCAP) q[pos] = x;
     else q_exec(S, used, x);                      // queue full (a chunk of wild pages): now
   };
-  ldg_stream(in, n, [&](uint4 e0, uint32_t i0, bool ok0, uint4 e1, uint32_t i1, bool ok1) {
-    if (!ok0) e0.w = 0;
-    if (!ok1) e1.w = 0;
-    O o0, o1;
-    D d0, d1;
-    first(e0, base + i0, o0, d0);
-    const uint32_t ra0 = ldcg_if(o0.p_a, o0.pa, 0u), rd0 = ldcg_if(o0.p_dd, o0.pd, EMPTY32);
-    first(e1, base + i1, o1, d1);
-    const uint32_t ra1 = ldcg_if(o1.p_a, o1.pa, 0u), rd1 = ldcg_if(o1.p_dd, o1.pd, EMPTY32);
-    second(e0, base + i0, o0, d0);
-    second(e1, base + i1, o1, d1);
-    // a smaller index of the same key already in the slot: a duplicate whatever comes later
-    const bool kd0 = (rd0 != EMPTY32) & ((rd0 & 7u) == (o0.vd & 7u)) & (rd0 < o0.vd);
-    const bool kd1 = (rd1 != EMPTY32) & ((rd1 & 7u) == (o1.vd & 7u)) & (rd1 < o1.vd);
-    const uint32_t lo0 = o0.lo | (kd0 ? R_KDUP : 0u), lo1 = o1.lo | (kd1 ? R_KDUP : 0u);
-    unsigned long long* rp = drec + i0;
-    const unsigned long long r0 = (unsigned long long)lo0 | ((unsigned long long)o0.hi << 32);
-    const unsigned long long r1 = (unsigned long long)lo1 | ((unsigned long long)o1.hi << 32);
-    if (ok1 && (((uintptr_t)rp & 15u) == 0)) __stcs(reinterpret_cast<ulonglong2*>(rp), make_ulonglong2(r0, r1));
-    else {
-      if (ok0) __stcs(rp, r0);
-      if (ok1) __stcs(rp + 1, r1);
+  stream_n<EPL>(in, n, [&](const uint4* e, uint32_t i0) {
+    O o[EPL];
+    D d[EPL];
+    uint32_t ra[EPL], rd[EPL];
+    bool ok[EPL], kd[EPL];
+#pragma unroll
+    for (int u = 0; u < EPL; ++u) {
+      ok[u] = i0 + u < (uint32_t)n;
+      uint4 eu = e[u];
+      if (!ok[u]) eu.w = 0;                            // past the end: decodes as a skipped entry
+      first(eu, base + i0 + u, o[u], d[u]);
+      ra[u] = ldcg_if(o[u].p_a, o[u].pa, 0u);
+      rd[u] = ldcg_if(o[u].p_dd, o[u].pd, EMPTY32);
     }
-    min_g_if(o0.p_a, ra0, o0.pa, o0.ok);
-    min_g_if(o1.p_a, ra1, o1.pa, o1.ok);
-    // dense slots: a predicated atomic MIN; claimed slots: claim (CAS), or MIN, or the hash
-    min_g_if(o0.p_dd & !sparse & !kd0, rd0, o0.pd, o0.vd);
-    min_g_if(o1.p_dd & !sparse & !kd1, rd1, o1.pd, o1.vd);
-    const bool cl0 = o0.p_dd & sparse & !kd0, cl1 = o1.p_dd & sparse & !kd1;
-    if (cl0) claim_resolve(S, used, o0.pd, o0.vd, rd0, key_of(o0));
-    if (cl1) claim_resolve(S, used, o1.pd, o1.vd, rd1, key_of(o1));
-    if (o0.qn | o0.qd | o1.qn | o1.qd) {
-      if (o0.qn) push(nr_key((o0.lo >> 14) & 63u, 0, o0.page), o0.ok, 1);
-      if (o0.qd) push(key_of(o0), o0.vd >> 3, 0);
-      if (o1.qn) push(nr_key((o1.lo >> 14) & 63u, 0, o1.page), o1.ok, 1);
-      if (o1.qd) push(key_of(o1), o1.vd >> 3, 0);
+#pragma unroll
+    for (int u = 0; u < EPL; ++u) second(e[u], base + i0 + u, o[u], d[u]);
+    unsigned long long r[EPL];
+#pragma unroll
+    for (int u = 0; u < EPL; ++u) {
+      // a smaller index of the same key already in the slot: a duplicate whatever comes later
+      kd[u] = (rd[u] != EMPTY32) & ((rd[u] & 7u) == (o[u].vd & 7u)) & (rd[u] < o[u].vd);
+      r[u] = (unsigned long long)(o[u].lo | (kd[u] ? R_KDUP : 0u)) | ((unsigned long long)o[u].hi << 32);
+    }
+    unsigned long long* rp = drec + i0;
+#pragma unroll
+    for (int u = 0; u < EPL; u += 2) {
+      if (ok[u + 1] && (((uintptr_t)(rp + u) & 15u) == 0)) __stcs(reinterpret_cast<ulonglong2*>(rp + u), make_ulonglong2(r[u], r[u + 1]));
+      else {
+        if (ok[u]) __stcs(rp + u, r[u]);
+        if (ok[u + 1]) __stcs(rp + u + 1, r[u + 1]);
+      }
+    }
+    bool any_q = false;
+#pragma unroll
+    for (int u = 0; u < EPL; ++u) {
+      min_g_if(o[u].p_a, ra[u], o[u].pa, o[u].ok);
+      // dense slots: a predicated atomic MIN; claimed slots: claim (CAS), or MIN, or the hash
+      min_g_if(o[u].p_dd & !sparse & !kd[u], rd[u], o[u].pd, o[u].vd);
+      if (o[u].p_dd & sparse & !kd[u]) claim_resolve(S, used, o[u].pd, o[u].vd, rd[u], key_of(o[u]));
+      any_q |= o[u].qn | o[u].qd;
+    }
+    if (any_q) {
+#pragma unroll
+      for (int u = 0; u < EPL; ++u) {
+        if (o[u].qn) push(nr_key((o[u].lo >> 14) & 63u, 0, o[u].page), o[u].ok, 1);
+        if (o[u].qd) push(key_of(o[u]), o[u].vd >> 3, 0);
+      }
     }
     __syncwarp();
     uint32_t qn = min(*qc, (uint32_t)QCAP);
@@ -293,7 +336,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_scan_fx(World W, Scratch S, const 
   unsigned long long* c64 = reinterpret_cast<unsigned long long*>(sm + O_C64);
   for (uint32_t i = tid; i < 3 * C + 2; i += nb) c64[i] = EMPTY64;
   uint32_t* iso = reinterpret_cast<uint32_t*>(sm + O_ISO);
-  for (uint32_t i = tid; i < 3 * 32 * C; i += nb) iso[i] = EMPTY32;
+  for (uint32_t i = tid; i < 3 * FX_C * 32; i += nb) iso[i] = EMPTY32;
   uint32_t* r32 = reinterpret_cast<uint32_t*>(sm + O_R32);
   for (uint32_t i = tid; i < R1; i += nb) { r32[i] = EMPTY32; r32[FX_R + i] = EMPTY32; }
   uint32_t* cnt = reinterpret_cast<uint32_t*>(sm + O_CNT);
@@ -308,10 +351,9 @@ __global__ void __launch_bounds__(BLOCK, 1) k_scan_fx(World W, Scratch S, const 
     if (cnt[i]) atomicAdd(counts + i, (unsigned long long)cnt[i]);
   // fold the block-local minima into the global ones (same slots as flush_minima)
   for (uint32_t i = tid; i < 3 * C; i += nb) {
-    const uint32_t* w = iso + i * 32;
     uint32_t m = EMPTY32;
 #pragma unroll 8
-    for (int k = 0; k < 32; ++k) m = min(m, w[k]);
+    for (int k = 0; k < 32; ++k) m = min(m, iso[k * (3 * FX_C) + i]);
     uint32_t* g = (i < C ? S.iso1 : (i < 2 * C ? S.iso2 : S.iso3)) + (i % C);
     if (m != EMPTY32) atomicMin(g, m);
     const unsigned long long t = c64[i];

@@ -1,6 +1,9 @@
 """Per-source-line instruction counts and stall samples from an ncu report (experiment tool).
 
-    python tools/sass_lines.py report.ncu-rep lib.so kernel-mangled-substring [top] [ncu-kernel-regex]
+    python tools/sass_lines.py report.ncu-rep lib.so kernel-mangled-substring [top] [ncu-kernel-regex] [column]
+
+column: the per-instruction metric to aggregate instead of "Instructions Executed" (e.g.
+"L1 Wavefronts Shared Excessive" for shared-memory bank conflicts).
 
 Exports the report's SASS page, disassembles the same kernel from the library with line info
 (nvdisasm -g), maps SASS offsets to (file, line) and aggregates executed warp instructions and
@@ -33,7 +36,7 @@ def main():
                 break
     rows = list(csv.reader(io.StringIO('"Kernel Name"' + pick)))
     hdr = rows[1]
-    ia = hdr.index("Instructions Executed")
+    ia = hdr.index(sys.argv[6] if len(sys.argv) > 6 else "Instructions Executed")
     isamp = hdr.index("Warp Stall Sampling (All Samples)")
     data = [r for r in rows[2:] if len(r) > ia and r[0].startswith("0x")]
     base = int(data[0][0], 16)
