@@ -23,6 +23,8 @@ constexpr uint32_t NCH = FX_CH + 1;            // channel rows (the last: invali
 constexpr uint32_t CH_COPIES = 8;              // replicas of a channel row (one per quarter-warp lane)
 constexpr uint32_t LUT2_XK = 16 * 16 * 8;      // [min(eng,3) * 4 + min(acc,3)][range class][state]
 constexpr uint32_t LUT2_N = LUT2_XK + 16;      // + the non-translation kinds
+// (not replicated per lane: a batch hits few distinct LUT words, which a single copy serves as
+// broadcasts; 8 replicas made k_scan 1.2 -> 2.1 ms at config 3 -- profiles/r02/ab_lut_replicas.txt)
 
 __host__ __device__ constexpr uint32_t a16(uint32_t x) { return (x + 15u) & ~15u; }
 
@@ -42,13 +44,17 @@ constexpr uint32_t O_CNT = O_R32 + 4 * 2 * FX_R;
 constexpr uint32_t O_USED = O_CNT + 4 * NSCEN * FX_C;
 constexpr uint32_t O_QCNT = O_USED + 16;
 constexpr uint32_t SCAN_BYTES = O_QCNT + 4 * WARPS;
-// pass 2
-constexpr uint32_t O_FCL = O_PASS;
-constexpr uint32_t O_RRID = O_FCL + 32 * FX_C;
-constexpr uint32_t O_EXT = O_RRID + 4 * FX_R;
-constexpr uint32_t O_NR0 = O_EXT + 4 * FX_R;
-constexpr uint32_t O_SLOWQ = O_NR0 + 4 * FX_R;
-constexpr uint32_t FIN_BYTES = O_SLOWQ + WARPS * 96 * 16;
+// pass 2 (its own layout: it needs neither the LUT nor the channel / skip tables)
+constexpr uint32_t RID_COPIES = 8;             // replicas of the rid table (one per quarter-warp lane)
+constexpr uint32_t F_SLUT = 0;
+constexpr uint32_t F_ROWS = 128;
+constexpr uint32_t F_FCA = F_ROWS + FX_R * 16;                     // [client][8 copies] {rel_lt, tie, flags, -}
+constexpr uint32_t F_FCB = F_FCA + FX_C * CH_COPIES * 16;          // [client] {trap_ok, ft0, ft1, -}
+constexpr uint32_t F_RRID = F_FCB + FX_C * 16;                     // [range][8 copies]
+constexpr uint32_t F_EXT = F_RRID + 4 * FX_R * RID_COPIES;
+constexpr uint32_t F_NR0 = F_EXT + 4 * FX_R;
+constexpr uint32_t F_SLOWQ = F_NR0 + 4 * FX_R;
+constexpr uint32_t FIN_BYTES = F_SLOWQ + WARPS * 96 * 16;
 static_assert(SCAN_BYTES <= 227 * 1024 && FIN_BYTES <= 227 * 1024, "fixed layout exceeds shared memory");
 
 __device__ __forceinline__ uint32_t lut2_word(uint32_t idx, bool isolation) {
@@ -106,19 +112,22 @@ __device__ __forceinline__ D decode(const uint8_t* sm, const uint8_t* __restrict
   d.slot = row.z + (d.page - row.x);
   const bool pp = d.inr & ((row.w & ROW_PERPAGE) != 0);
   const uint32_t pst = pp ? ps[d.slot] : row.w;                 // per-page state byte, else the uniform one
-  // LUT index: [engine][access][range class][state] (engine / access 3 -> a BAD word), or the kind
+  // LUT index: [engine][access][range class][state] (engine / access 3 -> a BAD word, > 3 caught
+  // below), or the kind
+  const uint32_t eng = w3 & 0xFFu;
+  const bool ea_bad = (w3 & 0xFCFCu) != 0;
   const uint32_t ea = ((w3 & 3u) << 9) | ((w3 & 0x300u) >> 1);
   const uint32_t t = d.inr ? ((row.w & 0x38u) | (pst & 7u)) : 64u;
   const uint32_t idx = ek == 0 ? ea + t : LUT2_XK + min(ek, 15u);
   const uint32_t f = reinterpret_cast<const uint32_t*>(sm + O_LUT)[idx];
   d.cw = cr.x;
-  const uint32_t eng = w3 & 0xFFu, ceng = (cr.x >> 16) & 3u;
-  const bool tbad = (ek == 0) & (((w3 & 0xFCFCu) != 0) | (eng != ceng) | (e.y >= (1u << 21)));
+  const uint32_t ceng = (cr.x >> 16) & 3u;
+  const bool tbad = (ek == 0) & (ea_bad | (eng != ceng) | (e.y >= (1u << 21)));
   const bool bad = !(cr.x & CH_VALID) | ((f & LF_BAD) != 0) | tbad;
   const bool valid = (w3 >> 24) & MPSF_ENTRY_VALID;
   if (valid && bad) {                                             // malformed entry (never in a valid trace)
     const uint32_t bit = !(cr.x & CH_VALID) ? EB_NO_CHANNEL
-                         : (((f & LF_BAD) != 0) | ((ek == 0) & ((w3 & 0xFCFCu) != 0))) ? EB_BAD_ENTRY
+                         : (((f & LF_BAD) != 0) | ((ek == 0) & ea_bad)) ? EB_BAD_ENTRY
                          : (eng != ceng ? EB_MISMATCH : EB_VA);
     raise_err(S, bit, gidx);
   }
@@ -393,21 +402,31 @@ __device__ __forceinline__ uint32_t slut2_word(uint32_t sid, bool isolation) {
          ((f & LF_REPL) ? 0u : S2_NONREPL);
 }
 
-// per-client decision row (32 B): epoch-1 threshold, applied trap, applied fatal reports, kill tie,
-// flags (bit0: benign always cancelled, bit1: same on a CE channel, bit2: epoch-1 keys are pass 1's)
-struct Fc2 {
-  uint32_t rel_lt, trap_ok, ft0, ft1;
-  uint32_t tie, flags, pad0, pad1;
-};
-
-__device__ __forceinline__ Fc2 fc2_of(const FinClient& f) {
-  Fc2 r;
+// per-client decision rows: A (every entry) = {epoch-1 threshold, kill tie, flags (bit0: benign
+// always cancelled, bit1: same on a CE channel, bit2: epoch-1 keys are pass 1's)}; B (trap and
+// fatal-report entries only) = {applied trap, applied fatal report on GR / SA, ... on CE}
+__device__ __forceinline__ void fc_rows(const FinClient& f, uint4& a, uint4& b) {
   // epoch 1 iff rel < ok32 (ok32 < 2^32 - 1):  ok32 >= rel + 1, with rel = REL_PRE -> 0, REL_NONE -> ~0
-  r.rel_lt = f.rel < 0 ? 0u : (f.rel >= (long long)0xFFFFFFFEll ? 0xFFFFFFFFu : (uint32_t)f.rel + 1u);
-  r.trap_ok = f.trap_ok; r.ft0 = f.ft0; r.ft1 = f.ft1; r.tie = f.tie;
-  r.flags = (f.bflags & 3u) | (f.pre_nrall ? 4u : 0u);
-  r.pad0 = r.pad1 = 0;
-  return r;
+  a.x = f.rel < 0 ? 0u : (f.rel >= (long long)0xFFFFFFFEll ? 0xFFFFFFFFu : (uint32_t)f.rel + 1u);
+  a.y = f.tie;
+  a.z = (f.bflags & 3u) | (f.pre_nrall ? 4u : 0u);
+  a.w = 0;
+  b = make_uint4(f.trap_ok, f.ft0, f.ft1, 0u);
+}
+
+__device__ __forceinline__ uint4 lds128_if(bool p, const void* a) {   // predicated shared load (zeros if !p)
+  uint4 v;
+  asm("{.reg .pred q; setp.ne.u32 q, %5, 0; mov.b32 %0, 0; mov.b32 %1, 0; mov.b32 %2, 0; mov.b32 %3, 0;"
+      " @q ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];}"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"((uint32_t)__cvta_generic_to_shared(a)), "r"((uint32_t)p));
+  return v;
+}
+
+__device__ __forceinline__ uint32_t lds32_if(bool p, const void* a, uint32_t dflt) {
+  uint32_t v;
+  asm("{.reg .pred q; setp.ne.u32 q, %2, 0; mov.b32 %0, %3; @q ld.shared.u32 %0, [%1];}"
+      : "=r"(v) : "r"((uint32_t)__cvta_generic_to_shared(a)), "r"((uint32_t)p), "r"(dflt));
+  return v;
 }
 
 __global__ void __launch_bounds__(BLOCK, 1) k_finalize_fx(World W, Scratch S, uint64_t n, Params P,
@@ -416,27 +435,41 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize_fx(World W, Scratch S, ui
   pdl_trigger();
   const uint32_t tid = threadIdx.x, nb = blockDim.x;
   const bool isolation = P.flags & MPSF_PF_ISOLATION;
-  stage_tables(sm, W, isolation);
-  uint32_t* slut2 = reinterpret_cast<uint32_t*>(sm + O_SLUT);      // (the pass-1 scenario words are not needed)
+  uint32_t* slut2 = reinterpret_cast<uint32_t*>(sm + F_SLUT);
   if (tid < 32) slut2[tid] = tid == 31 ? 0u : slut2_word(tid, isolation);
-  uint32_t* rrid = reinterpret_cast<uint32_t*>(sm + O_RRID);
-  for (uint32_t i = tid; i < FX_R; i += nb) rrid[i] = i <= W.n_ranges ? __ldg(W.rrid + i) : NO_RID;
+  uint4* rows_w = reinterpret_cast<uint4*>(sm + F_ROWS);
+  for (uint32_t i = tid; i <= W.n_ranges; i += nb) rows_w[i] = __ldg(W.row4 + i);
+  uint32_t* rrid = reinterpret_cast<uint32_t*>(sm + F_RRID);
+  for (uint32_t i = tid; i < FX_R * RID_COPIES; i += nb) {
+    const uint32_t r = i / RID_COPIES;
+    rrid[i] = r <= W.n_ranges ? __ldg(W.rrid + r) : NO_RID;
+  }
   pdl_wait();
   if (__ldcg(S.ctrl + C_ERR) != 0) return;
-  Fc2* fcl = reinterpret_cast<Fc2*>(sm + O_FCL);
-  for (uint32_t k = tid; k < W.n_clients; k += nb) fcl[k] = fc2_of(fin_client(S.cstate[k], *S.glob, S.nrall != nullptr));
-  uint32_t* ext = reinterpret_cast<uint32_t*>(sm + O_EXT);
-  uint32_t* nr0 = reinterpret_cast<uint32_t*>(sm + O_NR0);
+  uint4* fca = reinterpret_cast<uint4*>(sm + F_FCA);
+  uint4* fcb = reinterpret_cast<uint4*>(sm + F_FCB);
+  for (uint32_t k = tid; k < FX_C * CH_COPIES; k += nb) {
+    const uint32_t c = k / CH_COPIES;
+    uint4 a = make_uint4(0xFFFFFFFFu, EMPTY32, 0u, 0u), b = make_uint4(EMPTY32, EMPTY32, EMPTY32, 0u);
+    if (c < W.n_clients) fc_rows(fin_client(S.cstate[c], *S.glob, S.nrall != nullptr), a, b);
+    fca[k] = a;
+    if (k % CH_COPIES == 0) fcb[c] = b;
+  }
+  uint32_t* ext = reinterpret_cast<uint32_t*>(sm + F_EXT);
+  uint32_t* nr0 = reinterpret_cast<uint32_t*>(sm + F_NR0);
   for (uint32_t i = tid; i < FX_R; i += nb) {
     ext[i] = i < W.n_ranges ? __ldcg(S.ext + i) : EMPTY32;
     nr0[i] = i < W.n_ranges ? __ldcg(S.nr0 + i) : EMPTY32;
   }
   __syncthreads();
-  const uint4* rows = reinterpret_cast<const uint4*>(sm + O_ROWS);
+  const uint4* rows = reinterpret_cast<const uint4*>(sm + F_ROWS);
   const uint32_t lane = tid & 31, warp = tid >> 5;
+  const uint32_t copy16 = (lane & (CH_COPIES - 1)) * 16, copy4 = (lane & (RID_COPIES - 1)) * 4;
+  const uint8_t* fca_l = sm + F_FCA + copy16;        // this lane's replica: + c * 128
+  const uint8_t* rrid_l = sm + F_RRID + copy4;       // + k * 32
   const uint32_t base = (uint32_t)P.base_index;
   const uint32_t G = W.dd_groups, gmask = W.dd_groups == 1 ? 0u : 7u;
-  uint4* sq = reinterpret_cast<uint4*>(sm + O_SLOWQ) + warp * SQ_CAP;   // {lo, hi, batch index, dd word}
+  uint4* sq = reinterpret_cast<uint4*>(sm + F_SLOWQ) + warp * SQ_CAP;   // {lo, hi, batch index, dd word}
   uint32_t sqn = 0;
 
   // the general resolution of one queued entry (hash lookups allowed), by one lane
@@ -446,9 +479,9 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize_fx(World W, Scratch S, ui
     const uint32_t loc = (lo >> 10) & 3u, grp = (lo >> 5) & 7u, m = (lo >> 8) & 3u;
     const bool inr = loc == LOC_IN, inw = inr || loc == LOC_GUARD;
     const uint32_t sw = slut2[sid];
-    const Fc2 fc = fcl[c];
+    const uint4 fa = fca[c * CH_COPIES], fb = fcb[c];
     const uint32_t ok = gidx | (sw & S2_NONREPL);
-    const bool ep1 = ok >= fc.rel_lt, elig = sw & S2_ELIG, dd = sw & S2_DD;
+    const bool ep1 = ok >= fa.x, elig = sw & S2_ELIG, dd = sw & S2_DD;
     const uint64_t page = inw ? (uint64_t)(rows[k].x + (hi - rows[k].z)) : ((uint64_t)hi | ((uint64_t)k << 32));
     unsigned long long key = dd ? dedup_key(c, (int)ceng, (int)sid, page) : 0ull;
     uint32_t ri = ok;
@@ -457,12 +490,12 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize_fx(World W, Scratch S, ui
     const uint32_t rep_ok = dd ? ri : ok;
     const bool ce = ceng == 1;
     bool canc = false;
-    if (sw & S2_TRAP) canc = gidx != fc.trap_ok;
-    else if (sw & S2_SERV) canc = ((fc.flags >> (ce ? 1 : 0)) & 1u) || rep_ok > fc.tie;
-    else if (sw & S2_FATAL) canc = rep_ok != (ce ? fc.ft1 : fc.ft0);
+    if (sw & S2_TRAP) canc = gidx != fb.x;
+    else if (sw & S2_SERV) canc = ((fa.z >> (ce ? 1 : 0)) & 1u) || rep_ok > fa.y;
+    else if (sw & S2_FATAL) canc = rep_ok != (ce ? fb.z : fb.y);
     uint32_t mech = 0;
     if (elig && !dup) {
-      const bool e1 = ep1 && !(fc.flags & 4u);
+      const bool e1 = ep1 && !(fa.z & 4u);
       if (!inr || ep1) {
         uint32_t nr;
         if (!inw) nr = hash_get(S.hnr, nr_key(c, e1 ? 1 : 0, page));
@@ -474,7 +507,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize_fx(World W, Scratch S, ui
       }
     }
     const uint32_t verdict = (sw & 0x7Fu) | (mech << 2) | (canc ? 0x10u : 0u) | (dup ? 0x20u : 0u);
-    const uint32_t rid = inr ? rrid[k] : NO_RID;
+    const uint32_t rid = inr ? rrid[k * RID_COPIES] : NO_RID;
     __stcs(reinterpret_cast<unsigned long long*>(out) + i, (unsigned long long)rid | ((unsigned long long)sid << 32) |
            ((unsigned long long)verdict << 40) | ((unsigned long long)c << 48));
     const uint64_t qq = q_base + i / WCHUNK;
@@ -495,11 +528,11 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize_fx(World W, Scratch S, ui
     __syncwarp();
   };
 
-  // the common path of one entry: load addresses first (A), outcome after the loads (B)
+  // the common path of one entry: load addresses first (addr), outcome after the loads (fin)
   struct A {
     uint32_t lo, hi, sw, ok, k;
-    uint32_t flags;        // bit0 rep_free, bit1 want_rep, bit2 needs_nr, bit3 pe, bit4 slow, bit5 p_dd
-    uint32_t fcw[6];
+    uint32_t flags;        // bit0 rep_free, bit2 needs_nr, bit3 pe, bit4 slow
+    uint4 fa;              // the client's decision row A
     const uint32_t *pd, *pn;
     bool p_dd, p_nr;
     uint32_t smv;
@@ -510,26 +543,25 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize_fx(World W, Scratch S, ui
     a.sw = slut2[loc ? sid : 31u];
     const uint32_t sw = a.sw, c = (lo >> 14) & 63u;
     a.k = (lo >> 20) & 0x7FFu;
-    const uint4 f0 = *reinterpret_cast<const uint4*>(fcl + c);
-    const uint2 f1 = *reinterpret_cast<const uint2*>(&fcl[c].tie);
-    a.fcw[0] = f0.x; a.fcw[1] = f0.y; a.fcw[2] = f0.z; a.fcw[3] = f0.w; a.fcw[4] = f1.x; a.fcw[5] = f1.y;
+    a.fa = *reinterpret_cast<const uint4*>(fca_l + c * (CH_COPIES * 16));
+    const uint4 f0 = a.fa;
     a.ok = gidx | (sw & S2_NONREPL);
     const bool ep1 = a.ok >= f0.x;
     const bool inr = loc == LOC_IN, grd = loc == LOC_GUARD, inw = inr | grd, wild = loc == LOC_NONE;
     const bool kd = (lo & R_KDUP) != 0;
     const bool elig = (sw & S2_ELIG) != 0, dd = (sw & S2_DD) != 0, serv = (sw & S2_SERV) != 0;
-    const bool rep_free = kd & (elig | (serv & (f1.x == EMPTY32)));
+    const bool rep_free = kd & (elig | (serv & (f0.y == EMPTY32)));
     const bool want_rep = dd & !rep_free;
     const bool needs_nr = elig & !kd & (!inr | ep1);
-    const bool e1 = ep1 & !(f1.y & 4u);
+    const bool e1 = ep1 & !(f0.z & 4u);
     const bool pe = elig & !kd & inr & !ep1 & (((lo >> 8) & 3u) == 2u);
     const bool slow = wild & (want_rep | needs_nr);
     a.p_dd = want_rep & inw;
     a.pd = S.dd + (hi * G + (((lo >> 5) & 7u) & gmask));
     a.p_nr = needs_nr & (e1 ? inw : inr);
     a.pn = (e1 ? S.nr1 : S.nrall) + hi;
-    a.smv = (pe ? ext : nr0)[a.k];
-    a.flags = (rep_free ? 1u : 0u) | (want_rep ? 2u : 0u) | (needs_nr ? 4u : 0u) | (pe ? 8u : 0u) | (slow ? 16u : 0u);
+    a.smv = lds32_if(pe | (needs_nr & grd & !e1), (pe ? ext : nr0) + a.k, EMPTY32);
+    a.flags = (rep_free ? 1u : 0u) | (needs_nr ? 4u : 0u) | (pe ? 8u : 0u) | (slow ? 16u : 0u);
   };
   auto fin = [&](A& a, uint32_t wd, uint32_t wn, uint32_t gidx, unsigned long long& o8, bool& canc, bool& rep,
                  unsigned long long& key) {
@@ -543,19 +575,20 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize_fx(World W, Scratch S, ui
     const bool dup = dd & (rep_free | (ri != gidx));
     const uint32_t rep_ok = (dd & !rep_free) ? ri : a.ok;
     const uint32_t ce = ceng == 1 ? 1u : 0u;
-    const bool c_trap = gidx != a.fcw[1];
-    const bool c_serv = ((a.fcw[5] >> ce) & 1u) | (rep_ok > a.fcw[4]);
-    const bool c_fat = rep_ok != (ce ? a.fcw[3] : a.fcw[2]);
+    const uint4 fb = lds128_if((sw & (S2_TRAP | S2_FATAL)) != 0, fcb + c);   // trap / fatal entries only
+    const bool c_trap = gidx != fb.x;
+    const bool c_serv = ((a.fa.z >> ce) & 1u) | (rep_ok > a.fa.y);
+    const bool c_fat = rep_ok != (ce ? fb.z : fb.y);
     canc = ((sw & S2_TRAP) && c_trap) | ((sw & S2_SERV) && c_serv) | ((sw & S2_FATAL) && c_fat);
     const bool hit = wn == a.ok;
     const uint32_t mech = (elig & !dup) ? (needs_nr ? (hit ? 1u : 2u) : ((pe & hit) ? 3u : 2u)) : 0u;
     const uint32_t verdict = (sw & 0x7Fu) | (mech << 2) | (canc ? 0x10u : 0u) | (dup ? 0x20u : 0u);
-    const uint32_t rid = loc == LOC_IN ? rrid[k] : NO_RID;
+    const uint32_t rid = loc == LOC_IN ? *reinterpret_cast<const uint32_t*>(rrid_l + k * (RID_COPIES * 4)) : NO_RID;
     o8 = sw ? ((unsigned long long)rid | ((unsigned long long)sid << 32) | ((unsigned long long)verdict << 40) |
                ((unsigned long long)c << 48))
             : (0xFFFF000000000000ull | (0xFFull << 32) | NO_RID);
     rep = dd & !dup;
-    const uint4 row = rows[k];
+    const uint4 row = lds128_if(rep, rows + k);                          // representatives only
     key = dedup_key(c, (int)ceng, (int)sid, (uint64_t)(row.x + (hi - row.z)));
     if (a.flags & 16u) { canc = false; rep = false; }        // resolved by the slow path
   };
