@@ -1497,7 +1497,8 @@ static void set_attrs() {
   cudaFuncSetAttribute(k_general<kStaged, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(k_finalize<kStaged>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(fx::k_scan_fx, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-  cudaFuncSetAttribute(fx::k_finalize_fx, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(fx::k_finalize_fx<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(fx::k_finalize_fx<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   done = true;
 }
 
@@ -1572,8 +1573,9 @@ static int finalize_t(const World& W, const Scratch& S, const mpsf_fault_entry* 
   set_attrs<kStaged>();
   if (n == 0) return 0;
   if (kStaged && fx_fits(W)) {
-    const int g = clamp_grid(grid_for(fx::k_finalize_fx, fx::FIN_BYTES), n);
-    launch_pdl(fx::k_finalize_fx, dim3(g), dim3(BLOCK), fx::FIN_BYTES, st, W, S, n, P, out, q_base);
+    auto* k = W.dd_groups == 1 ? fx::k_finalize_fx<true> : fx::k_finalize_fx<false>;
+    const int g = clamp_grid(grid_for(k, fx::FIN_BYTES), n);
+    launch_pdl(k, dim3(g), dim3(BLOCK), fx::FIN_BYTES, st, W, S, n, P, out, q_base);
     mk.mark("k_finalize");
     return ok_or_err();
   }

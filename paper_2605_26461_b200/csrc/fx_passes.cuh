@@ -44,13 +44,14 @@ constexpr uint32_t O_CNT = O_R32 + 4 * 2 * FX_R;
 constexpr uint32_t O_USED = O_CNT + 4 * NSCEN * FX_C;
 constexpr uint32_t O_QCNT = O_USED + 16;
 constexpr uint32_t SCAN_BYTES = O_QCNT + 4 * WARPS;
-// pass 2 (its own layout: it needs neither the LUT nor the channel / skip tables)
+// pass 2 (its own layout: it needs neither the classification LUT nor the channel / skip tables)
 constexpr uint32_t RID_COPIES = 8;             // replicas of the rid table (one per quarter-warp lane)
-constexpr uint32_t F_SLUT = 0;
-constexpr uint32_t F_ROWS = 128;
-constexpr uint32_t F_FCA = F_ROWS + FX_R * 16;                     // [client][8 copies] {rel_lt, tie, flags, -}
-constexpr uint32_t F_FCB = F_FCA + FX_C * CH_COPIES * 16;          // [client] {trap_ok, ft0, ft1, -}
-constexpr uint32_t F_RRID = F_FCB + FX_C * 16;                     // [range][8 copies]
+constexpr uint32_t F_DLUT = 0;                                     // [3 epoch bands][1024 classes] uint2
+constexpr uint32_t F_SLUT = F_DLUT + 3 * 1024 * 8;
+constexpr uint32_t F_ROWS = F_SLUT + 128;
+constexpr uint32_t F_CROW = F_ROWS + FX_R * 16;                    // [(client, engine)][8 copies] uint4
+constexpr uint32_t F_TRAP = F_CROW + FX_C * 4 * CH_COPIES * 16;    // [client] applied trap
+constexpr uint32_t F_RRID = F_TRAP + 4 * FX_C;                     // [range][8 copies]
 constexpr uint32_t F_EXT = F_RRID + 4 * FX_R * RID_COPIES;
 constexpr uint32_t F_NR0 = F_EXT + 4 * FX_R;
 constexpr uint32_t F_SLOWQ = F_NR0 + 4 * FX_R;
@@ -135,11 +136,17 @@ __device__ __forceinline__ D decode(const uint8_t* sm, const uint8_t* __restrict
   return d;
 }
 
-// pass-1 record: lo = scenario [4:0] | dedup group [7:5] | mechanism class [9:8] | location
-// [11:10] (LOC_*) | channel engine [13:12] | client [19:14] | range index, or page bits 32.. of a
-// wild page, [30:20] | known duplicate [31];  hi = page-state slot (in range / guard) or page
-// bits 0..31
-constexpr uint32_t R_KDUP = 1u << 31;
+// pass-1 record: lo = scenario [4:0] | location [7:5] (L_*) | known duplicate [8] | non-replayable
+// [9] | dedup group [12:10] | channel engine [14:13] | client [20:15] | range index, or page bits
+// 32.. of a wild page, [31:21];  hi = page-state slot (in range / guard) or page bits 0..31.
+// lo[9:0] is the entry's class: pass 2 indexes its decision LUT with it directly.
+constexpr uint32_t L_SKIP = 0, L_INM = 1, L_INX = 2, L_GRD = 3, L_NONE = 4;   // in a managed / external range
+constexpr uint32_t R_KDUP = 1u << 8;
+__device__ __forceinline__ uint32_t rec_client(uint32_t lo) { return (lo >> 15) & 63u; }
+__device__ __forceinline__ uint32_t rec_ceng(uint32_t lo) { return (lo >> 13) & 3u; }
+__device__ __forceinline__ uint32_t rec_group(uint32_t lo) { return (lo >> 10) & 7u; }
+__device__ __forceinline__ uint32_t rec_loc(uint32_t lo) { return (lo >> 5) & 7u; }
+__device__ __forceinline__ uint32_t rec_k(uint32_t lo) { return lo >> 21; }
 
 // entries per lane per step of pass 1 (4 measured: k_scan 1.27 -> 1.87-2.24 ms at config 3 for
 // 512-1024-thread CTAs -- register spills / fewer warps; profiles/r02/ab_entries_per_lane.txt)
@@ -250,15 +257,15 @@ __device__ __forceinline__ void scan_body(const World& W, const Scratch& S, uint
     const bool dd = (f & LF_DD) != 0;
     o.qn = elig & !inw;
     o.qd = dd & !inw;
-    const uint32_t loc = f ? (d.inr ? LOC_IN : (d.grd ? LOC_GUARD : LOC_NONE)) : LOC_SKIP;
+    const uint32_t loc = f ? (d.inr ? m : (d.grd ? L_GRD : L_NONE)) : L_SKIP;   // in range: m is 1 or 2
     const uint32_t pagehi = (e.y >> 12) & 0x7FFu;
-    o.lo = (f & 0xFFu) | ((f >> (LF_M_SH - 8)) & 0x300u) | (loc << 10) | ((d.cw >> 4) & 0x3000u) | ((c & 63u) << 14) |
-           ((inw ? d.k : pagehi) << 20);
+    o.lo = (f & 31u) | (loc << 5) | ((f & LF_REPL) ? 0u : 0x200u) | ((f & 0xE0u) << 5) | ((d.cw >> 3) & 0x6000u) |
+           ((c & 63u) << 15) | ((inw ? d.k : pagehi) << 21);
     o.hi = inw ? d.slot : d.page;
     o.page = (uint64_t)d.page | ((uint64_t)pagehi << 32);
   };
   auto key_of = [&](const O& o) {     // the entry's dedup key
-    return dedup_key((o.lo >> 14) & 63u, (int)((o.lo >> 12) & 3u), (int)(o.lo & 31u), o.page);
+    return dedup_key(rec_client(o.lo), (int)rec_ceng(o.lo), (int)(o.lo & 31u), o.page);
   };
   // wild-page hash operations: appended to the warp's queue by the lanes that have them (a
   // shared counter, no ballot), executed 32 at a time by the whole warp
@@ -315,7 +322,7 @@ __device__ __forceinline__ void scan_body(const World& W, const Scratch& S, uint
     if (any_q) {
 #pragma unroll
       for (int u = 0; u < EPL; ++u) {
-        if (o[u].qn) push(nr_key((o[u].lo >> 14) & 63u, 0, o[u].page), o[u].ok, 1);
+        if (o[u].qn) push(nr_key(rec_client(o[u].lo), 0, o[u].page), o[u].ok, 1);
         if (o[u].qd) push(key_of(o[u]), o[u].vd >> 3, 0);
       }
     }
@@ -380,12 +387,14 @@ __global__ void __launch_bounds__(BLOCK, 1) k_scan_fx(World W, Scratch S, const 
 }
 
 // ---- pass 2 ----------------------------------------------------------------------------------
-// Per entry: the OutRecord from the record, the client's decision row and at most two loads (its
-// dedup slot, its first-isolation word).  The common path has no data-dependent branch: every
-// candidate value is computed and selected (a rare path inside a warp's 64 entries would make
-// the whole warp execute it).  Entries that need a wild-page hash lookup (no range and no guard
-// page, or a claimed page slot held by another dedup group) are queued per warp and resolved 32
-// at a time; their mask bits are OR-ed into the chunk masks afterwards.
+// Per entry: the OutRecord from the record's class, its client row and at most two L2 loads (its
+// dedup slot, its first-isolation word).  Every decision that depends only on the class (scenario,
+// location, known-duplicate bit -- lo[9:0]) and the entry's epoch band is evaluated once per CTA
+// into a decision LUT (dlut_word), so the per-entry path is two shared loads (client row, LUT
+// word), the predicated L2 / shared loads the word asks for, and a handful of compares and ORs,
+// with no data-dependent branch.  Entries that need a wild-page hash lookup (no range and no
+// guard page, or a claimed page slot held by another dedup group) are queued per warp and
+// resolved 32 at a time; their mask bits are OR-ed into the chunk masks afterwards.
 constexpr uint32_t SQ_CAP = 96;   // per-warp slow queue: < 32 kept + 64 per chunk
 
 // decision word per scenario id (slot 31: skipped entry)
@@ -402,16 +411,61 @@ __device__ __forceinline__ uint32_t slut2_word(uint32_t sid, bool isolation) {
          ((f & LF_REPL) ? 0u : S2_NONREPL);
 }
 
-// per-client decision rows: A (every entry) = {epoch-1 threshold, kill tie, flags (bit0: benign
-// always cancelled, bit1: same on a CE channel, bit2: epoch-1 keys are pass 1's)}; B (trap and
-// fatal-report entries only) = {applied trap, applied fatal report on GR / SA, ... on CE}
-__device__ __forceinline__ void fc_rows(const FinClient& f, uint4& a, uint4& b) {
-  // epoch 1 iff rel < ok32 (ok32 < 2^32 - 1):  ok32 >= rel + 1, with rel = REL_PRE -> 0, REL_NONE -> ~0
+// Decision LUT of pass 2: [epoch band E][class X] -> {w0 flags, w1 = scenario | static verdict << 8
+// (0xFFFF00FF for a skipped entry: scenario 0xFF, client 0xFFFF)}.  E = 0: the entry precedes its
+// client's release (epoch 0); 1: epoch 1; 2: epoch 1 with pass 1's first-record keys (a client
+// released before the drain in a world with per-page keys).  The bits restate rules C2-C7
+// for one class:
+//   LDD_A / LDD_B  load the dedup slot (B: only if the client's benign-cancel threshold is a tie)
+//   LD_NR, NR1     load the first-isolation word of the page (nr1: epoch-1 keys, else nrall)
+//   SM_EXT/SM_NR0  read the range's first external-isolation / guard-page key from shared memory
+//   SLOW_A/SLOW_B  wild page: resolved by the slow path (B: only with a tie threshold)
+//   MH / MM        mechanism when the loaded key is / is not the entry's own (0: not isolating)
+//   CGE / CNE      cancel compare: representative >= threshold (benign), != applied record
+constexpr uint32_t D_LDD_A = 1u, D_LDD_B = 2u, D_LD_NR = 4u, D_NR1 = 8u, D_SM_EXT = 16u, D_SM_NR0 = 32u,
+                   D_SLOW_A = 64u, D_SLOW_B = 128u, D_DD = 256u, D_INR = 512u, D_MH_SH = 10, D_MM_SH = 12,
+                   D_CGE = 1u << 14, D_CNE = 1u << 15, D_CTRAP = 1u << 16;
+constexpr uint32_t NCLASS = 1024, DBAND = NCLASS * 8;   // bytes per epoch band
+
+__device__ __forceinline__ uint2 dlut_word(uint32_t X, uint32_t E, bool isolation) {
+  const uint32_t sid = X & 31u, loc = (X >> 5) & 7u;
+  const bool kd = (X >> 8) & 1u;
+  const uint32_t sw = (loc == L_SKIP || loc > L_NONE) ? 0u : slut2_word(sid, isolation);
+  if (!sw) return make_uint2(0u, 0xFFFF00FFu);
+  const bool inr = loc == L_INM || loc == L_INX, grd = loc == L_GRD, wild = loc == L_NONE, inw = inr || grd;
+  const bool ep1 = E >= 1, e1 = E == 1;
+  const bool dd = sw & S2_DD, elig = sw & S2_ELIG, serv = sw & S2_SERV, fatal = sw & S2_FATAL, trap = sw & S2_TRAP;
+  // the representative is needed unless the entry is a known duplicate whose verdict ignores it
+  const bool want_a = dd && !(kd && (elig || serv));
+  const bool want_b = dd && kd && serv;
+  const bool needs_nr = elig && !kd && (!inr || ep1);
+  const bool pe = elig && !kd && inr && !ep1 && loc == L_INX;
+  const bool ld_nr = needs_nr && (e1 ? inw : inr);
+  const bool smv = pe || (needs_nr && grd && !e1);
+  const uint32_t mh = elig ? (needs_nr ? 1u : (pe ? 3u : 2u)) : 0u, mm = elig ? 2u : 0u;
+  const uint32_t w0 = (want_a && inw ? D_LDD_A : 0u) | (want_b && inw ? D_LDD_B : 0u) | (ld_nr ? D_LD_NR : 0u) |
+                      (e1 ? D_NR1 : 0u) | (smv ? (pe ? D_SM_EXT : D_SM_NR0) : 0u) |
+                      (wild && (want_a || needs_nr) ? D_SLOW_A : 0u) | (wild && want_b ? D_SLOW_B : 0u) |
+                      (dd ? D_DD : 0u) | (inr ? D_INR : 0u) | (mh << D_MH_SH) | (mm << D_MM_SH) |
+                      (serv ? D_CGE : 0u) | (trap || fatal ? D_CNE : 0u) | (trap ? D_CTRAP : 0u);
+  return make_uint2(w0, sid | ((sw & 0x7Fu) << 8));
+}
+
+// Client row per (client, channel engine): {epoch-1 threshold, benign-cancel threshold, applied
+// fatal report of the channel's TSG class, byte offset of the client's epoch-1 LUT band}.
+//   epoch 1 iff ok32 >= thr (rel = REL_PRE -> 0, REL_NONE -> ~0; ok32 < 2^32 - 1)
+//   a benign completion is cancelled iff its representative's ok32 >= T: T = 0 when the client's
+//   benign completions are always cancelled on this channel class, ~0 when never (no tie), else
+//   tie + 1 (rules C5/C6); a fatal report iff its representative's ok32 != the applied one (C4)
+__device__ __forceinline__ uint4 client_row(const FinClient& f, uint32_t ceng) {
+  const bool ce = ceng == 1;
+  uint4 a;
   a.x = f.rel < 0 ? 0u : (f.rel >= (long long)0xFFFFFFFEll ? 0xFFFFFFFFu : (uint32_t)f.rel + 1u);
-  a.y = f.tie;
-  a.z = (f.bflags & 3u) | (f.pre_nrall ? 4u : 0u);
-  a.w = 0;
-  b = make_uint4(f.trap_ok, f.ft0, f.ft1, 0u);
+  const bool always = (f.bflags >> (ce ? 1 : 0)) & 1u;
+  a.y = always ? 0u : (f.tie == EMPTY32 ? 0xFFFFFFFFu : f.tie + 1u);
+  a.z = ce ? f.ft1 : f.ft0;
+  a.w = (f.pre_nrall ? 2u : 1u) * DBAND;
+  return a;
 }
 
 __device__ __forceinline__ uint4 lds128_if(bool p, const void* a) {   // predicated shared load (zeros if !p)
@@ -429,12 +483,15 @@ __device__ __forceinline__ uint32_t lds32_if(bool p, const void* a, uint32_t dfl
   return v;
 }
 
+template <bool kSparse>
 __global__ void __launch_bounds__(BLOCK, 1) k_finalize_fx(World W, Scratch S, uint64_t n, Params P,
                                                           mpsf_out_record* __restrict__ out, uint64_t q_base) {
   extern __shared__ __align__(128) uint8_t sm[];
   pdl_trigger();
   const uint32_t tid = threadIdx.x, nb = blockDim.x;
   const bool isolation = P.flags & MPSF_PF_ISOLATION;
+  uint2* dl = reinterpret_cast<uint2*>(sm + F_DLUT);
+  for (uint32_t i = tid; i < 3 * NCLASS; i += nb) dl[i] = dlut_word(i % NCLASS, i / NCLASS, isolation);
   uint32_t* slut2 = reinterpret_cast<uint32_t*>(sm + F_SLUT);
   if (tid < 32) slut2[tid] = tid == 31 ? 0u : slut2_word(tid, isolation);
   uint4* rows_w = reinterpret_cast<uint4*>(sm + F_ROWS);
@@ -446,14 +503,18 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize_fx(World W, Scratch S, ui
   }
   pdl_wait();
   if (__ldcg(S.ctrl + C_ERR) != 0) return;
-  uint4* fca = reinterpret_cast<uint4*>(sm + F_FCA);
-  uint4* fcb = reinterpret_cast<uint4*>(sm + F_FCB);
-  for (uint32_t k = tid; k < FX_C * CH_COPIES; k += nb) {
-    const uint32_t c = k / CH_COPIES;
-    uint4 a = make_uint4(0xFFFFFFFFu, EMPTY32, 0u, 0u), b = make_uint4(EMPTY32, EMPTY32, EMPTY32, 0u);
-    if (c < W.n_clients) fc_rows(fin_client(S.cstate[c], *S.glob, S.nrall != nullptr), a, b);
-    fca[k] = a;
-    if (k % CH_COPIES == 0) fcb[c] = b;
+  uint4* crow = reinterpret_cast<uint4*>(sm + F_CROW);
+  uint32_t* trp = reinterpret_cast<uint32_t*>(sm + F_TRAP);
+  for (uint32_t k = tid; k < FX_C * 4 * CH_COPIES; k += nb) {
+    const uint32_t ci = k / CH_COPIES, c = ci >> 2;
+    uint4 a = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, EMPTY32, DBAND);
+    if (c < W.n_clients) {
+      const FinClient f = fin_client(S.cstate[c], *S.glob, S.nrall != nullptr);
+      a = client_row(f, ci & 3u);
+      // an applied trap, as the ok32 of a (non-replayable) trap record
+      if (k % (4 * CH_COPIES) == 0) trp[c] = f.trap_ok == EMPTY32 ? EMPTY32 : (f.trap_ok | 0x80000000u);
+    }
+    crow[k] = a;
   }
   uint32_t* ext = reinterpret_cast<uint32_t*>(sm + F_EXT);
   uint32_t* nr0 = reinterpret_cast<uint32_t*>(sm + F_NR0);
@@ -465,37 +526,35 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize_fx(World W, Scratch S, ui
   const uint4* rows = reinterpret_cast<const uint4*>(sm + F_ROWS);
   const uint32_t lane = tid & 31, warp = tid >> 5;
   const uint32_t copy16 = (lane & (CH_COPIES - 1)) * 16, copy4 = (lane & (RID_COPIES - 1)) * 4;
-  const uint8_t* fca_l = sm + F_FCA + copy16;        // this lane's replica: + c * 128
-  const uint8_t* rrid_l = sm + F_RRID + copy4;       // + k * 32
+  const uint8_t* crow_l = sm + F_CROW + copy16;       // this lane's replica: + (client, engine) * 128
+  const uint8_t* rrid_l = sm + F_RRID + copy4;        // + k * 32
   const uint32_t base = (uint32_t)P.base_index;
-  const uint32_t G = W.dd_groups, gmask = W.dd_groups == 1 ? 0u : 7u;
   uint4* sq = reinterpret_cast<uint4*>(sm + F_SLOWQ) + warp * SQ_CAP;   // {lo, hi, batch index, dd word}
   uint32_t sqn = 0;
 
   // the general resolution of one queued entry (hash lookups allowed), by one lane
   auto slow_one = [&](uint4 q) {
     const uint32_t lo = q.x, hi = q.y, i = q.z, wd = q.w, gidx = base + i;
-    const uint32_t sid = lo & 31u, c = (lo >> 14) & 63u, ceng = (lo >> 12) & 3u, k = (lo >> 20) & 0x7FFu;
-    const uint32_t loc = (lo >> 10) & 3u, grp = (lo >> 5) & 7u, m = (lo >> 8) & 3u;
-    const bool inr = loc == LOC_IN, inw = inr || loc == LOC_GUARD;
+    const uint32_t sid = lo & 31u, c = rec_client(lo), ceng = rec_ceng(lo), k = rec_k(lo), loc = rec_loc(lo);
+    const bool inr = loc == L_INM || loc == L_INX, inw = inr || loc == L_GRD;
     const uint32_t sw = slut2[sid];
-    const uint4 fa = fca[c * CH_COPIES], fb = fcb[c];
+    const uint4 r = crow[((lo >> 13) & 0xFFu) * CH_COPIES];
     const uint32_t ok = gidx | (sw & S2_NONREPL);
-    const bool ep1 = ok >= fa.x, elig = sw & S2_ELIG, dd = sw & S2_DD;
+    const bool ep1 = ok >= r.x, pre = r.w == 2 * DBAND;
+    const bool elig = sw & S2_ELIG, dd = sw & S2_DD;
     const uint64_t page = inw ? (uint64_t)(rows[k].x + (hi - rows[k].z)) : ((uint64_t)hi | ((uint64_t)k << 32));
     unsigned long long key = dd ? dedup_key(c, (int)ceng, (int)sid, page) : 0ull;
     uint32_t ri = ok;
-    if (dd) ri = (inw && wd != EMPTY32 && (wd & 7u) == grp) ? (wd >> 3) : hash_get(S.hdd, key);
+    if (dd) ri = (inw && wd != EMPTY32 && (wd & 7u) == rec_group(lo)) ? (wd >> 3) : hash_get(S.hdd, key);
     const bool dup = dd && ri != gidx;
     const uint32_t rep_ok = dd ? ri : ok;
-    const bool ce = ceng == 1;
     bool canc = false;
-    if (sw & S2_TRAP) canc = gidx != fb.x;
-    else if (sw & S2_SERV) canc = ((fa.z >> (ce ? 1 : 0)) & 1u) || rep_ok > fa.y;
-    else if (sw & S2_FATAL) canc = rep_ok != (ce ? fb.z : fb.y);
+    if (sw & S2_TRAP) canc = ok != trp[c];
+    else if (sw & S2_SERV) canc = rep_ok >= r.y;
+    else if (sw & S2_FATAL) canc = rep_ok != r.z;
     uint32_t mech = 0;
     if (elig && !dup) {
-      const bool e1 = ep1 && !(fa.z & 4u);
+      const bool e1 = ep1 && !pre;
       if (!inr || ep1) {
         uint32_t nr;
         if (!inw) nr = hash_get(S.hnr, nr_key(c, e1 ? 1 : 0, page));
@@ -503,7 +562,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize_fx(World W, Scratch S, ui
         else nr = inr ? __ldcg(S.nrall + hi) : nr0[k];
         mech = nr == ok ? 1u : 2u;
       } else {
-        mech = (m == 2 && ext[k] == ok) ? 3u : 2u;
+        mech = (loc == L_INX && ext[k] == ok) ? 3u : 2u;
       }
     }
     const uint32_t verdict = (sw & 0x7Fu) | (mech << 2) | (canc ? 0x10u : 0u) | (dup ? 0x20u : 0u);
@@ -528,83 +587,58 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize_fx(World W, Scratch S, ui
     __syncwarp();
   };
 
-  // the common path of one entry: load addresses first (addr), outcome after the loads (fin)
+  // one entry: the class word and the loads (a), the outcome after the loads (b)
   struct A {
-    uint32_t lo, hi, sw, ok, k;
-    uint32_t flags;        // bit0 rep_free, bit2 needs_nr, bit3 pe, bit4 slow
-    uint4 fa;              // the client's decision row A
-    const uint32_t *pd, *pn;
-    bool p_dd, p_nr;
-    uint32_t smv;
+    uint32_t lo, hi, w0, w1, ok, T, ft, wd, wn;
+    bool pdd;
   };
-  auto addr = [&](uint32_t lo, uint32_t hi, uint32_t gidx, A& a) {
+  auto fin_a = [&](uint32_t lo, uint32_t hi, uint32_t gidx, A& a) {
     a.lo = lo; a.hi = hi;
-    const uint32_t loc = (lo >> 10) & 3u, sid = lo & 31u;
-    a.sw = slut2[loc ? sid : 31u];
-    const uint32_t sw = a.sw, c = (lo >> 14) & 63u;
-    a.k = (lo >> 20) & 0x7FFu;
-    a.fa = *reinterpret_cast<const uint4*>(fca_l + c * (CH_COPIES * 16));
-    const uint4 f0 = a.fa;
-    a.ok = gidx | (sw & S2_NONREPL);
-    const bool ep1 = a.ok >= f0.x;
-    const bool inr = loc == LOC_IN, grd = loc == LOC_GUARD, inw = inr | grd, wild = loc == LOC_NONE;
-    const bool kd = (lo & R_KDUP) != 0;
-    const bool elig = (sw & S2_ELIG) != 0, dd = (sw & S2_DD) != 0, serv = (sw & S2_SERV) != 0;
-    const bool rep_free = kd & (elig | (serv & (f0.y == EMPTY32)));
-    const bool want_rep = dd & !rep_free;
-    const bool needs_nr = elig & !kd & (!inr | ep1);
-    const bool e1 = ep1 & !(f0.z & 4u);
-    const bool pe = elig & !kd & inr & !ep1 & (((lo >> 8) & 3u) == 2u);
-    const bool slow = wild & (want_rep | needs_nr);
-    a.p_dd = want_rep & inw;
-    a.pd = S.dd + (hi * G + (((lo >> 5) & 7u) & gmask));
-    a.p_nr = needs_nr & (e1 ? inw : inr);
-    a.pn = (e1 ? S.nr1 : S.nrall) + hi;
-    a.smv = lds32_if(pe | (needs_nr & grd & !e1), (pe ? ext : nr0) + a.k, EMPTY32);
-    a.flags = (rep_free ? 1u : 0u) | (needs_nr ? 4u : 0u) | (pe ? 8u : 0u) | (slow ? 16u : 0u);
+    a.ok = gidx | ((lo << 22) & 0x80000000u);
+    const uint4 r = *reinterpret_cast<const uint4*>(crow_l + ((lo >> 13) & 0xFFu) * (CH_COPIES * 16));
+    const uint2 w = *reinterpret_cast<const uint2*>(sm + F_DLUT + (a.ok >= r.x ? r.w : 0u) + (lo & 0x3FFu) * 8);
+    a.w0 = w.x; a.w1 = w.y; a.T = r.y; a.ft = r.z;
+    const bool tie = (r.y - 1u) < 0xFFFFFFFEu;
+    a.pdd = ((w.x & D_LDD_A) != 0) | (((w.x & D_LDD_B) != 0) & tie);
+    const uint32_t* pd = S.dd + (kSparse ? hi : hi * 5u + rec_group(lo));
+    const uint32_t* pn = ((w.x & D_NR1) ? S.nr1 : S.nrall) + hi;
+    const uint32_t smv = lds32_if(w.x & (D_SM_EXT | D_SM_NR0), sm + ((w.x & D_SM_EXT) ? F_EXT : F_NR0) + 4 * rec_k(lo),
+                                  EMPTY32);
+    a.wd = ldcg_if(a.pdd, pd, 0u);
+    a.wn = ldcg_if(w.x & D_LD_NR, pn, smv);
   };
-  auto fin = [&](A& a, uint32_t wd, uint32_t wn, uint32_t gidx, unsigned long long& o8, bool& canc, bool& rep,
-                 unsigned long long& key) {
-    const uint32_t lo = a.lo, hi = a.hi, sw = a.sw, k = a.k;
-    const uint32_t sid = lo & 31u, c = (lo >> 14) & 63u, ceng = (lo >> 12) & 3u, loc = (lo >> 10) & 3u;
-    const bool dd = (sw & S2_DD) != 0, elig = (sw & S2_ELIG) != 0;
-    const bool rep_free = a.flags & 1u, needs_nr = a.flags & 4u, pe = a.flags & 8u;
-    // a claimed page slot held by another dedup group: the key is in the hash (slow path)
-    if (a.p_dd && (wd == EMPTY32 || (wd & 7u) != ((lo >> 5) & 7u))) a.flags |= 16u;
-    const uint32_t ri = wd >> 3;
-    const bool dup = dd & (rep_free | (ri != gidx));
-    const uint32_t rep_ok = (dd & !rep_free) ? ri : a.ok;
-    const uint32_t ce = ceng == 1 ? 1u : 0u;
-    const uint4 fb = lds128_if((sw & (S2_TRAP | S2_FATAL)) != 0, fcb + c);   // trap / fatal entries only
-    const bool c_trap = gidx != fb.x;
-    const bool c_serv = ((a.fa.z >> ce) & 1u) | (rep_ok > a.fa.y);
-    const bool c_fat = rep_ok != (ce ? fb.z : fb.y);
-    canc = ((sw & S2_TRAP) && c_trap) | ((sw & S2_SERV) && c_serv) | ((sw & S2_FATAL) && c_fat);
-    const bool hit = wn == a.ok;
-    const uint32_t mech = (elig & !dup) ? (needs_nr ? (hit ? 1u : 2u) : ((pe & hit) ? 3u : 2u)) : 0u;
-    const uint32_t verdict = (sw & 0x7Fu) | (mech << 2) | (canc ? 0x10u : 0u) | (dup ? 0x20u : 0u);
-    const uint32_t rid = loc == LOC_IN ? *reinterpret_cast<const uint32_t*>(rrid_l + k * (RID_COPIES * 4)) : NO_RID;
-    o8 = sw ? ((unsigned long long)rid | ((unsigned long long)sid << 32) | ((unsigned long long)verdict << 40) |
-               ((unsigned long long)c << 48))
-            : (0xFFFF000000000000ull | (0xFFull << 32) | NO_RID);
-    rep = dd & !dup;
-    const uint4 row = lds128_if(rep, rows + k);                          // representatives only
-    key = dedup_key(c, (int)ceng, (int)sid, (uint64_t)(row.x + (hi - row.z)));
-    if (a.flags & 16u) { canc = false; rep = false; }        // resolved by the slow path
+  auto fin_b = [&](const A& a, uint32_t gidx, unsigned long long& o8, bool& canc, bool& rep, bool& slow,
+                   unsigned long long& key) {
+    const uint32_t lo = a.lo, w0 = a.w0;
+    const bool tie = (a.T - 1u) < 0xFFFFFFFEu;
+    slow = ((w0 & D_SLOW_A) != 0) | (((w0 & D_SLOW_B) != 0) & tie) |
+           (kSparse & a.pdd & ((a.wd == EMPTY32) | (((a.wd ^ (lo >> 10)) & 7u) != 0)));
+    const uint32_t ri = a.wd >> 3;
+    const bool dup = ((w0 & D_DD) != 0) & (ri != gidx);   // an unloaded slot reads 0: a known duplicate (gidx > 0)
+    const uint32_t rep_ok = a.pdd ? ri : a.ok;
+    const uint32_t ref = lds32_if(w0 & D_CTRAP, trp + rec_client(lo), a.ft);
+    canc = (((w0 & D_CGE) != 0) & (rep_ok >= a.T)) | (((w0 & D_CNE) != 0) & (rep_ok != ref));
+    const uint32_t mech = dup ? 0u : (a.wn == a.ok ? (w0 & 0xC00u) : ((w0 >> 2) & 0xC00u));
+    const uint32_t h32 = a.w1 | ((lo & 0x1F8000u) << 1) | mech | (canc ? 0x1000u : 0u) | (dup ? 0x2000u : 0u);
+    const uint32_t rid = lds32_if(w0 & D_INR, rrid_l + rec_k(lo) * (RID_COPIES * 4), NO_RID);
+    o8 = (unsigned long long)rid | ((unsigned long long)h32 << 32);
+    rep = ((w0 & D_DD) != 0) & !dup & !slow;
+    canc = canc & !slow;
+    const uint4 row = lds128_if(rep, rows + rec_k(lo));                  // representatives only
+    key = (unsigned long long)(row.x + (a.hi - row.z)) |
+          ((unsigned long long)(((lo & 0x1FE000u) << 1) | ((lo & 31u) << 9)) << 32);
   };
 
   const unsigned long long* rec = S.drec + (P.base_index - S.drec_base);
   const uint32_t below = (1u << lane) - 1u;
   rec_stream(rec, n, [&](ulonglong2 r, uint32_t i0, bool ok0, bool ok1) {
     A a0, a1;
-    addr(ok0 ? (uint32_t)r.x : 0u, (uint32_t)(r.x >> 32), base + i0, a0);
-    addr(ok1 ? (uint32_t)r.y : 0u, (uint32_t)(r.y >> 32), base + i0 + 1, a1);
-    const uint32_t wd0 = ldcg_if(a0.p_dd, a0.pd, EMPTY32), wn0 = ldcg_if(a0.p_nr, a0.pn, a0.smv);
-    const uint32_t wd1 = ldcg_if(a1.p_dd, a1.pd, EMPTY32), wn1 = ldcg_if(a1.p_nr, a1.pn, a1.smv);
+    fin_a(ok0 ? (uint32_t)r.x : 0u, (uint32_t)(r.x >> 32), base + i0, a0);
+    fin_a(ok1 ? (uint32_t)r.y : 0u, (uint32_t)(r.y >> 32), base + i0 + 1, a1);
     unsigned long long o0, o1, k0, k1;
-    bool c0, c1, p0, p1;
-    fin(a0, wd0, wn0, base + i0, o0, c0, p0, k0);
-    fin(a1, wd1, wn1, base + i0 + 1, o1, c1, p1, k1);
+    bool c0, c1, p0, p1, s0, s1;
+    fin_b(a0, base + i0, o0, c0, p0, s0, k0);
+    fin_b(a1, base + i0 + 1, o1, c1, p1, s1, k1);
     unsigned long long* o = reinterpret_cast<unsigned long long*>(out) + i0;
     if (ok1 && (((uintptr_t)o & 15u) == 0)) __stcs(reinterpret_cast<ulonglong2*>(o), make_ulonglong2(o0, o1));
     else {
@@ -622,12 +656,13 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize_fx(World W, Scratch S, ui
       if (nc | nd) atomicAdd(S.segcnt + qq / SEG_CHUNKS, (unsigned long long)nc | ((unsigned long long)nd << 32));
     }
     // entries needing a hash lookup: queued, resolved 32 at a time (after this chunk's mask store)
-    const bool s0 = ok0 && (a0.flags & 16u), s1 = ok1 && (a1.flags & 16u);
+    s0 = ok0 && s0;
+    s1 = ok1 && s1;
     const uint32_t b0 = __ballot_sync(0xFFFFFFFFu, s0), b1 = __ballot_sync(0xFFFFFFFFu, s1);
     if (b0 | b1) {
-      if (s0) sq[sqn + __popc(b0 & below)] = make_uint4(a0.lo, a0.hi, i0, wd0);
+      if (s0) sq[sqn + __popc(b0 & below)] = make_uint4(a0.lo, a0.hi, i0, a0.pdd ? a0.wd : EMPTY32);
       sqn += __popc(b0);
-      if (s1) sq[sqn + __popc(b1 & below)] = make_uint4(a1.lo, a1.hi, i0 + 1, wd1);
+      if (s1) sq[sqn + __popc(b1 & below)] = make_uint4(a1.lo, a1.hi, i0 + 1, a1.pdd ? a1.wd : EMPTY32);
       sqn += __popc(b1);
       while (sqn >= 32) slow_drain(32);
     }
