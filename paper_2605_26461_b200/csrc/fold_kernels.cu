@@ -7,34 +7,52 @@
 //
 // Batch form: S snapshots in consume order as SoA (request id or NO_REQ, delta lengths,
 // progress, done) plus the concatenated deltas.  The fold is a stable group-by with
-// variable-length payloads:
-//   k_fold_stats   per request id: first / last snapshot (atomicMin/Max), sticky done (atomicOr)
-//   head scan      heads (a request's first snapshot) counted in consume order, fed by an
-//                  iterator: ranks the requests in first-appearance order
-//   k_fold_rank    per head: rank, order, last progress, done, request count
-//   src scan       (blocks | tokens << 32) in consume order: each snapshot's source offsets
-//   sort           snapshot indices by request rank, stable (CUB onesweep radix sort over
-//                  only the bits min(R, S) needs; liveness-only snapshots sort last)
-//   dst scan       packed lengths in sorted order, scattered back to consume order through a
-//                  permutation output iterator: each snapshot's destination offsets
-//   k_fold_copy    thread per snapshot in consume order (coalesced reads of the SoA, the
-//                  offsets and the payload): its deltas to their destination; heads write
-//                  their request's CSR start, the last live snapshot in fold order the ends
-// CUB supplies the scans and the radix sort (library primitives, like cuBLAS for a GEMM).
-#include <cub/cub.cuh>
+// variable-length payloads.  Every primitive is written here (no library sort or scan); tiles
+// are 8192 snapshots:
+//   k_fold_init     clear the per-request tables and the head bitmap
+//   k_fold_stats    consume order: per request id first / last snapshot and sticky done
+//                   (fire-and-forget reductions); the block scan of the packed delta lengths
+//                   gives each snapshot's source offset inside the tile (meta, with its lengths)
+//                   and the tile total
+//   k_fold_bits     a request's first snapshot sets its bit in an S-bit head bitmap
+//   k_fold_bitcnt   per 8192-bit chunk of the bitmap: word prefixes inside the chunk, chunk total
+//   k_fold_scan     one CTA per small array (chunk totals, tile totals): exclusive prefix
+//   k_fold_rank     per request: rank = heads before its first snapshot (first-appearance
+//                   order); order / last progress / done at the rank
+//   radix sort      snapshot indices by request rank, stable LSD over the bits min(R, S) needs
+//                   (<= 9 bits per pass): k_sort_hist (per-tile digit counts) -> k_sort_hscan
+//                   (per-digit prefix over tiles) -> k_sort_scatter (per-warp digit counters,
+//                   ballot-matched ranks inside a round of 32, rounds in index order: stable;
+//                   the tile is staged in shared memory in digit order and written out as
+//                   coalesced runs); the last pass moves each snapshot's meta into fold order
+//                   with the tile base added (smeta = source offset + lengths)
+//   k_fold_dsum     fold order: tile totals of the live lengths (k_fold_scan: prefix)
+//   k_fold_place    fold order: the block scan of the lengths is each snapshot's destination
+//                   offset; heads write the CSR start of their request, the last live snapshot
+//                   the CSR end; the deltas move from source to destination (a thread's
+//                   destinations are one contiguous run)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <algorithm>
-#include <thrust/iterator/counting_iterator.h>
-#include <thrust/iterator/permutation_iterator.h>
-#include <thrust/iterator/transform_iterator.h>
 
 #include "mpsf_kernels.h"
 
 namespace mpsf {
 
 constexpr uint32_t NO_REQ = 0xFFFFFFFFu;
+constexpr uint32_t FTILE = 8192;              // snapshots per tile (every tiled kernel)
+constexpr int SB = 512;                       // sort blocks: 16 warps x 512 consecutive snapshots
+constexpr int SIPT = FTILE / SB;
+constexpr int SWARPS = SB / 32;
+constexpr uint32_t WITEMS = FTILE / SWARPS;
+constexpr int CB = 1024;                      // consume / sorted-order tile blocks: 8 per thread
+constexpr int CIPT = FTILE / CB;
+constexpr int CWARPS = CB / 32;
+constexpr int DB_MAX = 9;                     // radix bits per pass
+constexpr uint32_t NB_MAX = 1u << DB_MAX;     // digits per pass (<= SB: one per thread)
+static_assert(NB_MAX <= (uint32_t)SB, "one digit per thread");
+constexpr uint32_t CHUNK_WORDS = 256;         // head-bitmap chunk (8192 bits)
 
 struct FoldDev {            // device-side totals, read back once
   unsigned long long n_requests, n_blocks, n_tokens;
@@ -46,156 +64,464 @@ __device__ __forceinline__ unsigned long long pack_len(uint32_t nb, uint32_t nt)
   return (unsigned long long)nb | ((unsigned long long)nt << 32);
 }
 
-// The gather kernels (rank, keys) and the stats take FI snapshots per thread (block-strided, so every load stays
-// coalesced) and issue all of their loads before the dependent gathers / atomics: one
-// snapshot per thread left them latency-bound at 10-20 % issue activity.
-constexpr int FI = 4;
-__device__ __forceinline__ uint32_t fi_index(int u) { return blockIdx.x * (blockDim.x * FI) + u * blockDim.x + threadIdx.x; }
-
-__global__ void k_fold_stats(uint32_t S, uint32_t R, const uint32_t* __restrict__ req,
-                             const uint8_t* __restrict__ done, uint32_t* __restrict__ first,
-                             uint32_t* __restrict__ last, uint32_t* __restrict__ rdone, FoldDev* __restrict__ dev) {
-  uint32_t r[FI];
-  uint8_t dn[FI];
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+  const uint32_t lane = threadIdx.x & 31;
 #pragma unroll
-  for (int u = 0; u < FI; ++u) {
-    const uint32_t i = fi_index(u);
-    r[u] = i < S ? req[i] : NO_REQ;
-    dn[u] = i < S ? done[i] : 0;
+  for (int o = 1; o < 32; o <<= 1) {
+    const T u = __shfl_up_sync(0xFFFFFFFFu, v, o);
+    if (lane >= (uint32_t)o) v += u;
+  }
+  return v;
+}
+
+// Exclusive scan of one value per thread over the block (blockDim.x = 32 * NW); sw holds NW + 1.
+template <typename T, int NW>
+__device__ __forceinline__ T block_excl_scan(T v, T* sw, T& total) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const T inc = warp_incl_scan(v);
+  if (lane == 31) sw[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const T w = lane < (uint32_t)NW ? sw[lane] : T(0);
+    const T wi = warp_incl_scan(w);
+    if (lane < (uint32_t)NW) sw[lane] = wi - w;
+    if (lane == NW - 1) sw[NW] = wi;
+  }
+  __syncthreads();
+  const T ex = sw[warp] + inc - v;
+  total = sw[NW];
+  __syncthreads();   // sw reusable
+  return ex;
+}
+
+__global__ void k_fold_init(uint32_t R, uint32_t W, uint32_t* __restrict__ first, uint32_t* __restrict__ last,
+                            uint32_t* __restrict__ rdone, uint32_t* __restrict__ bitmap, FoldDev* __restrict__ dev) {
+  const uint32_t n = R > W ? R : W;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (i < R) {
+      first[i] = NO_REQ;
+      last[i] = 0;
+      rdone[i] = 0;
+    }
+    if (i < W) bitmap[i] = 0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *dev = FoldDev{0, 0, 0, NO_REQ, 0};
+}
+
+// Blocked loads of N consecutive u32 (vectorised when the run is whole and 16-byte aligned).
+template <int N>
+__device__ __forceinline__ void ldb(const uint32_t* __restrict__ a, uint32_t i0, uint32_t S, uint32_t (&v)[N],
+                                    uint32_t dflt) {
+  if (i0 + N <= S && ((reinterpret_cast<uintptr_t>(a + i0) & 15u) == 0)) {
+    const uint4* p = reinterpret_cast<const uint4*>(a + i0);
+#pragma unroll
+    for (int q = 0; q < N / 4; ++q) {
+      const uint4 x = __ldg(p + q);
+      v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < N; ++u) v[u] = i0 + u < S ? __ldg(a + i0 + u) : dflt;
+  }
+}
+
+// Consume-order tile, thread t owns [tile * FTILE + 8 t, + 8).
+__global__ void __launch_bounds__(CB) k_fold_stats(uint32_t S, uint32_t R, const uint32_t* __restrict__ req,
+                                                   const uint8_t* __restrict__ done, const uint32_t* __restrict__ nblk,
+                                                   const uint32_t* __restrict__ ntok, uint32_t* __restrict__ first,
+                                                   uint32_t* __restrict__ last, uint32_t* __restrict__ rdone,
+                                                   uint4* __restrict__ meta, unsigned long long* __restrict__ tsum,
+                                                   FoldDev* __restrict__ dev) {
+  __shared__ unsigned long long sw[CWARPS + 1];
+  const uint32_t i0 = blockIdx.x * FTILE + threadIdx.x * CIPT;
+  uint32_t r[CIPT], nb[CIPT], nt[CIPT];
+  ldb(req, i0, S, r, NO_REQ);
+  ldb(nblk, i0, S, nb, 0u);
+  ldb(ntok, i0, S, nt, 0u);
+  unsigned long long s = 0;
+#pragma unroll
+  for (int u = 0; u < CIPT; ++u) s += pack_len(nb[u], nt[u]);
+  unsigned long long total;
+  unsigned long long run = block_excl_scan<unsigned long long, CWARPS>(s, sw, total);
+  if (threadIdx.x == 0) tsum[blockIdx.x] = total;
+  // each snapshot's source offset inside the tile and its lengths (the tile base is added when
+  // the sort's last pass moves the word into fold order)
+#pragma unroll
+  for (int u = 0; u < CIPT; ++u) {
+    if (i0 + u < S) __stcg(meta + i0 + u, make_uint4((uint32_t)run, (uint32_t)(run >> 32), nb[u], nt[u]));
+    run += pack_len(nb[u], nt[u]);
+  }
+  uint2 dn = make_uint2(0, 0);
+  if (i0 + CIPT <= S && ((reinterpret_cast<uintptr_t>(done + i0) & 7u) == 0)) {
+    dn = __ldg(reinterpret_cast<const uint2*>(done + i0));
+  } else {
+    for (int u = 0; u < CIPT && i0 + u < S; ++u) (u < 4 ? dn.x : dn.y) |= (uint32_t)__ldg(done + i0 + u) << (8 * (u & 3));
   }
 #pragma unroll
-  for (int u = 0; u < FI; ++u) {
-    const uint32_t i = fi_index(u);
-    if (r[u] == NO_REQ) continue;
-    if (r[u] >= R) {   // request id outside the caller's id space: reported, not folded
+  for (int u = 0; u < CIPT; ++u) {
+    const uint32_t i = i0 + u, rr = r[u];
+    if (i >= S || rr == NO_REQ) continue;
+    if (rr >= R) {   // request id outside the caller's id space: reported, not folded
       atomicMin(&dev->err, i);
       continue;
     }
-    atomicMin(first + r[u], i);
-    atomicMax(last + r[u], i);
-    if (dn[u]) atomicOr(rdone + r[u], 1u);
+    atomicMin(first + rr, i);
+    atomicMax(last + rr, i);
+    if (((u < 4 ? dn.x : dn.y) >> (8 * (u & 3))) & 0xFFu) atomicOr(rdone + rr, 1u);
   }
 }
 
-struct HeadFlag {           // snapshot i is its request's first
-  const uint32_t* req;
-  const uint32_t* first;
-  uint32_t R;
-  __device__ uint32_t operator()(uint32_t i) const {
-    const uint32_t r = req[i];
-    return (r < R && first[r] == i) ? 1u : 0u;
+__global__ void k_fold_bits(uint32_t R, const uint32_t* __restrict__ first, uint32_t* __restrict__ bitmap) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
+    const uint32_t f = first[r];
+    if (f != NO_REQ) atomicOr(bitmap + (f >> 5), 1u << (f & 31));
   }
-};
+}
 
-struct PackLen {            // packed lengths of snapshot i, consume order (every snapshot)
-  const uint32_t* nblk;
-  const uint32_t* ntok;
-  __device__ unsigned long long operator()(uint32_t i) const { return pack_len(nblk[i], ntok[i]); }
-};
+// one block of 256 threads per bitmap chunk: heads before each word inside the chunk, the total
+__global__ void __launch_bounds__(CHUNK_WORDS) k_fold_bitcnt(uint32_t W, const uint32_t* __restrict__ bitmap,
+                                                             uint32_t* __restrict__ wloc,
+                                                             unsigned long long* __restrict__ ccount) {
+  __shared__ uint32_t sw[CHUNK_WORDS / 32 + 1];
+  const uint32_t w = blockIdx.x * CHUNK_WORDS + threadIdx.x;
+  const uint32_t c = w < W ? __popc(bitmap[w]) : 0u;
+  uint32_t tot;
+  const uint32_t ex = block_excl_scan<uint32_t, CHUNK_WORDS / 32>(c, sw, tot);
+  if (w < W) wloc[w] = ex;
+  if (threadIdx.x == 0) ccount[blockIdx.x] = tot;
+}
 
-struct PackLenSorted {      // packed lengths at sorted position p (liveness-only snapshots: 0)
-  const uint32_t* sidx;
-  const uint32_t* skey;
-  const uint32_t* nblk;
-  const uint32_t* ntok;
-  uint32_t live_bound;
-  __device__ unsigned long long operator()(uint32_t p) const {
-    if (skey[p] >= live_bound) return 0ull;
-    const uint32_t i = sidx[p];
-    return pack_len(nblk[i], ntok[i]);
+// One CTA of 1024 threads per small array (<= a few thousand entries): exclusive prefix, total.
+__device__ __forceinline__ void scan_small(const unsigned long long* __restrict__ in, unsigned long long* __restrict__ out,
+                                           uint32_t n, unsigned long long* total_out) {
+  __shared__ unsigned long long sw[33];
+  constexpr int K = 4;   // loads issued together
+  const uint32_t per = (n + 1023) / 1024, b = threadIdx.x * per, e = min(b + per, n);
+  unsigned long long s = 0;
+  for (uint32_t i = b; i < e; i += K) {
+    unsigned long long x[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) x[q] = i + q < e ? in[i + q] : 0ull;
+#pragma unroll
+    for (int q = 0; q < K; ++q) s += x[q];
   }
-};
+  unsigned long long total;
+  unsigned long long run = block_excl_scan<unsigned long long, 32>(s, sw, total);
+  for (uint32_t i = b; i < e; ++i) {
+    const unsigned long long v = in[i];
+    out[i] = run;
+    run += v;
+  }
+  if (threadIdx.x == 0 && total_out) *total_out = total;
+}
 
-// heads: rank, the request's order entry, its last progress and sticky done; the count
-__global__ void k_fold_rank(uint32_t S, uint32_t R, const uint32_t* __restrict__ req,
-                            const uint32_t* __restrict__ first, const uint32_t* __restrict__ last,
-                            const uint32_t* __restrict__ rdone, const uint32_t* __restrict__ progress,
-                            const uint32_t* __restrict__ head_pos, uint32_t* __restrict__ rank,
+// block j scans array j of up to two
+__global__ void __launch_bounds__(1024) k_fold_scan(const unsigned long long* __restrict__ a, unsigned long long* __restrict__ ao,
+                                                    uint32_t na, unsigned long long* a_total,
+                                                    const unsigned long long* __restrict__ b, unsigned long long* __restrict__ bo,
+                                                    uint32_t nb) {
+  if (blockIdx.x == 0) scan_small(a, ao, na, a_total);
+  else scan_small(b, bo, nb, nullptr);
+}
+
+__global__ void k_fold_rank(uint32_t R, const uint32_t* __restrict__ first, const uint32_t* __restrict__ last,
+                            const uint32_t* __restrict__ rdone, const uint32_t* __restrict__ bitmap,
+                            const uint32_t* __restrict__ wloc, const unsigned long long* __restrict__ cpre,
+                            const uint32_t* __restrict__ progress, uint32_t* __restrict__ rank,
                             uint32_t* __restrict__ order, uint32_t* __restrict__ prog_out,
-                            uint8_t* __restrict__ done_out, FoldDev* __restrict__ dev) {
-  uint32_t r[FI], f[FI];
+                            uint8_t* __restrict__ done_out) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
+    const uint32_t f = first[r];
+    if (f == NO_REQ) continue;
+    const uint32_t w = f >> 5;
+    const uint32_t k = (uint32_t)cpre[w / CHUNK_WORDS] + wloc[w] + __popc(bitmap[w] & ((1u << (f & 31)) - 1u));
+    rank[r] = k;
+    order[k] = r;
+    prog_out[k] = progress[last[r]];
+    done_out[k] = rdone[r] ? 1 : 0;
+  }
+}
+
+// ---- stable LSD radix sort of snapshot indices by request rank -------------------------------
+// Pass 0 reads the request ids and ranks them on the fly (key = rank, or live_bound for
+// liveness-only / rejected snapshots, which sort last); its values are the snapshot indices.
+__device__ __forceinline__ uint32_t key_of(uint32_t r, uint32_t R, uint32_t live_bound, const uint32_t* rank) {
+  return r < R ? __ldg(rank + r) : live_bound;
+}
+
+template <bool kFirst>
+__global__ void __launch_bounds__(SB) k_sort_hist(uint32_t S, uint32_t R, uint32_t live_bound,
+                                                  const uint32_t* __restrict__ kin, const uint32_t* __restrict__ rank,
+                                                  uint32_t shift, uint32_t nbk, uint32_t T, uint32_t* __restrict__ hist) {
+  __shared__ uint32_t cnt[NB_MAX];
+  for (uint32_t d = threadIdx.x; d < nbk; d += SB) cnt[d] = 0;
+  __syncthreads();
+  uint32_t k[SIPT];
 #pragma unroll
-  for (int u = 0; u < FI; ++u) {
-    const uint32_t i = fi_index(u);
-    r[u] = i < S ? req[i] : NO_REQ;
+  for (int u = 0; u < SIPT; ++u) {
+    const uint32_t i = blockIdx.x * FTILE + u * SB + threadIdx.x;
+    k[u] = i < S ? __ldg(kin + i) : NO_REQ;
   }
 #pragma unroll
-  for (int u = 0; u < FI; ++u) f[u] = r[u] < R ? first[r[u]] : NO_REQ;
-#pragma unroll
-  for (int u = 0; u < FI; ++u) {
-    const uint32_t i = fi_index(u);
+  for (int u = 0; u < SIPT; ++u) {
+    const uint32_t i = blockIdx.x * FTILE + u * SB + threadIdx.x;
     if (i >= S) break;
-    const bool head = r[u] < R && f[u] == i;
-    if (head) {
-      const uint32_t k = head_pos[i];
-      rank[r[u]] = k;
-      order[k] = r[u];
-      prog_out[k] = progress[last[r[u]]];
-      done_out[k] = rdone[r[u]] ? 1 : 0;
-    }
-    if (i == S - 1) dev->n_requests = head_pos[i] + (head ? 1u : 0u);
+    const uint32_t key = kFirst ? key_of(k[u], R, live_bound, rank) : k[u];
+    atomicAdd(cnt + ((key >> shift) & (nbk - 1)), 1u);
   }
+  __syncthreads();
+  for (uint32_t d = threadIdx.x; d < nbk; d += SB) hist[d * T + blockIdx.x] = cnt[d];
 }
 
-// sort keys: the request's rank; liveness-only (and rejected) snapshots key past every rank
-__global__ void k_fold_keys(uint32_t S, uint32_t R, uint32_t live_bound, const uint32_t* __restrict__ req,
-                            const uint32_t* __restrict__ rank, uint32_t* __restrict__ key,
-                            uint32_t* __restrict__ idx) {
-  uint32_t r[FI], k[FI];
-#pragma unroll
-  for (int u = 0; u < FI; ++u) {
-    const uint32_t i = fi_index(u);
-    r[u] = i < S ? req[i] : NO_REQ;
+// one block per digit: exclusive prefix of its row over the tiles, and the row total
+__global__ void __launch_bounds__(256) k_sort_hscan(uint32_t T, uint32_t* __restrict__ hist,
+                                                    uint32_t* __restrict__ rowtot) {
+  __shared__ uint32_t sw[9];
+  uint32_t* row = hist + (size_t)blockIdx.x * T;
+  uint32_t carry = 0;
+  for (uint32_t b = 0; b < T; b += 256) {
+    const uint32_t i = b + threadIdx.x;
+    const uint32_t v = i < T ? row[i] : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan<uint32_t, 8>(v, sw, tot);
+    if (i < T) row[i] = carry + ex;
+    carry += tot;
   }
+  if (threadIdx.x == 0) rowtot[blockIdx.x] = carry;
+}
+
+// lanes of the warp holding the same digit (ballots over its db bits), among the lanes in `valid`
+__device__ __forceinline__ uint32_t match_digit(uint32_t d, int db, uint32_t valid) {
+  uint32_t peers = valid;
+  for (int b = 0; b < db; ++b) {
+    const bool bit = (d >> b) & 1u;
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, bit);
+    peers &= bit ? m : ~m;
+  }
+  return peers;
+}
+
+// Dynamic shared memory of the scatter: per-warp digit counters / bases, the tile's digit
+// offsets and global bases, the tile staged in digit order.
+constexpr size_t SCATTER_SMEM = 4 * (SWARPS * NB_MAX + 2 * NB_MAX + 2 * FTILE + SWARPS + 1);
+
+template <bool kFirst, bool kLast>
+__global__ void __launch_bounds__(SB) k_sort_scatter(uint32_t S, uint32_t R, uint32_t live_bound,
+                                                     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                                     const uint32_t* __restrict__ rank, uint32_t shift, int db,
+                                                     uint32_t T, const uint32_t* __restrict__ hist,
+                                                     const uint32_t* __restrict__ rowtot, uint32_t* __restrict__ kout,
+                                                     uint32_t* __restrict__ vout, const uint4* __restrict__ meta,
+                                                     const unsigned long long* __restrict__ tbase,
+                                                     uint4* __restrict__ smeta) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  uint32_t* wc = sm;                              // [SWARPS][NB_MAX]
+  uint32_t* tdo = wc + SWARPS * NB_MAX;           // tile-local start of each digit
+  uint32_t* gb = tdo + NB_MAX;                    // global start of this tile's run of each digit
+  uint32_t* sk = gb + NB_MAX;                     // the tile in digit order
+  uint32_t* sv = sk + FTILE;
+  uint32_t* sw = sv + FTILE;                      // SWARPS + 1
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nbk = 1u << db;
+  const uint32_t t0 = blockIdx.x * FTILE, nt = min(FTILE, S - t0);
+  // global base per digit: digits before it (all tiles) + this digit in earlier tiles
+  uint32_t tot;
+  const uint32_t dex = block_excl_scan<uint32_t, SWARPS>(tid < nbk ? rowtot[tid] : 0u, sw, tot);
+  if (tid < nbk) gb[tid] = dex + hist[tid * T + blockIdx.x];
+  for (uint32_t x = tid; x < SWARPS * NB_MAX; x += SB) wc[x] = 0;
+  // the warp's WITEMS consecutive snapshots, round u = [.. + 32 u, + 32)
+  const uint32_t w0 = t0 + warp * WITEMS;
+  uint32_t k[SIPT], v[SIPT];
 #pragma unroll
-  for (int u = 0; u < FI; ++u) k[u] = r[u] < R ? rank[r[u]] : live_bound;
-#pragma unroll
-  for (int u = 0; u < FI; ++u) {
-    const uint32_t i = fi_index(u);
+  for (int u = 0; u < SIPT; ++u) {
+    const uint32_t i = w0 + u * 32 + lane;
     if (i < S) {
-      key[i] = k[u];
-      idx[i] = i;
+      k[u] = __ldg(kin + i);
+      v[u] = kFirst ? i : __ldg(vin + i);
+    } else {
+      k[u] = 0; v[u] = 0;
+    }
+  }
+  if (kFirst) {
+#pragma unroll
+    for (int u = 0; u < SIPT; ++u)
+      if (w0 + u * 32 + lane < S) k[u] = key_of(k[u], R, live_bound, rank);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < SIPT; ++u)
+    if (w0 + u * 32 + lane < S) atomicAdd(&wc[warp * NB_MAX + ((k[u] >> shift) & (nbk - 1))], 1u);
+  __syncthreads();
+  // tile-local layout: digits in order, inside a digit the warps in order
+  uint32_t tc = 0;
+  if (tid < nbk) {
+#pragma unroll
+    for (int w = 0; w < SWARPS; ++w) tc += wc[w * NB_MAX + tid];
+  }
+  const uint32_t toff = block_excl_scan<uint32_t, SWARPS>(tid < nbk ? tc : 0u, sw, tot);
+  if (tid < nbk) {
+    tdo[tid] = toff;
+    uint32_t run = toff;
+#pragma unroll
+    for (int w = 0; w < SWARPS; ++w) {
+      const uint32_t c = wc[w * NB_MAX + tid];
+      wc[w * NB_MAX + tid] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int u = 0; u < SIPT; ++u) {
+    const bool ok = w0 + u * 32 + lane < S;
+    const uint32_t valid = __ballot_sync(0xFFFFFFFFu, ok);
+    const uint32_t d = (k[u] >> shift) & (nbk - 1);
+    const uint32_t peers = match_digit(d, db, valid);
+    const uint32_t lr = __popc(peers & lt);
+    if (ok) {
+      const uint32_t pos = wc[warp * NB_MAX + d] + lr;
+      sk[pos] = k[u];
+      sv[pos] = v[u];
+    }
+    __syncwarp();
+    if (ok && lr == 0) wc[warp * NB_MAX + d] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // write-out in digit order: consecutive threads write consecutive positions of a digit's run
+#pragma unroll 4
+  for (uint32_t q = tid; q < nt; q += SB) {
+    const uint32_t key = sk[q], val = sv[q], d = (key >> shift) & (nbk - 1);
+    const uint32_t gpos = gb[d] + (q - tdo[d]);
+    kout[gpos] = key;
+    if (kLast) {
+      // into fold order: the snapshot's source offset (tile base + in-tile) and lengths
+      uint4 m = make_uint4(0, 0, 0, 0);
+      if (key < live_bound) {
+        m = __ldcg(meta + val);
+        const unsigned long long src = tbase[val / FTILE] + ((unsigned long long)m.x | ((unsigned long long)m.y << 32));
+        m.x = (uint32_t)src;
+        m.y = (uint32_t)(src >> 32);
+      }
+      smeta[gpos] = m;
+    } else {
+      vout[gpos] = val;
     }
   }
 }
 
-// thread per snapshot in consume order: coalesced reads of the SoA, offsets and payload
-__global__ void k_fold_copy(uint32_t S, uint32_t R, const uint32_t* __restrict__ req,
-                            const uint32_t* __restrict__ nblk, const uint32_t* __restrict__ ntok,
-                            const uint32_t* __restrict__ first, const uint32_t* __restrict__ last,
-                            const uint32_t* __restrict__ rank, const unsigned long long* __restrict__ src,
-                            const unsigned long long* __restrict__ dst, const uint32_t* __restrict__ blocks,
-                            const uint32_t* __restrict__ tokens, unsigned long long n_blocks_in,
-                            unsigned long long n_tokens_in, unsigned long long* __restrict__ blk_off,
-                            unsigned long long* __restrict__ tok_off, uint32_t* __restrict__ blocks_out,
-                            uint32_t* __restrict__ tokens_out, FoldDev* __restrict__ dev) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= S) return;
-  const uint32_t r = req[i];
-  if (r >= R) return;                        // liveness-only / rejected
-  const unsigned long long s = src[i], d = dst[i];
-  const uint32_t sb = (uint32_t)s, st = (uint32_t)(s >> 32), db = (uint32_t)d, dt = (uint32_t)(d >> 32);
-  const uint32_t nb = nblk[i], nt = ntok[i];
-  if ((unsigned long long)sb + nb > n_blocks_in || (unsigned long long)st + nt > n_tokens_in ||
-      (unsigned long long)db + nb > n_blocks_in || (unsigned long long)dt + nt > n_tokens_in) {
-    atomicOr(&dev->overrun, 1u);
-  } else {
-    for (uint32_t j = 0; j < nb; ++j) blocks_out[db + j] = blocks[sb + j];
-    for (uint32_t j = 0; j < nt; ++j) tokens_out[dt + j] = tokens[st + j];
+// sorted order: tile totals of the live lengths (smeta holds zero lengths for the others)
+__global__ void __launch_bounds__(CB) k_fold_dsum(uint32_t S, const uint4* __restrict__ smeta,
+                                                  unsigned long long* __restrict__ dsum) {
+  __shared__ unsigned long long sw[CWARPS + 1];
+  unsigned long long s = 0;
+#pragma unroll
+  for (int u = 0; u < CIPT; ++u) {
+    const uint32_t p = blockIdx.x * FTILE + u * CB + threadIdx.x;
+    if (p < S) {
+      const uint2 m = __ldcg(reinterpret_cast<const uint2*>(smeta + p) + 1);
+      s += pack_len(m.x, m.y);
+    }
   }
-  const bool head = first[r] == i, tail = last[r] == i;
-  if (head || tail) {
-    const uint32_t k = rank[r];
-    if (head) {                              // the request's CSR start
-      blk_off[k] = db;
-      tok_off[k] = dt;
+  unsigned long long tot;
+  block_excl_scan<unsigned long long, CWARPS>(s, sw, tot);
+  if (threadIdx.x == 0) dsum[blockIdx.x] = tot;
+}
+
+// Warp-cooperative copy of one payload stream: the warp's 256 snapshots (lane-major, 8 per lane)
+// have consecutive destinations, so the warp walks its destination range 32 words at a time
+// (one coalesced store per step); each word finds its snapshot by binary search over the staged
+// destination starts.  ds / sr: the warp's staged starts and sources (256 each).
+__device__ __forceinline__ void warp_copy(const uint32_t* __restrict__ in, unsigned long long n_in,
+                                          uint32_t* __restrict__ out, const uint32_t* ds, const uint32_t* sr,
+                                          uint32_t lo, uint32_t hi) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t o = lo + lane; o < hi; o += 32) {
+    uint32_t j = 0;
+#pragma unroll
+    for (uint32_t step = 128; step; step >>= 1)
+      if (ds[j + step] <= o) j += step;   // last snapshot starting at or before o
+    const unsigned long long src = (unsigned long long)sr[j] + (o - ds[j]);
+    if (src < n_in && o < n_in) out[o] = __ldg(in + src);
+  }
+}
+
+// Fold-order tile, thread t owns sorted positions [tile * FTILE + 8 t, + 8): the block scan of
+// the lengths is each snapshot's destination offset; heads write the CSR start of their request,
+// the last live snapshot the CSR end; the deltas move from their source offsets (smeta) with
+// the warp-cooperative copy (a snapshot's deltas reaching past the payload arrays set overrun).
+constexpr size_t PLACE_SMEM = (size_t)CWARPS * 2 * 256 * 4;
+
+__global__ void __launch_bounds__(CB) k_fold_place(uint32_t S, uint32_t live_bound, const uint32_t* __restrict__ skey,
+                                                   const uint4* __restrict__ smeta,
+                                                   const unsigned long long* __restrict__ dbase,
+                                                   const uint32_t* __restrict__ blocks, unsigned long long n_blocks_in,
+                                                   const uint32_t* __restrict__ tokens, unsigned long long n_tokens_in,
+                                                   unsigned long long* __restrict__ blk_off,
+                                                   unsigned long long* __restrict__ tok_off,
+                                                   uint32_t* __restrict__ blocks_out, uint32_t* __restrict__ tokens_out,
+                                                   FoldDev* __restrict__ dev) {
+  __shared__ unsigned long long sw[CWARPS + 1];
+  extern __shared__ __align__(16) uint32_t psm[];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* ds = psm + warp * 512;   // [256] destination starts, [256] sources
+  uint32_t* sr = ds + 256;
+  const uint32_t p0 = blockIdx.x * FTILE + threadIdx.x * CIPT;
+  uint32_t k[CIPT];
+  ldb(skey, p0, S, k, live_bound);
+  uint4 m[CIPT];
+#pragma unroll
+  for (int u = 0; u < CIPT; ++u) m[u] = p0 + u < S ? __ldg(smeta + p0 + u) : make_uint4(0, 0, 0, 0);
+  unsigned long long s = 0;
+#pragma unroll
+  for (int u = 0; u < CIPT; ++u) s += pack_len(m[u].z, m[u].w);
+  unsigned long long tot;
+  const unsigned long long d0 = dbase[blockIdx.x] + block_excl_scan<unsigned long long, CWARPS>(s, sw, tot);
+  unsigned long long d = d0;
+  uint32_t prev = p0 && p0 < S ? __ldg(skey + p0 - 1) : 0xFFFFFFFFu;
+  bool over = false;
+#pragma unroll
+  for (int u = 0; u < CIPT; ++u) {
+    const uint32_t p = p0 + u, key = k[u];
+    const unsigned long long len = pack_len(m[u].z, m[u].w);
+    if (p < S && key < live_bound) {
+      if (key != prev) {   // the request's first snapshot in fold order: its CSR start
+        blk_off[key] = (uint32_t)d;
+        tok_off[key] = (uint32_t)(d >> 32);
+      }
+      const uint32_t nxt = u + 1 < CIPT ? k[u + 1] : (p + 1 < S ? __ldg(skey + p + 1) : live_bound);
+      if (nxt >= live_bound) {   // the last live snapshot: the CSR ends
+        const unsigned long long e = d + len;
+        blk_off[key + 1] = (uint32_t)e;
+        tok_off[key + 1] = (uint32_t)(e >> 32);
+        dev->n_blocks = (uint32_t)e;
+        dev->n_tokens = (uint32_t)(e >> 32);
+      }
+      over |= (unsigned long long)m[u].x + m[u].z > n_blocks_in || (unsigned long long)m[u].y + m[u].w > n_tokens_in ||
+              (unsigned long long)(uint32_t)d + m[u].z > n_blocks_in ||
+              (unsigned long long)(uint32_t)(d >> 32) + m[u].w > n_tokens_in;
     }
-    if (tail && k + 1ull == dev->n_requests) {   // the last live snapshot in fold order: the CSR ends
-      blk_off[k + 1] = (unsigned long long)db + nb;
-      tok_off[k + 1] = (unsigned long long)dt + nt;
-      dev->n_blocks = (unsigned long long)db + nb;
-      dev->n_tokens = (unsigned long long)dt + nt;
+    prev = key;
+    d += len;
+  }
+  if (over) atomicOr(&dev->overrun, 1u);
+  // the warp's destination ranges: [lane 0's first start, lane 31's end) per stream
+  const unsigned long long wlo = __shfl_sync(0xFFFFFFFFu, d0, 0), whi = __shfl_sync(0xFFFFFFFFu, d, 31);
+  // tokens, then blocks (the staging buffers are reused)
+#pragma unroll
+  for (int stream = 0; stream < 2; ++stream) {
+    const int sh = stream == 0 ? 32 : 0;
+    unsigned long long dd = d0;
+#pragma unroll
+    for (int u = 0; u < CIPT; ++u) {
+      ds[lane * CIPT + u] = (uint32_t)(dd >> sh);
+      sr[lane * CIPT + u] = stream == 0 ? m[u].y : m[u].x;
+      dd += pack_len(m[u].z, m[u].w);
     }
+    __syncwarp();
+    if (stream == 0) warp_copy(tokens, n_tokens_in, tokens_out, ds, sr, (uint32_t)(wlo >> 32), (uint32_t)(whi >> 32));
+    else warp_copy(blocks, n_blocks_in, blocks_out, ds, sr, (uint32_t)wlo, (uint32_t)whi);
+    __syncwarp();
   }
 }
 
@@ -207,82 +533,107 @@ static int key_bits(uint32_t live_bound) {   // bits for keys in [0, live_bound]
   return b;
 }
 
+static uint32_t tiles(uint64_t S) { return (uint32_t)((S + FTILE - 1) / FTILE); }
+
 // scratch layout for S snapshots and R request ids
 size_t fold_scratch_bytes(uint64_t S, uint64_t R) {
-  size_t o = al256(sizeof(FoldDev)) + al256(4 * R) * 4;   // dev, first, last, rdone, rank
-  o += al256(4 * S) * 5;                                   // head_pos, key, idx, skey, sidx
-  o += al256(8 * S) * 2;                                   // src, dst
-  size_t cub_bytes = 0, t = 0;
-  thrust::counting_iterator<uint32_t> c0(0);
-  cub::DeviceScan::ExclusiveSum(nullptr, t, thrust::make_transform_iterator(c0, HeadFlag{}), (uint32_t*)nullptr,
-                                (int)S);
-  cub_bytes = t > cub_bytes ? t : cub_bytes;
-  cub::DeviceScan::ExclusiveSum(nullptr, t, thrust::make_transform_iterator(c0, PackLen{}),
-                                (unsigned long long*)nullptr, (int)S);
-  cub_bytes = t > cub_bytes ? t : cub_bytes;
-  cub::DeviceScan::ExclusiveSum(nullptr, t, thrust::make_transform_iterator(c0, PackLenSorted{}),
-                                thrust::make_permutation_iterator((unsigned long long*)nullptr, (const uint32_t*)nullptr),
-                                (int)S);
-  cub_bytes = t > cub_bytes ? t : cub_bytes;
-  cub::DeviceRadixSort::SortPairs(nullptr, t, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)S);
-  cub_bytes = t > cub_bytes ? t : cub_bytes;
-  return o + al256(cub_bytes) + 256;
+  const uint64_t T = tiles(S), W = S / 32 + 1, C = (W + CHUNK_WORDS - 1) / CHUNK_WORDS;
+  size_t o = al256(64) + al256(4 * R) * 4;                 // dev, first, last, rdone, rank
+  o += al256(4 * W) * 2 + al256(8 * C) * 2;                // bitmap, wloc, chunk counts / prefix
+  o += al256(8 * T) * 4;                                   // tsum, tbase, dsum, dbase
+  o += al256(4 * S) * 4;                                   // sort keys / values, two buffers
+  o += al256(16 * S) * 2;                                  // meta in consume order, in fold order
+  o += al256(4ull * NB_MAX * T) + al256(4 * NB_MAX);       // hist, rowtot
+  return o + 256;
+}
+
+static int sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
 }
 
 int launch_fold(uint8_t* scratch, size_t scratch_bytes, uint32_t S, uint32_t R, const uint32_t* req,
                 const uint32_t* nblk, const uint32_t* ntok, const uint32_t* progress, const uint8_t* done,
                 const uint32_t* blocks, uint64_t n_blocks_in, const uint32_t* tokens, uint64_t n_tokens_in,
                 uint32_t* order, uint64_t* blk_off, uint32_t* blocks_out, uint64_t* tok_off, uint32_t* tokens_out,
-                uint32_t* prog_out, uint8_t* done_out, FoldTotals* tot, cudaStream_t st) {
+                uint32_t* prog_out, uint8_t* done_out, FoldTotals* tot, cudaStream_t st, const Marker& mk) {
+  if (scratch_bytes < fold_scratch_bytes(S, R)) return -1;
+  const uint32_t T = tiles(S), W = S / 32 + 1, C = (W + CHUNK_WORDS - 1) / CHUNK_WORDS;
   uint8_t* p = scratch;
   auto take = [&](size_t bytes) { uint8_t* r = p; p += al256(bytes); return r; };
-  FoldDev* dev = reinterpret_cast<FoldDev*>(take(sizeof(FoldDev)));
-  uint32_t* first = reinterpret_cast<uint32_t*>(take(4ull * R));
-  uint32_t* last = reinterpret_cast<uint32_t*>(take(4ull * R));
-  uint32_t* rdone = reinterpret_cast<uint32_t*>(take(4ull * R));
-  uint32_t* rank = reinterpret_cast<uint32_t*>(take(4ull * R));
-  uint32_t* head_pos = reinterpret_cast<uint32_t*>(take(4ull * S));
-  uint32_t* key = reinterpret_cast<uint32_t*>(take(4ull * S));
-  uint32_t* idx = reinterpret_cast<uint32_t*>(take(4ull * S));
-  uint32_t* skey = reinterpret_cast<uint32_t*>(take(4ull * S));
-  uint32_t* sidx = reinterpret_cast<uint32_t*>(take(4ull * S));
-  unsigned long long* src = reinterpret_cast<unsigned long long*>(take(8ull * S));
-  unsigned long long* dst = reinterpret_cast<unsigned long long*>(take(8ull * S));
-  uint8_t* cub_tmp = p;
-  const size_t cub_bytes = scratch_bytes - (size_t)(p - scratch);
+  auto u32 = [&](size_t n) { return reinterpret_cast<uint32_t*>(take(4 * n)); };
+  auto u64 = [&](size_t n) { return reinterpret_cast<unsigned long long*>(take(8 * n)); };
+  FoldDev* dev = reinterpret_cast<FoldDev*>(take(64));
+  uint32_t *first = u32(R), *last = u32(R), *rdone = u32(R), *rank = u32(R);
+  uint32_t *bitmap = u32(W), *wloc = u32(W);
+  unsigned long long *ccount = u64(C), *cpre = u64(C);
+  unsigned long long *tsum = u64(T), *tbase = u64(T), *dsum = u64(T), *dbase = u64(T);
+  uint32_t *kA = u32(S), *vA = u32(S), *kB = u32(S), *vB = u32(S);
+  uint4* meta = reinterpret_cast<uint4*>(take(16ull * S));
+  uint4* smeta = reinterpret_cast<uint4*>(take(16ull * S));
+  uint32_t* hist = u32((size_t)NB_MAX * T);
+  uint32_t* rowtot = u32(NB_MAX);
   const uint32_t live_bound = R < S ? R : S;   // ranks < min(R, S)
-  const FoldDev init{0, 0, 0, NO_REQ, 0};
-  if (cudaMemcpyAsync(dev, &init, sizeof(init), cudaMemcpyHostToDevice, st) != cudaSuccess ||
-      cudaMemsetAsync(first, 0xFF, 4ull * R, st) != cudaSuccess ||
-      cudaMemsetAsync(last, 0, 4ull * R, st) != cudaSuccess || cudaMemsetAsync(rdone, 0, 4ull * R, st) != cudaSuccess)
+  const uint32_t gR = (uint32_t)std::min<uint64_t>((std::max(R, W) + 255) / 256, (uint64_t)sms() * 8);
+  int launches = 0;
+  auto done_launch = [&](const char* name) { mk.mark(name); ++launches; };
+
+  k_fold_init<<<gR, 256, 0, st>>>(R, W, first, last, rdone, bitmap, dev);
+  done_launch("k_fold_init");
+  k_fold_stats<<<T, CB, 0, st>>>(S, R, req, done, nblk, ntok, first, last, rdone, meta, tsum, dev);
+  done_launch("k_fold_stats");
+  k_fold_bits<<<gR, 256, 0, st>>>(R, first, bitmap);
+  done_launch("k_fold_bits");
+  k_fold_bitcnt<<<C, CHUNK_WORDS, 0, st>>>(W, bitmap, wloc, ccount);
+  done_launch("k_fold_bitcnt");
+  k_fold_scan<<<2, 1024, 0, st>>>(ccount, cpre, C, &dev->n_requests, tsum, tbase, T);
+  done_launch("k_fold_scan");
+  k_fold_rank<<<gR, 256, 0, st>>>(R, first, last, rdone, bitmap, wloc, cpre, progress, rank, order, prog_out, done_out);
+  done_launch("k_fold_rank");
+  // radix sort by rank: passes of <= DB_MAX bits over the bits live_bound needs
+  const int bits = key_bits(live_bound);
+  const int passes = (bits + DB_MAX - 1) / DB_MAX, db = (bits + passes - 1) / passes;
+  const uint32_t nbk = 1u << db;
+  const uint32_t* kin = req;
+  const uint32_t* vin = nullptr;
+  uint32_t* ko = kA;
+  uint32_t* vo = vA;
+  for (int ps = 0; ps < passes; ++ps) {
+    const uint32_t shift = (uint32_t)(ps * db);
+    const bool f = ps == 0, l = ps == passes - 1;
+    if (f) k_sort_hist<true><<<T, SB, 0, st>>>(S, R, live_bound, kin, rank, shift, nbk, T, hist);
+    else k_sort_hist<false><<<T, SB, 0, st>>>(S, R, live_bound, kin, rank, shift, nbk, T, hist);
+    done_launch("k_sort_hist");
+    k_sort_hscan<<<nbk, 256, 0, st>>>(T, hist, rowtot);
+    done_launch("k_sort_hscan");
+    auto* kern = f ? (l ? k_sort_scatter<true, true> : k_sort_scatter<true, false>)
+                   : (l ? k_sort_scatter<false, true> : k_sort_scatter<false, false>);
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SCATTER_SMEM) != cudaSuccess)
+      return -1;
+
+    kern<<<T, SB, SCATTER_SMEM, st>>>(S, R, live_bound, kin, vin, rank, shift, db, T, hist, rowtot, ko, vo, meta, tbase,
+                                      smeta);
+    done_launch("k_sort_scatter");
+    kin = ko;
+    vin = vo;
+    ko = ko == kA ? kB : kA;
+    vo = vo == vA ? vB : vA;
+  }
+  k_fold_dsum<<<T, CB, 0, st>>>(S, smeta, dsum);
+  done_launch("k_fold_dsum");
+  k_fold_scan<<<1, 1024, 0, st>>>(dsum, dbase, T, nullptr, nullptr, nullptr, 0);
+  done_launch("k_fold_scan");
+  if (cudaFuncSetAttribute(k_fold_place, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLACE_SMEM) != cudaSuccess)
     return -1;
-  const uint32_t b = 256, g = (S + b * FI - 1) / (b * FI);
-  k_fold_stats<<<g, b, 0, st>>>(S, R, req, done, first, last, rdone, dev);
-  thrust::counting_iterator<uint32_t> c0(0);
-  size_t t = cub_bytes;
-  if (cub::DeviceScan::ExclusiveSum(cub_tmp, t, thrust::make_transform_iterator(c0, HeadFlag{req, first, R}),
-                                    head_pos, (int)S, st) != cudaSuccess)
-    return -1;
-  k_fold_rank<<<g, b, 0, st>>>(S, R, req, first, last, rdone, progress, head_pos, rank, order, prog_out, done_out,
-                               dev);
-  k_fold_keys<<<g, b, 0, st>>>(S, R, live_bound, req, rank, key, idx);
-  t = cub_bytes;
-  if (cub::DeviceRadixSort::SortPairs(cub_tmp, t, key, skey, idx, sidx, (int)S, 0, key_bits(live_bound), st) !=
-      cudaSuccess)
-    return -1;
-  t = cub_bytes;
-  if (cub::DeviceScan::ExclusiveSum(cub_tmp, t, thrust::make_transform_iterator(c0, PackLen{nblk, ntok}), src,
-                                    (int)S, st) != cudaSuccess)
-    return -1;
-  t = cub_bytes;
-  if (cub::DeviceScan::ExclusiveSum(
-          cub_tmp, t, thrust::make_transform_iterator(c0, PackLenSorted{sidx, skey, nblk, ntok, live_bound}),
-          thrust::make_permutation_iterator(dst, sidx), (int)S, st) != cudaSuccess)
-    return -1;
-  k_fold_copy<<<(S + b - 1) / b, b, 0, st>>>(S, R, req, nblk, ntok, first, last, rank, src, dst, blocks, tokens, n_blocks_in,
-                               n_tokens_in, reinterpret_cast<unsigned long long*>(blk_off),
-                               reinterpret_cast<unsigned long long*>(tok_off), blocks_out, tokens_out, dev);
+  k_fold_place<<<T, CB, PLACE_SMEM, st>>>(S, live_bound, kin, smeta, dbase, blocks, n_blocks_in, tokens, n_tokens_in,
+                                 reinterpret_cast<unsigned long long*>(blk_off),
+                                 reinterpret_cast<unsigned long long*>(tok_off), blocks_out, tokens_out, dev);
+  done_launch("k_fold_place");
   FoldDev h{};
   if (cudaMemcpyAsync(&h, dev, sizeof(h), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
       cudaStreamSynchronize(st) != cudaSuccess)
@@ -299,6 +650,7 @@ int launch_fold(uint8_t* scratch, size_t scratch_bytes, uint32_t S, uint32_t R, 
   tot->n_tokens = h.n_tokens;
   tot->error_index = h.err == NO_REQ ? ~0ull : h.err;
   tot->overrun = h.overrun;
+  tot->launches = (uint32_t)launches;
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
@@ -306,7 +658,9 @@ int launch_fold(uint8_t* scratch, size_t scratch_bytes, uint32_t S, uint32_t R, 
 // complete_wake reserves every folded request's block ids in the standby's pool
 // (recovery.py:356-357); the pool's free list is then the unreserved ids, popped smallest
 // first.  Output: the reserved mask (the remap's valid mask over KV pages) and the free ids
-// ascending (the heap's pop order).  Ids >= total are not pool blocks: they mark nothing.
+// ascending (the heap's pop order): a stream compaction of the mask -- per-tile free counts,
+// their prefix (one CTA), then each tile writes its free ids at its base.  Ids >= total are not
+// pool blocks: they mark nothing.
 
 __global__ void k_kv_mark(const uint32_t* __restrict__ blocks, uint64_t nb, uint32_t total,
                           uint8_t* __restrict__ reserved) {
@@ -316,33 +670,65 @@ __global__ void k_kv_mark(const uint32_t* __restrict__ blocks, uint64_t nb, uint
   }
 }
 
-struct IsFree {
-  const uint8_t* reserved;
-  __device__ bool operator()(uint32_t b) const { return reserved[b] == 0; }
-};
+// thread t of tile b owns ids [b * FTILE + 8 t, + 8): its free mask as 8 bits
+__device__ __forceinline__ uint32_t free_bits(const uint8_t* __restrict__ reserved, uint32_t i0, uint32_t total) {
+  uint32_t m = 0;
+  if (i0 + CIPT <= total && ((reinterpret_cast<uintptr_t>(reserved + i0) & 7u) == 0)) {
+    const uint2 x = __ldg(reinterpret_cast<const uint2*>(reserved + i0));
+#pragma unroll
+    for (int b = 0; b < 8; ++b) m |= ((((b < 4 ? x.x : x.y) >> (8 * (b & 3))) & 0xFFu) == 0 ? 1u : 0u) << b;
+  } else {
+    for (uint32_t u = 0; u < CIPT && i0 + u < total; ++u) m |= (reserved[i0 + u] == 0 ? 1u : 0u) << u;
+  }
+  return m;
+}
+
+__global__ void __launch_bounds__(CB) k_kv_count(const uint8_t* __restrict__ reserved, uint32_t total,
+                                                 unsigned long long* __restrict__ tcnt) {
+  __shared__ unsigned long long sw[CWARPS + 1];
+  const uint32_t m = free_bits(reserved, blockIdx.x * FTILE + threadIdx.x * CIPT, total);
+  unsigned long long tot;
+  block_excl_scan<unsigned long long, CWARPS>((unsigned long long)__popc(m), sw, tot);
+  if (threadIdx.x == 0) tcnt[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(CB) k_kv_emit(const uint8_t* __restrict__ reserved, uint32_t total,
+                                                const unsigned long long* __restrict__ tbase,
+                                                uint32_t* __restrict__ free_ids) {
+  __shared__ unsigned long long sw[CWARPS + 1];
+  const uint32_t i0 = blockIdx.x * FTILE + threadIdx.x * CIPT;
+  uint32_t m = free_bits(reserved, i0, total);
+  unsigned long long tot;
+  unsigned long long o = tbase[blockIdx.x] + block_excl_scan<unsigned long long, CWARPS>((unsigned long long)__popc(m), sw, tot);
+  while (m) {
+    const int b = __ffs(m) - 1;
+    free_ids[o++] = i0 + b;
+    m &= m - 1;
+  }
+}
 
 size_t kv_reserve_scratch_bytes(uint32_t total) {
-  size_t t = 0;
-  thrust::counting_iterator<uint32_t> c0(0);
-  cub::DeviceSelect::If(nullptr, t, c0, (uint32_t*)nullptr, (unsigned long long*)nullptr, (int64_t)total, IsFree{});
-  return al256(8) + al256(t) + 256;
+  const uint64_t T = tiles(total);
+  return al256(8) + al256(8 * T) * 2 + 256;
 }
 
 int launch_kv_reserve(uint8_t* scratch, size_t scratch_bytes, uint32_t total, const uint32_t* blocks, uint64_t nb,
                       uint8_t* reserved, uint32_t* free_ids, uint64_t* n_free, cudaStream_t st) {
-  unsigned long long* d_nsel = reinterpret_cast<unsigned long long*>(scratch);
-  uint8_t* cub_tmp = scratch + al256(8);
-  size_t t = scratch_bytes - al256(8);
+  if (scratch_bytes < kv_reserve_scratch_bytes(total)) return -1;
+  const uint32_t T = tiles(total);
+  unsigned long long* d_nfree = reinterpret_cast<unsigned long long*>(scratch);
+  unsigned long long* tcnt = reinterpret_cast<unsigned long long*>(scratch + al256(8));
+  unsigned long long* tb = reinterpret_cast<unsigned long long*>(scratch + al256(8) + al256(8ull * T));
   if (cudaMemsetAsync(reserved, 0, total, st) != cudaSuccess) return -1;
   if (nb) {
-    const uint64_t g = std::min<uint64_t>((nb + 255) / 256, 148ull * 16);
+    const uint64_t g = std::min<uint64_t>((nb + 255) / 256, (uint64_t)sms() * 16);
     k_kv_mark<<<(uint32_t)g, 256, 0, st>>>(blocks, nb, total, reserved);
   }
-  thrust::counting_iterator<uint32_t> c0(0);
-  if (cub::DeviceSelect::If(cub_tmp, t, c0, free_ids, d_nsel, (int64_t)total, IsFree{reserved}, st) != cudaSuccess)
-    return -1;
+  k_kv_count<<<T, CB, 0, st>>>(reserved, total, tcnt);
+  k_fold_scan<<<1, 1024, 0, st>>>(tcnt, tb, T, d_nfree, nullptr, nullptr, 0);
+  k_kv_emit<<<T, CB, 0, st>>>(reserved, total, tb, free_ids);
   unsigned long long h = 0;
-  if (cudaMemcpyAsync(&h, d_nsel, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+  if (cudaMemcpyAsync(&h, d_nfree, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
       cudaStreamSynchronize(st) != cudaSuccess)
     return -1;
   *n_free = h;

@@ -1255,10 +1255,9 @@ int mpsf_fold(mpsf_ctx* c, uint64_t n_snap, uint32_t n_req_ids, const uint32_t* 
   c->mark_begin(st);
   if (launch_fold(c->d_fold, c->fold_cap, (uint32_t)n_snap, n_req_ids ? n_req_ids : 1, d_req, d_nblk, d_ntok,
                   d_progress, d_done, d_blocks, n_blocks, d_tokens, n_tokens, d_order, d_blk_off, d_blocks_out, d_tok_off, d_tokens_out,
-                  d_progress_out, d_done_out, &tot, st))
+                  d_progress_out, d_done_out, &tot, st, c->marker()))
     return MPSF_E_CUDA;
-  c->marker().mark("k_fold");
-  c->last_launches = 4;   // own kernels; the CUB scans and the radix sort add theirs
+  c->last_launches = (int)tot.launches;
   summary->n_requests = tot.n_requests;
   summary->n_blocks = tot.n_blocks;
   summary->n_tokens = tot.n_tokens;
@@ -1287,7 +1286,7 @@ int mpsf_kv_reserve(mpsf_ctx* c, uint32_t total_blocks, const uint32_t* d_block_
   if (launch_kv_reserve(c->d_fold, c->fold_cap, total_blocks, d_block_ids, n, d_reserved, d_free, n_free, st))
     return MPSF_E_CUDA;
   c->marker().mark("k_kv_reserve");
-  c->last_launches = n ? 1 : 0;   // own kernel; CUB's select adds its own
+  c->last_launches = n ? 4 : 3;
   return MPSF_OK;
 }
 

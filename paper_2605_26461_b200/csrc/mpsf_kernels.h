@@ -66,17 +66,19 @@ int launch_remap(uint64_t va_base, const uint64_t* phys, uint64_t npages4k, uint
 int launch_remap_blocks(uint64_t va_base, const uint64_t* phys, uint64_t npages4k,
                         const uint32_t* blocks, uint64_t nblocks, mpsf_remap_entry* out,
                         uint32_t* err_flag, cudaStream_t st);
-// snapshot delta fold (StandbyInstance.fold over a batch of snapshots); synchronous on st
+// snapshot delta fold (StandbyInstance.fold over a batch of snapshots); synchronous on st; every
+// primitive hand-written (fold_kernels.cu), each launch marked for the per-kernel profile
 struct FoldTotals {
   uint64_t n_requests, n_blocks, n_tokens, error_index;
   uint32_t overrun;   // the delta lengths reach past the payload arrays
+  uint32_t launches;  // kernels launched
 };
 size_t fold_scratch_bytes(uint64_t S, uint64_t R);
 int launch_fold(uint8_t* scratch, size_t scratch_bytes, uint32_t S, uint32_t R, const uint32_t* req,
                 const uint32_t* nblk, const uint32_t* ntok, const uint32_t* progress, const uint8_t* done,
                 const uint32_t* blocks, uint64_t n_blocks_in, const uint32_t* tokens, uint64_t n_tokens_in,
                 uint32_t* order, uint64_t* blk_off, uint32_t* blocks_out, uint64_t* tok_off, uint32_t* tokens_out,
-                uint32_t* prog_out, uint8_t* done_out, FoldTotals* tot, cudaStream_t st);
+                uint32_t* prog_out, uint8_t* done_out, FoldTotals* tot, cudaStream_t st, const Marker& mk);
 // KV pool restore (BlockPool.reserve of folded block ids): reserved mask + free ids ascending
 size_t kv_reserve_scratch_bytes(uint32_t total);
 int launch_kv_reserve(uint8_t* scratch, size_t scratch_bytes, uint32_t total, const uint32_t* blocks, uint64_t nb,
