@@ -1496,7 +1496,8 @@ static void set_attrs() {
   cudaFuncSetAttribute(k_general<kStaged, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(k_general<kStaged, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(k_finalize<kStaged>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-  cudaFuncSetAttribute(fx::k_scan_fx, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(fx::k_scan_fx<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(fx::k_scan_fx<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(fx::k_finalize_fx<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(fx::k_finalize_fx<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   done = true;
@@ -1536,8 +1537,9 @@ static int scan_t(const World& W, const Scratch& S, const mpsf_fault_entry* in, 
   set_attrs<kStaged>();
   if (n == 0) return 0;
   if (kStaged && fx_fits(W)) {
-    const int g = clamp_grid(grid_for(fx::k_scan_fx, fx::SCAN_BYTES), n);
-    launch_pdl(fx::k_scan_fx, dim3(g), dim3(BLOCK), fx::SCAN_BYTES, st, W, S, in, n, P, counts);
+    auto* k = W.dd_groups == 1 ? fx::k_scan_fx<true> : fx::k_scan_fx<false>;
+    const int g = clamp_grid(grid_for(k, fx::SCAN_BYTES), n);
+    launch_pdl(k, dim3(g), dim3(BLOCK), fx::SCAN_BYTES, st, W, S, in, n, P, counts);
     mk.mark("k_scan");
     return ok_or_err();
   }

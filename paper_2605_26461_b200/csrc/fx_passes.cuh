@@ -42,8 +42,7 @@ constexpr uint32_t O_ISO = a16(O_C64 + 8 * (3 * FX_C + 2));
 constexpr uint32_t O_R32 = O_ISO + 4 * 3 * FX_C * 32;
 constexpr uint32_t O_CNT = O_R32 + 4 * 2 * FX_R;
 constexpr uint32_t O_USED = O_CNT + 4 * NSCEN * FX_C;
-constexpr uint32_t O_QCNT = O_USED + 16;
-constexpr uint32_t SCAN_BYTES = O_QCNT + 4 * WARPS;
+constexpr uint32_t SCAN_BYTES = O_USED + 16;
 // pass 2 (its own layout: it needs neither the classification LUT nor the channel / skip tables)
 constexpr uint32_t RID_COPIES = 8;             // replicas of the rid table (one per quarter-warp lane)
 constexpr uint32_t F_DLUT = 0;                                     // [3 epoch bands][1024 classes] uint2
@@ -126,7 +125,9 @@ __device__ __forceinline__ D decode(const uint8_t* sm, const uint8_t* __restrict
   const bool tbad = (ek == 0) & (ea_bad | (eng != ceng) | (e.y >= (1u << 21)));
   const bool bad = !(cr.x & CH_VALID) | ((f & LF_BAD) != 0) | tbad;
   const bool valid = (w3 >> 24) & MPSF_ENTRY_VALID;
-  if (valid && bad) {                                             // malformed entry (never in a valid trace)
+  // malformed entry (never in a valid trace): a warp-uniform test keeps the common path free of
+  // a divergent branch
+  if (__any_sync(0xFFFFFFFFu, valid && bad) && valid && bad) {
     const uint32_t bit = !(cr.x & CH_VALID) ? EB_NO_CHANNEL
                          : (((f & LF_BAD) != 0) | ((ek == 0) & ea_bad)) ? EB_BAD_ENTRY
                          : (eng != ceng ? EB_MISMATCH : EB_VA);
@@ -193,14 +194,15 @@ __device__ __forceinline__ void q_exec(const Scratch& S, uint32_t* used, const Q
   }
 }
 
+template <bool kSparse>
 __device__ __forceinline__ void scan_body(const World& W, const Scratch& S, uint8_t* sm,
                                           const mpsf_fault_entry* __restrict__ in, uint64_t n, const Params& P) {
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t copy16 = (lane & (CH_COPIES - 1)) * 16;
   const uint32_t C = W.n_clients, nch = W.n_channels;
   const uint32_t base = (uint32_t)P.base_index;
-  const bool sparse = W.dd_groups == 1;
-  const uint32_t G = W.dd_groups, gmask = sparse ? 0u : 7u;
+  // claimed page slots (one per page, no first-eligible table) or dense (page, group) slots
+  constexpr uint32_t G = kSparse ? 1u : 5u, gmask = kSparse ? 0u : 7u;
   uint32_t* counts = reinterpret_cast<uint32_t*>(sm + O_CNT);
   // per-warp copies of the per-(mechanism class, client) minima, one row per warp: a warp's lanes
   // spread over the banks (a column-per-warp layout put every lane of a warp on one bank)
@@ -211,7 +213,7 @@ __device__ __forceinline__ void scan_body(const World& W, const Scratch& S, uint
   QOp* q = reinterpret_cast<QOp*>(sm + O_QUEUE) + warp * QCAP;
   unsigned long long* const drec = S.drec + (P.base_index - S.drec_base);
   const uint8_t* __restrict__ ps = W.page_state;
-  uint32_t* const nrall = S.nrall;
+  uint32_t* const nrall = S.nrall;   // present iff !kSparse
   struct O {
     uint32_t* pd; uint32_t vd;     // dedup slot and its value
     uint32_t* pa;                  // first eligible record of the page (dense worlds)
@@ -229,7 +231,7 @@ __device__ __forceinline__ void scan_body(const World& W, const Scratch& S, uint
     o.ok = ((f & LF_REPL) ? 0u : 0x80000000u) | gidx;
     const bool elig = (f & LF_ELIG) != 0;
     const bool inw = d.inr | d.grd;
-    o.p_a = elig & d.inr & (nrall != nullptr);
+    o.p_a = elig & d.inr & !kSparse;
     o.pa = nrall + d.slot;
     const bool dd = (f & LF_DD) != 0;
     const uint32_t group = (f >> LF_GROUP_SH) & 7u;
@@ -240,7 +242,7 @@ __device__ __forceinline__ void scan_body(const World& W, const Scratch& S, uint
   auto second = [&](uint4 e, uint32_t gidx, O& o, const D& d) {
     const uint32_t f = d.f, c = d.cw & 0xFFFFu, sid = f & LF_S;
     red_add_s(f != 0, counts + (f ? c * NSCEN + sid : 0u));
-    if (f & (LF_TRAP | LF_FATAL)) {                    // rare: traps and fatal reports
+    if (__any_sync(0xFFFFFFFFu, f & (LF_TRAP | LF_FATAL)) && (f & (LF_TRAP | LF_FATAL))) {   // rare: traps, fatal reports
       const bool sa = (d.cw >> 18) & 1u;
       const uint32_t ceng = (d.cw >> 16) & 3u;
       if (f & LF_TRAP) {
@@ -267,16 +269,25 @@ __device__ __forceinline__ void scan_body(const World& W, const Scratch& S, uint
   auto key_of = [&](const O& o) {     // the entry's dedup key
     return dedup_key(rec_client(o.lo), (int)rec_ceng(o.lo), (int)(o.lo & 31u), o.page);
   };
-  // wild-page hash operations: appended to the warp's queue by the lanes that have them (a
-  // shared counter, no ballot), executed 32 at a time by the whole warp
-  uint32_t* qc = reinterpret_cast<uint32_t*>(sm + O_QCNT) + warp;
-  if (lane == 0) *qc = 0;
-  __syncwarp();
-  auto push = [&](unsigned long long key, uint32_t val, uint32_t tab) {
-    QOp x; x.key = key; x.val = val; x.tab = tab;
-    const uint32_t pos = atomicAdd(qc, 1u);
-    if (pos < QCAP) q[pos] = x;
-    else q_exec(S, used, x);                      // queue full (a chunk of wild pages): now
+  // wild-page hash operations: appended to the warp's queue (ballot ranks; the warp-uniform count
+  // lives in a register), executed 32 at a time by the whole warp.  The count stays below 32
+  // before each append, so an append (<= 32 operations) never overflows QCAP = 64.
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t qn = 0;
+  auto push = [&](bool has, unsigned long long key, uint32_t val, uint32_t tab) {
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, has);
+    if (!m) return;
+    if (qn >= 32) {
+      __syncwarp();
+      q_exec(S, used, q[qn - 32 + lane]);
+      qn -= 32;
+      __syncwarp();
+    }
+    if (has) {
+      QOp x; x.key = key; x.val = val; x.tab = tab;
+      q[qn + __popc(m & lt)] = x;
+    }
+    qn += __popc(m);
   };
   stream_n<EPL>(in, n, [&](const uint4* e, uint32_t i0) {
     O o[EPL];
@@ -313,36 +324,30 @@ __device__ __forceinline__ void scan_body(const World& W, const Scratch& S, uint
     bool any_q = false;
 #pragma unroll
     for (int u = 0; u < EPL; ++u) {
-      min_g_if(o[u].p_a, ra[u], o[u].pa, o[u].ok);
+      if (!kSparse) min_g_if(o[u].p_a, ra[u], o[u].pa, o[u].ok);
       // dense slots: a predicated atomic MIN; claimed slots: claim (CAS), or MIN, or the hash
-      min_g_if(o[u].p_dd & !sparse & !kd[u], rd[u], o[u].pd, o[u].vd);
-      if (o[u].p_dd & sparse & !kd[u]) claim_resolve(S, used, o[u].pd, o[u].vd, rd[u], key_of(o[u]));
+      if (!kSparse) min_g_if(o[u].p_dd & !kd[u], rd[u], o[u].pd, o[u].vd);
+      if (kSparse && (o[u].p_dd & !kd[u])) claim_resolve(S, used, o[u].pd, o[u].vd, rd[u], key_of(o[u]));
       any_q |= o[u].qn | o[u].qd;
     }
-    if (any_q) {
+    if (__any_sync(0xFFFFFFFFu, any_q)) {
 #pragma unroll
       for (int u = 0; u < EPL; ++u) {
-        if (o[u].qn) push(nr_key(rec_client(o[u].lo), 0, o[u].page), o[u].ok, 1);
-        if (o[u].qd) push(key_of(o[u]), o[u].vd >> 3, 0);
+        push(o[u].qn, nr_key(rec_client(o[u].lo), 0, o[u].page), o[u].ok, 1);
+        push(o[u].qd, key_of(o[u]), o[u].vd >> 3, 0);
       }
-    }
-    __syncwarp();
-    uint32_t qn = min(*qc, (uint32_t)QCAP);
-    if (qn >= 32) {
-      do {
-        q_exec(S, used, q[qn - 32 + lane]);
-        qn -= 32;
-      } while (qn >= 32);
-      __syncwarp();
-      if (lane == 0) *qc = qn;
-      __syncwarp();
     }
   });
   __syncwarp();
-  const uint32_t qn = min(*qc, (uint32_t)QCAP);
+  if (qn >= 32) {
+    q_exec(S, used, q[qn - 32 + lane]);
+    qn -= 32;
+  }
+  __syncwarp();
   if (lane < qn) q_exec(S, used, q[lane]);
 }
 
+template <bool kSparse>
 __global__ void __launch_bounds__(BLOCK, 1) k_scan_fx(World W, Scratch S, const mpsf_fault_entry* __restrict__ in,
                                                       uint64_t n, Params P, unsigned long long* __restrict__ counts) {
   extern __shared__ __align__(128) uint8_t sm[];
@@ -361,7 +366,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_scan_fx(World W, Scratch S, const 
   if (tid < 2) used[tid] = 0;
   __syncthreads();
   pdl_wait();
-  scan_body(W, S, sm, in, n, P);
+  scan_body<kSparse>(W, S, sm, in, n, P);
   __syncthreads();
   for (uint32_t i = tid; i < NSCEN * C; i += nb)
     if (cnt[i]) atomicAdd(counts + i, (unsigned long long)cnt[i]);
