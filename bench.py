@@ -360,7 +360,8 @@ def run_mine(args):
         kb = kalg[dom][1]
         ktr = None
         if isinstance(traffic, dict):
-            ktr = traffic.get(f"{args.workload}_per_kernel", {}).get(f"{dom}<1>")
+            per_k = traffic.get(f"{args.workload}_per_kernel", {})
+            ktr = per_k.get(dom, per_k.get(f"{dom}<1>"))
         dom_roof = {"bound": "hbm", "achieved": kb / (kms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                     "frac": kb / (kms / 1e3) / 1e9 / hbm_peak, "traffic": ktr, "kernel": dom,
                     "alg_bytes_per_launch": kb, "alg_bytes_rule": kalg[dom][0], "launch_ms": kms,
@@ -591,6 +592,18 @@ def bench_storm(args, eng, hbm_peak, flush, ws=1, rank=0, local=0, threads=1):
     B = alg_bytes(N, nd, nc)
     ach = B / (ms / 1e3) / 1e9
     dup_ok = nd == u
+    # the dominant kernel (pass 1: 16 B per entry read) and the DRAM traffic ncu measured for this
+    # workload (profiles/ncu_traffic.json, c3 = the whole storm)
+    traffic = {}
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f)
+    ks = prof.get("k_scan", (1, ms))
+    k_ms = ks[1] / max(ks[0], 1)
+    scan_roof = {"kernel": "k_scan", "launch_ms": round(k_ms, 5), "alg_bytes_per_launch": 16 * N,
+                 "achieved": 16 * N / (k_ms / 1e3) / 1e9, "frac": 16 * N / (k_ms / 1e3) / 1e9 / hbm_peak,
+                 "traffic": traffic.get("c3_per_kernel", {}).get("k_scan") if ws == 1 else None}
     del d_in, full, bufs, res
     torch.cuda.empty_cache()
     return {"workload": f"c3: 48 clients x 32 ranges x 8192 pages, {N} replayable entries, {u} unique "
@@ -599,7 +612,10 @@ def bench_storm(args, eng, hbm_peak, flush, ws=1, rank=0, local=0, threads=1):
             "value": N / (ms / 1e3), "unit": "entries/s", "ms_per_step": ms, "steps": steps,
             "scaling": "strong" if ws > 1 else None,
             "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": ach / hbm_peak, "alg_bytes_per_step": B},
+                         "frac": ach / hbm_peak, "alg_bytes_per_step": B,
+                         "traffic": traffic.get("c3") if ws == 1 else None,
+                         "traffic_what": "ncu DRAM bytes of k_scan + k_finalize + k_lists (profiles/ncu_traffic.json)",
+                         "dominant": scan_roof},
             "kernels": {k: round(v[1] / max(v[0], 1), 5) for k, v in sorted(prof.items())},
             "n_dedup": nd, "n_cancel": nc, "dedup_count_exact": dup_ok, "parity": parity, "cpu_baseline": cpu_b}
 
