@@ -46,7 +46,11 @@ def check(got, want):
 
 
 @pytest.mark.parametrize("n_req,n_snap", [(1, 1), (1, 50), (7, 300), (200, 5000), (5000, 20000),
-                                          (100_000, 200_000)])
+                                          (100_000, 200_000),
+                                          # tile edges (8192 snapshots per tile), one request over
+                                          # many tiles, a three-pass radix sort (2^19 ranks)
+                                          (1000, 8191), (1000, 8192), (1000, 8193), (3, 16385), (1, 100_000),
+                                          (400_000, 600_000)])
 def test_fold_vs_oracle(eng, n_req, n_snap):
     rng = np.random.default_rng(n_req * 7 + n_snap)
     a = snapshots(rng, n_req, n_snap)
@@ -114,7 +118,8 @@ def test_fold_delta_overrun_rejected(eng):
         eng.fold(*a, n_req_ids=4)
 
 
-@pytest.mark.parametrize("total,n", [(0, 0), (1, 0), (1, 1), (64, 10), (1000, 5000), (1 << 20, 300_000)])
+@pytest.mark.parametrize("total,n", [(0, 0), (1, 0), (1, 1), (64, 10), (1000, 5000), (1 << 20, 300_000),
+                                     (8191, 3000), (8192, 8192), (8193, 100), (3 * 8192 + 5, 20_000)])
 def test_kv_reserve_vs_oracle(eng, total, n):
     rng = np.random.default_rng(total + n)
     ids = rng.integers(0, total + 50, n, dtype=np.uint32) if n else np.zeros(0, np.uint32)
