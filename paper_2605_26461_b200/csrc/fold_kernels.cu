@@ -10,7 +10,7 @@
 // variable-length payloads.  Every primitive is written here (no library sort or scan); tiles
 // are 8192 snapshots:
 //   k_fold_init     clear the per-request tables and the head bitmap
-//   k_fold_stats    consume order: per request id first / last snapshot and sticky done
+//   k_fold_stats    consume order: per request id first snapshot and sticky done
 //                   (fire-and-forget reductions); the block scan of the packed delta lengths
 //                   gives each snapshot's source offset inside the tile (meta, with its lengths)
 //                   and the tile total
@@ -18,7 +18,7 @@
 //   k_fold_bitcnt   per 8192-bit chunk of the bitmap: word prefixes inside the chunk, chunk total
 //   k_fold_scan     one CTA per small array (chunk totals, tile totals): exclusive prefix
 //   k_fold_rank     per request: rank = heads before its first snapshot (first-appearance
-//                   order); order / last progress / done at the rank
+//                   order); order / done at the rank
 //   radix sort      snapshot indices by request rank, stable LSD over the bits min(R, S) needs
 //                   (<= 9 bits per pass): k_sort_hist (per-tile digit counts) -> k_sort_hscan
 //                   (per-digit prefix over tiles) -> k_sort_scatter (per-warp digit counters,
@@ -28,7 +28,8 @@
 //                   with the tile base added (smeta = source offset + lengths)
 //   k_fold_dsum     fold order: tile totals of the live lengths (k_fold_scan: prefix)
 //   k_fold_place    fold order: the block scan of the lengths is each snapshot's destination
-//                   offset; heads write the CSR start of their request, the last live snapshot
+//                   offset; heads write the CSR start of their request, tails its last progress
+//                   (the stable sort puts the request's last snapshot there), the last live snapshot
 //                   the CSR end; the deltas move from source to destination (a thread's
 //                   destinations are one contiguous run)
 #include <cuda_runtime.h>
@@ -95,13 +96,12 @@ __device__ __forceinline__ T block_excl_scan(T v, T* sw, T& total) {
   return ex;
 }
 
-__global__ void k_fold_init(uint32_t R, uint32_t W, uint32_t* __restrict__ first, uint32_t* __restrict__ last,
-                            uint32_t* __restrict__ rdone, uint32_t* __restrict__ bitmap, FoldDev* __restrict__ dev) {
+__global__ void k_fold_init(uint32_t R, uint32_t W, uint32_t* __restrict__ first, uint32_t* __restrict__ rdone,
+                            uint32_t* __restrict__ bitmap, FoldDev* __restrict__ dev) {
   const uint32_t n = R > W ? R : W;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     if (i < R) {
       first[i] = NO_REQ;
-      last[i] = 0;
       rdone[i] = 0;
     }
     if (i < W) bitmap[i] = 0;
@@ -130,7 +130,7 @@ __device__ __forceinline__ void ldb(const uint32_t* __restrict__ a, uint32_t i0,
 __global__ void __launch_bounds__(CB) k_fold_stats(uint32_t S, uint32_t R, const uint32_t* __restrict__ req,
                                                    const uint8_t* __restrict__ done, const uint32_t* __restrict__ nblk,
                                                    const uint32_t* __restrict__ ntok, uint32_t* __restrict__ first,
-                                                   uint32_t* __restrict__ last, uint32_t* __restrict__ rdone,
+                                                   uint32_t* __restrict__ rdone,
                                                    uint4* __restrict__ meta, unsigned long long* __restrict__ tsum,
                                                    FoldDev* __restrict__ dev) {
   __shared__ unsigned long long sw[CWARPS + 1];
@@ -167,7 +167,6 @@ __global__ void __launch_bounds__(CB) k_fold_stats(uint32_t S, uint32_t R, const
       continue;
     }
     atomicMin(first + rr, i);
-    atomicMax(last + rr, i);
     if (((u < 4 ? dn.x : dn.y) >> (8 * (u & 3))) & 0xFFu) atomicOr(rdone + rr, 1u);
   }
 }
@@ -225,12 +224,10 @@ __global__ void __launch_bounds__(1024) k_fold_scan(const unsigned long long* __
   else scan_small(b, bo, nb, nullptr);
 }
 
-__global__ void k_fold_rank(uint32_t R, const uint32_t* __restrict__ first, const uint32_t* __restrict__ last,
-                            const uint32_t* __restrict__ rdone, const uint32_t* __restrict__ bitmap,
-                            const uint32_t* __restrict__ wloc, const unsigned long long* __restrict__ cpre,
-                            const uint32_t* __restrict__ progress, uint32_t* __restrict__ rank,
-                            uint32_t* __restrict__ order, uint32_t* __restrict__ prog_out,
-                            uint8_t* __restrict__ done_out) {
+__global__ void k_fold_rank(uint32_t R, const uint32_t* __restrict__ first, const uint32_t* __restrict__ rdone,
+                            const uint32_t* __restrict__ bitmap, const uint32_t* __restrict__ wloc,
+                            const unsigned long long* __restrict__ cpre, uint32_t* __restrict__ rank,
+                            uint32_t* __restrict__ order, uint8_t* __restrict__ done_out) {
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
     const uint32_t f = first[r];
     if (f == NO_REQ) continue;
@@ -238,7 +235,6 @@ __global__ void k_fold_rank(uint32_t R, const uint32_t* __restrict__ first, cons
     const uint32_t k = (uint32_t)cpre[w / CHUNK_WORDS] + wloc[w] + __popc(bitmap[w] & ((1u << (f & 31)) - 1u));
     rank[r] = k;
     order[k] = r;
-    prog_out[k] = progress[last[r]];
     done_out[k] = rdone[r] ? 1 : 0;
   }
 }
@@ -404,9 +400,8 @@ __global__ void __launch_bounds__(SB) k_sort_scatter(uint32_t S, uint32_t R, uin
         m.y = (uint32_t)(src >> 32);
       }
       smeta[gpos] = m;
-    } else {
-      vout[gpos] = val;
     }
+    vout[gpos] = val;
   }
 }
 
@@ -453,7 +448,8 @@ __device__ __forceinline__ void warp_copy(const uint32_t* __restrict__ in, unsig
 constexpr size_t PLACE_SMEM = (size_t)CWARPS * 2 * 256 * 4;
 
 __global__ void __launch_bounds__(CB) k_fold_place(uint32_t S, uint32_t live_bound, const uint32_t* __restrict__ skey,
-                                                   const uint4* __restrict__ smeta,
+                                                   const uint32_t* __restrict__ sval, const uint32_t* __restrict__ progress,
+                                                   uint32_t* __restrict__ prog_out, const uint4* __restrict__ smeta,
                                                    const unsigned long long* __restrict__ dbase,
                                                    const uint32_t* __restrict__ blocks, unsigned long long n_blocks_in,
                                                    const uint32_t* __restrict__ tokens, unsigned long long n_tokens_in,
@@ -490,6 +486,7 @@ __global__ void __launch_bounds__(CB) k_fold_place(uint32_t S, uint32_t live_bou
         tok_off[key] = (uint32_t)(d >> 32);
       }
       const uint32_t nxt = u + 1 < CIPT ? k[u + 1] : (p + 1 < S ? __ldg(skey + p + 1) : live_bound);
+      if (nxt != key) prog_out[key] = __ldg(progress + __ldg(sval + p));   // the request's last snapshot
       if (nxt >= live_bound) {   // the last live snapshot: the CSR ends
         const unsigned long long e = d + len;
         blk_off[key + 1] = (uint32_t)e;
@@ -538,7 +535,7 @@ static uint32_t tiles(uint64_t S) { return (uint32_t)((S + FTILE - 1) / FTILE); 
 // scratch layout for S snapshots and R request ids
 size_t fold_scratch_bytes(uint64_t S, uint64_t R) {
   const uint64_t T = tiles(S), W = S / 32 + 1, C = (W + CHUNK_WORDS - 1) / CHUNK_WORDS;
-  size_t o = al256(64) + al256(4 * R) * 4;                 // dev, first, last, rdone, rank
+  size_t o = al256(64) + al256(4 * R) * 3;                 // dev, first, rdone, rank
   o += al256(4 * W) * 2 + al256(8 * C) * 2;                // bitmap, wloc, chunk counts / prefix
   o += al256(8 * T) * 4;                                   // tsum, tbase, dsum, dbase
   o += al256(4 * S) * 4;                                   // sort keys / values, two buffers
@@ -569,7 +566,7 @@ int launch_fold(uint8_t* scratch, size_t scratch_bytes, uint32_t S, uint32_t R, 
   auto u32 = [&](size_t n) { return reinterpret_cast<uint32_t*>(take(4 * n)); };
   auto u64 = [&](size_t n) { return reinterpret_cast<unsigned long long*>(take(8 * n)); };
   FoldDev* dev = reinterpret_cast<FoldDev*>(take(64));
-  uint32_t *first = u32(R), *last = u32(R), *rdone = u32(R), *rank = u32(R);
+  uint32_t *first = u32(R), *rdone = u32(R), *rank = u32(R);
   uint32_t *bitmap = u32(W), *wloc = u32(W);
   unsigned long long *ccount = u64(C), *cpre = u64(C);
   unsigned long long *tsum = u64(T), *tbase = u64(T), *dsum = u64(T), *dbase = u64(T);
@@ -583,9 +580,9 @@ int launch_fold(uint8_t* scratch, size_t scratch_bytes, uint32_t S, uint32_t R, 
   int launches = 0;
   auto done_launch = [&](const char* name) { mk.mark(name); ++launches; };
 
-  k_fold_init<<<gR, 256, 0, st>>>(R, W, first, last, rdone, bitmap, dev);
+  k_fold_init<<<gR, 256, 0, st>>>(R, W, first, rdone, bitmap, dev);
   done_launch("k_fold_init");
-  k_fold_stats<<<T, CB, 0, st>>>(S, R, req, done, nblk, ntok, first, last, rdone, meta, tsum, dev);
+  k_fold_stats<<<T, CB, 0, st>>>(S, R, req, done, nblk, ntok, first, rdone, meta, tsum, dev);
   done_launch("k_fold_stats");
   k_fold_bits<<<gR, 256, 0, st>>>(R, first, bitmap);
   done_launch("k_fold_bits");
@@ -593,7 +590,7 @@ int launch_fold(uint8_t* scratch, size_t scratch_bytes, uint32_t S, uint32_t R, 
   done_launch("k_fold_bitcnt");
   k_fold_scan<<<2, 1024, 0, st>>>(ccount, cpre, C, &dev->n_requests, tsum, tbase, T);
   done_launch("k_fold_scan");
-  k_fold_rank<<<gR, 256, 0, st>>>(R, first, last, rdone, bitmap, wloc, cpre, progress, rank, order, prog_out, done_out);
+  k_fold_rank<<<gR, 256, 0, st>>>(R, first, rdone, bitmap, wloc, cpre, rank, order, done_out);
   done_launch("k_fold_rank");
   // radix sort by rank: passes of <= DB_MAX bits over the bits live_bound needs
   const int bits = key_bits(live_bound);
@@ -630,7 +627,7 @@ int launch_fold(uint8_t* scratch, size_t scratch_bytes, uint32_t S, uint32_t R, 
   done_launch("k_fold_scan");
   if (cudaFuncSetAttribute(k_fold_place, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLACE_SMEM) != cudaSuccess)
     return -1;
-  k_fold_place<<<T, CB, PLACE_SMEM, st>>>(S, live_bound, kin, smeta, dbase, blocks, n_blocks_in, tokens, n_tokens_in,
+  k_fold_place<<<T, CB, PLACE_SMEM, st>>>(S, live_bound, kin, vin, progress, prog_out, smeta, dbase, blocks, n_blocks_in, tokens, n_tokens_in,
                                  reinterpret_cast<unsigned long long*>(blk_off),
                                  reinterpret_cast<unsigned long long*>(tok_off), blocks_out, tokens_out, dev);
   done_launch("k_fold_place");
