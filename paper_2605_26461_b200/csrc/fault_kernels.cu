@@ -878,21 +878,52 @@ __global__ void __launch_bounds__(BLOCK, 1) k_general(World W, Scratch S, const 
   general_phase<kStaged, kStage>(W, S, v, in, n, P);
 }
 
+// k_resolve and k_general (stage 1) in one launch (single-GPU batches on the fixed layout): every
+// CTA resolves the client states itself into its shared copy -- O(clients), the same on every CTA;
+// CTA 0 writes the outputs k_resolve writes -- and runs the release-aware pass only when a client
+// needs it (otherwise the launch ends there: no separate k_resolve / k_general round trips).
+__global__ void __launch_bounds__(BLOCK, 1) k_resolve_general(World W, Scratch S, const mpsf_fault_entry* __restrict__ in,
+                                                              uint64_t n, Params P,
+                                                              mpsf_client_verdict* __restrict__ verdict) {
+  pdl_trigger();
+  extern __shared__ __align__(128) uint8_t smem[];
+  const Layout L = make_layout(W, true, true);
+  CState* cs = reinterpret_cast<CState*>(smem + L.cstate);
+  // (the layout is at the shared-memory limit: the resolution's scalars go into the decision-table
+  // region, which the release-aware pass does not use)
+  Globals* s_gl = reinterpret_cast<Globals*>(smem + L.fclient);
+  int* s_general = reinterpret_cast<int*>(smem + L.fclient + sizeof(Globals));
+  pdl_wait();
+  if (__ldcg(S.ctrl + C_ERR) != 0) return;
+  if (!resolve_phase(W, S, P, cs, s_gl, verdict, blockIdx.x == 0, s_general)) return;
+  // the tables of the release-aware pass only when it runs (setup leaves the client states alone)
+  View v = setup<true>(smem, L, W, S, false, true, P.flags & MPSF_PF_ISOLATION);
+  v.cst = cs;
+  __syncthreads();
+  general_phase<true, 1>(W, S, v, in, n, P);
+}
+
+// Kill thresholds from the exact minima of the general path, one client (idempotent: a client
+// state recomputed from the same minima is the same).
+__device__ __forceinline__ void resolve2_client(const Scratch& S, const Params& P, uint32_t c, CState& cs) {
+  if (cs.rel == REL_NONE && P.m2_us > P.benign_us) return;       // pass-1 minima are exact
+  bool kill_all;
+  uint32_t tie;
+  uint32_t g0 = __ldcg(S.giso + 3 * c), g1 = __ldcg(S.giso + 3 * c + 1), g2 = __ldcg(S.giso + 3 * c + 2);
+  if (cs.rel == REL_NONE) {                 // only M2 needed recomputing: keep exact M1 / M3
+    g0 = __ldcg(S.iso1 + c);
+    g2 = __ldcg(S.iso3 + c);
+  }
+  kill_thresholds(P, g0, g1, g2, true, kill_all, tie);
+  cs.kill_tie = tie;
+  cs.flags = (cs.flags & ~CS_KILL_ALL) | (kill_all ? CS_KILL_ALL : 0u);
+}
+
 // Kill thresholds from the exact minima of the general path (cs: global or the CTA's copy).
 __device__ __forceinline__ void resolve2_phase(const World& W, const Scratch& S, const Params& P, CState* cs_arr) {
   for (uint32_t c = threadIdx.x; c < W.n_clients; c += blockDim.x) {
     CState cs = cs_arr[c];
-    if (cs.rel == REL_NONE && P.m2_us > P.benign_us) continue;     // pass-1 minima are exact
-    bool kill_all;
-    uint32_t tie;
-    uint32_t g0 = __ldcg(S.giso + 3 * c), g1 = __ldcg(S.giso + 3 * c + 1), g2 = __ldcg(S.giso + 3 * c + 2);
-    if (cs.rel == REL_NONE) {                 // only M2 needed recomputing: keep exact M1 / M3
-      g0 = __ldcg(S.iso1 + c);
-      g2 = __ldcg(S.iso3 + c);
-    }
-    kill_thresholds(P, g0, g1, g2, true, kill_all, tie);
-    cs.kill_tie = tie;
-    cs.flags = (cs.flags & ~CS_KILL_ALL) | (kill_all ? CS_KILL_ALL : 0u);
+    resolve2_client(S, P, c, cs);
     cs_arr[c] = cs;
   }
 }
@@ -1496,6 +1527,7 @@ static void set_attrs() {
   cudaFuncSetAttribute(k_general<kStaged, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(k_general<kStaged, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(k_finalize<kStaged>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_resolve_general, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(fx::k_scan_fx<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(fx::k_scan_fx<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(fx::k_finalize_fx<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
@@ -1609,6 +1641,18 @@ int launch_general(const World& W, const Scratch& S, const mpsf_fault_entry* in,
                    int stage, cudaStream_t st, const Marker& mk) {
   return staged_fits(W) ? general_t<true>(W, S, in, n, P, stage, st, mk)
                         : general_t<false>(W, S, in, n, P, stage, st, mk);
+}
+
+bool resolve_fused_fits(const World& W) { return fx_fits(W); }
+
+int launch_resolve_general(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
+                           mpsf_client_verdict* verdict, cudaStream_t st, const Marker& mk) {
+  set_attrs<true>();
+  const uint32_t smem = make_layout(W, true, true).total;
+  const int g = clamp_grid(grid_for(k_resolve_general, smem), n);
+  launch_pdl(k_resolve_general, dim3(g), dim3(BLOCK), smem, st, W, S, in, n, P, verdict);
+  mk.mark("k_resolve_general");
+  return ok_or_err();
 }
 
 int launch_resolve2(const World& W, const Scratch& S, const Params& P, cudaStream_t st, const Marker& mk) {

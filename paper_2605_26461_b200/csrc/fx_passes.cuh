@@ -508,13 +508,17 @@ __global__ void __launch_bounds__(BLOCK, 1) k_finalize_fx(World W, Scratch S, ui
   }
   pdl_wait();
   if (__ldcg(S.ctrl + C_ERR) != 0) return;
+  const bool gpath = __ldcg(S.ctrl + C_PATH) != 0;
   uint4* crow = reinterpret_cast<uint4*>(sm + F_CROW);
   uint32_t* trp = reinterpret_cast<uint32_t*>(sm + F_TRAP);
   for (uint32_t k = tid; k < FX_C * 4 * CH_COPIES; k += nb) {
     const uint32_t ci = k / CH_COPIES, c = ci >> 2;
     uint4 a = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, EMPTY32, DBAND);
     if (c < W.n_clients) {
-      const FinClient f = fin_client(S.cstate[c], *S.glob, S.nrall != nullptr);
+      // the general path's exact minima (what k_resolve2 folds in; idempotent if it ran)
+      CState cs = S.cstate[c];
+      if (gpath) resolve2_client(S, P, c, cs);
+      const FinClient f = fin_client(cs, *S.glob, S.nrall != nullptr);
       a = client_row(f, ci & 3u);
       // an applied trap, as the ok32 of a (non-replayable) trap record
       if (k % (4 * CH_COPIES) == 0) trp[c] = f.trap_ok == EMPTY32 ? EMPTY32 : (f.trap_ok | 0x80000000u);

@@ -779,17 +779,49 @@ int mpsf_finalize(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const m
   return MPSF_OK;
 }
 
+// Between the passes of a single-GPU batch: the client resolution and, when a client needs it,
+// the release-aware pass.  On the fixed layout with isolation on, k_resolve + k_general stage 1 are
+// one launch and pass 2 folds in k_resolve2; otherwise the separate kernels of the phase API.
+static int mid_phases(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const mpsf_params* p,
+                      mpsf_client_verdict* d_verdict, cudaStream_t st, int& launches) {
+  const Marker mk = c->marker();
+  const Params P = to_params(p);
+  const bool iso = (p->flags & MPSF_PF_ISOLATION) && n;
+  if (iso && resolve_fused_fits(c->W)) {
+    if (launch_resolve_general(c->W, c->S, d_in, n, P, d_verdict, st, mk)) return MPSF_E_CUDA;
+    ++launches;
+    if (p->m2_us <= p->benign_us) {
+      if (launch_general(c->W, c->S, d_in, n, P, 2, st, mk)) return MPSF_E_CUDA;
+      ++launches;
+    }
+    return MPSF_OK;
+  }
+  if (launch_resolve(c->W, c->S, P, d_verdict, st, mk)) return MPSF_E_CUDA;
+  ++launches;
+  if (iso) {
+    if (launch_general(c->W, c->S, d_in, n, P, 1, st, mk)) return MPSF_E_CUDA;
+    ++launches;
+    if (p->m2_us <= p->benign_us) {
+      if (launch_general(c->W, c->S, d_in, n, P, 2, st, mk)) return MPSF_E_CUDA;
+      ++launches;
+    }
+    if (launch_resolve2(c->W, c->S, P, st, mk)) return MPSF_E_CUDA;
+    ++launches;
+  }
+  return MPSF_OK;
+}
+
 int mpsf_process(mpsf_ctx* c, const mpsf_fault_entry* d_in, uint64_t n, const mpsf_params* p,
                  mpsf_out_record* d_out, mpsf_client_verdict* d_verdict, uint64_t* d_counts,
                  uint64_t* d_dkeys, uint32_t* d_didx, uint32_t* d_cancel, void* stream) {
   if (!c || !p) return MPSF_E_ARG;
   if (n && (!d_in || !d_out || !d_dkeys || !d_didx || !d_cancel)) return MPSF_E_ARG;
+  if (c->W.n_clients && (!d_verdict || !d_counts)) return MPSF_E_ARG;
   int rc = mpsf_scan(c, d_in, n, p, d_counts, stream);
-  if (!rc) rc = mpsf_resolve(c, p, d_verdict, d_counts, stream);
-  if (!rc && (p->flags & MPSF_PF_ISOLATION) && n) {
-    rc = mpsf_general(c, d_in, n, p, 1, stream);
-    if (!rc && p->m2_us <= p->benign_us) rc = mpsf_general(c, d_in, n, p, 2, stream);
-    if (!rc) rc = mpsf_resolve2(c, p, stream);
+  if (!rc) {
+    int launches = 0;
+    rc = mid_phases(c, d_in, n, p, d_verdict, reinterpret_cast<cudaStream_t>(stream), launches);
+    c->last_launches += launches;
   }
   if (!rc) rc = mpsf_finalize(c, d_in, n, p, d_out, d_dkeys, d_didx, d_cancel, stream);
   return rc;
@@ -1081,19 +1113,7 @@ int mpsf_submit_host(mpsf_ctx* c, int slot, const mpsf_fault_entry* h_in, uint64
   }
   const Marker mk = c->marker();
   const Params P = to_params(p);
-  if (launch_resolve(c->W, c->S, P, d_v, st, mk))
-    return MPSF_E_CUDA;
-  ++launches;
-  if ((p->flags & MPSF_PF_ISOLATION) && n) {
-    if (launch_general(c->W, c->S, d_in, n, P, 1, st, mk)) return MPSF_E_CUDA;
-    ++launches;
-    if (p->m2_us <= p->benign_us) {
-      if (launch_general(c->W, c->S, d_in, n, P, 2, st, mk)) return MPSF_E_CUDA;
-      ++launches;
-    }
-    if (launch_resolve2(c->W, c->S, P, st, mk)) return MPSF_E_CUDA;
-    ++launches;
-  }
+  if ((rc = mid_phases(c, d_in, n, p, d_v, st, launches))) return rc;
   for (int k = 0; k < chunks; ++k) {
     const uint64_t lo = ent(k), cnt = ent(k + 1) - lo;
     Params Pk = P;

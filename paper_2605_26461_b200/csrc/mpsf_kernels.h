@@ -26,6 +26,11 @@ int launch_resolve(const World& W, const Scratch& S, const Params& P, mpsf_clien
 int launch_general(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
                    int stage, cudaStream_t st, const Marker& mk);
 int launch_resolve2(const World& W, const Scratch& S, const Params& P, cudaStream_t st, const Marker& mk);
+// single-GPU batches on the fixed layout: k_resolve + k_general stage 1 in one launch; pass 2 then
+// folds in what k_resolve2 would (so neither separate launch is needed)
+bool resolve_fused_fits(const World& W);
+int launch_resolve_general(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
+                           mpsf_client_verdict* verdict, cudaStream_t st, const Marker& mk);
 // pass 2 over entries [0, n) of `in`, a chunk of the batch starting at batch chunk q_base (the
 // chunk's first entry is batch entry 64 * q_base); then, once per batch, the ordered lists
 int launch_finalize(const World& W, const Scratch& S, const mpsf_fault_entry* in, uint64_t n, const Params& P,
