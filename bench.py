@@ -443,6 +443,7 @@ def run_mine(args):
     if not args.no_storm and ws == 1:
         extra["translate_f2"] = bench_translate(args, eng, hbm_peak, flush, w)
         extra["fold_f3"] = bench_fold(args, eng, hbm_peak, flush)
+        extra["c1"] = bench_c1(args, eng, flush, threads)
     elif args.sharded_translate:
         # opt-in: the multi-GPU form of the translation extra (NCCL between the phases)
         extra["translate_f2_sharded"] = bench_translate_sharded(args, eng, hbm_peak, flush, w, ws, rank)
@@ -622,6 +623,52 @@ def bench_storm(args, eng, hbm_peak, flush, ws=1, rank=0, local=0, threads=1):
                          "dominant": scan_roof},
             "kernels": {k: round(v[1] / max(v[0], 1), 5) for k, v in sorted(prof.items())},
             "n_dedup": nd, "n_cancel": nc, "dedup_count_exact": dup_ok, "parity": parity, "cpu_baseline": cpu_b}
+
+
+def bench_c1(args, eng, flush, threads):
+    """Config 1 (the reference's own CPU-replay scale: 4 MPS clients, 10^5 entries across the MMU
+    scenarios): one batch on the device, L2 flushed between steps, and end to end through
+    ``mpsf_process_host``; all six outputs checked against the C oracle, and the reference's
+    own per-entry path (channel_to_pid + faults.classify) timed on the whole trace beside it."""
+    import torch
+    from paper_2605_26461_b200 import synth
+    from paper_2605_26461_b200.engine import BatchParams, DeviceBuffers, alloc_host_outputs
+    from oracle import c_oracle as co
+    from oracle.seq_oracle import Params as OP
+    cfg = synth.CONFIGS["c1"]
+    w, trace = synth.make_config("c1")
+    n = len(trace)
+    eng.upload_world(w)
+    params = BatchParams(isolation=True)
+    d_in = torch.from_numpy(trace.view(np.uint8).copy()).cuda()
+    bufs = DeviceBuffers(n, w.n_clients)
+    for _ in range(5):
+        res = eng.process_resident(d_in, n, params, bufs)
+    want = co.process_batch(w, trace, OP(isolation=True), threads=threads)
+    exact = all(np.array_equal(getattr(res, f), getattr(want, f)) for f in
+                ("out", "verdict", "counts", "dedup_keys", "dedup_idx", "cancel"))
+    steps = max(50, args.steps)
+    total, _, prof = time_resident(eng, d_in, n, params, bufs, steps, flush)
+    ms = total / steps
+    pinned = torch.from_numpy(trace.view(np.uint8)).pin_memory().numpy().view(trace.dtype)
+    hb = alloc_host_outputs(n, w.n_clients, pinned=True)
+    ts = []
+    for _ in range(30):
+        t0 = time.perf_counter()
+        eng.process(pinned, params, hb)
+        ts.append(time.perf_counter() - t0)
+    e2e_ms = statistics.median(ts[5:]) * 1e3
+    ref = reference_cpu_path(cfg, trace, res.out, n_prefix=n)
+    out = {"workload": f"c1: {cfg['clients']} MPS clients x 32 ranges x {cfg['pages']} pages, {n} entries "
+                       f"(translation misses across the MMU scenarios), isolation on",
+           "value": n / (ms / 1e3), "unit": "entries/s", "ms_per_batch": ms, "steps": steps,
+           "e2e_ms_per_batch": e2e_ms, "e2e_value": n / (e2e_ms / 1e3),
+           "kernels": {k: round(v[1] / max(v[0], 1), 5) for k, v in sorted(prof.items())},
+           "parity": "bit-exact vs C oracle (six outputs)" if exact else "MISMATCH vs C oracle",
+           "reference_cpu_path": ref}
+    if isinstance(ref, dict) and ref.get("value_1core"):
+        out["e2e_vs_reference_1core"] = out["e2e_value"] / ref["value_1core"]
+    return out
 
 
 def bench_translate(args, eng, hbm_peak, flush, w):
