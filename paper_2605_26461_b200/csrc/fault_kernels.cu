@@ -1211,27 +1211,34 @@ __global__ void __launch_bounds__(SEG_CHUNKS) k_lists(Scratch S, const mpsf_faul
   const uint64_t pc = pre & 0xFFFFFFFFull;
   uint64_t pd = pre >> 32;
   const uint32_t g0 = (uint32_t)(base_index + q * WCHUNK);
-  // cancel list: the warp writes its 32 chunks one at a time, lane l the chunk's entries 2l, 2l+1
-  // (consecutive positions: coalesced stores)
+  // cancel list: each lane lists its chunk's cancelled entries (ascending) into the warp's shared
+  // buffer from its offset in the warp (a warp scan of the counts), then the warp copies the
+  // buffer out with coalesced stores -- the warp's chunks are consecutive, so are their cancels
+  __shared__ uint16_t s_code[SEG_CHUNKS / 32][32 * WCHUNK];   // per warp: its 32 chunks' entries
   {
-    const unsigned long long below = (1ull << (2 * lane)) - 1ull;
-    for (int j = 0; j < 32; ++j) {
-      const unsigned long long cm = __shfl_sync(0xFFFFFFFFu, mk.x, j);
-      if (!cm) continue;
-      const uint64_t cbj = __shfl_sync(0xFFFFFFFFu, pc, j);
-      const uint32_t gj = __shfl_sync(0xFFFFFFFFu, g0, j) + 2 * lane;
-      const uint32_t two = (uint32_t)(cm >> (2 * lane)) & 3u;
-      uint64_t pos = cbj + __popcll(cm & below);
-      if (two & 1u) cancel[pos++] = gj;
-      if (two & 2u) cancel[pos] = gj + 1;
+    uint16_t* buf = s_code[warp];            // (chunk in the warp << 6 | entry)
+    const uint32_t cnt = (uint32_t)__popcll(mk.x);
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+      if (lane >= o) inc += u;
     }
+    const uint32_t tot = __shfl_sync(0xFFFFFFFFu, inc, 31);
+    uint32_t pos = inc - cnt;
+    for (unsigned long long m = mk.x; m; m &= m - 1)
+      buf[pos++] = (uint16_t)((lane << 6) | (uint32_t)(__ffsll((long long)m) - 1));
+    __syncwarp();
+    const uint64_t cb0 = __shfl_sync(0xFFFFFFFFu, pc, 0);
+    const uint32_t gw0 = __shfl_sync(0xFFFFFFFFu, g0, 0);   // the warp's first entry
+    for (uint32_t t = lane; t < tot; t += 32) cancel[cb0 + t] = gw0 + buf[t];
+    __syncwarp();
   }
   // dedup set: the warp's representatives occupy consecutive positions from its first chunk's
   // offset on.  Each lane lists its chunk's representatives (chunk << 6 | entry) at their flat
   // ranks in a per-warp shared table, then lane l writes ranks l, l + 32, ... (coalesced) with
   // one table read each.  Keys were staged by k_finalize.
   {
-    __shared__ uint16_t s_code[SEG_CHUNKS / 32][32 * WCHUNK];   // per warp: its 32 chunks
     uint16_t* code = s_code[warp];
     unsigned long long dm_l = mk.y;
     const uint32_t cnt = (uint32_t)__popcll(dm_l);
