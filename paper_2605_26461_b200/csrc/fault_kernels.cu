@@ -1169,7 +1169,7 @@ __global__ void __launch_bounds__(SEG_CHUNKS) k_lists(Scratch S, const mpsf_faul
                                                    const mpsf_out_record* __restrict__ out, uint64_t nq,
                                                    uint64_t base_index, unsigned long long* __restrict__ dkeys,
                                                    uint32_t* __restrict__ didx, uint32_t* __restrict__ cancel,
-                                                   DevSummary* __restrict__ sum) {
+                                                   DevSummary* __restrict__ sum, bool prescan) {
   static_assert(SEG_CHUNKS % 32 == 0 && SEG_CHUNKS <= 1024, "one thread per chunk");
   pdl_wait();
   const bool last = blockIdx.x == gridDim.x - 1;
@@ -1181,14 +1181,19 @@ __global__ void __launch_bounds__(SEG_CHUNKS) k_lists(Scratch S, const mpsf_faul
   __shared__ unsigned long long s_w[32];
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t seg = blockIdx.x;
-  // base: counts of all earlier segments
-  unsigned long long acc = 0;
-  for (uint64_t i = threadIdx.x; i < seg; i += blockDim.x) acc += __ldcg(S.segcnt + i);
-  if (threadIdx.x == 0) s_base = 0;
-  __syncthreads();
+  // base: counts of all earlier segments (prescanned by k_seg_scan for large batches, where the
+  // per-block sums would read O(segments^2) counters)
+  if (prescan) {
+    if (threadIdx.x == 0) s_base = __ldcg(S.segbase + seg);
+  } else {
+    unsigned long long acc = 0;
+    for (uint64_t i = threadIdx.x; i < seg; i += blockDim.x) acc += __ldcg(S.segcnt + i);
+    if (threadIdx.x == 0) s_base = 0;
+    __syncthreads();
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
-  if (lane == 0 && acc) atomicAdd(&s_base, acc);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+    if (lane == 0 && acc) atomicAdd(&s_base, acc);
+  }
   const uint64_t q = seg * SEG_CHUNKS + threadIdx.x;
   ulonglong2 mk = make_ulonglong2(0, 0);
   if (q < nq) {
@@ -1273,6 +1278,53 @@ __global__ void __launch_bounds__(SEG_CHUNKS) k_lists(Scratch S, const mpsf_faul
           didx[pd0 + f] = gix[h];
         }
       }
+    }
+  }
+}
+
+// Exclusive prefix of the segment counters (one CTA; thread t owns a contiguous run).
+__global__ void __launch_bounds__(1024) k_seg_scan(const Scratch S, uint64_t nseg) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ unsigned long long sw[33];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t per = (nseg + 1023) / 1024, b = threadIdx.x * per, e = min(b + per, nseg);
+  unsigned long long s = 0;
+  for (uint64_t i0 = b; i0 < e; i0 += 8) {   // eight loads in flight
+    unsigned long long v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = i0 + k < e ? __ldcg(S.segcnt + i0 + k) : 0ull;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += v[k];
+  }
+  unsigned long long inc = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long u = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+    if (lane >= (uint32_t)o) inc += u;
+  }
+  if (lane == 31) sw[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const unsigned long long w = sw[lane];
+    unsigned long long wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long u = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+      if (lane >= (uint32_t)o) wi += u;
+    }
+    sw[lane] = wi - w;
+  }
+  __syncthreads();
+  unsigned long long run = sw[warp] + inc - s;
+  for (uint64_t i0 = b; i0 < e; i0 += 8) {
+    unsigned long long v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = i0 + k < e ? __ldcg(S.segcnt + i0 + k) : 0ull;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (i0 + k < e) S.segbase[i0 + k] = run;
+      run += v[k];
     }
   }
 }
@@ -1684,8 +1736,13 @@ int launch_lists(const Scratch& S, const mpsf_fault_entry* in, const mpsf_out_re
     mk.mark("k_summary");
     return ok_or_err();
   }
+  const bool prescan = nseg > 2048;
+  if (prescan) {
+    launch_pdl(k_seg_scan, dim3(1), dim3(1024), 0, st, S, nseg);
+    mk.mark("k_seg_scan");
+  }
   launch_pdl(k_lists, dim3((unsigned)nseg), dim3(SEG_CHUNKS), 0, st, S, in, out, chunks_for(n), base_index, dkeys,
-             didx, cancel, sum);
+             didx, cancel, sum, prescan);
   mk.mark("k_lists");
   return ok_or_err();
 }

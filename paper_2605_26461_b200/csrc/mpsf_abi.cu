@@ -601,7 +601,7 @@ int mpsf_upload_world(mpsf_ctx* c, const mpsf_range_entry* ranges, uint32_t nr, 
 
 static int ensure_call_scratch(mpsf_ctx* c, uint64_t n) {
   const uint64_t nq = chunks_for(n), nseg = segments_for(n);
-  const uint64_t mbytes = (16 + 8 * 64) * std::max<uint64_t>(nq, 1) + 8 * std::max<uint64_t>(nseg, 1);
+  const uint64_t mbytes = (16 + 8 * 64) * std::max<uint64_t>(nq, 1) + 16 * std::max<uint64_t>(nseg, 1);
   if (mbytes > c->tiles_cap) {
     cudaFree(c->d_masks);
     c->d_masks = nullptr;
@@ -620,6 +620,7 @@ static int ensure_call_scratch(mpsf_ctx* c, uint64_t n) {
   c->S.cmask = reinterpret_cast<uint4*>(c->d_masks);
   c->S.dstage = reinterpret_cast<unsigned long long*>(c->d_masks + 16 * std::max<uint64_t>(nq, 1));
   c->S.segcnt = c->S.dstage + 64 * std::max<uint64_t>(nq, 1);
+  c->S.segbase = c->S.segcnt + std::max<uint64_t>(nseg, 1);
   const uint64_t floor_cap = 1ull << 16;
   if (c->want_dd == 0 || c->last_n != n) {
     const uint64_t guess = next_pow2(std::max<uint64_t>(floor_cap, std::min<uint64_t>(n / 32, 1ull << 24)));

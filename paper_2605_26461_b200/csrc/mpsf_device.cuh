@@ -165,6 +165,7 @@ struct Scratch {
   unsigned long long* err_idx;
   uint4* cmask;                // [chunks] ballots: cancelled entries 2l / 2l+1, representatives 2l / 2l+1
   unsigned long long* segcnt;  // [segments] cancel count | dedup count << 32
+  unsigned long long* segbase; // [segments] exclusive prefix of segcnt (large batches: k_seg_scan)
   unsigned long long* dstage;  // [chunks][KSTAGE] first dedup keys of each chunk (k_finalize -> k_lists)
   unsigned long long* drec;    // [n] pass-1 records (fixed-layout worlds), entry drec_base first
   uint64_t drec_base;          // global index of drec[0] (params.base_index of the batch)
