@@ -30,8 +30,9 @@
 //   k_fold_place    fold order: the block scan of the lengths is each snapshot's destination
 //                   offset; heads write the CSR start of their request, tails its last progress
 //                   (the stable sort puts the request's last snapshot there), the last live snapshot
-//                   the CSR end; the deltas move from source to destination (a thread's
-//                   destinations are one contiguous run)
+//                   the CSR end; the deltas move from source to destination warp-cooperatively
+//                   (a warp's 256 snapshots have one contiguous destination range, walked 32
+//                   words per coalesced store)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
