@@ -16,3 +16,7 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 r = bench.bench_translate(SimpleNamespace(steps=int(sys.argv[1]) if len(sys.argv) > 1 else 5, n=None), eng, 6461.2,
                           flush, w)
 print(r)
+eng.set_profiling(True)
+bench.bench_translate(SimpleNamespace(steps=20, n=None), eng, 6461.2, flush, w)
+prof = eng.profile()
+print({k: round(v[1] / max(v[0], 1) * 1e3, 2) for k, v in sorted(prof.items())}, "us per call")
