@@ -1448,6 +1448,13 @@ __global__ void __launch_bounds__(BLOCK, 1) k_tr_classify(World W, Scratch S, co
     }
     const uint32_t bm0 = __ballot_sync(0xFFFFFFFFu, ok0 && m0), bm1 = __ballot_sync(0xFFFFFFFFu, ok1 && m1);
     const uint32_t bp0 = __ballot_sync(0xFFFFFFFFu, ok0 && p0), bp1 = __ballot_sync(0xFFFFFFFFu, ok1 && p1);
+    {   // the chunk's misses compacted in access order: k_tr_lists copies them out without
+        // re-reading the stream (which its scattered reads would pull in nearly whole)
+      const uint32_t below = (1u << lane) - 1u;
+      uint4* stg = S.trstage + (i0 / WCHUNK) * WCHUNK + __popc(bm0 & below) + __popc(bm1 & below);
+      if (ok0 && m0) __stcg(stg, e0);
+      if (ok1 && m1) __stcg(stg + ((ok0 && m0) ? 1 : 0), e1);
+    }
     if (lane == 0) {
       const uint64_t q = i0 / WCHUNK;
       S.cmask[q] = make_uint4(bm0, bm1, bp0, bp1);
@@ -1515,7 +1522,7 @@ __global__ void __launch_bounds__(SEG_CHUNKS) k_tr_lists(Scratch S, const mpsf_f
     for (int t = 0; t < 2; ++t) {
       if (two & (1u << t)) {
         fault_idx[pos] = gj + t;
-        reinterpret_cast<uint4*>(faults)[pos] = __ldcs(reinterpret_cast<const uint4*>(in) + qj * WCHUNK + 2 * lane + t);
+        reinterpret_cast<uint4*>(faults)[pos] = __ldcs(S.trstage + qj * WCHUNK + (pos - bj));
         ++pos;
       }
     }

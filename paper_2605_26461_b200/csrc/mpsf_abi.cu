@@ -171,6 +171,8 @@ struct mpsf_ctx {
   }
   uint32_t* d_remap_err = nullptr;
   uint8_t* d_fold = nullptr;    // snapshot-fold scratch (grown on demand)
+  uint4* d_trstage = nullptr;   // translation: staged miss entries, 64 per chunk (grown on demand)
+  uint64_t trstage_cap = 0;     // chunks
   size_t fold_cap = 0;
   // host-path buffers and the copy streams of the chunked pipeline
   HostSlot slots[kSlots];
@@ -322,6 +324,7 @@ void mpsf_destroy(mpsf_ctx* c) {
   }
   cudaFree(c->d_remap_err);
   cudaFree(c->d_fold);
+  cudaFree(c->d_trstage);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : c->pend_events) cudaEventDestroy(e);
   if (c->h_sum) cudaFreeHost(c->h_sum);
@@ -865,6 +868,16 @@ int mpsf_translate_prefetch(mpsf_ctx* c, const mpsf_fault_entry* d_acc, uint64_t
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int rc = ensure_call_scratch(c, n);
   if (rc) return rc;
+  const uint64_t nq = std::max<uint64_t>(chunks_for(n), 1);
+  if (nq > c->trstage_cap) {
+    CK(cudaStreamSynchronize(st));
+    cudaFree(c->d_trstage);
+    c->d_trstage = nullptr;
+    c->trstage_cap = 0;
+    CK(cudaMalloc(&c->d_trstage, 16ull * 64 * nq));
+    c->trstage_cap = nq;
+  }
+  c->S.trstage = c->d_trstage;
   InitSegs segs{};
   int k = 0;
   segs.p[k] = c->d_pf; segs.words[k] = c->W.n_pages; segs.val[k++] = EMPTY32;

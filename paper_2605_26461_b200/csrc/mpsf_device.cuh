@@ -166,6 +166,8 @@ struct Scratch {
   uint4* cmask;                // [chunks] ballots: cancelled entries 2l / 2l+1, representatives 2l / 2l+1
   unsigned long long* segcnt;  // [segments] cancel count | dedup count << 32
   unsigned long long* segbase; // [segments] exclusive prefix of segcnt (large batches: k_seg_scan)
+  uint4* trstage;              // [chunks][64] translation: each chunk's miss entries compacted in
+                               //  access order (k_tr_classify -> k_tr_lists)
   unsigned long long* dstage;  // [chunks][KSTAGE] first dedup keys of each chunk (k_finalize -> k_lists)
   unsigned long long* drec;    // [n] pass-1 records (fixed-layout worlds), entry drec_base first
   uint64_t drec_base;          // global index of drec[0] (params.base_index of the batch)
