@@ -698,17 +698,19 @@ static int batch_init(mpsf_ctx* c, uint64_t n, const mpsf_params* p, uint64_t* d
   c->S.drec_base = p->base_index;
   InitSegs segs{};
   int k = 0;
-  segs.p[k] = c->d_dd; segs.words[k] = c->W.n_pages * c->W.dd_groups; segs.val[k++] = EMPTY32;
+  // (pass 1 probes the dedup slots and first-eligible keys at random: they are cleared last, so
+  // they are the freshest lines in L2 when it starts; nr1 is only read by the release-aware pass)
   if (p->flags & MPSF_PF_ISOLATION) { segs.p[k] = c->d_nr1; segs.words[k] = c->W.n_pages; segs.val[k++] = EMPTY32; }
-  if ((p->flags & MPSF_PF_ISOLATION) && c->S.nrall) {
-    segs.p[k] = c->S.nrall; segs.words[k] = c->W.n_pages; segs.val[k++] = EMPTY32;
-  }
   segs.p[k] = c->d_small; segs.words[k] = c->small_empty_bytes / 4; segs.val[k++] = EMPTY32;
   segs.p[k] = c->d_small + c->small_zero_off; segs.words[k] = c->small_zero_bytes / 4; segs.val[k++] = 0;
   segs.p[k] = c->S.segcnt; segs.words[k] = 2 * segments_for(n); segs.val[k++] = 0;
   segs.p[k] = c->d_hdd; segs.words[k] = 4 * c->hcap_dd; segs.val[k++] = EMPTY32;
   segs.p[k] = c->d_hnr; segs.words[k] = 4 * c->hcap_nr; segs.val[k++] = EMPTY32;
   if (c->W.n_clients) { segs.p[k] = d_counts; segs.words[k] = 2ull * NSCEN * c->W.n_clients; segs.val[k++] = 0; }
+  if ((p->flags & MPSF_PF_ISOLATION) && c->S.nrall) {
+    segs.p[k] = c->S.nrall; segs.words[k] = c->W.n_pages; segs.val[k++] = EMPTY32;
+  }
+  segs.p[k] = c->d_dd; segs.words[k] = c->W.n_pages * c->W.dd_groups; segs.val[k++] = EMPTY32;
   segs.n = k;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
