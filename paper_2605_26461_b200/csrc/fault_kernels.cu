@@ -1537,7 +1537,7 @@ __global__ void k_hash_export(Hash h, uint64_t cap, unsigned long long* __restri
                               uint32_t* __restrict__ counter, uint64_t out_cap) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap; i += (uint64_t)gridDim.x * blockDim.x) {
     const unsigned long long k = h.keys[2 * i];
-    if (k == EMPTY64) continue;
+    if ((uint32_t)(h.keys[2 * i + 1] >> 32) != h.gen) continue;   // free in this batch
     const uint32_t o = atomicAdd(counter, 1u);
     if (o < out_cap) { keys[o] = k; vals[o] = *hash_val(h, (uint32_t)i); }
   }

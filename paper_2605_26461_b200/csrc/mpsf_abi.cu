@@ -112,6 +112,7 @@ struct mpsf_ctx {
   uint64_t hcap_dd = 0;
   unsigned long long* d_hnr = nullptr;
   uint64_t hcap_nr = 0;
+  uint32_t hash_gen = 0;        // the batch generation of the hash tables (bumped by every batch)
   uint64_t want_dd = 0, want_nr = 0;
   Scratch S{};
   // summary (mapped pinned host memory)
@@ -635,6 +636,7 @@ static int ensure_call_scratch(mpsf_ctx* c, uint64_t n) {
     c->d_hdd = nullptr;
     c->hcap_dd = 0;
     CK(cudaMalloc(&c->d_hdd, 16 * c->want_dd));
+    CK(cudaMemset(c->d_hdd, 0, 16 * c->want_dd));   // generation 0: free in every batch
     c->hcap_dd = c->want_dd;
   }
   if (c->want_nr != c->hcap_nr) {
@@ -642,6 +644,7 @@ static int ensure_call_scratch(mpsf_ctx* c, uint64_t n) {
     c->d_hnr = nullptr;
     c->hcap_nr = 0;
     CK(cudaMalloc(&c->d_hnr, 16 * c->want_nr));
+    CK(cudaMemset(c->d_hnr, 0, 16 * c->want_nr));
     c->hcap_nr = c->want_nr;
   }
   Scratch& S = c->S;
@@ -704,8 +707,9 @@ static int batch_init(mpsf_ctx* c, uint64_t n, const mpsf_params* p, uint64_t* d
   segs.p[k] = c->d_small; segs.words[k] = c->small_empty_bytes / 4; segs.val[k++] = EMPTY32;
   segs.p[k] = c->d_small + c->small_zero_off; segs.words[k] = c->small_zero_bytes / 4; segs.val[k++] = 0;
   segs.p[k] = c->S.segcnt; segs.words[k] = 2 * segments_for(n); segs.val[k++] = 0;
-  segs.p[k] = c->d_hdd; segs.words[k] = 4 * c->hcap_dd; segs.val[k++] = EMPTY32;
-  segs.p[k] = c->d_hnr; segs.words[k] = 4 * c->hcap_nr; segs.val[k++] = EMPTY32;
+  // (the wild-page hash tables need no clearing: a new generation frees every slot)
+  if (++c->hash_gen == 0) c->hash_gen = 1;
+  c->S.hdd.gen = c->S.hnr.gen = c->hash_gen;
   if (c->W.n_clients) { segs.p[k] = d_counts; segs.words[k] = 2ull * NSCEN * c->W.n_clients; segs.val[k++] = 0; }
   if ((p->flags & MPSF_PF_ISOLATION) && c->S.nrall) {
     segs.p[k] = c->S.nrall; segs.words[k] = c->W.n_pages; segs.val[k++] = EMPTY32;

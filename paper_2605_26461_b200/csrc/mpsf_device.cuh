@@ -135,9 +135,11 @@ constexpr uint32_t ROW_PERPAGE = 0x80u;
 constexpr uint32_t CH_VALID = 1u << 31;
 
 struct Hash {
-  unsigned long long* keys;   // 16-byte slots: [2s] key, [2s+1] low 32 bits = min value
+  unsigned long long* keys;   // 16-byte slots: [2s] key, [2s+1] = min value | generation << 32
   uint32_t mask;
   uint32_t used_slot;  // ctrl index counting claimed slots
+  uint32_t gen;        // this batch's generation: a slot of another generation is free (so the
+                       //  tables need no clearing between batches; never 0, fresh tables are zeroed)
 };
 
 struct Scratch {
@@ -288,25 +290,43 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   return x;
 }
 
-// Open addressing, linear probing over 16-byte slots {u64 key, u32 value, pad}: one load
-// reads key and value together; value = atomic min.  Returns false on overflow.
+// Open addressing, linear probing over 16-byte slots {u64 key, u32 value, u32 generation}: one
+// load reads the whole slot; value = atomic min.  A slot whose generation is not the batch's is
+// free: it is claimed with one 128-bit CAS of the whole slot.  Returns false on overflow.
 __device__ __forceinline__ uint32_t* hash_val(const Hash& h, uint32_t s) {
   return reinterpret_cast<uint32_t*>(h.keys + 2ull * s + 1);
+}
+
+__device__ __forceinline__ ulonglong2 cas128(ulonglong2* a, ulonglong2 cmp, ulonglong2 val) {
+  ulonglong2 old;
+  asm volatile("{ .reg .b128 c, n, d;\n\t"
+               "mov.b128 c, {%2, %3};\n\t"
+               "mov.b128 n, {%4, %5};\n\t"
+               "atom.global.cas.b128 d, [%6], c, n;\n\t"
+               "mov.b128 {%0, %1}, d; }"
+               : "=l"(old.x), "=l"(old.y)
+               : "l"(cmp.x), "l"(cmp.y), "l"(val.x), "l"(val.y), "l"(a)
+               : "memory");
+  return old;
 }
 
 // `used` counts claimed slots (a block-local smem counter in the scan, flushed once per block).
 __device__ __forceinline__ bool hash_min(const Hash& h, uint32_t* used, uint64_t key, uint32_t v) {
   uint32_t s = (uint32_t)mix64(key) & h.mask;
   for (int p = 0; p < HASH_MAX_PROBE; ++p) {
-    const ulonglong2 slot = __ldcg(reinterpret_cast<const ulonglong2*>(h.keys) + s);
-    unsigned long long k = slot.x;
-    uint32_t cur = (uint32_t)slot.y;
-    if (k == EMPTY64) {
-      k = atomicCAS(h.keys + 2ull * s, EMPTY64, (unsigned long long)key);
-      if (k == EMPTY64) { atomicAdd(used, 1u); k = key; cur = EMPTY32; }
+    ulonglong2* a = reinterpret_cast<ulonglong2*>(h.keys) + s;
+    ulonglong2 slot = __ldcg(a);
+    while ((uint32_t)(slot.y >> 32) != h.gen) {          // free in this batch: claim it whole
+      const ulonglong2 want = make_ulonglong2(key, (unsigned long long)v | ((unsigned long long)h.gen << 32));
+      const ulonglong2 old = cas128(a, slot, want);
+      if (old.x == slot.x && old.y == slot.y) {
+        atomicAdd(used, 1u);
+        return true;
+      }
+      slot = old;                                         // claimed meanwhile: look at it again
     }
-    if (k == key) {
-      if (cur > v) atomicMin(hash_val(h, s), v);
+    if (slot.x == key) {
+      if ((uint32_t)slot.y > v) atomicMin(hash_val(h, s), v);
       return true;
     }
     s = (s + 1) & h.mask;
@@ -318,8 +338,8 @@ __device__ __forceinline__ uint32_t hash_get(const Hash& h, uint64_t key) {
   uint32_t s = (uint32_t)mix64(key) & h.mask;
   for (int p = 0; p < HASH_MAX_PROBE; ++p) {
     const ulonglong2 slot = __ldcg(reinterpret_cast<const ulonglong2*>(h.keys) + s);
+    if ((uint32_t)(slot.y >> 32) != h.gen) return EMPTY32;   // a free slot ends the probe run
     if (slot.x == key) return (uint32_t)slot.y;
-    if (slot.x == EMPTY64) return EMPTY32;
     s = (s + 1) & h.mask;
   }
   return EMPTY32;
