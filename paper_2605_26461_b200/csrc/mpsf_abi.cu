@@ -188,6 +188,9 @@ struct mpsf_ctx {
 
 // `fault`: a fault-path batch (translation summaries carry no hash counts and must not size
 // the wild-page tables)
+// Wild-page hash capacity: 8x the previous batch's keys (load <= 1/8 keeps the probe runs short;
+// with generation-stamped slots a larger table costs no clearing)
+constexpr uint64_t kHashSlack = 8;
 static void fill_summary(mpsf_ctx* c, const DevSummary& d, mpsf_summary* out, bool fault) {
   memset(out, 0, sizeof(*out));
   const uint32_t err = d.ctrl[C_ERR];
@@ -209,8 +212,8 @@ static void fill_summary(mpsf_ctx* c, const DevSummary& d, mpsf_summary* out, bo
     if (d.ctrl[C_HASH_NR] * 2ull >= c->hcap_nr / 2) c->want_nr = c->hcap_nr * 4;
     if (c->want_dd == c->hcap_dd && c->want_nr == c->hcap_nr) { c->want_dd *= 4; c->want_nr *= 4; }
   } else if (out->status == MPSF_OK) {
-    c->want_dd = next_pow2(std::max<uint64_t>(1ull << 16, 4ull * d.ctrl[C_HASH_DD]));
-    c->want_nr = next_pow2(std::max<uint64_t>(1ull << 16, 4ull * d.ctrl[C_HASH_NR]));
+    c->want_dd = next_pow2(std::max<uint64_t>(1ull << 16, kHashSlack * d.ctrl[C_HASH_DD]));
+    c->want_nr = next_pow2(std::max<uint64_t>(1ull << 16, kHashSlack * d.ctrl[C_HASH_NR]));
   }
 }
 
