@@ -37,6 +37,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "mpsf_kernels.h"
 
@@ -523,6 +524,602 @@ __global__ void __launch_bounds__(CB) k_fold_place(uint32_t S, uint32_t live_bou
   }
 }
 
+// ---- bucketed fold (id spaces up to BK_MAX * BK_IDS) -------------------------------------
+// One consume-order pass scatters the live snapshots into buckets of 256 consecutive request
+// ids (stable: a bucket holds its snapshots in consume order), as 16-B records {snapshot index,
+// id & 255 | done << 31, lengths} plus their 8-B source offsets.  Each bucket is then cut into
+// chunks of 8192 records that are independent of each other:
+//   k_fb_count    consume-order tiles of 4096: per-tile bucket counts, exact per-tile delta
+//                 sums (blocks, tokens), rejected ids; clears the head bitmap
+//   k_fb_scan     per-bucket prefix over the tiles; the tiles' source offsets
+//   k_fb_scatter  per-warp bucket counters, ballot-matched ranks (stable), the tile staged in
+//                 bucket order in shared memory and written out as coalesced runs; block 0
+//                 publishes the bucket and chunk bases
+//   k_fb_stats    per chunk and id: delta sums, first / last snapshot, sticky done
+//   k_fb_ids      per id: the chunk sums become the chunk's prefix inside the request, first /
+//                 last / done / total over the chunks; the head bit of its first snapshot
+//   k_fold_bitcnt + k_fold_scan + k_fb_rank: first-appearance ranks, order, done, progress
+//   k_fb_csr      chained scan of the per-rank delta sums: the CSR offsets
+//   k_fb_place    per chunk: per-warp per-id running sums give each record its place among its
+//                 request's deltas (stable); the chunk's deltas are gathered into shared memory
+//                 grouped by request and written out as one contiguous run per request
+constexpr uint32_t BK_SH = 8, BK_IDS = 1u << BK_SH;   // request ids per bucket
+constexpr uint32_t BK_MAX = NB_MAX;                   // buckets (one ranking pass of <= 9 bits)
+constexpr uint32_t BT = 4096;                         // consume-order tile of the scatter
+constexpr int BTN = 512, BT_WARPS = BTN / 32;
+constexpr uint32_t BT_WITEMS = BT / BT_WARPS;         // 256 consecutive snapshots per warp
+constexpr int BT_ROUNDS = BT_WITEMS / 32;
+constexpr uint32_t CH = 4096;                         // records per bucket chunk
+constexpr int SCN = 1024, SC_ROUNDS = CH / SCN;       // k_fb_stats: 4 records per thread
+constexpr int CHN = 512, CH_WARPS = CHN / 32;         // k_fb_place: two CTAs per SM
+constexpr int CH_ROUNDS = CH / CHN;                   // 8 records per thread
+constexpr uint32_t STAGE_CAP = 14336;                 // delta words staged per chunk
+constexpr uint32_t CSR_TILE = 8192;
+
+struct FoldDevB {           // zeroed by one memset per fold
+  unsigned long long n_requests, n_blocks, n_tokens;
+  uint32_t err_enc;         // max of ~i over rejected snapshots (0: none)
+  uint32_t overrun;
+  uint32_t ticket;
+  uint32_t pad;
+  uint32_t flag[BK_MAX * BK_IDS / CSR_TILE];
+  unsigned long long incl[BK_MAX * BK_IDS / CSR_TILE];
+};
+
+__global__ void __launch_bounds__(BTN) k_fb_count(uint32_t S, uint32_t R, uint32_t nbk, uint32_t T, uint32_t W,
+                                                  const uint32_t* __restrict__ req, const uint32_t* __restrict__ nblk,
+                                                  const uint32_t* __restrict__ ntok, uint32_t* __restrict__ hist,
+                                                  unsigned long long* __restrict__ tsb,
+                                                  unsigned long long* __restrict__ tst, uint32_t* __restrict__ bitmap,
+                                                  FoldDevB* __restrict__ dev) {
+  __shared__ uint32_t cnt[BK_MAX];
+  __shared__ unsigned long long red[2][BT_WARPS];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (uint32_t d = tid; d < nbk; d += BTN) cnt[d] = 0;
+  const uint32_t wb = blockIdx.x * (BT / 32), we = blockIdx.x + 1 == gridDim.x ? W : wb + BT / 32;
+  for (uint32_t w = wb + tid; w < we; w += BTN) bitmap[w] = 0;
+  __syncthreads();
+  constexpr int IPT = BT / BTN;
+  const uint32_t i0 = blockIdx.x * BT + tid * IPT;
+  uint32_t r[IPT], nb[IPT], nt[IPT];
+  ldb(req, i0, S, r, NO_REQ);
+  ldb(nblk, i0, S, nb, 0u);
+  ldb(ntok, i0, S, nt, 0u);
+  unsigned long long sb = 0, st = 0;
+  uint32_t bad = NO_REQ;
+#pragma unroll
+  for (int u = 0; u < IPT; ++u) {
+    sb += nb[u];
+    st += nt[u];
+    if (r[u] < R) atomicAdd(cnt + (r[u] >> BK_SH), 1u);
+    else if (r[u] != NO_REQ && i0 + u < S) bad = min(bad, i0 + u);
+  }
+  if (bad != NO_REQ) atomicMax(&dev->err_enc, ~bad);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    sb += __shfl_xor_sync(0xFFFFFFFFu, sb, o);
+    st += __shfl_xor_sync(0xFFFFFFFFu, st, o);
+  }
+  if (lane == 0) {
+    red[0][warp] = sb;
+    red[1][warp] = st;
+  }
+  __syncthreads();
+  for (uint32_t d = tid; d < nbk; d += BTN) hist[d * T + blockIdx.x] = cnt[d];
+  if (tid < 2) {
+    unsigned long long s = 0;
+#pragma unroll
+    for (int w = 0; w < BT_WARPS; ++w) s += red[tid][w];
+    (tid ? tst : tsb)[blockIdx.x] = s;
+  }
+}
+
+// blocks [0, nbk): one bucket's row of tile counts -> exclusive prefix, row total; block nbk:
+// the tiles' consume-order delta offsets (exact 64-bit prefixes, packed blocks | tokens << 32;
+// totals that do not fit 32 bits are an overrun)
+__global__ void __launch_bounds__(256) k_fb_scan(uint32_t T, uint32_t nbk, uint32_t* __restrict__ hist,
+                                                 uint32_t* __restrict__ rowtot, const unsigned long long* __restrict__ tsb,
+                                                 const unsigned long long* __restrict__ tst,
+                                                 unsigned long long* __restrict__ tbase, FoldDevB* __restrict__ dev) {
+  __shared__ unsigned long long sw[9];
+  if (blockIdx.x < nbk) {
+    __shared__ uint32_t sw32[9];
+    uint32_t* row = hist + (size_t)blockIdx.x * T;
+    uint32_t carry = 0;
+    for (uint32_t b = 0; b < T; b += 256) {
+      const uint32_t i = b + threadIdx.x;
+      const uint32_t v = i < T ? row[i] : 0u;
+      uint32_t tot;
+      const uint32_t ex = block_excl_scan<uint32_t, 8>(v, sw32, tot);
+      if (i < T) row[i] = carry + ex;
+      carry += tot;
+    }
+    if (threadIdx.x == 0) rowtot[blockIdx.x] = carry;
+    return;
+  }
+  unsigned long long cb = 0, ct = 0;
+  for (uint32_t b = 0; b < T; b += 256) {
+    const uint32_t i = b + threadIdx.x;
+    unsigned long long tb, tt;
+    const unsigned long long eb = block_excl_scan<unsigned long long, 8>(i < T ? tsb[i] : 0ull, sw, tb);
+    const unsigned long long et = block_excl_scan<unsigned long long, 8>(i < T ? tst[i] : 0ull, sw, tt);
+    if (i < T) tbase[i] = (cb + eb) | ((ct + et) << 32);
+    cb += tb;
+    ct += tt;
+  }
+  if (threadIdx.x == 0 && ((cb >> 32) || (ct >> 32))) dev->overrun = 1;
+}
+
+constexpr size_t FB_SCATTER_SMEM = 4 * (BT_WARPS * BK_MAX + 2 * BK_MAX) + 2 * BT + 16 * BT;
+
+__global__ void __launch_bounds__(BTN, 2) k_fb_scatter(uint32_t S, uint32_t R, uint32_t nbk, int db, uint32_t T,
+                                                       const uint32_t* __restrict__ req, const uint32_t* __restrict__ nblk,
+                                                       const uint32_t* __restrict__ ntok, const uint8_t* __restrict__ done,
+                                                       const uint32_t* __restrict__ hist, const uint32_t* __restrict__ rowtot,
+                                                       const unsigned long long* __restrict__ tbase, uint64_t n_blocks_in,
+                                                       uint64_t n_tokens_in, uint4* __restrict__ rec,
+                                                       uint2* __restrict__ src, uint32_t* __restrict__ bbase,
+                                                       uint32_t* __restrict__ cbase, FoldDevB* __restrict__ dev) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  uint32_t* wc = sm;                                    // [BT_WARPS][BK_MAX]
+  uint32_t* tdo = wc + BT_WARPS * BK_MAX;               // tile-local start of each bucket
+  uint32_t* gb = tdo + BK_MAX;                          // global start of this tile's run
+  uint4* stg = reinterpret_cast<uint4*>(gb + BK_MAX);   // the tile in bucket order
+  uint16_t* sd = reinterpret_cast<uint16_t*>(stg + BT); // its bucket
+  __shared__ uint32_t sw[BT_WARPS + 1];
+  __shared__ unsigned long long swl[BT_WARPS + 1];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t tot;
+  const uint32_t rt = tid < nbk ? rowtot[tid] : 0u;
+  const uint32_t dex = block_excl_scan<uint32_t, BT_WARPS>(rt, sw, tot);
+  if (tid < nbk) gb[tid] = dex + hist[tid * T + blockIdx.x];
+  if (blockIdx.x == 0) {   // bucket bases and chunk bases for the per-chunk kernels
+    if (tid < nbk) bbase[tid] = dex;
+    if (tid == 0) bbase[nbk] = tot;
+    uint32_t ctot;
+    const uint32_t cex = block_excl_scan<uint32_t, BT_WARPS>((rt + CH - 1) / CH, sw, ctot);
+    if (tid < nbk) cbase[tid] = cex;
+    if (tid == 0) cbase[nbk] = ctot;
+  }
+  for (uint32_t x = tid; x < BT_WARPS * BK_MAX; x += BTN) wc[x] = 0;
+  const uint32_t w0 = blockIdx.x * BT + warp * BT_WITEMS;
+  uint32_t r[BT_ROUNDS], nb[BT_ROUNDS], nt[BT_ROUNDS], dn = 0;
+#pragma unroll
+  for (int u = 0; u < BT_ROUNDS; ++u) {
+    const uint32_t i = w0 + u * 32 + lane;
+    if (i < S) {
+      r[u] = __ldg(req + i);
+      nb[u] = __ldg(nblk + i);
+      nt[u] = __ldg(ntok + i);
+      dn |= (__ldg(done + i) ? 1u : 0u) << u;
+    } else {
+      r[u] = NO_REQ; nb[u] = 0; nt[u] = 0;
+    }
+  }
+  // consume-order source offsets inside the tile: per-round warp scans, then across the warps
+  unsigned long long pre[BT_ROUNDS], run = 0;
+#pragma unroll
+  for (int u = 0; u < BT_ROUNDS; ++u) {
+    const unsigned long long len = pack_len(nb[u], nt[u]);
+    const unsigned long long inc = warp_incl_scan(len);
+    pre[u] = run + inc - len;
+    run += __shfl_sync(0xFFFFFFFFu, inc, 31);
+  }
+  if (lane == 0) swl[warp] = run;
+  __syncthreads();
+  if (warp == 0) {
+    const unsigned long long w = lane < (uint32_t)BT_WARPS ? swl[lane] : 0ull;
+    const unsigned long long wi = warp_incl_scan(w);
+    if (lane < (uint32_t)BT_WARPS) swl[lane] = wi - w;
+  }
+#pragma unroll
+  for (int u = 0; u < BT_ROUNDS; ++u)
+    if (r[u] < R) atomicAdd(&wc[warp * BK_MAX + (r[u] >> BK_SH)], 1u);
+  __syncthreads();
+  const unsigned long long base = tbase[blockIdx.x] + swl[warp];
+  // tile-local layout: buckets in order, inside a bucket the warps in order
+  uint32_t tc = 0;
+  if (tid < nbk) {
+#pragma unroll
+    for (int w = 0; w < BT_WARPS; ++w) tc += wc[w * BK_MAX + tid];
+  }
+  uint32_t ntl;
+  const uint32_t toff = block_excl_scan<uint32_t, BT_WARPS>(tc, sw, ntl);
+  if (tid < nbk) {
+    tdo[tid] = toff;
+    uint32_t o = toff;
+#pragma unroll
+    for (int w = 0; w < BT_WARPS; ++w) {
+      const uint32_t c = wc[w * BK_MAX + tid];
+      wc[w * BK_MAX + tid] = o;
+      o += c;
+    }
+  }
+  __syncthreads();
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t pos[BT_ROUNDS];
+  bool over = false;
+#pragma unroll
+  for (int u = 0; u < BT_ROUNDS; ++u) {
+    const bool ok = r[u] < R;
+    const uint32_t valid = __ballot_sync(0xFFFFFFFFu, ok);
+    const uint32_t d = ok ? r[u] >> BK_SH : 0u;
+    const uint32_t peers = match_digit(d, db, valid);
+    const uint32_t lr = __popc(peers & lt);
+    pos[u] = 0;
+    if (ok) {
+      const uint32_t p = wc[warp * BK_MAX + d] + lr;
+      pos[u] = p;
+      stg[p] = make_uint4(w0 + u * 32 + lane, (r[u] & (BK_IDS - 1)) | (((dn >> u) & 1u) << 31), nb[u], nt[u]);
+      sd[p] = (uint16_t)d;
+      const unsigned long long s = base + pre[u];
+      over |= (s & 0xFFFFFFFFull) + nb[u] > n_blocks_in || (s >> 32) + nt[u] > n_tokens_in;
+    }
+    __syncwarp();
+    if (ok && lr == 0) wc[warp * BK_MAX + d] += __popc(peers);
+    __syncwarp();
+  }
+  if (over) atomicOr(&dev->overrun, 1u);
+  __syncthreads();
+  for (uint32_t q = tid; q < ntl; q += BTN) {
+    const uint32_t d = sd[q];
+    rec[gb[d] + (q - tdo[d])] = stg[q];
+  }
+  __syncthreads();
+  uint2* stg2 = reinterpret_cast<uint2*>(stg);
+#pragma unroll
+  for (int u = 0; u < BT_ROUNDS; ++u)
+    if (r[u] < R) {
+      const unsigned long long s = base + pre[u];
+      stg2[pos[u]] = make_uint2((uint32_t)s, (uint32_t)(s >> 32));
+    }
+  __syncthreads();
+  for (uint32_t q = tid; q < ntl; q += BTN) {
+    const uint32_t d = sd[q];
+    src[gb[d] + (q - tdo[d])] = stg2[q];
+  }
+}
+
+// L2 residency for the delta gathers of k_fb_place: the payload arrays are prefetched with
+// evict_last while the chunk kernels stream their records with evict_first
+__device__ __forceinline__ void prefetch_l2_last(const void* p) {
+  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
+}
+__device__ __forceinline__ void prefetch_slice(const uint32_t* a, uint64_t n, uint32_t part, uint32_t parts) {
+  const uint64_t lines = (n * 4 + 127) / 128, b = lines * part / parts, e = lines * (part + 1) / parts;
+  for (uint64_t x = b + threadIdx.x; x < e; x += blockDim.x) prefetch_l2_last(reinterpret_cast<const char*>(a) + x * 128);
+}
+__device__ __forceinline__ unsigned long long evict_first_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint4 ld_stream16(const uint4* p, unsigned long long pol) {
+  uint4 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint2 ld_stream8(const uint2* p, unsigned long long pol) {
+  uint2 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+
+// chunk c of the bucket layout: its bucket and record range (scb: chunk bases in shared memory)
+__device__ __forceinline__ bool chunk_of(uint32_t c, uint32_t nbk, const uint32_t* scb,
+                                         const uint32_t* __restrict__ bbase, uint32_t& d, uint32_t& p0,
+                                         uint32_t& p1) {
+  if (c >= scb[nbk]) return false;
+  uint32_t lo = 0;
+  for (uint32_t step = BK_MAX / 2; step; step >>= 1)
+    if (lo + step < nbk && scb[lo + step] <= c) lo += step;
+  d = lo;
+  p0 = __ldg(bbase + d) + (c - scb[d]) * CH;
+  p1 = min(p0 + CH, __ldg(bbase + d + 1));
+  return true;
+}
+
+__global__ void __launch_bounds__(SCN) k_fb_stats(uint32_t nbk, const uint32_t* __restrict__ bbase,
+                                                  const uint32_t* __restrict__ cbase, const uint4* __restrict__ rec,
+                                                  uint4* __restrict__ cstat, const uint32_t* __restrict__ blocks,
+                                                  uint64_t nbin, const uint32_t* __restrict__ tokens, uint64_t ntin) {
+  prefetch_slice(tokens, ntin, blockIdx.x, gridDim.x);
+  prefetch_slice(blocks, nbin, blockIdx.x, gridDim.x);
+  __shared__ uint32_t scb[BK_MAX + 1];
+  __shared__ uint32_t first[BK_IDS], last[BK_IDS], dn[BK_IDS], lb[BK_IDS], lt[BK_IDS];
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t x = tid; x <= nbk; x += SCN) scb[x] = __ldg(cbase + x);
+  if (tid < BK_IDS) {
+    first[tid] = NO_REQ;
+    last[tid] = 0;
+    dn[tid] = 0;
+    lb[tid] = 0;
+    lt[tid] = 0;
+  }
+  __syncthreads();
+  uint32_t d, p0, p1;
+  if (!chunk_of(blockIdx.x, nbk, scb, bbase, d, p0, p1)) return;
+  uint4 x[SC_ROUNDS];
+#pragma unroll
+  for (int u = 0; u < SC_ROUNDS; ++u) {
+    const uint32_t p = p0 + u * SCN + tid;
+    x[u] = p < p1 ? __ldg(rec + p) : make_uint4(0, 0, 0, 0);
+  }
+#pragma unroll
+  for (int u = 0; u < SC_ROUNDS; ++u) {
+    if (p0 + u * SCN + tid < p1) {
+      const uint32_t l = x[u].y & (BK_IDS - 1);
+      atomicMin(first + l, x[u].x);
+      atomicMax(last + l, x[u].x);
+      if (x[u].z) atomicAdd(lb + l, x[u].z);   // (chunk sums fit: the fold's totals are < 2^32)
+      atomicAdd(lt + l, x[u].w);
+      if (x[u].y >> 31) dn[l] = 1;
+    }
+  }
+  __syncthreads();
+  if (tid < BK_IDS)
+    cstat[(size_t)blockIdx.x * BK_IDS + tid] = make_uint4(lb[tid], lt[tid], first[tid] | (dn[tid] << 31), last[tid]);
+}
+
+// per id: the chunk sums become each chunk's prefix inside the request; the totals, first / last
+// snapshot and sticky done; the head bit of the first snapshot
+__global__ void k_fb_ids(uint32_t R, const uint32_t* __restrict__ cbase, uint4* __restrict__ cstat,
+                         uint32_t* __restrict__ first, uint32_t* __restrict__ lastx, uint32_t* __restrict__ rdone,
+                         unsigned long long* __restrict__ lensr, uint32_t* __restrict__ bitmap) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
+    const uint32_t d = r >> BK_SH, l = r & (BK_IDS - 1);
+    const uint32_t c0 = __ldg(cbase + d), c1 = __ldg(cbase + d + 1);
+    uint32_t f = NO_REQ, la = 0, dn = 0;
+    unsigned long long run = 0;
+    for (uint32_t c = c0; c < c1; ++c) {
+      uint4* sp = cstat + (size_t)c * BK_IDS + l;
+      const uint4 s = *sp;
+      if (s.z != NO_REQ) {
+        if (f == NO_REQ) f = s.z & 0x7FFFFFFFu;
+        dn |= s.z >> 31;
+        la = s.w;
+        *reinterpret_cast<uint2*>(sp) = make_uint2((uint32_t)run, (uint32_t)(run >> 32));
+        run += (unsigned long long)s.x | ((unsigned long long)s.y << 32);
+      }
+    }
+    first[r] = f;
+    lastx[r] = la;
+    rdone[r] = dn;
+    lensr[r] = run;
+    if (f != NO_REQ) atomicOr(bitmap + (f >> 5), 1u << (f & 31));
+  }
+}
+
+__global__ void k_fb_rank(uint32_t R, const uint32_t* __restrict__ first, const uint32_t* __restrict__ rdone,
+                          const uint32_t* __restrict__ lastx, const unsigned long long* __restrict__ lensr,
+                          const uint32_t* __restrict__ bitmap, const uint32_t* __restrict__ wloc,
+                          const unsigned long long* __restrict__ cpre, const uint32_t* __restrict__ progress,
+                          uint32_t* __restrict__ rank, uint32_t* __restrict__ order, uint8_t* __restrict__ done_out,
+                          uint32_t* __restrict__ prog_out, unsigned long long* __restrict__ rl) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
+    const uint32_t f = first[r];
+    if (f == NO_REQ) continue;
+    const uint32_t w = f >> 5;
+    const uint32_t k = (uint32_t)cpre[w / CHUNK_WORDS] + wloc[w] + __popc(bitmap[w] & ((1u << (f & 31)) - 1u));
+    rank[r] = k;
+    order[k] = r;
+    done_out[k] = rdone[r] ? 1 : 0;
+    prog_out[k] = __ldg(progress + lastx[r]);
+    rl[k] = lensr[r];
+  }
+}
+
+// scan of the per-rank delta sums over tiles of 8192 ranks (<= 16 tiles, all resident): every
+// tile publishes its total at once, then adds up its predecessors' totals; the CSR offsets and
+// the totals
+__global__ void __launch_bounds__(1024) k_fb_csr(const unsigned long long* __restrict__ rl,
+                                                 unsigned long long* __restrict__ blk_off,
+                                                 unsigned long long* __restrict__ tok_off, FoldDevB* dev) {
+  __shared__ unsigned long long sw[33];
+  __shared__ unsigned long long s_pre;
+  const uint32_t tile = blockIdx.x;
+  const uint32_t n = (uint32_t)*reinterpret_cast<volatile unsigned long long*>(&dev->n_requests);
+  const uint32_t k0 = tile * CSR_TILE;
+  if (k0 >= n) return;
+  constexpr int IPT = CSR_TILE / 1024;
+  const uint32_t kb = k0 + threadIdx.x * IPT;
+  unsigned long long v[IPT], s = 0;
+#pragma unroll
+  for (int u = 0; u < IPT; ++u) {
+    v[u] = kb + u < n ? rl[kb + u] : 0ull;
+    s += v[u];
+  }
+  unsigned long long tot;
+  unsigned long long run = block_excl_scan<unsigned long long, 32>(s, sw, tot);
+  if (threadIdx.x == 0) {
+    *reinterpret_cast<volatile unsigned long long*>(dev->incl + tile) = tot;
+    __threadfence();
+    *reinterpret_cast<volatile uint32_t*>(dev->flag + tile) = 1;
+  }
+  if (threadIdx.x < tile) {   // one lane per predecessor
+    volatile uint32_t* fl = dev->flag + threadIdx.x;
+    while (*fl == 0) {}
+    __threadfence();
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    unsigned long long pre = threadIdx.x < tile ? *reinterpret_cast<volatile unsigned long long*>(dev->incl + threadIdx.x) : 0ull;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) pre += __shfl_xor_sync(0xFFFFFFFFu, pre, o);
+    if (threadIdx.x == 0) s_pre = pre;
+  }
+  __syncthreads();
+  run += s_pre;
+#pragma unroll
+  for (int u = 0; u < IPT; ++u) {
+    const uint32_t k = kb + u;
+    if (k < n) {
+      blk_off[k] = run & 0xFFFFFFFFull;
+      tok_off[k] = run >> 32;
+      run += v[u];
+      if (k == n - 1) {
+        blk_off[n] = run & 0xFFFFFFFFull;
+        tok_off[n] = run >> 32;
+        dev->n_blocks = run & 0xFFFFFFFFull;
+        dev->n_tokens = run >> 32;
+      }
+    }
+  }
+}
+
+constexpr size_t FB_PLACE_SMEM = 8 * (CH_WARPS * BK_IDS + CH_WARPS * 32 + 2 * BK_IDS) + 4 * (2 * (BK_IDS + 1)) +
+                                 4 * (BK_MAX + 1) + 4 * STAGE_CAP;
+
+__device__ __forceinline__ uint32_t seg_of(const uint32_t* lb, uint32_t q) {   // last id starting at or before q
+  uint32_t l = 0;
+#pragma unroll
+  for (uint32_t step = BK_IDS / 2; step; step >>= 1)
+    if (lb[l + step] <= q) l += step;
+  return l;
+}
+
+__global__ void __launch_bounds__(CHN, 2) k_fb_place(uint32_t R, uint32_t nbk, const uint32_t* __restrict__ bbase,
+                                                     const uint32_t* __restrict__ cbase, const uint4* __restrict__ rec,
+                                                     const uint2* __restrict__ src, const uint4* __restrict__ cstat,
+                                                     const uint32_t* __restrict__ rank,
+                                                     const unsigned long long* __restrict__ blk_off,
+                                                     const unsigned long long* __restrict__ tok_off,
+                                                     const uint32_t* __restrict__ blocks, uint64_t nbin,
+                                                     const uint32_t* __restrict__ tokens, uint64_t ntin,
+                                                     uint32_t* __restrict__ blocks_out, uint32_t* __restrict__ tokens_out) {
+  extern __shared__ __align__(16) unsigned long long psm64[];
+  unsigned long long* wl = psm64;                       // [CH_WARPS][BK_IDS] per-warp running sums
+  unsigned long long* lbuf = wl + CH_WARPS * BK_IDS;    // [CH_WARPS][32] the round's lengths
+  unsigned long long* curb = lbuf + CH_WARPS * 32;      // [BK_IDS] destination of the id's first block word
+  unsigned long long* curt = curb + BK_IDS;             // [BK_IDS] ... token word
+  uint32_t* lbb = reinterpret_cast<uint32_t*>(curt + BK_IDS);   // [BK_IDS + 1] the id's start in the staged blocks
+  uint32_t* lbt = lbb + BK_IDS + 1;                     // [BK_IDS + 1] ... tokens
+  uint32_t* scb = lbt + BK_IDS + 1;                     // [BK_MAX + 1]
+  uint32_t* stage = scb + BK_MAX + 1;                   // [STAGE_CAP]
+  __shared__ unsigned long long sw[CH_WARPS + 1];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (uint32_t x = tid; x <= nbk; x += CHN) scb[x] = __ldg(cbase + x);
+  __syncthreads();
+  uint32_t d, p0, p1;
+  if (!chunk_of(blockIdx.x, nbk, scb, bbase, d, p0, p1)) return;
+  // the warp's records (256 consecutive), loaded up front; lanes past the chunk get a private id
+  const uint32_t pw = p0 + warp * (CH / CH_WARPS);
+  const unsigned long long pol = evict_first_policy();
+  uint32_t lv[CH_ROUNDS];
+  unsigned long long len[CH_ROUNDS];
+#pragma unroll
+  for (int u = 0; u < CH_ROUNDS; ++u) {
+    const uint32_t p = pw + u * 32 + lane;
+    if (p < p1) {
+      const uint4 x = ld_stream16(rec + p, pol);
+      lv[u] = x.y & (BK_IDS - 1);
+      len[u] = pack_len(x.z, x.w);
+    } else {
+      lv[u] = BK_IDS + lane;
+      len[u] = 0;
+    }
+  }
+  for (uint32_t x = tid; x < CH_WARPS * BK_IDS; x += CHN) wl[x] = 0;
+  if (tid < BK_IDS) {
+    const uint32_t r = d * BK_IDS + tid;
+    unsigned long long cb = 0, ct = 0;
+    if (r < R) {
+      const uint4 s = __ldg(cstat + (size_t)blockIdx.x * BK_IDS + tid);
+      if (s.z != NO_REQ) {
+        const uint32_t k = __ldg(rank + r);
+        cb = __ldg(blk_off + k) + s.x;
+        ct = __ldg(tok_off + k) + s.y;
+      }
+    }
+    curb[tid] = cb;
+    curt[tid] = ct;
+  }
+  __syncthreads();
+  // per warp, rounds of 32 records in order: the record's offset among its request's deltas
+  // inside the warp (earlier rounds + lower peer lanes)
+  const uint32_t lt = (1u << lane) - 1u;
+  unsigned long long wpre[CH_ROUNDS];
+#pragma unroll
+  for (int u = 0; u < CH_ROUNDS; ++u) {
+    const bool ok = lv[u] < BK_IDS;
+    const uint32_t peers = __match_any_sync(0xFFFFFFFFu, lv[u]);
+    lbuf[warp * 32 + lane] = len[u];
+    __syncwarp();
+    const unsigned long long old = ok ? wl[warp * BK_IDS + lv[u]] : 0ull;
+    unsigned long long pre = 0;
+    for (uint32_t m = peers & lt; m; m &= m - 1) pre += lbuf[warp * 32 + __ffs(m) - 1];
+    wpre[u] = old + pre;
+    __syncwarp();
+    if (ok && (peers >> lane) == 1u) wl[warp * BK_IDS + lv[u]] = old + pre + len[u];
+    __syncwarp();
+  }
+  __syncthreads();
+  // across warps: exclusive per id; the chunk's ids grouped in id order in the staging area
+  unsigned long long idt = 0;
+  if (tid < BK_IDS) {
+#pragma unroll
+    for (int w = 0; w < CH_WARPS; ++w) {
+      const unsigned long long t = wl[w * BK_IDS + tid];
+      wl[w * BK_IDS + tid] = idt;
+      idt += t;
+    }
+  }
+  unsigned long long ctot;
+  const unsigned long long lb = block_excl_scan<unsigned long long, CH_WARPS>(idt, sw, ctot);
+  if (tid < BK_IDS) {
+    lbb[tid] = (uint32_t)lb;
+    lbt[tid] = (uint32_t)(lb >> 32);
+  }
+  if (tid == 0) {
+    lbb[BK_IDS] = (uint32_t)ctot;
+    lbt[BK_IDS] = (uint32_t)(ctot >> 32);
+  }
+  __syncthreads();
+  const uint32_t totb = (uint32_t)ctot, tott = (uint32_t)(ctot >> 32);
+  const bool staged = (unsigned long long)totb + tott <= STAGE_CAP;
+  uint32_t* stok = stage + totb;
+#pragma unroll
+  for (int u = 0; u < CH_ROUNDS; ++u) {
+    const uint32_t l = lv[u];
+    if (l >= BK_IDS) continue;
+    const uint2 s = ld_stream8(src + pw + u * 32 + lane, pol);
+    const unsigned long long o = wl[warp * BK_IDS + l] + wpre[u];   // offset inside the id's group
+    const uint32_t nb = (uint32_t)len[u], nt = (uint32_t)(len[u] >> 32);
+    if (staged) {
+      uint32_t* bd = stage + lbb[l] + (uint32_t)o;
+      uint32_t* td = stok + lbt[l] + (uint32_t)(o >> 32);
+#pragma unroll
+      for (uint32_t j = 0; j < 4; ++j)   // the common short deltas: independent loads
+        if (j < nt && s.y + j < ntin) td[j] = __ldg(tokens + s.y + j);
+      if (nb && s.x < nbin) bd[0] = __ldg(blocks + s.x);
+      for (uint32_t j = 4; j < nt; ++j)
+        if (s.y + j < ntin) td[j] = __ldg(tokens + s.y + j);
+      for (uint32_t j = 1; j < nb; ++j)
+        if (s.x + j < nbin) bd[j] = __ldg(blocks + s.x + j);
+    } else {   // too many deltas to stage: straight to the destination
+      const unsigned long long db0 = curb[l] + (uint32_t)o, dt0 = curt[l] + (uint32_t)(o >> 32);
+      for (uint32_t j = 0; j < nb; ++j)
+        if (s.x + j < nbin && db0 + j < nbin) blocks_out[db0 + j] = __ldg(blocks + s.x + j);
+      for (uint32_t j = 0; j < nt; ++j)
+        if (s.y + j < ntin && dt0 + j < ntin) tokens_out[dt0 + j] = __ldg(tokens + s.y + j);
+    }
+  }
+  if (!staged) return;
+  __syncthreads();
+  // one contiguous destination run per request
+  for (uint32_t q = tid; q < totb; q += CHN) {
+    const uint32_t l = seg_of(lbb, q);
+    const unsigned long long o = curb[l] + (q - lbb[l]);
+    if (o < nbin) blocks_out[o] = stage[q];
+  }
+  for (uint32_t q = tid; q < tott; q += CHN) {
+    const uint32_t l = seg_of(lbt, q);
+    const unsigned long long o = curt[l] + (q - lbt[l]);
+    if (o < ntin) tokens_out[o] = stok[q];
+  }
+}
+
 static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 static int key_bits(uint32_t live_bound) {   // bits for keys in [0, live_bound]
@@ -533,8 +1130,8 @@ static int key_bits(uint32_t live_bound) {   // bits for keys in [0, live_bound]
 
 static uint32_t tiles(uint64_t S) { return (uint32_t)((S + FTILE - 1) / FTILE); }
 
-// scratch layout for S snapshots and R request ids
-size_t fold_scratch_bytes(uint64_t S, uint64_t R) {
+// scratch layout for S snapshots and R request ids (the larger of the two paths)
+static size_t radix_scratch_bytes(uint64_t S, uint64_t R) {
   const uint64_t T = tiles(S), W = S / 32 + 1, C = (W + CHUNK_WORDS - 1) / CHUNK_WORDS;
   size_t o = al256(64) + al256(4 * R) * 3;                 // dev, first, rdone, rank
   o += al256(4 * W) * 2 + al256(8 * C) * 2;                // bitmap, wloc, chunk counts / prefix
@@ -543,6 +1140,26 @@ size_t fold_scratch_bytes(uint64_t S, uint64_t R) {
   o += al256(16 * S) * 2;                                  // meta in consume order, in fold order
   o += al256(4ull * NB_MAX * T) + al256(4 * NB_MAX);       // hist, rowtot
   return o + 256;
+}
+
+static bool bucketed(uint64_t R) { return R <= (uint64_t)BK_MAX * BK_IDS; }
+static uint32_t n_buckets(uint64_t R) { return (uint32_t)((R + BK_IDS - 1) / BK_IDS); }
+static uint32_t max_chunks(uint64_t S, uint64_t R) { return (uint32_t)((S + CH - 1) / CH + n_buckets(R)); }
+
+static size_t bucket_scratch_bytes(uint64_t S, uint64_t R) {
+  const uint64_t T = (S + BT - 1) / BT, W = S / 32 + 1, C = (W + CHUNK_WORDS - 1) / CHUNK_WORDS, NB = n_buckets(R);
+  size_t o = al256(sizeof(FoldDevB)) + al256(4 * R) * 4 + al256(8 * R) * 2;   // dev; first, rdone, rank, last; lens, rl
+  o += al256(4 * W) * 2 + al256(8 * C) * 2;                // bitmap, wloc, chunk counts / prefix
+  o += al256(8 * T) * 3;                                   // tile delta sums, source bases
+  o += al256(4 * NB * T) + al256(4 * NB) + al256(4 * (NB + 1)) * 2;   // hist, rowtot, bucket / chunk bases
+  o += al256(16 * S) + al256(8 * S);                       // records, source offsets
+  o += al256(16ull * BK_IDS * max_chunks(S, R));           // per-chunk id stats
+  return o + 256;
+}
+
+size_t fold_scratch_bytes(uint64_t S, uint64_t R) {
+  const size_t a = radix_scratch_bytes(S, R);
+  return bucketed(R) ? std::max(a, bucket_scratch_bytes(S, R)) : a;
 }
 
 static int sms() {
@@ -555,12 +1172,102 @@ static int sms() {
   return n;
 }
 
+// MPSF_FOLD_RADIX=1 forces the radix path at any id space (tests and A/Bs)
+static bool force_radix() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MPSF_FOLD_RADIX");
+    v = e && e[0] == '1' ? 1 : 0;
+  }
+  return v == 1;
+}
+
+static int launch_fold_bucket(uint8_t* scratch, uint32_t S, uint32_t R, const uint32_t* req, const uint32_t* nblk,
+                              const uint32_t* ntok, const uint32_t* progress, const uint8_t* done,
+                              const uint32_t* blocks, uint64_t n_blocks_in, const uint32_t* tokens,
+                              uint64_t n_tokens_in, uint32_t* order, uint64_t* blk_off, uint32_t* blocks_out,
+                              uint64_t* tok_off, uint32_t* tokens_out, uint32_t* prog_out, uint8_t* done_out,
+                              FoldTotals* tot, cudaStream_t st, const Marker& mk) {
+  const uint32_t T = (S + BT - 1) / BT, W = S / 32 + 1, C = (W + CHUNK_WORDS - 1) / CHUNK_WORDS, NB = n_buckets(R);
+  const uint32_t NC = max_chunks(S, R);
+  uint8_t* p = scratch;
+  auto take = [&](size_t bytes) { uint8_t* r = p; p += al256(bytes); return r; };
+  auto u32 = [&](size_t n) { return reinterpret_cast<uint32_t*>(take(4 * n)); };
+  auto u64 = [&](size_t n) { return reinterpret_cast<unsigned long long*>(take(8 * n)); };
+  FoldDevB* dev = reinterpret_cast<FoldDevB*>(take(sizeof(FoldDevB)));
+  uint32_t *first = u32(R), *rdone = u32(R), *rank = u32(R), *lastx = u32(R);
+  unsigned long long *lensr = u64(R), *rl = u64(R);
+  uint32_t *bitmap = u32(W), *wloc = u32(W);
+  unsigned long long *ccount = u64(C), *cpre = u64(C);
+  unsigned long long *tsb = u64(T), *tst = u64(T), *tbase = u64(T);
+  uint32_t *hist = u32((size_t)NB * T), *rowtot = u32(NB), *bbase = u32(NB + 1), *cbase = u32(NB + 1);
+  uint4* rec = reinterpret_cast<uint4*>(take(16ull * S));
+  uint2* src = reinterpret_cast<uint2*>(take(8ull * S));
+  uint4* cstat = reinterpret_cast<uint4*>(take(16ull * BK_IDS * NC));
+  const uint32_t gR = (uint32_t)std::min<uint64_t>((R + 255) / 256, (uint64_t)sms() * 8);
+  int launches = 0;
+  auto done_launch = [&](const char* name) { mk.mark(name); ++launches; };
+  if (cudaMemsetAsync(dev, 0, sizeof(FoldDevB), st) != cudaSuccess) return -1;
+  k_fb_count<<<T, BTN, 0, st>>>(S, R, NB, T, W, req, nblk, ntok, hist, tsb, tst, bitmap, dev);
+  done_launch("k_fb_count");
+  k_fb_scan<<<NB + 1, 256, 0, st>>>(T, NB, hist, rowtot, tsb, tst, tbase, dev);
+  done_launch("k_fb_scan");
+  if (cudaFuncSetAttribute(k_fb_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FB_SCATTER_SMEM) !=
+          cudaSuccess ||
+      cudaFuncSetAttribute(k_fb_place, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FB_PLACE_SMEM) != cudaSuccess)
+    return -1;
+  const int db = NB > 1 ? key_bits(NB - 1) : 1;
+  k_fb_scatter<<<T, BTN, FB_SCATTER_SMEM, st>>>(S, R, NB, db, T, req, nblk, ntok, done, hist, rowtot, tbase,
+                                                n_blocks_in, n_tokens_in, rec, src, bbase, cbase, dev);
+  done_launch("k_fb_scatter");
+  k_fb_stats<<<NC, SCN, 0, st>>>(NB, bbase, cbase, rec, cstat, blocks, n_blocks_in, tokens, n_tokens_in);
+  done_launch("k_fb_stats");
+  k_fb_ids<<<gR, 256, 0, st>>>(R, cbase, cstat, first, lastx, rdone, lensr, bitmap);
+  done_launch("k_fb_ids");
+  k_fold_bitcnt<<<C, CHUNK_WORDS, 0, st>>>(W, bitmap, wloc, ccount);
+  done_launch("k_fold_bitcnt");
+  k_fold_scan<<<1, 1024, 0, st>>>(ccount, cpre, C, &dev->n_requests, nullptr, nullptr, 0);
+  done_launch("k_fold_scan");
+  k_fb_rank<<<gR, 256, 0, st>>>(R, first, rdone, lastx, lensr, bitmap, wloc, cpre, progress, rank, order, done_out,
+                                prog_out, rl);
+  done_launch("k_fb_rank");
+  k_fb_csr<<<(R + CSR_TILE - 1) / CSR_TILE, 1024, 0, st>>>(rl, reinterpret_cast<unsigned long long*>(blk_off),
+                                                           reinterpret_cast<unsigned long long*>(tok_off), dev);
+  done_launch("k_fb_csr");
+  k_fb_place<<<NC, CHN, FB_PLACE_SMEM, st>>>(R, NB, bbase, cbase, rec, src, cstat, rank,
+                                             reinterpret_cast<const unsigned long long*>(blk_off),
+                                             reinterpret_cast<const unsigned long long*>(tok_off), blocks, n_blocks_in,
+                                             tokens, n_tokens_in, blocks_out, tokens_out);
+  done_launch("k_fb_place");
+  FoldDevB h{};
+  if (cudaMemcpyAsync(&h, dev, 40, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return -1;
+  if (!h.n_requests) {   // no live request: the CSR is the single zero offset
+    const unsigned long long z = 0;
+    if (cudaMemcpyAsync(blk_off, &z, 8, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaMemcpyAsync(tok_off, &z, 8, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      return -1;
+  }
+  tot->n_requests = h.n_requests;
+  tot->n_blocks = h.n_blocks;
+  tot->n_tokens = h.n_tokens;
+  tot->error_index = h.err_enc ? (uint64_t)(uint32_t)~h.err_enc : ~0ull;
+  tot->overrun = h.overrun;
+  tot->launches = (uint32_t)launches;
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
 int launch_fold(uint8_t* scratch, size_t scratch_bytes, uint32_t S, uint32_t R, const uint32_t* req,
                 const uint32_t* nblk, const uint32_t* ntok, const uint32_t* progress, const uint8_t* done,
                 const uint32_t* blocks, uint64_t n_blocks_in, const uint32_t* tokens, uint64_t n_tokens_in,
                 uint32_t* order, uint64_t* blk_off, uint32_t* blocks_out, uint64_t* tok_off, uint32_t* tokens_out,
                 uint32_t* prog_out, uint8_t* done_out, FoldTotals* tot, cudaStream_t st, const Marker& mk) {
   if (scratch_bytes < fold_scratch_bytes(S, R)) return -1;
+  if (bucketed(R) && !force_radix())
+    return launch_fold_bucket(scratch, S, R, req, nblk, ntok, progress, done, blocks, n_blocks_in, tokens, n_tokens_in,
+                              order, blk_off, blocks_out, tok_off, tokens_out, prog_out, done_out, tot, st, mk);
   const uint32_t T = tiles(S), W = S / 32 + 1, C = (W + CHUNK_WORDS - 1) / CHUNK_WORDS;
   uint8_t* p = scratch;
   auto take = [&](size_t bytes) { uint8_t* r = p; p += al256(bytes); return r; };
