@@ -98,6 +98,29 @@ __device__ __forceinline__ T block_excl_scan(T v, T* sw, T& total) {
   return ex;
 }
 
+// Programmatic dependent launch for the bucketed chain: each kernel may be scheduled while its
+// predecessor drains, and waits (griddepcontrol.wait) before reading anything it produced; a
+// no-op when launched without the attribute (the radix path, kv_reserve).
+__device__ __forceinline__ void fold_pdl() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 __global__ void k_fold_init(uint32_t R, uint32_t W, uint32_t* __restrict__ first, uint32_t* __restrict__ rdone,
                             uint32_t* __restrict__ bitmap, FoldDev* __restrict__ dev) {
   const uint32_t n = R > W ? R : W;
@@ -184,6 +207,7 @@ __global__ void k_fold_bits(uint32_t R, const uint32_t* __restrict__ first, uint
 __global__ void __launch_bounds__(CHUNK_WORDS) k_fold_bitcnt(uint32_t W, const uint32_t* __restrict__ bitmap,
                                                              uint32_t* __restrict__ wloc,
                                                              unsigned long long* __restrict__ ccount) {
+  fold_pdl();
   __shared__ uint32_t sw[CHUNK_WORDS / 32 + 1];
   const uint32_t w = blockIdx.x * CHUNK_WORDS + threadIdx.x;
   const uint32_t c = w < W ? __popc(bitmap[w]) : 0u;
@@ -222,6 +246,7 @@ __global__ void __launch_bounds__(1024) k_fold_scan(const unsigned long long* __
                                                     uint32_t na, unsigned long long* a_total,
                                                     const unsigned long long* __restrict__ b, unsigned long long* __restrict__ bo,
                                                     uint32_t nb) {
+  fold_pdl();
   if (blockIdx.x == 0) scan_small(a, ao, na, a_total);
   else scan_small(b, bo, nb, nullptr);
 }
@@ -536,10 +561,10 @@ __global__ void __launch_bounds__(CB) k_fold_place(uint32_t S, uint32_t live_bou
 //                 bucket order in shared memory and written out as coalesced runs; block 0
 //                 publishes the bucket and chunk bases
 //   k_fb_stats    per chunk and id: delta sums, first / last snapshot, sticky done
-//   k_fb_ids      per id: the chunk sums become the chunk's prefix inside the request, first /
-//                 last / done / total over the chunks; the head bit of its first snapshot
-//   k_fold_bitcnt + k_fold_scan + k_fb_rank: first-appearance ranks, order, done, progress
-//   k_fb_csr      chained scan of the per-rank delta sums: the CSR offsets
+//   k_fb_mid      one cooperative kernel, grid barriers between its phases: per id, the chunk
+//                 sums become each chunk's prefix inside the request, first / last / done /
+//                 totals, the head bit of the first snapshot; the head-bitmap prefix; the
+//                 first-appearance ranks, order, done, progress; the CSR offsets
 //   k_fb_place    per chunk: per-warp per-id running sums give each record its place among its
 //                 request's deltas (stable); the chunk's deltas are gathered into shared memory
 //                 grouped by request and written out as one contiguous run per request
@@ -560,7 +585,7 @@ struct FoldDevB {           // zeroed by one memset per fold
   unsigned long long n_requests, n_blocks, n_tokens;
   uint32_t err_enc;         // max of ~i over rejected snapshots (0: none)
   uint32_t overrun;
-  uint32_t ticket;
+  uint32_t barrier;         // k_fb_mid's grid barrier count
   uint32_t pad;
   uint32_t flag[BK_MAX * BK_IDS / CSR_TILE];
   unsigned long long incl[BK_MAX * BK_IDS / CSR_TILE];
@@ -621,6 +646,7 @@ __global__ void __launch_bounds__(256) k_fb_scan(uint32_t T, uint32_t nbk, uint3
                                                  uint32_t* __restrict__ rowtot, const unsigned long long* __restrict__ tsb,
                                                  const unsigned long long* __restrict__ tst,
                                                  unsigned long long* __restrict__ tbase, FoldDevB* __restrict__ dev) {
+  fold_pdl();
   __shared__ unsigned long long sw[9];
   if (blockIdx.x < nbk) {
     __shared__ uint32_t sw32[9];
@@ -660,6 +686,7 @@ __global__ void __launch_bounds__(BTN, 2) k_fb_scatter(uint32_t S, uint32_t R, u
                                                        uint64_t n_tokens_in, uint4* __restrict__ rec,
                                                        uint2* __restrict__ src, uint32_t* __restrict__ bbase,
                                                        uint32_t* __restrict__ cbase, FoldDevB* __restrict__ dev) {
+  fold_pdl();
   extern __shared__ __align__(16) uint32_t sm[];
   uint32_t* wc = sm;                                    // [BT_WARPS][BK_MAX]
   uint32_t* tdo = wc + BT_WARPS * BK_MAX;               // tile-local start of each bucket
@@ -824,6 +851,7 @@ __global__ void __launch_bounds__(SCN) k_fb_stats(uint32_t nbk, const uint32_t* 
                                                   const uint32_t* __restrict__ cbase, const uint4* __restrict__ rec,
                                                   uint4* __restrict__ cstat, const uint32_t* __restrict__ blocks,
                                                   uint64_t nbin, const uint32_t* __restrict__ tokens, uint64_t ntin) {
+  fold_pdl();
   prefetch_slice(tokens, ntin, blockIdx.x, gridDim.x);
   prefetch_slice(blocks, nbin, blockIdx.x, gridDim.x);
   __shared__ uint32_t scb[BK_MAX + 1];
@@ -862,25 +890,58 @@ __global__ void __launch_bounds__(SCN) k_fb_stats(uint32_t nbk, const uint32_t* 
     cstat[(size_t)blockIdx.x * BK_IDS + tid] = make_uint4(lb[tid], lt[tid], first[tid] | (dn[tid] << 31), last[tid]);
 }
 
-// per id: the chunk sums become each chunk's prefix inside the request; the totals, first / last
-// snapshot and sticky done; the head bit of the first snapshot
-__global__ void k_fb_ids(uint32_t R, const uint32_t* __restrict__ cbase, uint4* __restrict__ cstat,
-                         uint32_t* __restrict__ first, uint32_t* __restrict__ lastx, uint32_t* __restrict__ rdone,
-                         unsigned long long* __restrict__ lensr, uint32_t* __restrict__ bitmap) {
-  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
+
+
+
+// The id / rank / CSR steps between the chunk statistics and the placement, as one cooperative
+// kernel (one CTA per SM, grid-wide barriers between the phases) instead of five dependent
+// launches: per id, chunk prefixes, totals and the head bit | per bitmap chunk, a warp's word
+// prefixes | the chunk prefix (CTA 0) | ranks, order, done, progress, per-rank sums | per
+// 8192-rank tile totals, then each tile's offsets after its predecessors' totals.
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int target = (gen + 1) * gridDim.x;
+    __threadfence();
+    atomicAdd(bar, 1u);
+    while (*reinterpret_cast<volatile unsigned int*>(bar) < target) {}
+    __threadfence();
+  }
+  ++gen;
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(1024, 1) k_fb_mid(uint32_t R, uint32_t W, uint32_t C, const uint32_t* __restrict__ cbase,
+                                                    uint4* __restrict__ cstat, uint32_t* __restrict__ first,
+                                                    uint32_t* __restrict__ lastx, uint32_t* __restrict__ rdone,
+                                                    unsigned long long* __restrict__ lensr, uint32_t* __restrict__ bitmap,
+                                                    uint32_t* __restrict__ wloc, unsigned long long* __restrict__ ccount,
+                                                    unsigned long long* __restrict__ cpre,
+                                                    const uint32_t* __restrict__ progress, uint32_t* __restrict__ rank,
+                                                    uint32_t* __restrict__ order, uint8_t* __restrict__ done_out,
+                                                    uint32_t* __restrict__ prog_out, unsigned long long* __restrict__ rl,
+                                                    unsigned long long* __restrict__ blk_off,
+                                                    unsigned long long* __restrict__ tok_off, FoldDevB* dev) {
+  fold_pdl();
+  __shared__ unsigned long long sw[33];
+  unsigned int gen = 0;
+  unsigned int* bar = &dev->barrier;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, gtid = blockIdx.x * 1024 + tid, gthreads = gridDim.x * 1024;
+  // ids
+  for (uint32_t r = gtid; r < R; r += gthreads) {
     const uint32_t d = r >> BK_SH, l = r & (BK_IDS - 1);
     const uint32_t c0 = __ldg(cbase + d), c1 = __ldg(cbase + d + 1);
     uint32_t f = NO_REQ, la = 0, dn = 0;
     unsigned long long run = 0;
     for (uint32_t c = c0; c < c1; ++c) {
       uint4* sp = cstat + (size_t)c * BK_IDS + l;
-      const uint4 s = *sp;
-      if (s.z != NO_REQ) {
-        if (f == NO_REQ) f = s.z & 0x7FFFFFFFu;
-        dn |= s.z >> 31;
-        la = s.w;
+      const uint4 sv = *sp;
+      if (sv.z != NO_REQ) {
+        if (f == NO_REQ) f = sv.z & 0x7FFFFFFFu;
+        dn |= sv.z >> 31;
+        la = sv.w;
         *reinterpret_cast<uint2*>(sp) = make_uint2((uint32_t)run, (uint32_t)(run >> 32));
-        run += (unsigned long long)s.x | ((unsigned long long)s.y << 32);
+        run += (unsigned long long)sv.x | ((unsigned long long)sv.y << 32);
       }
     }
     first[r] = f;
@@ -889,15 +950,31 @@ __global__ void k_fb_ids(uint32_t R, const uint32_t* __restrict__ cbase, uint4* 
     lensr[r] = run;
     if (f != NO_REQ) atomicOr(bitmap + (f >> 5), 1u << (f & 31));
   }
-}
-
-__global__ void k_fb_rank(uint32_t R, const uint32_t* __restrict__ first, const uint32_t* __restrict__ rdone,
-                          const uint32_t* __restrict__ lastx, const unsigned long long* __restrict__ lensr,
-                          const uint32_t* __restrict__ bitmap, const uint32_t* __restrict__ wloc,
-                          const unsigned long long* __restrict__ cpre, const uint32_t* __restrict__ progress,
-                          uint32_t* __restrict__ rank, uint32_t* __restrict__ order, uint8_t* __restrict__ done_out,
-                          uint32_t* __restrict__ prog_out, unsigned long long* __restrict__ rl) {
-  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
+  grid_barrier(bar, gen);
+  // bitmap chunks: a warp each
+  for (uint32_t c = gtid >> 5; c < C; c += gthreads >> 5) {
+    constexpr int WPL = CHUNK_WORDS / 32;
+    const uint32_t w0 = c * CHUNK_WORDS + lane * WPL;
+    uint32_t cnt[WPL], t = 0;
+#pragma unroll
+    for (int u = 0; u < WPL; ++u) {
+      cnt[u] = w0 + u < W ? __popc(bitmap[w0 + u]) : 0u;
+      t += cnt[u];
+    }
+    const uint32_t inc = warp_incl_scan(t);
+    uint32_t ex = inc - t;
+#pragma unroll
+    for (int u = 0; u < WPL; ++u) {
+      if (w0 + u < W) wloc[w0 + u] = ex;
+      ex += cnt[u];
+    }
+    if (lane == 31) ccount[c] = inc;
+  }
+  grid_barrier(bar, gen);
+  if (blockIdx.x == 0) scan_small(ccount, cpre, C, &dev->n_requests);
+  grid_barrier(bar, gen);
+  const uint32_t n = (uint32_t)*reinterpret_cast<volatile unsigned long long*>(&dev->n_requests);
+  for (uint32_t r = gtid; r < R; r += gthreads) {
     const uint32_t f = first[r];
     if (f == NO_REQ) continue;
     const uint32_t w = f >> 5;
@@ -908,61 +985,46 @@ __global__ void k_fb_rank(uint32_t R, const uint32_t* __restrict__ first, const 
     prog_out[k] = __ldg(progress + lastx[r]);
     rl[k] = lensr[r];
   }
-}
-
-// scan of the per-rank delta sums over tiles of 8192 ranks (<= 16 tiles, all resident): every
-// tile publishes its total at once, then adds up its predecessors' totals; the CSR offsets and
-// the totals
-__global__ void __launch_bounds__(1024) k_fb_csr(const unsigned long long* __restrict__ rl,
-                                                 unsigned long long* __restrict__ blk_off,
-                                                 unsigned long long* __restrict__ tok_off, FoldDevB* dev) {
-  __shared__ unsigned long long sw[33];
-  __shared__ unsigned long long s_pre;
-  const uint32_t tile = blockIdx.x;
-  const uint32_t n = (uint32_t)*reinterpret_cast<volatile unsigned long long*>(&dev->n_requests);
-  const uint32_t k0 = tile * CSR_TILE;
-  if (k0 >= n) return;
+  grid_barrier(bar, gen);
+  // CSR over ranks: tiles of 8192 (CTA t takes tile t), totals published, then offsets
   constexpr int IPT = CSR_TILE / 1024;
-  const uint32_t kb = k0 + threadIdx.x * IPT;
-  unsigned long long v[IPT], s = 0;
+  const uint32_t ntile = (n + CSR_TILE - 1) / CSR_TILE;
+  unsigned long long v[IPT], run = 0, tot = 0;
+  const uint32_t kb = blockIdx.x * CSR_TILE + tid * IPT;
+  const bool mine = blockIdx.x < ntile;
+  if (mine) {
+    unsigned long long s = 0;
 #pragma unroll
-  for (int u = 0; u < IPT; ++u) {
-    v[u] = kb + u < n ? rl[kb + u] : 0ull;
-    s += v[u];
+    for (int u = 0; u < IPT; ++u) {
+      v[u] = kb + u < n ? rl[kb + u] : 0ull;
+      s += v[u];
+    }
+    run = block_excl_scan<unsigned long long, 32>(s, sw, tot);
+    if (tid == 0) dev->incl[blockIdx.x] = tot;
   }
-  unsigned long long tot;
-  unsigned long long run = block_excl_scan<unsigned long long, 32>(s, sw, tot);
-  if (threadIdx.x == 0) {
-    *reinterpret_cast<volatile unsigned long long*>(dev->incl + tile) = tot;
-    __threadfence();
-    *reinterpret_cast<volatile uint32_t*>(dev->flag + tile) = 1;
-  }
-  if (threadIdx.x < tile) {   // one lane per predecessor
-    volatile uint32_t* fl = dev->flag + threadIdx.x;
-    while (*fl == 0) {}
-    __threadfence();
-  }
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    unsigned long long pre = threadIdx.x < tile ? *reinterpret_cast<volatile unsigned long long*>(dev->incl + threadIdx.x) : 0ull;
+  grid_barrier(bar, gen);
+  if (mine) {
+    if (tid < 32) {
+      unsigned long long pre = tid < blockIdx.x ? *reinterpret_cast<volatile unsigned long long*>(dev->incl + tid) : 0ull;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) pre += __shfl_xor_sync(0xFFFFFFFFu, pre, o);
-    if (threadIdx.x == 0) s_pre = pre;
-  }
-  __syncthreads();
-  run += s_pre;
+      for (int o = 16; o; o >>= 1) pre += __shfl_xor_sync(0xFFFFFFFFu, pre, o);
+      if (tid == 0) sw[32] = pre;
+    }
+    __syncthreads();
+    run += sw[32];
 #pragma unroll
-  for (int u = 0; u < IPT; ++u) {
-    const uint32_t k = kb + u;
-    if (k < n) {
-      blk_off[k] = run & 0xFFFFFFFFull;
-      tok_off[k] = run >> 32;
-      run += v[u];
-      if (k == n - 1) {
-        blk_off[n] = run & 0xFFFFFFFFull;
-        tok_off[n] = run >> 32;
-        dev->n_blocks = run & 0xFFFFFFFFull;
-        dev->n_tokens = run >> 32;
+    for (int u = 0; u < IPT; ++u) {
+      const uint32_t k = kb + u;
+      if (k < n) {
+        blk_off[k] = run & 0xFFFFFFFFull;
+        tok_off[k] = run >> 32;
+        run += v[u];
+        if (k == n - 1) {
+          blk_off[n] = run & 0xFFFFFFFFull;
+          tok_off[n] = run >> 32;
+          dev->n_blocks = run & 0xFFFFFFFFull;
+          dev->n_tokens = run >> 32;
+        }
       }
     }
   }
@@ -971,13 +1033,6 @@ __global__ void __launch_bounds__(1024) k_fb_csr(const unsigned long long* __res
 constexpr size_t FB_PLACE_SMEM = 8 * (CH_WARPS * BK_IDS + CH_WARPS * 32 + 2 * BK_IDS) + 4 * (2 * (BK_IDS + 1)) +
                                  4 * (BK_MAX + 1) + 4 * STAGE_CAP;
 
-__device__ __forceinline__ uint32_t seg_of(const uint32_t* lb, uint32_t q) {   // last id starting at or before q
-  uint32_t l = 0;
-#pragma unroll
-  for (uint32_t step = BK_IDS / 2; step; step >>= 1)
-    if (lb[l + step] <= q) l += step;
-  return l;
-}
 
 __global__ void __launch_bounds__(CHN, 2) k_fb_place(uint32_t R, uint32_t nbk, const uint32_t* __restrict__ bbase,
                                                      const uint32_t* __restrict__ cbase, const uint4* __restrict__ rec,
@@ -988,6 +1043,7 @@ __global__ void __launch_bounds__(CHN, 2) k_fb_place(uint32_t R, uint32_t nbk, c
                                                      const uint32_t* __restrict__ blocks, uint64_t nbin,
                                                      const uint32_t* __restrict__ tokens, uint64_t ntin,
                                                      uint32_t* __restrict__ blocks_out, uint32_t* __restrict__ tokens_out) {
+  fold_pdl();
   extern __shared__ __align__(16) unsigned long long psm64[];
   unsigned long long* wl = psm64;                       // [CH_WARPS][BK_IDS] per-warp running sums
   unsigned long long* lbuf = wl + CH_WARPS * BK_IDS;    // [CH_WARPS][32] the round's lengths
@@ -1043,7 +1099,7 @@ __global__ void __launch_bounds__(CHN, 2) k_fb_place(uint32_t R, uint32_t nbk, c
 #pragma unroll
   for (int u = 0; u < CH_ROUNDS; ++u) {
     const bool ok = lv[u] < BK_IDS;
-    const uint32_t peers = __match_any_sync(0xFFFFFFFFu, lv[u]);
+    const uint32_t peers = match_digit(lv[u], BK_SH, __ballot_sync(0xFFFFFFFFu, ok));
     lbuf[warp * 32 + lane] = len[u];
     __syncwarp();
     const unsigned long long old = ok ? wl[warp * BK_IDS + lv[u]] : 0ull;
@@ -1107,16 +1163,14 @@ __global__ void __launch_bounds__(CHN, 2) k_fb_place(uint32_t R, uint32_t nbk, c
   }
   if (!staged) return;
   __syncthreads();
-  // one contiguous destination run per request
-  for (uint32_t q = tid; q < totb; q += CHN) {
-    const uint32_t l = seg_of(lbb, q);
-    const unsigned long long o = curb[l] + (q - lbb[l]);
-    if (o < nbin) blocks_out[o] = stage[q];
-  }
-  for (uint32_t q = tid; q < tott; q += CHN) {
-    const uint32_t l = seg_of(lbt, q);
-    const unsigned long long o = curt[l] + (q - lbt[l]);
-    if (o < ntin) tokens_out[o] = stok[q];
+  // one contiguous destination run per request: a warp per id
+  for (uint32_t l = warp; l < BK_IDS; l += CH_WARPS) {
+    const uint32_t b0 = lbb[l], b1 = lbb[l + 1], t0 = lbt[l], t1 = lbt[l + 1];
+    const unsigned long long ob = curb[l] - b0, ot = curt[l] - t0;
+    for (uint32_t q = b0 + lane; q < b1; q += 32)
+      if (ob + q < nbin) blocks_out[ob + q] = stage[q];
+    for (uint32_t q = t0 + lane; q < t1; q += 32)
+      if (ot + q < ntin) tokens_out[ot + q] = stok[q];
   }
 }
 
@@ -1210,34 +1264,40 @@ static int launch_fold_bucket(uint8_t* scratch, uint32_t S, uint32_t R, const ui
   if (cudaMemsetAsync(dev, 0, sizeof(FoldDevB), st) != cudaSuccess) return -1;
   k_fb_count<<<T, BTN, 0, st>>>(S, R, NB, T, W, req, nblk, ntok, hist, tsb, tst, bitmap, dev);
   done_launch("k_fb_count");
-  k_fb_scan<<<NB + 1, 256, 0, st>>>(T, NB, hist, rowtot, tsb, tst, tbase, dev);
+  launch_pdl(k_fb_scan, NB + 1, 256, 0, st, T, NB, hist, rowtot, tsb, tst, tbase, dev);
   done_launch("k_fb_scan");
   if (cudaFuncSetAttribute(k_fb_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FB_SCATTER_SMEM) !=
           cudaSuccess ||
       cudaFuncSetAttribute(k_fb_place, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FB_PLACE_SMEM) != cudaSuccess)
     return -1;
   const int db = NB > 1 ? key_bits(NB - 1) : 1;
-  k_fb_scatter<<<T, BTN, FB_SCATTER_SMEM, st>>>(S, R, NB, db, T, req, nblk, ntok, done, hist, rowtot, tbase,
-                                                n_blocks_in, n_tokens_in, rec, src, bbase, cbase, dev);
+  launch_pdl(k_fb_scatter, T, BTN, FB_SCATTER_SMEM, st, S, R, NB, db, T, req, nblk, ntok, done, hist, rowtot, tbase,
+             n_blocks_in, n_tokens_in, rec, src, bbase, cbase, dev);
   done_launch("k_fb_scatter");
-  k_fb_stats<<<NC, SCN, 0, st>>>(NB, bbase, cbase, rec, cstat, blocks, n_blocks_in, tokens, n_tokens_in);
+  launch_pdl(k_fb_stats, NC, SCN, 0, st, NB, bbase, cbase, rec, cstat, blocks, n_blocks_in, tokens, n_tokens_in);
   done_launch("k_fb_stats");
-  k_fb_ids<<<gR, 256, 0, st>>>(R, cbase, cstat, first, lastx, rdone, lensr, bitmap);
-  done_launch("k_fb_ids");
-  k_fold_bitcnt<<<C, CHUNK_WORDS, 0, st>>>(W, bitmap, wloc, ccount);
-  done_launch("k_fold_bitcnt");
-  k_fold_scan<<<1, 1024, 0, st>>>(ccount, cpre, C, &dev->n_requests, nullptr, nullptr, 0);
-  done_launch("k_fold_scan");
-  k_fb_rank<<<gR, 256, 0, st>>>(R, first, rdone, lastx, lensr, bitmap, wloc, cpre, progress, rank, order, done_out,
-                                prog_out, rl);
-  done_launch("k_fb_rank");
-  k_fb_csr<<<(R + CSR_TILE - 1) / CSR_TILE, 1024, 0, st>>>(rl, reinterpret_cast<unsigned long long*>(blk_off),
-                                                           reinterpret_cast<unsigned long long*>(tok_off), dev);
-  done_launch("k_fb_csr");
-  k_fb_place<<<NC, CHN, FB_PLACE_SMEM, st>>>(R, NB, bbase, cbase, rec, src, cstat, rank,
-                                             reinterpret_cast<const unsigned long long*>(blk_off),
-                                             reinterpret_cast<const unsigned long long*>(tok_off), blocks, n_blocks_in,
-                                             tokens, n_tokens_in, blocks_out, tokens_out);
+  {   // one CTA per SM, all resident (the grid barrier needs every CTA running)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)sms());   // >= the 16 CSR tiles an id space of 2^17 needs
+    cfg.blockDim = dim3(1024);
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    if (cudaLaunchKernelEx(&cfg, k_fb_mid, R, W, C, (const uint32_t*)cbase, cstat, first, lastx, rdone, lensr, bitmap,
+                           wloc, ccount, cpre, progress, rank, order, done_out, prog_out, rl,
+                           reinterpret_cast<unsigned long long*>(blk_off), reinterpret_cast<unsigned long long*>(tok_off),
+                           dev) != cudaSuccess)
+      return -1;
+    done_launch("k_fb_mid");
+  }
+  launch_pdl(k_fb_place, NC, CHN, FB_PLACE_SMEM, st, R, NB, bbase, cbase, rec, src, cstat, rank,
+             reinterpret_cast<const unsigned long long*>(blk_off), reinterpret_cast<const unsigned long long*>(tok_off),
+             blocks, n_blocks_in, tokens, n_tokens_in, blocks_out, tokens_out);
   done_launch("k_fb_place");
   FoldDevB h{};
   if (cudaMemcpyAsync(&h, dev, 40, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
