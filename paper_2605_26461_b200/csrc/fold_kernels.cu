@@ -7,8 +7,9 @@
 //
 // Batch form: S snapshots in consume order as SoA (request id or NO_REQ, delta lengths,
 // progress, done) plus the concatenated deltas.  The fold is a stable group-by with
-// variable-length payloads.  Every primitive is written here (no library sort or scan); tiles
-// are 8192 snapshots:
+// variable-length payloads.  Every primitive is written here (no library sort or scan).  Id
+// spaces up to 2^17 take the bucketed path (further below: one scatter into 256-id buckets,
+// then chunk-local work); larger ones this radix path, whose tiles are 8192 snapshots:
 //   k_fold_init     clear the per-request tables and the head bitmap
 //   k_fold_stats    consume order: per request id first snapshot and sticky done
 //                   (fire-and-forget reductions); the block scan of the packed delta lengths
