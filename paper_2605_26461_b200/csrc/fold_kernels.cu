@@ -649,32 +649,38 @@ __global__ void __launch_bounds__(256) k_fb_scan(uint32_t T, uint32_t nbk, uint3
                                                  unsigned long long* __restrict__ tbase, FoldDevB* __restrict__ dev) {
   fold_pdl();
   __shared__ unsigned long long sw[9];
+  // thread t owns the P consecutive tiles [t P, t P + P): its loads are independent, one block
+  // scan per array
+  const uint32_t P = (T + 255) / 256, i0 = threadIdx.x * P, i1 = min(i0 + P, T);
   if (blockIdx.x < nbk) {
     __shared__ uint32_t sw32[9];
     uint32_t* row = hist + (size_t)blockIdx.x * T;
-    uint32_t carry = 0;
-    for (uint32_t b = 0; b < T; b += 256) {
-      const uint32_t i = b + threadIdx.x;
-      const uint32_t v = i < T ? row[i] : 0u;
-      uint32_t tot;
-      const uint32_t ex = block_excl_scan<uint32_t, 8>(v, sw32, tot);
-      if (i < T) row[i] = carry + ex;
-      carry += tot;
+    uint32_t s = 0;
+    for (uint32_t i = i0; i < i1; ++i) s += row[i];
+    uint32_t tot;
+    uint32_t run = block_excl_scan<uint32_t, 8>(s, sw32, tot);
+    for (uint32_t i = i0; i < i1; ++i) {
+      const uint32_t v = row[i];
+      row[i] = run;
+      run += v;
     }
-    if (threadIdx.x == 0) rowtot[blockIdx.x] = carry;
+    if (threadIdx.x == 0) rowtot[blockIdx.x] = tot;
     return;
   }
-  unsigned long long cb = 0, ct = 0;
-  for (uint32_t b = 0; b < T; b += 256) {
-    const uint32_t i = b + threadIdx.x;
-    unsigned long long tb, tt;
-    const unsigned long long eb = block_excl_scan<unsigned long long, 8>(i < T ? tsb[i] : 0ull, sw, tb);
-    const unsigned long long et = block_excl_scan<unsigned long long, 8>(i < T ? tst[i] : 0ull, sw, tt);
-    if (i < T) tbase[i] = (cb + eb) | ((ct + et) << 32);
-    cb += tb;
-    ct += tt;
+  unsigned long long sb = 0, st = 0;
+  for (uint32_t i = i0; i < i1; ++i) {
+    sb += tsb[i];
+    st += tst[i];
   }
-  if (threadIdx.x == 0 && ((cb >> 32) || (ct >> 32))) dev->overrun = 1;
+  unsigned long long tb, tt;
+  unsigned long long rb = block_excl_scan<unsigned long long, 8>(sb, sw, tb);
+  unsigned long long rt = block_excl_scan<unsigned long long, 8>(st, sw, tt);
+  for (uint32_t i = i0; i < i1; ++i) {
+    tbase[i] = rb | (rt << 32);
+    rb += tsb[i];
+    rt += tst[i];
+  }
+  if (threadIdx.x == 0 && ((tb >> 32) || (tt >> 32))) dev->overrun = 1;
 }
 
 constexpr size_t FB_SCATTER_SMEM = 4 * (BT_WARPS * BK_MAX + 2 * BK_MAX) + 2 * BT + 16 * BT;

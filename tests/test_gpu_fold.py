@@ -178,3 +178,17 @@ def test_sharded_fold_merge_on_gpu(eng, nshards):
     want = so.fold_snapshots(*a)
     for f in ("order", "blk_off", "blocks", "tok_off", "tokens", "progress", "done"):
         assert np.array_equal(getattr(got, f), getattr(want, f)), f
+
+
+def test_fold_radix_path_forced():
+    """The radix path (id spaces above 2^17) forced at every size of this suite: the same
+    parity cases in a subprocess with MPSF_FOLD_RADIX=1, so both fold paths stay bit-exact."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MPSF_FOLD_RADIX="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", os.path.abspath(__file__),
+                        "-k", "not radix_path_forced"], cwd=root, env=env, capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
