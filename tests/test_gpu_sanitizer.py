@@ -1,7 +1,7 @@
 """compute-sanitizer over every kernel family at small sizes (tools/sanitize_target.py): the
 fault-path passes (row-table and global-table variants, dense and claimed-slot layouts, the
 general path, the sharded phase API and the sparse exchange), the batched translation, the
-fold, the KV pool restore and the remaps.  memcheck (out-of-bounds / misaligned accesses),
+fold (both paths), the KV pool restore and the remaps.  memcheck (out-of-bounds / misaligned accesses),
 racecheck (shared-memory hazards between threads of a CTA: the per-warp queues, the block-local
 minima, the staged tables) and synccheck (barrier / __syncwarp misuse) must report 0 errors."""
 
@@ -21,6 +21,7 @@ SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitize
 @pytest.mark.parametrize("tool,part", [("memcheck", "all"), ("synccheck", "all"),
                                        ("racecheck", "fault"), ("racecheck", "sharded"),
                                        ("racecheck", "translate"), ("racecheck", "fold"),
+                                       ("memcheck", "fold_radix"), ("racecheck", "fold_radix"),
                                        ("racecheck", "remap")])
 def test_compute_sanitizer_clean(tool, part):
     cmd = [SAN, "--tool", tool, "--error-exitcode", "3", "--print-limit", "20"]

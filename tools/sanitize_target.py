@@ -20,6 +20,9 @@ def main():
     from paper_2605_26461_b200.engine import BatchParams, DeviceBuffers, FaultEngine
     from paper_2605_26461_b200.parallel import GpuShard, LocalShardGroup
     only = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if only == "fold_radix":   # the fold's radix path (id spaces above 2^17) at the same small size
+        os.environ["MPSF_FOLD_RADIX"] = "1"
+        only = "fold"
     eng = FaultEngine(0)
 
     def check(got, want, what):
