@@ -993,19 +993,25 @@ __global__ void __launch_bounds__(1024, 1) k_fb_mid(uint32_t R, uint32_t W, uint
     rl[k] = lensr[r];
   }
   grid_barrier(bar, gen);
-  // CSR over ranks: tiles of 8192 (CTA t takes tile t), totals published, then offsets
+  // CSR over ranks: tiles of 8192 (CTA t takes tile t), totals published, then offsets.  The tile
+  // goes through shared memory so both the loads and the two output arrays are coalesced
+  // (thread-blocked global accesses cost one sector request per 8 bytes).
   constexpr int IPT = CSR_TILE / 1024;
+  extern __shared__ __align__(16) unsigned long long csr_s[];   // [CSR_TILE]
   const uint32_t ntile = (n + CSR_TILE - 1) / CSR_TILE;
-  unsigned long long v[IPT], run = 0, tot = 0;
-  const uint32_t kb = blockIdx.x * CSR_TILE + tid * IPT;
+  const uint32_t k0 = blockIdx.x * CSR_TILE;
   const bool mine = blockIdx.x < ntile;
+  unsigned long long run = 0, tot = 0;
   if (mine) {
-    unsigned long long s = 0;
 #pragma unroll
     for (int u = 0; u < IPT; ++u) {
-      v[u] = kb + u < n ? rl[kb + u] : 0ull;
-      s += v[u];
+      const uint32_t k = k0 + u * 1024 + tid;
+      csr_s[u * 1024 + tid] = k < n ? rl[k] : 0ull;
     }
+    __syncthreads();
+    unsigned long long s = 0;
+#pragma unroll
+    for (int u = 0; u < IPT; ++u) s += csr_s[tid * IPT + u];
     run = block_excl_scan<unsigned long long, 32>(s, sw, tot);
     if (tid == 0) dev->incl[blockIdx.x] = tot;
   }
@@ -1020,18 +1026,25 @@ __global__ void __launch_bounds__(1024, 1) k_fb_mid(uint32_t R, uint32_t W, uint
     __syncthreads();
     run += sw[32];
 #pragma unroll
+    for (int u = 0; u < IPT; ++u) {   // exclusive offsets in place
+      const unsigned long long v = csr_s[tid * IPT + u];
+      csr_s[tid * IPT + u] = run;
+      run += v;
+    }
+    if (k0 + (tid + 1) * IPT >= n && k0 + tid * IPT < n) {   // the thread holding rank n - 1: the CSR end
+      blk_off[n] = run & 0xFFFFFFFFull;
+      tok_off[n] = run >> 32;
+      dev->n_blocks = run & 0xFFFFFFFFull;
+      dev->n_tokens = run >> 32;
+    }
+    __syncthreads();
+#pragma unroll
     for (int u = 0; u < IPT; ++u) {
-      const uint32_t k = kb + u;
+      const uint32_t k = k0 + u * 1024 + tid;
       if (k < n) {
-        blk_off[k] = run & 0xFFFFFFFFull;
-        tok_off[k] = run >> 32;
-        run += v[u];
-        if (k == n - 1) {
-          blk_off[n] = run & 0xFFFFFFFFull;
-          tok_off[n] = run >> 32;
-          dev->n_blocks = run & 0xFFFFFFFFull;
-          dev->n_tokens = run >> 32;
-        }
+        const unsigned long long o = csr_s[u * 1024 + tid];
+        blk_off[k] = o & 0xFFFFFFFFull;
+        tok_off[k] = o >> 32;
       }
     }
   }
@@ -1287,7 +1300,10 @@ static int launch_fold_bucket(uint8_t* scratch, uint32_t S, uint32_t R, const ui
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)sms());   // >= the 16 CSR tiles an id space of 2^17 needs
     cfg.blockDim = dim3(1024);
+    cfg.dynamicSmemBytes = 8 * CSR_TILE;
     cfg.stream = st;
+    if (cudaFuncSetAttribute(k_fb_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * CSR_TILE) != cudaSuccess)
+      return -1;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeCooperative;
     at[0].val.cooperative = 1;
