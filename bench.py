@@ -982,10 +982,11 @@ def main():
         sys.exit(relaunch(args))
     elif os.environ.get("MPSF_BENCH_LAUNCH_PROBE") == "1":
         # test hook (tests/test_bench_launch.py): report the rank layout and stop before any CUDA work
-        print(json.dumps({"probe": True, "rank": int(os.environ.get("RANK", "0")),
-                          "world_size": int(os.environ.get("WORLD_SIZE", "1")),
-                          "local_rank": int(os.environ.get("LOCAL_RANK", "0")),
-                          "master_addr": os.environ.get("MASTER_ADDR")}), flush=True)
+        # one write(2) per rank: print() may split the line and the newline, interleaving ranks
+        os.write(1, (json.dumps({"probe": True, "rank": int(os.environ.get("RANK", "0")),
+                                 "world_size": int(os.environ.get("WORLD_SIZE", "1")),
+                                 "local_rank": int(os.environ.get("LOCAL_RANK", "0")),
+                                 "master_addr": os.environ.get("MASTER_ADDR")}) + "\n").encode())
     else:
         run_mine(args)
 
