@@ -45,6 +45,7 @@ def fold_case(rng, rnd):
 
 def main():
     budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300.0
+    sbase = int(sys.argv[2]) if len(sys.argv) > 2 else 700_000
     eng = FaultEngine(0)
     t0 = time.time()
     st = {"fold_cases": 0, "fold_snapshots": 0, "fold_mismatches": 0, "kv_cases": 0, "kv_mismatches": 0,
@@ -52,8 +53,8 @@ def main():
     bad = []
     k = 0
     while time.time() - t0 < budget:
-        rnd = random.Random(700_000 + k)
-        rng = np.random.default_rng(700_000 + k)
+        rnd = random.Random(sbase + k)
+        rng = np.random.default_rng(sbase + k)
         k += 1
         if k % 3:
             snap, R = fold_case(rng, rnd)

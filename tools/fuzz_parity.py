@@ -4,7 +4,7 @@ latency ties), random batches (duplicates, same-page cross-engine records, parse
 traps, wild pages, invalid entries), every dedup layout (auto / dense / sparse) and both the
 device-resident and the host form, all six outputs compared bit for bit.
 
-    python tools/fuzz_parity.py [seconds]      # prints one JSON summary line
+    python tools/fuzz_parity.py [seconds] [seed base]   # prints one JSON summary line
 """
 import json
 import os
@@ -27,6 +27,7 @@ FIELDS = ("out", "verdict", "counts", "dedup_keys", "dedup_idx", "cancel")
 
 def main():
     budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300.0
+    sbase = int(sys.argv[2]) if len(sys.argv) > 2 else 900_000
     eng = FaultEngine(0)
     t0 = time.time()
     stats = {"batches": 0, "entries": 0, "mismatches": 0, "by_layout": {}, "by_form": {}, "isolation_on": 0,
@@ -34,7 +35,7 @@ def main():
     bad = []
     seed = 0
     while time.time() - t0 < budget:
-        rnd = random.Random(900_000 + seed)
+        rnd = random.Random(sbase + seed)
         seed += 1
         w = RW.random_world(rnd, max_mps=rnd.choice((2, 4, 6)), max_sa=rnd.choice((1, 2, 3)),
                             dead_p=rnd.choice((0.0, 0.0, 0.15, 0.3)))
@@ -63,7 +64,7 @@ def main():
         if not ok:
             stats["mismatches"] += 1
             if len(bad) < 5:
-                bad.append({"seed": 900_000 + seed - 1, "layout": layout, "form": form, "n": n,
+                bad.append({"seed": sbase + seed - 1, "layout": layout, "form": form, "n": n,
                             "fields": [f for f in FIELDS if not np.array_equal(getattr(got, f), getattr(want, f))]})
     stats["seconds"] = round(time.time() - t0, 1)
     stats["first_mismatches"] = bad
