@@ -695,7 +695,8 @@ def bench_translate(args, eng, hbm_peak, flush, w):
     nm, npop = int(s.n_miss), int(s.n_populated)
     exact = (np.array_equal(d_hit.cpu().numpy(), want.hit) and
              np.array_equal(d_fi[:4 * nm].cpu().numpy().view(np.uint32), want.fault_idx) and
-             np.array_equal(d_pi[:4 * npop].cpu().numpy().view(np.uint32), want.pop_idx))
+             np.array_equal(d_pi[:4 * npop].cpu().numpy().view(np.uint32), want.pop_idx) and
+             np.array_equal(d_f[:16 * nm].cpu().numpy(), acc.view(np.uint8).reshape(n, 16)[want.fault_idx].reshape(-1)))
     steps = max(20, min(args.steps, 50))
     rewarm(lambda: eng.translate_device(d_acc, n, d_hit, d_f, d_fi, d_pi))
     tot = 0.0

@@ -1510,25 +1510,39 @@ __global__ void __launch_bounds__(SEG_CHUNKS) k_tr_lists(Scratch S, const mpsf_f
   const uint64_t pm = pre & 0xFFFFFFFFull, pp = pre >> 32;
   const uint32_t g0 = (uint32_t)(base_index + q * WCHUNK);
   const unsigned long long below = (1ull << (2 * lane)) - 1ull;
-  for (int j = 0; j < 32; ++j) {                    // warp-cooperative, coalesced
-    const unsigned long long mm = __shfl_sync(0xFFFFFFFFu, mk.x, j), pm2 = __shfl_sync(0xFFFFFFFFu, mk.y, j);
-    if (!(mm | pm2)) continue;
-    const uint64_t bj = __shfl_sync(0xFFFFFFFFu, pm, j), pj = __shfl_sync(0xFFFFFFFFu, pp, j);
-    const uint32_t gj = __shfl_sync(0xFFFFFFFFu, g0, j) + 2 * lane;
-    const uint64_t qj = q - lane + j;
-    const uint32_t two = (uint32_t)(mm >> (2 * lane)) & 3u, twp = (uint32_t)(pm2 >> (2 * lane)) & 3u;
-    uint64_t pos = bj + __popcll(mm & below);
+  // warp-cooperative, coalesced: the 32 chunks of the warp in groups of TRL_J, every staged
+  // miss of a group loaded before any of its stores (one store-to-load ordering per group
+  // instead of per chunk: the stores may alias the staging area as far as the compiler knows,
+  // so a per-chunk load -> store loop waits a full L2 round trip per chunk)
+  constexpr int TRL_J = 4;
+  uint4* const faults4 = reinterpret_cast<uint4*>(faults);
+  for (int j0 = 0; j0 < 32; j0 += TRL_J) {
+    uint4 v[TRL_J][2];
+    uint32_t two[TRL_J], twp[TRL_J], gj[TRL_J];
+    uint64_t pos[TRL_J], ppos[TRL_J];
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      if (two & (1u << t)) {
-        fault_idx[pos] = gj + t;
-        reinterpret_cast<uint4*>(faults)[pos] = __ldcs(S.trstage + qj * WCHUNK + (pos - bj));
-        ++pos;
-      }
+    for (int u = 0; u < TRL_J; ++u) {
+      const int j = j0 + u;
+      const unsigned long long mm = __shfl_sync(0xFFFFFFFFu, mk.x, j), pm2 = __shfl_sync(0xFFFFFFFFu, mk.y, j);
+      const uint64_t bj = __shfl_sync(0xFFFFFFFFu, pm, j), pj = __shfl_sync(0xFFFFFFFFu, pp, j);
+      gj[u] = __shfl_sync(0xFFFFFFFFu, g0, j) + 2 * lane;
+      two[u] = (uint32_t)(mm >> (2 * lane)) & 3u;
+      twp[u] = (uint32_t)(pm2 >> (2 * lane)) & 3u;
+      pos[u] = bj + __popcll(mm & below);
+      ppos[u] = pj + __popcll(pm2 & below);
+      const uint4* src = S.trstage + (q - lane + j) * WCHUNK + (pos[u] - bj);
+      v[u][0] = (two[u] & 1u) ? __ldcs(src) : make_uint4(0u, 0u, 0u, 0u);
+      v[u][1] = (two[u] & 2u) ? __ldcs(src + (two[u] & 1u)) : make_uint4(0u, 0u, 0u, 0u);
     }
-    uint64_t ppos = pj + __popcll(pm2 & below);
-    if (twp & 1u) pop_idx[ppos++] = gj;
-    if (twp & 2u) pop_idx[ppos] = gj + 1;
+#pragma unroll
+    for (int u = 0; u < TRL_J; ++u) {
+      uint64_t p = pos[u];
+      if (two[u] & 1u) { fault_idx[p] = gj[u]; faults4[p] = v[u][0]; ++p; }
+      if (two[u] & 2u) { fault_idx[p] = gj[u] + 1; faults4[p] = v[u][1]; }
+      uint64_t pp2 = ppos[u];
+      if (twp[u] & 1u) pop_idx[pp2++] = gj[u];
+      if (twp[u] & 2u) pop_idx[pp2] = gj[u] + 1;
+    }
   }
 }
 
