@@ -1509,39 +1509,71 @@ __global__ void __launch_bounds__(SEG_CHUNKS) k_tr_lists(Scratch S, const mpsf_f
   pre += x - mine;
   const uint64_t pm = pre & 0xFFFFFFFFull, pp = pre >> 32;
   const uint32_t g0 = (uint32_t)(base_index + q * WCHUNK);
-  const unsigned long long below = (1ull << (2 * lane)) - 1ull;
-  // warp-cooperative, coalesced: the 32 chunks of the warp in groups of TRL_J, every staged
-  // miss of a group loaded before any of its stores (one store-to-load ordering per group
-  // instead of per chunk: the stores may alias the staging area as far as the compiler knows,
-  // so a per-chunk load -> store loop waits a full L2 round trip per chunk)
-  constexpr int TRL_J = 4;
-  uint4* const faults4 = reinterpret_cast<uint4*>(faults);
-  for (int j0 = 0; j0 < 32; j0 += TRL_J) {
-    uint4 v[TRL_J][2];
-    uint32_t two[TRL_J], twp[TRL_J], gj[TRL_J];
-    uint64_t pos[TRL_J], ppos[TRL_J];
+  // misses: each lane lists its chunk's misses (chunk in the warp << 6 | entry, ascending) at
+  // their flat ranks in the warp's shared table and notes its chunk's first rank; the warp then
+  // copies ranks l, l + 32, ... with TR_KEYS staged entries in flight per lane and coalesced
+  // stores (as k_lists: the warp's chunks are consecutive, so are their misses)
+  constexpr int TR_KEYS = 8;
+  __shared__ uint16_t s_code[SEG_CHUNKS / 32][32 * WCHUNK];
+  __shared__ uint32_t s_cst[SEG_CHUNKS / 32][32];
+  uint16_t* code = s_code[warp];
+  const uint64_t q0w = q - lane;
+  const uint32_t gw0 = __shfl_sync(0xFFFFFFFFu, g0, 0);   // the warp's first access
+  {
+    unsigned long long m = mk.x;
+    const uint32_t cnt = (uint32_t)__popcll(m);
+    uint32_t inc = cnt;
 #pragma unroll
-    for (int u = 0; u < TRL_J; ++u) {
-      const int j = j0 + u;
-      const unsigned long long mm = __shfl_sync(0xFFFFFFFFu, mk.x, j), pm2 = __shfl_sync(0xFFFFFFFFu, mk.y, j);
-      const uint64_t bj = __shfl_sync(0xFFFFFFFFu, pm, j), pj = __shfl_sync(0xFFFFFFFFu, pp, j);
-      gj[u] = __shfl_sync(0xFFFFFFFFu, g0, j) + 2 * lane;
-      two[u] = (uint32_t)(mm >> (2 * lane)) & 3u;
-      twp[u] = (uint32_t)(pm2 >> (2 * lane)) & 3u;
-      pos[u] = bj + __popcll(mm & below);
-      ppos[u] = pj + __popcll(pm2 & below);
-      const uint4* src = S.trstage + (q - lane + j) * WCHUNK + (pos[u] - bj);
-      v[u][0] = (two[u] & 1u) ? __ldcs(src) : make_uint4(0u, 0u, 0u, 0u);
-      v[u][1] = (two[u] & 2u) ? __ldcs(src + (two[u] & 1u)) : make_uint4(0u, 0u, 0u, 0u);
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+      if (lane >= o) inc += u;
     }
+    const uint32_t R = __shfl_sync(0xFFFFFFFFu, inc, 31);
+    const uint64_t pm0 = __shfl_sync(0xFFFFFFFFu, pm, 0);
+    s_cst[warp][lane] = inc - cnt;
+    for (uint32_t pos = inc - cnt; m; m &= m - 1)
+      code[pos++] = (uint16_t)((lane << 6) | (uint32_t)(__ffsll((long long)m) - 1));
+    __syncwarp();
+    uint4* const faults4 = reinterpret_cast<uint4*>(faults);
+    for (uint32_t r0 = 0; r0 < R; r0 += 32 * TR_KEYS) {
+      uint4 v[TR_KEYS];
+      uint32_t gi[TR_KEYS];
 #pragma unroll
-    for (int u = 0; u < TRL_J; ++u) {
-      uint64_t p = pos[u];
-      if (two[u] & 1u) { fault_idx[p] = gj[u]; faults4[p] = v[u][0]; ++p; }
-      if (two[u] & 2u) { fault_idx[p] = gj[u] + 1; faults4[p] = v[u][1]; }
-      uint64_t pp2 = ppos[u];
-      if (twp[u] & 1u) pop_idx[pp2++] = gj[u];
-      if (twp[u] & 2u) pop_idx[pp2] = gj[u] + 1;
+      for (int h = 0; h < TR_KEYS; ++h) {
+        const uint32_t f = r0 + 32 * h + lane;
+        const uint32_t c = f < R ? code[f] : 0u, ch = c >> 6;
+        v[h] = f < R ? __ldcs(S.trstage + (q0w + ch) * WCHUNK + (f - s_cst[warp][ch])) : make_uint4(0u, 0u, 0u, 0u);
+        gi[h] = gw0 + ch * WCHUNK + (c & 63u);
+      }
+#pragma unroll
+      for (int h = 0; h < TR_KEYS; ++h) {
+        const uint32_t f = r0 + 32 * h + lane;
+        if (f < R) {
+          faults4[pm0 + f] = v[h];
+          fault_idx[pm0 + f] = gi[h];
+        }
+      }
+    }
+    __syncwarp();
+  }
+  // populating prefetches: the same listing, indices only
+  {
+    unsigned long long m = mk.y;
+    const uint32_t cnt = (uint32_t)__popcll(m);
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+      if (lane >= o) inc += u;
+    }
+    const uint32_t R = __shfl_sync(0xFFFFFFFFu, inc, 31);
+    const uint64_t pp0 = __shfl_sync(0xFFFFFFFFu, pp, 0);
+    for (uint32_t pos = inc - cnt; m; m &= m - 1)
+      code[pos++] = (uint16_t)((lane << 6) | (uint32_t)(__ffsll((long long)m) - 1));
+    __syncwarp();
+    for (uint32_t f = lane; f < R; f += 32) {
+      const uint32_t c = code[f];
+      pop_idx[pp0 + f] = gw0 + (c >> 6) * WCHUNK + (c & 63u);
     }
   }
 }
